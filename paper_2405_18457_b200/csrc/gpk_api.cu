@@ -1,0 +1,1841 @@
+// Host C++ of libgpk: the C-ABI (include/gpk.h) over device-resident solver
+// state. Mirrors the reference's KernelOperator / LinearSystemBatch / solvers
+// / estimators / optimise (/root/reference/proj/core/src/*.cpp), with all
+// n-sized state on the GPU and only d+2-sized scalars (Adam, hyperparameters)
+// on the host.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/gpk.h"
+#include "gpk_internal.cuh"
+#include "philox.cuh"
+
+namespace gpk {
+thread_local long long* g_launch_counter = nullptr;
+}
+
+using namespace gpk;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct OutOfRange : std::out_of_range {
+  using std::out_of_range::out_of_range;
+};
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  T* ensure(size_t count) {
+    if (count > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      GPK_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+      cap = count;
+    }
+    return p;
+  }
+};
+
+double softplus(double x) {  // hyperparameters.cpp:8-11
+  if (x > 0.0) return x + std::log1p(std::exp(-x));
+  return std::log1p(std::exp(x));
+}
+double softplus_inverse(double y) {  // hyperparameters.cpp:13-17
+  if (y <= 0.0) throw InvalidArgument("softplus_inverse: argument must be positive");
+  return y + std::log(-std::expm1(-y));
+}
+double sigmoid(double x) {  // hyperparameters.cpp:19-23
+  if (x >= 0.0) return 1.0 / (1.0 + std::exp(-x));
+  const double e = std::exp(x);
+  return e / (1.0 + e);
+}
+
+}  // namespace
+
+struct gpk_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  long long launches = 0;
+  CgCtl* ctl_host = nullptr;  // pinned, 2 slots
+  cudaEvent_t ev[2]{};
+  double* stats = nullptr;    // device [evals x RHS, flops]
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof;  // K.V launch brackets
+  size_t prof_used = 0;
+};
+
+struct gpk_operator {
+  gpk_ctx* ctx = nullptr;
+  int n = 0, d = 0, dp = 0;
+  DBuf<double> x64;       // [n][d] unscaled
+  DBuf<float> xs32;       // [n][dp]
+  DBuf<double> xs64;      // [n][d]
+  DBuf<double> inv_ls_dev;
+  std::vector<double> raw, inv_ls;
+  double s = 1, s2 = 1, sigma = 1, sigma2 = 1;
+  DBuf<double> part;      // kv split partials
+  // scratch for host-facing calls
+  DBuf<float> v32;
+  DBuf<double> v64, out64, tmp64;
+  DBuf<int> idx;
+};
+
+struct gpk_precond {
+  gpk_operator* op = nullptr;
+  int n = 0, rank = 0, achieved = 0, stopped = 0;
+  DBuf<double> L;      // [n][rank] row-major
+  DBuf<double> minv;   // [r][r]
+  DBuf<int> pivots;
+  double sigma2 = 1;
+  DBuf<double> part, T, inner;
+};
+
+struct gpk_batch {
+  gpk_operator* op = nullptr;
+  int n = 0, m = 0;
+  DBuf<double> targets, solutions, residuals;
+  std::vector<double> scales;
+  DBuf<double> scales_dev;
+  // solver workspace
+  DBuf<double> w1, w2, w3, w4, red, vec1, vec2, vec3;
+  DBuf<float> f32;
+  DBuf<CgCtl> ctl;
+  DBuf<int> ibuf, ibuf2, flag;
+  DBuf<double> blocks;
+};
+
+struct gpk_rff_basis {
+  gpk_ctx* ctx = nullptr;
+  int d = 0, pairs = 0, samples = 0;
+  uint64_t seed = 0, substream = 0;
+  std::vector<double> freq;     // P x d col-major (host, exact)
+  std::vector<double> weights;  // 2P x S col-major
+  DBuf<double> w_dev, freq_dev;
+};
+
+namespace {
+
+struct LaunchScope {
+  explicit LaunchScope(gpk_ctx* c) {
+    prev = g_launch_counter;
+    g_launch_counter = &c->launches;
+    GPK_CUDA(cudaSetDevice(c->device));
+  }
+  ~LaunchScope() { g_launch_counter = prev; }
+  long long* prev;
+};
+
+template <class F>
+gpk_status guarded(F&& f) {
+  try {
+    f();
+    return GPK_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return GPK_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return GPK_ERANGE;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return GPK_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GPK_ENUMERIC;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw InvalidArgument(msg);
+}
+
+bool all_finite(const double* p, size_t count) {
+  for (size_t i = 0; i < count; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+// col-major host (rows x cols) -> row-major device [rows][cols]
+void upload_colmajor(gpk_operator* op, const double* host, int rows, int cols, double* dev) {
+  cudaStream_t s = op->ctx->stream;
+  double* tmp = op->tmp64.ensure(static_cast<size_t>(rows) * cols);
+  GPK_CUDA(cudaMemcpyAsync(tmp, host, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
+  transpose_launch(tmp, cols, rows, rows, dev, cols, s);
+}
+void download_colmajor(gpk_operator* op, const double* dev, int rows, int cols, double* host) {
+  cudaStream_t s = op->ctx->stream;
+  double* tmp = op->tmp64.ensure(static_cast<size_t>(rows) * cols);
+  transpose_launch(dev, rows, cols, cols, tmp, rows, s);
+  GPK_CUDA(cudaMemcpyAsync(host, tmp, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaStreamSynchronize(s));
+}
+
+void set_hyper(gpk_operator* op, const double* raw) {
+  const int d = op->d;
+  std::vector<double> r(raw, raw + d + 2);
+  for (int k = 0; k < d + 2; ++k) {
+    const double c = softplus(r[k]);
+    if (!std::isfinite(c) || c <= 0.0)
+      throw InvalidArgument("Hyperparameters: constrained value " + std::to_string(k) + " is not finite and positive");
+  }
+  op->raw = r;
+  op->inv_ls.resize(d);
+  for (int k = 0; k < d; ++k) op->inv_ls[k] = 1.0 / softplus(r[k]);
+  op->s = softplus(r[d]);
+  op->s2 = op->s * op->s;
+  op->sigma = softplus(r[d + 1]);
+  op->sigma2 = op->sigma * op->sigma;
+  cudaStream_t s = op->ctx->stream;
+  double* il = op->inv_ls_dev.ensure(d);
+  GPK_CUDA(cudaMemcpyAsync(il, op->inv_ls.data(), sizeof(double) * d, cudaMemcpyHostToDevice, s));
+  prescale_launch(op->x64.p, op->n, d, op->dp, il, op->xs32.p, op->xs64.p, s);
+  GPK_CUDA(cudaStreamSynchronize(s));  // inv_ls host buffer lifetime
+}
+
+// Core operator product: out = base + alpha * H[rows, cols] v.
+struct KvCall {
+  const float* v = nullptr;  // FP32 RHS [C][ld]
+  int m = 0;
+  const int* row_idx = nullptr;
+  int r0 = 0, R = 0;
+  int c0 = 0, C = 0;
+  const int* sel = nullptr;
+  int sel_block = 0;
+  const double* vdiag = nullptr;  // FP64 RHS for the diagonal, [C][m]
+  double* out = nullptr;
+  int ldo = 0;
+  const double* base = nullptr;
+  int ldb = 0;
+  double alpha = 1.0;
+  const int* skip = nullptr;
+};
+
+void run_kv(gpk_operator* op, const KvCall& c) {
+  cudaStream_t s = op->ctx->stream;
+  const int Cmax = c.sel ? c.sel_block : c.C;
+  int splits = kv_choose_splits(c.R, Cmax, op->ctx->sms);
+  int cps = (Cmax + splits - 1) / splits;
+  cps = (cps + 31) / 32 * 32;
+  splits = std::max(1, (Cmax + cps - 1) / cps);
+  double* part = op->part.ensure(static_cast<size_t>(splits) * c.R * c.m);
+  KvArgs a{};
+  a.xs = op->xs32.p;
+  a.n = op->n;
+  a.dp = op->dp;
+  a.row_idx = c.row_idx;
+  a.r0 = c.r0;
+  a.R = c.R;
+  a.c0 = c.c0;
+  a.C = c.C;
+  a.sel = c.sel;
+  a.sel_block = c.sel_block;
+  a.v = c.v;
+  a.ldv = kv_ld_for(c.m);
+  a.m = c.m;
+  a.log2_s2 = static_cast<float>(std::log2(op->s2));
+  a.part = part;
+  a.splits = splits;
+  a.cols_per_split = cps;
+  a.flush_chunks = 16;
+  a.skip = c.skip;
+  a.stats = op->ctx->stats;
+  a.d = op->d;
+  gpk_ctx* ctx = op->ctx;
+  if (ctx->profiling) {
+    if (ctx->prof_used == ctx->prof.size()) {
+      cudaEvent_t e0, e1;
+      GPK_CUDA(cudaEventCreate(&e0));
+      GPK_CUDA(cudaEventCreate(&e1));
+      ctx->prof.push_back({e0, e1});
+    }
+    auto& pr = ctx->prof[ctx->prof_used++];
+    GPK_CUDA(cudaEventRecord(pr.first, s));
+    kv_slab_launch(a, op->d, s);
+    GPK_CUDA(cudaEventRecord(pr.second, s));
+  } else {
+    kv_slab_launch(a, op->d, s);
+  }
+  KvReduceArgs r{};
+  r.part = part;
+  r.splits = splits;
+  r.R = c.R;
+  r.m = c.m;
+  r.vdiag = c.vdiag;
+  r.ldvd = c.m;
+  r.vdiag32 = c.v;
+  r.ldv32 = a.ldv;
+  r.row_idx = c.row_idx;
+  r.r0 = c.r0;
+  r.c0 = c.c0;
+  r.C = c.C;
+  r.sel = c.sel;
+  r.sel_block = c.sel_block;
+  r.n = op->n;
+  r.sigma2 = op->sigma2;
+  r.out = c.out;
+  r.ldo = c.ldo;
+  r.base = c.base;
+  r.ldb = c.ldb;
+  r.alpha = c.alpha;
+  r.skip = c.skip;
+  kv_reduce_launch(r, s);
+}
+
+// H V for V FP64 row-major [n][m] on device -> out row-major (ldo = m).
+void apply_dev64(gpk_operator* op, const double* v64, int m, double* out, const double* base, double alpha,
+                 float* v32buf, const int* skip) {
+  const int ld = kv_ld_for(m);
+  to_f32_launch(v64, op->n, m, m, v32buf, ld, skip, op->ctx->stream);
+  KvCall c;
+  c.v = v32buf;
+  c.m = m;
+  c.R = op->n;
+  c.C = op->n;
+  c.vdiag = v64;
+  c.out = out;
+  c.ldo = m;
+  c.base = base;
+  c.ldb = m;
+  c.alpha = alpha;
+  c.skip = skip;
+  run_kv(op, c);
+}
+
+// RHS groups of at most 65 columns (the kernel's widest tile).
+constexpr int kMaxRhs = 65;
+
+// -------------------------------------------------------------- precond
+void build_precond(gpk_precond* pc) {
+  gpk_operator* op = pc->op;
+  cudaStream_t s = op->ctx->stream;
+  const int n = op->n, rank = pc->rank;
+  pc->sigma2 = op->sigma2;
+  pc->achieved = 0;
+  pc->stopped = 0;
+  if (rank == 0) return;
+  double* L = pc->L.ensure(static_cast<size_t>(n) * rank);
+  int* piv = pc->pivots.ensure(rank);
+  DBuf<double> diag, pval;
+  DBuf<int> pidx, stop;
+  diag.ensure(n);
+  const int G = kReduceGroups;
+  pval.ensure(G);
+  pidx.ensure(G);
+  stop.ensure(2);
+  GPK_CUDA(cudaMemsetAsync(stop.p, 0, sizeof(int) * 2, s));
+  // diag = s^2 (kernel_diagonal, kernel.cpp:196-198)
+  std::vector<double> h(n, op->s2);
+  GPK_CUDA(cudaMemcpyAsync(diag.p, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  for (int mcol = 0; mcol < rank; ++mcol) {
+    argmax_partials_launch(diag.p, n, pval.p, pidx.p, G, s);
+    pchol_step_launch(op->xs64.p, n, op->d, op->s2, pval.p, pidx.p, G, L, rank, mcol, diag.p, piv, stop.p, s);
+  }
+  // achieved rank = number of pivots before the stop flag: recompute on host
+  std::vector<int> pv(rank);
+  int stop_h = 0;
+  GPK_CUDA(cudaMemcpyAsync(pv.data(), piv, sizeof(int) * rank, cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaMemcpyAsync(&stop_h, stop.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaStreamSynchronize(s));
+  // The stop flag is set at the first non-positive pivot; pivots written
+  // before it are valid. Recount by replaying: steps that ran wrote pivots
+  // in order, so find how many ran via a marker pass.
+  int achieved = rank;
+  if (stop_h) {
+    // Re-run the count cheaply: pivots of skipped steps were never written;
+    // mark them by a sentinel pass.
+    std::vector<int> marker(rank, -1);
+    GPK_CUDA(cudaMemcpyAsync(piv, marker.data(), sizeof(int) * rank, cudaMemcpyHostToDevice, s));
+    GPK_CUDA(cudaMemsetAsync(stop.p, 0, sizeof(int), s));
+    GPK_CUDA(cudaMemcpyAsync(diag.p, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    for (int mcol = 0; mcol < rank; ++mcol) {
+      argmax_partials_launch(diag.p, n, pval.p, pidx.p, G, s);
+      pchol_step_launch(op->xs64.p, n, op->d, op->s2, pval.p, pidx.p, G, L, rank, mcol, diag.p, piv, stop.p, s);
+    }
+    GPK_CUDA(cudaMemcpyAsync(pv.data(), piv, sizeof(int) * rank, cudaMemcpyDeviceToHost, s));
+    GPK_CUDA(cudaStreamSynchronize(s));
+    achieved = 0;
+    while (achieved < rank && pv[achieved] >= 0) ++achieved;
+    pc->stopped = 1;
+  }
+  pc->achieved = achieved;
+  if (achieved == 0) return;
+  // small = L^T L + sigma^2 I (achieved x achieved), then its inverse
+  const int r = achieved;
+  DBuf<double> gpart, gram;
+  gpart.ensure(static_cast<size_t>(G) * r * r);
+  gram.ensure(static_cast<size_t>(r) * r);
+  // gram over the first r columns of L (ld = rank)
+  gram_partials_launch(L, n, r, rank, gpart.p, G, s);
+  sum_partials_launch(gpart.p, G, r * r, gram.p, nullptr, s);
+  std::vector<double> gh(static_cast<size_t>(r) * r);
+  GPK_CUDA(cudaMemcpyAsync(gh.data(), gram.p, sizeof(double) * r * r, cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaStreamSynchronize(s));
+  for (int a = 0; a < r; ++a) gh[static_cast<size_t>(a) * r + a] += pc->sigma2;
+  // FP64 Cholesky + inverse on the host (r <= rank ~ 100: microseconds).
+  std::vector<double> Lc(static_cast<size_t>(r) * r, 0.0);
+  for (int j = 0; j < r; ++j) {
+    double sjj = gh[static_cast<size_t>(j) * r + j];
+    for (int k = 0; k < j; ++k) sjj -= Lc[static_cast<size_t>(j) * r + k] * Lc[static_cast<size_t>(j) * r + k];
+    if (!(sjj > 0.0)) throw NumericError("PivotedCholeskyPreconditioner: inner factorisation failed");
+    const double ljj = std::sqrt(sjj);
+    Lc[static_cast<size_t>(j) * r + j] = ljj;
+    for (int i = j + 1; i < r; ++i) {
+      double t = gh[static_cast<size_t>(i) * r + j];
+      for (int k = 0; k < j; ++k) t -= Lc[static_cast<size_t>(i) * r + k] * Lc[static_cast<size_t>(j) * r + k];
+      Lc[static_cast<size_t>(i) * r + j] = t / ljj;
+    }
+  }
+  std::vector<double> inv(static_cast<size_t>(r) * r, 0.0);
+  for (int c = 0; c < r; ++c) {
+    std::vector<double> y(r, 0.0);
+    y[c] = 1.0;
+    for (int i = 0; i < r; ++i) {
+      double t = y[i];
+      for (int k = 0; k < i; ++k) t -= Lc[static_cast<size_t>(i) * r + k] * y[k];
+      y[i] = t / Lc[static_cast<size_t>(i) * r + i];
+    }
+    for (int i = r - 1; i >= 0; --i) {
+      double t = y[i];
+      for (int k = i + 1; k < r; ++k) t -= Lc[static_cast<size_t>(k) * r + i] * y[k];
+      y[i] = t / Lc[static_cast<size_t>(i) * r + i];
+    }
+    for (int i = 0; i < r; ++i) inv[static_cast<size_t>(i) * r + c] = y[i];
+  }
+  pc->minv.ensure(static_cast<size_t>(r) * r);
+  GPK_CUDA(cudaMemcpyAsync(pc->minv.p, inv.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, s));
+  GPK_CUDA(cudaStreamSynchronize(s));
+}
+
+// out = P^-1 R (device, row-major [n][m]); P == nullptr -> identity copy.
+void precond_apply_dev(gpk_precond* pc, gpk_operator* op, const double* R, int m, double* out, const int* skip) {
+  cudaStream_t s = op->ctx->stream;
+  const int n = op->n;
+  if (!pc) {
+    scale_launch(R, n * m, 1.0, out, skip, s);
+    return;
+  }
+  if (pc->achieved == 0) {
+    scale_launch(R, n * m, pc->sigma2, out, skip, s);
+    return;
+  }
+  const int r = pc->achieved, G = kReduceGroups;
+  double* part = pc->part.ensure(static_cast<size_t>(G) * r * m);
+  double* T = pc->T.ensure(static_cast<size_t>(r) * m);
+  double* inner = pc->inner.ensure(static_cast<size_t>(r) * m);
+  lt_times_launch(pc->L.p, n, r, pc->rank, R, m, part, G, skip, s);
+  sum_partials_launch(part, G, r * m, T, skip, s);
+  small_gemm_launch(pc->minv.p, r, r, T, m, inner, skip, s);
+  woodbury_launch(R, pc->L.p, n, r, pc->rank, inner, m, pc->sigma2, out, skip, s);
+}
+
+// ----------------------------------------------------------------- batch
+void batch_norms(gpk_batch* b, const double* R, double tol, double* mean, double* probe, int* done) {
+  cudaStream_t s = b->op->ctx->stream;
+  const int G = kReduceGroups;
+  double* part = b->red.ensure(static_cast<size_t>(G) * 2 * b->m + 8);
+  double* o3 = b->vec3.ensure(std::max(3, b->m));
+  col_reduce_launch(R, nullptr, b->n, b->m, b->m, 2, part, G, nullptr, s);
+  norms_launch(part, G, b->m, b->scales_dev.p, tol, o3, s);
+  double h[3];
+  GPK_CUDA(cudaMemcpyAsync(h, o3, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaStreamSynchronize(s));
+  *mean = h[0];
+  *probe = h[1];
+  *done = h[2] != 0.0;
+}
+
+void refresh_residuals(gpk_batch* b) {
+  gpk_operator* op = b->op;
+  float* v32 = b->f32.ensure(static_cast<size_t>(b->n) * kv_ld_for(b->m));
+  for (int j0 = 0; j0 < b->m; j0 += kMaxRhs) {
+    if (b->m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
+  }
+  apply_dev64(op, b->solutions.p, b->m, b->residuals.p, b->targets.p, -1.0, v32, nullptr);
+}
+
+void validate(const gpk_solver_config* c) {  // linear_system.cpp:7-14
+  if (!(c->tolerance > 0.0)) throw InvalidArgument("SolverConfig: tolerance > 0");
+  if (c->max_epochs < 1) throw InvalidArgument("SolverConfig: max_epochs >= 1");
+  if (c->block_size < 1) throw InvalidArgument("SolverConfig: block_size >= 1");
+  if (c->batch_size < 1) throw InvalidArgument("SolverConfig: batch_size >= 1");
+  if (c->momentum < 0.0 || c->momentum >= 1.0) throw InvalidArgument("SolverConfig: 0 <= momentum < 1");
+  if (c->preconditioner_rank < 0) throw InvalidArgument("SolverConfig: preconditioner_rank >= 0");
+}
+
+using Clock = std::chrono::steady_clock;
+
+void finalise(gpk_batch* b, double tol, gpk_solver_report* rep, Clock::time_point start) {
+  int done;
+  batch_norms(b, b->residuals.p, tol, &rep->mean_residual_norm, &rep->probe_residual_norm, &done);
+  rep->reached_tolerance = done;
+  rep->wall_seconds = std::chrono::duration<double>(Clock::now() - start).count();
+}
+
+// Runs `enqueue_iteration` in groups, keeping one group in flight while the
+// previous group's control block is read back; stops once ctl.stop is set.
+template <class F>
+void drive(gpk_batch* b, CgCtl* ctl, int group, int max_iters, F&& enqueue_iteration) {
+  gpk_ctx* ctx = b->op->ctx;
+  cudaStream_t s = ctx->stream;
+  int issued = 0, k = 0;
+  bool pending = false;
+  while (true) {
+    const int g = std::min(group, max_iters - issued);
+    if (g > 0) {
+      for (int i = 0; i < g; ++i) enqueue_iteration();
+      issued += g;
+    }
+    GPK_CUDA(cudaMemcpyAsync(&ctx->ctl_host[k & 1], ctl, sizeof(CgCtl), cudaMemcpyDeviceToHost, s));
+    GPK_CUDA(cudaEventRecord(ctx->ev[k & 1], s));
+    if (pending) {
+      GPK_CUDA(cudaEventSynchronize(ctx->ev[(k - 1) & 1]));
+      if (ctx->ctl_host[(k - 1) & 1].stop) break;
+    }
+    if (g <= 0) {
+      GPK_CUDA(cudaEventSynchronize(ctx->ev[k & 1]));
+      break;
+    }
+    pending = true;
+    ++k;
+  }
+  GPK_CUDA(cudaStreamSynchronize(s));
+}
+
+void init_ctl(gpk_batch* b, int budget, int iters) {
+  CgCtl h{};
+  h.budget = budget;
+  h.iters = iters;
+  GPK_CUDA(cudaMemcpyAsync(b->ctl.ensure(1), &h, sizeof(CgCtl), cudaMemcpyHostToDevice, b->op->ctx->stream));
+  GPK_CUDA(cudaStreamSynchronize(b->op->ctx->stream));
+}
+
+CgCtl read_ctl(gpk_batch* b) {
+  CgCtl h{};
+  GPK_CUDA(cudaMemcpyAsync(&h, b->ctl.p, sizeof(CgCtl), cudaMemcpyDeviceToHost, b->op->ctx->stream));
+  GPK_CUDA(cudaStreamSynchronize(b->op->ctx->stream));
+  return h;
+}
+
+int iteration_group(int n) { return n >= 32768 ? 1 : (n >= 8192 ? 2 : 4); }
+
+// --------------------------------------------------------------- solvers
+void solve_cg(gpk_batch* b, const gpk_solver_config* c, gpk_precond* pc, gpk_solver_report* rep) {
+  validate(c);
+  const auto start = Clock::now();
+  gpk_operator* op = b->op;
+  cudaStream_t s = op->ctx->stream;
+  const int n = b->n, m = b->m, G = kReduceGroups;
+  if (m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
+  std::memset(rep, 0, sizeof(*rep));
+  const size_t nm = static_cast<size_t>(n) * m;
+  double* d = b->w1.ensure(nm);
+  double* p = b->w2.ensure(nm);
+  double* hd = b->w3.ensure(nm);
+  float* d32 = b->f32.ensure(static_cast<size_t>(n) * kv_ld_for(m));
+  double* part = b->red.ensure(static_cast<size_t>(G) * 2 * m + 8);
+  double* gamma = b->vec1.ensure(m);
+  double* alpha = b->vec2.ensure(m);
+  double* beta = b->vec3.ensure(std::max(m, 3));
+  init_ctl(b, c->max_epochs, 0);
+  CgCtl* ctl = b->ctl.p;
+  const int* stop = &ctl->stop;
+
+  refresh_residuals(b);                                       // solvers.cpp:45
+  precond_apply_dev(pc, op, b->residuals.p, m, p, nullptr);   // p = P^-1 r
+  GPK_CUDA(cudaMemcpyAsync(d, p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, s));
+  to_f32_launch(d, n, m, m, d32, kv_ld_for(m), nullptr, s);
+  col_reduce_launch(b->residuals.p, p, n, m, m, 1, part, G, nullptr, s);
+  cg_init_scalars_launch(part, G, m, b->scales_dev.p, c->tolerance, gamma, ctl, s);
+
+  auto iteration = [&]() {  // solvers.cpp:52-82
+    KvCall kc;
+    kc.v = d32;
+    kc.m = m;
+    kc.R = n;
+    kc.C = n;
+    kc.vdiag = d;
+    kc.out = hd;
+    kc.ldo = m;
+    kc.skip = stop;
+    run_kv(op, kc);
+    col_reduce_launch(d, hd, n, m, m, 0, part, G, stop, s);
+    cg_alpha_launch(part, G, m, gamma, alpha, ctl, s);
+    cg_update_launch(b->solutions.p, b->residuals.p, d, hd, alpha, n, m, stop, s);
+    precond_apply_dev(pc, op, b->residuals.p, m, p, stop);
+    col_reduce_launch(b->residuals.p, p, n, m, m, 1, part, G, stop, s);
+    cg_beta_launch(part, G, m, b->scales_dev.p, c->tolerance, gamma, beta, ctl, s);
+    cg_direction_launch(d, p, beta, n, m, d32, kv_ld_for(m), stop, s);
+  };
+  drive(b, ctl, iteration_group(n), c->max_epochs, iteration);
+  const CgCtl h = read_ctl(b);
+  rep->iterations = h.iters;
+  rep->epochs_consumed = h.iters;
+  rep->aborted = h.aborted;
+  if (h.aborted) std::strncpy(rep->abort_reason, "cg breakdown: non-finite step size", 127);
+  finalise(b, c->tolerance, rep, start);
+}
+
+// SPD inverses of `batch` dim x dim matrices (in place input destroyed).
+void spd_inverse_batched(gpk_ctx* ctx, double* mats, int dim, int batch, double* inv) {
+  cudaStream_t s = ctx->stream;
+  GPK_CUDA(cudaSetDevice(ctx->device));
+  if (cusolverDnSetStream(ctx->solver, s) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnSetStream");
+  if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+  std::vector<double*> ha(batch), hb(batch);
+  for (int k = 0; k < batch; ++k) {
+    ha[k] = mats + static_cast<size_t>(k) * dim * dim;
+    hb[k] = inv + static_cast<size_t>(k) * dim * dim;
+  }
+  DBuf<double*> da, db;
+  DBuf<int> info;
+  da.ensure(batch);
+  db.ensure(batch);
+  info.ensure(batch);
+  GPK_CUDA(cudaMemcpyAsync(da.p, ha.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice, s));
+  GPK_CUDA(cudaMemcpyAsync(db.p, hb.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice, s));
+  if (cusolverDnDpotrfBatched(ctx->solver, CUBLAS_FILL_MODE_LOWER, dim, da.p, dim, info.p, batch) !=
+      CUSOLVER_STATUS_SUCCESS)
+    throw CudaError("cusolverDnDpotrfBatched");
+  count_launch();
+  std::vector<int> hinfo(batch);
+  GPK_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
+  // identity into inv
+  std::vector<double> eye(static_cast<size_t>(dim) * dim, 0.0);
+  for (int i = 0; i < dim; ++i) eye[static_cast<size_t>(i) * dim + i] = 1.0;
+  for (int k = 0; k < batch; ++k)
+    GPK_CUDA(cudaMemcpyAsync(hb[k], eye.data(), sizeof(double) * dim * dim, cudaMemcpyHostToDevice, s));
+  GPK_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < batch; ++k)
+    if (hinfo[k] != 0)
+      throw NumericError("solve_ap: block Cholesky failed; block is not positive definite (noise scale too small)");
+  const double one = 1.0;
+  if (cublasDtrsmBatched(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, dim,
+                         dim, &one, da.p, dim, db.p, dim, batch) != CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDtrsmBatched");
+  if (cublasDtrsmBatched(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, dim,
+                         dim, &one, da.p, dim, db.p, dim, batch) != CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDtrsmBatched");
+  count_launch(2);
+  GPK_CUDA(cudaStreamSynchronize(s));
+}
+
+__global__ void pad_identity_kernel(double* blk, int block, int len) {
+  for (int i = len + blockIdx.x * blockDim.x + threadIdx.x; i < block; i += gridDim.x * blockDim.x)
+    blk[static_cast<size_t>(i) * block + i] = 1.0;
+}
+
+void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) {
+  validate(c);
+  const auto start = Clock::now();
+  gpk_operator* op = b->op;
+  cudaStream_t s = op->ctx->stream;
+  const int n = b->n, m = b->m, G = kReduceGroups;
+  if (m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
+  std::memset(rep, 0, sizeof(*rep));
+  const int block = std::min(c->block_size, n);
+  const int nblocks = (n + block - 1) / block;
+  const double max_iterations = static_cast<double>(c->max_epochs) * n / block;  // solvers.cpp:118
+  const int budget = static_cast<int>(std::ceil(max_iterations));
+  refresh_residuals(b);
+  // inverse of every diagonal block H[blk, blk] (FP64), computed once per call
+  const size_t bb = static_cast<size_t>(block) * block;
+  double* mats = b->w1.ensure(bb * nblocks);
+  double* inv = b->blocks.ensure(bb * nblocks);
+  GPK_CUDA(cudaMemsetAsync(mats, 0, sizeof(double) * bb * nblocks, s));
+  for (int k = 0; k < nblocks; ++k) {
+    const int r0 = k * block, len = std::min(block, n - r0);
+    dense_block64_launch(op->xs64.p, n, op->d, op->s2, op->sigma2, r0, len, r0, len, mats + k * bb, block, 1, s);
+    if (len < block) {
+      pad_identity_kernel<<<1, 256, 0, s>>>(mats + k * bb, block, len);
+      check_launch("pad_identity");
+    }
+  }
+  spd_inverse_batched(op->ctx, mats, block, nblocks, inv);
+  std::vector<double> inv_scales(m);
+  for (int j = 0; j < m; ++j) inv_scales[j] = 1.0 / b->scales[j];
+  double* inv_scales_dev = b->vec1.ensure(m);
+  GPK_CUDA(cudaMemcpyAsync(inv_scales_dev, inv_scales.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
+  double* scores = b->vec2.ensure(nblocks);
+  int* sel = b->ibuf.ensure(1);
+  double* upd64 = b->w2.ensure(static_cast<size_t>(block) * m);
+  float* upd32 = b->f32.ensure(static_cast<size_t>(std::max(block, n)) * kv_ld_for(m));
+  double* part = b->red.ensure(static_cast<size_t>(G) * 2 * m + 8);
+  init_ctl(b, budget, -1);
+  CgCtl* ctl = b->ctl.p;
+  const int* stop = &ctl->stop;
+  col_reduce_launch(b->residuals.p, nullptr, n, m, m, 2, part, G, nullptr, s);
+  ap_check_launch(part, G, m, b->scales_dev.p, c->tolerance, ctl, s);  // iters -1 -> 0, initial test
+
+  auto iteration = [&]() {  // solvers.cpp:120-140
+    ap_scores_launch(b->residuals.p, n, m, inv_scales_dev, block, nblocks, scores, stop, s);
+    ap_select_launch(scores, nblocks, sel, stop, s);
+    ap_block_update_launch(inv, block, n, sel, b->residuals.p, m, b->solutions.p, upd64, upd32, kv_ld_for(m), stop, s);
+    KvCall kc;
+    kc.v = upd32;
+    kc.m = m;
+    kc.R = n;
+    kc.sel = sel;
+    kc.sel_block = block;
+    kc.vdiag = upd64;
+    kc.out = b->residuals.p;
+    kc.ldo = m;
+    kc.base = b->residuals.p;
+    kc.ldb = m;
+    kc.alpha = -1.0;
+    kc.skip = stop;
+    run_kv(op, kc);
+    col_reduce_launch(b->residuals.p, nullptr, n, m, m, 2, part, G, stop, s);
+    ap_check_launch(part, G, m, b->scales_dev.p, c->tolerance, ctl, s);
+  };
+  drive(b, ctl, 8, budget, iteration);
+  const CgCtl h = read_ctl(b);
+  rep->iterations = h.iters;
+  rep->epochs_consumed = static_cast<double>(h.iters) * block / n;
+  finalise(b, c->tolerance, rep, start);
+}
+
+void solve_sgd(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) {
+  validate(c);
+  const auto start = Clock::now();
+  gpk_operator* op = b->op;
+  cudaStream_t s = op->ctx->stream;
+  const int n = b->n, m = b->m, G = kReduceGroups;
+  if (m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
+  std::memset(rep, 0, sizeof(*rep));
+  rep->residuals_estimated = 1;
+  const int bs = std::min(c->batch_size, n);
+  const double max_iterations = static_cast<double>(c->max_epochs) * n / bs;
+  const int budget = static_cast<int>(std::ceil(max_iterations));
+  const double step = c->learning_rate / bs;
+  const size_t nm = static_cast<size_t>(n) * m;
+  const int ld = kv_ld_for(m);
+  GPK_CUDA(cudaMemcpyAsync(b->residuals.p, b->targets.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, s));
+  double* M = b->w1.ensure(nm);
+  GPK_CUDA(cudaMemsetAsync(M, 0, sizeof(double) * nm, s));
+  float* V32 = b->f32.ensure(static_cast<size_t>(n) * ld);
+  to_f32_launch(b->solutions.p, n, m, m, V32, ld, nullptr, s);
+  double* hv = b->w2.ensure(static_cast<size_t>(bs) * m);
+  double* grad = b->w3.ensure(static_cast<size_t>(bs) * m);
+  double* part = b->red.ensure(static_cast<size_t>(G) * 2 * m + 8);
+  double* sumsq = b->vec1.ensure(m);
+  int* pos = b->ibuf2.ensure(n);
+  GPK_CUDA(cudaMemsetAsync(pos, 0xff, sizeof(int) * n, s));  // -1
+  int* nonfinite = b->flag.ensure(1);
+  GPK_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), s));
+  col_reduce_launch(b->residuals.p, nullptr, n, m, m, 2, part, G, nullptr, s);
+  sum_partials_launch(part, G, m, sumsq, nullptr, s);
+  init_ctl(b, budget, -1);
+  CgCtl* ctl = b->ctl.p;
+  const int* stop = &ctl->stop;
+  sgd_check_launch(sumsq, m, b->scales_dev.p, c->tolerance, nonfinite, ctl, s);  // initial test
+
+  const int chunk = 256;
+  int* idxbuf = b->ibuf.ensure(static_cast<size_t>(chunk) * bs);
+  int t = 0;
+  auto iteration = [&]() {  // solvers.cpp:164-178
+    if (t % chunk == 0) sgd_batches_launch(c->seed, c->substream, n, bs, t, std::min(chunk, budget - t), idxbuf, s);
+    const int* idx = idxbuf + static_cast<size_t>(t % chunk) * bs;
+    KvCall kc;
+    kc.v = V32;
+    kc.m = m;
+    kc.row_idx = idx;
+    kc.R = bs;
+    kc.C = n;
+    kc.vdiag = b->solutions.p;
+    kc.out = hv;
+    kc.ldo = m;
+    kc.skip = stop;
+    run_kv(op, kc);
+    sgd_step_launch(hv, idx, bs, b->targets.p, grad, m, stop, s);
+    sgd_scatter_launch(idx, bs, pos, 1, stop, s);
+    sgd_update_launch(M, b->solutions.p, V32, ld, pos, grad, c->momentum, step, n, m, nonfinite, stop, s);
+    sgd_residual_launch(b->residuals.p, idx, bs, grad, m, sumsq, stop, s);
+    sgd_scatter_launch(idx, bs, pos, 0, stop, s);
+    sgd_check_launch(sumsq, m, b->scales_dev.p, c->tolerance, nonfinite, ctl, s);
+    ++t;
+  };
+  // Batches of a chunk are generated before its first iteration; the driver
+  // must not run ahead past a chunk boundary with a stale buffer, which the
+  // in-order stream guarantees.
+  drive(b, ctl, std::max(1, iteration_group(n) * 4), budget, iteration);
+  const CgCtl h = read_ctl(b);
+  rep->iterations = h.iters;
+  rep->epochs_consumed = static_cast<double>(h.iters) * bs / n;
+  rep->aborted = h.aborted;
+  if (h.aborted) std::strncpy(rep->abort_reason, "sgd divergence: non-finite iterate", 127);
+  finalise(b, c->tolerance, rep, start);
+}
+
+void solve_dispatch(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) {  // solvers.cpp:186-202
+  switch (c->kind) {
+    case GPK_CG:
+      if (c->preconditioner_rank > 0) {
+        gpk_precond pc;
+        pc.op = b->op;
+        pc.n = b->n;
+        pc.rank = std::min(c->preconditioner_rank, b->n);
+        build_precond(&pc);
+        return solve_cg(b, c, &pc, rep);
+      }
+      return solve_cg(b, c, nullptr, rep);
+    case GPK_AP:
+      return solve_ap(b, c, rep);
+    case GPK_SGD:
+      return solve_sgd(b, c, rep);
+  }
+  throw std::logic_error("solve: unknown solver kind");
+}
+
+// ------------------------------------------------------------- gradients
+// Quadratic forms for pairs given as device FP64 row-major matrices with a
+// column offset (so batch solutions can be used in place). out: npairs x (d+2).
+struct PairDev {
+  const double* u;
+  const double* w;
+  int ldu, ldw, col0, cols;
+};
+
+__global__ void extract_f32_kernel(const double* src, int n, int lds, int col0, int cols, float* dst, int ldd) {
+  const long long total = static_cast<long long>(n) * ldd;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / ldd), j = static_cast<int>(e % ldd);
+    dst[e] = j < cols ? static_cast<float>(src[static_cast<size_t>(i) * lds + col0 + j]) : 0.f;
+  }
+}
+
+__global__ void pair_dot_kernel(const double* u, const double* w, int n, int ldu, int ldw, int col0, int cols,
+                                double* part) {
+  __shared__ double red[256];
+  const int g = blockIdx.x, G = gridDim.x;
+  const long long rb = static_cast<long long>(n) * g / G, re = static_cast<long long>(n) * (g + 1) / G;
+  double acc = 0.0;
+  for (long long e = rb * cols + threadIdx.x; e < re * cols; e += blockDim.x) {
+    const long long i = e / cols;
+    const int j = static_cast<int>(e % cols);
+    acc += u[i * ldu + col0 + j] * w[i * ldw + col0 + j];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[g] = red[0];
+}
+
+std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vector<PairDev>& pairs) {
+  cudaStream_t s = op->ctx->stream;
+  const int n = op->n, d = op->d, P = static_cast<int>(pairs.size());
+  if (P < 1 || P > 2) throw InvalidArgument("derivative_quadratic_forms: 1 or 2 pairs supported");
+  std::vector<DBuf<float>> bufs(2 * P);
+  GradArgs a{};
+  a.xs = op->xs32.p;
+  a.n = n;
+  a.d = d;
+  a.dp = op->dp;
+  a.npairs = P;
+  a.symmetric = 1;
+  for (int p = 0; p < P; ++p) {
+    const PairDev& pd = pairs[p];
+    const int ld = (pd.cols + 3) / 4 * 4;
+    float* u32 = bufs[2 * p].ensure(static_cast<size_t>(n) * ld);
+    const long long tot = static_cast<long long>(n) * ld;
+    const int nb = static_cast<int>(std::min<long long>((tot + 255) / 256, 148 * 16));
+    extract_f32_kernel<<<nb, 256, 0, s>>>(pd.u, n, pd.ldu, pd.col0, pd.cols, u32, ld);
+    check_launch("extract_f32");
+    const float* w32 = u32;
+    if (pd.w != pd.u || pd.ldw != pd.ldu) {
+      float* wb = bufs[2 * p + 1].ensure(static_cast<size_t>(n) * ld);
+      extract_f32_kernel<<<nb, 256, 0, s>>>(pd.w, n, pd.ldw, pd.col0, pd.cols, wb, ld);
+      check_launch("extract_f32");
+      w32 = wb;
+      a.symmetric = 0;
+    }
+    a.u[p] = u32;
+    a.w[p] = w32;
+    a.mcols[p] = pd.cols;
+    a.ldu[p] = ld;
+  }
+  a.s2 = static_cast<float>(op->s2);
+  a.log2_s2 = static_cast<float>(std::log2(op->s2));
+  a.blocks = 2 * op->ctx->sms;
+  const int per = P * (d + 1);
+  DBuf<double> part, tot, dots;
+  part.ensure(static_cast<size_t>(a.blocks) * per);
+  tot.ensure(per);
+  a.part = part.p;
+  grad_launch(a, s);
+  sum_partials_launch(part.p, a.blocks, per, tot.p, nullptr, s);
+  // noise terms: sum u.w (FP64)
+  const int G = kReduceGroups;
+  dots.ensure(static_cast<size_t>(G) * P);
+  for (int p = 0; p < P; ++p) {
+    pair_dot_kernel<<<G, 256, 0, s>>>(pairs[p].u, pairs[p].w, n, pairs[p].ldu, pairs[p].ldw, pairs[p].col0,
+                                      pairs[p].cols, dots.p + static_cast<size_t>(p) * G);
+    check_launch("pair_dot");
+  }
+  std::vector<double> th(per), dh(static_cast<size_t>(G) * P);
+  GPK_CUDA(cudaMemcpyAsync(th.data(), tot.p, sizeof(double) * per, cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaMemcpyAsync(dh.data(), dots.p, sizeof(double) * G * P, cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaStreamSynchronize(s));
+  std::vector<std::vector<double>> out(P, std::vector<double>(d + 2, 0.0));
+  for (int p = 0; p < P; ++p) {
+    double uw = 0.0;
+    for (int g = 0; g < G; ++g) uw += dh[static_cast<size_t>(p) * G + g];
+    out[p][d + 1] = 2.0 * op->sigma * uw;                                     // kernel.cpp:249-252
+    out[p][d] = (2.0 / op->s) * (op->s2 * th[static_cast<size_t>(p) * (d + 1) + d]);  // kernel.cpp:264
+    for (int k = 0; k < d; ++k)                                                // kernel.cpp:265-268
+      out[p][k] = op->inv_ls[k] * (3.0 * op->s2 * th[static_cast<size_t>(p) * (d + 1) + k]);
+  }
+  return out;
+}
+
+void assemble(const std::vector<std::vector<double>>& f, int s_count, int P, double* values, double* quad,
+              double* trace) {  // gradients.cpp:39-50
+  for (int k = 0; k < P; ++k) {
+    const double q = f[0][k], t = f[1][k] / s_count;
+    if (quad) quad[k] = q;
+    if (trace) trace[k] = t;
+    if (values) values[k] = 0.5 * q - 0.5 * t;
+  }
+}
+
+// ------------------------------------------------------------------ RFF
+void build_basis_host(gpk_rff_basis* b) {  // rff.cpp:10-34
+  const int P = b->pairs, d = b->d, S = b->samples;
+  b->freq.assign(static_cast<size_t>(P) * d, 0.0);
+  HostStream fs(b->seed, 3, b->substream);
+  auto gauss = [](HostStream& st) -> double {
+    if (st.has_cached) {
+      st.has_cached = false;
+      return st.cached;
+    }
+    const double u1 = static_cast<double>((st.next_u64() >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>(st.next_u64() >> 11) * 0x1.0p-53;
+    const double radius = std::sqrt(-2.0 * std::log(u1));
+    const double angle = 2.0 * 3.141592653589793 * u2;
+    st.cached = radius * std::sin(angle);
+    st.has_cached = true;
+    return radius * std::cos(angle);
+  };
+  for (int p = 0; p < P; ++p) {
+    double chi2 = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      const double g = gauss(fs);
+      chi2 += g * g;
+    }
+    const double scale = std::sqrt(3.0 / chi2);
+    for (int k = 0; k < d; ++k) b->freq[static_cast<size_t>(k) * P + p] = scale * gauss(fs);
+  }
+  b->weights.assign(static_cast<size_t>(2 * P) * S, 0.0);
+  HostStream ws(b->seed, 4, b->substream);
+  for (auto& w : b->weights) w = gauss(ws);
+}
+
+// prior (row-major [n][s]) at the operator's inputs; freq divided by current l.
+void rff_prior_dev(gpk_operator* op, gpk_rff_basis* b, int s_count, double* prior) {
+  cudaStream_t s = op->ctx->stream;
+  const int P = b->pairs, d = op->d;
+  std::vector<double> f(static_cast<size_t>(P) * d);  // row-major [P][d]
+  for (int p = 0; p < P; ++p)
+    for (int k = 0; k < d; ++k) f[static_cast<size_t>(p) * d + k] = b->freq[static_cast<size_t>(k) * P + p] * op->inv_ls[k];
+  double* fd = b->freq_dev.ensure(f.size());
+  GPK_CUDA(cudaMemcpyAsync(fd, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice, s));
+  if (!b->w_dev.p) {
+    b->w_dev.ensure(b->weights.size());
+    GPK_CUDA(cudaMemcpyAsync(b->w_dev.p, b->weights.data(), sizeof(double) * b->weights.size(),
+                             cudaMemcpyHostToDevice, s));
+  }
+  const double amplitude = op->s / std::sqrt(static_cast<double>(P));  // rff.cpp:47
+  rff_prior_launch(op->x64.p, op->n, d, fd, P, b->w_dev.p, 2 * P, s_count, amplitude, prior, s);
+  GPK_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* gpk_last_error(void) { return g_err.c_str(); }
+const char* gpk_version(void) { return "gpk 0.1 (sm_100a)"; }
+int gpk_rhs_ld(int m) { return kv_ld_for(m); }
+
+gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
+  return guarded([&] {
+    auto c = std::make_unique<gpk_ctx>();
+    c->device = device;
+    GPK_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    GPK_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CudaError("gpk: libgpk is built for sm_100a (B200); device is sm_" +
+                                          std::to_string(prop.major) + std::to_string(prop.minor));
+    c->sms = prop.multiProcessorCount;
+    GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate");
+    if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate");
+    GPK_CUDA(cudaMallocHost(&c->ctl_host, 2 * sizeof(CgCtl)));
+    GPK_CUDA(cudaEventCreateWithFlags(&c->ev[0], cudaEventDisableTiming));
+    GPK_CUDA(cudaEventCreateWithFlags(&c->ev[1], cudaEventDisableTiming));
+    GPK_CUDA(cudaMalloc(&c->stats, 2 * sizeof(double)));
+    GPK_CUDA(cudaMemset(c->stats, 0, 2 * sizeof(double)));
+    *out = c.release();
+  });
+}
+
+gpk_status gpk_ctx_destroy(gpk_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cublasDestroy(c->blas);
+    cusolverDnDestroy(c->solver);
+    cudaFreeHost(c->ctl_host);
+    cudaEventDestroy(c->ev[0]);
+    cudaEventDestroy(c->ev[1]);
+    for (auto& pr : c->prof) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    cudaFree(c->stats);
+    cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+gpk_status gpk_ctx_synchronize(gpk_ctx* c) {
+  return guarded([&] { GPK_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+gpk_status gpk_ctx_launch_count(gpk_ctx* c, long long* out) {
+  return guarded([&] { *out = c->launches; });
+}
+gpk_status gpk_ctx_stream(gpk_ctx* c, void** out) {
+  return guarded([&] { *out = static_cast<void*>(c->stream); });
+}
+gpk_status gpk_ctx_set_profiling(gpk_ctx* c, int enable) {
+  return guarded([&] { c->profiling = enable != 0; });
+}
+gpk_status gpk_ctx_reset_stats(gpk_ctx* c) {
+  return guarded([&] {
+    GPK_CUDA(cudaSetDevice(c->device));
+    GPK_CUDA(cudaStreamSynchronize(c->stream));
+    GPK_CUDA(cudaMemset(c->stats, 0, 2 * sizeof(double)));
+    c->prof_used = 0;
+  });
+}
+gpk_status gpk_ctx_stats(gpk_ctx* c, double* out) {
+  return guarded([&] {
+    GPK_CUDA(cudaSetDevice(c->device));
+    GPK_CUDA(cudaStreamSynchronize(c->stream));
+    GPK_CUDA(cudaMemcpy(out, c->stats, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+    double ms = 0.0;
+    for (size_t i = 0; i < c->prof_used; ++i) {
+      float t = 0.f;
+      GPK_CUDA(cudaEventElapsedTime(&t, c->prof[i].first, c->prof[i].second));
+      ms += t;
+    }
+    out[2] = static_cast<double>(c->prof_used);
+    out[3] = ms;
+  });
+}
+
+gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d, const double* raw,
+                               gpk_operator** out) {
+  return guarded([&] {
+    LaunchScope ls(ctx);
+    require(n >= 1 && d >= 1, "KernelOperator: n >= 1 and d >= 1");
+    if (d > 32) throw InvalidArgument("gpk: input dimension > 32 is not supported");
+    require(all_finite(inputs, static_cast<size_t>(n) * d), "KernelOperator: non-finite input");
+    auto op = std::make_unique<gpk_operator>();
+    op->ctx = ctx;
+    op->n = n;
+    op->d = d;
+    op->dp = (d + 3) / 4 * 4;
+    op->x64.ensure(static_cast<size_t>(n) * d);
+    op->xs32.ensure(static_cast<size_t>(n) * op->dp);
+    op->xs64.ensure(static_cast<size_t>(n) * d);
+    upload_colmajor(op.get(), inputs, n, d, op->x64.p);
+    set_hyper(op.get(), raw);
+    *out = op.release();
+  });
+}
+
+gpk_status gpk_operator_set_hyperparameters(gpk_operator* op, const double* raw) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    set_hyper(op, raw);
+  });
+}
+
+gpk_status gpk_operator_destroy(gpk_operator* op) {
+  return guarded([&] { delete op; });
+}
+
+gpk_status gpk_operator_size(const gpk_operator* op, int* n, int* d) {
+  return guarded([&] {
+    *n = op->n;
+    *d = op->d;
+  });
+}
+
+gpk_status gpk_apply(gpk_operator* op, const double* v, int m, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(m >= 1, "KernelOperator::apply: m >= 1");
+    require(all_finite(v, static_cast<size_t>(op->n) * m), "KernelOperator::apply: non-finite input");  // kernel.cpp:135
+    const int n = op->n;
+    double* v64 = op->v64.ensure(static_cast<size_t>(n) * m);
+    double* o64 = op->out64.ensure(static_cast<size_t>(n) * m);
+    upload_colmajor(op, v, n, m, v64);
+    std::vector<double> tmp(static_cast<size_t>(n) * std::min(m, kMaxRhs));
+    for (int j0 = 0; j0 < m; j0 += kMaxRhs) {
+      const int mm = std::min(kMaxRhs, m - j0);
+      DBuf<double> sub, so;
+      const double* src = v64;
+      double* dst = o64;
+      if (mm != m) {
+        sub.ensure(static_cast<size_t>(n) * mm);
+        so.ensure(static_cast<size_t>(n) * mm);
+        // gather columns j0..j0+mm of row-major v64
+        GPK_CUDA(cudaMemcpy2DAsync(sub.p, sizeof(double) * mm, v64 + j0, sizeof(double) * m, sizeof(double) * mm, n,
+                                   cudaMemcpyDeviceToDevice, op->ctx->stream));
+        src = sub.p;
+        dst = so.p;
+      }
+      float* v32 = op->v32.ensure(static_cast<size_t>(n) * kv_ld_for(mm));
+      apply_dev64(op, src, mm, dst, nullptr, 1.0, v32, nullptr);
+      if (mm != m)
+        GPK_CUDA(cudaMemcpy2DAsync(o64 + j0, sizeof(double) * m, so.p, sizeof(double) * mm, sizeof(double) * mm, n,
+                                   cudaMemcpyDeviceToDevice, op->ctx->stream));
+      if (mm != m) GPK_CUDA(cudaStreamSynchronize(op->ctx->stream));
+    }
+    download_colmajor(op, o64, n, m, out);
+  });
+}
+
+gpk_status gpk_apply_device(gpk_operator* op, const float* v, int m, double* out, int ldo) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(m >= 1 && m <= kMaxRhs, "gpk_apply_device: 1 <= m <= 65");
+    KvCall c;
+    c.v = v;
+    c.m = m;
+    c.R = op->n;
+    c.C = op->n;
+    c.out = out;
+    c.ldo = ldo;
+    run_kv(op, c);
+  });
+}
+
+gpk_status gpk_apply_rows(gpk_operator* op, const int* rows, int count, const double* v, int m, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(m >= 1 && m <= kMaxRhs, "apply_rows: 1 <= m <= 65");
+    require(count >= 1, "apply_rows: count >= 1");
+    for (int r = 0; r < count; ++r)
+      if (rows[r] < 0 || rows[r] >= op->n) throw OutOfRange("apply_rows: row index");
+    const int n = op->n;
+    cudaStream_t s = op->ctx->stream;
+    double* v64 = op->v64.ensure(static_cast<size_t>(n) * m);
+    upload_colmajor(op, v, n, m, v64);
+    float* v32 = op->v32.ensure(static_cast<size_t>(n) * kv_ld_for(m));
+    to_f32_launch(v64, n, m, m, v32, kv_ld_for(m), nullptr, s);
+    int* idx = op->idx.ensure(count);
+    GPK_CUDA(cudaMemcpyAsync(idx, rows, sizeof(int) * count, cudaMemcpyHostToDevice, s));
+    double* o64 = op->out64.ensure(static_cast<size_t>(count) * m);
+    KvCall c;
+    c.v = v32;
+    c.m = m;
+    c.row_idx = idx;
+    c.R = count;
+    c.C = n;
+    c.vdiag = v64;
+    c.out = o64;
+    c.ldo = m;
+    run_kv(op, c);
+    download_colmajor(op, o64, count, m, out);
+  });
+}
+
+gpk_status gpk_apply_columns(gpk_operator* op, int c0, int len, const double* u, int m, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(m >= 1 && m <= kMaxRhs, "apply_columns: 1 <= m <= 65");
+    if (c0 < 0 || len < 1 || c0 + len > op->n) throw OutOfRange("apply_columns: column range");
+    const int n = op->n;
+    cudaStream_t s = op->ctx->stream;
+    double* u64 = op->v64.ensure(static_cast<size_t>(len) * m);
+    upload_colmajor(op, u, len, m, u64);
+    float* u32 = op->v32.ensure(static_cast<size_t>(len) * kv_ld_for(m));
+    to_f32_launch(u64, len, m, m, u32, kv_ld_for(m), nullptr, s);
+    double* o64 = op->out64.ensure(static_cast<size_t>(n) * m);
+    KvCall c;
+    c.v = u32;
+    c.m = m;
+    c.R = n;
+    c.c0 = c0;
+    c.C = len;
+    c.vdiag = u64;
+    c.out = o64;
+    c.ldo = m;
+    run_kv(op, c);
+    download_colmajor(op, o64, n, m, out);
+  });
+}
+
+gpk_status gpk_dense_block(gpk_operator* op, int r0, int rows, int c0, int cols, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    if (r0 < 0 || c0 < 0 || rows < 0 || cols < 0 || r0 + rows > op->n || c0 + cols > op->n)
+      throw OutOfRange("dense_block: range");
+    if (rows == 0 || cols == 0) return;
+    double* o = op->out64.ensure(static_cast<size_t>(rows) * cols);
+    dense_block64_launch(op->xs64.p, op->n, op->d, op->s2, op->sigma2, r0, rows, c0, cols, o, cols, 1,
+                         op->ctx->stream);
+    download_colmajor(op, o, rows, cols, out);
+  });
+}
+
+gpk_status gpk_kernel_column(gpk_operator* op, int i, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    if (i < 0 || i >= op->n) throw OutOfRange("kernel_column: index");
+    double* o = op->out64.ensure(op->n);
+    dense_block64_launch(op->xs64.p, op->n, op->d, op->s2, op->sigma2, i, 1, 0, op->n, o, op->n, 0, op->ctx->stream);
+    GPK_CUDA(cudaMemcpyAsync(out, o, sizeof(double) * op->n, cudaMemcpyDeviceToHost, op->ctx->stream));
+    GPK_CUDA(cudaStreamSynchronize(op->ctx->stream));
+  });
+}
+
+gpk_status gpk_kernel_diagonal(gpk_operator* op, double* out) {
+  return guarded([&] {
+    for (int i = 0; i < op->n; ++i) out[i] = op->s2;
+  });
+}
+
+gpk_status gpk_derivative_quadratic_forms_many(gpk_operator* op, int npairs, const double* const* u,
+                                               const double* const* w, const int* cols, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(npairs >= 1 && npairs <= 2, "derivative_quadratic_forms: 1 or 2 pairs supported");
+    const int n = op->n;
+    std::vector<std::unique_ptr<DBuf<double>>> bufs;
+    std::vector<PairDev> pairs;
+    for (int p = 0; p < npairs; ++p) {
+      require(cols[p] >= 1, "derivative_quadratic_forms: shape mismatch");
+      auto ub = std::make_unique<DBuf<double>>();
+      ub->ensure(static_cast<size_t>(n) * cols[p]);
+      upload_colmajor(op, u[p], n, cols[p], ub->p);
+      const double* wp = ub->p;
+      if (w[p] != u[p]) {
+        auto wb = std::make_unique<DBuf<double>>();
+        wb->ensure(static_cast<size_t>(n) * cols[p]);
+        upload_colmajor(op, w[p], n, cols[p], wb->p);
+        wp = wb->p;
+        bufs.push_back(std::move(wb));
+      }
+      pairs.push_back({ub->p, wp, cols[p], cols[p], 0, cols[p]});
+      bufs.push_back(std::move(ub));
+    }
+    const auto f = quad_forms_dev(op, pairs);
+    for (int p = 0; p < npairs; ++p)
+      for (int k = 0; k < op->d + 2; ++k) out[static_cast<size_t>(p) * (op->d + 2) + k] = f[p][k];
+  });
+}
+
+// ---- precond ----
+gpk_status gpk_precond_create(gpk_operator* op, int rank, gpk_precond** out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    if (rank < 0 || rank > op->n) throw InvalidArgument("PivotedCholeskyPreconditioner: rank must be in [0, n]");
+    auto p = std::make_unique<gpk_precond>();
+    p->op = op;
+    p->n = op->n;
+    p->rank = rank;
+    build_precond(p.get());
+    *out = p.release();
+  });
+}
+gpk_status gpk_precond_destroy(gpk_precond* p) {
+  return guarded([&] { delete p; });
+}
+gpk_status gpk_precond_info(const gpk_precond* p, int* achieved, int* stopped) {
+  return guarded([&] {
+    *achieved = p->achieved;
+    *stopped = p->stopped;
+  });
+}
+gpk_status gpk_precond_factor(gpk_precond* p, double* factor, int* pivots) {
+  return guarded([&] {
+    LaunchScope ls(p->op->ctx);
+    const int r = p->achieved, n = p->n;
+    if (r == 0) return;
+    cudaStream_t s = p->op->ctx->stream;
+    std::vector<double> h(static_cast<size_t>(n) * p->rank);
+    GPK_CUDA(cudaMemcpyAsync(h.data(), p->L.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    std::vector<int> pv(p->rank);
+    GPK_CUDA(cudaMemcpyAsync(pv.data(), p->pivots.p, sizeof(int) * p->rank, cudaMemcpyDeviceToHost, s));
+    GPK_CUDA(cudaStreamSynchronize(s));
+    if (factor)
+      for (int k = 0; k < r; ++k)
+        for (int i = 0; i < n; ++i) factor[static_cast<size_t>(k) * n + i] = h[static_cast<size_t>(i) * p->rank + k];
+    if (pivots) std::memcpy(pivots, pv.data(), sizeof(int) * r);
+  });
+}
+gpk_status gpk_precond_apply(gpk_precond* p, const double* v, int m, double* out) {
+  return guarded([&] {
+    gpk_operator* op = p->op;
+    LaunchScope ls(op->ctx);
+    const int n = op->n;
+    DBuf<double> v64, o64;
+    v64.ensure(static_cast<size_t>(n) * m);
+    o64.ensure(static_cast<size_t>(n) * m);
+    upload_colmajor(op, v, n, m, v64.p);
+    precond_apply_dev(p, op, v64.p, m, o64.p, nullptr);
+    download_colmajor(op, o64.p, n, m, out);
+  });
+}
+
+// ---- batch ----
+gpk_status gpk_batch_create(gpk_operator* op, const double* targets, int m, gpk_batch** out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(m >= 1, "LinearSystemBatch: at least one column");
+    auto b = std::make_unique<gpk_batch>();
+    b->op = op;
+    b->n = op->n;
+    b->m = m;
+    const size_t nm = static_cast<size_t>(op->n) * m;
+    b->targets.ensure(nm);
+    b->solutions.ensure(nm);
+    b->residuals.ensure(nm);
+    upload_colmajor(op, targets, op->n, m, b->targets.p);
+    GPK_CUDA(cudaMemsetAsync(b->solutions.p, 0, sizeof(double) * nm, op->ctx->stream));
+    GPK_CUDA(cudaMemsetAsync(b->residuals.p, 0, sizeof(double) * nm, op->ctx->stream));
+    b->scales.resize(m);
+    for (int j = 0; j < m; ++j) {  // linear_system.cpp:21
+      double acc = 0.0;
+      const double* col = targets + static_cast<size_t>(j) * op->n;
+      for (int i = 0; i < op->n; ++i) acc += col[i] * col[i];
+      b->scales[j] = std::sqrt(acc) + 1e-12;
+    }
+    b->scales_dev.ensure(m);
+    GPK_CUDA(cudaMemcpyAsync(b->scales_dev.p, b->scales.data(), sizeof(double) * m, cudaMemcpyHostToDevice,
+                             op->ctx->stream));
+    GPK_CUDA(cudaStreamSynchronize(op->ctx->stream));
+    *out = b.release();
+  });
+}
+gpk_status gpk_batch_destroy(gpk_batch* b) {
+  return guarded([&] { delete b; });
+}
+gpk_status gpk_batch_warm_start(gpk_batch* b, const double* prev) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    upload_colmajor(b->op, prev, b->n, b->m, b->solutions.p);
+    GPK_CUDA(cudaStreamSynchronize(b->op->ctx->stream));
+  });
+}
+gpk_status gpk_batch_warm_start_from(gpk_batch* b, const gpk_batch* prev) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    if (prev->n != b->n || prev->m != b->m) throw InvalidArgument("LinearSystemBatch::warm_start: shape mismatch");
+    GPK_CUDA(cudaMemcpyAsync(b->solutions.p, prev->solutions.p, sizeof(double) * b->n * b->m,
+                             cudaMemcpyDeviceToDevice, b->op->ctx->stream));
+  });
+}
+gpk_status gpk_batch_refresh_residuals(gpk_batch* b) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    refresh_residuals(b);
+    GPK_CUDA(cudaStreamSynchronize(b->op->ctx->stream));
+  });
+}
+gpk_status gpk_batch_get(gpk_batch* b, int which, double* out) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    if (which == 3) {
+      std::memcpy(out, b->scales.data(), sizeof(double) * b->m);
+      return;
+    }
+    const double* src = which == 0 ? b->targets.p : which == 1 ? b->solutions.p : which == 2 ? b->residuals.p : nullptr;
+    if (!src) throw OutOfRange("gpk_batch_get: which");
+    download_colmajor(b->op, src, b->n, b->m, out);
+  });
+}
+gpk_status gpk_batch_set(gpk_batch* b, int which, const double* in) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    double* dst = which == 0 ? b->targets.p : which == 1 ? b->solutions.p : which == 2 ? b->residuals.p : nullptr;
+    if (!dst) throw OutOfRange("gpk_batch_set: which");
+    upload_colmajor(b->op, in, b->n, b->m, dst);
+    GPK_CUDA(cudaStreamSynchronize(b->op->ctx->stream));
+  });
+}
+gpk_status gpk_termination_check(gpk_batch* b, double tol, double* mean, double* probe, int* done) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    batch_norms(b, b->residuals.p, tol, mean, probe, done);
+  });
+}
+
+// ---- solvers ----
+gpk_status gpk_solve_cg(gpk_batch* b, const gpk_solver_config* c, gpk_precond* p, gpk_solver_report* r) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    solve_cg(b, c, p, r);
+  });
+}
+gpk_status gpk_solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* r) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    solve_ap(b, c, r);
+  });
+}
+gpk_status gpk_solve_sgd(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* r) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    solve_sgd(b, c, r);
+  });
+}
+gpk_status gpk_solve(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* r) {
+  return guarded([&] {
+    LaunchScope ls(b->op->ctx);
+    solve_dispatch(b, c, r);
+  });
+}
+gpk_status gpk_sgd_batches(gpk_ctx* ctx, int n, const gpk_solver_config* c, int first, int count, int* out) {
+  return guarded([&] {
+    LaunchScope ls(ctx);
+    const int bs = std::min(c->batch_size, n);
+    DBuf<int> buf;
+    buf.ensure(static_cast<size_t>(count) * bs);
+    sgd_batches_launch(c->seed, c->substream, n, bs, first, count, buf.p, ctx->stream);
+    GPK_CUDA(cudaMemcpyAsync(out, buf.p, sizeof(int) * count * bs, cudaMemcpyDeviceToHost, ctx->stream));
+    GPK_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---- gradients ----
+gpk_status gpk_estimate_gradient_pathwise(gpk_operator* op, const double* v_y, const double* zhat, int s,
+                                          double* values, double* quad, double* trace) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(s >= 1, "estimate_gradient_pathwise: shape mismatch");
+    const int n = op->n;
+    DBuf<double> vy, z;
+    vy.ensure(n);
+    z.ensure(static_cast<size_t>(n) * s);
+    GPK_CUDA(cudaMemcpyAsync(vy.p, v_y, sizeof(double) * n, cudaMemcpyHostToDevice, op->ctx->stream));
+    upload_colmajor(op, zhat, n, s, z.p);
+    const auto f = quad_forms_dev(op, {{vy.p, vy.p, 1, 1, 0, 1}, {z.p, z.p, s, s, 0, s}});
+    assemble(f, s, op->d + 2, values, quad, trace);
+  });
+}
+gpk_status gpk_estimate_gradient_standard(gpk_operator* op, const double* v_y, const double* sol,
+                                          const double* probes, int s, double* values, double* quad, double* trace) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(s >= 1, "estimate_gradient_standard: shape mismatch");
+    const int n = op->n;
+    DBuf<double> vy, z, pr;
+    vy.ensure(n);
+    z.ensure(static_cast<size_t>(n) * s);
+    pr.ensure(static_cast<size_t>(n) * s);
+    GPK_CUDA(cudaMemcpyAsync(vy.p, v_y, sizeof(double) * n, cudaMemcpyHostToDevice, op->ctx->stream));
+    upload_colmajor(op, sol, n, s, z.p);
+    upload_colmajor(op, probes, n, s, pr.p);
+    const auto f = quad_forms_dev(op, {{vy.p, vy.p, 1, 1, 0, 1}, {z.p, pr.p, s, s, 0, s}});
+    assemble(f, s, op->d + 2, values, quad, trace);
+  });
+}
+gpk_status gpk_batch_gradient_pathwise(gpk_batch* b, double* values, double* quad, double* trace) {
+  return guarded([&] {
+    gpk_operator* op = b->op;
+    LaunchScope ls(op->ctx);
+    require(b->m >= 2, "estimate_gradient_pathwise: shape mismatch");
+    const int m = b->m;
+    const auto f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1},
+                                       {b->solutions.p, b->solutions.p, m, m, 1, m - 1}});
+    assemble(f, m - 1, op->d + 2, values, quad, trace);
+  });
+}
+
+// ---- RFF ----
+gpk_status gpk_rff_basis_build(gpk_ctx* ctx, int d, int m_pairs, int sample_count, uint64_t seed, uint64_t substream,
+                               gpk_rff_basis** out) {
+  return guarded([&] {
+    if (m_pairs < 1) throw InvalidArgument("build_rff_basis: m_pairs >= 1");
+    if (sample_count < 1) throw InvalidArgument("build_rff_basis: sample_count >= 1");
+    auto b = std::make_unique<gpk_rff_basis>();
+    b->ctx = ctx;
+    b->d = d;
+    b->pairs = m_pairs;
+    b->samples = sample_count;
+    b->seed = seed;
+    b->substream = substream;
+    build_basis_host(b.get());
+    *out = b.release();
+  });
+}
+gpk_status gpk_rff_basis_destroy(gpk_rff_basis* b) {
+  return guarded([&] { delete b; });
+}
+gpk_status gpk_rff_basis_get(const gpk_rff_basis* b, double* freq, double* weights) {
+  return guarded([&] {
+    if (freq) std::memcpy(freq, b->freq.data(), sizeof(double) * b->freq.size());
+    if (weights) std::memcpy(weights, b->weights.data(), sizeof(double) * b->weights.size());
+  });
+}
+gpk_status gpk_pathwise_targets(gpk_operator* op, gpk_rff_basis* basis, int s, uint64_t seed, uint64_t substream,
+                                double* prior, double* noise, double* xi) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    if (s < 1) throw InvalidArgument("pathwise_targets: s >= 1");
+    if (s > basis->samples) throw InvalidArgument("pathwise_targets: basis holds fewer samples than requested");
+    if (basis->d != op->d) throw InvalidArgument("rff_features: point dimension does not match basis");
+    const int n = op->n;
+    cudaStream_t st = op->ctx->stream;
+    DBuf<double> pr, no, x;
+    pr.ensure(static_cast<size_t>(n) * s);
+    no.ensure(static_cast<size_t>(n) * s);
+    x.ensure(static_cast<size_t>(n) * s);
+    rff_prior_dev(op, basis, s, pr.p);
+    gaussian_fill_launch(seed, 5, substream, static_cast<int64_t>(n) * s, n, s, no.p, st);
+    xi_assemble_launch(pr.p, no.p, n, s, op->sigma, nullptr, 0, 0, x.p, st);
+    if (prior) download_colmajor(op, pr.p, n, s, prior);
+    if (noise) download_colmajor(op, no.p, n, s, noise);
+    if (xi) download_colmajor(op, x.p, n, s, xi);
+  });
+}
+
+// ---- outer loop (outer_loop.cpp:57-246) ----
+}  // extern "C"
+
+struct gpk_optimiser {
+  gpk_ctx* ctx = nullptr;
+  gpk_outer_config cfg{};
+  int n = 0, d = 0, s = 0, P = 0, m = 0;
+  std::vector<double> raw, am, av;
+  int astep = 0, t = 0;
+  bool sgd_halved = false, have_previous = false, have_noise = false, aborted = false;
+  uint64_t noise_sub = ~0ull;
+  gpk_solver_config sc{};
+  std::unique_ptr<gpk_operator> op;
+  std::unique_ptr<gpk_batch> batch;
+  std::unique_ptr<gpk_rff_basis> basis;
+  DBuf<double> prev, prior, noise, probes, ycol;
+};
+
+namespace {
+
+void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const double* targets, int n, int d,
+                    const gpk_outer_config* cfg, const double* init_constrained) {
+  validate(&cfg->solver);
+  if (cfg->steps < 0) throw InvalidArgument("optimise: steps >= 0");
+  o->ctx = ctx;
+  o->cfg = *cfg;
+  o->n = n;
+  o->d = d;
+  o->s = cfg->probe_count;
+  o->P = d + 2;
+  o->m = o->s + 1;
+  if (o->s < 1) throw InvalidArgument("optimise: probe_count >= 1");
+  if (cfg->estimator != 1 && cfg->probe_distribution != 0)
+    throw InvalidArgument("gpk_optimise: only Gaussian standard probes are implemented");
+  o->raw.resize(o->P);
+  for (int k = 0; k < o->P; ++k) o->raw[k] = softplus_inverse(init_constrained ? init_constrained[k] : cfg->init_value);
+  o->am.assign(o->P, 0.0);
+  o->av.assign(o->P, 0.0);
+  o->sc = cfg->solver;
+  o->sc.warm_start = cfg->warm_start;
+  gpk_operator* opp = nullptr;
+  if (gpk_operator_create(ctx, inputs, n, d, o->raw.data(), &opp) != GPK_OK) throw InvalidArgument(g_err);
+  o->op.reset(opp);
+  cudaStream_t stream = ctx->stream;
+  o->batch = std::make_unique<gpk_batch>();
+  gpk_batch* b = o->batch.get();
+  b->op = opp;
+  b->n = n;
+  b->m = o->m;
+  const size_t nm = static_cast<size_t>(n) * o->m;
+  b->targets.ensure(nm);
+  b->solutions.ensure(nm);
+  b->residuals.ensure(nm);
+  b->scales.resize(o->m);
+  b->scales_dev.ensure(o->m);
+  o->prev.ensure(nm);
+  o->ycol.ensure(n);
+  GPK_CUDA(cudaMemcpyAsync(o->ycol.p, targets, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+  GPK_CUDA(cudaMemcpy2DAsync(b->targets.p, sizeof(double) * o->m, o->ycol.p, sizeof(double), sizeof(double), n,
+                             cudaMemcpyDeviceToDevice, stream));
+  o->prior.ensure(static_cast<size_t>(n) * o->s);
+  o->noise.ensure(static_cast<size_t>(n) * o->s);
+  GPK_CUDA(cudaStreamSynchronize(stream));
+}
+
+// One outer step (outer_loop.cpp:125-238). Returns false once the run aborted.
+bool optimiser_one_step(gpk_optimiser* o, double* row) {
+  const auto t0 = Clock::now();
+  gpk_ctx* ctx = o->ctx;
+  cudaStream_t stream = ctx->stream;
+  gpk_operator* op = o->op.get();
+  gpk_batch* b = o->batch.get();
+  const int n = o->n, s = o->s, m = o->m, P = o->P, t = o->t;
+  const gpk_outer_config& cfg = o->cfg;
+  const bool pathwise = cfg.estimator == 1;
+  const size_t nm = static_cast<size_t>(n) * m;
+  set_hyper(op, o->raw.data());
+  const uint64_t substream = cfg.warm_start ? 0 : static_cast<uint64_t>(t);
+  if (pathwise) {
+    if (!o->basis || !cfg.warm_start) {
+      gpk_rff_basis* bp = nullptr;
+      if (gpk_rff_basis_build(ctx, o->d, cfg.rff_pairs, s, cfg.feature_seed, substream, &bp) != GPK_OK)
+        throw InvalidArgument(g_err);
+      o->basis.reset(bp);
+    }
+    rff_prior_dev(op, o->basis.get(), s, o->prior.p);
+    if (!o->have_noise || o->noise_sub != substream) {
+      gaussian_fill_launch(cfg.feature_seed, 5, substream, static_cast<int64_t>(n) * s, n, s, o->noise.p, stream);
+      o->have_noise = true;
+      o->noise_sub = substream;
+    }
+    xi_assemble_launch(o->prior.p, o->noise.p, n, s, op->sigma, b->targets.p, m, 1, nullptr, stream);
+  } else {
+    if (!o->have_noise || !cfg.warm_start) {
+      o->probes.ensure(static_cast<size_t>(n) * s);
+      gaussian_fill_launch(cfg.probe_seed, 2, substream, static_cast<int64_t>(n) * s, n, s, o->probes.p, stream);
+      o->have_noise = true;
+    }
+    GPK_CUDA(cudaMemcpy2DAsync(b->targets.p + 1, sizeof(double) * m, o->probes.p, sizeof(double) * s,
+                               sizeof(double) * s, n, cudaMemcpyDeviceToDevice, stream));
+  }
+  {  // scales = ||b_j|| + eps (linear_system.cpp:21)
+    const int G = kReduceGroups;
+    double* part = b->red.ensure(static_cast<size_t>(G) * 2 * m + 8);
+    double* ss = b->vec1.ensure(m);
+    col_reduce_launch(b->targets.p, nullptr, n, m, m, 2, part, G, nullptr, stream);
+    sum_partials_launch(part, G, m, ss, nullptr, stream);
+    std::vector<double> h(m);
+    GPK_CUDA(cudaMemcpyAsync(h.data(), ss, sizeof(double) * m, cudaMemcpyDeviceToHost, stream));
+    GPK_CUDA(cudaStreamSynchronize(stream));
+    for (int j = 0; j < m; ++j) b->scales[j] = std::sqrt(h[j]) + 1e-12;
+    GPK_CUDA(cudaMemcpyAsync(b->scales_dev.p, b->scales.data(), sizeof(double) * m, cudaMemcpyHostToDevice, stream));
+  }
+  if (cfg.warm_start && o->have_previous)
+    GPK_CUDA(cudaMemcpyAsync(b->solutions.p, o->prev.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, stream));
+  else
+    GPK_CUDA(cudaMemsetAsync(b->solutions.p, 0, sizeof(double) * nm, stream));
+  GPK_CUDA(cudaMemsetAsync(b->residuals.p, 0, sizeof(double) * nm, stream));
+  o->sc.substream = static_cast<uint64_t>(t);
+  o->sc.seed = cfg.solver_seed;
+  gpk_solver_report rep{};
+  solve_dispatch(b, &o->sc, &rep);
+  const double solver_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  const int stride = 2 * P + 8;
+  std::memset(row, 0, sizeof(double) * stride);
+  for (int k = 0; k < P; ++k) row[k] = softplus(o->raw[k]);
+  row[2 * P + 0] = rep.mean_residual_norm;
+  row[2 * P + 1] = rep.probe_residual_norm;
+  row[2 * P + 2] = rep.epochs_consumed;
+  row[2 * P + 4] = rep.iterations;
+  row[2 * P + 5] = rep.aborted;
+  bool keep_going = true;
+  if (rep.aborted) {
+    if (cfg.divergence_policy == 1) {
+      o->aborted = true;
+      keep_going = false;
+    } else if (o->sc.kind == GPK_SGD && !o->sgd_halved) {
+      o->sc.learning_rate *= 0.5;
+      o->sgd_halved = true;
+    }
+  } else {
+    std::vector<double> g(P);
+    std::vector<std::vector<double>> f;
+    if (pathwise)
+      f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1}, {b->solutions.p, b->solutions.p, m, m, 1, s}});
+    else
+      f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1}, {b->solutions.p, b->targets.p, m, m, 1, s}});
+    assemble(f, s, P, g.data(), nullptr, nullptr);
+    double inf = 0.0;
+    for (int k = 0; k < P; ++k) {
+      row[P + k] = g[k];
+      inf = std::max(inf, std::abs(g[k]));
+    }
+    row[2 * P + 3] = inf;
+    // raw += adam.update(-raw_gradient(g, raw)) (outer_loop.cpp:42-55, 229-230)
+    const double lr = cfg.learning_rate, b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    ++o->astep;
+    const double ms = 1.0 / (1.0 - std::pow(b1, o->astep));
+    const double vs = 1.0 / (1.0 - std::pow(b2, o->astep));
+    std::vector<double> upd(P);
+    for (int k = 0; k < P; ++k) {
+      const double gr = -(g[k] * sigmoid(o->raw[k]));
+      o->am[k] = b1 * o->am[k] + (1.0 - b1) * gr;
+      o->av[k] = b2 * o->av[k] + (1.0 - b2) * (gr * gr);
+      upd[k] = (-lr) * (ms * o->am[k] / (std::sqrt(vs * o->av[k]) + eps));
+    }
+    for (int k = 0; k < P; ++k) o->raw[k] += upd[k];
+    GPK_CUDA(cudaMemcpyAsync(o->prev.p, b->solutions.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, stream));
+    o->have_previous = true;
+  }
+  GPK_CUDA(cudaStreamSynchronize(stream));
+  row[2 * P + 6] = std::chrono::duration<double>(Clock::now() - t0).count();
+  row[2 * P + 7] = solver_seconds;
+  ++o->t;
+  return keep_going;
+}
+
+}  // namespace
+
+extern "C" {
+
+gpk_status gpk_optimiser_create(gpk_ctx* ctx, const double* inputs, const double* targets, int n, int d,
+                                const gpk_outer_config* cfg, const double* init_constrained, gpk_optimiser** out) {
+  return guarded([&] {
+    LaunchScope ls(ctx);
+    auto o = std::make_unique<gpk_optimiser>();
+    optimiser_init(o.get(), ctx, inputs, targets, n, d, cfg, init_constrained);
+    *out = o.release();
+  });
+}
+
+gpk_status gpk_optimiser_step(gpk_optimiser* o, int steps, double* trace, int* rows_written) {
+  return guarded([&] {
+    LaunchScope ls(o->ctx);
+    *rows_written = 0;
+    const int stride = 2 * o->P + 8;
+    for (int k = 0; k < steps && !o->aborted; ++k) {
+      const bool go = optimiser_one_step(o, trace + static_cast<size_t>(k) * stride);
+      *rows_written = k + 1;
+      if (!go) break;
+    }
+  });
+}
+
+gpk_status gpk_optimiser_state(gpk_optimiser* o, double* raw, int* step, int* aborted) {
+  return guarded([&] {
+    if (raw) std::memcpy(raw, o->raw.data(), sizeof(double) * o->P);
+    if (step) *step = o->t;
+    if (aborted) *aborted = o->aborted;
+  });
+}
+
+gpk_status gpk_optimiser_destroy(gpk_optimiser* o) {
+  return guarded([&] { delete o; });
+}
+
+gpk_status gpk_optimise(gpk_ctx* ctx, const double* inputs, const double* targets, int n, int d,
+                        const gpk_outer_config* cfg, const double* init_constrained, double* trace, int* rows_written,
+                        double* final_raw, int* aborted) {
+  return guarded([&] {
+    LaunchScope ls(ctx);
+    gpk_optimiser o;
+    optimiser_init(&o, ctx, inputs, targets, n, d, cfg, init_constrained);
+    *rows_written = 0;
+    const int stride = 2 * o.P + 8;
+    for (int k = 0; k < cfg->steps; ++k) {
+      const bool go = optimiser_one_step(&o, trace + static_cast<size_t>(k) * stride);
+      *rows_written = k + 1;
+      if (!go) break;
+    }
+    std::memcpy(final_raw, o.raw.data(), sizeof(double) * o.P);
+    *aborted = o.aborted;
+  });
+}
+
+gpk_status gpk_sinsum_dataset(int n, int d, int uniform, double noise, uint64_t seed, float* x_rowmajor, float* yout) {
+  return guarded([&] {
+    require(n >= 1 && d >= 1, "gpk_sinsum_dataset: n >= 1 and d >= 1");
+    auto gauss = [](HostStream& st) -> double {  // rng.cpp:64-77
+      if (st.has_cached) {
+        st.has_cached = false;
+        return st.cached;
+      }
+      const double u1 = static_cast<double>((st.next_u64() >> 11) + 1) * 0x1.0p-53;
+      const double u2 = static_cast<double>(st.next_u64() >> 11) * 0x1.0p-53;
+      const double radius = std::sqrt(-2.0 * std::log(u1));
+      const double angle = 2.0 * 3.141592653589793 * u2;
+      st.cached = radius * std::sin(angle);
+      st.has_cached = true;
+      return radius * std::cos(angle);
+    };
+    std::vector<double> x(static_cast<size_t>(n) * d);  // column-major fill order
+    HostStream xs(seed, 7, 0);
+    if (uniform) {
+      for (auto& v : x) v = 2.0 * (static_cast<double>(xs.next_u64() >> 11) * 0x1.0p-53) - 1.0;
+    } else {
+      for (auto& v : x) v = gauss(xs);
+    }
+    std::vector<double> w(static_cast<size_t>(d) * 4);
+    HostStream ws(seed, 7, 1);
+    for (auto& v : w) v = gauss(ws);
+    const double wscale = 1.0 / std::sqrt(static_cast<double>(d));
+    std::vector<double> eps(n);
+    HostStream es(seed, 7, 2);
+    for (auto& v : eps) v = gauss(es);
+    std::vector<double> yy(n);
+    for (int i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < 4; ++k) {
+        double dot = 0.0;
+        for (int q = 0; q < d; ++q)
+          dot += x[static_cast<size_t>(q) * n + i] * (w[static_cast<size_t>(k) * d + q] * wscale);
+        acc += std::sin(dot);
+      }
+      yy[i] = acc + noise * eps[i];
+    }
+    for (int q = 0; q < d; ++q) {
+      double mean = 0.0;
+      for (int i = 0; i < n; ++i) mean += x[static_cast<size_t>(q) * n + i];
+      mean /= n;
+      double var = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double t = x[static_cast<size_t>(q) * n + i] - mean;
+        var += t * t;
+      }
+      var /= n;
+      double scale = std::sqrt(var);
+      if (!(scale > 0.0)) scale = 1.0;
+      const double inv = 1.0 / scale;
+      for (int i = 0; i < n; ++i)
+        x_rowmajor[static_cast<size_t>(i) * d + q] = static_cast<float>((x[static_cast<size_t>(q) * n + i] - mean) * inv);
+    }
+    double mean = 0.0;
+    for (double v : yy) mean += v;
+    mean /= n;
+    double var = 0.0;
+    for (double v : yy) var += (v - mean) * (v - mean);
+    var /= n;
+    const double scale = var > 0.0 ? std::sqrt(var) : 1.0;
+    for (int i = 0; i < n; ++i) yout[i] = static_cast<float>((yy[i] - mean) / scale);
+  });
+}
+
+}  // extern "C"
+

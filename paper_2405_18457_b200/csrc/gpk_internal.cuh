@@ -1,0 +1,194 @@
+// Internal declarations shared by the CUDA kernels and the host C++ of libgpk.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace gpk {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define GPK_CUDA(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      throw ::gpk::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+// Launch-count bookkeeping (bench.py reports gpu_launches).
+extern thread_local long long* g_launch_counter;
+inline void count_launch(int k = 1) {
+  if (g_launch_counter) *g_launch_counter += k;
+}
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  count_launch();
+}
+
+constexpr double kSqrt3 = 1.7320508075688772;
+
+// ---- operator slab (K1/K2/K3) -------------------------------------------
+// out_part[split][r][j] = sum over the split's columns c of k(x_row(r), x_c) v[c - c0][j]
+// (kernel only; the sigma^2 diagonal is added by kv_reduce).
+struct KvArgs {
+  const float* xs;     // scaled inputs FP32 [n][dp]
+  int n, dp;
+  const int* row_idx;  // device row indices (SGD) or null
+  int r0, R;           // rows r0..r0+R (when row_idx null)
+  int c0, C;           // column range
+  const int* sel;      // device block index (AP) or null: c0 = *sel*sel_block
+  int sel_block;
+  const float* v;      // FP32 RHS [C][ldv]; row (c - c0) <-> column c
+  int ldv, m;
+  float log2_s2;       // log2(signal variance)
+  double* part;        // [splits][R][m]
+  int splits, cols_per_split, flush_chunks;
+  const int* skip;     // device flag: nonzero => no-op (solver predication)
+  double* stats;       // device counters [evals x RHS, algorithmic flops] or null
+  int d;               // true input dimension (flop accounting)
+};
+int kv_tc_for(int m);        // columns-per-lane template parameter for m
+int kv_ld_for(int m);        // FP32 RHS leading dimension for m
+void kv_slab_launch(const KvArgs& a, int dmax, cudaStream_t s);
+int kv_choose_splits(int R, int C, int sms);
+
+struct KvReduceArgs {
+  const double* part;
+  int splits, R, m;
+  const double* vdiag;  // FP64 RHS for the diagonal term, [C][ldvd] (row c - c0), or null
+  int ldvd;
+  const float* vdiag32; // fallback FP32 RHS for the diagonal
+  int ldv32;
+  const int* row_idx;
+  int r0, c0, C;
+  const int* sel;
+  int sel_block, n;
+  double sigma2;
+  double* out;
+  int ldo;
+  const double* base;   // out = base + alpha * (H v)
+  int ldb;
+  double alpha;
+  const int* skip;
+};
+void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s);
+
+// ---- gradient pass (K4) ---------------------------------------------------
+struct GradArgs {
+  const float* xs;      // [n][dp] scaled FP32
+  int n, d, dp;
+  const float* u[2];    // per pair: [n][ldu] FP32
+  const float* w[2];
+  int mcols[2], ldu[2];
+  int npairs;
+  int symmetric;        // all pairs have U == W
+  float log2_s2, s2;
+  double* part;         // [blocks][npairs*(d+1)]
+  int blocks;
+};
+void grad_launch(const GradArgs& a, cudaStream_t s);
+
+// ---- misc device kernels (la_kernels.cu) ---------------------------------
+void prescale_launch(const double* x64, int n, int d, int dp, const double* inv_ls, float* xs32,
+                     double* xs64, cudaStream_t s);
+void to_f32_launch(const double* src, int n, int m, int lds, float* dst, int ldd, const int* skip,
+                   cudaStream_t s);
+void transpose_launch(const double* src, int rows, int cols, int lds, double* dst, int ldd,
+                      cudaStream_t s);  // dst[c][r] = src[r][c]
+
+// Deterministic column reductions: part[g][k*m + j] for nout outputs.
+// mode 0: sum a*b ; mode 1: (sum a*b, sum a*a) ; mode 2: sum a*a
+void col_reduce_launch(const double* a, const double* b, int n, int m, int lda, int mode,
+                       double* part, int groups, const int* skip, cudaStream_t s);
+constexpr int kReduceGroups = 296;
+
+// CG scalar kernels (single block), all predicated on ctl.
+struct CgCtl {
+  int done;        // termination reached
+  int aborted;     // breakdown
+  int stop;        // done || aborted (skip flag for predicated kernels)
+  int iters;       // iterations taken
+  int budget;      // max iterations
+  int pad;
+  double mean_norm, probe_norm;
+};
+void cg_init_scalars_launch(const double* part, int groups, int m, const double* scales, double tol,
+                            double* gamma, CgCtl* ctl, cudaStream_t s);
+void cg_alpha_launch(const double* part, int groups, int m, const double* gamma, double* alpha,
+                     CgCtl* ctl, cudaStream_t s);
+void cg_update_launch(double* v, double* r, const double* d, const double* hd, const double* alpha,
+                      int n, int m, const int* skip, cudaStream_t s);
+void cg_beta_launch(const double* part, int groups, int m, const double* scales, double tol,
+                    double* gamma, double* beta, CgCtl* ctl, cudaStream_t s);
+void cg_direction_launch(double* d, const double* p, const double* beta, int n, int m, float* d32,
+                         int ldv, const int* skip, cudaStream_t s);
+void norms_launch(const double* part, int groups, int m, const double* scales, double tol,
+                  double* out3, cudaStream_t s);  // mean, probe, done
+
+// preconditioner (K7)
+void argmax_partials_launch(const double* diag, int n, double* pval, int* pidx, int groups,
+                            cudaStream_t s);
+void pchol_step_launch(const double* xs64, int n, int d, double s2, const double* pval,
+                       const int* pidx, int groups, double* L, int ldl, int mcol, double* diag,
+                       int* pivots, int* stop_flag, cudaStream_t s);
+void gram_partials_launch(const double* L, int n, int r, int ldl, double* part, int groups,
+                          cudaStream_t s);
+void lt_times_launch(const double* L, int n, int r, int ldl, const double* R, int m, double* part,
+                     int groups, const int* skip, cudaStream_t s);
+void sum_partials_launch(const double* part, int groups, int count, double* out, const int* skip,
+                         cudaStream_t s);
+void small_gemm_launch(const double* A, int ra, int ca, const double* B, int cb, double* C,
+                       const int* skip, cudaStream_t s);  // C = A(ra x ca, row-major) B(ca x cb)
+void woodbury_launch(const double* R, const double* L, int n, int r, int ldl, const double* inner,
+                     int m, double sigma2, double* out, const int* skip, cudaStream_t s);
+void scale_launch(const double* src, int count, double factor, double* dst, const int* skip,
+                  cudaStream_t s);
+void dense_block64_launch(const double* xs64, int n, int d, double s2, double sigma2, int r0,
+                          int rows, int c0, int cols, double* out, int ldo, int add_noise,
+                          cudaStream_t s);  // out row-major [rows][ldo]
+
+// AP (K8)
+void ap_scores_launch(const double* R, int n, int m, const double* inv_scales, int block,
+                      int nblocks, double* scores, const int* skip, cudaStream_t s);
+void ap_select_launch(const double* scores, int nblocks, int* sel, const int* skip, cudaStream_t s);
+void ap_block_update_launch(const double* inv_blocks, int block, int n, const int* sel,
+                            const double* R, int m, double* V, double* upd64, float* upd32,
+                            int ldv32, const int* skip, cudaStream_t s);
+void ap_check_launch(const double* part, int groups, int m, const double* scales, double tol,
+                     CgCtl* ctl, cudaStream_t s);
+
+// SGD (K2 + K9)
+void sgd_batches_launch(uint64_t seed, uint64_t substream, int n, int b, int first, int count,
+                        int* out, cudaStream_t s);
+void sgd_step_launch(const double* hv_part_reduced, const int* idx, int b, const double* targets,
+                     double* grad, int m, const int* skip, cudaStream_t s);  // grad = hv - t[idx]
+void sgd_update_launch(double* M, double* V, float* V32, int ldv, const int* pos, const double* grad,
+                       double rho, double step, int n, int m, int* nonfinite, const int* skip,
+                       cudaStream_t s);
+void sgd_scatter_launch(const int* idx, int b, int* pos, int value_is_q, const int* skip,
+                        cudaStream_t s);
+void sgd_residual_launch(double* R, const int* idx, int b, const double* grad, int m,
+                         double* sumsq, const int* skip, cudaStream_t s);
+void sgd_check_launch(const double* sumsq, int m, const double* scales, double tol,
+                      const int* nonfinite, CgCtl* ctl, cudaStream_t s);
+
+// RFF (K5) + noise (K9)
+void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs,
+                      const double* weights, int ldw, int s, double amplitude, double* prior,
+                      cudaStream_t s_);  // prior row-major [n][s]
+void gaussian_fill_launch(uint64_t seed, uint64_t stream, uint64_t substream, int64_t count,
+                          int n, int s, double* out_rowmajor, cudaStream_t st);  // col-major order
+void xi_assemble_launch(const double* prior, const double* noise, int n, int s, double sigma,
+                        double* out, int ldo, int col0, double* xi_copy, cudaStream_t st);
+
+}  // namespace gpk

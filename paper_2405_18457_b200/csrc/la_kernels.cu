@@ -1,0 +1,853 @@
+// Solver-state kernels: CG recurrences (K6), pivoted-Cholesky preconditioner
+// (K7), alternating-projection block steps (K8), SGD minibatch sampling and
+// momentum updates (K2 epilogue + K9), RFF pathwise targets (K5).
+//
+// All solver vectors are FP64 row-major [n][m] (m = s+1 RHS). Every
+// reduction is deterministic: a fixed grid of row groups writes partials and
+// a single block sums them in ascending group order — no float atomics.
+// Kernels that run inside a solver iteration take a `skip` flag (device int)
+// so the host can enqueue iterations ahead of the termination test: once the
+// device sets the flag, the remaining enqueued kernels are no-ops.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+
+#include "gpk_internal.cuh"
+#include "philox.cuh"
+
+namespace gpk {
+
+namespace {
+inline int blocks_for(long long n, int threads, int cap = 148 * 16) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return static_cast<int>(b);
+}
+#define SKIP_IF(flag) \
+  if ((flag) && *(flag)) return;
+}  // namespace
+
+// ---------------------------------------------------------------- layout
+__global__ void prescale_kernel(const double* x64, int n, int d, int dp, const double* inv_ls,
+                                float* xs32, double* xs64) {
+  const long long total = static_cast<long long>(n) * dp;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / dp), k = static_cast<int>(e % dp);
+    if (k < d) {
+      const double v = x64[static_cast<size_t>(i) * d + k] * inv_ls[k];  // kernel.cpp:94
+      xs32[e] = static_cast<float>(v);
+      xs64[static_cast<size_t>(i) * d + k] = v;
+    } else {
+      xs32[e] = 0.f;
+    }
+  }
+}
+void prescale_launch(const double* x64, int n, int d, int dp, const double* inv_ls, float* xs32,
+                     double* xs64, cudaStream_t s) {
+  prescale_kernel<<<blocks_for(static_cast<long long>(n) * dp, 256), 256, 0, s>>>(x64, n, d, dp, inv_ls, xs32, xs64);
+  check_launch("prescale");
+}
+
+__global__ void to_f32_kernel(const double* src, int n, int m, int lds, float* dst, int ldd, const int* skip) {
+  SKIP_IF(skip);
+  const long long total = static_cast<long long>(n) * ldd;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / ldd), j = static_cast<int>(e % ldd);
+    dst[e] = j < m ? static_cast<float>(src[static_cast<size_t>(i) * lds + j]) : 0.f;
+  }
+}
+void to_f32_launch(const double* src, int n, int m, int lds, float* dst, int ldd, const int* skip, cudaStream_t s) {
+  to_f32_kernel<<<blocks_for(static_cast<long long>(n) * ldd, 256), 256, 0, s>>>(src, n, m, lds, dst, ldd, skip);
+  check_launch("to_f32");
+}
+
+__global__ void transpose_kernel(const double* src, int rows, int cols, int lds, double* dst, int ldd) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / cols), c = static_cast<int>(e % cols);
+    dst[static_cast<size_t>(c) * ldd + r] = src[static_cast<size_t>(r) * lds + c];
+  }
+}
+void transpose_launch(const double* src, int rows, int cols, int lds, double* dst, int ldd, cudaStream_t s) {
+  transpose_kernel<<<blocks_for(static_cast<long long>(rows) * cols, 256), 256, 0, s>>>(src, rows, cols, lds, dst, ldd);
+  check_launch("transpose");
+}
+
+// ---------------------------------------------------------- reductions
+// part[g][k*m + j]: per-column sums over rows [g*n/G, (g+1)*n/G).
+__global__ void col_reduce_kernel(const double* a, const double* b, int n, int m, int lda, int mode,
+                                  double* part, const int* skip) {
+  SKIP_IF(skip);
+  __shared__ double s1[8][33], s2[8][33];
+  const int g = blockIdx.x, G = gridDim.x;
+  const long long rb = static_cast<long long>(n) * g / G, re = static_cast<long long>(n) * (g + 1) / G;
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+  const int nout = mode == 1 ? 2 : 1;
+  for (int j0 = 0; j0 < m; j0 += 32) {
+    const int j = j0 + tx;
+    double acc1 = 0.0, acc2 = 0.0;
+    if (j < m) {
+      for (long long i = rb + ty; i < re; i += 8) {
+        const double x = a[i * lda + j];
+        if (mode == 2) {
+          acc1 = fma(x, x, acc1);
+        } else {
+          acc1 = fma(x, b[i * lda + j], acc1);
+          if (mode == 1) acc2 = fma(x, x, acc2);
+        }
+      }
+    }
+    s1[ty][tx] = acc1;
+    s2[ty][tx] = acc2;
+    __syncthreads();
+    if (ty == 0 && j < m) {
+      double t1 = 0.0, t2 = 0.0;
+      for (int q = 0; q < 8; ++q) {
+        t1 += s1[q][tx];
+        t2 += s2[q][tx];
+      }
+      part[static_cast<size_t>(g) * nout * m + j] = t1;
+      if (mode == 1) part[static_cast<size_t>(g) * nout * m + m + j] = t2;
+    }
+    __syncthreads();
+  }
+}
+void col_reduce_launch(const double* a, const double* b, int n, int m, int lda, int mode, double* part,
+                       int groups, const int* skip, cudaStream_t s) {
+  col_reduce_kernel<<<groups, 256, 0, s>>>(a, b, n, m, lda, mode, part, skip);
+  check_launch("col_reduce");
+}
+
+namespace {
+// Sum of partial k for column j over groups, fixed order.
+__device__ double gsum(const double* part, int groups, int stride, int off) {
+  double acc = 0.0;
+  for (int g = 0; g < groups; ++g) acc += part[static_cast<size_t>(g) * stride + off];
+  return acc;
+}
+// Termination norms (linear_system.cpp:38-53) from per-column sums of squares.
+__device__ void termination(const double* ss, int m, const double* scales, double tol, double& mean,
+                            double& probe, int& done) {
+  mean = sqrt(ss[0]) / scales[0];
+  double sum = 0.0;
+  for (int j = 1; j < m; ++j) sum += sqrt(ss[j]) / scales[j];
+  probe = m > 1 ? sum / (m - 1) : 0.0;
+  done = (mean <= tol && probe <= tol) ? 1 : 0;
+}
+}  // namespace
+
+// gamma = r.p ; termination from r.r
+__global__ void cg_init_scalars_kernel(const double* part, int groups, int m, const double* scales,
+                                       double tol, double* gamma, CgCtl* ctl) {
+  __shared__ double ss[512];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    gamma[j] = gsum(part, groups, 2 * m, j);
+    ss[j] = gsum(part, groups, 2 * m, m + j);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int done;
+    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    ctl->done = done;
+    ctl->aborted = 0;
+    ctl->iters = 0;
+    ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
+  }
+}
+void cg_init_scalars_launch(const double* part, int groups, int m, const double* scales, double tol,
+                            double* gamma, CgCtl* ctl, cudaStream_t s) {
+  cg_init_scalars_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, gamma, ctl);
+  check_launch("cg_init");
+}
+
+// alpha_j = gamma_j / d_j.Hd_j with the reference's breakdown rules (solvers.cpp:55-71).
+__global__ void cg_alpha_kernel(const double* part, int groups, int m, const double* gamma, double* alpha,
+                                CgCtl* ctl) {
+  if (ctl->stop) return;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const double denom = gsum(part, groups, m, j);
+    double a;
+    if (denom > 0.0) a = gamma[j] / denom;
+    else if (gamma[j] == 0.0 && denom == 0.0) a = 0.0;
+    else a = __longlong_as_double(0x7ff8000000000000ULL);
+    alpha[j] = a;
+    if (!isfinite(a)) atomicOr(&bad, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bad) {
+    ctl->aborted = 1;
+    ctl->stop = 1;
+  }
+}
+void cg_alpha_launch(const double* part, int groups, int m, const double* gamma, double* alpha, CgCtl* ctl,
+                     cudaStream_t s) {
+  cg_alpha_kernel<<<1, 256, 0, s>>>(part, groups, m, gamma, alpha, ctl);
+  check_launch("cg_alpha");
+}
+
+// v += d*alpha ; r -= hd*alpha (solvers.cpp:72-73); products rounded before the add.
+__global__ void cg_update_kernel(double* v, double* r, const double* d, const double* hd, const double* alpha,
+                                 int n, int m, const int* skip) {
+  SKIP_IF(skip);
+  const long long total = static_cast<long long>(n) * m;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double a = alpha[e % m];
+    v[e] = __dadd_rn(v[e], __dmul_rn(d[e], a));
+    r[e] = __dsub_rn(r[e], __dmul_rn(hd[e], a));
+  }
+}
+void cg_update_launch(double* v, double* r, const double* d, const double* hd, const double* alpha, int n, int m,
+                      const int* skip, cudaStream_t s) {
+  cg_update_kernel<<<blocks_for(static_cast<long long>(n) * m, 256), 256, 0, s>>>(v, r, d, hd, alpha, n, m, skip);
+  check_launch("cg_update");
+}
+
+// gamma' = r.p, beta = gamma'/gamma (0 if gamma == 0), iteration++, termination.
+__global__ void cg_beta_kernel(const double* part, int groups, int m, const double* scales, double tol,
+                               double* gamma, double* beta, CgCtl* ctl) {
+  if (ctl->stop) return;
+  __shared__ double ss[512];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const double gn = gsum(part, groups, 2 * m, j);
+    beta[j] = gamma[j] != 0.0 ? gn / gamma[j] : 0.0;
+    gamma[j] = gn;
+    ss[j] = gsum(part, groups, 2 * m, m + j);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->iters += 1;
+    int done;
+    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    ctl->done = done;
+    ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
+  }
+}
+void cg_beta_launch(const double* part, int groups, int m, const double* scales, double tol, double* gamma,
+                    double* beta, CgCtl* ctl, cudaStream_t s) {
+  cg_beta_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, gamma, beta, ctl);
+  check_launch("cg_beta");
+}
+
+// d = p + d*beta (solvers.cpp:80) and its FP32 copy for the next operator product.
+__global__ void cg_direction_kernel(double* d, const double* p, const double* beta, int n, int m, float* d32,
+                                    int ldv, const int* skip) {
+  SKIP_IF(skip);
+  const long long total = static_cast<long long>(n) * ldv;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / ldv), j = static_cast<int>(e % ldv);
+    if (j < m) {
+      const size_t o = static_cast<size_t>(i) * m + j;
+      const double nd = __dadd_rn(p[o], __dmul_rn(d[o], beta[j]));
+      d[o] = nd;
+      d32[e] = static_cast<float>(nd);
+    } else {
+      d32[e] = 0.f;
+    }
+  }
+}
+void cg_direction_launch(double* d, const double* p, const double* beta, int n, int m, float* d32, int ldv,
+                         const int* skip, cudaStream_t s) {
+  cg_direction_kernel<<<blocks_for(static_cast<long long>(n) * ldv, 256), 256, 0, s>>>(d, p, beta, n, m, d32, ldv, skip);
+  check_launch("cg_direction");
+}
+
+__global__ void norms_kernel(const double* part, int groups, int m, const double* scales, double tol, double* out3) {
+  __shared__ double ss[512];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) ss[j] = gsum(part, groups, m, j);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int done;
+    termination(ss, m, scales, tol, out3[0], out3[1], done);
+    out3[2] = done;
+  }
+}
+void norms_launch(const double* part, int groups, int m, const double* scales, double tol, double* out3,
+                  cudaStream_t s) {
+  norms_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, out3);
+  check_launch("norms");
+}
+
+// ------------------------------------------------------ preconditioner K7
+// Per-group (max, lowest index) of diag; strict '>' scan semantics
+// (pivoted_cholesky.cpp:22-27).
+__global__ void argmax_partials_kernel(const double* diag, int n, double* pval, int* pidx) {
+  __shared__ double sv[256];
+  __shared__ int si[256];
+  const int g = blockIdx.x, G = gridDim.x;
+  const int rb = static_cast<int>(static_cast<long long>(n) * g / G);
+  const int re = static_cast<int>(static_cast<long long>(n) * (g + 1) / G);
+  double best = -DBL_MAX;
+  int bi = 0x7fffffff;
+  for (int i = rb + threadIdx.x; i < re; i += blockDim.x) {
+    const double v = diag[i];
+    if (v > best) { best = v; bi = i; }  // ascending i per thread: first max kept
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      const double v2 = sv[threadIdx.x + off];
+      const int i2 = si[threadIdx.x + off];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pval[g] = sv[0];
+    pidx[g] = si[0];
+  }
+}
+void argmax_partials_launch(const double* diag, int n, double* pval, int* pidx, int groups, cudaStream_t s) {
+  argmax_partials_kernel<<<groups, 256, 0, s>>>(diag, n, pval, pidx);
+  check_launch("argmax_partials");
+}
+
+__device__ __forceinline__ double matern64(const double* xs64, int d, int i, int c, double s2) {
+  const double* a = xs64 + static_cast<size_t>(i) * d;
+  const double* b = xs64 + static_cast<size_t>(c) * d;
+  double r2 = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = b[k] - a[k];
+    r2 += t * t;
+  }
+  const double r = sqrt(r2);
+  return s2 * (1.0 + kSqrt3 * r) * exp(-kSqrt3 * r);  // kernel.cpp:35-39
+}
+
+// One greedy step (pivoted_cholesky.cpp:19-39): pivot = argmax diag; column
+// = (k(:, pivot) - L[:, :m] L[pivot, :m]^T) / sqrt(best); diag -= column^2.
+__global__ void pchol_step_kernel(const double* xs64, int n, int d, double s2, const double* pval, const int* pidx,
+                                  int groups, double* L, int ldl, int mcol, double* diag, int* pivots,
+                                  int* stop_flag) {
+  if (*stop_flag) return;
+  __shared__ double s_best;
+  __shared__ int s_piv;
+  if (threadIdx.x == 0) {
+    double best = -DBL_MAX;
+    int bi = 0x7fffffff;
+    for (int g = 0; g < groups; ++g)
+      if (pval[g] > best || (pval[g] == best && pidx[g] < bi)) { best = pval[g]; bi = pidx[g]; }
+    s_best = best;
+    s_piv = bi;
+  }
+  __syncthreads();
+  const double best = s_best;
+  const int piv = s_piv;
+  if (!(best > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *stop_flag = 1;
+    return;
+  }
+  const double sb = sqrt(best);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double col = matern64(xs64, d, piv, i, s2);
+    if (mcol > 0) {
+      double acc = 0.0;
+      const double* li = L + static_cast<size_t>(i) * ldl;
+      const double* lp = L + static_cast<size_t>(piv) * ldl;
+      for (int k = 0; k < mcol; ++k) acc += li[k] * lp[k];
+      col -= acc;
+    }
+    col /= sb;
+    L[static_cast<size_t>(i) * ldl + mcol] = col;
+    diag[i] = (i == piv) ? 0.0 : diag[i] - col * col;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) pivots[mcol] = piv;
+}
+void pchol_step_launch(const double* xs64, int n, int d, double s2, const double* pval, const int* pidx, int groups,
+                       double* L, int ldl, int mcol, double* diag, int* pivots, int* stop_flag, cudaStream_t s) {
+  pchol_step_kernel<<<blocks_for(n, 256, 148 * 8), 256, 0, s>>>(xs64, n, d, s2, pval, pidx, groups, L, ldl, mcol,
+                                                               diag, pivots, stop_flag);
+  check_launch("pchol_step");
+}
+
+// part[g][a*r + b] = sum_{i in group} L[i][a] L[i][b]
+__global__ void gram_partials_kernel(const double* L, int n, int r, int ldl, double* part) {
+  const int g = blockIdx.x, G = gridDim.x;
+  const int rb = static_cast<int>(static_cast<long long>(n) * g / G);
+  const int re = static_cast<int>(static_cast<long long>(n) * (g + 1) / G);
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int a = e / r, b = e % r;
+    double acc = 0.0;
+    for (int i = rb; i < re; ++i) acc += L[static_cast<size_t>(i) * ldl + a] * L[static_cast<size_t>(i) * ldl + b];
+    part[static_cast<size_t>(g) * r * r + e] = acc;
+  }
+}
+void gram_partials_launch(const double* L, int n, int r, int ldl, double* part, int groups, cudaStream_t s) {
+  gram_partials_kernel<<<groups, 256, 0, s>>>(L, n, r, ldl, part);
+  check_launch("gram_partials");
+}
+
+// part[g][k*m + j] = sum_{i in group} L[i][k] R[i][j]
+__global__ void lt_times_kernel(const double* L, int n, int r, int ldl, const double* R, int m, double* part,
+                                const int* skip) {
+  SKIP_IF(skip);
+  const int g = blockIdx.x, G = gridDim.x;
+  const int rb = static_cast<int>(static_cast<long long>(n) * g / G);
+  const int re = static_cast<int>(static_cast<long long>(n) * (g + 1) / G);
+  for (int e = threadIdx.x; e < r * m; e += blockDim.x) {
+    const int k = e / m, j = e % m;
+    double acc = 0.0;
+    for (int i = rb; i < re; ++i) acc += L[static_cast<size_t>(i) * ldl + k] * R[static_cast<size_t>(i) * m + j];
+    part[static_cast<size_t>(g) * r * m + e] = acc;
+  }
+}
+void lt_times_launch(const double* L, int n, int r, int ldl, const double* R, int m, double* part, int groups,
+                     const int* skip, cudaStream_t s) {
+  lt_times_kernel<<<groups, 256, 0, s>>>(L, n, r, ldl, R, m, part, skip);
+  check_launch("lt_times");
+}
+
+__global__ void sum_partials_kernel(const double* part, int groups, int count, double* out, const int* skip) {
+  SKIP_IF(skip);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x)
+    out[e] = gsum(part, groups, count, e);
+}
+void sum_partials_launch(const double* part, int groups, int count, double* out, const int* skip, cudaStream_t s) {
+  sum_partials_kernel<<<blocks_for(count, 256, 256), 256, 0, s>>>(part, groups, count, out, skip);
+  check_launch("sum_partials");
+}
+
+// C[ra x cb] = A[ra x ca] B[ca x cb], all row-major.
+__global__ void small_gemm_kernel(const double* A, int ra, int ca, const double* B, int cb, double* Cm,
+                                  const int* skip) {
+  SKIP_IF(skip);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ra * cb; e += gridDim.x * blockDim.x) {
+    const int i = e / cb, j = e % cb;
+    double acc = 0.0;
+    for (int k = 0; k < ca; ++k) acc += A[static_cast<size_t>(i) * ca + k] * B[static_cast<size_t>(k) * cb + j];
+    Cm[e] = acc;
+  }
+}
+void small_gemm_launch(const double* A, int ra, int ca, const double* B, int cb, double* Cm, const int* skip,
+                       cudaStream_t s) {
+  small_gemm_kernel<<<blocks_for(static_cast<long long>(ra) * cb, 128, 512), 128, 0, s>>>(A, ra, ca, B, cb, Cm, skip);
+  check_launch("small_gemm");
+}
+
+// out = (R - L inner) / sigma^2 (pivoted_cholesky.cpp:56-57).
+__global__ void woodbury_kernel(const double* R, const double* L, int n, int r, int ldl, const double* inner, int m,
+                                double sigma2, double* out, const int* skip) {
+  SKIP_IF(skip);
+  const long long total = static_cast<long long>(n) * m;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / m), j = static_cast<int>(e % m);
+    const double* li = L + static_cast<size_t>(i) * ldl;
+    double acc = 0.0;
+    for (int k = 0; k < r; ++k) acc += li[k] * inner[static_cast<size_t>(k) * m + j];
+    out[e] = (R[e] - acc) / sigma2;
+  }
+}
+void woodbury_launch(const double* R, const double* L, int n, int r, int ldl, const double* inner, int m,
+                     double sigma2, double* out, const int* skip, cudaStream_t s) {
+  woodbury_kernel<<<blocks_for(static_cast<long long>(n) * m, 256), 256, 0, s>>>(R, L, n, r, ldl, inner, m, sigma2,
+                                                                               out, skip);
+  check_launch("woodbury");
+}
+
+__global__ void scale_kernel(const double* src, long long count, double factor, double* dst, const int* skip) {
+  SKIP_IF(skip);
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[e] = src[e] / factor;
+}
+void scale_launch(const double* src, int count, double factor, double* dst, const int* skip, cudaStream_t s) {
+  scale_kernel<<<blocks_for(count, 256), 256, 0, s>>>(src, count, factor, dst, skip);
+  check_launch("scale");
+}
+
+// FP64 dense block of H (kernel.cpp:179-184), row-major [rows][ldo].
+__global__ void dense_block64_kernel(const double* xs64, int n, int d, double s2, double sigma2, int r0, int rows,
+                                     int c0, int cols, double* out, int ldo, int add_noise) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / cols), c = static_cast<int>(e % cols);
+    double v = matern64(xs64, d, r0 + r, c0 + c, s2);
+    if (add_noise && r0 + r == c0 + c) v += sigma2;
+    out[static_cast<size_t>(r) * ldo + c] = v;
+  }
+}
+void dense_block64_launch(const double* xs64, int n, int d, double s2, double sigma2, int r0, int rows, int c0,
+                          int cols, double* out, int ldo, int add_noise, cudaStream_t s) {
+  dense_block64_kernel<<<blocks_for(static_cast<long long>(rows) * cols, 256), 256, 0, s>>>(
+      xs64, n, d, s2, sigma2, r0, rows, c0, cols, out, ldo, add_noise);
+  check_launch("dense_block64");
+}
+
+// ------------------------------------------------------------------ AP K8
+// score_k = || R[blk_k] * inv_scales || (solvers.cpp:123-132); one CTA per block.
+__global__ void ap_scores_kernel(const double* R, int n, int m, const double* inv_scales, int block, double* scores,
+                                 const int* skip) {
+  SKIP_IF(skip);
+  __shared__ double red[256];
+  const int k = blockIdx.x;
+  const int r0 = k * block, r1 = min(n, r0 + block);
+  double acc = 0.0;
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    double w = 0.0;
+    const double* row = R + static_cast<size_t>(i) * m;
+    for (int j = 0; j < m; ++j) w += row[j] * inv_scales[j];
+    acc += w * w;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) scores[k] = sqrt(red[0]);
+}
+void ap_scores_launch(const double* R, int n, int m, const double* inv_scales, int block, int nblocks, double* scores,
+                      const int* skip, cudaStream_t s) {
+  ap_scores_kernel<<<nblocks, 256, 0, s>>>(R, n, m, inv_scales, block, scores, skip);
+  check_launch("ap_scores");
+}
+
+__global__ void ap_select_kernel(const double* scores, int nblocks, int* sel, const int* skip) {
+  SKIP_IF(skip);
+  int best_k = 0;
+  double best = -1.0;
+  for (int k = 0; k < nblocks; ++k)
+    if (scores[k] > best) { best = scores[k]; best_k = k; }
+  *sel = best_k;
+}
+void ap_select_launch(const double* scores, int nblocks, int* sel, const int* skip, cudaStream_t s) {
+  ap_select_kernel<<<1, 1, 0, s>>>(scores, nblocks, sel, skip);
+  check_launch("ap_select");
+}
+
+// upd = Hinv[sel] R[blk]; V[blk] += upd; FP32 copy for the slab kernel.
+__global__ void ap_block_update_kernel(const double* inv_blocks, int block, int n, const int* sel, const double* R,
+                                       int m, double* V, double* upd64, float* upd32, int ldv32, const int* skip) {
+  SKIP_IF(skip);
+  const int k = *sel;
+  const int r0 = k * block, len = min(block, n - r0);
+  const double* Hi = inv_blocks + static_cast<size_t>(k) * block * block;
+  const int rows_per_cta = 8;
+  const int i0 = blockIdx.x * rows_per_cta;
+  for (int e = threadIdx.x; e < rows_per_cta * ldv32; e += blockDim.x) {
+    const int i = i0 + e / ldv32, j = e % ldv32;
+    if (i >= len) continue;
+    if (j >= m) {
+      upd32[static_cast<size_t>(i) * ldv32 + j] = 0.f;
+      continue;
+    }
+    double acc = 0.0;
+    const double* hrow = Hi + static_cast<size_t>(i) * block;
+    for (int c = 0; c < len; ++c) acc += hrow[c] * R[static_cast<size_t>(r0 + c) * m + j];
+    upd64[static_cast<size_t>(i) * m + j] = acc;
+    upd32[static_cast<size_t>(i) * ldv32 + j] = static_cast<float>(acc);
+    V[static_cast<size_t>(r0 + i) * m + j] += acc;
+  }
+}
+void ap_block_update_launch(const double* inv_blocks, int block, int n, const int* sel, const double* R, int m,
+                            double* V, double* upd64, float* upd32, int ldv32, const int* skip, cudaStream_t s) {
+  ap_block_update_kernel<<<(block + 7) / 8, 256, 0, s>>>(inv_blocks, block, n, sel, R, m, V, upd64, upd32, ldv32, skip);
+  check_launch("ap_block_update");
+}
+
+// iteration++ ; termination from sum of squares partials.
+__global__ void ap_check_kernel(const double* part, int groups, int m, const double* scales, double tol, CgCtl* ctl) {
+  if (ctl->stop) return;
+  __shared__ double ss[512];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) ss[j] = gsum(part, groups, m, j);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->iters += 1;
+    int done;
+    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    ctl->done = done;
+    ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
+  }
+}
+void ap_check_launch(const double* part, int groups, int m, const double* scales, double tol, CgCtl* ctl,
+                     cudaStream_t s) {
+  ap_check_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, ctl);
+  check_launch("ap_check");
+}
+
+// ----------------------------------------------------------------- SGD
+// Floyd sampling (rng.cpp:108-126) for iterations first..first+count-1 of a
+// solve: iteration t consumes u64 draws [t*b, (t+1)*b) of stream
+// (seed, kSolver = 6, substream). The modulo reductions are independent and
+// run in parallel; the sequential collision pass touches only a bitmap; the
+// sorted output is the bitmap's set bits in ascending order.
+__global__ void sgd_batches_kernel(uint64_t seed, uint64_t substream, int n, int b, int first, int* out) {
+  extern __shared__ unsigned bitmap[];
+  __shared__ int tvals[1024];
+  __shared__ int wcount[1025];
+  const int t = first + blockIdx.x;
+  const int words = (n + 31) / 32;
+  for (int w = threadIdx.x; w < words; w += blockDim.x) bitmap[w] = 0u;
+  for (int q = threadIdx.x; q < b; q += blockDim.x) {
+    const uint64_t k = static_cast<uint64_t>(t) * b + q;
+    const uint64_t u = stream_u64(seed, 6, substream, k);
+    const uint64_t bound = static_cast<uint64_t>(n - b + q) + 1;
+    tvals[q] = static_cast<int>(u % bound);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < b; ++q) {
+      const int j = n - b + q;
+      const int tv = tvals[q];
+      const int pick = ((bitmap[tv >> 5] >> (tv & 31)) & 1u) ? j : tv;
+      bitmap[pick >> 5] |= 1u << (pick & 31);
+    }
+  }
+  __syncthreads();
+  // ascending set-bit positions: per-thread word ranges + exclusive scan
+  const int per = (words + blockDim.x - 1) / blockDim.x;
+  const int w0 = threadIdx.x * per, w1 = min(words, w0 + per);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(bitmap[w]);
+  wcount[threadIdx.x + 1] = cnt;
+  if (threadIdx.x == 0) wcount[0] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 1; i <= blockDim.x; ++i) wcount[i] += wcount[i - 1];
+  __syncthreads();
+  int pos = wcount[threadIdx.x];
+  int* o = out + static_cast<size_t>(blockIdx.x) * b;
+  for (int w = w0; w < w1; ++w) {
+    unsigned bits = bitmap[w];
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      o[pos++] = w * 32 + bit;
+      bits &= bits - 1;
+    }
+  }
+}
+void sgd_batches_launch(uint64_t seed, uint64_t substream, int n, int b, int first, int count, int* out,
+                        cudaStream_t s) {
+  if (b > 1024) throw std::invalid_argument("gpk: SGD batch_size > 1024 is not supported");
+  const size_t smem = sizeof(unsigned) * ((n + 31) / 32);
+  if (smem > 200 * 1024) throw std::invalid_argument("gpk: SGD sampling supports n <= 1.6M");
+  static size_t configured = 0;
+  // dynamic bitmap + ~8 KB static scratch must fit; raise the opt-in limit whenever it grows
+  if (smem > configured) {
+    GPK_CUDA(cudaFuncSetAttribute(sgd_batches_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  sgd_batches_kernel<<<count, 256, smem, s>>>(seed, substream, n, b, first, out);
+  check_launch("sgd_batches");
+}
+
+// grad[q][j] = hv[q][j] - targets[idx[q]][j]
+__global__ void sgd_step_kernel(const double* hv, const int* idx, int b, const double* targets, double* grad, int m,
+                                const int* skip) {
+  SKIP_IF(skip);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < b * m; e += gridDim.x * blockDim.x) {
+    const int q = e / m, j = e % m;
+    grad[e] = hv[e] - targets[static_cast<size_t>(idx[q]) * m + j];
+  }
+}
+void sgd_step_launch(const double* hv, const int* idx, int b, const double* targets, double* grad, int m,
+                     const int* skip, cudaStream_t s) {
+  sgd_step_kernel<<<blocks_for(static_cast<long long>(b) * m, 256), 256, 0, s>>>(hv, idx, b, targets, grad, m, skip);
+  check_launch("sgd_step");
+}
+
+__global__ void sgd_scatter_kernel(const int* idx, int b, int* pos, int value_is_q, const int* skip) {
+  SKIP_IF(skip);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < b; q += gridDim.x * blockDim.x)
+    pos[idx[q]] = value_is_q ? q : -1;
+}
+void sgd_scatter_launch(const int* idx, int b, int* pos, int value_is_q, const int* skip, cudaStream_t s) {
+  sgd_scatter_kernel<<<blocks_for(b, 256), 256, 0, s>>>(idx, b, pos, value_is_q, skip);
+  check_launch("sgd_scatter");
+}
+
+// momentum *= rho; momentum[idx] -= step*g; V += momentum (solvers.cpp:168-170).
+__global__ void sgd_update_kernel(double* M, double* V, float* V32, int ldv, const int* pos, const double* grad,
+                                  double rho, double step, int n, int m, int* nonfinite, const int* skip) {
+  SKIP_IF(skip);
+  const long long total = static_cast<long long>(n) * m;
+  int bad = 0;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / m), j = static_cast<int>(e % m);
+    double mo = __dmul_rn(M[e], rho);
+    const int q = pos[i];
+    if (q >= 0) mo = __dsub_rn(mo, __dmul_rn(step, grad[static_cast<size_t>(q) * m + j]));
+    M[e] = mo;
+    const double v = __dadd_rn(V[e], mo);
+    V[e] = v;
+    V32[static_cast<size_t>(i) * ldv + j] = static_cast<float>(v);
+    if (!isfinite(v)) bad = 1;
+  }
+  if (bad) atomicOr(nonfinite, 1);
+}
+void sgd_update_launch(double* M, double* V, float* V32, int ldv, const int* pos, const double* grad, double rho,
+                       double step, int n, int m, int* nonfinite, const int* skip, cudaStream_t s) {
+  sgd_update_kernel<<<blocks_for(static_cast<long long>(n) * m, 256), 256, 0, s>>>(M, V, V32, ldv, pos, grad, rho,
+                                                                                 step, n, m, nonfinite, skip);
+  check_launch("sgd_update");
+}
+
+// R[idx] = -g, with the per-column sum of squares updated incrementally.
+__global__ void sgd_residual_kernel(double* R, const int* idx, int b, const double* grad, int m, double* sumsq,
+                                    const int* skip) {
+  SKIP_IF(skip);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    double delta = 0.0;
+    for (int q = 0; q < b; ++q) {
+      double* rp = R + static_cast<size_t>(idx[q]) * m + j;
+      const double old = *rp;
+      const double nw = -grad[static_cast<size_t>(q) * m + j];
+      delta += nw * nw - old * old;
+      *rp = nw;
+    }
+    sumsq[j] += delta;
+  }
+}
+void sgd_residual_launch(double* R, const int* idx, int b, const double* grad, int m, double* sumsq, const int* skip,
+                         cudaStream_t s) {
+  sgd_residual_kernel<<<1, 128, 0, s>>>(R, idx, b, grad, m, sumsq, skip);
+  check_launch("sgd_residual");
+}
+
+__global__ void sgd_check_kernel(const double* sumsq, int m, const double* scales, double tol, const int* nonfinite,
+                                 CgCtl* ctl) {
+  if (ctl->stop) return;
+  ctl->iters += 1;
+  if (*nonfinite) {
+    ctl->aborted = 1;
+    ctl->stop = 1;
+    return;
+  }
+  double ss[512];
+  for (int j = 0; j < m; ++j) ss[j] = fmax(sumsq[j], 0.0);
+  int done;
+  termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+  ctl->done = done;
+  ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
+}
+void sgd_check_launch(const double* sumsq, int m, const double* scales, double tol, const int* nonfinite, CgCtl* ctl,
+                      cudaStream_t s) {
+  sgd_check_kernel<<<1, 1, 0, s>>>(sumsq, m, scales, tol, nonfinite, ctl);
+  check_launch("sgd_check");
+}
+
+// ------------------------------------------------------------ RFF (K5)
+// prior[i][j] = sum_q feat(i,q) W(q,j), feat(i,2p) = amp cos(theta), feat(i,2p+1)
+// = amp sin(theta), theta = x_i . (Omega_p / l) in FP64 (rff.cpp:36-54, 73).
+// Features are formed per 16-pair chunk in smem and never materialised in HBM.
+__global__ void rff_prior_kernel(const double* x64, int n, int d, const double* freq, int pairs, const double* W,
+                                 int ldw, int s, double amplitude, double* prior) {
+  constexpr int RB = 64, PC = 16, FC = 2 * PC;
+  __shared__ double feat[RB][FC + 1];
+  __shared__ double wch[FC][64];
+  const int r0 = blockIdx.x * RB, j0 = blockIdx.y * 64;
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  double acc[4][4];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int p0 = 0; p0 < pairs; p0 += PC) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * PC; e += blockDim.x) {
+      const int rr = e / PC, pp = e % PC;
+      const int i = min(r0 + rr, n - 1), p = p0 + pp;
+      double c = 0.0, sn = 0.0;
+      if (p < pairs) {
+        double ang = 0.0;
+        for (int k = 0; k < d; ++k) ang += x64[static_cast<size_t>(i) * d + k] * freq[static_cast<size_t>(p) * d + k];
+        sincos(ang, &sn, &c);
+        c *= amplitude;
+        sn *= amplitude;
+      }
+      feat[rr][2 * pp] = c;
+      feat[rr][2 * pp + 1] = sn;
+    }
+    for (int e = threadIdx.x; e < FC * 64; e += blockDim.x) {
+      const int q = e / 64, j = e % 64;
+      const int gq = 2 * p0 + q;
+      wch[q][j] = (gq < 2 * pairs && j0 + j < s) ? W[static_cast<size_t>(j0 + j) * ldw + gq] : 0.0;
+    }
+    __syncthreads();
+    for (int q = 0; q < FC; ++q) {
+      double fv[4], wv[4];
+      for (int a = 0; a < 4; ++a) fv[a] = feat[ty * 4 + a][q];
+      for (int b = 0; b < 4; ++b) wv[b] = wch[q][tx * 4 + b];
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(fv[a], wv[b], acc[a][b]);
+    }
+  }
+  for (int a = 0; a < 4; ++a) {
+    const int i = r0 + ty * 4 + a;
+    if (i >= n) continue;
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + tx * 4 + b;
+      if (j < s) prior[static_cast<size_t>(i) * s + j] = acc[a][b];
+    }
+  }
+}
+void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs, const double* weights, int ldw,
+                      int s, double amplitude, double* prior, cudaStream_t st) {
+  dim3 grid((n + 63) / 64, (s + 63) / 64);
+  rff_prior_kernel<<<grid, 256, 0, st>>>(x64, n, d, freq, pairs, weights, ldw, s, amplitude, prior);
+  check_launch("rff_prior");
+}
+
+// Box-Muller pairs (rng.cpp:64-77), element e of the column-major n x s fill
+// (rng.cpp:86-90) -> out[i][j] row-major, i = e % n, j = e / n.
+__global__ void gaussian_fill_kernel(uint64_t seed, uint64_t stream, uint64_t substream, long long count, int n, int s,
+                                     double* out) {
+  const long long pairs = (count + 1) / 2;
+  for (long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; p < pairs;
+       p += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const U64x4 blk = philox4x64(static_cast<uint64_t>(p) >> 1, substream, 0, 0, seed, stream);
+    const int o = static_cast<int>((p & 1) * 2);
+    const double u1 = static_cast<double>((blk.v[o] >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>(blk.v[o + 1] >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 6.283185307179586 * u2;  // 2.0 * pi, as rng.cpp:73
+    double sn, cs;
+    sincos(angle, &sn, &cs);
+    const long long e0 = 2 * p, e1 = 2 * p + 1;
+    out[(e0 % n) * s + e0 / n] = radius * cs;
+    if (e1 < count) out[(e1 % n) * s + e1 / n] = radius * sn;
+  }
+}
+void gaussian_fill_launch(uint64_t seed, uint64_t stream, uint64_t substream, int64_t count, int n, int s,
+                          double* out_rowmajor, cudaStream_t st) {
+  gaussian_fill_kernel<<<blocks_for((count + 1) / 2, 256), 256, 0, st>>>(seed, stream, substream, count, n, s,
+                                                                        out_rowmajor);
+  check_launch("gaussian_fill");
+}
+
+// out[i][col0 + j] = prior[i][j] + sigma * noise[i][j] (rff.cpp:77)
+__global__ void xi_assemble_kernel(const double* prior, const double* noise, int n, int s, double sigma, double* out,
+                                   int ldo, int col0, double* xi_copy) {
+  const long long total = static_cast<long long>(n) * s;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / s), j = static_cast<int>(e % s);
+    const double v = __dadd_rn(prior[e], __dmul_rn(sigma, noise[e]));
+    if (out) out[static_cast<size_t>(i) * ldo + col0 + j] = v;
+    if (xi_copy) xi_copy[e] = v;
+  }
+}
+void xi_assemble_launch(const double* prior, const double* noise, int n, int s, double sigma, double* out, int ldo,
+                        int col0, double* xi_copy, cudaStream_t st) {
+  xi_assemble_kernel<<<blocks_for(static_cast<long long>(n) * s, 256), 256, 0, st>>>(prior, noise, n, s, sigma, out,
+                                                                                   ldo, col0, xi_copy);
+  check_launch("xi_assemble");
+}
+
+}  // namespace gpk

@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C-ABI, via the Python mirror of the
+reference API) against the FP64 oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): FP32 operator products and gradients
+within 1e-4 relative (we test tighter where the kernel allows: operator
+products 2e-5 of the column max); FP64 paths (dense blocks, kernel columns,
+preconditioner, RFF prior) to ~1e-10; integer work (SGD minibatches,
+preconditioner pivots) bit-exact; solver residual norms within 1e-4
+relative; iteration counts within +-1.
+"""
+import numpy as np
+import pytest
+
+from _problems import default_test_raw, gp_problem
+
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2405_18457_b200 as G
+    return G
+
+
+def colrel(a, b):
+    """max over columns of max|a-b| / max|b|."""
+    a, b = np.atleast_2d(a.T).T, np.atleast_2d(b.T).T
+    return max(np.max(np.abs(a[:, j] - b[:, j])) / max(np.max(np.abs(b[:, j])), 1e-300) for j in range(b.shape[1]))
+
+
+def make_op(G, ctx, X, raw):
+    return G.KernelOperator(X, G.Hyperparameters.from_raw(raw), ctx)
+
+
+@pytest.mark.parametrize("n,d,m", [(300, 3, 1), (1000, 8, 17), (2048, 26, 65), (777, 20, 65), (513, 1, 9),
+                                   (1500, 11, 33), (4096, 3, 65)])
+def test_apply_matches_oracle(G, gpk_ctx, oracle, n, d, m):
+    X, _ = gp_problem(n, d, 1000 + n)
+    raw = default_test_raw(d, oracle)
+    V = np.asfortranarray(np.random.default_rng(n).standard_normal((n, m)))
+    op = make_op(G, gpk_ctx, X, raw)
+    got = op.apply(V)
+    ref = oracle.apply(X, raw, V, threads=8)
+    assert colrel(got, ref) <= OP_TOL
+
+
+def test_apply_identity_is_dense(G, gpk_ctx, oracle):
+    n, d = 64, 3
+    X, _ = gp_problem(n, d, 101)
+    raw = default_test_raw(d, oracle)
+    op = make_op(G, gpk_ctx, X, raw)
+    H = oracle.dense(X, raw)
+    assert np.max(np.abs(op.apply(np.eye(n)) - H)) <= 1e-6
+    assert np.max(np.abs(op.dense() - H)) <= 1e-12
+    assert np.max(np.abs(op.apply(np.zeros((n, 5))))) == 0.0
+
+
+def test_apply_rejects_bad_input(G, gpk_ctx, oracle):
+    X, _ = gp_problem(50, 2, 3)
+    op = make_op(G, gpk_ctx, X, default_test_raw(2, oracle))
+    with pytest.raises(ValueError):
+        op.apply(np.full((50, 2), np.nan))
+    with pytest.raises(ValueError):
+        op.apply(np.ones((49, 2)))
+    with pytest.raises(ValueError):
+        G.KernelOperator(X, G.Hyperparameters.from_constrained([1.0, 1.0, -1.0, 1.0]), gpk_ctx)
+
+
+def test_apply_is_deterministic(G, gpk_ctx, oracle):
+    X, _ = gp_problem(3000, 5, 7)
+    op = make_op(G, gpk_ctx, X, default_test_raw(5, oracle))
+    V = np.random.default_rng(0).standard_normal((3000, 65))
+    assert np.array_equal(op.apply(V), op.apply(V))
+
+
+@pytest.mark.parametrize("n,d,m,b", [(2000, 3, 65, 512), (600, 8, 17, 37), (50, 2, 3, 5)])
+def test_apply_rows_matches_oracle(G, gpk_ctx, oracle, n, d, m, b):
+    X, _ = gp_problem(n, d, 2 * n)
+    raw = default_test_raw(d, oracle)
+    V = np.asfortranarray(np.random.default_rng(1).standard_normal((n, m)))
+    rows = np.sort(np.random.default_rng(2).choice(n, b, replace=False)).astype(np.int32)
+    op = make_op(G, gpk_ctx, X, raw)
+    assert colrel(op.apply_rows(rows, V), oracle.apply_rows(X, raw, rows, V, threads=8)) <= OP_TOL
+    with pytest.raises(IndexError):
+        op.apply_rows([n], V)
+
+
+@pytest.mark.parametrize("n,d,m,c0,ln", [(2048, 26, 65, 512, 512), (1000, 4, 17, 990, 10), (300, 2, 5, 0, 300)])
+def test_apply_columns_matches_oracle(G, gpk_ctx, oracle, n, d, m, c0, ln):
+    X, _ = gp_problem(n, d, 3 * n)
+    raw = default_test_raw(d, oracle)
+    U = np.asfortranarray(np.random.default_rng(1).standard_normal((ln, m)))
+    op = make_op(G, gpk_ctx, X, raw)
+    assert colrel(op.apply_columns(c0, ln, U), oracle.apply_columns(X, raw, c0, ln, U, threads=8)) <= OP_TOL
+
+
+def test_dense_block_and_kernel_column_fp64(G, gpk_ctx, oracle):
+    n, d = 300, 4
+    X, _ = gp_problem(n, d, 5)
+    raw = default_test_raw(d, oracle)
+    op = make_op(G, gpk_ctx, X, raw)
+    assert np.max(np.abs(op.dense_block(5, 12, 7, 20) - oracle.dense_block(X, raw, 5, 12, 7, 20))) <= 1e-13
+    assert np.max(np.abs(op.kernel_column(17) - oracle.kernel_column(X, raw, 17))) <= 1e-13
+    s2 = G.gpiter.softplus(raw[-2]) ** 2
+    assert np.all(op.kernel_diagonal() == s2)
+
+
+@pytest.mark.parametrize("n,d,s", [(500, 2, 8), (1200, 20, 64), (2048, 26, 64), (700, 3, 16)])
+def test_quadratic_forms_match_oracle(G, gpk_ctx, oracle, n, d, s):
+    X, _ = gp_problem(n, d, 4 * n)
+    raw = default_test_raw(d, oracle)
+    rng = np.random.default_rng(n)
+    vy = rng.standard_normal(n)
+    Z = rng.standard_normal((n, s))
+    op = make_op(G, gpk_ctx, X, raw)
+    g = G.estimate_gradient_pathwise(op, vy, Z)
+    r = oracle.gradient(X, raw, vy, Z, threads=8)
+    for key in ("quadratic_term", "trace_term"):
+        a, b = getattr(g, key), r[key]
+        assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-3 * np.max(np.abs(b)))) <= 1e-4, key
+    # standard estimator (U != W, non-symmetric pass)
+    P = rng.standard_normal((n, s))
+    gs = G.estimate_gradient_standard(op, vy, Z, P)
+    rs = oracle.gradient(X, raw, vy, Z, probes=P, threads=8)
+    b = rs["trace_term"]
+    assert np.max(np.abs(gs.trace_term - b) / np.maximum(np.abs(b), 1e-3 * np.max(np.abs(b)))) <= 1e-4
+
+
+def test_gradient_zero_inputs(G, gpk_ctx, oracle):
+    X, _ = gp_problem(20, 1, 85)
+    op = make_op(G, gpk_ctx, X, default_test_raw(1, oracle))
+    g = G.estimate_gradient_pathwise(op, np.zeros(20), np.zeros((20, 4)))
+    assert np.max(np.abs(g.values)) == 0.0 and np.max(np.abs(g.trace_term)) == 0.0
+
+
+@pytest.mark.parametrize("n,d,rank", [(400, 3, 100), (1000, 8, 50), (40, 1, 40), (300, 2, 0)])
+def test_preconditioner_matches_oracle(G, gpk_ctx, oracle, n, d, rank):
+    X, _ = gp_problem(n, d, 5 * n)
+    raw = default_test_raw(d, oracle)
+    op = make_op(G, gpk_ctx, X, raw)
+    pc = G.PivotedCholeskyPreconditioner(op, rank)
+    V = np.random.default_rng(3).standard_normal((n, 5))
+    ref = oracle.precond(X, raw, rank, V)
+    assert pc.achieved_rank() == ref["achieved_rank"]
+    if rank:
+        assert np.array_equal(pc.pivots(), ref["pivots"])
+        assert np.max(np.abs(pc.factor() - ref["factor"])) <= 1e-10
+    assert colrel(pc.apply(V), ref["apply"]) <= 1e-9
+
+
+def _targets(oracle, n, s, seed, y):
+    T = np.empty((n, s + 1), order="F")
+    T[:, 0] = y
+    T[:, 1:] = oracle.stream_draw(seed, 2, 0, "gaussian", n * s).reshape((n, s), order="F")
+    return T
+
+
+@pytest.mark.parametrize("kind,n,d,s,extra", [
+    (0, 1024, 8, 16, dict(preconditioner_rank=100)),
+    (0, 2048, 20, 64, dict(preconditioner_rank=100)),
+    (1, 1024, 8, 16, dict(block_size=128)),
+    (1, 2048, 26, 64, dict(block_size=512)),
+    (2, 1024, 3, 16, dict(batch_size=128, learning_rate=10.0, max_epochs=5)),
+])
+def test_solvers_match_oracle(G, gpk_ctx, oracle, kind, n, d, s, extra):
+    X, y = gp_problem(n, d, 6 * n + kind)
+    raw = oracle.raw_from_constrained([1.0] * d + [1.0, 0.1 if kind < 2 else 0.5])
+    T = _targets(oracle, n, s, 11, y)
+    cfg = dict(kind=kind, tolerance=0.01, max_epochs=50, seed=4, substream=1)
+    cfg.update(extra)
+    ref = oracle.solve(X, raw, T, oracle.solver_config(**cfg), threads=8)
+    op = make_op(G, gpk_ctx, X, raw)
+    batch = G.LinearSystemBatch(op, T)
+    rep = G.solve(batch, G.SolverConfig(**cfg))
+    assert not rep.aborted
+    assert abs(rep.iterations - ref["iterations"]) <= 1
+    assert rep.reached_tolerance == ref["reached_tolerance"] or abs(rep.iterations - ref["iterations"]) == 1
+    if rep.iterations == ref["iterations"]:
+        assert abs(rep.mean_residual_norm - ref["mean_residual_norm"]) <= 1e-4 * ref["mean_residual_norm"]
+        assert abs(rep.probe_residual_norm - ref["probe_residual_norm"]) <= 1e-4 * ref["probe_residual_norm"]
+
+
+def test_cg_pre_solved_terminates_immediately(G, gpk_ctx, oracle):  # test_solvers.cpp:113-127
+    n, d = 300, 2
+    X, y = gp_problem(n, d, 305)
+    raw = oracle.raw_from_constrained([1.0, 1.0, 1.0, 0.4])
+    T = _targets(oracle, n, 2, 306, y)
+    direct = np.linalg.solve(oracle.dense(X, raw), T)
+    op = make_op(G, gpk_ctx, X, raw)
+    b = G.LinearSystemBatch(op, T)
+    b.warm_start(direct)
+    # tolerance 1e-4: the exact FP64 solution has an FP32-operator residual of ~1e-6..1e-5
+    rep = G.solve_cg(b, G.SolverConfig(tolerance=1e-4, max_epochs=50))
+    assert rep.iterations == 0 and rep.reached_tolerance
+    assert np.array_equal(b.solutions, direct)
+
+
+def test_cg_converges_to_dense_solution(G, gpk_ctx, oracle):
+    n, d = 400, 3
+    X, y = gp_problem(n, d, 307)
+    raw = oracle.raw_from_constrained([1.0, 1.0, 1.0, 1.0, 0.5])
+    T = _targets(oracle, n, 4, 308, y)
+    direct = np.linalg.solve(oracle.dense(X, raw), T)
+    op = make_op(G, gpk_ctx, X, raw)
+    b = G.LinearSystemBatch(op, T)
+    pc = G.PivotedCholeskyPreconditioner(op, 50)
+    rep = G.solve_cg(b, G.SolverConfig(tolerance=1e-5, max_epochs=200), pc)
+    assert rep.reached_tolerance
+    err = max(np.linalg.norm(b.solutions[:, j] - direct[:, j]) / np.linalg.norm(direct[:, j]) for j in range(5))
+    assert err <= 1e-4
+
+
+def test_sgd_zero_lr_and_divergence(G, gpk_ctx, oracle):  # test_solvers.cpp:268-283, 331-343
+    n = 256
+    X, y = gp_problem(n, 2, 331)
+    raw = oracle.raw_from_constrained([1.0, 1.0, 1.0, 0.4])
+    T = _targets(oracle, n, 2, 332, y)
+    op = make_op(G, gpk_ctx, X, raw)
+    b = G.LinearSystemBatch(op, T)
+    rep = G.solve_sgd(b, G.SolverConfig(kind=2, tolerance=1e-12, max_epochs=1, batch_size=16, learning_rate=0.0))
+    assert np.max(np.abs(b.solutions)) == 0.0 and np.array_equal(b.residuals, T) and rep.residuals_estimated
+    b2 = G.LinearSystemBatch(op, T)
+    rep2 = G.solve_sgd(b2, G.SolverConfig(kind=2, tolerance=1e-10, max_epochs=50, batch_size=16,
+                                          learning_rate=1e6))
+    assert rep2.aborted and "divergence" in rep2.abort_reason
+
+
+def test_sgd_minibatches_bit_exact(G, gpk_ctx, oracle):
+    n, b, rounds = 393216, 512, 6
+    cfg = G.SolverConfig(kind=2, batch_size=b, seed=4, substream=7)
+    got = G.sgd_batches(gpk_ctx, n, cfg, 0, rounds)
+    ref = oracle.sample_without_replacement(4, 6, 7, n, b, rounds)
+    assert np.array_equal(got, ref)
+    got2 = G.sgd_batches(gpk_ctx, n, cfg, 3, 2)
+    assert np.array_equal(got2, ref[3:5])
+    small = G.sgd_batches(gpk_ctx, 97, G.SolverConfig(kind=2, batch_size=31, seed=5, substream=0), 0, 20)
+    assert np.array_equal(small, oracle.sample_without_replacement(5, 6, 0, 97, 31, 20))
+
+
+def test_epoch_budget_law(G, gpk_ctx, oracle):  # test_solvers.cpp:345-364
+    n = 512
+    X, y = gp_problem(n, 2, 349)
+    raw = oracle.raw_from_constrained([1.0, 1.0, 1.0, 0.05])
+    T = _targets(oracle, n, 3, 350, y)
+    op = make_op(G, gpk_ctx, X, raw)
+    for kind, per in ((0, 1.0), (1, 33 / n), (2, 20 / n)):
+        b = G.LinearSystemBatch(op, T)
+        rep = G.solve(b, G.SolverConfig(kind=kind, tolerance=1e-14, max_epochs=3, block_size=33, batch_size=20,
+                                         learning_rate=1.0))
+        assert rep.epochs_consumed <= 3.0 + per + 1e-12
+
+
+@pytest.mark.parametrize("n,d,pairs,s", [(600, 3, 64, 8), (2048, 26, 1024, 64)])
+def test_pathwise_targets_match_oracle(G, gpk_ctx, oracle, n, d, pairs, s):
+    X, _ = gp_problem(n, d, 7 * n)
+    raw = default_test_raw(d, oracle)
+    op = make_op(G, gpk_ctx, X, raw)
+    basis = G.build_rff_basis(gpk_ctx, d, pairs, s, 3)
+    f, w = basis.arrays()
+    rf, rw = oracle.rff_basis(d, pairs, s, 3)
+    assert np.array_equal(f, rf) and np.array_equal(w, rw)  # host Philox/Box-Muller port: bit-exact
+    t = G.pathwise_targets(basis, op, s, 3)
+    r = oracle.pathwise_targets(X, raw, pairs, s, s, 3)
+    assert np.max(np.abs(t.noise - r["noise"])) <= 1e-12
+    assert np.max(np.abs(t.prior_values - r["prior_values"])) <= 1e-10 * max(1, np.max(np.abs(r["prior_values"])))
+    assert np.max(np.abs(t.xi - r["xi"])) <= 1e-10 * max(1, np.max(np.abs(r["xi"])))
+
+
+def test_optimise_trajectory_matches_oracle(G, gpk_ctx, oracle):
+    """C1-shaped run at reduced n: pathwise + warm start + CG, 10 Adam steps."""
+    n, d = 1024, 8
+    X32, y32 = oracle.sinsum_dataset(n, d, seed=0)
+    X, y = X32.astype(np.float64), y32.astype(np.float64)
+    scfg = dict(kind=0, tolerance=0.01, max_epochs=50, preconditioner_rank=100)
+    ocfg = dict(estimator=1, warm_start=True, steps=10, learning_rate=0.1, probe_count=16, rff_pairs=512,
+                probe_seed=2, feature_seed=3, solver_seed=4)
+    ref = oracle.optimise(X, y, oracle.outer_config(solver=oracle.solver_config(**scfg), **ocfg), threads=8)
+    got = G.optimise(gpk_ctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
+    assert np.max(np.abs(got["constrained"] - ref["constrained"]) / ref["constrained"]) <= 1e-3
+    assert np.max(np.abs(got["iterations"] - ref["iterations"])) <= 1
+    same = got["iterations"] == ref["iterations"]
+    g, rg = got["gradient"][same], ref["gradient"][same]
+    assert np.max(np.abs(g - rg) / np.maximum(np.abs(rg), 1e-2 * np.max(np.abs(rg)))) <= 1e-3
