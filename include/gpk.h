@@ -96,6 +96,9 @@ gpk_status gpk_ctx_stream(gpk_ctx* ctx, void** stream_out);
  * out[3] = summed CUDA-event duration of those launches in ms (only while
  * profiling is on). gpk_ctx_reset_stats zeroes them. */
 gpk_status gpk_ctx_set_profiling(gpk_ctx* ctx, int enable);
+/* Operator kernel: 0 = FP32 SIMT (kv_slab_kernel), 1 = tcgen05 3xTF32
+ * (kv_tc_kernel; K evaluated into TMEM, contraction on the tensor cores). */
+gpk_status gpk_ctx_set_operator_kernel(gpk_ctx* ctx, int kernel);
 gpk_status gpk_ctx_reset_stats(gpk_ctx* ctx);
 gpk_status gpk_ctx_stats(gpk_ctx* ctx, double* out4);
 

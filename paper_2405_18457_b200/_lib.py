@@ -59,6 +59,7 @@ def _sig(lib):
         "gpk_ctx_launch_count": (C.c_int, [H, C.POINTER(C.c_longlong)]),
         "gpk_ctx_stream": (C.c_int, [H, C.POINTER(vp)]),
         "gpk_ctx_set_profiling": (C.c_int, [H, C.c_int]),
+        "gpk_ctx_set_operator_kernel": (C.c_int, [H, C.c_int]),
         "gpk_ctx_reset_stats": (C.c_int, [H]),
         "gpk_ctx_stats": (C.c_int, [H, dp]),
         "gpk_operator_create": (C.c_int, [H, dp, C.c_int, C.c_int, dp, C.POINTER(H)]),

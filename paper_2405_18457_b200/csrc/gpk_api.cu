@@ -86,6 +86,7 @@ struct gpk_ctx {
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof;  // K.V launch brackets
   size_t prof_used = 0;
+  int kernel = 0;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32
 };
 
 struct gpk_operator {
@@ -98,6 +99,7 @@ struct gpk_operator {
   std::vector<double> raw, inv_ls;
   double s = 1, s2 = 1, sigma = 1, sigma2 = 1;
   DBuf<double> part;      // kv split partials
+  DBuf<float> vpk;        // packed TF32 hi/lo RHS images (tcgen05 path)
   // scratch for host-facing calls
   DBuf<float> v32;
   DBuf<double> v64, out64, tmp64;
@@ -237,7 +239,8 @@ struct KvCall {
 void run_kv(gpk_operator* op, const KvCall& c) {
   cudaStream_t s = op->ctx->stream;
   const int Cmax = c.sel ? c.sel_block : c.C;
-  int splits = kv_choose_splits(c.R, Cmax, op->ctx->sms);
+  const bool tc = op->ctx->kernel == 1 && c.m <= 80;
+  int splits = kv_choose_splits(c.R, Cmax, op->ctx->sms, tc ? 128 : 256);
   int cps = (Cmax + splits - 1) / splits;
   cps = (cps + 31) / 32 * 32;
   splits = std::max(1, (Cmax + cps - 1) / cps);
@@ -273,9 +276,20 @@ void run_kv(gpk_operator* op, const KvCall& c) {
       ctx->prof.push_back({e0, e1});
     }
     auto& pr = ctx->prof[ctx->prof_used++];
-    GPK_CUDA(cudaEventRecord(pr.first, s));
-    kv_slab_launch(a, op->d, s);
+    if (tc) {
+      float* vpk = op->vpk.ensure(kv_tc_pack_floats(c.m, Cmax));
+      kv_tc_pack_launch(c.vdiag, c.v, c.vdiag ? c.m : a.ldv, Cmax, c.m, c.sel, c.sel_block, op->n, vpk, c.skip, s);
+      GPK_CUDA(cudaEventRecord(pr.first, s));
+      kv_tc_launch(a, vpk, s);
+    } else {
+      GPK_CUDA(cudaEventRecord(pr.first, s));
+      kv_slab_launch(a, op->d, s);
+    }
     GPK_CUDA(cudaEventRecord(pr.second, s));
+  } else if (tc) {
+    float* vpk = op->vpk.ensure(kv_tc_pack_floats(c.m, Cmax));
+    kv_tc_pack_launch(c.vdiag, c.v, c.vdiag ? c.m : a.ldv, Cmax, c.m, c.sel, c.sel_block, op->n, vpk, c.skip, s);
+    kv_tc_launch(a, vpk, s);
   } else {
     kv_slab_launch(a, op->d, s);
   }
@@ -1036,6 +1050,12 @@ gpk_status gpk_ctx_launch_count(gpk_ctx* c, long long* out) {
 gpk_status gpk_ctx_stream(gpk_ctx* c, void** out) {
   return guarded([&] { *out = static_cast<void*>(c->stream); });
 }
+gpk_status gpk_ctx_set_operator_kernel(gpk_ctx* c, int kernel) {
+  return guarded([&] {
+    if (kernel < 0 || kernel > 1) throw InvalidArgument("gpk_ctx_set_operator_kernel: 0 (SIMT) or 1 (tcgen05)");
+    c->kernel = kernel;
+  });
+}
 gpk_status gpk_ctx_set_profiling(gpk_ctx* c, int enable) {
   return guarded([&] { c->profiling = enable != 0; });
 }
@@ -1076,7 +1096,9 @@ gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d,
     op->d = d;
     op->dp = (d + 3) / 4 * 4;
     op->x64.ensure(static_cast<size_t>(n) * d);
-    op->xs32.ensure(static_cast<size_t>(n) * op->dp);
+    // 32 zero rows of padding: the tensor-core kernel bulk-copies whole 32-row chunks
+    op->xs32.ensure(static_cast<size_t>(n + 32) * op->dp);
+    GPK_CUDA(cudaMemsetAsync(op->xs32.p, 0, sizeof(float) * (n + 32) * op->dp, ctx->stream));
     op->xs64.ensure(static_cast<size_t>(n) * d);
     upload_colmajor(op.get(), inputs, n, d, op->x64.p);
     set_hyper(op.get(), raw);

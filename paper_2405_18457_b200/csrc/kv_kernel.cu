@@ -312,8 +312,8 @@ int kv_ld_for(int m) { return 8 * kv_tc_for(m) + 4; }
 
 // Split-K factor: fill 2 CTAs/SM x 148 SMs in whole waves while keeping each
 // split at least one chunk; prefers the split count whose last wave is fullest.
-int kv_choose_splits(int R, int C, int sms) {
-  const int tiles = (R + BM - 1) / BM;
+int kv_choose_splits(int R, int C, int sms, int rows_per_cta) {
+  const int tiles = (R + rows_per_cta - 1) / rows_per_cta;
   const int slots = 2 * sms;
   const int max_splits = std::max(1, (C + BK - 1) / BK);
   if (tiles >= 4 * slots) return 1;

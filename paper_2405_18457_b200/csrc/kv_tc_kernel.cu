@@ -1,0 +1,438 @@
+// K1/K2/K3 on the 5th-generation tensor cores: fused ARD distance ->
+// Matérn-3/2 -> K.V with the contraction on tcgen05 (3xTF32, FP32 accumulate
+// in TMEM), replacing KernelOperator::apply / apply_rows / apply_columns
+// (/root/reference/proj/core/src/kernel.cpp:133-177).
+//
+// CTA = 128 output rows (one per TMEM lane) x NPAD RHS columns (m rounded up
+// to a multiple of 16). Warp roles (10 warps):
+//   warps 0-7  evaluate K: warp w owns TMEM lanes 32(w%4).. and half (w/4)
+//              of every 32-column chunk; each thread computes 16 kernel
+//              entries k(x_row, x_c) (FP32, MUFU sqrt/ex2), splits them into
+//              TF32 hi + lo and writes both into TMEM with tcgen05.st — the
+//              A operand never touches shared memory.
+//   warp 8     producer: cp.async.bulk of the pre-packed V chunk (hi and lo
+//              images in the canonical no-swizzle K-major UMMA layout) and of
+//              the chunk's x_c rows into a 3-stage smem ring (mbarrier
+//              complete_tx).
+//   warp 9     one elected thread issues, per 32-column chunk, 12
+//              tcgen05.mma.kind::tf32 (M=128, N=NPAD, K=8):
+//              D += A_hi B_hi + A_hi B_lo + A_lo B_hi, and tcgen05.commit
+//              frees the smem stage and the TMEM A buffer.
+// Every `flush_chunks` chunks the eval warps drain D (tcgen05.ld) into the
+// FP64 per-split partial (deterministic, each thread owns its outputs) and the
+// next group restarts accumulation. kv_reduce (kv_kernel.cu) sums splits and
+// adds sigma^2 V on the diagonal.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "gpk_internal.cuh"
+
+namespace gpk {
+
+namespace {
+
+constexpr int TBM = 128;
+constexpr int TBK = 32;
+constexpr int STAGES = 3;
+constexpr int NTHREADS = 320;
+constexpr int EVAL_WARPS = 8;
+constexpr int TMEM_COLS = 256;
+constexpr int A_BASE = 128;  // TMEM column of the first A buffer (D uses [0, NPAD))
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kNegSqrt3Log2e = -2.4988211106473432f;  // -sqrt(3) * log2(e)
+constexpr float kSqrt3f = 1.7320508075688772f;
+
+// Canonical no-swizzle K-major UMMA smem descriptor (version 1 = tcgen05):
+// core matrices of 8 rows x 16 B; LBO = K-adjacent core-matrix stride,
+// SBO = 8-row-group stride (both in bytes).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version
+  return d;                             // base offset 0, lbo mode 0, SWIZZLE_NONE (0)
+}
+
+// kind::tf32 instruction descriptor: D F32, A/B TF32, both K-major, M=128.
+constexpr uint32_t tf32_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(TBM >> 4) << 24);
+}
+
+template <int NPAD>
+struct TcLayout {
+  static constexpr int IMG_FLOATS = NPAD * TBK;                 // one TF32 image of a chunk
+  static constexpr int CHUNK_FLOATS = 2 * IMG_FLOATS;           // hi + lo
+  static constexpr uint32_t CHUNK_BYTES = CHUNK_FLOATS * 4;
+};
+
+template <int NPAD, int DP4>
+__global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk) {
+  constexpr int DP = 4 * DP4;
+  using L = TcLayout<NPAD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* smB = reinterpret_cast<float*>(smem_raw);                    // [STAGES][CHUNK_FLOATS]
+  float* smX = smB + STAGES * L::CHUNK_FLOATS;                        // [STAGES][TBK][DP]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * TBK * DP);
+  uint64_t* full = bars;              // [STAGES]
+  uint64_t* empty = bars + STAGES;    // [STAGES]
+  uint64_t* a_full = bars + 2 * STAGES;       // [2]
+  uint64_t* a_empty = bars + 2 * STAGES + 2;  // [2]
+  uint64_t* d_full = bars + 2 * STAGES + 4;
+  uint64_t* d_empty = bars + 2 * STAGES + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 6);
+
+  if (a.skip && *a.skip) return;
+  int c0 = a.c0, C = a.C;
+  if (a.sel) {
+    c0 = *a.sel * a.sel_block;
+    C = min(a.sel_block, a.n - c0);
+  }
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int cb = split * a.cols_per_split;
+  const int ce = min(C, cb + a.cols_per_split);
+  const int nq = ce > cb ? (ce - cb + TBK - 1) / TBK : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (a.stats && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    const double entries = static_cast<double>(a.R) * C;
+    atomicAdd(a.stats, entries * a.m);
+    atomicAdd(a.stats + 1, entries * (2.0 * a.m + 3.0 * a.d + 6.0));
+  }
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], EVAL_WARPS);
+      mbar_init(&a_empty[b], 1);
+    }
+    mbar_init(d_full, 1);
+    mbar_init(d_empty, EVAL_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int flush = a.flush_chunks;
+  const int ngroups = (nq + flush - 1) / flush;
+
+  if (warp == 8) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      for (int k = 0; k < nq; ++k) {
+        const int s = k % STAGES;
+        if (k >= STAGES) mbar_wait(&empty[s], ((k - STAGES) / STAGES) & 1);
+        const int chunk = (cb / TBK) + k;  // cb is a multiple of TBK
+        const uint32_t xbytes = TBK * DP * 4;
+        mbar_expect_tx(&full[s], L::CHUNK_BYTES + xbytes);
+        bulk_g2s(smB + s * L::CHUNK_FLOATS, vpk + static_cast<size_t>(chunk) * L::CHUNK_FLOATS, L::CHUNK_BYTES,
+                 &full[s]);
+        bulk_g2s(smX + s * TBK * DP, a.xs + static_cast<size_t>(c0 + cb + k * TBK) * DP, xbytes, &full[s]);
+      }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc(NPAD);
+      for (int k = 0; k < nq; ++k) {
+        const int s = k % STAGES, b = k & 1;
+        const int g = k / flush;
+        const bool first_in_group = (k % flush) == 0;
+        const bool last_in_group = ((k + 1) % flush) == 0 || k + 1 == nq;
+        mbar_wait(&full[s], (k / STAGES) & 1);
+        mbar_wait(&a_full[b], (k / 2) & 1);
+        if (first_in_group && g > 0) mbar_wait(d_empty, (g - 1) & 1);
+        tc_fence_after();
+        const uint32_t bh = smem_u32(smB + s * L::CHUNK_FLOATS);
+        const uint32_t bl = bh + L::IMG_FLOATS * 4;
+        const uint32_t ah = tmem + A_BASE + b * 64;
+        const uint32_t al = ah + 32;
+#pragma unroll
+        for (int kk = 0; kk < TBK / 8; ++kk) {
+          const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
+          const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
+          tc_mma_tf32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
+          tc_mma_tf32(tmem, ah + kk * 8, dl, idesc, 1u);
+          tc_mma_tf32(tmem, al + kk * 8, dh, idesc, 1u);
+        }
+        tc_commit(&empty[s]);
+        tc_commit(&a_empty[b]);
+        if (last_in_group) tc_commit(d_full);
+      }
+    }
+  } else {
+    // ---------------- evaluation + epilogue warps ----------------
+    const int lg = warp & 3;           // TMEM lane group
+    const int half = warp >> 2;        // chunk columns [16*half, 16*half + 16)
+    const int row = lg * 32 + lane;    // row within the tile == TMEM lane
+    const int er = tile * TBM + row;
+    const int er_c = er < a.R ? er : 0;
+    const int gi = a.row_idx ? a.row_idx[er_c] : a.r0 + er_c;
+    float4 xi[DP4];
+#pragma unroll
+    for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(gi) * DP) + u);
+    const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
+    double* part = a.part + static_cast<size_t>(split) * a.R * a.m;
+    constexpr int DCOLS = NPAD / 2;  // D columns this thread drains
+    bool wrote = false;
+
+    for (int k = 0; k < nq; ++k) {
+      const int s = k % STAGES, b = k & 1;
+      mbar_wait(&full[s], (k / STAGES) & 1);
+      if (k >= 2) mbar_wait(&a_empty[b], ((k - 2) / 2) & 1);
+      tc_fence_after();
+      const float* xc = smX + s * TBK * DP + half * 16 * DP;
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const float4* xv = reinterpret_cast<const float4*>(xc + t * DP);
+        float r2a = 0.f, r2b = 0.f;
+#pragma unroll
+        for (int u = 0; u < DP4; ++u) {
+          const float4 c = xv[u];
+          const float d0 = c.x - xi[u].x, d1 = c.y - xi[u].y, d2 = c.z - xi[u].z, d3 = c.w - xi[u].w;
+          r2a = fmaf(d0, d0, r2a);
+          r2b = fmaf(d1, d1, r2b);
+          r2a = fmaf(d2, d2, r2a);
+          r2b = fmaf(d3, d3, r2b);
+        }
+        const float r = sqrt_approx(r2a + r2b);
+        const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
+        hi[t] = tf32_rna(kv);
+        lo[t] = tf32_rna(kv - __uint_as_float(hi[t]));
+      }
+      const uint32_t abase = tmem + lane_addr + A_BASE + b * 64 + half * 16;
+      tc_st16(abase, hi);
+      tc_st16(abase + 32, lo);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[b]);
+
+      const bool last_in_group = ((k + 1) % flush) == 0 || k + 1 == nq;
+      if (last_in_group) {
+        const int g = k / flush;
+        mbar_wait(d_full, g & 1);
+        tc_fence_after();
+        const bool row_ok = er < a.R;
+        double* prow = part + static_cast<size_t>(er_c) * a.m;
+#pragma unroll
+        for (int q = 0; q < DCOLS / 8; ++q) {
+          const int col0 = half * DCOLS + q * 8;
+          uint32_t v[8];
+          tc_ld8(tmem + lane_addr + col0, v);
+          tc_wait_ld();
+          if (row_ok) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int col = col0 + e;
+              if (col < a.m) prow[col] = (wrote ? prow[col] : 0.0) + static_cast<double>(__uint_as_float(v[e]));
+            }
+          }
+        }
+        wrote = true;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d_empty);
+      }
+    }
+    if (nq == 0 && er < a.R) {  // empty split: zero partial
+      double* prow = part + static_cast<size_t>(er) * a.m;
+      for (int col = half * DCOLS; col < min(a.m, (half + 1) * DCOLS); ++col) prow[col] = 0.0;
+    }
+  }
+  (void)ngroups;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+// Packs the FP32 (or FP64) RHS into per-chunk TF32 hi/lo images in the
+// canonical K-major no-swizzle layout: element (c, j) of chunk q sits at
+// ((j/8) * (TBK/4) + (c%TBK)/4) * 32 + (j%8) * 4 + c%4 within each image.
+__global__ void kv_pack_kernel(const double* v64, const float* v32, int ldv, int rows_max, int m, int npad,
+                               int nchunks, const int* sel, int sel_block, int n, float* vpk, const int* skip) {
+  if (skip && *skip) return;
+  int rows = rows_max;
+  if (sel) rows = min(sel_block, n - *sel * sel_block);
+  const long long total = static_cast<long long>(nchunks) * TBK * npad;
+  const int img = npad * TBK;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(e % npad);
+    const long long c = e / npad;
+    const int q = static_cast<int>(c / TBK), kk = static_cast<int>(c % TBK);
+    float hi = 0.f, lo = 0.f;
+    if (c < rows && j < m) {
+      if (v64) {
+        const double x = v64[c * ldv + j];
+        const float h = __uint_as_float(tf32_rna(static_cast<float>(x)));
+        hi = h;
+        lo = __uint_as_float(tf32_rna(static_cast<float>(x - static_cast<double>(h))));
+      } else {
+        const float x = v32[c * ldv + j];
+        const float h = __uint_as_float(tf32_rna(x));
+        hi = h;
+        lo = __uint_as_float(tf32_rna(x - h));
+      }
+    }
+    const size_t base = static_cast<size_t>(q) * 2 * img;
+    const int off = ((j / 8) * (TBK / 4) + kk / 4) * 32 + (j % 8) * 4 + (kk % 4);
+    vpk[base + off] = hi;
+    vpk[base + img + off] = lo;
+  }
+}
+
+template <int NPAD, int DP4>
+void launch_tc_one(const KvArgs& a, const float* vpk, cudaStream_t s) {
+  using L = TcLayout<NPAD>;
+  const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 16 * sizeof(uint64_t);
+  // at most 2 CTAs per SM: each allocates 256 of the 512 TMEM columns
+  const size_t smem = std::max<size_t>(need, 100 * 1024);
+  static bool configured = false;
+  if (!configured) {
+    GPK_CUDA(cudaFuncSetAttribute(kv_tc_kernel<NPAD, DP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = true;
+  }
+  dim3 grid((a.R + TBM - 1) / TBM, a.splits);
+  kv_tc_kernel<NPAD, DP4><<<grid, NTHREADS, smem, s>>>(a, vpk);
+  check_launch("kv_tc_kernel");
+}
+
+template <int NPAD>
+void launch_tc_n(const KvArgs& a, const float* vpk, cudaStream_t s) {
+  switch (a.dp / 4) {
+    case 1: return launch_tc_one<NPAD, 1>(a, vpk, s);
+    case 2: return launch_tc_one<NPAD, 2>(a, vpk, s);
+    case 3: return launch_tc_one<NPAD, 3>(a, vpk, s);
+    case 4: return launch_tc_one<NPAD, 4>(a, vpk, s);
+    case 5: return launch_tc_one<NPAD, 5>(a, vpk, s);
+    case 6: return launch_tc_one<NPAD, 6>(a, vpk, s);
+    case 7: return launch_tc_one<NPAD, 7>(a, vpk, s);
+    case 8: return launch_tc_one<NPAD, 8>(a, vpk, s);
+    default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
+  }
+}
+
+}  // namespace
+
+int kv_tc_npad(int m) { return std::max(16, (m + 15) / 16 * 16); }
+
+size_t kv_tc_pack_floats(int m, int rows) {
+  const int nchunks = (rows + TBK - 1) / TBK;
+  return static_cast<size_t>(nchunks) * 2 * kv_tc_npad(m) * TBK;
+}
+
+void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_max, int m, const int* sel,
+                       int sel_block, int n, float* vpk, const int* skip, cudaStream_t s) {
+  const int npad = kv_tc_npad(m);
+  const int nchunks = (rows_max + TBK - 1) / TBK;
+  const long long total = static_cast<long long>(nchunks) * TBK * npad;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  kv_pack_kernel<<<std::max(blocks, 1), 256, 0, s>>>(v64, v32, ldv, rows_max, m, npad, nchunks, sel, sel_block, n,
+                                                     vpk, skip);
+  check_launch("kv_pack_kernel");
+}
+
+void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s) {
+  switch (kv_tc_npad(a.m)) {
+    case 16: return launch_tc_n<16>(a, vpk, s);
+    case 32: return launch_tc_n<32>(a, vpk, s);
+    case 48: return launch_tc_n<48>(a, vpk, s);
+    case 64: return launch_tc_n<64>(a, vpk, s);
+    case 80: return launch_tc_n<80>(a, vpk, s);
+    default: throw std::invalid_argument("gpk: tensor-core operator supports m <= 80");
+  }
+}
+
+}  // namespace gpk

@@ -126,6 +126,10 @@ class Context:
         check(self._lib.gpk_ctx_stream(self.handle, C.byref(v)))
         return v.value
 
+    def set_operator_kernel(self, kernel: int):
+        """0 = FP32 SIMT operator kernel, 1 = tcgen05 3xTF32 operator kernel."""
+        check(self._lib.gpk_ctx_set_operator_kernel(self.handle, int(kernel)))
+
     def set_profiling(self, enable: bool):
         check(self._lib.gpk_ctx_set_profiling(self.handle, int(enable)))
 

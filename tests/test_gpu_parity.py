@@ -24,6 +24,16 @@ def G():
     return G
 
 
+KERNELS = [0, 1]  # 0: FP32 SIMT operator kernel, 1: tcgen05 3xTF32 operator kernel
+
+
+@pytest.fixture(params=KERNELS, ids=["simt", "tcgen05"])
+def kctx(request, gpk_ctx):
+    gpk_ctx.set_operator_kernel(request.param)
+    yield gpk_ctx
+    gpk_ctx.set_operator_kernel(0)
+
+
 def colrel(a, b):
     """max over columns of max|a-b| / max|b|."""
     a, b = np.atleast_2d(a.T).T, np.atleast_2d(b.T).T
@@ -36,21 +46,21 @@ def make_op(G, ctx, X, raw):
 
 @pytest.mark.parametrize("n,d,m", [(300, 3, 1), (1000, 8, 17), (2048, 26, 65), (777, 20, 65), (513, 1, 9),
                                    (1500, 11, 33), (4096, 3, 65)])
-def test_apply_matches_oracle(G, gpk_ctx, oracle, n, d, m):
+def test_apply_matches_oracle(G, kctx, oracle, n, d, m):
     X, _ = gp_problem(n, d, 1000 + n)
     raw = default_test_raw(d, oracle)
     V = np.asfortranarray(np.random.default_rng(n).standard_normal((n, m)))
-    op = make_op(G, gpk_ctx, X, raw)
+    op = make_op(G, kctx, X, raw)
     got = op.apply(V)
     ref = oracle.apply(X, raw, V, threads=8)
     assert colrel(got, ref) <= OP_TOL
 
 
-def test_apply_identity_is_dense(G, gpk_ctx, oracle):
+def test_apply_identity_is_dense(G, kctx, oracle):
     n, d = 64, 3
     X, _ = gp_problem(n, d, 101)
     raw = default_test_raw(d, oracle)
-    op = make_op(G, gpk_ctx, X, raw)
+    op = make_op(G, kctx, X, raw)
     H = oracle.dense(X, raw)
     assert np.max(np.abs(op.apply(np.eye(n)) - H)) <= 1e-6
     assert np.max(np.abs(op.dense() - H)) <= 1e-12
@@ -68,31 +78,31 @@ def test_apply_rejects_bad_input(G, gpk_ctx, oracle):
         G.KernelOperator(X, G.Hyperparameters.from_constrained([1.0, 1.0, -1.0, 1.0]), gpk_ctx)
 
 
-def test_apply_is_deterministic(G, gpk_ctx, oracle):
+def test_apply_is_deterministic(G, kctx, oracle):
     X, _ = gp_problem(3000, 5, 7)
-    op = make_op(G, gpk_ctx, X, default_test_raw(5, oracle))
+    op = make_op(G, kctx, X, default_test_raw(5, oracle))
     V = np.random.default_rng(0).standard_normal((3000, 65))
     assert np.array_equal(op.apply(V), op.apply(V))
 
 
 @pytest.mark.parametrize("n,d,m,b", [(2000, 3, 65, 512), (600, 8, 17, 37), (50, 2, 3, 5)])
-def test_apply_rows_matches_oracle(G, gpk_ctx, oracle, n, d, m, b):
+def test_apply_rows_matches_oracle(G, kctx, oracle, n, d, m, b):
     X, _ = gp_problem(n, d, 2 * n)
     raw = default_test_raw(d, oracle)
     V = np.asfortranarray(np.random.default_rng(1).standard_normal((n, m)))
     rows = np.sort(np.random.default_rng(2).choice(n, b, replace=False)).astype(np.int32)
-    op = make_op(G, gpk_ctx, X, raw)
+    op = make_op(G, kctx, X, raw)
     assert colrel(op.apply_rows(rows, V), oracle.apply_rows(X, raw, rows, V, threads=8)) <= OP_TOL
     with pytest.raises(IndexError):
         op.apply_rows([n], V)
 
 
 @pytest.mark.parametrize("n,d,m,c0,ln", [(2048, 26, 65, 512, 512), (1000, 4, 17, 990, 10), (300, 2, 5, 0, 300)])
-def test_apply_columns_matches_oracle(G, gpk_ctx, oracle, n, d, m, c0, ln):
+def test_apply_columns_matches_oracle(G, kctx, oracle, n, d, m, c0, ln):
     X, _ = gp_problem(n, d, 3 * n)
     raw = default_test_raw(d, oracle)
     U = np.asfortranarray(np.random.default_rng(1).standard_normal((ln, m)))
-    op = make_op(G, gpk_ctx, X, raw)
+    op = make_op(G, kctx, X, raw)
     assert colrel(op.apply_columns(c0, ln, U), oracle.apply_columns(X, raw, c0, ln, U, threads=8)) <= OP_TOL
 
 
@@ -164,14 +174,14 @@ def _targets(oracle, n, s, seed, y):
     (1, 2048, 26, 64, dict(block_size=512)),
     (2, 1024, 3, 16, dict(batch_size=128, learning_rate=10.0, max_epochs=5)),
 ])
-def test_solvers_match_oracle(G, gpk_ctx, oracle, kind, n, d, s, extra):
+def test_solvers_match_oracle(G, kctx, oracle, kind, n, d, s, extra):
     X, y = gp_problem(n, d, 6 * n + kind)
     raw = oracle.raw_from_constrained([1.0] * d + [1.0, 0.1 if kind < 2 else 0.5])
     T = _targets(oracle, n, s, 11, y)
     cfg = dict(kind=kind, tolerance=0.01, max_epochs=50, seed=4, substream=1)
     cfg.update(extra)
     ref = oracle.solve(X, raw, T, oracle.solver_config(**cfg), threads=8)
-    op = make_op(G, gpk_ctx, X, raw)
+    op = make_op(G, kctx, X, raw)
     batch = G.LinearSystemBatch(op, T)
     rep = G.solve(batch, G.SolverConfig(**cfg))
     assert not rep.aborted
@@ -268,7 +278,7 @@ def test_pathwise_targets_match_oracle(G, gpk_ctx, oracle, n, d, pairs, s):
     assert np.max(np.abs(t.xi - r["xi"])) <= 1e-10 * max(1, np.max(np.abs(r["xi"])))
 
 
-def test_optimise_trajectory_matches_oracle(G, gpk_ctx, oracle):
+def test_optimise_trajectory_matches_oracle(G, kctx, oracle):
     """C1-shaped run at reduced n: pathwise + warm start + CG, 10 Adam steps."""
     n, d = 1024, 8
     X32, y32 = oracle.sinsum_dataset(n, d, seed=0)
@@ -277,7 +287,7 @@ def test_optimise_trajectory_matches_oracle(G, gpk_ctx, oracle):
     ocfg = dict(estimator=1, warm_start=True, steps=10, learning_rate=0.1, probe_count=16, rff_pairs=512,
                 probe_seed=2, feature_seed=3, solver_seed=4)
     ref = oracle.optimise(X, y, oracle.outer_config(solver=oracle.solver_config(**scfg), **ocfg), threads=8)
-    got = G.optimise(gpk_ctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
+    got = G.optimise(kctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
     assert np.max(np.abs(got["constrained"] - ref["constrained"]) / ref["constrained"]) <= 1e-3
     assert np.max(np.abs(got["iterations"] - ref["iterations"])) <= 1
     same = got["iterations"] == ref["iterations"]
