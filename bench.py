@@ -309,7 +309,7 @@ def run_ours(args, world, rank, local):
                                parallelism="replicas" if world > 1 else "single-gpu"),
                 "seconds_per_ml_step": ms_max / args.steps / 1e3,
                 "solver_iterations_per_step": iters, "epochs_per_step": epochs,
-                "roofline": {"bound": "fp32_simt", "kernel": "kv_slab_kernel", "achieved": achieved,
+                "roofline": {"bound": "fp32_simt", "kernel": "kv_tc_kernel (tcgen05 3xTF32)", "achieved": achieved,
                              "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                              "traffic": traffic,
                              "peak_source": "148 SM x 128 FP32 lanes x 2 x median SM clock under load "

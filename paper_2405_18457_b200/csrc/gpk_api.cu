@@ -86,11 +86,17 @@ struct gpk_ctx {
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof;  // K.V launch brackets
   size_t prof_used = 0;
-  int kernel = 0;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32
+  int kernel = 1;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32 (default)
+  DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
+  DBuf<int> info;
+  int* info_host = nullptr;    // pinned
 };
 
 struct gpk_operator {
   gpk_ctx* ctx = nullptr;
+  // gradient-pass workspace (persistent across steps)
+  DBuf<float> gbuf[4];
+  DBuf<double> gpart, gtot, gdots;
   int n = 0, d = 0, dp = 0;
   DBuf<double> x64;       // [n][d] unscaled
   DBuf<float> xs32;       // [n][dp]
@@ -114,6 +120,8 @@ struct gpk_precond {
   DBuf<int> pivots;
   double sigma2 = 1;
   DBuf<double> part, T, inner;
+  DBuf<double> diag, pval, gpart, gram;
+  DBuf<int> pidx, stop;
 };
 
 struct gpk_batch {
@@ -128,6 +136,7 @@ struct gpk_batch {
   DBuf<CgCtl> ctl;
   DBuf<int> ibuf, ibuf2, flag;
   DBuf<double> blocks;
+  std::unique_ptr<gpk_precond> pc;  // dispatch-built preconditioner, reused across solves
 };
 
 struct gpk_rff_basis {
@@ -234,6 +243,8 @@ struct KvCall {
   int ldb = 0;
   double alpha = 1.0;
   const int* skip = nullptr;
+  const double* dotw = nullptr;  // fused column dot of the result (see KvReduceArgs)
+  double* dpart = nullptr;
 };
 
 void run_kv(gpk_operator* op, const KvCall& c) {
@@ -316,6 +327,9 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.ldb = c.ldb;
   r.alpha = c.alpha;
   r.skip = c.skip;
+  r.dotw = c.dotw;
+  r.dpart = c.dpart;
+  r.groups = kReduceGroups;
   kv_reduce_launch(r, s);
 }
 
@@ -353,8 +367,10 @@ void build_precond(gpk_precond* pc) {
   if (rank == 0) return;
   double* L = pc->L.ensure(static_cast<size_t>(n) * rank);
   int* piv = pc->pivots.ensure(rank);
-  DBuf<double> diag, pval;
-  DBuf<int> pidx, stop;
+  DBuf<double>& diag = pc->diag;
+  DBuf<double>& pval = pc->pval;
+  DBuf<int>& pidx = pc->pidx;
+  DBuf<int>& stop = pc->stop;
   diag.ensure(n);
   const int G = kReduceGroups;
   pval.ensure(G);
@@ -399,7 +415,8 @@ void build_precond(gpk_precond* pc) {
   if (achieved == 0) return;
   // small = L^T L + sigma^2 I (achieved x achieved), then its inverse
   const int r = achieved;
-  DBuf<double> gpart, gram;
+  DBuf<double>& gpart = pc->gpart;
+  DBuf<double>& gram = pc->gram;
   gpart.ensure(static_cast<size_t>(G) * r * r);
   gram.ensure(static_cast<size_t>(r) * r);
   // gram over the first r columns of L (ld = rank)
@@ -595,8 +612,9 @@ void solve_cg(gpk_batch* b, const gpk_solver_config* c, gpk_precond* pc, gpk_sol
     kc.out = hd;
     kc.ldo = m;
     kc.skip = stop;
+    kc.dotw = d;      // fused d.Hd column partials
+    kc.dpart = part;
     run_kv(op, kc);
-    col_reduce_launch(d, hd, n, m, m, 0, part, G, stop, s);
     cg_alpha_launch(part, G, m, gamma, alpha, ctl, s);
     cg_update_launch(b->solutions.p, b->residuals.p, d, hd, alpha, n, m, stop, s);
     precond_apply_dev(pc, op, b->residuals.p, m, p, stop);
@@ -619,42 +637,35 @@ void spd_inverse_batched(gpk_ctx* ctx, double* mats, int dim, int batch, double*
   GPK_CUDA(cudaSetDevice(ctx->device));
   if (cusolverDnSetStream(ctx->solver, s) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnSetStream");
   if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
-  std::vector<double*> ha(batch), hb(batch);
+  std::vector<double*> ha(2 * batch);
   for (int k = 0; k < batch; ++k) {
     ha[k] = mats + static_cast<size_t>(k) * dim * dim;
-    hb[k] = inv + static_cast<size_t>(k) * dim * dim;
+    ha[batch + k] = inv + static_cast<size_t>(k) * dim * dim;
   }
-  DBuf<double*> da, db;
-  DBuf<int> info;
-  da.ensure(batch);
-  db.ensure(batch);
-  info.ensure(batch);
-  GPK_CUDA(cudaMemcpyAsync(da.p, ha.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice, s));
-  GPK_CUDA(cudaMemcpyAsync(db.p, hb.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice, s));
-  if (cusolverDnDpotrfBatched(ctx->solver, CUBLAS_FILL_MODE_LOWER, dim, da.p, dim, info.p, batch) !=
+  double** da = ctx->ptr_a.ensure(2 * batch);
+  double** db = da + batch;
+  int* info = ctx->info.ensure(batch);
+  if (!ctx->info_host) GPK_CUDA(cudaMallocHost(&ctx->info_host, sizeof(int) * 4096));
+  if (batch > 4096) throw InvalidArgument("gpk: at most 4096 AP blocks");
+  GPK_CUDA(cudaMemcpyAsync(da, ha.data(), sizeof(double*) * 2 * batch, cudaMemcpyHostToDevice, s));
+  if (cusolverDnDpotrfBatched(ctx->solver, CUBLAS_FILL_MODE_LOWER, dim, da, dim, info, batch) !=
       CUSOLVER_STATUS_SUCCESS)
     throw CudaError("cusolverDnDpotrfBatched");
   count_launch();
-  std::vector<int> hinfo(batch);
-  GPK_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
-  // identity into inv
-  std::vector<double> eye(static_cast<size_t>(dim) * dim, 0.0);
-  for (int i = 0; i < dim; ++i) eye[static_cast<size_t>(i) * dim + i] = 1.0;
+  GPK_CUDA(cudaMemcpyAsync(ctx->info_host, info, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
+  set_identity_launch(inv, dim, batch, s);
+  GPK_CUDA(cudaStreamSynchronize(s));  // ha lifetime + info check
   for (int k = 0; k < batch; ++k)
-    GPK_CUDA(cudaMemcpyAsync(hb[k], eye.data(), sizeof(double) * dim * dim, cudaMemcpyHostToDevice, s));
-  GPK_CUDA(cudaStreamSynchronize(s));
-  for (int k = 0; k < batch; ++k)
-    if (hinfo[k] != 0)
+    if (ctx->info_host[k] != 0)
       throw NumericError("solve_ap: block Cholesky failed; block is not positive definite (noise scale too small)");
   const double one = 1.0;
   if (cublasDtrsmBatched(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, dim,
-                         dim, &one, da.p, dim, db.p, dim, batch) != CUBLAS_STATUS_SUCCESS)
+                         dim, &one, da, dim, db, dim, batch) != CUBLAS_STATUS_SUCCESS)
     throw CudaError("cublasDtrsmBatched");
   if (cublasDtrsmBatched(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, dim,
-                         dim, &one, da.p, dim, db.p, dim, batch) != CUBLAS_STATUS_SUCCESS)
+                         dim, &one, da, dim, db, dim, batch) != CUBLAS_STATUS_SUCCESS)
     throw CudaError("cublasDtrsmBatched");
   count_launch(2);
-  GPK_CUDA(cudaStreamSynchronize(s));
 }
 
 __global__ void pad_identity_kernel(double* blk, int block, int len) {
@@ -721,8 +732,9 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     kc.ldb = m;
     kc.alpha = -1.0;
     kc.skip = stop;
+    kc.dotw = b->residuals.p;  // fused ||R_j||^2 partials of the updated residual
+    kc.dpart = part;
     run_kv(op, kc);
-    col_reduce_launch(b->residuals.p, nullptr, n, m, m, 2, part, G, stop, s);
     ap_check_launch(part, G, m, b->scales_dev.p, c->tolerance, ctl, s);
   };
   drive(b, ctl, 8, budget, iteration);
@@ -808,12 +820,13 @@ void solve_dispatch(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   switch (c->kind) {
     case GPK_CG:
       if (c->preconditioner_rank > 0) {
-        gpk_precond pc;
-        pc.op = b->op;
-        pc.n = b->n;
-        pc.rank = std::min(c->preconditioner_rank, b->n);
-        build_precond(&pc);
-        return solve_cg(b, c, &pc, rep);
+        if (!b->pc) b->pc = std::make_unique<gpk_precond>();
+        gpk_precond* pc = b->pc.get();
+        pc->op = b->op;
+        pc->n = b->n;
+        pc->rank = std::min(c->preconditioner_rank, b->n);
+        build_precond(pc);
+        return solve_cg(b, c, pc, rep);
       }
       return solve_cg(b, c, nullptr, rep);
     case GPK_AP:
@@ -866,7 +879,7 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
   cudaStream_t s = op->ctx->stream;
   const int n = op->n, d = op->d, P = static_cast<int>(pairs.size());
   if (P < 1 || P > 2) throw InvalidArgument("derivative_quadratic_forms: 1 or 2 pairs supported");
-  std::vector<DBuf<float>> bufs(2 * P);
+  DBuf<float>* bufs = op->gbuf;
   GradArgs a{};
   a.xs = op->xs32.p;
   a.n = n;
@@ -899,7 +912,9 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
   a.log2_s2 = static_cast<float>(std::log2(op->s2));
   a.blocks = 2 * op->ctx->sms;
   const int per = P * (d + 1);
-  DBuf<double> part, tot, dots;
+  DBuf<double>& part = op->gpart;
+  DBuf<double>& tot = op->gtot;
+  DBuf<double>& dots = op->gdots;
   part.ensure(static_cast<size_t>(a.blocks) * per);
   tot.ensure(per);
   a.part = part.p;

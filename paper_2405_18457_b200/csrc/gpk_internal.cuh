@@ -87,6 +87,12 @@ struct KvReduceArgs {
   int ldb;
   double alpha;
   const int* skip;
+  // optional fused column reduction of the result: dpart[g][j] = sum over the
+  // group's rows of out[r][j] * w[r][j] (w = dotw, or out itself when
+  // dotw == out). Deterministic grouping as col_reduce.
+  const double* dotw;
+  double* dpart;
+  int groups;
 };
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s);
 
@@ -163,6 +169,8 @@ void scale_launch(const double* src, int count, double factor, double* dst, cons
 void dense_block64_launch(const double* xs64, int n, int d, double s2, double sigma2, int r0,
                           int rows, int c0, int cols, double* out, int ldo, int add_noise,
                           cudaStream_t s);  // out row-major [rows][ldo]
+
+void set_identity_launch(double* mats, int dim, int batch, cudaStream_t s);
 
 // AP (K8)
 void ap_scores_launch(const double* R, int n, int m, const double* inv_scales, int block,

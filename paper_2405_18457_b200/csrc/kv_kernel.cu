@@ -299,6 +299,53 @@ __global__ void kv_reduce_kernel(const KvReduceArgs a) {
   }
 }
 
+// Grouped variant: block g owns rows [g*R/G, (g+1)*R/G) and also emits the
+// per-column partial sum of out * w over its rows (fixed order).
+__global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
+  if (a.skip && *a.skip) return;
+  __shared__ double red[8][33];
+  int c0 = a.c0, C = a.C;
+  if (a.sel) {
+    c0 = *a.sel * a.sel_block;
+    C = min(a.sel_block, a.n - c0);
+  }
+  const int g = blockIdx.x, G = gridDim.x;
+  const int rb = static_cast<int>(static_cast<long long>(a.R) * g / G);
+  const int re = static_cast<int>(static_cast<long long>(a.R) * (g + 1) / G);
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+  for (int j0 = 0; j0 < a.m; j0 += 32) {
+    const int j = j0 + tx;
+    double dot = 0.0;
+    if (j < a.m) {
+      for (int r = rb + ty; r < re; r += 8) {
+        double acc = 0.0;
+        for (int s = 0; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
+        const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
+        if (gi >= c0 && gi < c0 + C) {
+          const int vr = gi - c0;
+          const double vv = a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
+                                    : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]);
+          acc += a.sigma2 * vv;
+        }
+        double* o = a.out + static_cast<size_t>(r) * a.ldo + j;
+        const double b = a.base ? a.base[static_cast<size_t>(r) * a.ldb + j] : 0.0;
+        const double val = b + a.alpha * acc;
+        *o = val;
+        const double w = (a.dotw == a.out) ? val : a.dotw[static_cast<size_t>(r) * a.ldo + j];
+        dot = fma(val, w, dot);
+      }
+    }
+    red[ty][tx] = dot;
+    __syncthreads();
+    if (ty == 0 && j < a.m) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q][tx];
+      a.dpart[static_cast<size_t>(g) * a.m + j] = t;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 int kv_tc_for(int m) {
@@ -344,6 +391,11 @@ void kv_slab_launch(const KvArgs& a, int /*dmax*/, cudaStream_t s) {
 }
 
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s) {
+  if (a.dpart) {
+    kv_reduce_dot_kernel<<<a.groups, 256, 0, s>>>(a);
+    check_launch("kv_reduce_dot_kernel");
+    return;
+  }
   const long long total = static_cast<long long>(a.R) * a.m;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
   kv_reduce_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);

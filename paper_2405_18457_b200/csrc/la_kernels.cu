@@ -124,10 +124,21 @@ void col_reduce_launch(const double* a, const double* b, int n, int m, int lda, 
 }
 
 namespace {
-// Sum of partial k for column j over groups, fixed order.
+// Sum of partial `off` over groups, fixed order (single thread; small counts only).
 __device__ double gsum(const double* part, int groups, int stride, int off) {
   double acc = 0.0;
   for (int g = 0; g < groups; ++g) acc += part[static_cast<size_t>(g) * stride + off];
+  return acc;
+}
+// Same sum by one warp: lane l adds groups l, l+32, ... then a fixed xor tree.
+// Deterministic (the summation shape depends only on `groups`); every lane
+// returns the total.
+__device__ __forceinline__ double warp_gsum(const double* part, int groups, int stride, int off) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int g = lane; g < groups; g += 32) acc += part[static_cast<size_t>(g) * stride + off];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
 }
 // Termination norms (linear_system.cpp:38-53) from per-column sums of squares.
@@ -145,9 +156,14 @@ __device__ void termination(const double* ss, int m, const double* scales, doubl
 __global__ void cg_init_scalars_kernel(const double* part, int groups, int m, const double* scales,
                                        double tol, double* gamma, CgCtl* ctl) {
   __shared__ double ss[512];
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    gamma[j] = gsum(part, groups, 2 * m, j);
-    ss[j] = gsum(part, groups, 2 * m, m + j);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < m; j += nw) {
+    const double g = warp_gsum(part, groups, 2 * m, j);
+    const double q = warp_gsum(part, groups, 2 * m, m + j);
+    if (lane == 0) {
+      gamma[j] = g;
+      ss[j] = q;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -161,7 +177,7 @@ __global__ void cg_init_scalars_kernel(const double* part, int groups, int m, co
 }
 void cg_init_scalars_launch(const double* part, int groups, int m, const double* scales, double tol,
                             double* gamma, CgCtl* ctl, cudaStream_t s) {
-  cg_init_scalars_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, gamma, ctl);
+  cg_init_scalars_kernel<<<1, 1024, 0, s>>>(part, groups, m, scales, tol, gamma, ctl);
   check_launch("cg_init");
 }
 
@@ -172,14 +188,17 @@ __global__ void cg_alpha_kernel(const double* part, int groups, int m, const dou
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    const double denom = gsum(part, groups, m, j);
-    double a;
-    if (denom > 0.0) a = gamma[j] / denom;
-    else if (gamma[j] == 0.0 && denom == 0.0) a = 0.0;
-    else a = __longlong_as_double(0x7ff8000000000000ULL);
-    alpha[j] = a;
-    if (!isfinite(a)) atomicOr(&bad, 1);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < m; j += nw) {
+    const double denom = warp_gsum(part, groups, m, j);
+    if (lane == 0) {
+      double a;
+      if (denom > 0.0) a = gamma[j] / denom;
+      else if (gamma[j] == 0.0 && denom == 0.0) a = 0.0;
+      else a = __longlong_as_double(0x7ff8000000000000ULL);
+      alpha[j] = a;
+      if (!isfinite(a)) atomicOr(&bad, 1);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0 && bad) {
@@ -189,7 +208,7 @@ __global__ void cg_alpha_kernel(const double* part, int groups, int m, const dou
 }
 void cg_alpha_launch(const double* part, int groups, int m, const double* gamma, double* alpha, CgCtl* ctl,
                      cudaStream_t s) {
-  cg_alpha_kernel<<<1, 256, 0, s>>>(part, groups, m, gamma, alpha, ctl);
+  cg_alpha_kernel<<<1, 1024, 0, s>>>(part, groups, m, gamma, alpha, ctl);
   check_launch("cg_alpha");
 }
 
@@ -216,11 +235,15 @@ __global__ void cg_beta_kernel(const double* part, int groups, int m, const doub
                                double* gamma, double* beta, CgCtl* ctl) {
   if (ctl->stop) return;
   __shared__ double ss[512];
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    const double gn = gsum(part, groups, 2 * m, j);
-    beta[j] = gamma[j] != 0.0 ? gn / gamma[j] : 0.0;
-    gamma[j] = gn;
-    ss[j] = gsum(part, groups, 2 * m, m + j);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < m; j += nw) {
+    const double gn = warp_gsum(part, groups, 2 * m, j);
+    const double q = warp_gsum(part, groups, 2 * m, m + j);
+    if (lane == 0) {
+      beta[j] = gamma[j] != 0.0 ? gn / gamma[j] : 0.0;
+      gamma[j] = gn;
+      ss[j] = q;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -233,7 +256,7 @@ __global__ void cg_beta_kernel(const double* part, int groups, int m, const doub
 }
 void cg_beta_launch(const double* part, int groups, int m, const double* scales, double tol, double* gamma,
                     double* beta, CgCtl* ctl, cudaStream_t s) {
-  cg_beta_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, gamma, beta, ctl);
+  cg_beta_kernel<<<1, 1024, 0, s>>>(part, groups, m, scales, tol, gamma, beta, ctl);
   check_launch("cg_beta");
 }
 
@@ -263,7 +286,11 @@ void cg_direction_launch(double* d, const double* p, const double* beta, int n, 
 
 __global__ void norms_kernel(const double* part, int groups, int m, const double* scales, double tol, double* out3) {
   __shared__ double ss[512];
-  for (int j = threadIdx.x; j < m; j += blockDim.x) ss[j] = gsum(part, groups, m, j);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < m; j += nw) {
+    const double q = warp_gsum(part, groups, m, j);
+    if (lane == 0) ss[j] = q;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int done;
@@ -273,7 +300,7 @@ __global__ void norms_kernel(const double* part, int groups, int m, const double
 }
 void norms_launch(const double* part, int groups, int m, const double* scales, double tol, double* out3,
                   cudaStream_t s) {
-  norms_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, out3);
+  norms_kernel<<<1, 1024, 0, s>>>(part, groups, m, scales, tol, out3);
   check_launch("norms");
 }
 
@@ -413,11 +440,15 @@ void lt_times_launch(const double* L, int n, int r, int ldl, const double* R, in
 
 __global__ void sum_partials_kernel(const double* part, int groups, int count, double* out, const int* skip) {
   SKIP_IF(skip);
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x)
-    out[e] = gsum(part, groups, count, e);
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = gw; e < count; e += nw) {
+    const double v = warp_gsum(part, groups, count, e);
+    if ((threadIdx.x & 31) == 0) out[e] = v;
+  }
 }
 void sum_partials_launch(const double* part, int groups, int count, double* out, const int* skip, cudaStream_t s) {
-  sum_partials_kernel<<<blocks_for(count, 256, 256), 256, 0, s>>>(part, groups, count, out, skip);
+  sum_partials_kernel<<<blocks_for(static_cast<long long>(count) * 32, 256, 1024), 256, 0, s>>>(part, groups, count,
+                                                                                               out, skip);
   check_launch("sum_partials");
 }
 
@@ -489,6 +520,19 @@ void dense_block64_launch(const double* xs64, int n, int d, double s2, double si
   check_launch("dense_block64");
 }
 
+__global__ void set_identity_kernel(double* mats, int dim, long long total) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long w = e % (static_cast<long long>(dim) * dim);
+    mats[e] = (w / dim == w % dim) ? 1.0 : 0.0;
+  }
+}
+void set_identity_launch(double* mats, int dim, int batch, cudaStream_t s) {
+  const long long total = static_cast<long long>(dim) * dim * batch;
+  set_identity_kernel<<<blocks_for(total, 256), 256, 0, s>>>(mats, dim, total);
+  check_launch("set_identity");
+}
+
 // ------------------------------------------------------------------ AP K8
 // score_k = || R[blk_k] * inv_scales || (solvers.cpp:123-132); one CTA per block.
 __global__ void ap_scores_kernel(const double* R, int n, int m, const double* inv_scales, int block, double* scores,
@@ -497,14 +541,17 @@ __global__ void ap_scores_kernel(const double* R, int n, int m, const double* in
   __shared__ double red[256];
   const int k = blockIdx.x;
   const int r0 = k * block, r1 = min(n, r0 + block);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   double acc = 0.0;
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+  for (int i = r0 + warp; i < r1; i += nw) {  // warp per row: coalesced
     double w = 0.0;
     const double* row = R + static_cast<size_t>(i) * m;
-    for (int j = 0; j < m; ++j) w += row[j] * inv_scales[j];
-    acc += w * w;
+    for (int j = lane; j < m; j += 32) w += row[j] * inv_scales[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    acc += w * w;  // identical on every lane
   }
-  red[threadIdx.x] = acc;
+  red[threadIdx.x] = lane == 0 ? acc : 0.0;
   __syncthreads();
   for (int off = blockDim.x / 2; off > 0; off >>= 1) {
     if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
@@ -535,28 +582,54 @@ void ap_select_launch(const double* scores, int nblocks, int* sel, const int* sk
 __global__ void ap_block_update_kernel(const double* inv_blocks, int block, int n, const int* sel, const double* R,
                                        int m, double* V, double* upd64, float* upd32, int ldv32, const int* skip) {
   SKIP_IF(skip);
+  // upd[i][j] = sum_c Hinv[i][c] R[r0 + c][j]; CTA = 8 rows x all m columns,
+  // thread (ty = row, tx) owns columns tx, tx+32, tx+64; R staged by 64-row chunks.
+  constexpr int RPC = 8, KC = 32, MAXM = 96;
+  __shared__ double rs[KC][MAXM];
+  __shared__ double hs[RPC][KC];
   const int k = *sel;
   const int r0 = k * block, len = min(block, n - r0);
   const double* Hi = inv_blocks + static_cast<size_t>(k) * block * block;
-  const int rows_per_cta = 8;
-  const int i0 = blockIdx.x * rows_per_cta;
-  for (int e = threadIdx.x; e < rows_per_cta * ldv32; e += blockDim.x) {
-    const int i = i0 + e / ldv32, j = e % ldv32;
-    if (i >= len) continue;
-    if (j >= m) {
-      upd32[static_cast<size_t>(i) * ldv32 + j] = 0.f;
-      continue;
+  const int i0 = blockIdx.x * RPC;
+  if (i0 >= len) return;
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int c0 = 0; c0 < len; c0 += KC) {
+    const int kc = min(KC, len - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kc * m; e += blockDim.x) {
+      const int c = e / m, j = e % m;
+      rs[c][j] = R[static_cast<size_t>(r0 + c0 + c) * m + j];
     }
-    double acc = 0.0;
-    const double* hrow = Hi + static_cast<size_t>(i) * block;
-    for (int c = 0; c < len; ++c) acc += hrow[c] * R[static_cast<size_t>(r0 + c) * m + j];
-    upd64[static_cast<size_t>(i) * m + j] = acc;
-    upd32[static_cast<size_t>(i) * ldv32 + j] = static_cast<float>(acc);
-    V[static_cast<size_t>(r0 + i) * m + j] += acc;
+    for (int e = threadIdx.x; e < RPC * KC; e += blockDim.x) {
+      const int rr = e / KC, c = e % KC;
+      hs[rr][c] = (i0 + rr < len && c < kc) ? Hi[static_cast<size_t>(i0 + rr) * block + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < kc; ++c) {
+      const double h = hs[ty][c];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (tx + 32 * q < m) acc[q] += h * rs[c][tx + 32 * q];
+    }
+  }
+  const int i = i0 + ty;
+  if (i < len) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int j = tx + 32 * q;
+      if (j < m) {
+        upd64[static_cast<size_t>(i) * m + j] = acc[q];
+        upd32[static_cast<size_t>(i) * ldv32 + j] = static_cast<float>(acc[q]);
+        V[static_cast<size_t>(r0 + i) * m + j] += acc[q];
+      }
+    }
+    for (int j = m + tx; j < ldv32; j += 32) upd32[static_cast<size_t>(i) * ldv32 + j] = 0.f;
   }
 }
 void ap_block_update_launch(const double* inv_blocks, int block, int n, const int* sel, const double* R, int m,
                             double* V, double* upd64, float* upd32, int ldv32, const int* skip, cudaStream_t s) {
+  if (m > 96) throw std::invalid_argument("gpk: AP supports at most 96 right-hand sides");
   ap_block_update_kernel<<<(block + 7) / 8, 256, 0, s>>>(inv_blocks, block, n, sel, R, m, V, upd64, upd32, ldv32, skip);
   check_launch("ap_block_update");
 }
@@ -565,7 +638,11 @@ void ap_block_update_launch(const double* inv_blocks, int block, int n, const in
 __global__ void ap_check_kernel(const double* part, int groups, int m, const double* scales, double tol, CgCtl* ctl) {
   if (ctl->stop) return;
   __shared__ double ss[512];
-  for (int j = threadIdx.x; j < m; j += blockDim.x) ss[j] = gsum(part, groups, m, j);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < m; j += nw) {
+    const double q = warp_gsum(part, groups, m, j);
+    if (lane == 0) ss[j] = q;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     ctl->iters += 1;
@@ -577,7 +654,7 @@ __global__ void ap_check_kernel(const double* part, int groups, int m, const dou
 }
 void ap_check_launch(const double* part, int groups, int m, const double* scales, double tol, CgCtl* ctl,
                      cudaStream_t s) {
-  ap_check_kernel<<<1, 256, 0, s>>>(part, groups, m, scales, tol, ctl);
+  ap_check_kernel<<<1, 1024, 0, s>>>(part, groups, m, scales, tol, ctl);
   check_launch("ap_check");
 }
 

@@ -31,7 +31,7 @@ KERNELS = [0, 1]  # 0: FP32 SIMT operator kernel, 1: tcgen05 3xTF32 operator ker
 def kctx(request, gpk_ctx):
     gpk_ctx.set_operator_kernel(request.param)
     yield gpk_ctx
-    gpk_ctx.set_operator_kernel(0)
+    gpk_ctx.set_operator_kernel(1)
 
 
 def colrel(a, b):

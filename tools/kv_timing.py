@@ -44,9 +44,12 @@ def time_apply(ctx, n, d, m, reps=5, warm=2):
 
 if __name__ == "__main__":
     ctx = G.Context(0)
+    kernel = int(os.environ.get("GPK_KERNEL", "1"))
+    ctx.set_operator_kernel(kernel)
     shapes = [(4096, 8, 17), (16384, 26, 65), (43008, 20, 65), (131072, 3, 65), (131072, 11, 65)]
     if len(sys.argv) == 4:  # single shape: n d m
         shapes = [tuple(int(a) for a in sys.argv[1:4])]
     for n, d, m in shapes:
         r = time_apply(ctx, n, d, m)
+        r["kernel"] = ["simt", "tcgen05"][kernel]
         print(json.dumps(r), flush=True)
