@@ -251,7 +251,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   cudaStream_t s = op->ctx->stream;
   const int Cmax = c.sel ? c.sel_block : c.C;
   const bool tc = op->ctx->kernel == 1 && c.m <= 80;
-  int splits = kv_choose_splits(c.R, Cmax, op->ctx->sms, tc ? 128 : 256);
+  int splits = tc ? kv_tc_choose_splits(c.R, Cmax, op->ctx->sms) : kv_choose_splits(c.R, Cmax, op->ctx->sms);
   int cps = (Cmax + splits - 1) / splits;
   cps = (cps + 31) / 32 * 32;
   splits = std::max(1, (Cmax + cps - 1) / cps);

@@ -61,6 +61,7 @@ int kv_tc_for(int m);        // columns-per-lane template parameter for m
 int kv_ld_for(int m);        // FP32 RHS leading dimension for m
 void kv_slab_launch(const KvArgs& a, int dmax, cudaStream_t s);
 int kv_choose_splits(int R, int C, int sms, int rows_per_cta = 256);
+int kv_tc_choose_splits(int R, int C, int sms);
 
 // tcgen05 (3xTF32) variant of the operator slab (kv_tc_kernel.cu)
 int kv_tc_npad(int m);

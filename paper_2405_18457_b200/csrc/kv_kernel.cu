@@ -381,6 +381,30 @@ int kv_choose_splits(int R, int C, int sms, int rows_per_cta) {
   return best;
 }
 
+// Split count for the tensor-core kernel: minimise the busiest SM's work,
+// ceil(ctas / SMs) * (chunks per CTA + per-CTA overhead), where the overhead
+// (TMEM alloc, pipeline fill, FP64 epilogue, split-K partial traffic) is
+// worth ~4 chunks. Favours few long CTAs for short column ranges (AP slabs)
+// and enough CTAs to balance 148 SMs for full products.
+int kv_tc_choose_splits(int R, int C, int sms) {
+  const int tiles = (R + 127) / 128;
+  const int chunks = (C + BK - 1) / BK;
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= std::max(1, chunks); ++s) {
+    const long long ctas = static_cast<long long>(tiles) * s;
+    const double per = static_cast<double>((chunks + s - 1) / s) + 4.0;
+    const long long slots = 2LL * sms;  // two co-resident CTAs per SM (256 TMEM columns each)
+    const double cost = static_cast<double>((ctas + slots - 1) / slots) * per * (1.0 + 1e-3 * s);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = s;
+    }
+    if (ctas > 64LL * sms) break;
+  }
+  return best;
+}
+
 void kv_slab_launch(const KvArgs& a, int /*dmax*/, cudaStream_t s) {
   switch (kv_tc_for(a.m)) {
     case 1: return launch_tc<1>(a, s);
