@@ -245,6 +245,10 @@ struct KvCall {
   const int* skip = nullptr;
   const double* dotw = nullptr;  // fused column dot of the result (see KvReduceArgs)
   double* dpart = nullptr;
+  int groups = kReduceGroups;
+  const double* inv_scales = nullptr;  // fused AP block scores
+  double* spart = nullptr;
+  int score_block = 0, gpb = 1;
 };
 
 void run_kv(gpk_operator* op, const KvCall& c) {
@@ -329,7 +333,11 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.skip = c.skip;
   r.dotw = c.dotw;
   r.dpart = c.dpart;
-  r.groups = kReduceGroups;
+  r.groups = c.groups;
+  r.inv_scales = c.inv_scales;
+  r.spart = c.spart;
+  r.score_block = c.score_block;
+  r.gpb = c.gpb;
   kv_reduce_launch(r, s);
 }
 
@@ -677,15 +685,16 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   validate(c);
   const auto start = Clock::now();
   gpk_operator* op = b->op;
-  cudaStream_t s = op->ctx->stream;
-  const int n = b->n, m = b->m, G = kReduceGroups;
+  gpk_ctx* ctx = op->ctx;
+  cudaStream_t s = ctx->stream;
+  const int n = b->n, m = b->m;
   if (m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
   std::memset(rep, 0, sizeof(*rep));
   const int block = std::min(c->block_size, n);
   const int nblocks = (n + block - 1) / block;
   const double max_iterations = static_cast<double>(c->max_epochs) * n / block;  // solvers.cpp:118
   const int budget = static_cast<int>(std::ceil(max_iterations));
-  refresh_residuals(b);
+  const bool tc = ctx->kernel == 1;
   // inverse of every diagonal block H[blk, blk] (FP64), computed once per call
   const size_t bb = static_cast<size_t>(block) * block;
   double* mats = b->w1.ensure(bb * nblocks);
@@ -699,26 +708,66 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
       check_launch("pad_identity");
     }
   }
-  spd_inverse_batched(op->ctx, mats, block, nblocks, inv);
+  spd_inverse_batched(ctx, mats, block, nblocks, inv);
   std::vector<double> inv_scales(m);
   for (int j = 0; j < m; ++j) inv_scales[j] = 1.0 / b->scales[j];
   double* inv_scales_dev = b->vec1.ensure(m);
   GPK_CUDA(cudaMemcpyAsync(inv_scales_dev, inv_scales.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
-  double* scores = b->vec2.ensure(nblocks);
+  const int gpb = std::max(1, 256 / nblocks);  // reduction groups per AP block
+  const int groups = nblocks * gpb;
+  double* spart = b->vec2.ensure(groups);
+  double* part = b->red.ensure(static_cast<size_t>(groups) * m + 8);
   int* sel = b->ibuf.ensure(1);
+  double* Rs = b->w3.ensure(static_cast<size_t>(block) * m);
   double* upd64 = b->w2.ensure(static_cast<size_t>(block) * m);
-  float* upd32 = b->f32.ensure(static_cast<size_t>(std::max(block, n)) * kv_ld_for(m));
-  double* part = b->red.ensure(static_cast<size_t>(G) * 2 * m + 8);
+  float* upd32 = tc ? nullptr : b->f32.ensure(static_cast<size_t>(std::max(block, n)) * kv_ld_for(m));
+  double** ptrs = ctx->ptr_b.ensure(4);
+  {
+    double* hp[3] = {Rs, inv, upd64};
+    GPK_CUDA(cudaMemcpyAsync(ptrs, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
+  }
   init_ctl(b, budget, -1);
   CgCtl* ctl = b->ctl.p;
   const int* stop = &ctl->stop;
-  col_reduce_launch(b->residuals.p, nullptr, n, m, m, 2, part, G, nullptr, s);
-  ap_check_launch(part, G, m, b->scales_dev.p, c->tolerance, ctl, s);  // iters -1 -> 0, initial test
 
+  // refresh_residuals (solvers.cpp:98) with the fused norms and block scores
+  float* v32 = b->f32.ensure(static_cast<size_t>(std::max(block, n)) * kv_ld_for(m));
+  to_f32_launch(b->solutions.p, n, m, m, v32, kv_ld_for(m), nullptr, s);
+  {
+    KvCall kc;
+    kc.v = v32;
+    kc.m = m;
+    kc.R = n;
+    kc.C = n;
+    kc.vdiag = b->solutions.p;
+    kc.out = b->residuals.p;
+    kc.ldo = m;
+    kc.base = b->targets.p;
+    kc.ldb = m;
+    kc.alpha = -1.0;
+    kc.dotw = b->residuals.p;
+    kc.dpart = part;
+    kc.groups = groups;
+    kc.inv_scales = inv_scales_dev;
+    kc.spart = spart;
+    kc.score_block = block;
+    kc.gpb = gpb;
+    run_kv(op, kc);
+  }
+  ap_check_launch(part, groups, m, b->scales_dev.p, c->tolerance, ctl, s);  // iters -1 -> 0, initial test
+
+  if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
   auto iteration = [&]() {  // solvers.cpp:120-140
-    ap_scores_launch(b->residuals.p, n, m, inv_scales_dev, block, nblocks, scores, stop, s);
-    ap_select_launch(scores, nblocks, sel, stop, s);
-    ap_block_update_launch(inv, block, n, sel, b->residuals.p, m, b->solutions.p, upd64, upd32, kv_ld_for(m), stop, s);
+    ap_select_groups_launch(spart, nblocks, gpb, sel, stop, s);
+    ap_gather_launch(b->residuals.p, n, m, block, sel, Rs, inv, upd64, ptrs, stop, s);
+    // upd (m x block, column-major == row-major [block][m]) = R_blk^T Hinv  (Hinv symmetric)
+    const double one = 1.0, zero = 0.0;
+    if (cublasDgemmBatched(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, m, block, block, &one,
+                           const_cast<const double* const*>(ptrs), m, const_cast<const double* const*>(ptrs + 1),
+                           block, &zero, ptrs + 2, m, 1) != CUBLAS_STATUS_SUCCESS)
+      throw CudaError("cublasDgemmBatched");
+    count_launch();
+    ap_apply_update_launch(upd64, n, m, block, sel, b->solutions.p, upd32, kv_ld_for(m), stop, s);
     KvCall kc;
     kc.v = upd32;
     kc.m = m;
@@ -732,10 +781,15 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     kc.ldb = m;
     kc.alpha = -1.0;
     kc.skip = stop;
-    kc.dotw = b->residuals.p;  // fused ||R_j||^2 partials of the updated residual
+    kc.dotw = b->residuals.p;  // fused ||R_j||^2 and block scores of the updated residual
     kc.dpart = part;
+    kc.groups = groups;
+    kc.inv_scales = inv_scales_dev;
+    kc.spart = spart;
+    kc.score_block = block;
+    kc.gpb = gpb;
     run_kv(op, kc);
-    ap_check_launch(part, G, m, b->scales_dev.p, c->tolerance, ctl, s);
+    ap_check_launch(part, groups, m, b->scales_dev.p, c->tolerance, ctl, s);
   };
   drive(b, ctl, 8, budget, iteration);
   const CgCtl h = read_ctl(b);

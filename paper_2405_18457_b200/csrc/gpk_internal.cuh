@@ -94,6 +94,12 @@ struct KvReduceArgs {
   const double* dotw;
   double* dpart;
   int groups;
+  // optional AP block scores (solvers.cpp:123-132): spart[g] = sum over the
+  // group's rows of (sum_j out[r][j] * inv_scales[j])^2. Groups are then laid
+  // out inside AP blocks: gpb groups per block of `score_block` rows.
+  const double* inv_scales;
+  double* spart;
+  int score_block, gpb;
 };
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s);
 
@@ -177,6 +183,14 @@ void set_identity_launch(double* mats, int dim, int batch, cudaStream_t s);
 void ap_scores_launch(const double* R, int n, int m, const double* inv_scales, int block,
                       int nblocks, double* scores, const int* skip, cudaStream_t s);
 void ap_select_launch(const double* scores, int nblocks, int* sel, const int* skip, cudaStream_t s);
+// scores from per-group partials (gpb groups per block), then argmax
+void ap_select_groups_launch(const double* spart, int nblocks, int gpb, int* sel, const int* skip, cudaStream_t s);
+// R block -> zero-padded staging [block][m]; pointer arrays for the batched GEMM upd = Hinv[sel] R_blk
+void ap_gather_launch(const double* R, int n, int m, int block, const int* sel, double* Rs, const double* inv_blocks,
+                      double* upd, double** ptrs, const int* skip, cudaStream_t s);
+// V[blk] += upd; optional FP32 copy of upd for the SIMT operator kernel
+void ap_apply_update_launch(const double* upd, int n, int m, int block, const int* sel, double* V, float* upd32,
+                            int ldv32, const int* skip, cudaStream_t s);
 void ap_block_update_launch(const double* inv_blocks, int block, int n, const int* sel,
                             const double* R, int m, double* V, double* upd64, float* upd32,
                             int ldv32, const int* skip, cudaStream_t s);

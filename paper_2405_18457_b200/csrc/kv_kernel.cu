@@ -299,50 +299,90 @@ __global__ void kv_reduce_kernel(const KvReduceArgs a) {
   }
 }
 
-// Grouped variant: block g owns rows [g*R/G, (g+1)*R/G) and also emits the
-// per-column partial sum of out * w over its rows (fixed order).
+// Grouped variant (warp per row, coalesced 520-byte row reads): block g owns a
+// contiguous row range, writes out = base + alpha * (sum of split partials +
+// sigma^2 V on the diagonal), and emits in a fixed order
+//   dpart[g][j] = sum_r out[r][j] * w[r][j]            (w = dotw, or out itself)
+//   spart[g]    = sum_r (sum_j out[r][j] inv_scales[j])^2   (AP block scores)
+__device__ __forceinline__ void group_rows(const KvReduceArgs& a, int g, int& rb, int& re) {
+  if (a.spart) {  // gpb groups inside each AP block of score_block rows
+    const int blk = g / a.gpb, sub = g % a.gpb;
+    const int b0 = blk * a.score_block, len = min(a.score_block, a.R - b0);
+    rb = b0 + static_cast<int>(static_cast<long long>(len) * sub / a.gpb);
+    re = b0 + static_cast<int>(static_cast<long long>(len) * (sub + 1) / a.gpb);
+  } else {
+    rb = static_cast<int>(static_cast<long long>(a.R) * g / gridDim.x);
+    re = static_cast<int>(static_cast<long long>(a.R) * (g + 1) / gridDim.x);
+  }
+}
+
 __global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
   if (a.skip && *a.skip) return;
-  __shared__ double red[8][33];
+  constexpr int NW = 8, MQ = 3;  // 8 warps; lane owns columns lane + 32 q, q < 3 (m <= 96)
+  __shared__ double red[NW][96];
+  __shared__ double sred[NW];
   int c0 = a.c0, C = a.C;
   if (a.sel) {
     c0 = *a.sel * a.sel_block;
     C = min(a.sel_block, a.n - c0);
   }
-  const int g = blockIdx.x, G = gridDim.x;
-  const int rb = static_cast<int>(static_cast<long long>(a.R) * g / G);
-  const int re = static_cast<int>(static_cast<long long>(a.R) * (g + 1) / G);
-  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
-  for (int j0 = 0; j0 < a.m; j0 += 32) {
-    const int j = j0 + tx;
-    double dot = 0.0;
-    if (j < a.m) {
-      for (int r = rb + ty; r < re; r += 8) {
+  const int g = blockIdx.x;
+  int rb, re;
+  group_rows(a, g, rb, re);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double dot[MQ] = {0.0, 0.0, 0.0};
+  double sc = 0.0;
+  double isc[MQ];
+#pragma unroll
+  for (int q = 0; q < MQ; ++q) {
+    const int j = lane + 32 * q;
+    isc[q] = (a.spart && j < a.m) ? a.inv_scales[j] : 0.0;
+  }
+  for (int r = rb + warp; r < re; r += NW) {
+    const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
+    const bool diag = gi >= c0 && gi < c0 + C;
+    double wsum = 0.0;
+#pragma unroll
+    for (int q = 0; q < MQ; ++q) {
+      const int j = lane + 32 * q;
+      if (j < a.m) {
         double acc = 0.0;
         for (int s = 0; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
-        const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
-        if (gi >= c0 && gi < c0 + C) {
+        if (diag) {
           const int vr = gi - c0;
-          const double vv = a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
-                                    : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]);
-          acc += a.sigma2 * vv;
+          acc += a.sigma2 * (a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
+                                     : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]));
         }
-        double* o = a.out + static_cast<size_t>(r) * a.ldo + j;
         const double b = a.base ? a.base[static_cast<size_t>(r) * a.ldb + j] : 0.0;
         const double val = b + a.alpha * acc;
-        *o = val;
+        a.out[static_cast<size_t>(r) * a.ldo + j] = val;
         const double w = (a.dotw == a.out) ? val : a.dotw[static_cast<size_t>(r) * a.ldo + j];
-        dot = fma(val, w, dot);
+        dot[q] = fma(val, w, dot[q]);
+        wsum += val * isc[q];
       }
     }
-    red[ty][tx] = dot;
-    __syncthreads();
-    if (ty == 0 && j < a.m) {
-      double t = 0.0;
-      for (int q = 0; q < 8; ++q) t += red[q][tx];
-      a.dpart[static_cast<size_t>(g) * a.m + j] = t;
+    if (a.spart) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+      sc += wsum * wsum;
     }
-    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < MQ; ++q) {
+    const int j = lane + 32 * q;
+    if (j < a.m) red[warp][j] = dot[q];
+  }
+  if (lane == 0) sred[warp] = sc;
+  __syncthreads();
+  for (int j = threadIdx.x; j < a.m; j += blockDim.x) {
+    double t = 0.0;
+    for (int w = 0; w < NW; ++w) t += red[w][j];
+    a.dpart[static_cast<size_t>(g) * a.m + j] = t;
+  }
+  if (a.spart && threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NW; ++w) t += sred[w];
+    a.spart[g] = t;
   }
 }
 
@@ -416,6 +456,7 @@ void kv_slab_launch(const KvArgs& a, int /*dmax*/, cudaStream_t s) {
 
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s) {
   if (a.dpart) {
+    if (a.m > 96) throw std::invalid_argument("gpk: fused reductions support m <= 96");
     kv_reduce_dot_kernel<<<a.groups, 256, 0, s>>>(a);
     check_launch("kv_reduce_dot_kernel");
     return;

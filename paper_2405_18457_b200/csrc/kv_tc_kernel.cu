@@ -40,6 +40,10 @@ constexpr int EVAL_WARPS = 8;
 constexpr int TMEM_COLS = 256;
 constexpr int A_BASE = 128;  // TMEM column of the first A buffer (D uses [0, NPAD))
 
+#ifndef GPK_EVAL_F32X2
+#define GPK_EVAL_F32X2 1  // packed FP32x2 distance loop (FADD2/FFMA2)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -257,6 +261,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
     float4 xi[DP4];
 #pragma unroll
     for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(gi) * DP) + u);
+#if GPK_EVAL_F32X2
+    uint64_t xi2[2 * DP4];
+#pragma unroll
+    for (int u = 0; u < DP4; ++u) {
+      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(xi[u].x), "f"(xi[u].y));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(xi[u].z), "f"(xi[u].w));
+    }
+#endif
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
     double* part = a.part + static_cast<size_t>(split) * a.R * a.m;
     constexpr int DCOLS = NPAD / 2;  // D columns this thread drains
@@ -271,6 +283,25 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
       uint32_t hi[16], lo[16];
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
+#if GPK_EVAL_F32X2
+        // packed FP32x2 (FADD2/FFMA2): two dimensions per instruction
+        uint64_t acc0 = 0ull, acc1 = 0ull;
+        const uint32_t xaddr = smem_u32(xc + t * DP);
+#pragma unroll
+        for (int u = 0; u < DP4; ++u) {
+          uint64_t c01, c23, d01, d23;
+          asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(c01), "=l"(c23) : "r"(xaddr + 16 * u));
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(c01), "l"(xi2[2 * u]));
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(c23), "l"(xi2[2 * u + 1]));
+          asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc0) : "l"(d01));
+          asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc1) : "l"(d23));
+        }
+        uint64_t accs;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(accs) : "l"(acc0), "l"(acc1));
+        float s0, s1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(accs));
+        const float r = sqrt_approx(s0 + s1);
+#else
         const float4* xv = reinterpret_cast<const float4*>(xc + t * DP);
         float r2a = 0.f, r2b = 0.f;
 #pragma unroll
@@ -283,9 +314,13 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
           r2b = fmaf(d3, d3, r2b);
         }
         const float r = sqrt_approx(r2a + r2b);
+#endif
         const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
-        hi[t] = tf32_rna(kv);
-        lo[t] = tf32_rna(kv - __uint_as_float(hi[t]));
+        // TF32 split: hi = kv with the 13 low mantissa bits cleared (exact), lo =
+        // kv - hi (exact in FP32); the tensor core reads lo's top 19 bits, so
+        // hi + lo carries ~21-22 bits of kv.
+        hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
+        lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
       }
       const uint32_t abase = tmem + lane_addr + A_BASE + b * 64 + half * 16;
       tc_st16(abase, hi);

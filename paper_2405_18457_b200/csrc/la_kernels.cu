@@ -634,6 +634,74 @@ void ap_block_update_launch(const double* inv_blocks, int block, int n, const in
   check_launch("ap_block_update");
 }
 
+__global__ void ap_select_groups_kernel(const double* spart, int nblocks, int gpb, int* sel, const int* skip) {
+  SKIP_IF(skip);
+  __shared__ double sc[4096];
+  for (int k = threadIdx.x; k < nblocks; k += blockDim.x) {
+    double t = 0.0;
+    for (int q = 0; q < gpb; ++q) t += spart[static_cast<size_t>(k) * gpb + q];
+    sc[k] = sqrt(t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int best_k = 0;
+    double best = -1.0;
+    for (int k = 0; k < nblocks; ++k)
+      if (sc[k] > best) { best = sc[k]; best_k = k; }  // strict '>' as solvers.cpp:129
+    *sel = best_k;
+  }
+}
+void ap_select_groups_launch(const double* spart, int nblocks, int gpb, int* sel, const int* skip, cudaStream_t s) {
+  if (nblocks > 4096) throw std::invalid_argument("gpk: at most 4096 AP blocks");
+  ap_select_groups_kernel<<<1, 256, 0, s>>>(spart, nblocks, gpb, sel, skip);
+  check_launch("ap_select_groups");
+}
+
+__global__ void ap_gather_kernel(const double* R, int n, int m, int block, const int* sel, double* Rs,
+                                 const double* inv_blocks, double* upd, double** ptrs, const int* skip) {
+  SKIP_IF(skip);
+  const int k = *sel;
+  const int r0 = k * block, len = min(block, n - r0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ptrs[0] = Rs;
+    ptrs[1] = const_cast<double*>(inv_blocks) + static_cast<size_t>(k) * block * block;
+    ptrs[2] = upd;
+  }
+  const long long total = static_cast<long long>(block) * m;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = e / m;
+    Rs[e] = c < len ? R[static_cast<size_t>(r0) * m + e] : 0.0;
+  }
+}
+void ap_gather_launch(const double* R, int n, int m, int block, const int* sel, double* Rs, const double* inv_blocks,
+                      double* upd, double** ptrs, const int* skip, cudaStream_t s) {
+  ap_gather_kernel<<<blocks_for(static_cast<long long>(block) * m, 256, 148), 256, 0, s>>>(R, n, m, block, sel, Rs,
+                                                                                         inv_blocks, upd, ptrs, skip);
+  check_launch("ap_gather");
+}
+
+__global__ void ap_apply_update_kernel(const double* upd, int n, int m, int block, const int* sel, double* V,
+                                       float* upd32, int ldv32, const int* skip) {
+  SKIP_IF(skip);
+  const int k = *sel;
+  const int r0 = k * block, len = min(block, n - r0);
+  const long long total = static_cast<long long>(len) * m;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / m;
+    const int j = static_cast<int>(e % m);
+    V[static_cast<size_t>(r0) * m + e] += upd[e];  // solutions[blk] += update (solvers.cpp:136)
+    if (upd32) upd32[i * ldv32 + j] = static_cast<float>(upd[e]);
+  }
+}
+void ap_apply_update_launch(const double* upd, int n, int m, int block, const int* sel, double* V, float* upd32,
+                            int ldv32, const int* skip, cudaStream_t s) {
+  ap_apply_update_kernel<<<blocks_for(static_cast<long long>(block) * m, 256, 148), 256, 0, s>>>(
+      upd, n, m, block, sel, V, upd32, ldv32, skip);
+  check_launch("ap_apply_update");
+}
+
 // iteration++ ; termination from sum of squares partials.
 __global__ void ap_check_kernel(const double* part, int groups, int m, const double* scales, double tol, CgCtl* ctl) {
   if (ctl->stop) return;
