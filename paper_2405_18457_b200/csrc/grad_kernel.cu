@@ -165,38 +165,50 @@ __global__ void __launch_bounds__(NT, 1) grad_kernel(const GradArgs a) {
     const int gi = row0 + pr;
     const bool row_ok = gi < a.n;
     const int gic = row_ok ? gi : a.n - 1;
-    float4 xi[DP4];
+    // x_row as FP32x2 pairs; distance, squares and the d lengthscale sums run
+    // on packed FADD2/FMUL2/FFMA2 (two dimensions per instruction)
+    uint64_t xi2[2 * DP4];
 #pragma unroll
-    for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(gic) * a.dp) + u);
+    for (int u = 0; u < DP4; ++u) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(gic) * a.dp) + u);
+      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(v.x), "f"(v.y));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(v.z), "f"(v.w));
+    }
     float u1[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p)
       u1[p] = (a.mcols[p] == 1 && row_ok) ? __ldg(a.u[p] + static_cast<size_t>(gic) * a.ldu[p]) : 0.f;
 
-    float accs[NP], accl[NP][DMAX];
+    float accs[NP];
+    uint64_t accl2[NP][DP / 2];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       accs[p] = 0.f;
 #pragma unroll
-      for (int k = 0; k < DMAX; ++k) accl[p][k] = 0.f;
+      for (int k = 0; k < DP / 2; ++k) accl2[p][k] = 0ull;
     }
+    const uint32_t xbase = static_cast<uint32_t>(__cvta_generic_to_shared(Xc));
 #pragma unroll 2
     for (int t = 0; t < 16; ++t) {
       const int c = pc + 4 * t;
-      const float4* xc = reinterpret_cast<const float4*>(Xc + c * DP);
-      float sq[DP];
-      float r2 = 0.f;
+      uint64_t sq2[DP / 2];
+      uint64_t r2a = 0ull, r2b = 0ull;
 #pragma unroll
       for (int u = 0; u < DP4; ++u) {
-        const float4 v = xc[u];
-        const float d0 = v.x - xi[u].x, d1 = v.y - xi[u].y, d2 = v.z - xi[u].z, d3 = v.w - xi[u].w;
-        sq[4 * u] = d0 * d0;
-        sq[4 * u + 1] = d1 * d1;
-        sq[4 * u + 2] = d2 * d2;
-        sq[4 * u + 3] = d3 * d3;
-        r2 += (sq[4 * u] + sq[4 * u + 1]) + (sq[4 * u + 2] + sq[4 * u + 3]);
+        uint64_t c01, c23, d01, d23;
+        asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(c01), "=l"(c23) : "r"(xbase + (c * DP + 4 * u) * 4));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(c01), "l"(xi2[2 * u]));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(c23), "l"(xi2[2 * u + 1]));
+        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(sq2[2 * u]) : "l"(d01));
+        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(sq2[2 * u + 1]) : "l"(d23));
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(r2a) : "l"(sq2[2 * u]));
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(r2b) : "l"(sq2[2 * u + 1]));
       }
-      const float r = sqrt_approx(r2);
+      uint64_t r2s;
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r2s) : "l"(r2a), "l"(r2b));
+      float q0, q1;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(q0), "=f"(q1) : "l"(r2s));
+      const float r = sqrt_approx(q0 + q1);
       const float e0 = ex2_approx(r * kNegSqrt3Log2e);           // exp(-sqrt3 r)
       const float kv = fmaf(r, kSqrt3f, 1.f) * e0;               // k / s^2
 #pragma unroll
@@ -204,10 +216,19 @@ __global__ void __launch_bounds__(NT, 1) grad_kernel(const GradArgs a) {
         const float g = (a.mcols[p] == 1) ? u1[p] * W1[p][c] : Gs[p][pr * GS + c];
         accs[p] = fmaf(kv, g, accs[p]);
         const float coeff = e0 * g;
+        uint64_t coeff2;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(coeff2) : "f"(coeff));
 #pragma unroll
-        for (int k = 0; k < DMAX; ++k) accl[p][k] = fmaf(coeff, sq[k], accl[p][k]);
+        for (int k = 0; k < DP / 2; ++k)
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(accl2[p][k]) : "l"(sq2[k]), "l"(coeff2));
       }
     }
+    float accl[NP][DMAX];
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k)
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(accl[p][2 * k]), "=f"(accl[p][2 * k + 1]) : "l"(accl2[p][k]));
     // ---- per-tile flush: warp reduce, then FP64 per-warp accumulators ----
 #pragma unroll
     for (int p = 0; p < NP; ++p) {

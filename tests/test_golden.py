@@ -1,0 +1,101 @@
+"""Committed golden fixtures (tests/golden/*.npz, made by tools/make_golden.py
+from the FP64 oracle at the BASELINE.json configurations).
+
+CPU: the oracle reproduces its fixtures bit for bit (regression pin).
+GPU: the CUDA path matches them within the north-star tolerances."""
+import os
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+CFG = {  # mirrors tools/make_golden.py
+    "c1": dict(n=4096, d=8, uniform=False, noise=0.1, s=16, pairs=512),
+    "c4": dict(n=393216, d=3, uniform=True, noise=0.05, s=64, pairs=1000),
+    "c5": dict(n=1835008, d=11, uniform=False, noise=0.1, s=64, pairs=2048),
+}
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLD, f"{name}.npz")))
+
+
+def inputs(oracle, name):
+    c = CFG[name]
+    X32, y32 = oracle.sinsum_dataset(c["n"], c["d"], c["uniform"], c["noise"], 0)
+    return np.asfortranarray(X32.astype(np.float64)), y32.astype(np.float64)
+
+
+def rhs(oracle, n, m):
+    return np.asfortranarray(oracle.stream_draw(11, 2, 0, "gaussian", n * m).reshape((n, m), order="F"))
+
+
+@pytest.mark.parametrize("name,rows", [("c1", 256), ("c4", 16), ("c5", 8)])
+def test_oracle_reproduces_slab_fixture(oracle, name, rows):
+    g = load(name)
+    X, _ = inputs(oracle, name)
+    m = CFG[name]["s"] + 1
+    hv = oracle.apply_rows(X, g["raw"], np.arange(rows, dtype=np.int32), rhs(oracle, X.shape[0], m), threads=8)
+    assert np.array_equal(hv, g["hv_rows"][:rows])
+
+
+def test_oracle_reproduces_sgd_batches(oracle):
+    g = load("c4")
+    got = oracle.sample_without_replacement(4, 6, 0, CFG["c4"]["n"], 512, 4)
+    assert np.array_equal(got, g["sgd_batches"])
+
+
+def test_c1_trajectory_fixture_is_sane():
+    g = load("c1")
+    c = g["traj_constrained"]
+    assert c.shape == (10, 10) and np.all(c > 0)
+    assert np.all(g["traj_iterations"] >= 1) and np.all(g["traj_iterations"] <= 50)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c4", "c5"])
+def test_gpu_slab_matches_fixture(gpk_ctx, oracle, name):
+    import paper_2405_18457_b200 as G
+    g = load(name)
+    c = CFG[name]
+    X32, _ = G.sinsum_dataset(c["n"], c["d"], c["uniform"], c["noise"], 0)
+    X = X32.astype(np.float64)
+    m = c["s"] + 1
+    op = G.KernelOperator(X, G.Hyperparameters.from_raw(g["raw"]), gpk_ctx)
+    rows = int(g["rows"])
+    got = op.apply_rows(np.arange(rows, dtype=np.int32), rhs(oracle, c["n"], m))
+    ref = g["hv_rows"]
+    err = max(np.max(np.abs(got[:, j] - ref[:, j])) / np.max(np.abs(ref[:, j])) for j in range(m))
+    assert err <= 2e-5, err
+
+
+@pytest.mark.gpu
+def test_gpu_sgd_batches_match_fixture(gpk_ctx):
+    import paper_2405_18457_b200 as G
+    g = load("c4")
+    got = G.sgd_batches(gpk_ctx, CFG["c4"]["n"], G.SolverConfig(kind=2, batch_size=512, seed=4, substream=0), 0, 4)
+    assert np.array_equal(got, g["sgd_batches"])
+
+
+@pytest.mark.gpu
+def test_gpu_c1_trajectory_matches_fixture(gpk_ctx):
+    """BASELINE configs[0] in full: n=4096 d=8, pathwise s=16, 1024 RFF, CG tol 0.01 warm start, 10 Adam steps."""
+    import paper_2405_18457_b200 as G
+    g = load("c1")
+    c = CFG["c1"]
+    X32, y32 = G.sinsum_dataset(c["n"], c["d"], c["uniform"], c["noise"], 0)
+    sc = G.SolverConfig(kind=0, tolerance=0.01, max_epochs=50, preconditioner_rank=100)
+    oc = G.OuterConfig(estimator=1, solver=sc, warm_start=True, steps=10, learning_rate=0.1, probe_count=16,
+                       rff_pairs=512, probe_seed=2, feature_seed=3, solver_seed=4)
+    r = G.optimise(gpk_ctx, X32.astype(np.float64), y32.astype(np.float64), oc)
+    ref = g["traj_constrained"]
+    assert np.max(np.abs(r["constrained"] - ref) / ref) <= 1e-3
+    assert np.max(np.abs(r["iterations"] - g["traj_iterations"])) <= 1
+    same = r["iterations"] == g["traj_iterations"]
+    for key in ("mean_residual_norm", "probe_residual_norm"):
+        a, b = r[key][same], g["traj_" + key][same]
+        assert np.max(np.abs(a - b) / b) <= 1e-4, key
+    gr, rg = r["gradient"][same], g["traj_gradient"][same]
+    assert np.max(np.abs(gr - rg) / np.maximum(np.abs(rg), 1e-2 * np.max(np.abs(rg)))) <= 1e-3
