@@ -102,6 +102,19 @@ gpk_status gpk_ctx_set_operator_kernel(gpk_ctx* ctx, int kernel);
 gpk_status gpk_ctx_reset_stats(gpk_ctx* ctx);
 gpk_status gpk_ctx_stats(gpk_ctx* ctx, double* out4);
 
+/* ---- multi-GPU (row-sharded; one process per GPU) ----------------------
+ * Rank 0 calls gpk_comm_unique_id and ships the 128 bytes to every rank out
+ * of band (e.g. a torch.distributed broadcast); each rank then calls
+ * gpk_ctx_init_comm on its own context. Afterwards gpk_optimiser_* / gpk_optimise
+ * on that context shard the n rows: rank r owns rows [r*S, min(n, (r+1)*S)),
+ * S = 32-row-aligned ceil(n / nranks) (gpk_shard_rows), holds only those rows of
+ * the solver state, and exchanges the packed search direction (all-gather
+ * over NVLink) and per-column partial sums (all-gathered, then summed in rank
+ * order so every rank takes bitwise identical decisions). X is replicated. */
+gpk_status gpk_comm_unique_id(unsigned char* id128);
+gpk_status gpk_ctx_init_comm(gpk_ctx* ctx, const unsigned char* id128, int nranks, int rank);
+gpk_status gpk_shard_rows(int n, int nranks, int rank, int* row0, int* row1);
+
 /* ---- KernelOperator (kernel.hpp:37-97) --------------------------------
  * gpk_operator_create replaces KernelOperator(shared_ptr<const Dataset>,
  * Hyperparameters, KernelOperatorOptions) (kernel.hpp:39-40, kernel.cpp:83-109):

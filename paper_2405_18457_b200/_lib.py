@@ -105,6 +105,9 @@ def _sig(lib):
         "gpk_optimiser_step": (C.c_int, [H, C.c_int, dp, ip]),
         "gpk_optimiser_state": (C.c_int, [H, dp, ip, ip]),
         "gpk_optimiser_destroy": (C.c_int, [H]),
+        "gpk_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+        "gpk_ctx_init_comm": (C.c_int, [H, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
+        "gpk_shard_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, ip, ip]),
         "gpk_sinsum_dataset": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                          C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     }

@@ -6,6 +6,8 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -90,10 +92,16 @@ struct gpk_ctx {
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
   int* info_host = nullptr;    // pinned
+  ncclComm_t comm = nullptr;   // multi-GPU (one process per GPU)
+  int nranks = 1, rank = 0;
 };
 
 struct gpk_operator {
   gpk_ctx* ctx = nullptr;
+  // row shard owned by this rank (nr == 1: the whole problem). Only operators
+  // built by the sharded optimiser have nr > 1.
+  int nr = 1, rk = 0, row0 = 0, nloc = 0, S = 0;
+  bool sharded = false;  // built by the optimiser on a context with a communicator
   // gradient-pass workspace (persistent across steps)
   DBuf<float> gbuf[4];
   DBuf<double> gpart, gtot, gdots;
@@ -180,6 +188,45 @@ gpk_status guarded(F&& f) {
   }
 }
 
+// NCCL is resolved at run time (dlopen) so libgpk carries no link-time NCCL
+// dependency: a process that already loaded one (e.g. PyTorch's bundled
+// libnccl.so.2) shares it, otherwise the system library is loaded.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw std::runtime_error(std::string("gpk: cannot load libnccl.so.2: ") + dlerror());
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.get_unique_id || !a.comm_init_rank || !a.comm_destroy || !a.all_gather || !a.error_string)
+      throw std::runtime_error("gpk: libnccl.so.2 lacks required symbols");
+    return a;
+  }();
+  return api;
+}
+
+// In-place all-gather of equal per-rank slices (no-op on one rank).
+void gather_inplace(gpk_operator* op, void* buf, size_t bytes_per_rank) {
+  if (!op->sharded) return;  // (a 1-rank communicator still issues the in-place all-gather)
+  gpk_ctx* ctx = op->ctx;
+  char* b = static_cast<char*>(buf);
+  const ncclResult_t r = nccl().all_gather(b + static_cast<size_t>(op->rk) * bytes_per_rank, b, bytes_per_rank,
+                                           ncclChar, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllGather: ") + nccl().error_string(r));
+  count_launch();
+}
+
 void require(bool ok, const char* msg) {
   if (!ok) throw InvalidArgument(msg);
 }
@@ -249,6 +296,8 @@ struct KvCall {
   const double* inv_scales = nullptr;  // fused AP block scores
   double* spart = nullptr;
   int score_block = 0, gpb = 1;
+  const float* vpk = nullptr;  // pre-packed (and, sharded, all-gathered) TF32 RHS images
+  int vshift = 0;              // diagonal RHS row offset (row shard start)
 };
 
 void run_kv(gpk_operator* op, const KvCall& c) {
@@ -283,6 +332,14 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.stats = op->ctx->stats;
   a.d = op->d;
   gpk_ctx* ctx = op->ctx;
+  if (c.vpk && !tc) throw InvalidArgument("gpk: pre-packed operator input needs the tcgen05 kernel");
+  const float* vpk = c.vpk;
+  if (tc && !vpk) {
+    float* buf = op->vpk.ensure(kv_tc_pack_floats(c.m, Cmax));
+    kv_tc_pack_launch(c.vdiag, c.v, c.vdiag ? c.m : a.ldv, Cmax, c.m, c.sel, c.sel_block, op->n, buf, c.skip, s);
+    vpk = buf;
+  }
+  cudaEvent_t* prof_end = nullptr;
   if (ctx->profiling) {
     if (ctx->prof_used == ctx->prof.size()) {
       cudaEvent_t e0, e1;
@@ -291,23 +348,14 @@ void run_kv(gpk_operator* op, const KvCall& c) {
       ctx->prof.push_back({e0, e1});
     }
     auto& pr = ctx->prof[ctx->prof_used++];
-    if (tc) {
-      float* vpk = op->vpk.ensure(kv_tc_pack_floats(c.m, Cmax));
-      kv_tc_pack_launch(c.vdiag, c.v, c.vdiag ? c.m : a.ldv, Cmax, c.m, c.sel, c.sel_block, op->n, vpk, c.skip, s);
-      GPK_CUDA(cudaEventRecord(pr.first, s));
-      kv_tc_launch(a, vpk, s);
-    } else {
-      GPK_CUDA(cudaEventRecord(pr.first, s));
-      kv_slab_launch(a, op->d, s);
-    }
-    GPK_CUDA(cudaEventRecord(pr.second, s));
-  } else if (tc) {
-    float* vpk = op->vpk.ensure(kv_tc_pack_floats(c.m, Cmax));
-    kv_tc_pack_launch(c.vdiag, c.v, c.vdiag ? c.m : a.ldv, Cmax, c.m, c.sel, c.sel_block, op->n, vpk, c.skip, s);
-    kv_tc_launch(a, vpk, s);
-  } else {
-    kv_slab_launch(a, op->d, s);
+    GPK_CUDA(cudaEventRecord(pr.first, s));
+    prof_end = &pr.second;
   }
+  if (tc)
+    kv_tc_launch(a, vpk, s);
+  else
+    kv_slab_launch(a, op->d, s);
+  if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
   KvReduceArgs r{};
   r.part = part;
   r.splits = splits;
@@ -338,7 +386,42 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.spart = c.spart;
   r.score_block = c.score_block;
   r.gpb = c.gpb;
+  r.vshift = c.vshift;
   kv_reduce_launch(r, s);
+}
+
+// out_local = base + alpha * H[own rows, :] V, for V given by this rank's rows
+// v_local (FP64 [nloc][m]). The local rows are packed into this rank's slice
+// of the TF32 image buffer and all-gathered so every rank holds the full RHS.
+// Optional fused column dot (dotw/dpart) as in KvCall.
+void apply_local(gpk_operator* op, const double* v_local, int m, double* out, const double* base, double alpha,
+                 const int* skip, const double* dotw = nullptr, double* dpart = nullptr) {
+  cudaStream_t s = op->ctx->stream;
+  const int S = op->S, nr = op->nr;
+  const size_t chunk_floats = kv_tc_pack_floats(m, 32);
+  const size_t mine = kv_tc_pack_floats(m, S);
+  float* vpk = op->vpk.ensure(mine * nr);
+  kv_tc_pack_launch(v_local, nullptr, m, S, m, nullptr, 0, op->n, vpk + mine * op->rk, skip, s, op->nloc);
+  gather_inplace(op, vpk, mine * sizeof(float));
+  (void)chunk_floats;
+  KvCall c;
+  c.vpk = vpk;
+  c.m = m;
+  c.r0 = op->row0;
+  c.R = op->nloc;
+  c.c0 = 0;
+  c.C = op->n;
+  c.vdiag = v_local;
+  c.vshift = op->row0;
+  c.out = out;
+  c.ldo = m;
+  c.base = base;
+  c.ldb = m;
+  c.alpha = alpha;
+  c.skip = skip;
+  c.dotw = dotw;
+  c.dpart = dpart;
+  run_kv(op, c);
 }
 
 // H V for V FP64 row-major [n][m] on device -> out row-major (ldo = m).
@@ -472,7 +555,7 @@ void build_precond(gpk_precond* pc) {
 // out = P^-1 R (device, row-major [n][m]); P == nullptr -> identity copy.
 void precond_apply_dev(gpk_precond* pc, gpk_operator* op, const double* R, int m, double* out, const int* skip) {
   cudaStream_t s = op->ctx->stream;
-  const int n = op->n;
+  const int n = op->nloc;  // this rank's rows (the whole problem on one GPU)
   if (!pc) {
     scale_launch(R, n * m, 1.0, out, skip, s);
     return;
@@ -481,24 +564,31 @@ void precond_apply_dev(gpk_precond* pc, gpk_operator* op, const double* R, int m
     scale_launch(R, n * m, pc->sigma2, out, skip, s);
     return;
   }
-  const int r = pc->achieved, G = kReduceGroups;
-  double* part = pc->part.ensure(static_cast<size_t>(G) * r * m);
+  // (L L^T + s2 I)^-1 R = (R - L (s2 I + L^T L)^-1 L^T R) / s2 ; L is replicated
+  // (identical pivots on every rank), L^T R is a sum over rows -> partials of
+  // this rank's rows, all-gathered and summed in rank order.
+  const int r = pc->achieved, G = kReduceGroups, nr = op->nr;
+  const double* Lloc = pc->L.p + static_cast<size_t>(op->row0) * pc->rank;
+  double* part = pc->part.ensure(static_cast<size_t>(nr) * G * r * m);
   double* T = pc->T.ensure(static_cast<size_t>(r) * m);
   double* inner = pc->inner.ensure(static_cast<size_t>(r) * m);
-  lt_times_launch(pc->L.p, n, r, pc->rank, R, m, part, G, skip, s);
-  sum_partials_launch(part, G, r * m, T, skip, s);
+  lt_times_launch(Lloc, n, r, pc->rank, R, m, part + static_cast<size_t>(op->rk) * G * r * m, G, skip, s);
+  gather_inplace(op, part, sizeof(double) * G * r * m);
+  sum_partials_launch(part, G * nr, r * m, T, skip, s);
   small_gemm_launch(pc->minv.p, r, r, T, m, inner, skip, s);
-  woodbury_launch(R, pc->L.p, n, r, pc->rank, inner, m, pc->sigma2, out, skip, s);
+  woodbury_launch(R, Lloc, n, r, pc->rank, inner, m, pc->sigma2, out, skip, s);
 }
 
 // ----------------------------------------------------------------- batch
 void batch_norms(gpk_batch* b, const double* R, double tol, double* mean, double* probe, int* done) {
-  cudaStream_t s = b->op->ctx->stream;
-  const int G = kReduceGroups;
-  double* part = b->red.ensure(static_cast<size_t>(G) * 2 * b->m + 8);
+  gpk_operator* op = b->op;
+  cudaStream_t s = op->ctx->stream;
+  const int G = kReduceGroups, nr = op->nr;
+  double* part = b->red.ensure(static_cast<size_t>(nr) * G * 2 * b->m + 8);
   double* o3 = b->vec3.ensure(std::max(3, b->m));
-  col_reduce_launch(R, nullptr, b->n, b->m, b->m, 2, part, G, nullptr, s);
-  norms_launch(part, G, b->m, b->scales_dev.p, tol, o3, s);
+  col_reduce_launch(R, nullptr, b->n, b->m, b->m, 2, part + static_cast<size_t>(op->rk) * G * b->m, G, nullptr, s);
+  gather_inplace(op, part, sizeof(double) * G * b->m);
+  norms_launch(part, G * nr, b->m, b->scales_dev.p, tol, o3, s);
   double h[3];
   GPK_CUDA(cudaMemcpyAsync(h, o3, sizeof(h), cudaMemcpyDeviceToHost, s));
   GPK_CUDA(cudaStreamSynchronize(s));
@@ -507,13 +597,16 @@ void batch_norms(gpk_batch* b, const double* R, double tol, double* mean, double
   *done = h[2] != 0.0;
 }
 
-void refresh_residuals(gpk_batch* b) {
+void refresh_residuals(gpk_batch* b) {  // linear_system.cpp:33
   gpk_operator* op = b->op;
-  float* v32 = b->f32.ensure(static_cast<size_t>(b->n) * kv_ld_for(b->m));
-  for (int j0 = 0; j0 < b->m; j0 += kMaxRhs) {
-    if (b->m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
+  if (b->m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
+  if (op->ctx->kernel == 1) {
+    apply_local(op, b->solutions.p, b->m, b->residuals.p, b->targets.p, -1.0, nullptr);
+  } else {
+    if (op->nr > 1) throw InvalidArgument("gpk: the sharded operator needs the tcgen05 kernel");
+    float* v32 = b->f32.ensure(static_cast<size_t>(b->n) * kv_ld_for(b->m));
+    apply_dev64(op, b->solutions.p, b->m, b->residuals.p, b->targets.p, -1.0, v32, nullptr);
   }
-  apply_dev64(op, b->solutions.p, b->m, b->residuals.p, b->targets.p, -1.0, v32, nullptr);
 }
 
 void validate(const gpk_solver_config* c) {  // linear_system.cpp:7-14
@@ -587,15 +680,21 @@ void solve_cg(gpk_batch* b, const gpk_solver_config* c, gpk_precond* pc, gpk_sol
   const auto start = Clock::now();
   gpk_operator* op = b->op;
   cudaStream_t s = op->ctx->stream;
-  const int n = b->n, m = b->m, G = kReduceGroups;
+  const int n = b->n, m = b->m, G = kReduceGroups;  // n: this rank's rows
+  const int nr = op->nr, rk = op->rk;
+  const bool tc = op->ctx->kernel == 1;
+  if (!tc && nr > 1) throw InvalidArgument("gpk: the sharded operator needs the tcgen05 kernel");
   if (m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
   std::memset(rep, 0, sizeof(*rep));
   const size_t nm = static_cast<size_t>(n) * m;
   double* d = b->w1.ensure(nm);
   double* p = b->w2.ensure(nm);
   double* hd = b->w3.ensure(nm);
-  float* d32 = b->f32.ensure(static_cast<size_t>(n) * kv_ld_for(m));
-  double* part = b->red.ensure(static_cast<size_t>(G) * 2 * m + 8);
+  float* d32 = tc ? nullptr : b->f32.ensure(static_cast<size_t>(n) * kv_ld_for(m));
+  // per-rank reduction partials [nr][G][2m]; each rank fills its slice, then all-gather
+  double* part = b->red.ensure(static_cast<size_t>(nr) * G * 2 * m + 8);
+  double* part2 = part + static_cast<size_t>(rk) * G * 2 * m;  // mode-1 slice ([G][2m])
+  double* part1 = part + static_cast<size_t>(rk) * G * m;      // dot slice ([G][m])
   double* gamma = b->vec1.ensure(m);
   double* alpha = b->vec2.ensure(m);
   double* beta = b->vec3.ensure(std::max(m, 3));
@@ -606,31 +705,38 @@ void solve_cg(gpk_batch* b, const gpk_solver_config* c, gpk_precond* pc, gpk_sol
   refresh_residuals(b);                                       // solvers.cpp:45
   precond_apply_dev(pc, op, b->residuals.p, m, p, nullptr);   // p = P^-1 r
   GPK_CUDA(cudaMemcpyAsync(d, p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, s));
-  to_f32_launch(d, n, m, m, d32, kv_ld_for(m), nullptr, s);
-  col_reduce_launch(b->residuals.p, p, n, m, m, 1, part, G, nullptr, s);
-  cg_init_scalars_launch(part, G, m, b->scales_dev.p, c->tolerance, gamma, ctl, s);
+  if (!tc) to_f32_launch(d, n, m, m, d32, kv_ld_for(m), nullptr, s);
+  col_reduce_launch(b->residuals.p, p, n, m, m, 1, part2, G, nullptr, s);
+  gather_inplace(op, part, sizeof(double) * G * 2 * m);
+  cg_init_scalars_launch(part, G * nr, m, b->scales_dev.p, c->tolerance, gamma, ctl, s);
 
   auto iteration = [&]() {  // solvers.cpp:52-82
-    KvCall kc;
-    kc.v = d32;
-    kc.m = m;
-    kc.R = n;
-    kc.C = n;
-    kc.vdiag = d;
-    kc.out = hd;
-    kc.ldo = m;
-    kc.skip = stop;
-    kc.dotw = d;      // fused d.Hd column partials
-    kc.dpart = part;
-    run_kv(op, kc);
-    cg_alpha_launch(part, G, m, gamma, alpha, ctl, s);
+    if (tc) {
+      apply_local(op, d, m, hd, nullptr, 1.0, stop, d, part1);  // Hd and the fused d.Hd partials
+    } else {
+      KvCall kc;
+      kc.v = d32;
+      kc.m = m;
+      kc.R = n;
+      kc.C = n;
+      kc.vdiag = d;
+      kc.out = hd;
+      kc.ldo = m;
+      kc.skip = stop;
+      kc.dotw = d;
+      kc.dpart = part1;
+      run_kv(op, kc);
+    }
+    gather_inplace(op, part, sizeof(double) * G * m);
+    cg_alpha_launch(part, G * nr, m, gamma, alpha, ctl, s);
     cg_update_launch(b->solutions.p, b->residuals.p, d, hd, alpha, n, m, stop, s);
     precond_apply_dev(pc, op, b->residuals.p, m, p, stop);
-    col_reduce_launch(b->residuals.p, p, n, m, m, 1, part, G, stop, s);
-    cg_beta_launch(part, G, m, b->scales_dev.p, c->tolerance, gamma, beta, ctl, s);
-    cg_direction_launch(d, p, beta, n, m, d32, kv_ld_for(m), stop, s);
+    col_reduce_launch(b->residuals.p, p, n, m, m, 1, part2, G, stop, s);
+    gather_inplace(op, part, sizeof(double) * G * 2 * m);
+    cg_beta_launch(part, G * nr, m, b->scales_dev.p, c->tolerance, gamma, beta, ctl, s);
+    cg_direction_launch(d, p, beta, n, m, d32, tc ? 0 : kv_ld_for(m), stop, s);
   };
-  drive(b, ctl, iteration_group(n), c->max_epochs, iteration);
+  drive(b, ctl, iteration_group(op->n), c->max_epochs, iteration);
   const CgCtl h = read_ctl(b);
   rep->iterations = h.iters;
   rep->epochs_consumed = h.iters;
@@ -878,7 +984,7 @@ void solve_dispatch(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
         gpk_precond* pc = b->pc.get();
         pc->op = b->op;
         pc->n = b->n;
-        pc->rank = std::min(c->preconditioner_rank, b->n);
+        pc->rank = std::min(c->preconditioner_rank, b->op->n);
         build_precond(pc);
         return solve_cg(b, c, pc, rep);
       }
@@ -929,9 +1035,15 @@ __global__ void pair_dot_kernel(const double* u, const double* w, int n, int ldu
   if (threadIdx.x == 0) part[g] = red[0];
 }
 
+// Pairs are given by this rank's rows (nloc of them). On a sharded operator the
+// FP32 copies of U and W are all-gathered to full height (every tile needs all
+// columns), the global tile list is split evenly across ranks, and the per-block
+// partial sums are all-gathered and summed in (rank, block) order.
 std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vector<PairDev>& pairs) {
   cudaStream_t s = op->ctx->stream;
   const int n = op->n, d = op->d, P = static_cast<int>(pairs.size());
+  const int nloc = op->nloc, nr = op->nr, rk = op->rk;
+  const int rows_alloc = op->S * nr;  // >= n; slot r holds rows [r*S, r*S + S)
   if (P < 1 || P > 2) throw InvalidArgument("derivative_quadratic_forms: 1 or 2 pairs supported");
   DBuf<float>* bufs = op->gbuf;
   GradArgs a{};
@@ -944,16 +1056,20 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
   for (int p = 0; p < P; ++p) {
     const PairDev& pd = pairs[p];
     const int ld = (pd.cols + 3) / 4 * 4;
-    float* u32 = bufs[2 * p].ensure(static_cast<size_t>(n) * ld);
-    const long long tot = static_cast<long long>(n) * ld;
+    float* u32 = bufs[2 * p].ensure(static_cast<size_t>(rows_alloc) * ld);
+    const long long tot = static_cast<long long>(nloc) * ld;
     const int nb = static_cast<int>(std::min<long long>((tot + 255) / 256, 148 * 16));
-    extract_f32_kernel<<<nb, 256, 0, s>>>(pd.u, n, pd.ldu, pd.col0, pd.cols, u32, ld);
+    extract_f32_kernel<<<nb, 256, 0, s>>>(pd.u, nloc, pd.ldu, pd.col0, pd.cols, u32 + static_cast<size_t>(op->row0) * ld,
+                                          ld);
     check_launch("extract_f32");
+    gather_inplace(op, u32, sizeof(float) * op->S * ld);
     const float* w32 = u32;
     if (pd.w != pd.u || pd.ldw != pd.ldu) {
-      float* wb = bufs[2 * p + 1].ensure(static_cast<size_t>(n) * ld);
-      extract_f32_kernel<<<nb, 256, 0, s>>>(pd.w, n, pd.ldw, pd.col0, pd.cols, wb, ld);
+      float* wb = bufs[2 * p + 1].ensure(static_cast<size_t>(rows_alloc) * ld);
+      extract_f32_kernel<<<nb, 256, 0, s>>>(pd.w, nloc, pd.ldw, pd.col0, pd.cols,
+                                            wb + static_cast<size_t>(op->row0) * ld, ld);
       check_launch("extract_f32");
+      gather_inplace(op, wb, sizeof(float) * op->S * ld);
       w32 = wb;
       a.symmetric = 0;
     }
@@ -965,31 +1081,40 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
   a.s2 = static_cast<float>(op->s2);
   a.log2_s2 = static_cast<float>(std::log2(op->s2));
   a.blocks = 2 * op->ctx->sms;
+  {
+    const long long T = (n + 63) / 64;
+    const long long ntiles = a.symmetric ? T * (T + 1) / 2 : T * T;
+    a.tile_begin = ntiles * rk / nr;
+    a.tile_end = ntiles * (rk + 1) / nr;
+  }
   const int per = P * (d + 1);
   DBuf<double>& part = op->gpart;
   DBuf<double>& tot = op->gtot;
   DBuf<double>& dots = op->gdots;
-  part.ensure(static_cast<size_t>(a.blocks) * per);
+  part.ensure(static_cast<size_t>(nr) * a.blocks * per);
   tot.ensure(per);
-  a.part = part.p;
+  a.part = part.p + static_cast<size_t>(rk) * a.blocks * per;
   grad_launch(a, s);
-  sum_partials_launch(part.p, a.blocks, per, tot.p, nullptr, s);
-  // noise terms: sum u.w (FP64)
+  gather_inplace(op, part.p, sizeof(double) * a.blocks * per);
+  sum_partials_launch(part.p, a.blocks * nr, per, tot.p, nullptr, s);
+  // noise terms: sum u.w (FP64) over this rank's rows, gathered
   const int G = kReduceGroups;
-  dots.ensure(static_cast<size_t>(G) * P);
+  dots.ensure(static_cast<size_t>(nr) * G * P);
   for (int p = 0; p < P; ++p) {
-    pair_dot_kernel<<<G, 256, 0, s>>>(pairs[p].u, pairs[p].w, n, pairs[p].ldu, pairs[p].ldw, pairs[p].col0,
-                                      pairs[p].cols, dots.p + static_cast<size_t>(p) * G);
+    pair_dot_kernel<<<G, 256, 0, s>>>(pairs[p].u, pairs[p].w, nloc, pairs[p].ldu, pairs[p].ldw, pairs[p].col0,
+                                      pairs[p].cols, dots.p + static_cast<size_t>(rk) * G * P + static_cast<size_t>(p) * G);
     check_launch("pair_dot");
   }
-  std::vector<double> th(per), dh(static_cast<size_t>(G) * P);
+  gather_inplace(op, dots.p, sizeof(double) * G * P);
+  std::vector<double> th(per), dh(static_cast<size_t>(nr) * G * P);
   GPK_CUDA(cudaMemcpyAsync(th.data(), tot.p, sizeof(double) * per, cudaMemcpyDeviceToHost, s));
-  GPK_CUDA(cudaMemcpyAsync(dh.data(), dots.p, sizeof(double) * G * P, cudaMemcpyDeviceToHost, s));
+  GPK_CUDA(cudaMemcpyAsync(dh.data(), dots.p, sizeof(double) * nr * G * P, cudaMemcpyDeviceToHost, s));
   GPK_CUDA(cudaStreamSynchronize(s));
   std::vector<std::vector<double>> out(P, std::vector<double>(d + 2, 0.0));
   for (int p = 0; p < P; ++p) {
     double uw = 0.0;
-    for (int g = 0; g < G; ++g) uw += dh[static_cast<size_t>(p) * G + g];
+    for (int r = 0; r < nr; ++r)
+      for (int g = 0; g < G; ++g) uw += dh[static_cast<size_t>(r) * G * P + static_cast<size_t>(p) * G + g];
     out[p][d + 1] = 2.0 * op->sigma * uw;                                     // kernel.cpp:249-252
     out[p][d] = (2.0 / op->s) * (op->s2 * th[static_cast<size_t>(p) * (d + 1) + d]);  // kernel.cpp:264
     for (int k = 0; k < d; ++k)                                                // kernel.cpp:265-268
@@ -1055,7 +1180,9 @@ void rff_prior_dev(gpk_operator* op, gpk_rff_basis* b, int s_count, double* prio
                              cudaMemcpyHostToDevice, s));
   }
   const double amplitude = op->s / std::sqrt(static_cast<double>(P));  // rff.cpp:47
-  rff_prior_launch(op->x64.p, op->n, d, fd, P, b->w_dev.p, 2 * P, s_count, amplitude, prior, s);
+  // this rank's rows only (all rows on one GPU)
+  rff_prior_launch(op->x64.p + static_cast<size_t>(op->row0) * d, op->nloc, d, fd, P, b->w_dev.p, 2 * P, s_count,
+                   amplitude, prior, s);
   GPK_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1105,6 +1232,7 @@ gpk_status gpk_ctx_destroy(gpk_ctx* c) {
       cudaEventDestroy(pr.second);
     }
     cudaFree(c->stats);
+    if (c->comm) nccl().comm_destroy(c->comm);
     cudaStreamDestroy(c->stream);
     delete c;
   });
@@ -1152,6 +1280,39 @@ gpk_status gpk_ctx_stats(gpk_ctx* c, double* out) {
   });
 }
 
+gpk_status gpk_comm_unique_id(unsigned char* id128) {
+  return guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    const ncclResult_t r = nccl().get_unique_id(&id);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclGetUniqueId: ") + nccl().error_string(r));
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+gpk_status gpk_ctx_init_comm(gpk_ctx* ctx, const unsigned char* id128, int nranks, int rank) {
+  return guarded([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "gpk_ctx_init_comm: 0 <= rank < nranks");
+    GPK_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    if (ctx->comm) nccl().comm_destroy(ctx->comm);
+    const ncclResult_t r = nccl().comm_init_rank(&ctx->comm, nranks, id, rank);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclCommInitRank: ") + nccl().error_string(r));
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+gpk_status gpk_shard_rows(int n, int nranks, int rank, int* row0, int* row1) {
+  return guarded([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "gpk_shard_rows: 0 <= rank < nranks");
+    const int S = (((n + nranks - 1) / nranks) + 31) / 32 * 32;  // whole 32-row operator chunks
+    *row0 = std::min(n, rank * S);
+    *row1 = std::min(n, (rank + 1) * S);
+  });
+}
+
 gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d, const double* raw,
                                gpk_operator** out) {
   return guarded([&] {
@@ -1164,6 +1325,8 @@ gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d,
     op->n = n;
     op->d = d;
     op->dp = (d + 3) / 4 * 4;
+    op->nloc = n;
+    op->S = n;
     op->x64.ensure(static_cast<size_t>(n) * d);
     // 32 zero rows of padding: the tensor-core kernel bulk-copies whole 32-row chunks
     op->xs32.ensure(static_cast<size_t>(n + 32) * op->dp);
@@ -1668,25 +1831,38 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
   gpk_operator* opp = nullptr;
   if (gpk_operator_create(ctx, inputs, n, d, o->raw.data(), &opp) != GPK_OK) throw InvalidArgument(g_err);
   o->op.reset(opp);
+  if (ctx->comm) {  // row shard of this rank (X stays replicated)
+    if (cfg->solver.kind != GPK_CG)
+      throw InvalidArgument("gpk_optimise: multi-GPU row sharding is implemented for the CG solver");
+    if (ctx->kernel != 1) throw InvalidArgument("gpk_optimise: multi-GPU needs the tcgen05 operator kernel");
+    opp->sharded = true;
+    opp->nr = ctx->nranks;
+    opp->rk = ctx->rank;
+    gpk_shard_rows(n, ctx->nranks, ctx->rank, &opp->row0, &opp->nloc);
+    opp->nloc -= opp->row0;
+    opp->S = (((n + ctx->nranks - 1) / ctx->nranks) + 31) / 32 * 32;
+    if (opp->nloc < 1) throw InvalidArgument("gpk_optimise: fewer rows than ranks * 32");
+  }
+  const int nloc = opp->nloc;
   cudaStream_t stream = ctx->stream;
   o->batch = std::make_unique<gpk_batch>();
   gpk_batch* b = o->batch.get();
   b->op = opp;
-  b->n = n;
+  b->n = nloc;
   b->m = o->m;
-  const size_t nm = static_cast<size_t>(n) * o->m;
+  const size_t nm = static_cast<size_t>(nloc) * o->m;
   b->targets.ensure(nm);
   b->solutions.ensure(nm);
   b->residuals.ensure(nm);
   b->scales.resize(o->m);
   b->scales_dev.ensure(o->m);
   o->prev.ensure(nm);
-  o->ycol.ensure(n);
-  GPK_CUDA(cudaMemcpyAsync(o->ycol.p, targets, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
-  GPK_CUDA(cudaMemcpy2DAsync(b->targets.p, sizeof(double) * o->m, o->ycol.p, sizeof(double), sizeof(double), n,
+  o->ycol.ensure(nloc);
+  GPK_CUDA(cudaMemcpyAsync(o->ycol.p, targets + opp->row0, sizeof(double) * nloc, cudaMemcpyHostToDevice, stream));
+  GPK_CUDA(cudaMemcpy2DAsync(b->targets.p, sizeof(double) * o->m, o->ycol.p, sizeof(double), sizeof(double), nloc,
                              cudaMemcpyDeviceToDevice, stream));
-  o->prior.ensure(static_cast<size_t>(n) * o->s);
-  o->noise.ensure(static_cast<size_t>(n) * o->s);
+  o->prior.ensure(static_cast<size_t>(nloc) * o->s);
+  o->noise.ensure(static_cast<size_t>(nloc) * o->s);
   GPK_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -1698,9 +1874,10 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
   gpk_operator* op = o->op.get();
   gpk_batch* b = o->batch.get();
   const int n = o->n, s = o->s, m = o->m, P = o->P, t = o->t;
+  const int nloc = op->nloc;
   const gpk_outer_config& cfg = o->cfg;
   const bool pathwise = cfg.estimator == 1;
-  const size_t nm = static_cast<size_t>(n) * m;
+  const size_t nm = static_cast<size_t>(nloc) * m;
   set_hyper(op, o->raw.data());
   const uint64_t substream = cfg.warm_start ? 0 : static_cast<uint64_t>(t);
   if (pathwise) {
@@ -1711,27 +1888,29 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
       o->basis.reset(bp);
     }
     rff_prior_dev(op, o->basis.get(), s, o->prior.p);
-    if (!o->have_noise || o->noise_sub != substream) {
-      gaussian_fill_launch(cfg.feature_seed, 5, substream, static_cast<int64_t>(n) * s, n, s, o->noise.p, stream);
+    if (!o->have_noise || o->noise_sub != substream) {  // rows of this rank of the n x s draw
+      gaussian_fill_rows_launch(cfg.feature_seed, 5, substream, n, s, op->row0, nloc, o->noise.p, stream);
       o->have_noise = true;
       o->noise_sub = substream;
     }
-    xi_assemble_launch(o->prior.p, o->noise.p, n, s, op->sigma, b->targets.p, m, 1, nullptr, stream);
+    xi_assemble_launch(o->prior.p, o->noise.p, nloc, s, op->sigma, b->targets.p, m, 1, nullptr, stream);
   } else {
     if (!o->have_noise || !cfg.warm_start) {
-      o->probes.ensure(static_cast<size_t>(n) * s);
-      gaussian_fill_launch(cfg.probe_seed, 2, substream, static_cast<int64_t>(n) * s, n, s, o->probes.p, stream);
+      o->probes.ensure(static_cast<size_t>(nloc) * s);
+      gaussian_fill_rows_launch(cfg.probe_seed, 2, substream, n, s, op->row0, nloc, o->probes.p, stream);
       o->have_noise = true;
     }
     GPK_CUDA(cudaMemcpy2DAsync(b->targets.p + 1, sizeof(double) * m, o->probes.p, sizeof(double) * s,
-                               sizeof(double) * s, n, cudaMemcpyDeviceToDevice, stream));
+                               sizeof(double) * s, nloc, cudaMemcpyDeviceToDevice, stream));
   }
-  {  // scales = ||b_j|| + eps (linear_system.cpp:21)
-    const int G = kReduceGroups;
-    double* part = b->red.ensure(static_cast<size_t>(G) * 2 * m + 8);
+  {  // scales = ||b_j|| + eps (linear_system.cpp:21); column sums over all ranks' rows
+    const int G = kReduceGroups, nr = op->nr;
+    double* part = b->red.ensure(static_cast<size_t>(nr) * G * 2 * m + 8);
     double* ss = b->vec1.ensure(m);
-    col_reduce_launch(b->targets.p, nullptr, n, m, m, 2, part, G, nullptr, stream);
-    sum_partials_launch(part, G, m, ss, nullptr, stream);
+    col_reduce_launch(b->targets.p, nullptr, nloc, m, m, 2, part + static_cast<size_t>(op->rk) * G * m, G, nullptr,
+                      stream);
+    gather_inplace(op, part, sizeof(double) * G * m);
+    sum_partials_launch(part, G * nr, m, ss, nullptr, stream);
     std::vector<double> h(m);
     GPK_CUDA(cudaMemcpyAsync(h.data(), ss, sizeof(double) * m, cudaMemcpyDeviceToHost, stream));
     GPK_CUDA(cudaStreamSynchronize(stream));

@@ -67,7 +67,7 @@ int kv_tc_choose_splits(int R, int C, int sms);
 int kv_tc_npad(int m);
 size_t kv_tc_pack_floats(int m, int rows);
 void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_max, int m, const int* sel,
-                       int sel_block, int n, float* vpk, const int* skip, cudaStream_t s);
+                       int sel_block, int n, float* vpk, const int* skip, cudaStream_t s, int rows_valid = -1);
 void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s);
 
 struct KvReduceArgs {
@@ -88,6 +88,7 @@ struct KvReduceArgs {
   int ldb;
   double alpha;
   const int* skip;
+  int vshift;           // diagonal RHS row = gi - c0 - vshift (row shard offset)
   // optional fused column reduction of the result: dpart[g][j] = sum over the
   // group's rows of out[r][j] * w[r][j] (w = dotw, or out itself when
   // dotw == out). Deterministic grouping as col_reduce.
@@ -115,6 +116,7 @@ struct GradArgs {
   float log2_s2, s2;
   double* part;         // [blocks][npairs*(d+1)]
   int blocks;
+  long long tile_begin, tile_end;  // global tile range of this rank (tile_end < 0: all tiles)
 };
 void grad_launch(const GradArgs& a, cudaStream_t s);
 
@@ -218,6 +220,9 @@ void rff_prior_launch(const double* x64, int n, int d, const double* freq, int p
                       cudaStream_t s_);  // prior row-major [n][s]
 void gaussian_fill_launch(uint64_t seed, uint64_t stream, uint64_t substream, int64_t count,
                           int n, int s, double* out_rowmajor, cudaStream_t st);  // col-major order
+// rows [row0, row0 + nloc) of the same n x s column-major fill, row-major [nloc][s]
+void gaussian_fill_rows_launch(uint64_t seed, uint64_t stream, uint64_t substream, int n, int s, int row0, int nloc,
+                               double* out_rowmajor, cudaStream_t st);
 void xi_assemble_launch(const double* prior, const double* noise, int n, int s, double sigma,
                         double* out, int ldo, int col0, double* xi_copy, cudaStream_t st);
 

@@ -77,9 +77,11 @@ __global__ void __launch_bounds__(NT, 1) grad_kernel(const GradArgs a) {
   const int T = (a.n + TB - 1) / TB;
   const long long ntiles = a.symmetric ? static_cast<long long>(T) * (T + 1) / 2
                                        : static_cast<long long>(T) * T;
-  const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const long long L0 = blockIdx.x * per;
-  const long long L1 = min(ntiles, L0 + per);
+  const long long tb = a.tile_end >= 0 ? a.tile_begin : 0;   // this rank's share of the tile list
+  const long long te = a.tile_end >= 0 ? min(a.tile_end, ntiles) : ntiles;
+  const long long per = (te - tb + gridDim.x - 1) / gridDim.x;
+  const long long L0 = tb + blockIdx.x * per;
+  const long long L1 = min(te, L0 + per);
 
   for (int e = tid; e < (NT / 32) * NP * (DMAX + 1); e += NT) (&wacc[0][0])[e] = 0.0;
 

@@ -288,7 +288,7 @@ __global__ void kv_reduce_kernel(const KvReduceArgs a) {
     for (int s = 0; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
     const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
     if (gi >= c0 && gi < c0 + C) {
-      const int vr = gi - c0;
+      const int vr = gi - c0 - a.vshift;
       const double vv = a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
                                 : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]);
       acc += a.sigma2 * vv;
@@ -349,7 +349,7 @@ __global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
         double acc = 0.0;
         for (int s = 0; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
         if (diag) {
-          const int vr = gi - c0;
+          const int vr = gi - c0 - a.vshift;
           acc += a.sigma2 * (a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
                                      : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]));
         }

@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
 __global__ void kv_pack_kernel(const double* v64, const float* v32, int ldv, int rows_max, int m, int npad,
                                int nchunks, const int* sel, int sel_block, int n, float* vpk, const int* skip) {
   if (skip && *skip) return;
-  int rows = rows_max;
+  int rows = rows_max;  // valid rows (rows beyond are zero-filled up to nchunks * TBK)
   if (sel) rows = min(sel_block, n - *sel * sel_block);
   const long long total = static_cast<long long>(nchunks) * TBK * npad;
   const int img = npad * TBK;
@@ -449,13 +449,13 @@ size_t kv_tc_pack_floats(int m, int rows) {
 }
 
 void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_max, int m, const int* sel,
-                       int sel_block, int n, float* vpk, const int* skip, cudaStream_t s) {
+                       int sel_block, int n, float* vpk, const int* skip, cudaStream_t s, int rows_valid) {
   const int npad = kv_tc_npad(m);
   const int nchunks = (rows_max + TBK - 1) / TBK;
   const long long total = static_cast<long long>(nchunks) * TBK * npad;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-  kv_pack_kernel<<<std::max(blocks, 1), 256, 0, s>>>(v64, v32, ldv, rows_max, m, npad, nchunks, sel, sel_block, n,
-                                                     vpk, skip);
+  kv_pack_kernel<<<std::max(blocks, 1), 256, 0, s>>>(v64, v32, ldv, rows_valid >= 0 ? rows_valid : rows_max, m, npad,
+                                                     nchunks, sel, sel_block, n, vpk, skip);
   check_launch("kv_pack_kernel");
 }
 

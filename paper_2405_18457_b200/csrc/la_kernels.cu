@@ -264,6 +264,13 @@ void cg_beta_launch(const double* part, int groups, int m, const double* scales,
 __global__ void cg_direction_kernel(double* d, const double* p, const double* beta, int n, int m, float* d32,
                                     int ldv, const int* skip) {
   SKIP_IF(skip);
+  if (!d32) {  // tcgen05 path: the operator packs d itself
+    const long long tot = static_cast<long long>(n) * m;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<long long>(gridDim.x) * blockDim.x)
+      d[e] = __dadd_rn(p[e], __dmul_rn(d[e], beta[e % m]));
+    return;
+  }
   const long long total = static_cast<long long>(n) * ldv;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -280,7 +287,8 @@ __global__ void cg_direction_kernel(double* d, const double* p, const double* be
 }
 void cg_direction_launch(double* d, const double* p, const double* beta, int n, int m, float* d32, int ldv,
                          const int* skip, cudaStream_t s) {
-  cg_direction_kernel<<<blocks_for(static_cast<long long>(n) * ldv, 256), 256, 0, s>>>(d, p, beta, n, m, d32, ldv, skip);
+  cg_direction_kernel<<<blocks_for(static_cast<long long>(n) * (d32 ? ldv : m), 256), 256, 0, s>>>(d, p, beta, n, m,
+                                                                                                 d32, ldv, skip);
   check_launch("cg_direction");
 }
 
@@ -974,6 +982,35 @@ void gaussian_fill_launch(uint64_t seed, uint64_t stream, uint64_t substream, in
   gaussian_fill_kernel<<<blocks_for((count + 1) / 2, 256), 256, 0, st>>>(seed, stream, substream, count, n, s,
                                                                         out_rowmajor);
   check_launch("gaussian_fill");
+}
+
+// Element (i, j) of the column-major n x s Gaussian fill for local rows
+// i in [row0, row0 + nloc): draw e = j*n + i is the cos (e even) or sin (e odd)
+// half of Box-Muller pair e/2, counter-indexed so any row block can be drawn.
+__global__ void gaussian_fill_rows_kernel(uint64_t seed, uint64_t stream, uint64_t substream, int n, int s, int row0,
+                                          int nloc, double* out) {
+  const long long total = static_cast<long long>(nloc) * s;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int il = static_cast<int>(q / s), j = static_cast<int>(q % s);
+    const long long e = static_cast<long long>(j) * n + row0 + il;
+    const long long p = e >> 1;
+    const U64x4 blk = philox4x64(static_cast<uint64_t>(p) >> 1, substream, 0, 0, seed, stream);
+    const int o = static_cast<int>((p & 1) * 2);
+    const double u1 = static_cast<double>((blk.v[o] >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>(blk.v[o + 1] >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 6.283185307179586 * u2;
+    double sn, cs;
+    sincos(angle, &sn, &cs);
+    out[q] = (e & 1) ? radius * sn : radius * cs;
+  }
+}
+void gaussian_fill_rows_launch(uint64_t seed, uint64_t stream, uint64_t substream, int n, int s, int row0, int nloc,
+                               double* out_rowmajor, cudaStream_t st) {
+  gaussian_fill_rows_kernel<<<blocks_for(static_cast<long long>(nloc) * s, 256), 256, 0, st>>>(
+      seed, stream, substream, n, s, row0, nloc, out_rowmajor);
+  check_launch("gaussian_fill_rows");
 }
 
 // out[i][col0 + j] = prior[i][j] + sigma * noise[i][j] (rff.cpp:77)

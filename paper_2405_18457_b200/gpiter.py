@@ -126,6 +126,11 @@ class Context:
         check(self._lib.gpk_ctx_stream(self.handle, C.byref(v)))
         return v.value
 
+    def init_comm(self, unique_id: bytes, nranks: int, rank: int):
+        """Joins the NCCL communicator (one process per GPU); see gpk_ctx_init_comm."""
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        check(self._lib.gpk_ctx_init_comm(self.handle, buf, nranks, rank))
+
     def set_operator_kernel(self, kernel: int):
         """0 = FP32 SIMT operator kernel, 1 = tcgen05 3xTF32 operator kernel."""
         check(self._lib.gpk_ctx_set_operator_kernel(self.handle, int(kernel)))

@@ -293,3 +293,22 @@ def test_optimise_trajectory_matches_oracle(G, kctx, oracle):
     same = got["iterations"] == ref["iterations"]
     g, rg = got["gradient"][same], ref["gradient"][same]
     assert np.max(np.abs(g - rg) / np.maximum(np.abs(rg), 1e-2 * np.max(np.abs(rg)))) <= 1e-3
+
+
+def test_sharded_optimiser_world1_matches_plain(G, gpk_ctx, oracle):
+    """The row-sharded optimiser (NCCL communicator, all-gathered packed
+    directions and partial sums) on a 1-rank communicator reproduces the plain
+    single-GPU run bit for bit."""
+    from paper_2405_18457_b200 import parallel as P
+    n, d = 2048, 8
+    X32, y32 = G.sinsum_dataset(n, d, False, 0.1, 0)
+    X, y = X32.astype(np.float64), y32.astype(np.float64)
+    scfg = dict(kind=0, tolerance=0.01, max_epochs=50, preconditioner_rank=100)
+    ocfg = dict(estimator=1, warm_start=True, steps=4, learning_rate=0.1, probe_count=16, rff_pairs=256,
+                probe_seed=2, feature_seed=3, solver_seed=4)
+    plain = G.optimise(gpk_ctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
+    ctx1 = G.Context(0)
+    ctx1.init_comm(P.comm_unique_id(), 1, 0)
+    sharded = G.optimise(ctx1, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
+    for key in ("constrained", "gradient", "mean_residual_norm", "probe_residual_norm", "iterations"):
+        assert np.array_equal(plain[key], sharded[key]), key
