@@ -89,7 +89,7 @@ def test_gpu_c1_trajectory_matches_fixture(gpk_ctx):
     sc = G.SolverConfig(kind=0, tolerance=0.01, max_epochs=50, preconditioner_rank=100)
     oc = G.OuterConfig(estimator=1, solver=sc, warm_start=True, steps=10, learning_rate=0.1, probe_count=16,
                        rff_pairs=512, probe_seed=2, feature_seed=3, solver_seed=4)
-    r = G.optimise(gpk_ctx, X32.astype(np.float64), y32.astype(np.float64), oc)
+    r = G.optimise(gpk_ctx, X32.astype(np.float64), y32.astype(np.float64), oc, init_constrained=[1.0] * 8 + [1.0, 0.1])
     ref = g["traj_constrained"]
     assert np.max(np.abs(r["constrained"] - ref) / ref) <= 1e-3
     assert np.max(np.abs(r["iterations"] - g["traj_iterations"])) <= 1

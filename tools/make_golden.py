@@ -21,7 +21,7 @@ THREADS = os.cpu_count() or 8
 CFG = {
     "c1": dict(n=4096, d=8, uniform=False, noise=0.1, s=16, pairs=512, kind=0, steps=10, max_epochs=50, block=1000,
                batch=500, lr_sgd=30.0),
-    "c2": dict(n=16384, d=26, uniform=False, noise=0.1, s=64, pairs=1024, kind=1, steps=20, max_epochs=50, block=512,
+    "c2": dict(n=16384, d=26, uniform=False, noise=0.1, s=64, pairs=1024, kind=1, steps=2, max_epochs=50, block=512,
                batch=500, lr_sgd=30.0),
     "c3": dict(n=43008, d=20, uniform=False, noise=0.1, s=64, pairs=1000, kind=0, steps=2, max_epochs=10, block=1000,
                batch=500, lr_sgd=30.0),
@@ -30,7 +30,9 @@ CFG = {
     "c5": dict(n=1835008, d=11, uniform=False, noise=0.1, s=64, pairs=2048, kind=0, steps=15, max_epochs=5,
                block=1000, batch=500, lr_sgd=30.0),
 }
-INIT = lambda d: O.raw_from_constrained([1.0] * d + [1.0, 0.1])  # noqa: E731
+# BASELINE.json: init lengthscales 1, signal 1, noise 0.1
+INIT_CONSTRAINED = lambda d: [1.0] * d + [1.0, 0.1]  # noqa: E731
+INIT = lambda d: O.raw_from_constrained(INIT_CONSTRAINED(d))  # noqa: E731
 
 
 def dataset(c):
@@ -63,7 +65,7 @@ def trajectory(name, steps=None):
     oc = O.outer_config(estimator=1, solver=sc, warm_start=True, steps=steps or c["steps"], learning_rate=0.1,
                         probe_count=c["s"], rff_pairs=c["pairs"], probe_seed=2, feature_seed=3, solver_seed=4)
     t = time.time()
-    r = O.optimise(X, y, oc, threads=THREADS)
+    r = O.optimise(X, y, oc, init_constrained=INIT_CONSTRAINED(c["d"]), threads=THREADS)
     print(f"{name}: {len(r['iterations'])} steps in {time.time() - t:.1f}s, iterations {list(r['iterations'])}",
           flush=True)
     return {k: np.asarray(v) for k, v in r.items()}
