@@ -145,6 +145,8 @@ struct gpk_batch {
   DBuf<int> ibuf, ibuf2, flag;
   DBuf<double> blocks;
   std::unique_ptr<gpk_precond> pc;  // dispatch-built preconditioner, reused across solves
+  DBuf<unsigned> ticket;             // last-block ticket of fused reductions (kept at 0 between uses)
+  DBuf<float> apk;                   // AP block update's TF32 operator images
 };
 
 struct gpk_rff_basis {
@@ -298,6 +300,13 @@ struct KvCall {
   int score_block = 0, gpb = 1;
   const float* vpk = nullptr;  // pre-packed (and, sharded, all-gathered) TF32 RHS images
   int vshift = 0;              // diagonal RHS row offset (row shard start)
+  // fused AP epilogue (see KvReduceArgs)
+  CgCtl* ctl = nullptr;
+  const double* scales = nullptr;
+  double tol = 0.0;
+  int* sel_out = nullptr;
+  int nblocks = 0;
+  unsigned* ticket = nullptr;
 };
 
 void run_kv(gpk_operator* op, const KvCall& c) {
@@ -387,6 +396,12 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.score_block = c.score_block;
   r.gpb = c.gpb;
   r.vshift = c.vshift;
+  r.ctl = c.ctl;
+  r.scales = c.scales;
+  r.tol = c.tol;
+  r.sel_out = c.sel_out;
+  r.nblocks = c.nblocks;
+  r.ticket = c.ticket;
   kv_reduce_launch(r, s);
 }
 
@@ -835,6 +850,12 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   init_ctl(b, budget, -1);
   CgCtl* ctl = b->ctl.p;
   const int* stop = &ctl->stop;
+  if (!b->ticket.p) {
+    b->ticket.ensure(1);
+    GPK_CUDA(cudaMemsetAsync(b->ticket.p, 0, sizeof(unsigned), s));
+  }
+  unsigned* ticket = b->ticket.p;
+  float* vpk_blk = tc ? b->apk.ensure(kv_tc_pack_floats(m, block)) : nullptr;
 
   // refresh_residuals (solvers.cpp:98) with the fused norms and block scores
   float* v32 = b->f32.ensure(static_cast<size_t>(std::max(block, n)) * kv_ld_for(m));
@@ -858,12 +879,50 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     kc.spart = spart;
     kc.score_block = block;
     kc.gpb = gpb;
+    kc.ctl = ctl;  // fused initial test (iters -1 -> 0) and first block choice
+    kc.scales = b->scales_dev.p;
+    kc.tol = c->tolerance;
+    kc.sel_out = sel;
+    kc.nblocks = nblocks;
+    kc.ticket = ticket;
     run_kv(op, kc);
   }
-  ap_check_launch(part, groups, m, b->scales_dev.p, c->tolerance, ctl, s);  // iters -1 -> 0, initial test
 
   if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
   auto iteration = [&]() {  // solvers.cpp:120-140
+    if (tc) {
+      // fused: block update + V update + TF32 images; slab; reduce + test + next block
+      ap_update_pack_launch(b->residuals.p, n, m, block, sel, inv, b->solutions.p, upd64, vpk_blk, kv_tc_npad(m), stop,
+                            s);
+      KvCall kc;
+      kc.vpk = vpk_blk;
+      kc.m = m;
+      kc.R = n;
+      kc.sel = sel;
+      kc.sel_block = block;
+      kc.vdiag = upd64;
+      kc.out = b->residuals.p;
+      kc.ldo = m;
+      kc.base = b->residuals.p;
+      kc.ldb = m;
+      kc.alpha = -1.0;
+      kc.skip = stop;
+      kc.dotw = b->residuals.p;
+      kc.dpart = part;
+      kc.groups = groups;
+      kc.inv_scales = inv_scales_dev;
+      kc.spart = spart;
+      kc.score_block = block;
+      kc.gpb = gpb;
+      kc.ctl = ctl;
+      kc.scales = b->scales_dev.p;
+      kc.tol = c->tolerance;
+      kc.sel_out = sel;
+      kc.nblocks = nblocks;
+      kc.ticket = ticket;
+      run_kv(op, kc);
+      return;
+    }
     ap_select_groups_launch(spart, nblocks, gpb, sel, stop, s);
     ap_gather_launch(b->residuals.p, n, m, block, sel, Rs, inv, upd64, ptrs, stop, s);
     // upd (m x block, column-major == row-major [block][m]) = R_blk^T Hinv  (Hinv symmetric)

@@ -10,6 +10,8 @@
 
 namespace gpk {
 
+struct CgCtl;
+
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -101,6 +103,15 @@ struct KvReduceArgs {
   const double* inv_scales;
   double* spart;
   int score_block, gpb;
+  // optional fused AP epilogue, run by the last block to finish (ticket):
+  // iteration count + termination test (ap_check) and next block choice
+  // (ap_select) from the complete partials, in a fixed order.
+  CgCtl* ctl;
+  const double* scales;
+  double tol;
+  int* sel_out;
+  int nblocks;
+  unsigned* ticket;
 };
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s);
 
@@ -193,6 +204,10 @@ void ap_gather_launch(const double* R, int n, int m, int block, const int* sel, 
 // V[blk] += upd; optional FP32 copy of upd for the SIMT operator kernel
 void ap_apply_update_launch(const double* upd, int n, int m, int block, const int* sel, double* V, float* upd32,
                             int ldv32, const int* skip, cudaStream_t s);
+// Fused block step: upd = Hinv[sel] R_blk (FP64), V[blk] += upd, upd64 for the
+// diagonal term, and upd's TF32 hi/lo operator images (tcgen05 layout) in vpk.
+void ap_update_pack_launch(const double* R, int n, int m, int block, const int* sel, const double* inv_blocks,
+                           double* V, double* upd64, float* vpk, int npad, const int* skip, cudaStream_t s);
 void ap_block_update_launch(const double* inv_blocks, int block, int n, const int* sel,
                             const double* R, int m, double* V, double* upd64, float* upd32,
                             int ldv32, const int* skip, cudaStream_t s);

@@ -384,6 +384,52 @@ __global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
     for (int w = 0; w < NW; ++w) t += sred[w];
     a.spart[g] = t;
   }
+  if (!a.ctl) return;
+  // ---- fused AP epilogue in the last block (ticket) ----
+  __shared__ unsigned last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double ss[96];
+  const int G = gridDim.x;
+  for (int j = warp; j < a.m; j += NW) {  // sum_g dpart[g][j], fixed xor tree per warp
+    double acc = 0.0;
+    for (int q = lane; q < G; q += 32) acc += __ldcg(a.dpart + static_cast<size_t>(q) * a.m + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ss[j] = acc;
+  }
+  __shared__ double bscore[1024];
+  for (int k = threadIdx.x; k < a.nblocks; k += blockDim.x) {
+    double t = 0.0;
+    for (int q = 0; q < a.gpb; ++q) t += __ldcg(a.spart + static_cast<size_t>(k) * a.gpb + q);
+    if (k < 1024) bscore[k] = sqrt(t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    CgCtl* c = a.ctl;
+    c->iters += 1;  // ap_check (solvers.cpp:119-141)
+    const double mean = sqrt(ss[0]) / a.scales[0];
+    double sum = 0.0;
+    for (int j = 1; j < a.m; ++j) sum += sqrt(ss[j]) / a.scales[j];
+    const double probe = a.m > 1 ? sum / (a.m - 1) : 0.0;
+    c->mean_norm = mean;
+    c->probe_norm = probe;
+    c->done = (mean <= a.tol && probe <= a.tol) ? 1 : 0;
+    c->stop = (c->done || c->iters >= c->budget) ? 1 : 0;
+    int best_k = 0;  // ap_select: strict '>' from -1 (solvers.cpp:125-132)
+    double best = -1.0;
+    for (int k = 0; k < a.nblocks; ++k)
+      if (bscore[k] > best) {
+        best = bscore[k];
+        best_k = k;
+      }
+    *a.sel_out = best_k;
+    *a.ticket = 0u;
+  }
 }
 
 }  // namespace
@@ -457,6 +503,7 @@ void kv_slab_launch(const KvArgs& a, int /*dmax*/, cudaStream_t s) {
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s) {
   if (a.dpart) {
     if (a.m > 96) throw std::invalid_argument("gpk: fused reductions support m <= 96");
+    if (a.ctl && a.nblocks > 1024) throw std::invalid_argument("gpk: fused AP epilogue supports <= 1024 blocks");
     kv_reduce_dot_kernel<<<a.groups, 256, 0, s>>>(a);
     check_launch("kv_reduce_dot_kernel");
     return;

@@ -710,6 +710,60 @@ void ap_apply_update_launch(const double* upd, int n, int m, int block, const in
   check_launch("ap_apply_update");
 }
 
+// One warp per update row i (8 rows per CTA); lane owns columns lane + 32 q.
+__global__ void ap_update_pack_kernel(const double* R, int n, int m, int block, const int* sel,
+                                      const double* inv_blocks, double* V, double* upd64, float* vpk, int npad,
+                                      int rows_pad, const int* skip) {
+  SKIP_IF(skip);
+  const int k = *sel;
+  const int r0 = k * block, len = min(block, n - r0);
+  const double* Hi = inv_blocks + static_cast<size_t>(k) * block * block;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + warp;
+  if (i >= rows_pad) return;  // rows in [len, rows_pad) pack as zeros
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (i < len) {
+    const double* hrow = Hi + static_cast<size_t>(i) * block;  // Hinv symmetric: row i == column i
+    const double* rb = R + static_cast<size_t>(r0) * m;
+#pragma unroll 4
+    for (int c = 0; c < len; ++c) {
+      const double h = hrow[c];
+      const double* rr = rb + static_cast<size_t>(c) * m;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (lane + 32 * q < m) acc[q] = fma(h, rr[lane + 32 * q], acc[q]);
+    }
+  }
+  const int img = npad * 32;
+  const int chunk = i / 32, kk = i % 32;
+  float* base = vpk + static_cast<size_t>(chunk) * 2 * img;
+  for (int j = lane; j < npad; j += 32) {
+    const int q = j / 32;
+    double x = 0.0;
+    if (i < len && j < m) {
+      x = acc[q];
+      upd64[static_cast<size_t>(i) * m + j] = x;
+      V[static_cast<size_t>(r0 + i) * m + j] += x;  // solutions[blk] += update (solvers.cpp:136)
+    }
+    uint32_t hb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(static_cast<float>(x)));
+    const float h = __uint_as_float(hb);
+    uint32_t lb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(static_cast<float>(x - static_cast<double>(h))));
+    const int off = ((j / 8) * 8 + kk / 4) * 32 + (j % 8) * 4 + (kk % 4);
+    base[off] = h;
+    base[img + off] = __uint_as_float(lb);
+  }
+}
+void ap_update_pack_launch(const double* R, int n, int m, int block, const int* sel, const double* inv_blocks,
+                           double* V, double* upd64, float* vpk, int npad, const int* skip, cudaStream_t s) {
+  if (m > 96) throw std::invalid_argument("gpk: AP supports at most 96 right-hand sides");
+  const int rows = (block + 31) / 32 * 32;  // whole 32-row chunks (zero rows beyond the block)
+  ap_update_pack_kernel<<<(rows + 7) / 8, 256, 0, s>>>(R, n, m, block, sel, inv_blocks, V, upd64, vpk, npad, rows,
+                                                       skip);
+  check_launch("ap_update_pack");
+}
+
 // iteration++ ; termination from sum of squares partials.
 __global__ void ap_check_kernel(const double* part, int groups, int m, const double* scales, double tol, CgCtl* ctl) {
   if (ctl->stop) return;
