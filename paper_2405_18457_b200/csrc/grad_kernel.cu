@@ -64,7 +64,7 @@ __device__ __forceinline__ void tile_coords(long long L, int T, int symmetric, i
 }
 
 template <int DP4, int NP>
-__global__ void __launch_bounds__(NT, 1) grad_kernel(const GradArgs a) {
+__global__ void __launch_bounds__(NT, 2) grad_kernel(const GradArgs a) {
   constexpr int DP = 4 * DP4;
   constexpr int DMAX = DP;
   __shared__ __align__(16) float Gs[NP][TB * GS];
