@@ -307,6 +307,10 @@ struct KvCall {
   int* sel_out = nullptr;
   int nblocks = 0;
   unsigned* ticket = nullptr;
+  double** ap_ptrs = nullptr;
+  double* ap_inv = nullptr;
+  long long ap_bb = 0;
+  double* ap_upd = nullptr;
 };
 
 void run_kv(gpk_operator* op, const KvCall& c) {
@@ -402,6 +406,10 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.sel_out = c.sel_out;
   r.nblocks = c.nblocks;
   r.ticket = c.ticket;
+  r.ap_ptrs = c.ap_ptrs;
+  r.ap_inv = c.ap_inv;
+  r.ap_bb = c.ap_bb;
+  r.ap_upd = c.ap_upd;
   kv_reduce_launch(r, s);
 }
 
@@ -461,6 +469,9 @@ void apply_dev64(gpk_operator* op, const double* v64, int m, double* out, const 
 
 // RHS groups of at most 65 columns (the kernel's widest tile).
 constexpr int kMaxRhs = 65;
+// Zero rows after the residual block: AP's batched GEMM reads a whole block of
+// rows in place, which may run past row n for the last (partial) block.
+constexpr int kResidPad = 1024;
 
 // -------------------------------------------------------------- precond
 void build_precond(gpk_precond* pc) {
@@ -856,6 +867,8 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   }
   unsigned* ticket = b->ticket.p;
   float* vpk_blk = tc ? b->apk.ensure(kv_tc_pack_floats(m, block)) : nullptr;
+  // the GEMM reads R_blk in place when the zero padding covers the last block
+  const bool in_place = tc && (static_cast<long long>(nblocks) * block - n) <= kResidPad;
 
   // refresh_residuals (solvers.cpp:98) with the fused norms and block scores
   float* v32 = b->f32.ensure(static_cast<size_t>(std::max(block, n)) * kv_ld_for(m));
@@ -885,15 +898,29 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     kc.sel_out = sel;
     kc.nblocks = nblocks;
     kc.ticket = ticket;
+    if (in_place) {
+      kc.ap_ptrs = ptrs;
+      kc.ap_inv = inv;
+      kc.ap_bb = static_cast<long long>(bb);
+      kc.ap_upd = upd64;
+    }
     run_kv(op, kc);
   }
 
   if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
   auto iteration = [&]() {  // solvers.cpp:120-140
     if (tc) {
-      // fused: block update + V update + TF32 images; slab; reduce + test + next block
-      ap_update_pack_launch(b->residuals.p, n, m, block, sel, inv, b->solutions.p, upd64, vpk_blk, kv_tc_npad(m), stop,
-                            s);
+      // upd = R_blk^T Hinv (batched GEMM, pointers written by the previous reduce
+      // or by the gather) -> V += upd and TF32 images -> slab -> fused reduce
+      // (norms, termination test, next block, next GEMM pointers)
+      if (!in_place) ap_gather_launch(b->residuals.p, n, m, block, sel, Rs, inv, upd64, ptrs, stop, s);
+      const double one = 1.0, zero = 0.0;
+      if (cublasDgemmBatched(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, m, block, block, &one,
+                             const_cast<const double* const*>(ptrs), m, const_cast<const double* const*>(ptrs + 1),
+                             block, &zero, ptrs + 2, m, 1) != CUBLAS_STATUS_SUCCESS)
+        throw CudaError("cublasDgemmBatched");
+      count_launch();
+      ap_apply_pack_launch(upd64, n, m, block, sel, b->solutions.p, vpk_blk, kv_tc_npad(m), stop, s);
       KvCall kc;
       kc.vpk = vpk_blk;
       kc.m = m;
@@ -920,6 +947,12 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
       kc.sel_out = sel;
       kc.nblocks = nblocks;
       kc.ticket = ticket;
+      if (in_place) {
+        kc.ap_ptrs = ptrs;
+        kc.ap_inv = inv;
+        kc.ap_bb = static_cast<long long>(bb);
+        kc.ap_upd = upd64;
+      }
       run_kv(op, kc);
       return;
     }
@@ -1646,10 +1679,11 @@ gpk_status gpk_batch_create(gpk_operator* op, const double* targets, int m, gpk_
     const size_t nm = static_cast<size_t>(op->n) * m;
     b->targets.ensure(nm);
     b->solutions.ensure(nm);
-    b->residuals.ensure(nm);
+    b->residuals.ensure(nm + static_cast<size_t>(kResidPad) * m);
     upload_colmajor(op, targets, op->n, m, b->targets.p);
     GPK_CUDA(cudaMemsetAsync(b->solutions.p, 0, sizeof(double) * nm, op->ctx->stream));
-    GPK_CUDA(cudaMemsetAsync(b->residuals.p, 0, sizeof(double) * nm, op->ctx->stream));
+    GPK_CUDA(cudaMemsetAsync(b->residuals.p, 0, sizeof(double) * (nm + static_cast<size_t>(kResidPad) * m),
+                             op->ctx->stream));
     b->scales.resize(m);
     for (int j = 0; j < m; ++j) {  // linear_system.cpp:21
       double acc = 0.0;
@@ -1912,7 +1946,8 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
   const size_t nm = static_cast<size_t>(nloc) * o->m;
   b->targets.ensure(nm);
   b->solutions.ensure(nm);
-  b->residuals.ensure(nm);
+  b->residuals.ensure(nm + static_cast<size_t>(kResidPad) * o->m);
+  GPK_CUDA(cudaMemsetAsync(b->residuals.p, 0, sizeof(double) * (nm + static_cast<size_t>(kResidPad) * o->m), stream));
   b->scales.resize(o->m);
   b->scales_dev.ensure(o->m);
   o->prev.ensure(nm);

@@ -112,6 +112,11 @@ struct KvReduceArgs {
   int* sel_out;
   int nblocks;
   unsigned* ticket;
+  // and the next block update's batched-GEMM pointers: {R + sel*b*m, Hinv[sel], upd}
+  double** ap_ptrs;
+  double* ap_inv;
+  long long ap_bb;
+  double* ap_upd;
 };
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s);
 
@@ -208,6 +213,9 @@ void ap_apply_update_launch(const double* upd, int n, int m, int block, const in
 // diagonal term, and upd's TF32 hi/lo operator images (tcgen05 layout) in vpk.
 void ap_update_pack_launch(const double* R, int n, int m, int block, const int* sel, const double* inv_blocks,
                            double* V, double* upd64, float* vpk, int npad, const int* skip, cudaStream_t s);
+// V[blk] += upd (upd from the batched GEMM) and upd's TF32 images.
+void ap_apply_pack_launch(const double* upd64, int n, int m, int block, const int* sel, double* V, float* vpk,
+                          int npad, const int* skip, cudaStream_t s);
 void ap_block_update_launch(const double* inv_blocks, int block, int n, const int* sel,
                             const double* R, int m, double* V, double* upd64, float* upd32,
                             int ldv32, const int* skip, cudaStream_t s);

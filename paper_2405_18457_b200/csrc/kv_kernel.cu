@@ -428,6 +428,11 @@ __global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
         best_k = k;
       }
     *a.sel_out = best_k;
+    if (a.ap_ptrs) {
+      a.ap_ptrs[0] = a.out + static_cast<size_t>(best_k) * a.score_block * a.m;  // R rows of the block (padded)
+      a.ap_ptrs[1] = a.ap_inv + static_cast<size_t>(best_k) * a.ap_bb;
+      a.ap_ptrs[2] = a.ap_upd;
+    }
     *a.ticket = 0u;
   }
 }

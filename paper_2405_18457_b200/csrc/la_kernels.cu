@@ -764,6 +764,40 @@ void ap_update_pack_launch(const double* R, int n, int m, int block, const int* 
   check_launch("ap_update_pack");
 }
 
+__global__ void ap_apply_pack_kernel(const double* upd64, int n, int m, int block, const int* sel, double* V,
+                                     float* vpk, int npad, int rows_pad, const int* skip) {
+  SKIP_IF(skip);
+  const int k = *sel;
+  const int r0 = k * block, len = min(block, n - r0);
+  const int img = npad * 32;
+  const long long total = static_cast<long long>(rows_pad) * npad;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / npad), j = static_cast<int>(e % npad);
+    double x = 0.0;
+    if (i < len && j < m) {
+      x = upd64[static_cast<size_t>(i) * m + j];
+      V[static_cast<size_t>(r0 + i) * m + j] += x;  // solutions[blk] += update (solvers.cpp:136)
+    }
+    uint32_t hb, lb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(static_cast<float>(x)));
+    const float h = __uint_as_float(hb);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(static_cast<float>(x - static_cast<double>(h))));
+    const int kk = i % 32;
+    float* base = vpk + static_cast<size_t>(i / 32) * 2 * img;
+    const int off = ((j / 8) * 8 + kk / 4) * 32 + (j % 8) * 4 + (kk % 4);
+    base[off] = h;
+    base[img + off] = __uint_as_float(lb);
+  }
+}
+void ap_apply_pack_launch(const double* upd64, int n, int m, int block, const int* sel, double* V, float* vpk,
+                          int npad, const int* skip, cudaStream_t s) {
+  const int rows = (block + 31) / 32 * 32;
+  ap_apply_pack_kernel<<<blocks_for(static_cast<long long>(rows) * npad, 256), 256, 0, s>>>(upd64, n, m, block, sel,
+                                                                                          V, vpk, npad, rows, skip);
+  check_launch("ap_apply_pack");
+}
+
 // iteration++ ; termination from sum of squares partials.
 __global__ void ap_check_kernel(const double* part, int groups, int m, const double* scales, double tol, CgCtl* ctl) {
   if (ctl->stop) return;
