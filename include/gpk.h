@@ -215,6 +215,23 @@ gpk_status gpk_rff_basis_get(const gpk_rff_basis* b, double* base_frequencies, d
 gpk_status gpk_pathwise_targets(gpk_operator* op, gpk_rff_basis* basis, int s, uint64_t seed,
                                 uint64_t substream, double* prior, double* noise, double* xi);
 
+/* ---- posterior predictions (posterior.hpp:14-51) ---------------------- */
+/* k(P, X) V for query points P (p x d, column-major), V n x m: cross_kernel_apply
+ * (kernel.hpp:24-26, kernel.cpp:72-81); no noise term. out: p x m. */
+gpk_status gpk_cross_apply(gpk_operator* op, const double* points, int p, const double* v, int m, double* out);
+/* posterior mean k(P, X) v_y (posterior.cpp:11-17). out: p. */
+gpk_status gpk_predict_mean(gpk_operator* op, const double* points, int p, const double* v_y, double* out);
+/* pathwise posterior samples f_j(P) + k(P, X)(v_y - zhat_j), j < s, with f_j the
+ * RFF prior draws of `basis` (posterior.cpp:19-27; basis NULL = zero prior).
+ * zhat: n x s; out: p x s. */
+gpk_status gpk_sample_posterior(gpk_operator* op, gpk_rff_basis* basis, const double* points, int p,
+                                const double* v_y, const double* zhat, int s, double* out);
+/* test_metrics (posterior.cpp:29-59): out4 = {rmse, llh, rmse_raw, llh_raw};
+ * llh entries are NaN unless s >= 2 and a basis is given. */
+gpk_status gpk_test_metrics(gpk_operator* op, gpk_rff_basis* basis, const double* points, int p,
+                            const double* targets, const double* v_y, const double* zhat, int s, double target_scale,
+                            double* out4);
+
 /* ---- outer loop (outer_loop.hpp:37-90, optimise) ----------------------- */
 typedef struct {
   int estimator;          /* 0 standard, 1 pathwise */

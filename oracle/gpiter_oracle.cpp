@@ -949,6 +949,106 @@ PathwiseTargets pathwise_targets(const RffBasis& basis, const Hyper& hp, const D
   return t;
 }
 
+// ===================== posterior =========================================
+// kernel.cpp:57-81: ps = P diag(1/l), xs = X diag(1/l); row i of k(P, X) from
+// the squared distances; products accumulate in ascending training index.
+Mat cross_kernel_apply(const Mat& points, const Mat& inputs, const Hyper& hp, const Mat& v, int block_rows,
+                       int threads) {
+  const int p = points.rows, n = inputs.rows, d = inputs.cols, m = v.cols;
+  if (points.cols != d) throw std::invalid_argument("predict_mean: point dimension mismatch");
+  const Vec ls = hp.lengthscales();
+  Vec inv(d);
+  for (int k = 0; k < d; ++k) inv[k] = 1.0 / ls[k];
+  const double s2 = hp.signal_scale() * hp.signal_scale();
+  std::vector<double> xs(static_cast<size_t>(n) * d), ps(static_cast<size_t>(p) * d);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < d; ++k) xs[static_cast<size_t>(i) * d + k] = inputs(i, k) * inv[k];
+  for (int i = 0; i < p; ++i)
+    for (int k = 0; k < d; ++k) ps[static_cast<size_t>(i) * d + k] = points(i, k) * inv[k];
+  Mat out(p, m);
+  (void)block_rows;  // per-row results do not depend on the tile height
+  parallel_for(threads, p, [&](int, int i) {
+    std::vector<double> row(n);
+    const double* pi = &ps[static_cast<size_t>(i) * d];
+    for (int c = 0; c < n; ++c) {
+      const double* xc = &xs[static_cast<size_t>(c) * d];
+      double r2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double t = xc[k] - pi[k];
+        r2 += t * t;
+      }
+      row[c] = matern_profile(r2, s2);
+    }
+    for (int j = 0; j < m; ++j) {
+      double acc = 0.0;
+      for (int c = 0; c < n; ++c) acc += row[c] * v(c, j);
+      out(i, j) = acc;
+    }
+  });
+  return out;
+}
+
+Mat evaluate_prior_all(const RffBasis& basis, const Hyper& hp, const Mat& points, int s) {  // rff.cpp:56-62
+  const Mat feat = rff_features(basis, hp, points);
+  const int F = feat.cols;
+  Mat out(points.rows, s);
+  for (int j = 0; j < s; ++j)
+    for (int i = 0; i < points.rows; ++i) {
+      double acc = 0.0;
+      for (int q = 0; q < F; ++q) acc += feat(i, q) * basis.weights(q, j);
+      out(i, j) = acc;
+    }
+  return out;
+}
+
+Mat sample_posterior_all(const Mat& prior, const Mat& points, const Mat& inputs, const Hyper& hp, const Vec& v_y,
+                         const Mat& zhat, int threads) {  // posterior.cpp:19-27
+  const int n = inputs.rows, s = zhat.cols;
+  Mat corr(n, s);
+  for (int j = 0; j < s; ++j)
+    for (int i = 0; i < n; ++i) corr(i, j) = v_y[i] - zhat(i, j);
+  Mat out = cross_kernel_apply(points, inputs, hp, corr, 1024, threads);
+  if (prior.size())
+    for (size_t e = 0; e < out.size(); ++e) out.a[e] = prior.a[e] + out.a[e];
+  return out;
+}
+
+TestMetrics test_metrics(const Mat& prior, const Mat& points, const Vec& targets, const Mat& inputs, const Hyper& hp,
+                         const Vec& v_y, const Mat& zhat, double target_scale, int threads) {  // posterior.cpp:29-59
+  const int p = points.rows, n = inputs.rows;
+  Mat vy(n, 1);
+  vy.a = v_y;
+  const Mat mean = cross_kernel_apply(points, inputs, hp, vy, 1024, threads);
+  TestMetrics mt;
+  double se = 0.0;
+  Vec err(p);
+  for (int i = 0; i < p; ++i) {
+    err[i] = targets[i] - mean.a[i];
+    se += err[i] * err[i];
+  }
+  mt.rmse = std::sqrt(se / p);
+  mt.rmse_raw = mt.rmse * target_scale;
+  const int s = zhat.cols;
+  if (s >= 2 && prior.size()) {
+    const Mat samples = sample_posterior_all(prior, points, inputs, hp, v_y, zhat, threads);
+    const double noise_var = hp.noise_variance();
+    double llh = 0.0;
+    for (int i = 0; i < p; ++i) {
+      double mu = 0.0;
+      for (int j = 0; j < s; ++j) mu += samples(i, j);
+      mu /= s;
+      double var = 0.0;
+      for (int j = 0; j < s; ++j) var += (samples(i, j) - mu) * (samples(i, j) - mu);
+      var = var / (s - 1) + noise_var;
+      llh += -0.5 * std::log(2.0 * kPi * var) - 0.5 * err[i] * err[i] / var;
+    }
+    mt.llh = llh / p;
+    mt.llh_raw = mt.llh - std::log(target_scale);
+    mt.has_llh = true;
+  }
+  return mt;
+}
+
 // ===================== outer_loop.cpp:39-246 ===============================
 namespace {
 struct Adam {

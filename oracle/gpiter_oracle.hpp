@@ -229,6 +229,19 @@ struct PathwiseTargets { Mat prior_values, noise, xi; };
 PathwiseTargets pathwise_targets(const RffBasis& basis, const Hyper& hp, const Dataset& data,
                                  int s, uint64_t seed, uint64_t substream);
 
+// ---- posterior (kernel.cpp:57-81, rff.cpp:56-62, posterior.cpp:11-59) ----
+// k(P, X) V for m columns, row tiles of block_rows (cross_kernel_apply).
+Mat cross_kernel_apply(const Mat& points, const Mat& inputs, const Hyper& hp, const Mat& v, int block_rows = 1024,
+                       int threads = 1);
+// prior sample j at points: rff_features(points) W[:, j] (evaluate_prior), all j < s.
+Mat evaluate_prior_all(const RffBasis& basis, const Hyper& hp, const Mat& points, int s);
+// f_j(P) + k(P, X)(v_y - zhat_j) for every j < s (sample_posterior); prior may be empty (zero prior).
+Mat sample_posterior_all(const Mat& prior, const Mat& points, const Mat& inputs, const Hyper& hp, const Vec& v_y,
+                         const Mat& zhat, int threads = 1);
+struct TestMetrics { double rmse = 0, llh = 0, rmse_raw = 0, llh_raw = 0; bool has_llh = false; };
+TestMetrics test_metrics(const Mat& prior, const Mat& points, const Vec& targets, const Mat& inputs, const Hyper& hp,
+                         const Vec& v_y, const Mat& zhat, double target_scale, int threads = 1);
+
 // ---- outer loop (outer_loop.cpp:39-246) ----------------------------------
 struct OuterConfig {
   int estimator = 1;  // 0 standard, 1 pathwise

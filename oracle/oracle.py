@@ -357,3 +357,35 @@ def sinsum_dataset(n, d, uniform=False, noise=0.1, seed=0):
     lib().oracle_sinsum_dataset(n, d, int(uniform), C.c_double(noise), C.c_ulonglong(seed),
                                 x.ctypes.data_as(C.POINTER(C.c_float)), y.ctypes.data_as(C.POINTER(C.c_float)))
     return x, y
+
+
+# ---- posterior (posterior.cpp) ---------------------------------------------
+def cross_apply(points, X, raw, V, threads=1):
+    P, X, raw, V = _f(points), _f(X), _f(raw), _f(V)
+    if V.ndim == 1:
+        V = V[:, None]
+    out = np.empty((P.shape[0], V.shape[1]), order="F")
+    _check(lib().oracle_cross_apply(_p(P), P.shape[0], _p(X), X.shape[0], X.shape[1], _p(raw), _p(V), V.shape[1],
+                                    _p(out), threads))
+    return out
+
+
+def prior_at(d, pairs, samples, seed, raw, points, s, substream=0):
+    raw, P = _f(raw), _f(points)
+    out = np.empty((P.shape[0], s), order="F")
+    _check(lib().oracle_prior_at(d, pairs, samples, C.c_ulonglong(seed), C.c_ulonglong(substream), _p(raw), _p(P),
+                                 P.shape[0], s, _p(out)))
+    return out
+
+
+def posterior(points, X, raw, v_y, zhat, prior=None, test_targets=None, target_scale=1.0, threads=1):
+    P, X, raw, vy, Z = _f(points), _f(X), _f(raw), _f(v_y), _f(zhat)
+    pr = _f(prior) if prior is not None else None
+    tt = _f(test_targets) if test_targets is not None else None
+    p, s = P.shape[0], Z.shape[1]
+    samples = np.empty((p, s), order="F")
+    metrics = np.zeros(5)
+    _check(lib().oracle_posterior(_p(P), p, _p(X), X.shape[0], X.shape[1], _p(raw), _p(vy), _p(Z), s, _p(pr), _p(tt),
+                                  C.c_double(target_scale), _p(samples), _p(metrics), threads))
+    return {"samples": samples, "rmse": metrics[0], "llh": metrics[1] if metrics[4] else None,
+            "rmse_raw": metrics[2], "llh_raw": metrics[3] if metrics[4] else None}

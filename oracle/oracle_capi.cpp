@@ -397,6 +397,47 @@ int oracle_exact(const double* x, const double* y, int n, int d, const double* r
   });
 }
 
+// k(P, X) V (p x m), P p x d, X n x d, V n x m.
+int oracle_cross_apply(const double* points, int p, const double* x, int n, int d, const double* raw, const double* v,
+                       int m, double* out, int threads) {
+  return guarded([&] {
+    put(cross_kernel_apply(make_mat(points, p, d), make_mat(x, n, d), make_hp(raw, d), make_mat(v, n, m), 1024, threads),
+        out);
+  });
+}
+
+// RFF prior at points (p x s) for basis (d, pairs, samples, seed, substream).
+int oracle_prior_at(int d, int pairs, int samples, unsigned long long seed, unsigned long long substream,
+                    const double* raw, const double* points, int p, int s, double* out) {
+  return guarded([&] {
+    const RffBasis b = build_rff_basis(d, pairs, samples, seed, substream);
+    put(evaluate_prior_all(b, make_hp(raw, d), make_mat(points, p, d), s), out);
+  });
+}
+
+// samples (p x s) and metrics {rmse, llh, rmse_raw, llh_raw, has_llh}; prior p x s (nullable = zero prior).
+int oracle_posterior(const double* points, int p, const double* x, int n, int d, const double* raw, const double* v_y,
+                     const double* zhat, int s, const double* prior, const double* test_targets, double target_scale,
+                     double* samples, double* metrics, int threads) {
+  return guarded([&] {
+    const Mat P = make_mat(points, p, d), X = make_mat(x, n, d);
+    const Hyper hp = make_hp(raw, d);
+    const Vec vy(v_y, v_y + n);
+    const Mat Z = make_mat(zhat, n, s);
+    const Mat pr = prior ? make_mat(prior, p, s) : Mat();
+    if (samples) put(sample_posterior_all(pr, P, X, hp, vy, Z, threads), samples);
+    if (metrics && test_targets) {
+      const TestMetrics mt = test_metrics(pr, P, Vec(test_targets, test_targets + p), X, hp, vy, Z, target_scale,
+                                          threads);
+      metrics[0] = mt.rmse;
+      metrics[1] = mt.llh;
+      metrics[2] = mt.rmse_raw;
+      metrics[3] = mt.llh_raw;
+      metrics[4] = mt.has_llh;
+    }
+  });
+}
+
 void oracle_sinsum_dataset(int n, int d, int uniform, double noise, unsigned long long seed, float* x_rowmajor,
                            float* y) {
   std::vector<float> xv, yv;

@@ -7,3 +7,4 @@ from .gpiter import (  # noqa: F401
     PivotedCholeskyPreconditioner, RffBasis, SolverConfig, SolverReport, build_rff_basis, estimate_gradient_pathwise,
     estimate_gradient_standard, optimise, pathwise_targets, sgd_batches, sinsum_dataset, solve, solve_ap, solve_cg, solve_sgd,
     termination_check)
+from .gpiter import cross_kernel_apply, predict_mean, sample_posterior, test_metrics  # noqa: F401

@@ -108,6 +108,10 @@ def _sig(lib):
         "gpk_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
         "gpk_ctx_init_comm": (C.c_int, [H, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
         "gpk_shard_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, ip, ip]),
+        "gpk_cross_apply": (C.c_int, [H, dp, C.c_int, dp, C.c_int, dp]),
+        "gpk_predict_mean": (C.c_int, [H, dp, C.c_int, dp, dp]),
+        "gpk_sample_posterior": (C.c_int, [H, H, dp, C.c_int, dp, dp, C.c_int, dp]),
+        "gpk_test_metrics": (C.c_int, [H, H, dp, C.c_int, dp, dp, dp, C.c_int, C.c_double, dp]),
         "gpk_sinsum_dataset": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                          C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     }

@@ -114,6 +114,8 @@ struct gpk_operator {
   double s = 1, s2 = 1, sigma = 1, sigma2 = 1;
   DBuf<double> part;      // kv split partials
   DBuf<float> vpk;        // packed TF32 hi/lo RHS images (tcgen05 path)
+  DBuf<double> pts64, pts64s;  // posterior query points FP64 [p][d] (raw, scaled)
+  DBuf<float> pts32;           // and scaled FP32 [p + 32][dp]
   // scratch for host-facing calls
   DBuf<float> v32;
   DBuf<double> v64, out64, tmp64;
@@ -311,6 +313,7 @@ struct KvCall {
   double* ap_inv = nullptr;
   long long ap_bb = 0;
   double* ap_upd = nullptr;
+  const float* xs_rows = nullptr;  // cross kernel: rows from these scaled points, no noise diagonal
 };
 
 void run_kv(gpk_operator* op, const KvCall& c) {
@@ -344,6 +347,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.skip = c.skip;
   a.stats = op->ctx->stats;
   a.d = op->d;
+  a.xs_rows = c.xs_rows;
   gpk_ctx* ctx = op->ctx;
   if (c.vpk && !tc) throw InvalidArgument("gpk: pre-packed operator input needs the tcgen05 kernel");
   const float* vpk = c.vpk;
@@ -410,6 +414,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.ap_inv = c.ap_inv;
   r.ap_bb = c.ap_bb;
   r.ap_upd = c.ap_upd;
+  r.nodiag = c.xs_rows != nullptr;
   kv_reduce_launch(r, s);
 }
 
@@ -1278,6 +1283,85 @@ void rff_prior_dev(gpk_operator* op, gpk_rff_basis* b, int s_count, double* prio
   GPK_CUDA(cudaStreamSynchronize(s));
 }
 
+// ------------------------------------------------------------- posterior
+// Query points (host column-major p x d) -> pts64 [p][d] raw, pts32 [p+32][dp]
+// scaled by the operator's current lengthscales (kernel.cpp:59-61).
+void upload_points(gpk_operator* op, const double* points, int p) {
+  cudaStream_t s = op->ctx->stream;
+  const int d = op->d, dp = op->dp;
+  double* p64 = op->pts64.ensure(static_cast<size_t>(p) * d);
+  upload_colmajor(op, points, p, d, p64);
+  float* p32 = op->pts32.ensure(static_cast<size_t>(p + 32) * dp);
+  GPK_CUDA(cudaMemsetAsync(p32, 0, sizeof(float) * (p + 32) * dp, s));
+  prescale_launch(p64, p, d, dp, op->inv_ls_dev.p, p32, op->pts64s.ensure(static_cast<size_t>(p) * d), s);
+}
+
+// out [p][m] = k(P, X) v, v device FP64 [n][m] (cross_kernel_apply, kernel.cpp:72-81; no noise term)
+void cross_apply_dev(gpk_operator* op, int p, const double* v64, int m, double* out) {
+  KvCall c;
+  c.xs_rows = op->pts32.p;
+  c.m = m;
+  c.R = p;
+  c.C = op->n;
+  c.vdiag = v64;  // packing source for the tensor-core kernel
+  if (op->ctx->kernel != 1) {
+    float* v32 = op->v32.ensure(static_cast<size_t>(op->n) * kv_ld_for(m));
+    to_f32_launch(v64, op->n, m, m, v32, kv_ld_for(m), nullptr, op->ctx->stream);
+    c.v = v32;
+  }
+  c.out = out;
+  c.ldo = m;
+  run_kv(op, c);
+}
+
+// Prior samples f_j(P), j < s, from the RFF basis at the query points (rff.cpp:56-62).
+void prior_at_points(gpk_operator* op, gpk_rff_basis* b, int p, int s_count, double* prior) {
+  cudaStream_t s = op->ctx->stream;
+  const int P = b->pairs, d = op->d;
+  std::vector<double> f(static_cast<size_t>(P) * d);
+  for (int q = 0; q < P; ++q)
+    for (int k = 0; k < d; ++k) f[static_cast<size_t>(q) * d + k] = b->freq[static_cast<size_t>(k) * P + q] * op->inv_ls[k];
+  double* fd = b->freq_dev.ensure(f.size());
+  GPK_CUDA(cudaMemcpyAsync(fd, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice, s));
+  if (!b->w_dev.p) {
+    b->w_dev.ensure(b->weights.size());
+    GPK_CUDA(cudaMemcpyAsync(b->w_dev.p, b->weights.data(), sizeof(double) * b->weights.size(),
+                             cudaMemcpyHostToDevice, s));
+  }
+  const double amplitude = op->s / std::sqrt(static_cast<double>(P));
+  rff_prior_launch(op->pts64.p, p, d, fd, P, b->w_dev.p, 2 * P, s_count, amplitude, prior, s);
+  GPK_CUDA(cudaStreamSynchronize(s));
+}
+
+__global__ void posterior_corr_kernel(const double* vy, const double* zhat, int n, int s, double* corr) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(n) * s;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    corr[e] = vy[e / s] - zhat[e];  // v_y - zhat_j (posterior.cpp:24)
+}
+
+// samples [p][s] = f_j(P) + k(P, X)(v_y - zhat_j) for all j (posterior.cpp:19-27); basis null: zero prior.
+void sample_posterior_dev(gpk_operator* op, gpk_rff_basis* basis, int p, const double* vy_host, const double* zhat_host,
+                          int s, double* samples_dev) {
+  cudaStream_t st = op->ctx->stream;
+  const int n = op->n;
+  DBuf<double> vy, z, corr, prior;
+  vy.ensure(n);
+  z.ensure(static_cast<size_t>(n) * s);
+  corr.ensure(static_cast<size_t>(n) * s);
+  GPK_CUDA(cudaMemcpyAsync(vy.p, vy_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  upload_colmajor(op, zhat_host, n, s, z.p);
+  posterior_corr_kernel<<<std::max(1, std::min(148 * 16, static_cast<int>((static_cast<long long>(n) * s + 255) / 256))),
+                          256, 0, st>>>(vy.p, z.p, n, s, corr.p);
+  check_launch("posterior_corr");
+  cross_apply_dev(op, p, corr.p, s, samples_dev);
+  if (basis) {
+    prior.ensure(static_cast<size_t>(p) * s);
+    prior_at_points(op, basis, p, s, prior.p);
+    xi_assemble_launch(samples_dev, prior.p, p, s, 1.0, samples_dev, s, 0, nullptr, st);  // samples += prior
+  }
+  GPK_CUDA(cudaStreamSynchronize(st));
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -2130,6 +2214,84 @@ gpk_status gpk_optimise(gpk_ctx* ctx, const double* inputs, const double* target
     }
     std::memcpy(final_raw, o.raw.data(), sizeof(double) * o.P);
     *aborted = o.aborted;
+  });
+}
+
+gpk_status gpk_cross_apply(gpk_operator* op, const double* points, int p, const double* v, int m, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(p >= 1 && m >= 1 && m <= kMaxRhs, "cross_kernel_apply: 1 <= m <= 65 and p >= 1");
+    const int n = op->n;
+    upload_points(op, points, p);
+    DBuf<double> v64, o64;
+    v64.ensure(static_cast<size_t>(n) * m);
+    o64.ensure(static_cast<size_t>(p) * m);
+    upload_colmajor(op, v, n, m, v64.p);
+    cross_apply_dev(op, p, v64.p, m, o64.p);
+    download_colmajor(op, o64.p, p, m, out);
+  });
+}
+
+gpk_status gpk_predict_mean(gpk_operator* op, const double* points, int p, const double* v_y, double* out) {
+  return gpk_cross_apply(op, points, p, v_y, 1, out);
+}
+
+gpk_status gpk_sample_posterior(gpk_operator* op, gpk_rff_basis* basis, const double* points, int p,
+                                const double* v_y, const double* zhat, int s, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(p >= 1 && s >= 1 && s <= kMaxRhs, "sample_posterior: 1 <= s <= 65 and p >= 1");
+    if (basis && (basis->d != op->d || s > basis->samples))
+      throw InvalidArgument("sample_posterior: basis does not match the samples");
+    upload_points(op, points, p);
+    DBuf<double> smp;
+    smp.ensure(static_cast<size_t>(p) * s);
+    sample_posterior_dev(op, basis, p, v_y, zhat, s, smp.p);
+    download_colmajor(op, smp.p, p, s, out);
+  });
+}
+
+gpk_status gpk_test_metrics(gpk_operator* op, gpk_rff_basis* basis, const double* points, int p,
+                            const double* targets, const double* v_y, const double* zhat, int s, double target_scale,
+                            double* out4) {
+  return guarded([&] {  // posterior.cpp:29-59
+    LaunchScope ls(op->ctx);
+    require(p >= 1, "test_metrics: p >= 1");
+    std::vector<double> mean(p);
+    {
+      gpk_status st = gpk_predict_mean(op, points, p, v_y, mean.data());
+      if (st != GPK_OK) throw InvalidArgument(g_err);
+    }
+    std::vector<double> err(p);
+    double se = 0.0;
+    for (int i = 0; i < p; ++i) {
+      err[i] = targets[i] - mean[i];
+      se += err[i] * err[i];
+    }
+    out4[0] = std::sqrt(se / p);
+    out4[2] = out4[0] * target_scale;
+    out4[1] = out4[3] = std::nan("");
+    if (s >= 2 && basis) {
+      std::vector<double> smp(static_cast<size_t>(p) * s);
+      gpk_status st = gpk_sample_posterior(op, basis, points, p, v_y, zhat, s, smp.data());
+      if (st != GPK_OK) throw InvalidArgument(g_err);
+      const double noise_var = op->sigma2;
+      double llh = 0.0;
+      for (int i = 0; i < p; ++i) {
+        double mu = 0.0;
+        for (int j = 0; j < s; ++j) mu += smp[static_cast<size_t>(j) * p + i];
+        mu /= s;
+        double var = 0.0;
+        for (int j = 0; j < s; ++j) {
+          const double t = smp[static_cast<size_t>(j) * p + i] - mu;
+          var += t * t;
+        }
+        var = var / (s - 1) + noise_var;
+        llh += -0.5 * std::log(2.0 * 3.141592653589793 * var) - 0.5 * err[i] * err[i] / var;
+      }
+      out4[1] = llh / p;
+      out4[3] = out4[1] - std::log(target_scale);
+    }
   });
 }
 

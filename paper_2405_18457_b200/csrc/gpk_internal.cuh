@@ -58,6 +58,7 @@ struct KvArgs {
   const int* skip;     // device flag: nonzero => no-op (solver predication)
   double* stats;       // device counters [evals x RHS, algorithmic flops] or null
   int d;               // true input dimension (flop accounting)
+  const float* xs_rows;  // scaled FP32 inputs of the rows (cross kernel k(P, X)); null: xs
 };
 int kv_tc_for(int m);        // columns-per-lane template parameter for m
 int kv_ld_for(int m);        // FP32 RHS leading dimension for m
@@ -91,6 +92,7 @@ struct KvReduceArgs {
   double alpha;
   const int* skip;
   int vshift;           // diagonal RHS row = gi - c0 - vshift (row shard offset)
+  int nodiag;           // cross kernel k(P, X): no sigma^2 diagonal
   // optional fused column reduction of the result: dpart[g][j] = sum over the
   // group's rows of out[r][j] * w[r][j] (w = dotw, or out itself when
   // dotw == out). Deterministic grouping as col_reduce.

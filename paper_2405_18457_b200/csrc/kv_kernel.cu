@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(NT, (TC >= 8 ? 1 : 2)) kv_slab_kernel(const Kv
   const int er = tile * BM + tid;
   const int er_c = er < a.R ? er : 0;
   const int gi = a.row_idx ? a.row_idx[er_c] : a.r0 + er_c;
-  const float4* xi_ptr = reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(gi) * a.dp);
+  const float4* xi_ptr =
+      reinterpret_cast<const float4*>((a.xs_rows ? a.xs_rows : a.xs) + static_cast<size_t>(gi) * a.dp);
 
   // ---- GEMM role ----
   const int rg = warp >> 1, wcg = warp & 1, lr = lane >> 2, lc = lane & 3;
@@ -287,7 +288,7 @@ __global__ void kv_reduce_kernel(const KvReduceArgs a) {
     double acc = 0.0;
     for (int s = 0; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
     const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
-    if (gi >= c0 && gi < c0 + C) {
+    if (!a.nodiag && gi >= c0 && gi < c0 + C) {
       const int vr = gi - c0 - a.vshift;
       const double vv = a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
                                 : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]);
@@ -340,7 +341,7 @@ __global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
   }
   for (int r = rb + warp; r < re; r += NW) {
     const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
-    const bool diag = gi >= c0 && gi < c0 + C;
+    const bool diag = !a.nodiag && gi >= c0 && gi < c0 + C;
     double wsum = 0.0;
 #pragma unroll
     for (int q = 0; q < MQ; ++q) {

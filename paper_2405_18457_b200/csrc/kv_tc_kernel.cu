@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
     const int gi = a.row_idx ? a.row_idx[er_c] : a.r0 + er_c;
     float4 xi[DP4];
 #pragma unroll
-    for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(gi) * DP) + u);
+    const float* xrow = (a.xs_rows ? a.xs_rows : a.xs) + static_cast<size_t>(gi) * DP;
+    for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(xrow) + u);
 #if GPK_EVAL_F32X2
     uint64_t xi2[2 * DP4];
 #pragma unroll

@@ -663,3 +663,42 @@ def sinsum_dataset(n, d, uniform=False, noise=0.1, seed=0):
     check(lib.gpk_sinsum_dataset(n, d, int(uniform), noise, seed, x.ctypes.data_as(C.POINTER(C.c_float)),
                                  y.ctypes.data_as(C.POINTER(C.c_float))))
     return x, y
+
+
+# ---- posterior predictions (posterior.hpp:14-51) ----------------------------
+def cross_kernel_apply(op: KernelOperator, points, v):
+    """k(P, X) V without the noise term (kernel.cpp:72-81)."""
+    P, V = _f64(points), _f64(v)
+    out = np.empty((P.shape[0], V.shape[1]), order="F")
+    check(op._lib.gpk_cross_apply(op.handle, _p(P), P.shape[0], _p(V), V.shape[1], _p(out)))
+    return out
+
+
+def predict_mean(op: KernelOperator, points, v_y):
+    P = _f64(points)
+    vy = np.ascontiguousarray(v_y, dtype=np.float64).reshape(-1)
+    out = np.empty(P.shape[0])
+    check(op._lib.gpk_predict_mean(op.handle, _p(P), P.shape[0], _p(vy), _p(out)))
+    return out
+
+
+def sample_posterior(op: KernelOperator, basis, points, v_y, zhat):
+    """All pathwise posterior samples f_j(P) + k(P,X)(v_y - zhat_j) (posterior.cpp:19-27); basis None = zero prior."""
+    P, Z = _f64(points), _f64(zhat)
+    vy = np.ascontiguousarray(v_y, dtype=np.float64).reshape(-1)
+    out = np.empty((P.shape[0], Z.shape[1]), order="F")
+    check(op._lib.gpk_sample_posterior(op.handle, basis.handle if basis is not None else None, _p(P), P.shape[0],
+                                       _p(vy), _p(Z), Z.shape[1], _p(out)))
+    return out
+
+
+def test_metrics(op: KernelOperator, basis, points, targets, v_y, zhat, target_scale=1.0):
+    """posterior.cpp:29-59 -> dict(rmse, llh, rmse_raw, llh_raw); llh None without >= 2 samples and a basis."""
+    P, Z = _f64(points), _f64(zhat)
+    t = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1)
+    vy = np.ascontiguousarray(v_y, dtype=np.float64).reshape(-1)
+    out = np.empty(4)
+    check(op._lib.gpk_test_metrics(op.handle, basis.handle if basis is not None else None, _p(P), P.shape[0], _p(t),
+                                   _p(vy), _p(Z), Z.shape[1], target_scale, _p(out)))
+    llh = None if np.isnan(out[1]) else out[1]
+    return {"rmse": out[0], "llh": llh, "rmse_raw": out[2], "llh_raw": None if llh is None else out[3]}
