@@ -277,6 +277,10 @@ gpk_status gpk_optimiser_destroy(gpk_optimiser* o);
 gpk_status gpk_sinsum_dataset(int n, int d, int uniform, double noise, uint64_t seed, float* x_rowmajor,
                               float* y);
 
+/* write_trace_csv (trace.cpp:20-44) for rows of gpk_optimise's trace: same
+ * header, columns and shortest round-trip doubles (test columns empty). */
+gpk_status gpk_write_trace_csv(const char* path, const double* trace, int rows, int d);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1997,8 +1997,8 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
   o->P = d + 2;
   o->m = o->s + 1;
   if (o->s < 1) throw InvalidArgument("optimise: probe_count >= 1");
-  if (cfg->estimator != 1 && cfg->probe_distribution != 0)
-    throw InvalidArgument("gpk_optimise: only Gaussian standard probes are implemented");
+  if (cfg->estimator != 1 && (cfg->probe_distribution < 0 || cfg->probe_distribution > 1))
+    throw InvalidArgument("gpk_optimise: probe_distribution 0 (Gaussian) or 1 (Rademacher)");
   o->raw.resize(o->P);
   for (int k = 0; k < o->P; ++k) o->raw[k] = softplus_inverse(init_constrained ? init_constrained[k] : cfg->init_value);
   o->am.assign(o->P, 0.0);
@@ -2075,7 +2075,10 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
   } else {
     if (!o->have_noise || !cfg.warm_start) {
       o->probes.ensure(static_cast<size_t>(nloc) * s);
-      gaussian_fill_rows_launch(cfg.probe_seed, 2, substream, n, s, op->row0, nloc, o->probes.p, stream);
+      if (cfg.probe_distribution == 1)  // gradients.cpp:21-22, rng.cpp:92-96
+        rademacher_fill_rows_launch(cfg.probe_seed, 2, substream, n, s, op->row0, nloc, o->probes.p, stream);
+      else
+        gaussian_fill_rows_launch(cfg.probe_seed, 2, substream, n, s, op->row0, nloc, o->probes.p, stream);
       o->have_noise = true;
     }
     GPK_CUDA(cudaMemcpy2DAsync(b->targets.p + 1, sizeof(double) * m, o->probes.p, sizeof(double) * s,
@@ -2292,6 +2295,44 @@ gpk_status gpk_test_metrics(gpk_operator* op, gpk_rff_basis* basis, const double
       out4[1] = llh / p;
       out4[3] = out4[1] - std::log(target_scale);
     }
+  });
+}
+
+// trace.cpp:7-44: shortest round-trip doubles, same header and columns.
+gpk_status gpk_write_trace_csv(const char* path, const double* trace, int rows, int d) {
+  return guarded([&] {
+    auto fmt = [](double value) {
+      char buffer[40];
+      for (int precision = 15; precision <= 17; ++precision) {
+        std::snprintf(buffer, sizeof(buffer), "%.*g", precision, value);
+        double parsed = 0.0;
+        std::sscanf(buffer, "%lf", &parsed);
+        if (parsed == value) return std::string(buffer);
+      }
+      std::snprintf(buffer, sizeof(buffer), "%.17g", value);
+      return std::string(buffer);
+    };
+    FILE* f = std::fopen(path, "w");
+    if (!f) throw std::runtime_error(std::string("gpk_write_trace_csv: cannot open ") + path);
+    std::string h = "step";
+    for (int i = 0; i < d; ++i) h += ",lengthscale_" + std::to_string(i);
+    h += ",signal_scale,noise_scale,mean_residual_norm,probe_residual_norm,epochs";
+    h += ",solver_seconds_cum,total_seconds_cum,test_rmse,test_llh,grad_inf_norm,diverged";
+    std::fprintf(f, "%s\n", h.c_str());
+    const int P = d + 2, stride = 2 * P + 8;
+    double solver_cum = 0.0, total_cum = 0.0;
+    for (int t = 0; t < rows; ++t) {
+      const double* r = trace + static_cast<size_t>(t) * stride;
+      solver_cum += r[2 * P + 7];
+      total_cum += r[2 * P + 6];
+      std::string line = std::to_string(t);
+      for (int k = 0; k < P; ++k) line += "," + fmt(r[k]);
+      line += "," + fmt(r[2 * P + 0]) + "," + fmt(r[2 * P + 1]) + "," + fmt(r[2 * P + 2]);
+      line += "," + fmt(solver_cum) + "," + fmt(total_cum) + ",,";
+      line += "," + fmt(r[2 * P + 3]) + "," + (r[2 * P + 5] != 0.0 ? "1" : "0");
+      std::fprintf(f, "%s\n", line.c_str());
+    }
+    std::fclose(f);
   });
 }
 

@@ -248,6 +248,9 @@ void gaussian_fill_launch(uint64_t seed, uint64_t stream, uint64_t substream, in
 // rows [row0, row0 + nloc) of the same n x s column-major fill, row-major [nloc][s]
 void gaussian_fill_rows_launch(uint64_t seed, uint64_t stream, uint64_t substream, int n, int s, int row0, int nloc,
                                double* out_rowmajor, cudaStream_t st);
+// Rademacher +-1 from the low bit of u64 draw j*n + i (rng.cpp:92-96)
+void rademacher_fill_rows_launch(uint64_t seed, uint64_t stream, uint64_t substream, int n, int s, int row0, int nloc,
+                                 double* out_rowmajor, cudaStream_t st);
 void xi_assemble_launch(const double* prior, const double* noise, int n, int s, double sigma,
                         double* out, int ldo, int col0, double* xi_copy, cudaStream_t st);
 

@@ -1101,6 +1101,23 @@ void gaussian_fill_rows_launch(uint64_t seed, uint64_t stream, uint64_t substrea
   check_launch("gaussian_fill_rows");
 }
 
+__global__ void rademacher_fill_rows_kernel(uint64_t seed, uint64_t stream, uint64_t substream, int n, int s,
+                                            int row0, int nloc, double* out) {
+  const long long total = static_cast<long long>(nloc) * s;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int il = static_cast<int>(q / s), j = static_cast<int>(q % s);
+    const uint64_t e = static_cast<uint64_t>(j) * n + row0 + il;
+    out[q] = (stream_u64(seed, stream, substream, e) & 1u) ? 1.0 : -1.0;
+  }
+}
+void rademacher_fill_rows_launch(uint64_t seed, uint64_t stream, uint64_t substream, int n, int s, int row0, int nloc,
+                                 double* out_rowmajor, cudaStream_t st) {
+  rademacher_fill_rows_kernel<<<blocks_for(static_cast<long long>(nloc) * s, 256), 256, 0, st>>>(
+      seed, stream, substream, n, s, row0, nloc, out_rowmajor);
+  check_launch("rademacher_fill_rows");
+}
+
 // out[i][col0 + j] = prior[i][j] + sigma * noise[i][j] (rff.cpp:77)
 __global__ void xi_assemble_kernel(const double* prior, const double* noise, int n, int s, double sigma, double* out,
                                    int ldo, int col0, double* xi_copy) {

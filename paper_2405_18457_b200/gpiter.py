@@ -702,3 +702,21 @@ def test_metrics(op: KernelOperator, basis, points, targets, v_y, zhat, target_s
                                    _p(vy), _p(Z), Z.shape[1], target_scale, _p(out)))
     llh = None if np.isnan(out[1]) else out[1]
     return {"rmse": out[0], "llh": llh, "rmse_raw": out[2], "llh_raw": None if llh is None else out[3]}
+
+
+def write_trace_csv(path, trace: dict, input_dim: int):
+    """write_trace_csv (trace.cpp:20-44) for a trace dict returned by optimise()/Optimiser.step()."""
+    P = input_dim + 2
+    rows = len(trace["iterations"])
+    t = np.zeros((max(rows, 1), 2 * P + 8))
+    t[:rows, :P] = trace["constrained"]
+    t[:rows, P:2 * P] = trace["gradient"]
+    t[:rows, 2 * P + 0] = trace["mean_residual_norm"]
+    t[:rows, 2 * P + 1] = trace["probe_residual_norm"]
+    t[:rows, 2 * P + 2] = trace["epochs"]
+    t[:rows, 2 * P + 3] = trace["grad_inf_norm"]
+    t[:rows, 2 * P + 4] = trace["iterations"]
+    t[:rows, 2 * P + 5] = trace["solver_diverged"]
+    t[:rows, 2 * P + 6] = trace.get("step_seconds", np.zeros(rows))
+    t[:rows, 2 * P + 7] = trace.get("solver_seconds", np.zeros(rows))
+    check(_lib.load().gpk_write_trace_csv(str(path).encode(), _p(np.ascontiguousarray(t)), rows, input_dim))
