@@ -850,7 +850,9 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   for (int j = 0; j < m; ++j) inv_scales[j] = 1.0 / b->scales[j];
   double* inv_scales_dev = b->vec1.ensure(m);
   GPK_CUDA(cudaMemcpyAsync(inv_scales_dev, inv_scales.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
-  const int gpb = std::max(1, 256 / nblocks);  // reduction groups per AP block
+  // reduction groups per AP block: one resident wave (3 x 148 blocks of 8 row-warps) keeps enough
+  // row loads in flight for the latency-bound fused reduce
+  const int gpb = std::max(1, std::min(block / 8, 3 * ctx->sms / nblocks));
   const int groups = nblocks * gpb;
   double* spart = b->vec2.ensure(groups);
   double* part = b->red.ensure(static_cast<size_t>(groups) * m + 8);
@@ -1001,12 +1003,90 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   finalise(b, c->tolerance, rep, start);
 }
 
+// SGD on the tcgen05 operator, single rank or row-sharded: the
+// minibatch rows idx are contracted against this rank's own rows only; the
+// b x m partial gradients (+ the owning rank's target and diagonal terms) are
+// all-gathered and summed in rank order, so every rank holds the same g and
+// takes the same termination decision, and updates only its own rows of
+// momentum, solution and residual estimate -- writing the solution's TF32
+// operator images in the same pass, so the next contraction reads them as is.
+void solve_sgd_tc(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep, int bs, int budget,
+                  double step, Clock::time_point start) {
+  gpk_operator* op = b->op;
+  cudaStream_t s = op->ctx->stream;
+  const int n = op->n, nloc = b->n, m = b->m, G = kReduceGroups, nr = op->nr;
+  const int row0 = op->sharded ? op->row0 : 0;
+  const size_t nm = static_cast<size_t>(nloc) * m;
+  GPK_CUDA(cudaMemcpyAsync(b->residuals.p, b->targets.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, s));
+  double* M = b->w1.ensure(nm);
+  GPK_CUDA(cudaMemsetAsync(M, 0, sizeof(double) * nm, s));
+  const int npad = kv_tc_npad(m);
+  float* vpk = b->apk.ensure(kv_tc_pack_floats(m, nloc));
+  kv_tc_pack_launch(b->solutions.p, nullptr, m, nloc, m, nullptr, 0, n, vpk, nullptr, s);
+  double* hv = b->w2.ensure(static_cast<size_t>(bs) * m);
+  double* grad = b->w3.ensure(static_cast<size_t>(bs) * m);
+  const long long stride = (static_cast<long long>(bs) * m + m + 1 + 31) / 32 * 32;  // doubles per rank slice
+  double* gbuf = b->w4.ensure(static_cast<size_t>(nr) * stride);
+  double* part = b->red.ensure(static_cast<size_t>(nr) * G * 2 * m + 8);
+  double* sumsq = b->vec1.ensure(m);
+  int* pos = b->ibuf2.ensure(nloc);
+  GPK_CUDA(cudaMemsetAsync(pos, 0xff, sizeof(int) * nloc, s));  // -1
+  int* nonfinite = b->flag.ensure(1);
+  GPK_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), s));
+  col_reduce_launch(b->residuals.p, nullptr, nloc, m, m, 2, part + static_cast<size_t>(op->rk) * G * m, G, nullptr,
+                    s);
+  gather_inplace(op, part, sizeof(double) * G * m);
+  sum_partials_launch(part, G * nr, m, sumsq, nullptr, s);
+  init_ctl(b, budget, -1);
+  CgCtl* ctl = b->ctl.p;
+  const int* stop = &ctl->stop;
+  sgd_check_launch(sumsq, m, b->scales_dev.p, c->tolerance, nonfinite, ctl, s);  // initial test
+
+  const int chunk = 256;
+  int* idxbuf = b->ibuf.ensure(static_cast<size_t>(chunk) * bs);
+  int t = 0;
+  auto iteration = [&]() {  // solvers.cpp:164-178
+    if (t % chunk == 0) sgd_batches_launch(c->seed, c->substream, n, bs, t, std::min(chunk, budget - t), idxbuf, s);
+    const int* idx = idxbuf + static_cast<size_t>(t % chunk) * bs;
+    KvCall kc;
+    kc.vpk = vpk;
+    kc.m = m;
+    kc.row_idx = idx;
+    kc.R = bs;
+    kc.c0 = row0;
+    kc.C = nloc;
+    kc.vdiag = b->solutions.p;
+    kc.out = hv;
+    kc.ldo = m;
+    kc.skip = stop;
+    run_kv(op, kc);
+    double* slice = gbuf + static_cast<size_t>(op->sharded ? op->rk : 0) * stride;
+    sgd_prep_launch(hv, idx, bs, b->targets.p, b->residuals.p, row0, nloc, m, pos, nonfinite, slice, stop, s);
+    gather_inplace(op, gbuf, sizeof(double) * stride);
+    sgd_gsum_launch(gbuf, nr, stride, bs, m, grad, stop, s);
+    sgd_check_sharded_launch(gbuf, nr, stride, grad, bs, m, sumsq, b->scales_dev.p, c->tolerance, ctl, s);
+    // the update runs for the iteration the check just counted (skip reads
+    // stop before it is set for the next one: test the pre-check flag)
+    sgd_update_pack_launch(M, b->solutions.p, b->residuals.p, vpk, npad, pos, grad, c->momentum, step, nloc, m,
+                           nonfinite, &ctl->pad, s);
+    sgd_unscatter_launch(idx, bs, row0, nloc, pos, &ctl->pad, s);
+    ++t;
+  };
+  drive(b, ctl, std::max(1, iteration_group(n) * 4), budget, iteration);
+  const CgCtl h = read_ctl(b);
+  rep->iterations = h.iters;
+  rep->epochs_consumed = static_cast<double>(h.iters) * bs / n;
+  rep->aborted = h.aborted;
+  if (h.aborted) std::strncpy(rep->abort_reason, "sgd divergence: non-finite iterate", 127);
+  finalise(b, c->tolerance, rep, start);
+}
+
 void solve_sgd(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) {
   validate(c);
   const auto start = Clock::now();
   gpk_operator* op = b->op;
   cudaStream_t s = op->ctx->stream;
-  const int n = b->n, m = b->m, G = kReduceGroups;
+  const int n = op->n, m = b->m, G = kReduceGroups;  // global rows (b->n is the shard on a sharded operator)
   if (m > kMaxRhs) throw InvalidArgument("gpk: batches wider than 65 columns are not supported by the solvers");
   std::memset(rep, 0, sizeof(*rep));
   rep->residuals_estimated = 1;
@@ -1014,6 +1094,8 @@ void solve_sgd(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep)
   const double max_iterations = static_cast<double>(c->max_epochs) * n / bs;
   const int budget = static_cast<int>(std::ceil(max_iterations));
   const double step = c->learning_rate / bs;
+  if (op->ctx->kernel == 1) return solve_sgd_tc(b, c, rep, bs, budget, step, start);
+  if (op->nr > 1) throw InvalidArgument("gpk: the sharded operator needs the tcgen05 kernel");
   const size_t nm = static_cast<size_t>(n) * m;
   const int ld = kv_ld_for(m);
   GPK_CUDA(cudaMemcpyAsync(b->residuals.p, b->targets.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, s));
@@ -2009,8 +2091,8 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
   if (gpk_operator_create(ctx, inputs, n, d, o->raw.data(), &opp) != GPK_OK) throw InvalidArgument(g_err);
   o->op.reset(opp);
   if (ctx->comm) {  // row shard of this rank (X stays replicated)
-    if (cfg->solver.kind != GPK_CG)
-      throw InvalidArgument("gpk_optimise: multi-GPU row sharding is implemented for the CG solver");
+    if (cfg->solver.kind == GPK_AP)
+      throw InvalidArgument("gpk_optimise: multi-GPU row sharding is implemented for the CG and SGD solvers");
     if (ctx->kernel != 1) throw InvalidArgument("gpk_optimise: multi-GPU needs the tcgen05 operator kernel");
     opp->sharded = true;
     opp->nr = ctx->nranks;

@@ -239,6 +239,21 @@ void sgd_residual_launch(double* R, const int* idx, int b, const double* grad, i
 void sgd_check_launch(const double* sumsq, int m, const double* scales, double tol,
                       const int* nonfinite, CgCtl* ctl, cudaStream_t s);
 
+// Row-sharded SGD on the tcgen05 operator (one rank = one row shard; with
+// one rank the same kernels run without the all-gather). Exchange slice per
+// rank: [b*m gradient partials | m own old-residual squares | 1 non-finite flag].
+void sgd_prep_launch(const double* hv_part, const int* idx, int b, const double* targets, const double* R,
+                     int row0, int nloc, int m, int* pos, const int* nonfinite, double* slice, const int* skip,
+                     cudaStream_t s);
+void sgd_gsum_launch(const double* gbuf, int nr, long long stride, int b, int m, double* grad, const int* skip,
+                     cudaStream_t s);
+void sgd_check_sharded_launch(const double* gbuf, int nr, long long stride, const double* grad, int b, int m,
+                              double* sumsq, const double* scales, double tol, CgCtl* ctl, cudaStream_t s);
+void sgd_update_pack_launch(double* M, double* V, double* R, float* vpk, int npad, const int* pos,
+                            const double* grad, double rho, double step, int nloc, int m, int* nonfinite,
+                            const int* skip, cudaStream_t s);
+void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, const int* skip, cudaStream_t s);
+
 // RFF (K5) + noise (K9)
 void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs,
                       const double* weights, int ldw, int s, double amplitude, double* prior,

@@ -317,7 +317,7 @@ __device__ __forceinline__ void group_rows(const KvReduceArgs& a, int g, int& rb
   }
 }
 
-__global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
+__global__ void __launch_bounds__(256, 3) kv_reduce_dot_kernel(const KvReduceArgs a) {
   if (a.skip && *a.skip) return;
   constexpr int NW = 8, MQ = 3;  // 8 warps; lane owns columns lane + 32 q, q < 3 (m <= 96)
   __shared__ double red[NW][96];
@@ -339,25 +339,40 @@ __global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
     const int j = lane + 32 * q;
     isc[q] = (a.spart && j < a.m) ? a.inv_scales[j] : 0.0;
   }
+  // Row loop, latency-bound: all loads of a row (split partials, base,
+  // diagonal term, dot weights) are issued before any is consumed; the split
+  // partials are summed in split order as before.
   for (int r = rb + warp; r < re; r += NW) {
     const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
     const bool diag = !a.nodiag && gi >= c0 && gi < c0 + C;
+    const int vr = gi - c0 - a.vshift;
+    double pv[MQ][2], bv[MQ], dv[MQ], wv[MQ];
+#pragma unroll
+    for (int q = 0; q < MQ; ++q) {
+      const int j = lane + 32 * q;
+      const bool ok = j < a.m;
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        pv[q][s] = (ok && s < a.splits) ? __ldcs(a.part + (static_cast<size_t>(s) * a.R + r) * a.m + j) : 0.0;
+      bv[q] = (ok && a.base) ? a.base[static_cast<size_t>(r) * a.ldb + j] : 0.0;
+      dv[q] = 0.0;
+      if (ok && diag)
+        dv[q] = a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
+                        : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]);
+      wv[q] = (ok && a.dotw != a.out) ? a.dotw[static_cast<size_t>(r) * a.ldo + j] : 0.0;
+    }
     double wsum = 0.0;
 #pragma unroll
     for (int q = 0; q < MQ; ++q) {
       const int j = lane + 32 * q;
       if (j < a.m) {
-        double acc = 0.0;
-        for (int s = 0; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
-        if (diag) {
-          const int vr = gi - c0 - a.vshift;
-          acc += a.sigma2 * (a.vdiag ? a.vdiag[static_cast<size_t>(vr) * a.ldvd + j]
-                                     : static_cast<double>(a.vdiag32[static_cast<size_t>(vr) * a.ldv32 + j]));
-        }
-        const double b = a.base ? a.base[static_cast<size_t>(r) * a.ldb + j] : 0.0;
-        const double val = b + a.alpha * acc;
+        double acc = pv[q][0];
+        if (a.splits > 1) acc += pv[q][1];
+        for (int s = 2; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
+        if (diag) acc += a.sigma2 * dv[q];
+        const double val = bv[q] + a.alpha * acc;
         a.out[static_cast<size_t>(r) * a.ldo + j] = val;
-        const double w = (a.dotw == a.out) ? val : a.dotw[static_cast<size_t>(r) * a.ldo + j];
+        const double w = (a.dotw == a.out) ? val : wv[q];
         dot[q] = fma(val, w, dot[q]);
         wsum += val * isc[q];
       }
@@ -404,10 +419,12 @@ __global__ void kv_reduce_dot_kernel(const KvReduceArgs a) {
     if (lane == 0) ss[j] = acc;
   }
   __shared__ double bscore[1024];
-  for (int k = threadIdx.x; k < a.nblocks; k += blockDim.x) {
+  for (int k = warp; k < a.nblocks; k += NW) {  // fixed xor tree per block
     double t = 0.0;
-    for (int q = 0; q < a.gpb; ++q) t += __ldcg(a.spart + static_cast<size_t>(k) * a.gpb + q);
-    if (k < 1024) bscore[k] = sqrt(t);
+    for (int q = lane; q < a.gpb; q += 32) t += __ldcg(a.spart + static_cast<size_t>(k) * a.gpb + q);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0 && k < 1024) bscore[k] = sqrt(t);
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -985,6 +985,183 @@ void sgd_check_launch(const double* sumsq, int m, const double* scales, double t
   check_launch("sgd_check");
 }
 
+// ------------------------------------------------- SGD, row-sharded form
+// H[idx] V = sum over ranks of K[idx, own rows] V_own (+ s2 V[idx] on the
+// owning rank). Each rank contributes hv_part - B[idx] on its own rows, so the
+// rank-ordered sum of slices is g = H[idx] V - B[idx] (solvers.cpp:166-167).
+// The residual-estimate update R[idx] = -g changes the squared norms by
+// sum_q g^2 - sum_{own q} R_old[idx_q]^2; the old squares travel with the
+// slice so every rank updates an identical replicated copy.
+__global__ void sgd_prep_kernel(const double* hv_part, const int* idx, int b, const double* targets,
+                                const double* R, int row0, int nloc, int m, int* pos, const int* nonfinite,
+                                double* slice, const int* skip) {
+  SKIP_IF(skip);
+  const int bm = b * m;
+  if (blockIdx.x == gridDim.x - 1) {  // old squares, pos map, flag
+    for (int q = threadIdx.x; q < b; q += blockDim.x) {
+      const int li = idx[q] - row0;
+      if (li >= 0 && li < nloc) pos[li] = q;
+    }
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      double acc = 0.0;
+      for (int q = 0; q < b; ++q) {
+        const int li = idx[q] - row0;
+        if (li >= 0 && li < nloc) {
+          const double r = R[static_cast<size_t>(li) * m + j];
+          acc += r * r;
+        }
+      }
+      slice[bm + j] = acc;
+    }
+    if (threadIdx.x == 0) slice[bm + m] = *nonfinite ? 1.0 : 0.0;
+    return;
+  }
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bm; e += (gridDim.x - 1) * blockDim.x) {
+    const int q = e / m, j = e - q * m;
+    const int li = idx[q] - row0;
+    double g = hv_part[e];
+    if (li >= 0 && li < nloc) g -= targets[static_cast<size_t>(li) * m + j];
+    slice[e] = g;
+  }
+}
+void sgd_prep_launch(const double* hv_part, const int* idx, int b, const double* targets, const double* R,
+                     int row0, int nloc, int m, int* pos, const int* nonfinite, double* slice, const int* skip,
+                     cudaStream_t s) {
+  const int blocks = blocks_for(static_cast<long long>(b) * m, 256, 64) + 1;
+  sgd_prep_kernel<<<blocks, 256, 0, s>>>(hv_part, idx, b, targets, R, row0, nloc, m, pos, nonfinite, slice, skip);
+  check_launch("sgd_prep");
+}
+
+__global__ void sgd_gsum_kernel(const double* gbuf, int nr, long long stride, int bm, double* grad,
+                                const int* skip) {
+  SKIP_IF(skip);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bm; e += gridDim.x * blockDim.x) {
+    double g = gbuf[e];
+    for (int r = 1; r < nr; ++r) g += gbuf[r * stride + e];  // rank order
+    grad[e] = g;
+  }
+}
+void sgd_gsum_launch(const double* gbuf, int nr, long long stride, int b, int m, double* grad, const int* skip,
+                     cudaStream_t s) {
+  sgd_gsum_kernel<<<blocks_for(static_cast<long long>(b) * m, 256, 64), 256, 0, s>>>(gbuf, nr, stride, b * m, grad,
+                                                                                    skip);
+  check_launch("sgd_gsum");
+}
+
+// Replicated termination test (solvers.cpp:172-177): one warp per column.
+__global__ void sgd_check_sharded_kernel(const double* gbuf, int nr, long long stride, const double* grad, int b,
+                                         int m, double* sumsq, const double* scales, double tol, CgCtl* ctl) {
+  // pad = stop as it was before this test: this iteration's update still runs
+  // when the test below terminates (solvers.cpp updates, then tests)
+  const int stopped = ctl->stop;
+  __syncthreads();
+  if (threadIdx.x == 0) ctl->pad = stopped;
+  if (stopped) return;
+  __shared__ double ss[512];
+  __shared__ int bad;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int bm = b * m;
+  if (threadIdx.x == 0) {
+    double f = 0.0;
+    for (int r = 0; r < nr; ++r) f += gbuf[r * stride + bm + m];
+    bad = f != 0.0;
+  }
+  for (int j = warp; j < m; j += nw) {
+    double acc = 0.0;
+    for (int q = lane; q < b; q += 32) {
+      const double g = grad[static_cast<size_t>(q) * m + j];
+      acc += g * g;
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      double old = 0.0;
+      for (int r = 0; r < nr; ++r) old += gbuf[r * stride + bm + j];
+      const double v = sumsq[j] + (acc - old);
+      sumsq[j] = v;
+      ss[j] = fmax(v, 0.0);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->iters += 1;
+    if (bad) {
+      ctl->aborted = 1;
+      ctl->stop = 1;
+      return;
+    }
+    int done;
+    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    ctl->done = done;
+    ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
+  }
+}
+void sgd_check_sharded_launch(const double* gbuf, int nr, long long stride, const double* grad, int b, int m,
+                              double* sumsq, const double* scales, double tol, CgCtl* ctl, cudaStream_t s) {
+  sgd_check_sharded_kernel<<<1, 1024, 0, s>>>(gbuf, nr, stride, grad, b, m, sumsq, scales, tol, ctl);
+  check_launch("sgd_check_sharded");
+}
+
+// momentum *= rho; momentum[idx] -= step g; V += momentum; R[idx] = -g, over
+// this rank's rows, writing V's TF32 hi/lo operator images in the same pass
+// (the kv_tc B-operand layout, see kv_pack_kernel).
+__global__ void sgd_update_pack_kernel(double* M, double* V, double* R, float* vpk, int npad, int rows_pad,
+                                       const int* pos, const double* grad, double rho, double step, int nloc, int m,
+                                       int* nonfinite, const int* skip) {
+  SKIP_IF(skip);
+  const int img = npad * 32;
+  const long long total = static_cast<long long>(rows_pad) * npad;
+  int bad = 0;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / npad), j = static_cast<int>(e % npad);
+    double v = 0.0;
+    if (i < nloc && j < m) {
+      const size_t o = static_cast<size_t>(i) * m + j;
+      double mo = __dmul_rn(M[o], rho);
+      const int q = pos[i];
+      if (q >= 0) {
+        const double g = grad[static_cast<size_t>(q) * m + j];
+        mo = __dsub_rn(mo, __dmul_rn(step, g));
+        R[o] = -g;
+      }
+      M[o] = mo;
+      v = __dadd_rn(V[o], mo);
+      V[o] = v;
+      if (!isfinite(v)) bad = 1;
+    }
+    uint32_t hb, lb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(static_cast<float>(v)));
+    const float h = __uint_as_float(hb);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(static_cast<float>(v - static_cast<double>(h))));
+    const int kk = i % 32;
+    float* base = vpk + static_cast<size_t>(i / 32) * 2 * img;
+    const int off = ((j / 8) * 8 + kk / 4) * 32 + (j % 8) * 4 + (kk % 4);
+    base[off] = h;
+    base[img + off] = __uint_as_float(lb);
+  }
+  if (bad) atomicOr(nonfinite, 1);
+}
+void sgd_update_pack_launch(double* M, double* V, double* R, float* vpk, int npad, const int* pos,
+                            const double* grad, double rho, double step, int nloc, int m, int* nonfinite,
+                            const int* skip, cudaStream_t s) {
+  const int rows_pad = (nloc + 31) / 32 * 32;
+  sgd_update_pack_kernel<<<blocks_for(static_cast<long long>(rows_pad) * npad, 256), 256, 0, s>>>(
+      M, V, R, vpk, npad, rows_pad, pos, grad, rho, step, nloc, m, nonfinite, skip);
+  check_launch("sgd_update_pack");
+}
+
+__global__ void sgd_unscatter_kernel(const int* idx, int b, int row0, int nloc, int* pos, const int* skip) {
+  SKIP_IF(skip);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < b; q += gridDim.x * blockDim.x) {
+    const int li = idx[q] - row0;
+    if (li >= 0 && li < nloc) pos[li] = -1;
+  }
+}
+void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, const int* skip, cudaStream_t s) {
+  sgd_unscatter_kernel<<<blocks_for(b, 256), 256, 0, s>>>(idx, b, row0, nloc, pos, skip);
+  check_launch("sgd_unscatter");
+}
+
 // ------------------------------------------------------------ RFF (K5)
 // prior[i][j] = sum_q feat(i,q) W(q,j), feat(i,2p) = amp cos(theta), feat(i,2p+1)
 // = amp sin(theta), theta = x_i . (Omega_p / l) in FP64 (rff.cpp:36-54, 73).

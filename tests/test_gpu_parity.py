@@ -295,15 +295,17 @@ def test_optimise_trajectory_matches_oracle(G, kctx, oracle):
     assert np.max(np.abs(g - rg) / np.maximum(np.abs(rg), 1e-2 * np.max(np.abs(rg)))) <= 1e-3
 
 
-def test_sharded_optimiser_world1_matches_plain(G, gpk_ctx, oracle):
+@pytest.mark.parametrize("solver", ["cg", "sgd"])
+def test_sharded_optimiser_world1_matches_plain(G, gpk_ctx, oracle, solver):
     """The row-sharded optimiser (NCCL communicator, all-gathered packed
-    directions and partial sums) on a 1-rank communicator reproduces the plain
-    single-GPU run bit for bit."""
+    directions / SGD gradient partials and partial sums) on a 1-rank
+    communicator reproduces the plain single-GPU run bit for bit."""
     from paper_2405_18457_b200 import parallel as P
     n, d = 2048, 8
     X32, y32 = G.sinsum_dataset(n, d, False, 0.1, 0)
     X, y = X32.astype(np.float64), y32.astype(np.float64)
-    scfg = dict(kind=0, tolerance=0.01, max_epochs=50, preconditioner_rank=100)
+    scfg = dict(kind=0, tolerance=0.01, max_epochs=50, preconditioner_rank=100) if solver == "cg" else \
+        dict(kind=2, tolerance=0.01, max_epochs=10, batch_size=256, learning_rate=10.0, momentum=0.9)
     ocfg = dict(estimator=1, warm_start=True, steps=4, learning_rate=0.1, probe_count=16, rff_pairs=256,
                 probe_seed=2, feature_seed=3, solver_seed=4)
     plain = G.optimise(gpk_ctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))

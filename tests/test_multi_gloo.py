@@ -134,6 +134,85 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def _sgd_worker(rank, world, port, q, cfg):
+    """Row-sharded SGD exactly as solve_sgd_tc (csrc/gpk_api.cu) decomposes it:
+    the minibatch rows are contracted against this rank's own rows, the owning
+    rank folds in -B[idx] (and, inside H's block, the noise diagonal), and the
+    b x m slices plus the old residual squares are all-gathered and summed in
+    rank order; each rank updates only its own momentum/solution/residual rows."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2405_18457_b200 import parallel as P
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    X, T, _ = _problem()
+    n = X.shape[0]
+    raw = O.raw_from_constrained([0.9, 1.1, 1.3, 1.0, 0.5])
+    H = O.dense(X, raw)
+    S = P.shard_stride(n, world)
+    r0, r1 = P.shard_rows(n, world, rank)
+    b = min(cfg["batch_size"], n)
+    budget = int(np.ceil(cfg["max_epochs"] * n / b))
+    step = cfg["learning_rate"] / b
+    batches = O.sample_without_replacement(cfg["seed"], 6, cfg["substream"], n, b, budget)
+    scales = np.sqrt(_sum_in_rank_order(dist, (T[r0:r1] ** 2).sum(0), world)) + 1e-12
+    V = np.zeros((r1 - r0, T.shape[1]))
+    M = np.zeros_like(V)
+    R = T[r0:r1].copy()
+    sumsq = _sum_in_rank_order(dist, (R ** 2).sum(0), world)
+
+    def done(ss):
+        ss = np.maximum(ss, 0.0)
+        return np.sqrt(ss[0]) / scales[0] <= cfg["tolerance"] and \
+            np.mean(np.sqrt(ss[1:]) / scales[1:]) <= cfg["tolerance"]
+
+    t = 0
+    finished = done(sumsq)
+    while not finished and t < budget:
+        idx = batches[t]
+        own = (idx >= r0) & (idx < r1)
+        part = H[idx][:, r0:r1] @ V
+        part[own] -= T[idx[own]]
+        old = (R[idx[own] - r0] ** 2).sum(0)
+        g = _sum_in_rank_order(dist, part, world)
+        sumsq = sumsq + ((g ** 2).sum(0) - _sum_in_rank_order(dist, old, world))
+        t += 1
+        finished = done(sumsq)
+        M *= cfg["momentum"]
+        M[idx[own] - r0] -= step * g[own]
+        V += M
+        R[idx[own] - r0] = -g[own]
+    q.put((rank, t, _gather_rows(dist, V, S, world)[:n]))
+    dist.destroy_process_group()
+
+
+def test_world2_gloo_sharded_sgd_matches_single_process(oracle):
+    import torch.multiprocessing as mp
+    cfg = dict(kind=2, tolerance=0.05, max_epochs=30, batch_size=24, learning_rate=1.0, momentum=0.9, seed=4,
+               substream=1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sgd_worker, args=(r, 2, port, q, cfg)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, t0, V0), (_, t1, V1) = res
+    assert t0 == t1 and np.array_equal(V0, V1)
+    X, T, _ = _problem()
+    raw = oracle.raw_from_constrained([0.9, 1.1, 1.3, 1.0, 0.5])
+    ref = oracle.solve(X, raw, T, oracle.solver_config(**{k: v for k, v in cfg.items()}))
+    assert abs(ref["iterations"] - t0) <= 1
+    if ref["iterations"] == t0:
+        assert np.max(np.abs(V0 - ref["solutions"])) <= 1e-9 * np.max(np.abs(ref["solutions"]))
+
+
 def test_shard_partition_matches_library():
     import sys
     sys.path.insert(0, ROOT)
