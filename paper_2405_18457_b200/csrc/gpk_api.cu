@@ -105,6 +105,7 @@ struct gpk_operator {
   // gradient-pass workspace (persistent across steps)
   DBuf<float> gbuf[4];
   DBuf<double> gpart, gtot, gdots;
+  DBuf<float> gpk_b, gpk_n;  // tensor-core gradient pass: packed W images, narrow-pair vectors
   int n = 0, d = 0, dp = 0;
   DBuf<double> x64;       // [n][d] unscaled
   DBuf<float> xs32;       // [n][dp]
@@ -1259,21 +1260,60 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
   }
   a.s2 = static_cast<float>(op->s2);
   a.log2_s2 = static_cast<float>(std::log2(op->s2));
-  a.blocks = 2 * op->ctx->sms;
-  {
-    const long long T = (n + 63) / 64;
-    const long long ntiles = a.symmetric ? T * (T + 1) / 2 : T * T;
-    a.tile_begin = ntiles * rk / nr;
-    a.tile_end = ntiles * (rk + 1) / nr;
-  }
   const int per = P * (d + 1);
   DBuf<double>& part = op->gpart;
   DBuf<double>& tot = op->gtot;
   DBuf<double>& dots = op->gdots;
-  part.ensure(static_cast<size_t>(nr) * a.blocks * per);
+  // tensor-core pass: one wide pair (1 < s <= 64) and at most one narrow pair
+  int pw = -1, pn = -1;
+  for (int p = 0; p < P; ++p) {
+    if (a.mcols[p] > 1 && pw < 0)
+      pw = p;
+    else if (a.mcols[p] == 1 && pn < 0)
+      pn = p;
+  }
+  const bool tc = op->ctx->kernel == 1 && pw >= 0 && a.mcols[pw] <= 64 && (P == 1 || pn >= 0);
+  if (tc) {
+    GradTcArgs t{};
+    t.xs = op->xs32.p;
+    t.n = n;
+    t.d = d;
+    t.dp = op->dp;
+    t.ua = a.u[pw];
+    t.lda = a.ldu[pw];
+    t.cols = a.mcols[pw];
+    t.kp = grad_tc_kp(t.cols);
+    const int rows_pad = grad_tc_rows_pad(n);
+    float* bpk = op->gpk_b.ensure(static_cast<size_t>(rows_pad) * 2 * t.kp);
+    float* nar = pn >= 0 ? op->gpk_n.ensure(static_cast<size_t>(2) * rows_pad) : nullptr;
+    grad_tc_pack_launch(a.w[pw], a.ldu[pw], n, t.cols, t.kp, bpk, pn >= 0 ? a.u[pn] : nullptr,
+                        pn >= 0 ? a.w[pn] : nullptr, pn >= 0 ? a.ldu[pn] : 0, nar, nar ? nar + rows_pad : nullptr, s);
+    t.bpk = bpk;
+    t.u1 = nar;
+    t.w1 = nar ? nar + rows_pad : nullptr;
+    t.symmetric = a.symmetric;
+    t.pw = pw;
+    t.pn = pn >= 0 ? pn : 0;
+    t.npairs = P;
+    t.blocks = op->ctx->sms;
+    const long long ntiles = grad_tc_tiles(n, a.symmetric);
+    t.tile_begin = ntiles * rk / nr;
+    t.tile_end = ntiles * (rk + 1) / nr;
+    a.blocks = t.blocks;
+    part.ensure(static_cast<size_t>(nr) * a.blocks * per);
+    t.part = part.p + static_cast<size_t>(rk) * a.blocks * per;
+    grad_tc_launch(t, s);
+  } else {
+    a.blocks = 2 * op->ctx->sms;
+    const long long T = (n + 63) / 64;
+    const long long ntiles = a.symmetric ? T * (T + 1) / 2 : T * T;
+    a.tile_begin = ntiles * rk / nr;
+    a.tile_end = ntiles * (rk + 1) / nr;
+    part.ensure(static_cast<size_t>(nr) * a.blocks * per);
+    a.part = part.p + static_cast<size_t>(rk) * a.blocks * per;
+    grad_launch(a, s);
+  }
   tot.ensure(per);
-  a.part = part.p + static_cast<size_t>(rk) * a.blocks * per;
-  grad_launch(a, s);
   gather_inplace(op, part.p, sizeof(double) * a.blocks * per);
   sum_partials_launch(part.p, a.blocks * nr, per, tot.p, nullptr, s);
   // noise terms: sum u.w (FP64) over this rank's rows, gathered
@@ -1586,9 +1626,10 @@ gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d,
     op->nloc = n;
     op->S = n;
     op->x64.ensure(static_cast<size_t>(n) * d);
-    // 32 zero rows of padding: the tensor-core kernel bulk-copies whole 32-row chunks
-    op->xs32.ensure(static_cast<size_t>(n + 32) * op->dp);
-    GPK_CUDA(cudaMemsetAsync(op->xs32.p, 0, sizeof(float) * (n + 32) * op->dp, ctx->stream));
+    // 128 zero rows of padding: the tensor-core kernels bulk-copy whole 32-row
+    // (operator) and 64-row (gradient pass) chunks up to the 128-row tile edge
+    op->xs32.ensure(static_cast<size_t>(n + 128) * op->dp);
+    GPK_CUDA(cudaMemsetAsync(op->xs32.p, 0, sizeof(float) * (n + 128) * op->dp, ctx->stream));
     op->xs64.ensure(static_cast<size_t>(n) * d);
     upload_colmajor(op.get(), inputs, n, d, op->x64.p);
     set_hyper(op.get(), raw);

@@ -138,6 +138,31 @@ struct GradArgs {
 };
 void grad_launch(const GradArgs& a, cudaStream_t s);
 
+// Tensor-core gradient pass (grad_tc_kernel.cu): one wide pair (G on tcgen05)
+// plus optionally one narrow (single-column) pair.
+struct GradTcArgs {
+  const float* xs;      // [rows_pad][dp] scaled FP32 (zero rows beyond n)
+  int n, d, dp;
+  const float* ua;      // wide pair U rows, FP32 [n][lda]
+  int lda, cols;
+  const float* bpk;     // wide pair W, packed TF32 hi|lo images per 64-row chunk
+  int kp;               // cols rounded up to 16
+  const float* u1;      // narrow pair U, W as contiguous [rows_pad] (nullptr: none)
+  const float* w1;
+  int symmetric;
+  int pw, pn;           // output slots of the wide / narrow pair
+  int npairs;
+  double* part;         // [blocks][npairs*(d+1)]
+  int blocks;
+  long long tile_begin, tile_end;  // 128 x 128 tiles of this rank
+};
+int grad_tc_kp(int cols);
+int grad_tc_rows_pad(int n);
+long long grad_tc_tiles(int n, int symmetric);
+void grad_tc_pack_launch(const float* w32, int ld, int n, int cols, int kp, float* bpk, const float* n_u,
+                         const float* n_w, int n_ld, float* u1, float* w1, cudaStream_t s);
+void grad_tc_launch(const GradTcArgs& a, cudaStream_t s);
+
 // ---- misc device kernels (la_kernels.cu) ---------------------------------
 void prescale_launch(const double* x64, int n, int d, int dp, const double* inv_ls, float* xs32,
                      double* xs64, cudaStream_t s);

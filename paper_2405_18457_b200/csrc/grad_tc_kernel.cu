@@ -1,0 +1,429 @@
+// K4 on the 5th-generation tensor cores: the fused hyperparameter-gradient
+// quadratic forms of KernelOperator::derivative_quadratic_forms_many
+// (/root/reference/proj/core/src/kernel.cpp:238-272), for the estimator's
+// usual pair set: one wide pair (U, W with s probe columns) and optionally one
+// narrow pair (the mean solve, one column). For every entry (i, c):
+//   g_ic    = sum_j U[i,j] W[c,j]          -> tcgen05 (3xTF32), D in TMEM
+//   signal += k_ic g_ic ; l_k += e_ic g_ic (x_ck - x_ik)^2     -> FP32 SIMT
+// (same sums and FP32 evaluation as grad_kernel.cu, whose SIMT phase-1 GEMM
+// this replaces; the host scales them exactly as kernel.cpp:264-268).
+//
+// CTA (one per SM, persistent over a contiguous range of 128 x 128 tiles of
+// the symmetric (ti <= tc) or full tile list; each tile = two 64-column chunks):
+//   warps 0-7  A operand: on every row-block change each thread writes its
+//              row of U (TF32 hi | lo) into TMEM with tcgen05.st; per chunk it
+//              reads 32 G values of its row (tcgen05.ld), evaluates the kernel
+//              against the chunk's x_c (smem broadcast) and accumulates the
+//              d + 1 sums per pair in FP32; per tile the sums are reduce-
+//              scattered across the warp (butterfly) into FP64 per-warp slots.
+//   warp 8     producer: cp.async.bulk of the chunk's pre-packed W images,
+//              x_c rows and narrow-pair w values into a 3-stage ring.
+//   warp 9     one thread issues 3 x KP/8 tcgen05.mma.kind::tf32 (M=128,
+//              N=64, A from TMEM, B from smem) per chunk into one of two TMEM
+//              D buffers; tcgen05.commit releases the stage and the buffer.
+// Deterministic: fixed tile ranges, fixed butterfly, fixed warp order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "gpk_internal.cuh"
+#include "tc_util.cuh"
+
+namespace gpk {
+
+namespace {
+
+using namespace tc;
+
+constexpr int TBM = 128;  // tile edge (rows per CTA pass, columns per tile)
+constexpr int CN = 64;    // columns per chunk == MMA N
+constexpr int STAGES = 3;
+constexpr int NTHREADS = 320;
+constexpr int EVAL_WARPS = 8;
+constexpr int TMEM_COLS = 256;
+constexpr int A_BASE = 2 * CN;  // D buffers at TMEM columns [0, 64) and [64, 128)
+
+__device__ __forceinline__ void tile_coords_tc(long long L, int T, int symmetric, int& ti, int& tc) {
+  if (!symmetric) {
+    ti = static_cast<int>(L / T);
+    tc = static_cast<int>(L % T);
+    return;
+  }
+  const double b = 2.0 * T + 1.0;
+  int r = static_cast<int>((b - sqrt(b * b - 8.0 * static_cast<double>(L))) / 2.0);
+  r = max(0, min(r, T - 1));
+  auto off = [&](long long rr) { return rr * T - rr * (rr - 1) / 2; };
+  while (r > 0 && off(r) > L) --r;
+  while (r + 1 < T && off(r + 1) <= L) ++r;
+  ti = r;
+  tc = r + static_cast<int>(L - off(r));
+}
+
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = tf32_rna(x);
+  lo = tf32_rna(x - __uint_as_float(hi));
+}
+
+template <int NV>
+__device__ __forceinline__ void butterfly_flush(float (&v)[NV], int lane, double* slot, int nused, double weight) {
+  // reduce-scatter across the warp: after 5 halvings lane l holds NV/32 sums
+  int base = 0;
+#pragma unroll
+  for (int o = 16, cnt = NV; o > 0; o >>= 1, cnt >>= 1) {
+    const int half = cnt / 2;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < half; ++k) {
+      const float send = up ? v[k] : v[k + half];
+      const float keep = up ? v[k + half] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    if (up) base += half;
+  }
+#pragma unroll
+  for (int k = 0; k < NV / 32; ++k) {
+    const int idx = base + k;
+    if (idx < nused) slot[idx] += static_cast<double>(v[k]) * weight;
+  }
+}
+
+template <int DP4, bool NARROW>
+__global__ void __maxnreg__(200) grad_tc_kernel(const GradTcArgs a) {
+  constexpr int DP = 4 * DP4;
+  constexpr int NPR = NARROW ? 2 : 1;
+  constexpr int NUSED = NPR * (DP + 1);
+  constexpr int NV = NUSED <= 32 ? 32 : (NUSED <= 64 ? 64 : 128);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int KP = a.kp;
+  const int img = CN * KP;  // floats per TF32 image of a chunk
+  float* smB = reinterpret_cast<float*>(smem_raw);  // [STAGES][2 * img]
+  float* smX = smB + STAGES * 2 * img;               // [STAGES][CN][DP]
+  float* smW = smX + STAGES * CN * DP;               // [STAGES][CN]
+  double* wacc = reinterpret_cast<double*>(smW + STAGES * CN);  // [EVAL_WARPS][NV]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wacc + EVAL_WARPS * NV);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* d_full = bars + 2 * STAGES;
+  uint64_t* d_empty = d_full + 2;
+  uint64_t* a_full = d_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = (a.n + TBM - 1) / TBM;
+  const long long ntiles = a.symmetric ? static_cast<long long>(T) * (T + 1) / 2 : static_cast<long long>(T) * T;
+  const long long tb = a.tile_end >= 0 ? a.tile_begin : 0;
+  const long long te = a.tile_end >= 0 ? min(a.tile_end, ntiles) : ntiles;
+  const long long per = (te - tb + gridDim.x - 1) / gridDim.x;
+  const long long L0 = tb + blockIdx.x * per;
+  const long long L1 = min(te, L0 + per);
+  const int nq = L1 > L0 ? static_cast<int>(2 * (L1 - L0)) : 0;
+
+  for (int e = tid; e < EVAL_WARPS * NV; e += NTHREADS) wacc[e] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + EVAL_WARPS);  // MMA commit + every eval warp (x_c, w reads)
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&d_full[b], 1);
+      mbar_init(&d_empty[b], EVAL_WARPS);
+    }
+    mbar_init(a_full, EVAL_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint32_t bbytes = 2u * img * 4u, xbytes = CN * DP * 4u, wbytes = NARROW ? CN * 4u : 0u;
+      for (int k = 0; k < nq; ++k) {
+        const int s = k % STAGES;
+        if (k >= STAGES) mbar_wait(&empty[s], ((k - STAGES) / STAGES) & 1);
+        int ti, tcol;
+        tile_coords_tc(L0 + k / 2, T, a.symmetric, ti, tcol);
+        const int col0 = tcol * TBM + (k & 1) * CN;
+        mbar_expect_tx(&full[s], bbytes + xbytes + wbytes);
+        bulk_g2s(smB + s * 2 * img, a.bpk + static_cast<size_t>(col0 / CN) * 2 * img, bbytes, &full[s]);
+        bulk_g2s(smX + s * CN * DP, a.xs + static_cast<size_t>(col0) * DP, xbytes, &full[s]);
+        if (NARROW) bulk_g2s(smW + s * CN, a.w1 + col0, wbytes, &full[s]);
+      }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc(CN, TBM);
+      const uint32_t sbo = static_cast<uint32_t>(KP / 4) * 128u;
+      int prev_ti = -1, rows_loaded = 0;
+      for (int k = 0; k < nq; ++k) {
+        const int s = k % STAGES, b = k & 1;
+        int ti, tcol;
+        tile_coords_tc(L0 + k / 2, T, a.symmetric, ti, tcol);
+        if (ti != prev_ti) {  // new A rows in TMEM
+          mbar_wait(a_full, rows_loaded & 1);
+          ++rows_loaded;
+          prev_ti = ti;
+        }
+        mbar_wait(&full[s], (k / STAGES) & 1);
+        if (k >= 2) mbar_wait(&d_empty[b], ((k - 2) / 2) & 1);
+        tc_fence_after();
+        const uint32_t bh = smem_u32(smB + s * 2 * img);
+        const uint32_t bl = bh + img * 4;
+        const uint32_t dt = tmem + b * CN;
+        const uint32_t ah = tmem + A_BASE, al = ah + KP;
+        for (int kk = 0; kk < KP / 8; ++kk) {
+          const uint64_t dh = umma_desc(bh + kk * 256, 128, sbo);
+          const uint64_t dl = umma_desc(bl + kk * 256, 128, sbo);
+          tc_mma_tf32(dt, ah + kk * 8, dh, idesc, kk == 0 ? 0u : 1u);
+          tc_mma_tf32(dt, ah + kk * 8, dl, idesc, 1u);
+          tc_mma_tf32(dt, al + kk * 8, dh, idesc, 1u);
+        }
+        tc_commit(&empty[s]);
+        tc_commit(&d_full[b]);
+      }
+    }
+  } else {
+    // ---------------- A writers + evaluation ----------------
+    const int lg = warp & 3, half = warp >> 2;
+    const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
+    uint64_t xi2[2 * DP4];
+    float u1i = 0.f;
+    uint64_t lw[DP / 2], ln[NARROW ? DP / 2 : 1];
+    float sw = 0.f, sn = 0.f;
+#pragma unroll
+    for (int k = 0; k < DP / 2; ++k) lw[k] = 0ull;
+#pragma unroll
+    for (int k = 0; k < (NARROW ? DP / 2 : 1); ++k) ln[k] = 0ull;
+    int prev_ti = -1;
+    for (int k = 0; k < nq; ++k) {
+      const int s = k % STAGES, b = k & 1;
+      int ti, tcol;
+      tile_coords_tc(L0 + k / 2, T, a.symmetric, ti, tcol);
+      if (ti != prev_ti) {
+        // the previous chunk's D was consumed, so every MMA reading the old A is done
+        prev_ti = ti;
+        const int i = ti * TBM + lg * 32 + lane;  // < T * 128: xs / u1 are padded to that
+        const bool row_ok = i < a.n;
+        const float* urow = a.ua + static_cast<size_t>(row_ok ? i : 0) * a.lda;
+        for (int q = 0; q < KP / 16; ++q) {
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int col = half * (KP / 2) + q * 8 + e;
+            const float x = (row_ok && col < a.cols) ? __ldg(urow + col) : 0.f;
+            split_tf32(x, hi[e], lo[e]);
+          }
+          const uint32_t at = tmem + lane_addr + A_BASE + half * (KP / 2) + q * 8;
+          tc_st8(at, hi);
+          tc_st8(at + KP, lo);
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full);
+#pragma unroll
+        for (int u = 0; u < DP4; ++u) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(i) * DP) + u);
+          asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(v.x), "f"(v.y));
+          asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(v.z), "f"(v.w));
+        }
+        if (NARROW) u1i = __ldg(a.u1 + i);
+      }
+      mbar_wait(&full[s], (k / STAGES) & 1);
+      mbar_wait(&d_full[b], (k / 2) & 1);
+      tc_fence_after();
+      const uint32_t xbase = smem_u32(smX + s * CN * DP + half * 32 * DP);
+      const float* wc = smW + s * CN + half * 32;
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        uint32_t g[8];
+        tc_ld8(tmem + lane_addr + b * CN + half * 32 + q * 8, g);
+        tc_wait_ld();
+        if (q == 3) {  // D buffer fully read: let the next-but-one chunk's MMAs in
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[b]);
+        }
+#pragma unroll 2
+        for (int e = 0; e < 8; ++e) {
+          const int c = q * 8 + e;
+          uint64_t sq[DP / 2];
+          uint64_t r2a = 0ull, r2b = 0ull;
+#pragma unroll
+          for (int u = 0; u < DP4; ++u) {
+            uint64_t c01, c23, d01, d23;
+            asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(c01), "=l"(c23) : "r"(xbase + (c * DP + 4 * u) * 4));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(c01), "l"(xi2[2 * u]));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(c23), "l"(xi2[2 * u + 1]));
+            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(sq[2 * u]) : "l"(d01));
+            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(sq[2 * u + 1]) : "l"(d23));
+            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(r2a) : "l"(sq[2 * u]));
+            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(r2b) : "l"(sq[2 * u + 1]));
+          }
+          uint64_t r2s;
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r2s) : "l"(r2a), "l"(r2b));
+          float q0, q1;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(q0), "=f"(q1) : "l"(r2s));
+          const float r = sqrt_approx(q0 + q1);
+          const float e0 = ex2_approx(r * kNegSqrt3Log2e);  // exp(-sqrt3 r)
+          const float kv = fmaf(r, kSqrt3f, 1.f) * e0;      // k / s^2
+          const float gw = __uint_as_float(g[e]);
+          sw = fmaf(kv, gw, sw);
+          uint64_t cw2;
+          const float cw = e0 * gw;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(cw2) : "f"(cw));
+#pragma unroll
+          for (int t = 0; t < DP / 2; ++t) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(lw[t]) : "l"(sq[t]), "l"(cw2));
+          if (NARROW) {
+            const float gn = u1i * wc[c];
+            sn = fmaf(kv, gn, sn);
+            uint64_t cn2;
+            const float cnv = e0 * gn;
+            asm("mov.b64 %0, {%1, %1};" : "=l"(cn2) : "f"(cnv));
+#pragma unroll
+            for (int t = 0; t < (NARROW ? DP / 2 : 1); ++t)
+              asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(ln[t]) : "l"(sq[t]), "l"(cn2));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // x_c / w reads of this stage done
+      if (k & 1) {  // tile complete: flush its FP32 sums into the warp's FP64 slots
+        float v[NV];
+#pragma unroll
+        for (int t = 0; t < NV; ++t) v[t] = 0.f;
+#pragma unroll
+        for (int t = 0; t < DP / 2; ++t) {
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2 * t]), "=f"(v[2 * t + 1]) : "l"(lw[t]));
+          lw[t] = 0ull;
+        }
+        v[DP] = sw;
+        sw = 0.f;
+        if (NARROW) {
+#pragma unroll
+          for (int t = 0; t < (NARROW ? DP / 2 : 1); ++t) {
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(v[DP + 1 + 2 * t]), "=f"(v[DP + 2 + 2 * t]) : "l"(ln[t]));
+            ln[t] = 0ull;
+          }
+          v[2 * DP + 1] = sn;
+          sn = 0.f;
+        }
+        const double weight = (a.symmetric && tcol != ti) ? 2.0 : 1.0;
+        butterfly_flush<NV>(v, lane, wacc + warp * NV, NUSED, weight);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+  }
+  // block result in the caller's pair order: fixed-order sum over warps
+  const int d = a.d, per_pair = d + 1;
+  for (int e = tid; e < NPR * per_pair; e += NTHREADS) {
+    const int p = e / per_pair, k = e % per_pair;
+    const int slot = p * (DP + 1) + (k == d ? DP : k);
+    double acc = 0.0;
+    for (int w = 0; w < EVAL_WARPS; ++w) acc += wacc[w * NV + slot];
+    const int po = p == 0 ? a.pw : a.pn;
+    a.part[static_cast<size_t>(blockIdx.x) * a.npairs * per_pair + po * per_pair + k] = acc;
+  }
+}
+
+// W (rows x cols, FP32, ld) -> per-64-row-chunk TF32 hi | lo images in the
+// canonical K-major no-swizzle layout: element (r, k) of chunk r / 64 at
+// ((r%64/8) * (KP/4) + k/4) * 32 + (r%8) * 4 + k%4 of each image. Rows >= n
+// and columns >= cols are zero. Narrow-pair vectors go to contiguous arrays.
+__global__ void grad_tc_pack_kernel(const float* w32, int ld, int n, int cols, int kp, int rows_pad, float* bpk,
+                                    const float* n_u, const float* n_w, int n_ld, float* u1, float* w1) {
+  const long long total = static_cast<long long>(rows_pad) * kp;
+  const int img = CN * kp;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / kp), k = static_cast<int>(e % kp);
+    const float x = (r < n && k < cols) ? w32[static_cast<size_t>(r) * ld + k] : 0.f;
+    uint32_t hi, lo;
+    split_tf32(x, hi, lo);
+    const int q = r / CN, rr = r % CN;
+    float* base = bpk + static_cast<size_t>(q) * 2 * img;
+    const int off = ((rr / 8) * (kp / 4) + k / 4) * 32 + (rr % 8) * 4 + (k % 4);
+    base[off] = __uint_as_float(hi);
+    base[img + off] = __uint_as_float(lo);
+    if (k == 0 && u1) {
+      u1[r] = r < n ? n_u[static_cast<size_t>(r) * n_ld] : 0.f;
+      w1[r] = r < n ? n_w[static_cast<size_t>(r) * n_ld] : 0.f;
+    }
+  }
+}
+
+template <int DP4, bool NARROW>
+void launch_one(const GradTcArgs& a, cudaStream_t s) {
+  constexpr int DP = 4 * DP4;
+  constexpr int NPR = NARROW ? 2 : 1;
+  constexpr int NUSED = NPR * (DP + 1);
+  constexpr int NV = NUSED <= 32 ? 32 : (NUSED <= 64 ? 64 : 128);
+  const size_t smem = sizeof(float) * (STAGES * 2 * CN * a.kp + STAGES * CN * DP + STAGES * CN) +
+                      sizeof(double) * EVAL_WARPS * NV + 16 * sizeof(uint64_t);
+  static size_t configured = 0;
+  if (smem > configured) {
+    GPK_CUDA(cudaFuncSetAttribute(grad_tc_kernel<DP4, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  grad_tc_kernel<DP4, NARROW><<<a.blocks, NTHREADS, smem, s>>>(a);
+  check_launch("grad_tc_kernel");
+}
+
+template <int DP4>
+void launch_dp(const GradTcArgs& a, cudaStream_t s) {
+  if (a.u1)
+    launch_one<DP4, true>(a, s);
+  else
+    launch_one<DP4, false>(a, s);
+}
+
+}  // namespace
+
+int grad_tc_kp(int cols) { return (cols + 15) / 16 * 16; }
+int grad_tc_rows_pad(int n) { return (n + TBM - 1) / TBM * TBM; }
+long long grad_tc_tiles(int n, int symmetric) {
+  const long long T = (n + TBM - 1) / TBM;
+  return symmetric ? T * (T + 1) / 2 : T * T;
+}
+
+void grad_tc_pack_launch(const float* w32, int ld, int n, int cols, int kp, float* bpk, const float* n_u,
+                         const float* n_w, int n_ld, float* u1, float* w1, cudaStream_t s) {
+  const int rows_pad = grad_tc_rows_pad(n);
+  const long long total = static_cast<long long>(rows_pad) * kp;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  grad_tc_pack_kernel<<<blocks, 256, 0, s>>>(w32, ld, n, cols, kp, rows_pad, bpk, n_u, n_w, n_ld, u1, w1);
+  check_launch("grad_tc_pack");
+}
+
+void grad_tc_launch(const GradTcArgs& a, cudaStream_t s) {
+  if (a.kp < 16 || a.kp > 64 || a.kp % 16) throw std::invalid_argument("gpk: tensor-core grad pass needs 1 < s <= 64");
+  switch (a.dp / 4) {
+    case 1: return launch_dp<1>(a, s);
+    case 2: return launch_dp<2>(a, s);
+    case 3: return launch_dp<3>(a, s);
+    case 4: return launch_dp<4>(a, s);
+    case 5: return launch_dp<5>(a, s);
+    case 6: return launch_dp<6>(a, s);
+    case 7: return launch_dp<7>(a, s);
+    case 8: return launch_dp<8>(a, s);
+    default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
+  }
+}
+
+}  // namespace gpk

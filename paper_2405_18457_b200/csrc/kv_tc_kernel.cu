@@ -27,6 +27,7 @@
 #include <algorithm>
 
 #include "gpk_internal.cuh"
+#include "tc_util.cuh"
 
 namespace gpk {
 
@@ -44,100 +45,7 @@ constexpr int A_BASE = 128;  // TMEM column of the first A buffer (D uses [0, NP
 #define GPK_EVAL_F32X2 1  // packed FP32x2 distance loop (FADD2/FFMA2)
 #endif
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                            uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-}
-__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-               : "r"(taddr)
-               : "memory");
-}
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float y;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-constexpr float kNegSqrt3Log2e = -2.4988211106473432f;  // -sqrt(3) * log2(e)
-constexpr float kSqrt3f = 1.7320508075688772f;
-
-// Canonical no-swizzle K-major UMMA smem descriptor (version 1 = tcgen05):
-// core matrices of 8 rows x 16 B; LBO = K-adjacent core-matrix stride,
-// SBO = 8-row-group stride (both in bytes).
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // version
-  return d;                             // base offset 0, lbo mode 0, SWIZZLE_NONE (0)
-}
-
-// kind::tf32 instruction descriptor: D F32, A/B TF32, both K-major, M=128.
-constexpr uint32_t tf32_idesc(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(TBM >> 4) << 24);
-}
+using namespace tc;
 
 template <int NPAD>
 struct TcLayout {
@@ -223,7 +131,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
   } else if (warp == 9) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = tf32_idesc(NPAD);
+      constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
       for (int k = 0; k < nq; ++k) {
         const int s = k % STAGES, b = k & 1;
         const int g = k / flush;
@@ -382,11 +290,15 @@ __global__ void kv_pack_kernel(const double* v64, const float* v32, int ldv, int
   if (sel) rows = min(sel_block, n - *sel * sel_block);
   const long long total = static_cast<long long>(nchunks) * TBK * npad;
   const int img = npad * TBK;
+  // e walks the images linearly (coalesced stores): e % img = core * 32 + lane,
+  // core = (j/8) * (TBK/4) + kk/4, lane = (j%8) * 4 + kk%4
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(e % npad);
-    const long long c = e / npad;
-    const int q = static_cast<int>(c / TBK), kk = static_cast<int>(c % TBK);
+    const int q = static_cast<int>(e / img), w = static_cast<int>(e % img);
+    const int core = w >> 5, ln = w & 31;
+    const int j = (core / (TBK / 4)) * 8 + (ln >> 2);
+    const int kk = (core % (TBK / 4)) * 4 + (ln & 3);
+    const long long c = static_cast<long long>(q) * TBK + kk;
     float hi = 0.f, lo = 0.f;
     if (c < rows && j < m) {
       if (v64) {
@@ -402,9 +314,8 @@ __global__ void kv_pack_kernel(const double* v64, const float* v32, int ldv, int
       }
     }
     const size_t base = static_cast<size_t>(q) * 2 * img;
-    const int off = ((j / 8) * (TBK / 4) + kk / 4) * 32 + (j % 8) * 4 + (kk % 4);
-    vpk[base + off] = hi;
-    vpk[base + img + off] = lo;
+    vpk[base + w] = hi;
+    vpk[base + img + w] = lo;
   }
 }
 

@@ -773,7 +773,11 @@ __global__ void ap_apply_pack_kernel(const double* upd64, int n, int m, int bloc
   const long long total = static_cast<long long>(rows_pad) * npad;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int i = static_cast<int>(e / npad), j = static_cast<int>(e % npad);
+    // e walks the 32-row TF32 images linearly (coalesced stores), see kv_pack_kernel
+    const int q32 = static_cast<int>(e / img), w = static_cast<int>(e % img);
+    const int core = w >> 5, ln = w & 31;
+    const int j = (core >> 3) * 8 + (ln >> 2);
+    const int i = q32 * 32 + (core & 7) * 4 + (ln & 3);
     double x = 0.0;
     if (i < len && j < m) {
       x = upd64[static_cast<size_t>(i) * m + j];
@@ -783,11 +787,9 @@ __global__ void ap_apply_pack_kernel(const double* upd64, int n, int m, int bloc
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(static_cast<float>(x)));
     const float h = __uint_as_float(hb);
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(static_cast<float>(x - static_cast<double>(h))));
-    const int kk = i % 32;
-    float* base = vpk + static_cast<size_t>(i / 32) * 2 * img;
-    const int off = ((j / 8) * 8 + kk / 4) * 32 + (j % 8) * 4 + (kk % 4);
-    base[off] = h;
-    base[img + off] = __uint_as_float(lb);
+    float* base = vpk + static_cast<size_t>(q32) * 2 * img;
+    base[w] = h;
+    base[img + w] = __uint_as_float(lb);
   }
 }
 void ap_apply_pack_launch(const double* upd64, int n, int m, int block, const int* sel, double* V, float* vpk,
@@ -1066,6 +1068,7 @@ __global__ void sgd_check_sharded_kernel(const double* gbuf, int nr, long long s
     for (int r = 0; r < nr; ++r) f += gbuf[r * stride + bm + m];
     bad = f != 0.0;
   }
+  __syncthreads();
   for (int j = warp; j < m; j += nw) {
     double acc = 0.0;
     for (int q = lane; q < b; q += 32) {
@@ -1074,6 +1077,9 @@ __global__ void sgd_check_sharded_kernel(const double* gbuf, int nr, long long s
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
+      // a non-finite gradient makes this iteration's update non-finite
+      // (solvers.cpp:168-171 tests the iterate right after it)
+      if (!isfinite(acc)) bad = 1;
       double old = 0.0;
       for (int r = 0; r < nr; ++r) old += gbuf[r * stride + bm + j];
       const double v = sumsq[j] + (acc - old);
@@ -1113,7 +1119,11 @@ __global__ void sgd_update_pack_kernel(double* M, double* V, double* R, float* v
   int bad = 0;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int i = static_cast<int>(e / npad), j = static_cast<int>(e % npad);
+    // e walks the 32-row TF32 images linearly (coalesced stores), see kv_pack_kernel
+    const int q32 = static_cast<int>(e / img), w = static_cast<int>(e % img);
+    const int core = w >> 5, ln = w & 31;
+    const int j = (core >> 3) * 8 + (ln >> 2);
+    const int i = q32 * 32 + (core & 7) * 4 + (ln & 3);
     double v = 0.0;
     if (i < nloc && j < m) {
       const size_t o = static_cast<size_t>(i) * m + j;
@@ -1133,11 +1143,9 @@ __global__ void sgd_update_pack_kernel(double* M, double* V, double* R, float* v
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(static_cast<float>(v)));
     const float h = __uint_as_float(hb);
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(static_cast<float>(v - static_cast<double>(h))));
-    const int kk = i % 32;
-    float* base = vpk + static_cast<size_t>(i / 32) * 2 * img;
-    const int off = ((j / 8) * 8 + kk / 4) * 32 + (j % 8) * 4 + (kk % 4);
-    base[off] = h;
-    base[img + off] = __uint_as_float(lb);
+    float* base = vpk + static_cast<size_t>(q32) * 2 * img;
+    base[w] = h;
+    base[img + w] = __uint_as_float(lb);
   }
   if (bad) atomicOr(nonfinite, 1);
 }

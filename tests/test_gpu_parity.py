@@ -117,14 +117,17 @@ def test_dense_block_and_kernel_column_fp64(G, gpk_ctx, oracle):
     assert np.all(op.kernel_diagonal() == s2)
 
 
-@pytest.mark.parametrize("n,d,s", [(500, 2, 8), (1200, 20, 64), (2048, 26, 64), (700, 3, 16)])
-def test_quadratic_forms_match_oracle(G, gpk_ctx, oracle, n, d, s):
+@pytest.mark.parametrize("n,d,s", [(500, 2, 8), (1200, 20, 64), (2048, 26, 64), (700, 3, 16), (300, 3, 80),
+                                   (129, 5, 2)])
+def test_quadratic_forms_match_oracle(G, kctx, oracle, n, d, s):
+    """tcgen05 context: G = Z Z^T on the tensor cores (grad_tc_kernel, s <= 64;
+    s = 80 takes the SIMT pass); simt context: grad_kernel throughout."""
     X, _ = gp_problem(n, d, 4 * n)
     raw = default_test_raw(d, oracle)
     rng = np.random.default_rng(n)
     vy = rng.standard_normal(n)
     Z = rng.standard_normal((n, s))
-    op = make_op(G, gpk_ctx, X, raw)
+    op = make_op(G, kctx, X, raw)
     g = G.estimate_gradient_pathwise(op, vy, Z)
     r = oracle.gradient(X, raw, vy, Z, threads=8)
     for key in ("quadratic_term", "trace_term"):

@@ -66,5 +66,8 @@ def test_gpu_posterior_matches_oracle(gpk_ctx, oracle):
     rm = oracle.posterior(P, X, raw, vy, Z, prior=prior, test_targets=t, target_scale=1.7, threads=8)
     for k in ("rmse", "rmse_raw", "llh", "llh_raw"):
         assert abs(gm[k] - rm[k]) <= 1e-4 * abs(rm[k]), k
+    # no prior, zero probe solutions: every sample is the posterior mean (the
+    # wider right-hand side runs a different kernel instance: FP32 rounding)
     gz = G.sample_posterior(op, None, P[:3], vy, np.zeros((n, 3)))
-    assert np.max(np.abs(gz[:, 1] - got[:3])) <= 1e-12 * np.max(np.abs(got))
+    assert np.max(np.abs(gz[:, 1] - got[:3])) <= 2e-5 * np.max(np.abs(got))
+    assert np.array_equal(gz[:, 0], gz[:, 1]) and np.array_equal(gz[:, 1], gz[:, 2])
