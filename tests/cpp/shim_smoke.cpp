@@ -57,6 +57,9 @@ int main() {
       const GradientEstimate g = estimate_gradient_pathwise(op, vy, z);
       std::printf(", \"grad\": [");
       for (int k = 0; k < d + 2; ++k) std::printf("%s%.17g", k ? ", " : "", g.values[k]);
+      std::printf("], \"cg_solutions\": [");
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j <= s; ++j) std::printf("%s%.17g", (i || j) ? ", " : "", sol(i, j));
       std::printf("]");
     }
   }
