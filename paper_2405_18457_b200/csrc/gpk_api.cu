@@ -91,6 +91,7 @@ struct gpk_ctx {
   int kernel = 1;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32 (default)
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
+  DBuf<double> rff_feat;  // RFF feature rows (prior GEMM), reused across calls
   int* info_host = nullptr;    // pinned
   ncclComm_t comm = nullptr;   // multi-GPU (one process per GPU)
   int nranks = 1, rank = 0;
@@ -814,11 +815,6 @@ void spd_inverse_batched(gpk_ctx* ctx, double* mats, int dim, int batch, double*
   count_launch(2);
 }
 
-__global__ void pad_identity_kernel(double* blk, int block, int len) {
-  for (int i = len + blockIdx.x * blockDim.x + threadIdx.x; i < block; i += gridDim.x * blockDim.x)
-    blk[static_cast<size_t>(i) * block + i] = 1.0;
-}
-
 void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) {
   validate(c);
   const auto start = Clock::now();
@@ -838,14 +834,7 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   double* mats = b->w1.ensure(bb * nblocks);
   double* inv = b->blocks.ensure(bb * nblocks);
   GPK_CUDA(cudaMemsetAsync(mats, 0, sizeof(double) * bb * nblocks, s));
-  for (int k = 0; k < nblocks; ++k) {
-    const int r0 = k * block, len = std::min(block, n - r0);
-    dense_block64_launch(op->xs64.p, n, op->d, op->s2, op->sigma2, r0, len, r0, len, mats + k * bb, block, 1, s);
-    if (len < block) {
-      pad_identity_kernel<<<1, 256, 0, s>>>(mats + k * bb, block, len);
-      check_launch("pad_identity");
-    }
-  }
+  ap_blocks_launch(op->xs64.p, n, op->d, op->s2, op->sigma2, block, nblocks, mats, s);
   spd_inverse_batched(ctx, mats, block, nblocks, inv);
   std::vector<double> inv_scales(m);
   for (int j = 0; j < m; ++j) inv_scales[j] = 1.0 / b->scales[j];
@@ -1384,6 +1373,28 @@ void build_basis_host(gpk_rff_basis* b) {  // rff.cpp:10-34
   for (auto& w : b->weights) w = gauss(ws);
 }
 
+// prior (row-major [rows][s]) = F W: FP64 feature rows (rff_features_kernel)
+// in chunks of <= 512 MB, contracted with the weights by cuBLAS DGEMM
+// (prior^T = W^T F^T in column-major terms; W is stored [samples][2P]).
+void rff_prior_gemm(gpk_ctx* ctx, const double* x64, int rows, int d, const double* fd, int P, const double* W,
+                    int s_count, double amplitude, double* prior) {
+  cudaStream_t s = ctx->stream;
+  const int F = 2 * P;
+  const long long chunk = std::max<long long>(1, std::min<long long>(rows, (512LL << 20) / (8LL * F)));
+  double* feat = ctx->rff_feat.ensure(static_cast<size_t>(chunk) * F);
+  if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+  for (long long r0 = 0; r0 < rows; r0 += chunk) {
+    const int len = static_cast<int>(std::min<long long>(chunk, rows - r0));
+    rff_features_launch(x64 + r0 * d, len, d, fd, P, amplitude, feat, s);
+    count_launch();
+    const double one = 1.0, zero = 0.0;
+    if (cublasDgemm(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, s_count, len, F, &one, W, F, feat, F, &zero,
+                    prior + r0 * s_count, s_count) != CUBLAS_STATUS_SUCCESS)
+      throw CudaError("cublasDgemm (RFF prior)");
+    count_launch();
+  }
+}
+
 // prior (row-major [n][s]) at the operator's inputs; freq divided by current l.
 void rff_prior_dev(gpk_operator* op, gpk_rff_basis* b, int s_count, double* prior) {
   cudaStream_t s = op->ctx->stream;
@@ -1400,8 +1411,8 @@ void rff_prior_dev(gpk_operator* op, gpk_rff_basis* b, int s_count, double* prio
   }
   const double amplitude = op->s / std::sqrt(static_cast<double>(P));  // rff.cpp:47
   // this rank's rows only (all rows on one GPU)
-  rff_prior_launch(op->x64.p + static_cast<size_t>(op->row0) * d, op->nloc, d, fd, P, b->w_dev.p, 2 * P, s_count,
-                   amplitude, prior, s);
+  rff_prior_gemm(op->ctx, op->x64.p + static_cast<size_t>(op->row0) * d, op->nloc, d, fd, P, b->w_dev.p, s_count,
+                 amplitude, prior);
   GPK_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1451,7 +1462,7 @@ void prior_at_points(gpk_operator* op, gpk_rff_basis* b, int p, int s_count, dou
                              cudaMemcpyHostToDevice, s));
   }
   const double amplitude = op->s / std::sqrt(static_cast<double>(P));
-  rff_prior_launch(op->pts64.p, p, d, fd, P, b->w_dev.p, 2 * P, s_count, amplitude, prior, s);
+  rff_prior_gemm(op->ctx, op->pts64.p, p, d, fd, P, b->w_dev.p, s_count, amplitude, prior);
   GPK_CUDA(cudaStreamSynchronize(s));
 }
 

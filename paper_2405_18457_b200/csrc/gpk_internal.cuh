@@ -222,6 +222,8 @@ void dense_block64_launch(const double* xs64, int n, int d, double s2, double si
                           int rows, int c0, int cols, double* out, int ldo, int add_noise,
                           cudaStream_t s);  // out row-major [rows][ldo]
 
+void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks, double* mats,
+                      cudaStream_t s);
 void set_identity_launch(double* mats, int dim, int batch, cudaStream_t s);
 
 // AP (K8)
@@ -280,6 +282,8 @@ void sgd_update_pack_launch(double* M, double* V, double* R, float* vpk, int npa
 void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, const int* skip, cudaStream_t s);
 
 // RFF (K5) + noise (K9)
+void rff_features_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude, double* F,
+                         cudaStream_t s);
 void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs,
                       const double* weights, int ldw, int s, double amplitude, double* prior,
                       cudaStream_t s_);  // prior row-major [n][s]

@@ -89,7 +89,7 @@ __device__ __forceinline__ void butterfly_flush(float (&v)[NV], int lane, double
 }
 
 template <int DP4, bool NARROW>
-__global__ void __maxnreg__(192) grad_tc_kernel(const GradTcArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a) {
   constexpr int DP = 4 * DP4;
   constexpr int NPR = NARROW ? 2 : 1;
   constexpr int NUSED = NPR * (DP + 1);

@@ -528,6 +528,35 @@ void dense_block64_launch(const double* xs64, int n, int d, double s2, double si
   check_launch("dense_block64");
 }
 
+// All AP diagonal blocks H[blk_k, blk_k] (block x block, FP64) in one launch;
+// the last block's rows/columns beyond n are identity padding.
+__global__ void ap_blocks_kernel(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks,
+                                 double* mats) {
+  const long long bb = static_cast<long long>(block) * block;
+  const long long total = bb * nblocks;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(e / bb);
+    const long long w = e % bb;
+    const int r = static_cast<int>(w / block), c = static_cast<int>(w % block);
+    const int r0 = k * block, len = min(block, n - r0);
+    double v;
+    if (r < len && c < len) {
+      v = matern64(xs64, d, r0 + r, r0 + c, s2);
+      if (r == c) v += sigma2;
+    } else {
+      v = r == c ? 1.0 : 0.0;
+    }
+    mats[e] = v;
+  }
+}
+void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks, double* mats,
+                      cudaStream_t s) {
+  const long long total = static_cast<long long>(block) * block * nblocks;
+  ap_blocks_kernel<<<blocks_for(total, 256), 256, 0, s>>>(xs64, n, d, s2, sigma2, block, nblocks, mats);
+  check_launch("ap_blocks");
+}
+
 __global__ void set_identity_kernel(double* mats, int dim, long long total) {
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -1223,6 +1252,31 @@ __global__ void rff_prior_kernel(const double* x64, int n, int d, const double* 
     }
   }
 }
+// Feature rows for the GEMM form of the prior: F[i][2p] = amp cos(theta_ip),
+// F[i][2p+1] = amp sin(theta_ip), theta_ip = x_i . (Omega_p / l) in FP64
+// (rff.cpp:36-54); one thread per (i, p), consecutive p -> coalesced rows.
+__global__ void rff_features_kernel(const double* x64, int n, int d, const double* freq, int pairs, double amplitude,
+                                    double* F) {
+  const long long total = static_cast<long long>(n) * pairs;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / pairs;
+    const int p = static_cast<int>(e % pairs);
+    double ang = 0.0;
+    for (int k = 0; k < d; ++k) ang += x64[i * d + k] * freq[static_cast<size_t>(p) * d + k];
+    double sn, c;
+    sincos(ang, &sn, &c);
+    F[i * 2 * pairs + 2 * p] = amplitude * c;
+    F[i * 2 * pairs + 2 * p + 1] = amplitude * sn;
+  }
+}
+void rff_features_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude, double* F,
+                         cudaStream_t s) {
+  rff_features_kernel<<<blocks_for(static_cast<long long>(n) * pairs, 256), 256, 0, s>>>(x64, n, d, freq, pairs,
+                                                                                      amplitude, F);
+  check_launch("rff_features");
+}
+
 void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs, const double* weights, int ldw,
                       int s, double amplitude, double* prior, cudaStream_t st) {
   dim3 grid((n + 63) / 64, (s + 63) / 64);
