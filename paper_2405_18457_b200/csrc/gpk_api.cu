@@ -1273,7 +1273,7 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
     t.cols = a.mcols[pw];
     t.kp = grad_tc_kp(t.cols);
     const int rows_pad = grad_tc_rows_pad(n);
-    float* bpk = op->gpk_b.ensure(static_cast<size_t>(rows_pad) * 2 * t.kp);
+    float* bpk = op->gpk_b.ensure(grad_tc_pack_floats(n, t.kp));
     float* nar = pn >= 0 ? op->gpk_n.ensure(static_cast<size_t>(2) * rows_pad) : nullptr;
     grad_tc_pack_launch(a.w[pw], a.ldu[pw], n, t.cols, t.kp, bpk, pn >= 0 ? a.u[pn] : nullptr,
                         pn >= 0 ? a.w[pn] : nullptr, pn >= 0 ? a.ldu[pn] : 0, nar, nar ? nar + rows_pad : nullptr, s);

@@ -158,6 +158,7 @@ struct GradTcArgs {
 };
 int grad_tc_kp(int cols);
 int grad_tc_rows_pad(int n);
+size_t grad_tc_pack_floats(int n, int kp);
 long long grad_tc_tiles(int n, int symmetric);
 void grad_tc_pack_launch(const float* w32, int ld, int n, int cols, int kp, float* bpk, const float* n_u,
                          const float* n_w, int n_ld, float* u1, float* w1, cudaStream_t s);

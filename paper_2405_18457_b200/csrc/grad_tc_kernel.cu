@@ -18,9 +18,16 @@
 //              scattered across the warp (butterfly) into FP64 per-warp slots.
 //   warp 8     producer: cp.async.bulk of the chunk's pre-packed W images,
 //              x_c rows and narrow-pair w values into a 3-stage ring.
-//   warp 9     one thread issues 3 x KP/8 tcgen05.mma.kind::tf32 (M=128,
+//   warp 9     one thread issues 6 x KP/8 tcgen05.mma.kind::tf32 (M=128,
 //              N=64, A from TMEM, B from smem) per chunk into one of two TMEM
 //              D buffers; tcgen05.commit releases the stage and the buffer.
+// Operands are split exactly into three TF32 pieces, x = hi + mid + lo
+// (hi, mid: 11 significant bits by truncation; lo: the <= 3 remaining bits),
+// and G takes the six products down to 2^-22 relative (hi.hi, hi.mid, mid.hi,
+// mid.mid, hi.lo, lo.hi): FP32-grade G, as the SIMT pass. G = Z Z^T sums
+// terms of both signs and the trace forms are sensitive to it; the two-piece
+// 3xTF32 split used by the K.V operator (whose kernel values are positive)
+// measured ~10x worse here.
 // Deterministic: fixed tile ranges, fixed butterfly, fixed warp order.
 #include <cuda_runtime.h>
 
@@ -41,8 +48,9 @@ constexpr int CN = 64;    // columns per chunk == MMA N
 constexpr int STAGES = 3;
 constexpr int NTHREADS = 320;
 constexpr int EVAL_WARPS = 8;
-constexpr int TMEM_COLS = 256;
-constexpr int A_BASE = 2 * CN;  // D buffers at TMEM columns [0, 64) and [64, 128)
+constexpr int TMEM_COLS = 512;  // one CTA per SM
+constexpr int A_BASE = 2 * CN;  // D buffers at TMEM columns [0, 64) and [64, 128); A pieces from 128
+constexpr int NPIECE = 3;
 
 __device__ __forceinline__ void tile_coords_tc(long long L, int T, int symmetric, int& ti, int& tc) {
   if (!symmetric) {
@@ -60,9 +68,12 @@ __device__ __forceinline__ void tile_coords_tc(long long L, int T, int symmetric
   tc = r + static_cast<int>(L - off(r));
 }
 
-__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  hi = tf32_rna(x);
-  lo = tf32_rna(x - __uint_as_float(hi));
+// exact three-piece TF32 split: x == hi + mid + lo in FP32 arithmetic
+__device__ __forceinline__ void split3_tf32(float x, uint32_t& hi, uint32_t& mid, uint32_t& lo) {
+  hi = __float_as_uint(x) & 0xFFFFE000u;
+  const float r1 = x - __uint_as_float(hi);
+  mid = __float_as_uint(r1) & 0xFFFFE000u;
+  lo = __float_as_uint(r1 - __uint_as_float(mid));
 }
 
 template <int NV>
@@ -97,8 +108,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int KP = a.kp;
   const int img = CN * KP;  // floats per TF32 image of a chunk
-  float* smB = reinterpret_cast<float*>(smem_raw);  // [STAGES][2 * img]
-  float* smX = smB + STAGES * 2 * img;               // [STAGES][CN][DP]
+  float* smB = reinterpret_cast<float*>(smem_raw);  // [STAGES][NPIECE * img]
+  float* smX = smB + STAGES * NPIECE * img;          // [STAGES][CN][DP]
   float* smW = smX + STAGES * CN * DP;               // [STAGES][CN]
   double* wacc = reinterpret_cast<double*>(smW + STAGES * CN);  // [EVAL_WARPS][NV]
   uint64_t* bars = reinterpret_cast<uint64_t*>(wacc + EVAL_WARPS * NV);
@@ -146,7 +157,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
   if (warp == 8) {
     // ---------------- producer ----------------
     if (lane == 0) {
-      const uint32_t bbytes = 2u * img * 4u, xbytes = CN * DP * 4u, wbytes = NARROW ? CN * 4u : 0u;
+      const uint32_t bbytes = NPIECE * img * 4u, xbytes = CN * DP * 4u, wbytes = NARROW ? CN * 4u : 0u;
       for (int k = 0; k < nq; ++k) {
         const int s = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[s], ((k - STAGES) / STAGES) & 1);
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         tile_coords_tc(L0 + k / 2, T, a.symmetric, ti, tcol);
         const int col0 = tcol * TBM + (k & 1) * CN;
         mbar_expect_tx(&full[s], bbytes + xbytes + wbytes);
-        bulk_g2s(smB + s * 2 * img, a.bpk + static_cast<size_t>(col0 / CN) * 2 * img, bbytes, &full[s]);
+        bulk_g2s(smB + s * NPIECE * img, a.bpk + static_cast<size_t>(col0 / CN) * NPIECE * img, bbytes, &full[s]);
         bulk_g2s(smX + s * CN * DP, a.xs + static_cast<size_t>(col0) * DP, xbytes, &full[s]);
         if (NARROW) bulk_g2s(smW + s * CN, a.w1 + col0, wbytes, &full[s]);
       }
@@ -177,14 +188,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         mbar_wait(&full[s], (k / STAGES) & 1);
         if (k >= 2) mbar_wait(&d_empty[b], ((k - 2) / 2) & 1);
         tc_fence_after();
-        const uint32_t bh = smem_u32(smB + s * 2 * img);
-        const uint32_t bl = bh + img * 4;
+        const uint32_t bh = smem_u32(smB + s * NPIECE * img);
+        const uint32_t bm = bh + img * 4, bl = bm + img * 4;
         const uint32_t dt = tmem + b * CN;
-        const uint32_t ah = tmem + A_BASE, al = ah + KP;
+        const uint32_t ah = tmem + A_BASE, am = ah + KP, al = am + KP;
         for (int kk = 0; kk < KP / 8; ++kk) {
           const uint64_t dh = umma_desc(bh + kk * 256, 128, sbo);
+          const uint64_t dm = umma_desc(bm + kk * 256, 128, sbo);
           const uint64_t dl = umma_desc(bl + kk * 256, 128, sbo);
           tc_mma_tf32(dt, ah + kk * 8, dh, idesc, kk == 0 ? 0u : 1u);
+          tc_mma_tf32(dt, ah + kk * 8, dm, idesc, 1u);
+          tc_mma_tf32(dt, am + kk * 8, dh, idesc, 1u);
+          tc_mma_tf32(dt, am + kk * 8, dm, idesc, 1u);
           tc_mma_tf32(dt, ah + kk * 8, dl, idesc, 1u);
           tc_mma_tf32(dt, al + kk * 8, dh, idesc, 1u);
         }
@@ -216,16 +231,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         const bool row_ok = i < a.n;
         const float* urow = a.ua + static_cast<size_t>(row_ok ? i : 0) * a.lda;
         for (int q = 0; q < KP / 16; ++q) {
-          uint32_t hi[8], lo[8];
+          uint32_t hi[8], md[8], lo[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int col = half * (KP / 2) + q * 8 + e;
             const float x = (row_ok && col < a.cols) ? __ldg(urow + col) : 0.f;
-            split_tf32(x, hi[e], lo[e]);
+            split3_tf32(x, hi[e], md[e], lo[e]);
           }
           const uint32_t at = tmem + lane_addr + A_BASE + half * (KP / 2) + q * 8;
           tc_st8(at, hi);
-          tc_st8(at + KP, lo);
+          tc_st8(at + KP, md);
+          tc_st8(at + 2 * KP, lo);
         }
         tc_wait_st();
         tc_fence_before();
@@ -341,7 +357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
   }
 }
 
-// W (rows x cols, FP32, ld) -> per-64-row-chunk TF32 hi | lo images in the
+// W (rows x cols, FP32, ld) -> per-64-row-chunk TF32 hi | mid | lo images in the
 // canonical K-major no-swizzle layout: element (r, k) of chunk r / 64 at
 // ((r%64/8) * (KP/4) + k/4) * 32 + (r%8) * 4 + k%4 of each image. Rows >= n
 // and columns >= cols are zero. Narrow-pair vectors go to contiguous arrays.
@@ -353,13 +369,14 @@ __global__ void grad_tc_pack_kernel(const float* w32, int ld, int n, int cols, i
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(e / kp), k = static_cast<int>(e % kp);
     const float x = (r < n && k < cols) ? w32[static_cast<size_t>(r) * ld + k] : 0.f;
-    uint32_t hi, lo;
-    split_tf32(x, hi, lo);
+    uint32_t hi, md, lo;
+    split3_tf32(x, hi, md, lo);
     const int q = r / CN, rr = r % CN;
-    float* base = bpk + static_cast<size_t>(q) * 2 * img;
+    float* base = bpk + static_cast<size_t>(q) * NPIECE * img;
     const int off = ((rr / 8) * (kp / 4) + k / 4) * 32 + (rr % 8) * 4 + (k % 4);
     base[off] = __uint_as_float(hi);
-    base[img + off] = __uint_as_float(lo);
+    base[img + off] = __uint_as_float(md);
+    base[2 * img + off] = __uint_as_float(lo);
     if (k == 0 && u1) {
       u1[r] = r < n ? n_u[static_cast<size_t>(r) * n_ld] : 0.f;
       w1[r] = r < n ? n_w[static_cast<size_t>(r) * n_ld] : 0.f;
@@ -373,7 +390,7 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
   constexpr int NPR = NARROW ? 2 : 1;
   constexpr int NUSED = NPR * (DP + 1);
   constexpr int NV = NUSED <= 32 ? 32 : (NUSED <= 64 ? 64 : 128);
-  const size_t smem = sizeof(float) * (STAGES * 2 * CN * a.kp + STAGES * CN * DP + STAGES * CN) +
+  const size_t smem = sizeof(float) * (STAGES * NPIECE * CN * a.kp + STAGES * CN * DP + STAGES * CN) +
                       sizeof(double) * EVAL_WARPS * NV + 16 * sizeof(uint64_t);
   static size_t configured = 0;
   if (smem > configured) {
@@ -397,6 +414,7 @@ void launch_dp(const GradTcArgs& a, cudaStream_t s) {
 
 int grad_tc_kp(int cols) { return (cols + 15) / 16 * 16; }
 int grad_tc_rows_pad(int n) { return (n + TBM - 1) / TBM * TBM; }
+size_t grad_tc_pack_floats(int n, int kp) { return static_cast<size_t>(grad_tc_rows_pad(n)) * NPIECE * kp; }
 long long grad_tc_tiles(int n, int symmetric) {
   const long long T = (n + TBM - 1) / TBM;
   return symmetric ? T * (T + 1) / 2 : T * T;

@@ -427,12 +427,15 @@ __global__ void __launch_bounds__(256, 3) kv_reduce_dot_kernel(const KvReduceArg
     if (lane == 0 && k < 1024) bscore[k] = sqrt(t);
   }
   __syncthreads();
+  // per-column norm terms in parallel; thread 0 adds them in column order
+  for (int j = threadIdx.x; j < a.m; j += blockDim.x) ss[j] = sqrt(ss[j]) / a.scales[j];
+  __syncthreads();
   if (threadIdx.x == 0) {
     CgCtl* c = a.ctl;
     c->iters += 1;  // ap_check (solvers.cpp:119-141)
-    const double mean = sqrt(ss[0]) / a.scales[0];
+    const double mean = ss[0];
     double sum = 0.0;
-    for (int j = 1; j < a.m; ++j) sum += sqrt(ss[j]) / a.scales[j];
+    for (int j = 1; j < a.m; ++j) sum += ss[j];
     const double probe = a.m > 1 ? sum / (a.m - 1) : 0.0;
     c->mean_norm = mean;
     c->probe_norm = probe;

@@ -141,14 +141,27 @@ __device__ __forceinline__ double warp_gsum(const double* part, int groups, int 
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
 }
-// Termination norms (linear_system.cpp:38-53) from per-column sums of squares.
-__device__ void termination(const double* ss, int m, const double* scales, double tol, double& mean,
-                            double& probe, int& done) {
-  mean = sqrt(ss[0]) / scales[0];
-  double sum = 0.0;
-  for (int j = 1; j < m; ++j) sum += sqrt(ss[j]) / scales[j];
-  probe = m > 1 ? sum / (m - 1) : 0.0;
-  done = (mean <= tol && probe <= tol) ? 1 : 0;
+// Termination norms (linear_system.cpp:38-53) from per-column sums of squares
+// in shared memory (overwritten). Called by every thread of the block: the
+// per-column terms sqrt(ss_j) / scale_j are formed in parallel, then one thread
+// adds them in column order (the reference's order). The results are valid in
+// every thread on return.
+__device__ void termination_block(double* ss, int m, const double* scales, double tol, double& mean, double& probe,
+                                  int& done) {
+  __shared__ double res[3];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) ss[j] = sqrt(ss[j]) / scales[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int j = 1; j < m; ++j) sum += ss[j];
+    res[0] = ss[0];
+    res[1] = m > 1 ? sum / (m - 1) : 0.0;
+    res[2] = (res[0] <= tol && res[1] <= tol) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  mean = res[0];
+  probe = res[1];
+  done = res[2] != 0.0;
 }
 }  // namespace
 
@@ -166,9 +179,12 @@ __global__ void cg_init_scalars_kernel(const double* part, int groups, int m, co
     }
   }
   __syncthreads();
+  double mean, probe;
+  int done;
+  termination_block(ss, m, scales, tol, mean, probe, done);
   if (threadIdx.x == 0) {
-    int done;
-    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    ctl->mean_norm = mean;
+    ctl->probe_norm = probe;
     ctl->done = done;
     ctl->aborted = 0;
     ctl->iters = 0;
@@ -246,10 +262,13 @@ __global__ void cg_beta_kernel(const double* part, int groups, int m, const doub
     }
   }
   __syncthreads();
+  double mean, probe;
+  int done;
+  termination_block(ss, m, scales, tol, mean, probe, done);
   if (threadIdx.x == 0) {
     ctl->iters += 1;
-    int done;
-    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    ctl->mean_norm = mean;
+    ctl->probe_norm = probe;
     ctl->done = done;
     ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
   }
@@ -300,9 +319,12 @@ __global__ void norms_kernel(const double* part, int groups, int m, const double
     if (lane == 0) ss[j] = q;
   }
   __syncthreads();
+  double mean, probe;
+  int done;
+  termination_block(ss, m, scales, tol, mean, probe, done);
   if (threadIdx.x == 0) {
-    int done;
-    termination(ss, m, scales, tol, out3[0], out3[1], done);
+    out3[0] = mean;
+    out3[1] = probe;
     out3[2] = done;
   }
 }
@@ -839,10 +861,13 @@ __global__ void ap_check_kernel(const double* part, int groups, int m, const dou
     if (lane == 0) ss[j] = q;
   }
   __syncthreads();
+  double mean, probe;
+  int done;
+  termination_block(ss, m, scales, tol, mean, probe, done);
   if (threadIdx.x == 0) {
     ctl->iters += 1;
-    int done;
-    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    ctl->mean_norm = mean;
+    ctl->probe_norm = probe;
     ctl->done = done;
     ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
   }
@@ -997,22 +1022,31 @@ void sgd_residual_launch(double* R, const int* idx, int b, const double* grad, i
 __global__ void sgd_check_kernel(const double* sumsq, int m, const double* scales, double tol, const int* nonfinite,
                                  CgCtl* ctl) {
   if (ctl->stop) return;
-  ctl->iters += 1;
   if (*nonfinite) {
-    ctl->aborted = 1;
-    ctl->stop = 1;
+    if (threadIdx.x == 0) {
+      ctl->iters += 1;
+      ctl->aborted = 1;
+      ctl->stop = 1;
+    }
     return;
   }
-  double ss[512];
-  for (int j = 0; j < m; ++j) ss[j] = fmax(sumsq[j], 0.0);
+  __shared__ double ss[512];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) ss[j] = fmax(sumsq[j], 0.0);
+  __syncthreads();
+  double mean, probe;
   int done;
-  termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
-  ctl->done = done;
-  ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
+  termination_block(ss, m, scales, tol, mean, probe, done);
+  if (threadIdx.x == 0) {
+    ctl->iters += 1;
+    ctl->mean_norm = mean;
+    ctl->probe_norm = probe;
+    ctl->done = done;
+    ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
+  }
 }
 void sgd_check_launch(const double* sumsq, int m, const double* scales, double tol, const int* nonfinite, CgCtl* ctl,
                       cudaStream_t s) {
-  sgd_check_kernel<<<1, 1, 0, s>>>(sumsq, m, scales, tol, nonfinite, ctl);
+  sgd_check_kernel<<<1, 128, 0, s>>>(sumsq, m, scales, tol, nonfinite, ctl);
   check_launch("sgd_check");
 }
 
@@ -1117,15 +1151,21 @@ __global__ void sgd_check_sharded_kernel(const double* gbuf, int nr, long long s
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    ctl->iters += 1;
-    if (bad) {
+  if (bad) {
+    if (threadIdx.x == 0) {
+      ctl->iters += 1;
       ctl->aborted = 1;
       ctl->stop = 1;
-      return;
     }
-    int done;
-    termination(ss, m, scales, tol, ctl->mean_norm, ctl->probe_norm, done);
+    return;
+  }
+  double mean, probe;
+  int done;
+  termination_block(ss, m, scales, tol, mean, probe, done);
+  if (threadIdx.x == 0) {
+    ctl->iters += 1;
+    ctl->mean_norm = mean;
+    ctl->probe_norm = probe;
     ctl->done = done;
     ctl->stop = (done || ctl->iters >= ctl->budget) ? 1 : 0;
   }
