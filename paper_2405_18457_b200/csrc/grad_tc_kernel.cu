@@ -76,26 +76,32 @@ __device__ __forceinline__ void split3_tf32(float x, uint32_t& hi, uint32_t& mid
   lo = __float_as_uint(r1 - __uint_as_float(mid));
 }
 
+// Adds the warp's per-lane FP32 sums v[0..NV) into FP64 slots: each 32-value
+// slab is widened to FP64 and reduce-scattered across the lanes (5 halvings,
+// fixed order), after which every lane owns one slab entry.
 template <int NV>
-__device__ __forceinline__ void butterfly_flush(float (&v)[NV], int lane, double* slot, int nused, double weight) {
-  // reduce-scatter across the warp: after 5 halvings lane l holds NV/32 sums
-  int base = 0;
+__device__ __forceinline__ void butterfly_flush(const float (&v)[NV], int lane, double* slot, int nused,
+                                                double weight) {
 #pragma unroll
-  for (int o = 16, cnt = NV; o > 0; o >>= 1, cnt >>= 1) {
-    const int half = cnt / 2;
-    const bool up = (lane & o) != 0;
+  for (int sl = 0; sl < NV / 32; ++sl) {
+    double w[32];
 #pragma unroll
-    for (int k = 0; k < half; ++k) {
-      const float send = up ? v[k] : v[k + half];
-      const float keep = up ? v[k + half] : v[k];
-      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    for (int k = 0; k < 32; ++k) w[k] = static_cast<double>(v[sl * 32 + k]);
+    int base = 0;
+#pragma unroll
+    for (int o = 16, cnt = 32; o > 0; o >>= 1, cnt >>= 1) {
+      const int half = cnt / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int k = 0; k < half; ++k) {
+        const double send = up ? w[k] : w[k + half];
+        const double keep = up ? w[k + half] : w[k];
+        w[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      if (up) base += half;
     }
-    if (up) base += half;
-  }
-#pragma unroll
-  for (int k = 0; k < NV / 32; ++k) {
-    const int idx = base + k;
-    if (idx < nused) slot[idx] += static_cast<double>(v[k]) * weight;
+    const int idx = sl * 32 + base;
+    if (idx < nused) slot[idx] += w[0] * weight;
   }
 }
 
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // x_c / w reads of this stage done
-      if (k & 1) {  // tile complete: flush its FP32 sums into the warp's FP64 slots
+      {  // chunk complete: flush its FP32 sums into the warp's FP64 slots
         float v[NV];
 #pragma unroll
         for (int t = 0; t < NV; ++t) v[t] = 0.f;
@@ -390,8 +396,11 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
   constexpr int NPR = NARROW ? 2 : 1;
   constexpr int NUSED = NPR * (DP + 1);
   constexpr int NV = NUSED <= 32 ? 32 : (NUSED <= 64 ? 64 : 128);
-  const size_t smem = sizeof(float) * (STAGES * NPIECE * CN * a.kp + STAGES * CN * DP + STAGES * CN) +
-                      sizeof(double) * EVAL_WARPS * NV + 16 * sizeof(uint64_t);
+  // >= 120 KB keeps one CTA per SM: each allocates all 512 TMEM columns
+  const size_t smem = std::max<size_t>(
+      sizeof(float) * (STAGES * NPIECE * CN * a.kp + STAGES * CN * DP + STAGES * CN) +
+          sizeof(double) * EVAL_WARPS * NV + 16 * sizeof(uint64_t),
+      120 * 1024);
   static size_t configured = 0;
   if (smem > configured) {
     GPK_CUDA(cudaFuncSetAttribute(grad_tc_kernel<DP4, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
