@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -89,6 +90,7 @@ struct gpk_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof;  // K.V launch brackets
   size_t prof_used = 0;
   int kernel = 1;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32 (default)
+  bool fused_ap = true;  // AP slabs: reduce + epilogue fused into the tcgen05 kernel
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
   DBuf<double> rff_feat;  // RFF feature rows (prior GEMM), reused across calls
@@ -151,6 +153,7 @@ struct gpk_batch {
   std::unique_ptr<gpk_precond> pc;  // dispatch-built preconditioner, reused across solves
   DBuf<unsigned> ticket;             // last-block ticket of fused reductions (kept at 0 between uses)
   DBuf<float> apk;                   // AP block update's TF32 operator images
+  DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
 };
 
 struct gpk_rff_basis {
@@ -316,13 +319,20 @@ struct KvCall {
   long long ap_bb = 0;
   double* ap_upd = nullptr;
   const float* xs_rows = nullptr;  // cross kernel: rows from these scaled points, no noise diagonal
+  bool fused = false;              // AP slab: reduce + epilogue inside the tcgen05 kernel
 };
 
 void run_kv(gpk_operator* op, const KvCall& c) {
   cudaStream_t s = op->ctx->stream;
   const int Cmax = c.sel ? c.sel_block : c.C;
   const bool tc = op->ctx->kernel == 1 && c.m <= 80;
-  int splits = tc ? kv_tc_choose_splits(c.R, Cmax, op->ctx->sms) : kv_choose_splits(c.R, Cmax, op->ctx->sms);
+  // AP slab on the tensor cores: one column split, reduce + AP epilogue fused
+  // into the operator kernel (every 128-row tile lies inside one AP block)
+  const bool fused = c.fused;
+  if (fused && !(tc && c.sel && c.ctl && c.spart && c.dotw == c.out && !c.row_idx && c.r0 == 0 &&
+                 c.score_block % 128 == 0 && c.groups == (c.R + 127) / 128 && c.gpb == c.score_block / 128))
+    throw std::logic_error("run_kv: fused AP slab preconditions");
+  int splits = fused ? 1 : tc ? kv_tc_choose_splits(c.R, Cmax, op->ctx->sms) : kv_choose_splits(c.R, Cmax, op->ctx->sms);
   int cps = (Cmax + splits - 1) / splits;
   cps = (cps + 31) / 32 * 32;
   splits = std::max(1, (Cmax + cps - 1) / cps);
@@ -345,7 +355,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.part = part;
   a.splits = splits;
   a.cols_per_split = cps;
-  a.flush_chunks = 16;
+  a.flush_chunks = fused ? std::max(16, (cps + 31) / 32) : 16;
   a.skip = c.skip;
   a.stats = op->ctx->stats;
   a.d = op->d;
@@ -370,11 +380,6 @@ void run_kv(gpk_operator* op, const KvCall& c) {
     GPK_CUDA(cudaEventRecord(pr.first, s));
     prof_end = &pr.second;
   }
-  if (tc)
-    kv_tc_launch(a, vpk, s);
-  else
-    kv_slab_launch(a, op->d, s);
-  if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
   KvReduceArgs r{};
   r.part = part;
   r.splits = splits;
@@ -417,6 +422,16 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.ap_bb = c.ap_bb;
   r.ap_upd = c.ap_upd;
   r.nodiag = c.xs_rows != nullptr;
+  if (fused) {
+    kv_tc_fused_launch(a, vpk, r, s);
+    if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
+    return;
+  }
+  if (tc)
+    kv_tc_launch(a, vpk, s);
+  else
+    kv_slab_launch(a, op->d, s);
+  if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
   kv_reduce_launch(r, s);
 }
 
@@ -845,7 +860,16 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   const int gpb = std::max(1, std::min(block / 8, 3 * ctx->sms / nblocks));
   const int groups = nblocks * gpb;
   double* spart = b->vec2.ensure(groups);
-  double* part = b->red.ensure(static_cast<size_t>(groups) * m + 8);
+  // fused slab iterations (run_kv): one partial per 128-row tile, block scores
+  // from block/128 tiles; the tail tiles of a partial last block stay zero
+  const bool fused = tc && ctx->fused_ap && block % 128 == 0 && m <= 96 && nblocks <= 1024;
+  const int tiles = (n + 127) / 128, gpb_t = block / 128;
+  double* spart_t = nullptr;
+  if (fused) {
+    spart_t = b->spart_t.ensure(static_cast<size_t>(nblocks) * gpb_t);
+    GPK_CUDA(cudaMemsetAsync(spart_t, 0, sizeof(double) * nblocks * gpb_t, s));
+  }
+  double* part = b->red.ensure(static_cast<size_t>(std::max(groups, tiles)) * m + 8);
   int* sel = b->ibuf.ensure(1);
   double* Rs = b->w3.ensure(static_cast<size_t>(block) * m);
   double* upd64 = b->w2.ensure(static_cast<size_t>(block) * m);
@@ -933,17 +957,18 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
       kc.skip = stop;
       kc.dotw = b->residuals.p;
       kc.dpart = part;
-      kc.groups = groups;
+      kc.groups = fused ? tiles : groups;
       kc.inv_scales = inv_scales_dev;
-      kc.spart = spart;
+      kc.spart = fused ? spart_t : spart;
       kc.score_block = block;
-      kc.gpb = gpb;
+      kc.gpb = fused ? gpb_t : gpb;
       kc.ctl = ctl;
       kc.scales = b->scales_dev.p;
       kc.tol = c->tolerance;
       kc.sel_out = sel;
       kc.nblocks = nblocks;
       kc.ticket = ticket;
+      kc.fused = fused;
       if (in_place) {
         kc.ap_ptrs = ptrs;
         kc.ap_inv = inv;
@@ -1399,9 +1424,9 @@ void rff_prior_gemm(gpk_ctx* ctx, const double* x64, int rows, int d, const doub
 void rff_prior_dev(gpk_operator* op, gpk_rff_basis* b, int s_count, double* prior) {
   cudaStream_t s = op->ctx->stream;
   const int P = b->pairs, d = op->d;
-  std::vector<double> f(static_cast<size_t>(P) * d);  // row-major [P][d]
-  for (int p = 0; p < P; ++p)
-    for (int k = 0; k < d; ++k) f[static_cast<size_t>(p) * d + k] = b->freq[static_cast<size_t>(k) * P + p] * op->inv_ls[k];
+  std::vector<double> f(static_cast<size_t>(P) * d);  // [d][P], scaled by 1/l
+  for (int k = 0; k < d; ++k)
+    for (int p = 0; p < P; ++p) f[static_cast<size_t>(k) * P + p] = b->freq[static_cast<size_t>(k) * P + p] * op->inv_ls[k];
   double* fd = b->freq_dev.ensure(f.size());
   GPK_CUDA(cudaMemcpyAsync(fd, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice, s));
   if (!b->w_dev.p) {
@@ -1451,9 +1476,9 @@ void cross_apply_dev(gpk_operator* op, int p, const double* v64, int m, double* 
 void prior_at_points(gpk_operator* op, gpk_rff_basis* b, int p, int s_count, double* prior) {
   cudaStream_t s = op->ctx->stream;
   const int P = b->pairs, d = op->d;
-  std::vector<double> f(static_cast<size_t>(P) * d);
-  for (int q = 0; q < P; ++q)
-    for (int k = 0; k < d; ++k) f[static_cast<size_t>(q) * d + k] = b->freq[static_cast<size_t>(k) * P + q] * op->inv_ls[k];
+  std::vector<double> f(static_cast<size_t>(P) * d);  // [d][P], scaled by 1/l
+  for (int k = 0; k < d; ++k)
+    for (int q = 0; q < P; ++q) f[static_cast<size_t>(k) * P + q] = b->freq[static_cast<size_t>(k) * P + q] * op->inv_ls[k];
   double* fd = b->freq_dev.ensure(f.size());
   GPK_CUDA(cudaMemcpyAsync(fd, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice, s));
   if (!b->w_dev.p) {
@@ -1514,6 +1539,7 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     if (prop.major != 10) throw CudaError("gpk: libgpk is built for sm_100a (B200); device is sm_" +
                                           std::to_string(prop.major) + std::to_string(prop.minor));
     c->sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("GPK_FUSED_AP")) c->fused_ap = std::atoi(e) != 0;  // A/B switch
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate");
     if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate");

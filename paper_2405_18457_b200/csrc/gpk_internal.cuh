@@ -72,6 +72,11 @@ size_t kv_tc_pack_floats(int m, int rows);
 void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_max, int m, const int* sel,
                        int sel_block, int n, float* vpk, const int* skip, cudaStream_t s, int rows_valid = -1);
 void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s);
+struct KvReduceArgs;
+// AP slab with the reduce fused into the tensor-core kernel (splits == 1,
+// one accumulation group, score_block a multiple of 128): writes out, the
+// per-tile dpart/spart partials and runs the AP epilogue in the last CTA.
+void kv_tc_fused_launch(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s);
 
 struct KvReduceArgs {
   const double* part;
@@ -285,9 +290,7 @@ void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, c
 // RFF (K5) + noise (K9)
 void rff_features_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude, double* F,
                          cudaStream_t s);
-void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs,
-                      const double* weights, int ldw, int s, double amplitude, double* prior,
-                      cudaStream_t s_);  // prior row-major [n][s]
+  // prior row-major [n][s]
 void gaussian_fill_launch(uint64_t seed, uint64_t stream, uint64_t substream, int64_t count,
                           int n, int s, double* out_rowmajor, cudaStream_t st);  // col-major order
 // rows [row0, row0 + nloc) of the same n x s column-major fill, row-major [nloc][s]

@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "gpk_internal.cuh"
+#include "ap_epilogue.cuh"
 
 namespace gpk {
 
@@ -410,52 +411,8 @@ __global__ void __launch_bounds__(256, 3) kv_reduce_dot_kernel(const KvReduceArg
   if (!last) return;
   __threadfence();
   __shared__ double ss[96];
-  const int G = gridDim.x;
-  for (int j = warp; j < a.m; j += NW) {  // sum_g dpart[g][j], fixed xor tree per warp
-    double acc = 0.0;
-    for (int q = lane; q < G; q += 32) acc += __ldcg(a.dpart + static_cast<size_t>(q) * a.m + j);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) ss[j] = acc;
-  }
   __shared__ double bscore[1024];
-  for (int k = warp; k < a.nblocks; k += NW) {  // fixed xor tree per block
-    double t = 0.0;
-    for (int q = lane; q < a.gpb; q += 32) t += __ldcg(a.spart + static_cast<size_t>(k) * a.gpb + q);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0 && k < 1024) bscore[k] = sqrt(t);
-  }
-  __syncthreads();
-  // per-column norm terms in parallel; thread 0 adds them in column order
-  for (int j = threadIdx.x; j < a.m; j += blockDim.x) ss[j] = sqrt(ss[j]) / a.scales[j];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    CgCtl* c = a.ctl;
-    c->iters += 1;  // ap_check (solvers.cpp:119-141)
-    const double mean = ss[0];
-    double sum = 0.0;
-    for (int j = 1; j < a.m; ++j) sum += ss[j];
-    const double probe = a.m > 1 ? sum / (a.m - 1) : 0.0;
-    c->mean_norm = mean;
-    c->probe_norm = probe;
-    c->done = (mean <= a.tol && probe <= a.tol) ? 1 : 0;
-    c->stop = (c->done || c->iters >= c->budget) ? 1 : 0;
-    int best_k = 0;  // ap_select: strict '>' from -1 (solvers.cpp:125-132)
-    double best = -1.0;
-    for (int k = 0; k < a.nblocks; ++k)
-      if (bscore[k] > best) {
-        best = bscore[k];
-        best_k = k;
-      }
-    *a.sel_out = best_k;
-    if (a.ap_ptrs) {
-      a.ap_ptrs[0] = a.out + static_cast<size_t>(best_k) * a.score_block * a.m;  // R rows of the block (padded)
-      a.ap_ptrs[1] = a.ap_inv + static_cast<size_t>(best_k) * a.ap_bb;
-      a.ap_ptrs[2] = a.ap_upd;
-    }
-    *a.ticket = 0u;
-  }
+  ap_epilogue(a, static_cast<int>(gridDim.x), threadIdx.x, NW, ss, bscore, [] { __syncthreads(); });
 }
 
 }  // namespace

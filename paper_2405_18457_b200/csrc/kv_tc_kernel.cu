@@ -28,6 +28,7 @@
 
 #include "gpk_internal.cuh"
 #include "tc_util.cuh"
+#include "ap_epilogue.cuh"
 
 namespace gpk {
 
@@ -54,8 +55,94 @@ struct TcLayout {
   static constexpr uint32_t CHUNK_BYTES = CHUNK_FLOATS * 4;
 };
 
-template <int NPAD, int DP4>
-__global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk) {
+__device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// Fused reduce for an AP slab (splits == 1): each eval thread owns one row and
+// half of the D columns. out = base + alpha (D + sigma^2 upd on the diagonal);
+// the CTA's column sums of out^2 and its AP block-score partial
+// sum_r (sum_j out[r][j] inv_scales[j])^2 go to dpart[tile] / spart[tile] in a
+// fixed order (warp reduce-scatter, then lane groups in order), and the last
+// CTA (ticket) runs the AP epilogue. Replaces kv_reduce_dot_kernel for slabs.
+template <int NPAD>
+__device__ __forceinline__ void fused_drain(const KvArgs& a, const KvReduceArgs& f, uint32_t trow, int er, int gi,
+                                            int c0, int C, int half, int lg, int lane, int warp, double* scratch) {
+  constexpr int DCOLS = NPAD / 2;
+  double* red = scratch;                 // [4][NPAD] column sums per lane group
+  double* rd = red + 4 * NPAD;           // [2][128] row dot halves
+  double* ssc = rd + 256;                // [4]
+  double* ss = ssc + 8;                  // [96]
+  double* bscore = ss + 96;              // [1024]
+  unsigned* last = reinterpret_cast<unsigned*>(bscore + 1024);
+  const int tid = warp * 32 + lane;
+  const bool row_ok = er < a.R;
+  const bool diag = row_ok && gi >= c0 && gi < c0 + C;
+  const int vr = gi - c0 - f.vshift;
+  double rowdot = 0.0;
+#pragma unroll 1
+  for (int q = 0; q < DCOLS / 8; ++q) {
+    const int col0 = half * DCOLS + q * 8;
+    uint32_t v[8];
+    tc_ld8(trow + col0, v);
+    tc_wait_ld();
+    double cs[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int j = col0 + e;
+      cs[e] = 0.0;
+      if (row_ok && j < a.m) {
+        double acc = static_cast<double>(__uint_as_float(v[e]));
+        if (diag) acc += f.sigma2 * f.vdiag[static_cast<size_t>(vr) * f.ldvd + j];
+        const double b = f.base ? f.base[static_cast<size_t>(er) * f.ldb + j] : 0.0;
+        const double val = b + f.alpha * acc;
+        f.out[static_cast<size_t>(er) * f.ldo + j] = val;
+        cs[e] = val * val;
+        rowdot += val * f.inv_scales[j];
+      }
+    }
+    // reduce-scatter the 8 column sums over the 32 rows of this warp
+    int base = 0;
+#pragma unroll
+    for (int o = 16, cnt = 8; o >= 4; o >>= 1, cnt >>= 1) {
+      const int hf = cnt / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int k = 0; k < hf; ++k) {
+        const double send = up ? cs[k] : cs[k + hf];
+        const double keep = up ? cs[k + hf] : cs[k];
+        cs[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      if (up) base += hf;
+    }
+    cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 2);
+    cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 1);
+    if ((lane & 3) == 0) red[lg * NPAD + col0 + base] = cs[0];
+  }
+  rd[half * 128 + lg * 32 + lane] = rowdot;
+  eval_bar();
+  for (int j = tid; j < a.m; j += 256)
+    f.dpart[static_cast<size_t>(blockIdx.x) * a.m + j] = ((red[j] + red[NPAD + j]) + red[2 * NPAD + j]) + red[3 * NPAD + j];
+  if (half == 0) {
+    const double w = rd[lg * 32 + lane] + rd[128 + lg * 32 + lane];
+    double sc = row_ok ? w * w : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    if (lane == 0) ssc[lg] = sc;
+  }
+  eval_bar();
+  if (tid == 0) {
+    f.spart[blockIdx.x] = ((ssc[0] + ssc[1]) + ssc[2]) + ssc[3];
+    __threadfence();
+    *last = (atomicAdd(f.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  eval_bar();
+  if (!*last) return;
+  __threadfence();
+  ap_epilogue(f, static_cast<int>(gridDim.x), tid, 8, ss, bscore, [] { eval_bar(); });
+}
+
+template <int NPAD, int DP4, bool FUSED>
+__global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk,
+                                                            const KvReduceArgs f) {
   constexpr int DP = 4 * DP4;
   using L = TcLayout<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -244,6 +331,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
         const int g = k / flush;
         mbar_wait(d_full, g & 1);
         tc_fence_after();
+        if constexpr (FUSED) {
+          // single accumulation group (host guarantees): D holds the whole slab
+          fused_drain<NPAD>(a, f, tmem + lane_addr, er, gi, c0, C, half, lg, lane, warp, reinterpret_cast<double*>(bars + 64));
+        } else {
         const bool row_ok = er < a.R;
         double* prow = part + static_cast<size_t>(er_c) * a.m;
 #pragma unroll
@@ -259,6 +350,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
               if (col < a.m) prow[col] = (wrote ? prow[col] : 0.0) + static_cast<double>(__uint_as_float(v[e]));
             }
           }
+        }
         }
         wrote = true;
         tc_fence_before();
@@ -319,35 +411,49 @@ __global__ void kv_pack_kernel(const double* v64, const float* v32, int ldv, int
   }
 }
 
-template <int NPAD, int DP4>
-void launch_tc_one(const KvArgs& a, const float* vpk, cudaStream_t s) {
+template <int NPAD, int DP4, bool FUSED>
+void launch_tc_one(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   using L = TcLayout<NPAD>;
-  const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 16 * sizeof(uint64_t);
+  // + the fused drain's scratch behind the barriers (bars + 64 words: ~14 KB)
+  const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 16 * sizeof(uint64_t) +
+                      (FUSED ? 64 * sizeof(uint64_t) + sizeof(double) * (4 * NPAD + 256 + 8 + 96 + 1024) + 16 : 0);
   // at most 2 CTAs per SM: each allocates 256 of the 512 TMEM columns
   const size_t smem = std::max<size_t>(need, 100 * 1024);
   static bool configured = false;
   if (!configured) {
-    GPK_CUDA(cudaFuncSetAttribute(kv_tc_kernel<NPAD, DP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GPK_CUDA(cudaFuncSetAttribute(kv_tc_kernel<NPAD, DP4, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = true;
   }
   dim3 grid((a.R + TBM - 1) / TBM, a.splits);
-  kv_tc_kernel<NPAD, DP4><<<grid, NTHREADS, smem, s>>>(a, vpk);
+  kv_tc_kernel<NPAD, DP4, FUSED><<<grid, NTHREADS, smem, s>>>(a, vpk, f);
   check_launch("kv_tc_kernel");
 }
 
-template <int NPAD>
-void launch_tc_n(const KvArgs& a, const float* vpk, cudaStream_t s) {
+template <int NPAD, bool FUSED>
+void launch_tc_n(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   switch (a.dp / 4) {
-    case 1: return launch_tc_one<NPAD, 1>(a, vpk, s);
-    case 2: return launch_tc_one<NPAD, 2>(a, vpk, s);
-    case 3: return launch_tc_one<NPAD, 3>(a, vpk, s);
-    case 4: return launch_tc_one<NPAD, 4>(a, vpk, s);
-    case 5: return launch_tc_one<NPAD, 5>(a, vpk, s);
-    case 6: return launch_tc_one<NPAD, 6>(a, vpk, s);
-    case 7: return launch_tc_one<NPAD, 7>(a, vpk, s);
-    case 8: return launch_tc_one<NPAD, 8>(a, vpk, s);
+    case 1: return launch_tc_one<NPAD, 1, FUSED>(a, vpk, f, s);
+    case 2: return launch_tc_one<NPAD, 2, FUSED>(a, vpk, f, s);
+    case 3: return launch_tc_one<NPAD, 3, FUSED>(a, vpk, f, s);
+    case 4: return launch_tc_one<NPAD, 4, FUSED>(a, vpk, f, s);
+    case 5: return launch_tc_one<NPAD, 5, FUSED>(a, vpk, f, s);
+    case 6: return launch_tc_one<NPAD, 6, FUSED>(a, vpk, f, s);
+    case 7: return launch_tc_one<NPAD, 7, FUSED>(a, vpk, f, s);
+    case 8: return launch_tc_one<NPAD, 8, FUSED>(a, vpk, f, s);
     default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
+  }
+}
+
+template <bool FUSED>
+void launch_tc(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
+  switch (kv_tc_npad(a.m)) {
+    case 16: return launch_tc_n<16, FUSED>(a, vpk, f, s);
+    case 32: return launch_tc_n<32, FUSED>(a, vpk, f, s);
+    case 48: return launch_tc_n<48, FUSED>(a, vpk, f, s);
+    case 64: return launch_tc_n<64, FUSED>(a, vpk, f, s);
+    case 80: return launch_tc_n<80, FUSED>(a, vpk, f, s);
+    default: throw std::invalid_argument("gpk: tensor-core operator supports m <= 80");
   }
 }
 
@@ -372,14 +478,13 @@ void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_ma
 }
 
 void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s) {
-  switch (kv_tc_npad(a.m)) {
-    case 16: return launch_tc_n<16>(a, vpk, s);
-    case 32: return launch_tc_n<32>(a, vpk, s);
-    case 48: return launch_tc_n<48>(a, vpk, s);
-    case 64: return launch_tc_n<64>(a, vpk, s);
-    case 80: return launch_tc_n<80>(a, vpk, s);
-    default: throw std::invalid_argument("gpk: tensor-core operator supports m <= 80");
-  }
+  const KvReduceArgs none{};
+  launch_tc<false>(a, vpk, none, s);
+}
+
+void kv_tc_fused_launch(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
+  if (a.splits != 1) throw std::invalid_argument("gpk: fused slab reduce needs one column split");
+  launch_tc<true>(a, vpk, f, s);
 }
 
 }  // namespace gpk

@@ -551,31 +551,46 @@ void dense_block64_launch(const double* xs64, int n, int d, double s2, double si
 }
 
 // All AP diagonal blocks H[blk_k, blk_k] (block x block, FP64) in one launch;
-// the last block's rows/columns beyond n are identity padding.
-__global__ void ap_blocks_kernel(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks,
-                                 double* mats) {
-  const long long bb = static_cast<long long>(block) * block;
-  const long long total = bb * nblocks;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int k = static_cast<int>(e / bb);
-    const long long w = e % bb;
-    const int r = static_cast<int>(w / block), c = static_cast<int>(w % block);
-    const int r0 = k * block, len = min(block, n - r0);
+// the last block's rows/columns beyond n are identity padding. CTA = one 32 x 32
+// tile of one block (grid.z = block index): its 32 row and 32 column points are
+// staged in shared memory, each thread forms 4 entries (same arithmetic as
+// matern64, kernel.cpp:35-39).
+__global__ void ap_blocks_kernel(const double* xs64, int n, int d, double s2, double sigma2, int block, double* mats) {
+  __shared__ double xr[32][33], xc[32][33];
+  const int k = blockIdx.z, r0 = k * block, len = min(block, n - r0);
+  const int tr = blockIdx.y * 32, tcl = blockIdx.x * 32;
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+    const int a = e / 32, q = e % 32;
+    xr[a][q] = (q < d && tr + a < len) ? xs64[static_cast<size_t>(r0 + tr + a) * d + q] : 0.0;
+    xc[a][q] = (q < d && tcl + a < len) ? xs64[static_cast<size_t>(r0 + tcl + a) * d + q] : 0.0;
+  }
+  __syncthreads();
+  const int c = threadIdx.x & 31;
+  double* out = mats + static_cast<size_t>(k) * block * block;
+  for (int rr = threadIdx.x >> 5; rr < 32; rr += blockDim.x >> 5) {
+    const int r = tr + rr, cc = tcl + c;
+    if (r >= block || cc >= block) continue;
     double v;
-    if (r < len && c < len) {
-      v = matern64(xs64, d, r0 + r, r0 + c, s2);
-      if (r == c) v += sigma2;
+    if (r < len && cc < len) {
+      double r2 = 0.0;
+      for (int q = 0; q < d; ++q) {
+        const double t = xc[c][q] - xr[rr][q];
+        r2 += t * t;
+      }
+      const double rad = sqrt(r2);
+      v = s2 * (1.0 + kSqrt3 * rad) * exp(-kSqrt3 * rad);
+      if (r == cc) v += sigma2;
     } else {
-      v = r == c ? 1.0 : 0.0;
+      v = r == cc ? 1.0 : 0.0;
     }
-    mats[e] = v;
+    out[static_cast<size_t>(r) * block + cc] = v;
   }
 }
 void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks, double* mats,
                       cudaStream_t s) {
-  const long long total = static_cast<long long>(block) * block * nblocks;
-  ap_blocks_kernel<<<blocks_for(total, 256), 256, 0, s>>>(xs64, n, d, s2, sigma2, block, nblocks, mats);
+  if (d > 32) throw std::invalid_argument("gpk: input dimension > 32 is not supported");
+  dim3 grid((block + 31) / 32, (block + 31) / 32, nblocks);
+  ap_blocks_kernel<<<grid, 256, 0, s>>>(xs64, n, d, s2, sigma2, block, mats);
   check_launch("ap_blocks");
 }
 
@@ -1240,61 +1255,10 @@ void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, c
 }
 
 // ------------------------------------------------------------ RFF (K5)
-// prior[i][j] = sum_q feat(i,q) W(q,j), feat(i,2p) = amp cos(theta), feat(i,2p+1)
-// = amp sin(theta), theta = x_i . (Omega_p / l) in FP64 (rff.cpp:36-54, 73).
-// Features are formed per 16-pair chunk in smem and never materialised in HBM.
-__global__ void rff_prior_kernel(const double* x64, int n, int d, const double* freq, int pairs, const double* W,
-                                 int ldw, int s, double amplitude, double* prior) {
-  constexpr int RB = 64, PC = 16, FC = 2 * PC;
-  __shared__ double feat[RB][FC + 1];
-  __shared__ double wch[FC][64];
-  const int r0 = blockIdx.x * RB, j0 = blockIdx.y * 64;
-  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-  double acc[4][4];
-  for (int a = 0; a < 4; ++a)
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int p0 = 0; p0 < pairs; p0 += PC) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < RB * PC; e += blockDim.x) {
-      const int rr = e / PC, pp = e % PC;
-      const int i = min(r0 + rr, n - 1), p = p0 + pp;
-      double c = 0.0, sn = 0.0;
-      if (p < pairs) {
-        double ang = 0.0;
-        for (int k = 0; k < d; ++k) ang += x64[static_cast<size_t>(i) * d + k] * freq[static_cast<size_t>(p) * d + k];
-        sincos(ang, &sn, &c);
-        c *= amplitude;
-        sn *= amplitude;
-      }
-      feat[rr][2 * pp] = c;
-      feat[rr][2 * pp + 1] = sn;
-    }
-    for (int e = threadIdx.x; e < FC * 64; e += blockDim.x) {
-      const int q = e / 64, j = e % 64;
-      const int gq = 2 * p0 + q;
-      wch[q][j] = (gq < 2 * pairs && j0 + j < s) ? W[static_cast<size_t>(j0 + j) * ldw + gq] : 0.0;
-    }
-    __syncthreads();
-    for (int q = 0; q < FC; ++q) {
-      double fv[4], wv[4];
-      for (int a = 0; a < 4; ++a) fv[a] = feat[ty * 4 + a][q];
-      for (int b = 0; b < 4; ++b) wv[b] = wch[q][tx * 4 + b];
-      for (int a = 0; a < 4; ++a)
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(fv[a], wv[b], acc[a][b]);
-    }
-  }
-  for (int a = 0; a < 4; ++a) {
-    const int i = r0 + ty * 4 + a;
-    if (i >= n) continue;
-    for (int b = 0; b < 4; ++b) {
-      const int j = j0 + tx * 4 + b;
-      if (j < s) prior[static_cast<size_t>(i) * s + j] = acc[a][b];
-    }
-  }
-}
 // Feature rows for the GEMM form of the prior: F[i][2p] = amp cos(theta_ip),
 // F[i][2p+1] = amp sin(theta_ip), theta_ip = x_i . (Omega_p / l) in FP64
-// (rff.cpp:36-54); one thread per (i, p), consecutive p -> coalesced rows.
+// (rff.cpp:36-54); one thread per (i, p), consecutive p -> coalesced rows;
+// freq is [d][pairs] (already divided by the lengthscales).
 __global__ void rff_features_kernel(const double* x64, int n, int d, const double* freq, int pairs, double amplitude,
                                     double* F) {
   const long long total = static_cast<long long>(n) * pairs;
@@ -1302,8 +1266,8 @@ __global__ void rff_features_kernel(const double* x64, int n, int d, const doubl
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long i = e / pairs;
     const int p = static_cast<int>(e % pairs);
-    double ang = 0.0;
-    for (int k = 0; k < d; ++k) ang += x64[i * d + k] * freq[static_cast<size_t>(p) * d + k];
+    double ang = 0.0;  // freq is [d][pairs]: consecutive p read consecutive words
+    for (int k = 0; k < d; ++k) ang += x64[i * d + k] * freq[static_cast<size_t>(k) * pairs + p];
     double sn, c;
     sincos(ang, &sn, &c);
     F[i * 2 * pairs + 2 * p] = amplitude * c;
@@ -1317,12 +1281,6 @@ void rff_features_launch(const double* x64, int n, int d, const double* freq, in
   check_launch("rff_features");
 }
 
-void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs, const double* weights, int ldw,
-                      int s, double amplitude, double* prior, cudaStream_t st) {
-  dim3 grid((n + 63) / 64, (s + 63) / 64);
-  rff_prior_kernel<<<grid, 256, 0, st>>>(x64, n, d, freq, pairs, weights, ldw, s, amplitude, prior);
-  check_launch("rff_prior");
-}
 
 // Box-Muller pairs (rng.cpp:64-77), element e of the column-major n x s fill
 // (rng.cpp:86-90) -> out[i][j] row-major, i = e % n, j = e / n.
