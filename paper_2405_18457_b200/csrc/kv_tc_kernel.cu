@@ -55,7 +55,9 @@ struct TcLayout {
   static constexpr uint32_t CHUNK_BYTES = CHUNK_FLOATS * 4;
 };
 
-__device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+template <int EW>
+__device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory"); }
+constexpr int FUSED_SCRATCH_DOUBLES = 4 * 80 + 512 + 8 + 96 + 1024 + 8;  // fused_drain scratch (NPAD <= 80)
 
 // Fused reduce for an AP slab (splits == 1): each eval thread owns one row and
 // half of the D columns. out = base + alpha (D + sigma^2 upd on the diagonal);
@@ -63,46 +65,50 @@ __device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, 256;" :::
 // sum_r (sum_j out[r][j] inv_scales[j])^2 go to dpart[tile] / spart[tile] in a
 // fixed order (warp reduce-scatter, then lane groups in order), and the last
 // CTA (ticket) runs the AP epilogue. Replaces kv_reduce_dot_kernel for slabs.
-template <int NPAD>
+template <int NPAD, int EW>
 __device__ __forceinline__ void fused_drain(const KvArgs& a, const KvReduceArgs& f, uint32_t trow, int er, int gi,
-                                            int c0, int C, int half, int lg, int lane, int warp, double* scratch) {
-  constexpr int DCOLS = NPAD / 2;
-  double* red = scratch;                 // [4][NPAD] column sums per lane group
-  double* rd = red + 4 * NPAD;           // [2][128] row dot halves
-  double* ssc = rd + 256;                // [4]
-  double* ss = ssc + 8;                  // [96]
-  double* bscore = ss + 96;              // [1024]
+                                            int c0, int C, int qtr, int lg, int lane, int warp, double* scratch,
+                                            const double* sbase) {
+  constexpr int NQ = EW / 4;          // warps per TMEM lane group
+  constexpr int DC = NPAD / NQ;       // D columns drained by this thread (multiple of 4)
+  double* red = scratch;              // [4][NPAD] column sums per lane group
+  double* rd = red + 4 * NPAD;        // [NQ][128] row-dot parts
+  double* ssc = rd + 4 * 128;         // [4]
+  double* ss = ssc + 8;               // [96]
+  double* bscore = ss + 96;           // [1024]
   unsigned* last = reinterpret_cast<unsigned*>(bscore + 1024);
   const int tid = warp * 32 + lane;
   const bool row_ok = er < a.R;
   const bool diag = row_ok && gi >= c0 && gi < c0 + C;
   const int vr = gi - c0 - f.vshift;
+  const int lrow = er - blockIdx.x * 128;
   double rowdot = 0.0;
 #pragma unroll 1
-  for (int q = 0; q < DCOLS / 8; ++q) {
-    const int col0 = half * DCOLS + q * 8;
-    uint32_t v[8];
-    tc_ld8(trow + col0, v);
+  for (int q = 0; q < DC / 4; ++q) {
+    const int col0 = qtr * DC + q * 4;
+    uint32_t v[4];
+    tc_ld4(trow + col0, v);
     tc_wait_ld();
-    double cs[8];
+    double cs[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < 4; ++e) {
       const int j = col0 + e;
       cs[e] = 0.0;
       if (row_ok && j < a.m) {
         double acc = static_cast<double>(__uint_as_float(v[e]));
         if (diag) acc += f.sigma2 * f.vdiag[static_cast<size_t>(vr) * f.ldvd + j];
-        const double b = f.base ? f.base[static_cast<size_t>(er) * f.ldb + j] : 0.0;
+        const double b = sbase ? sbase[static_cast<size_t>(lrow) * a.m + j]
+                               : f.base ? f.base[static_cast<size_t>(er) * f.ldb + j] : 0.0;
         const double val = b + f.alpha * acc;
         f.out[static_cast<size_t>(er) * f.ldo + j] = val;
         cs[e] = val * val;
         rowdot += val * f.inv_scales[j];
       }
     }
-    // reduce-scatter the 8 column sums over the 32 rows of this warp
+    // reduce-scatter the 4 column sums over the 32 rows of this warp
     int base = 0;
 #pragma unroll
-    for (int o = 16, cnt = 8; o >= 4; o >>= 1, cnt >>= 1) {
+    for (int o = 16, cnt = 4; o >= 8; o >>= 1, cnt >>= 1) {
       const int hf = cnt / 2;
       const bool up = (lane & o) != 0;
 #pragma unroll
@@ -113,49 +119,64 @@ __device__ __forceinline__ void fused_drain(const KvArgs& a, const KvReduceArgs&
       }
       if (up) base += hf;
     }
+    cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 4);
     cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 2);
     cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 1);
-    if ((lane & 3) == 0) red[lg * NPAD + col0 + base] = cs[0];
+    if ((lane & 7) == 0) red[lg * NPAD + col0 + base] = cs[0];
   }
-  rd[half * 128 + lg * 32 + lane] = rowdot;
-  eval_bar();
-  for (int j = tid; j < a.m; j += 256)
+  rd[qtr * 128 + lg * 32 + lane] = rowdot;
+  eval_bar<EW>();
+  for (int j = tid; j < a.m; j += 32 * EW)
     f.dpart[static_cast<size_t>(blockIdx.x) * a.m + j] = ((red[j] + red[NPAD + j]) + red[2 * NPAD + j]) + red[3 * NPAD + j];
-  if (half == 0) {
-    const double w = rd[lg * 32 + lane] + rd[128 + lg * 32 + lane];
+  if (qtr == 0) {
+    double w = rd[lg * 32 + lane];
+#pragma unroll
+    for (int p = 1; p < NQ; ++p) w += rd[p * 128 + lg * 32 + lane];
     double sc = row_ok ? w * w : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
     if (lane == 0) ssc[lg] = sc;
   }
-  eval_bar();
+  eval_bar<EW>();
   if (tid == 0) {
     f.spart[blockIdx.x] = ((ssc[0] + ssc[1]) + ssc[2]) + ssc[3];
     __threadfence();
     *last = (atomicAdd(f.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
   }
-  eval_bar();
+  eval_bar<EW>();
   if (!*last) return;
   __threadfence();
-  ap_epilogue(f, static_cast<int>(gridDim.x), tid, 8, ss, bscore, [] { eval_bar(); });
+  ap_epilogue(f, static_cast<int>(gridDim.x), tid, EW, ss, bscore, [] { eval_bar<EW>(); });
 }
 
+template <bool FUSED>
+struct TcRoles {
+  static constexpr int EW = FUSED ? 16 : EVAL_WARPS;  // evaluation warps
+  static constexpr int THREADS = 32 * (EW + 2);
+  static constexpr int CPT = TBK * 4 / EW;            // chunk columns per eval thread
+};
+
 template <int NPAD, int DP4, bool FUSED>
-__global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk,
-                                                            const KvReduceArgs f) {
+__global__ void __launch_bounds__(TcRoles<FUSED>::THREADS, FUSED ? 1 : 2)
+    kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk, const KvReduceArgs f) {
+  constexpr int EW = TcRoles<FUSED>::EW, CPT = TcRoles<FUSED>::CPT;
   constexpr int DP = 4 * DP4;
   using L = TcLayout<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // the fused AP slab runs one CTA per SM: 4 TMEM A buffers (512 columns)
+  constexpr int NAB = FUSED ? 4 : 2;
+  constexpr int TCOLS = FUSED ? 512 : TMEM_COLS;
   float* smB = reinterpret_cast<float*>(smem_raw);                    // [STAGES][CHUNK_FLOATS]
   float* smX = smB + STAGES * L::CHUNK_FLOATS;                        // [STAGES][TBK][DP]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * TBK * DP);
   uint64_t* full = bars;              // [STAGES]
   uint64_t* empty = bars + STAGES;    // [STAGES]
-  uint64_t* a_full = bars + 2 * STAGES;       // [2]
-  uint64_t* a_empty = bars + 2 * STAGES + 2;  // [2]
-  uint64_t* d_full = bars + 2 * STAGES + 4;
-  uint64_t* d_empty = bars + 2 * STAGES + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 6);
+  uint64_t* a_full = bars + 2 * STAGES;         // [NAB]
+  uint64_t* a_empty = bars + 2 * STAGES + 4;    // [NAB]
+  uint64_t* d_full = bars + 2 * STAGES + 8;
+  uint64_t* d_empty = bars + 2 * STAGES + 9;
+  uint64_t* base_full = bars + 2 * STAGES + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 11);
 
   if (a.skip && *a.skip) return;
   int c0 = a.c0, C = a.C;
@@ -180,17 +201,18 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&a_full[b], EVAL_WARPS);
+    for (int b = 0; b < NAB; ++b) {
+      mbar_init(&a_full[b], EW);
       mbar_init(&a_empty[b], 1);
     }
     mbar_init(d_full, 1);
-    mbar_init(d_empty, EVAL_WARPS);
+    mbar_init(d_empty, EW);
+    if (FUSED) mbar_init(base_full, 1);  // base tile landed
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(TMEM_COLS)
+                 "n"(TCOLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -201,7 +223,21 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
   const int flush = a.flush_chunks;
   const int ngroups = (nq + flush - 1) / flush;
 
-  if (warp == 8) {
+  // fused AP slab: the tile's rows of `base` (the residual) are staged in smem
+  // by one bulk copy issued before the chunk loop, so the drain never waits on
+  // global loads; sbase sits behind the drain scratch.
+  double* sbase = reinterpret_cast<double*>(bars + 64) + FUSED_SCRATCH_DOUBLES;
+  bool base_staged = false;
+  if constexpr (FUSED) {
+    const int rows = min(TBM, a.R - tile * TBM);
+    const uint32_t bytes = static_cast<uint32_t>(rows) * f.ldb * 8u;
+    base_staged = f.base && f.ldb == a.m && a.m <= 96 && (bytes % 16u) == 0u;
+    if (base_staged && warp == EW && lane == 0) {
+      mbar_expect_tx(base_full, bytes);
+      bulk_g2s(sbase, f.base + static_cast<size_t>(tile) * TBM * f.ldb, bytes, base_full);
+    }
+  }
+  if (warp == EW) {
     // ---------------- producer ----------------
     if (lane == 0) {
       for (int k = 0; k < nq; ++k) {
@@ -215,17 +251,17 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
         bulk_g2s(smX + s * TBK * DP, a.xs + static_cast<size_t>(c0 + cb + k * TBK) * DP, xbytes, &full[s]);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == EW + 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
       for (int k = 0; k < nq; ++k) {
-        const int s = k % STAGES, b = k & 1;
+        const int s = k % STAGES, b = k % NAB;
         const int g = k / flush;
         const bool first_in_group = (k % flush) == 0;
         const bool last_in_group = ((k + 1) % flush) == 0 || k + 1 == nq;
         mbar_wait(&full[s], (k / STAGES) & 1);
-        mbar_wait(&a_full[b], (k / 2) & 1);
+        mbar_wait(&a_full[b], (k / NAB) & 1);
         if (first_in_group && g > 0) mbar_wait(d_empty, (g - 1) & 1);
         tc_fence_after();
         const uint32_t bh = smem_u32(smB + s * L::CHUNK_FLOATS);
@@ -248,7 +284,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
   } else {
     // ---------------- evaluation + epilogue warps ----------------
     const int lg = warp & 3;           // TMEM lane group
-    const int half = warp >> 2;        // chunk columns [16*half, 16*half + 16)
+    const int half = warp >> 2;        // chunk columns [CPT*half, CPT*half + CPT)
     const int row = lg * 32 + lane;    // row within the tile == TMEM lane
     const int er = tile * TBM + row;
     const int er_c = er < a.R ? er : 0;
@@ -271,14 +307,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
     bool wrote = false;
 
     for (int k = 0; k < nq; ++k) {
-      const int s = k % STAGES, b = k & 1;
+      const int s = k % STAGES, b = k % NAB;
       mbar_wait(&full[s], (k / STAGES) & 1);
-      if (k >= 2) mbar_wait(&a_empty[b], ((k - 2) / 2) & 1);
+      if (k >= NAB) mbar_wait(&a_empty[b], ((k - NAB) / NAB) & 1);
       tc_fence_after();
-      const float* xc = smX + s * TBK * DP + half * 16 * DP;
-      uint32_t hi[16], lo[16];
+      const float* xc = smX + s * TBK * DP + half * CPT * DP;
+      uint32_t hi[CPT], lo[CPT];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
+      for (int t = 0; t < CPT; ++t) {
 #if GPK_EVAL_F32X2
         // packed FP32x2 (FADD2/FFMA2): two dimensions per instruction
         uint64_t acc0 = 0ull, acc1 = 0ull;
@@ -318,9 +354,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
         hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
         lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
       }
-      const uint32_t abase = tmem + lane_addr + A_BASE + b * 64 + half * 16;
-      tc_st16(abase, hi);
-      tc_st16(abase + 32, lo);
+      const uint32_t abase = tmem + lane_addr + A_BASE + b * 64 + half * CPT;
+      if constexpr (CPT == 16) {
+        tc_st16(abase, hi);
+        tc_st16(abase + 32, lo);
+      } else {
+        tc_st8(abase, hi);
+        tc_st8(abase + 32, lo);
+      }
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -333,7 +374,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
         tc_fence_after();
         if constexpr (FUSED) {
           // single accumulation group (host guarantees): D holds the whole slab
-          fused_drain<NPAD>(a, f, tmem + lane_addr, er, gi, c0, C, half, lg, lane, warp, reinterpret_cast<double*>(bars + 64));
+          if (base_staged) mbar_wait(base_full, 0);
+          fused_drain<NPAD, EW>(a, f, tmem + lane_addr, er, gi, c0, C, half, lg, lane, warp,
+                            reinterpret_cast<double*>(bars + 64), base_staged ? sbase : nullptr);
         } else {
         const bool row_ok = er < a.R;
         double* prow = part + static_cast<size_t>(er_c) * a.m;
@@ -368,7 +411,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) kv_tc_kernel(const KvArgs a, cons
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS) : "memory");
   }
 }
 
@@ -415,8 +458,8 @@ template <int NPAD, int DP4, bool FUSED>
 void launch_tc_one(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   using L = TcLayout<NPAD>;
   // + the fused drain's scratch behind the barriers (bars + 64 words: ~14 KB)
-  const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 16 * sizeof(uint64_t) +
-                      (FUSED ? 64 * sizeof(uint64_t) + sizeof(double) * (4 * NPAD + 256 + 8 + 96 + 1024) + 16 : 0);
+  const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 32 * sizeof(uint64_t) +
+                      (FUSED ? 64 * sizeof(uint64_t) + sizeof(double) * (FUSED_SCRATCH_DOUBLES + TBM * 96) : 0);
   // at most 2 CTAs per SM: each allocates 256 of the 512 TMEM columns
   const size_t smem = std::max<size_t>(need, 100 * 1024);
   static bool configured = false;
@@ -426,7 +469,7 @@ void launch_tc_one(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cud
     configured = true;
   }
   dim3 grid((a.R + TBM - 1) / TBM, a.splits);
-  kv_tc_kernel<NPAD, DP4, FUSED><<<grid, NTHREADS, smem, s>>>(a, vpk, f);
+  kv_tc_kernel<NPAD, DP4, FUSED><<<grid, TcRoles<FUSED>::THREADS, smem, s>>>(a, vpk, f);
   check_launch("kv_tc_kernel");
 }
 
