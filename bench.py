@@ -12,9 +12,16 @@ of the n x 65 system -> fused gradient pass -> Adam, all device-resident.
               (256 MiB write) between timed steps.
   e2e         the same metric through the public C-ABI call gpk_optimise on
               host buffers (dataset H2D and trace D2H inside the timed region).
-  roofline    fused K.V kernel (kv_slab_kernel): algorithmic FP32 flops
-              (2m + 3d + 6 per entry) / summed CUDA-event launch time, against
-              the FP32 SIMT peak 148 SM x 128 lanes x 2 x measured SM clock.
+  roofline    fused K.V kernel (kv_tc_kernel): it evaluates every kernel
+              entry on the FP32 pipe (ARD distance, sqrt, exp: 3d + 6 flops per
+              entry) and contracts K.V (2m flops per entry) on the tcgen05
+              tensor cores, so its binding roofline is the FP32 SIMT pipe:
+              achieved = FP32-pipe flops (3d + 6 per executed entry, counted on
+              the device) / summed CUDA-event launch time, against the FP32
+              peak 148 SM x 128 lanes x 2 x measured SM clock. The
+              FP32-equivalent rate of the whole fused K.V product
+              (2m + 3d + 6 per entry, the north star's "FP32 compute" metric)
+              is reported beside it as fp32_equivalent_tflops.
   cpu_baseline the FP64 oracle (restated reference, C++) on the host cores,
               one H.V row slab per sample.
 
@@ -275,7 +282,8 @@ def run_ours(args, world, rank, local):
     clk = clocks.summary()
     f_sm = (clk["sm_mhz"] or 1965.0) * 1e6
     peak = 148 * 128 * 2 * f_sm / 1e12
-    achieved = st["flops"] / (st["kv_ms"] / 1e3) / 1e12 if st["kv_ms"] > 0 else None
+    achieved = st["fp32_pipe_flops"] / (st["kv_ms"] / 1e3) / 1e12 if st["kv_ms"] > 0 else None
+    fp32_equiv = st["flops"] / (st["kv_ms"] / 1e3) / 1e12 if st["kv_ms"] > 0 else None
     iters = [int(t["iterations"][0]) for t in traces]
     epochs = [float(t["epochs"][0]) for t in traces]
     traffic = None
@@ -319,6 +327,10 @@ def run_ours(args, world, rank, local):
                              "traffic": traffic,
                              "peak_source": "148 SM x 128 FP32 lanes x 2 x median SM clock under load "
                                             "(MEASURED_PEAKS.json holds no FP32 SIMT figure)",
+                             "achieved_counts": "FP32-pipe flops only: 3d+6 per kernel entry (the 2m-flop K.V "
+                                                "contraction runs on tcgen05)",
+                             "fp32_equivalent_tflops": fp32_equiv,
+                             "fp32_equivalent_frac": (fp32_equiv / peak) if fp32_equiv else None,
                              "kv_launches": st["kv_launches"], "kv_ms": st["kv_ms"],
                              "kv_share_of_step": st["kv_ms"] / ms if ms > 0 else None},
                 "cpu_baseline": cpu,

@@ -100,7 +100,11 @@ gpk_status gpk_ctx_set_profiling(gpk_ctx* ctx, int enable);
  * (kv_tc_kernel; K evaluated into TMEM, contraction on the tensor cores). */
 gpk_status gpk_ctx_set_operator_kernel(gpk_ctx* ctx, int kernel);
 gpk_status gpk_ctx_reset_stats(gpk_ctx* ctx);
-gpk_status gpk_ctx_stats(gpk_ctx* ctx, double* out4);
+/* out5: [evals x RHS, FP32-equivalent operator flops (2m + 3d + 6 per kernel
+ * entry), profiled operator launches, profiled operator ms, flops executed on
+ * the FP32 pipe (3d + 6 per entry on the tcgen05 kernel, whose 2m-flop
+ * contraction runs on the tensor cores; all of them on the SIMT kernel)]. */
+gpk_status gpk_ctx_stats(gpk_ctx* ctx, double* out5);
 
 /* ---- multi-GPU (row-sharded; one process per GPU) ----------------------
  * Rank 0 calls gpk_comm_unique_id and ships the 128 bytes to every rank out

@@ -1546,8 +1546,8 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     GPK_CUDA(cudaMallocHost(&c->ctl_host, 2 * sizeof(CgCtl)));
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev[0], cudaEventDisableTiming));
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev[1], cudaEventDisableTiming));
-    GPK_CUDA(cudaMalloc(&c->stats, 2 * sizeof(double)));
-    GPK_CUDA(cudaMemset(c->stats, 0, 2 * sizeof(double)));
+    GPK_CUDA(cudaMalloc(&c->stats, 3 * sizeof(double)));
+    GPK_CUDA(cudaMemset(c->stats, 0, 3 * sizeof(double)));
     *out = c.release();
   });
 }
@@ -1595,7 +1595,7 @@ gpk_status gpk_ctx_reset_stats(gpk_ctx* c) {
   return guarded([&] {
     GPK_CUDA(cudaSetDevice(c->device));
     GPK_CUDA(cudaStreamSynchronize(c->stream));
-    GPK_CUDA(cudaMemset(c->stats, 0, 2 * sizeof(double)));
+    GPK_CUDA(cudaMemset(c->stats, 0, 3 * sizeof(double)));
     c->prof_used = 0;
   });
 }
@@ -1603,7 +1603,11 @@ gpk_status gpk_ctx_stats(gpk_ctx* c, double* out) {
   return guarded([&] {
     GPK_CUDA(cudaSetDevice(c->device));
     GPK_CUDA(cudaStreamSynchronize(c->stream));
-    GPK_CUDA(cudaMemcpy(out, c->stats, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+    double dev[3];
+    GPK_CUDA(cudaMemcpy(dev, c->stats, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    out[0] = dev[0];
+    out[1] = dev[1];
+    out[4] = dev[2];
     double ms = 0.0;
     for (size_t i = 0; i < c->prof_used; ++i) {
       float t = 0.f;

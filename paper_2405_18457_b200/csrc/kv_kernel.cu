@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(NT, (TC >= 8 ? 1 : 2)) kv_slab_kernel(const Kv
     const double entries = static_cast<double>(a.R) * C;
     atomicAdd(a.stats, entries * a.m);
     atomicAdd(a.stats + 1, entries * (2.0 * a.m + 3.0 * a.d + 6.0));
+    atomicAdd(a.stats + 2, entries * (2.0 * a.m + 3.0 * a.d + 6.0));  // all on the FP32 pipe
   }
 
   // ---- evaluation role: this thread's K row ----

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(TcRoles<FUSED>::THREADS, FUSED ? 1 : 2)
     const double entries = static_cast<double>(a.R) * C;
     atomicAdd(a.stats, entries * a.m);
     atomicAdd(a.stats + 1, entries * (2.0 * a.m + 3.0 * a.d + 6.0));
+    atomicAdd(a.stats + 2, entries * (3.0 * a.d + 6.0));  // FP32 pipe share; the 2m contraction is on tcgen05
   }
 
   if (tid == 0) {

@@ -142,10 +142,12 @@ class Context:
         check(self._lib.gpk_ctx_reset_stats(self.handle))
 
     def stats(self):
-        """K.V operator counters: evals x RHS, algorithmic flops, profiled launches, profiled ms."""
-        out = np.zeros(4)
+        """K.V operator counters: evals x RHS, FP32-equivalent flops (2m+3d+6 per entry), profiled
+        launches, profiled ms, flops on the FP32 pipe (3d+6 per entry on the tcgen05 kernel)."""
+        out = np.zeros(5)
         check(self._lib.gpk_ctx_stats(self.handle, _p(out)))
-        return {"evals_x_rhs": out[0], "flops": out[1], "kv_launches": int(out[2]), "kv_ms": out[3]}
+        return {"evals_x_rhs": out[0], "flops": out[1], "kv_launches": int(out[2]), "kv_ms": out[3],
+                "fp32_pipe_flops": out[4]}
 
     def close(self):
         if getattr(self, "handle", None):
