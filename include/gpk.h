@@ -285,6 +285,13 @@ gpk_status gpk_sinsum_dataset(int n, int d, int uniform, double noise, uint64_t 
  * header, columns and shortest round-trip doubles (test columns empty). */
 gpk_status gpk_write_trace_csv(const char* path, const double* trace, int rows, int d);
 
+/* Batched SPD inverse used for the AP diagonal blocks (host buffers, batch
+ * column-major dim x dim matrices). mode 1: recursive Schur complement with
+ * strided-batched DGEMMs (the solver's default); mode 0: cuSOLVER
+ * potrfBatched + two batched triangular solves. GPK_ENUMERIC if a matrix is
+ * not positive definite. Exposed for testing the block solves. */
+gpk_status gpk_spd_inverse(gpk_ctx* ctx, const double* mats, int dim, int batch, int mode, double* inv);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,6 +113,7 @@ def _sig(lib):
         "gpk_sample_posterior": (C.c_int, [H, H, dp, C.c_int, dp, dp, C.c_int, dp]),
         "gpk_test_metrics": (C.c_int, [H, H, dp, C.c_int, dp, dp, dp, C.c_int, C.c_double, dp]),
         "gpk_write_trace_csv": (C.c_int, [C.c_char_p, dp, C.c_int, C.c_int]),
+        "gpk_spd_inverse": (C.c_int, [vp, dp, C.c_int, C.c_int, C.c_int, dp]),
         "gpk_sinsum_dataset": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                          C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     }

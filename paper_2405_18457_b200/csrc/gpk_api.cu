@@ -91,10 +91,15 @@ struct gpk_ctx {
   size_t prof_used = 0;
   int kernel = 1;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32 (default)
   bool fused_ap = true;  // AP slabs: reduce + epilogue fused into the tcgen05 kernel
+  int spd_inverse = 1;   // AP block inverses: 1 recursive Schur/DGEMM, 0 cuSOLVER potrf + 2 trsm
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
   DBuf<double> rff_feat;  // RFF feature rows (prior GEMM), reused across calls
   int* info_host = nullptr;    // pinned
+  // auxiliary stream: AP block factorisation runs here, overlapped with the
+  // pathwise targets and the residual refresh on the main stream
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_m2a = nullptr, ev_aux = nullptr;
   ncclComm_t comm = nullptr;   // multi-GPU (one process per GPU)
   int nranks = 1, rank = 0;
 };
@@ -105,6 +110,7 @@ struct gpk_operator {
   // built by the sharded optimiser have nr > 1.
   int nr = 1, rk = 0, row0 = 0, nloc = 0, S = 0;
   bool sharded = false;  // built by the optimiser on a context with a communicator
+  uint64_t hyper_version = 0;  // bumped by every set_hyper (AP block inverses are keyed on it)
   // gradient-pass workspace (persistent across steps)
   DBuf<float> gbuf[4];
   DBuf<double> gpart, gtot, gdots;
@@ -145,7 +151,7 @@ struct gpk_batch {
   std::vector<double> scales;
   DBuf<double> scales_dev;
   // solver workspace
-  DBuf<double> w1, w2, w3, w4, red, vec1, vec2, vec3;
+  DBuf<double> w1, w2, w3, w4, w5, red, vec1, vec2, vec3;
   DBuf<float> f32;
   DBuf<CgCtl> ctl;
   DBuf<int> ibuf, ibuf2, flag;
@@ -154,6 +160,10 @@ struct gpk_batch {
   DBuf<unsigned> ticket;             // last-block ticket of fused reductions (kept at 0 between uses)
   DBuf<float> apk;                   // AP block update's TF32 operator images
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
+  // AP block inverses enqueued on the auxiliary stream (ap_prepare)
+  bool ap_ready = false;
+  int ap_block = 0;
+  uint64_t ap_version = 0;
 };
 
 struct gpk_rff_basis {
@@ -270,6 +280,7 @@ void set_hyper(gpk_operator* op, const double* raw) {
       throw InvalidArgument("Hyperparameters: constrained value " + std::to_string(k) + " is not finite and positive");
   }
   op->raw = r;
+  ++op->hyper_version;
   op->inv_ls.resize(d);
   for (int k = 0; k < d; ++k) op->inv_ls[k] = 1.0 / softplus(r[k]);
   op->s = softplus(r[d]);
@@ -668,6 +679,45 @@ void validate(const gpk_solver_config* c) {  // linear_system.cpp:7-14
 
 using Clock = std::chrono::steady_clock;
 
+// GPK_PHASE_TIMING=1: synchronising phase timer for the outer step (stderr,
+// one JSON line per step). Diagnostic only; off by default.
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t stream = nullptr;
+  Clock::time_point last;
+  std::string line;
+  static bool enabled() {
+    static const bool e = [] {
+      const char* v = std::getenv("GPK_PHASE_TIMING");
+      return v && std::atoi(v) != 0;
+    }();
+    return e;
+  }
+  void start(cudaStream_t s) {
+    on = enabled();
+    if (!on) return;
+    stream = s;
+    cudaStreamSynchronize(s);
+    last = Clock::now();
+    line = "{";
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(stream);
+    const auto now = Clock::now();
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), "%s\"%s\": %.1f", line.size() > 1 ? ", " : "", name,
+                  std::chrono::duration<double, std::micro>(now - last).count());
+    line += buf;
+    last = now;
+  }
+  void finish() {
+    if (!on) return;
+    std::fprintf(stderr, "%s}\n", line.c_str());
+  }
+};
+PhaseTimer g_phase;
+
 void finalise(gpk_batch* b, double tol, gpk_solver_report* rep, Clock::time_point start) {
   int done;
   batch_norms(b, b->residuals.p, tol, &rep->mean_residual_norm, &rep->probe_residual_norm, &done);
@@ -794,32 +844,35 @@ void solve_cg(gpk_batch* b, const gpk_solver_config* c, gpk_precond* pc, gpk_sol
 }
 
 // SPD inverses of `batch` dim x dim matrices (in place input destroyed).
-void spd_inverse_batched(gpk_ctx* ctx, double* mats, int dim, int batch, double* inv) {
-  cudaStream_t s = ctx->stream;
-  GPK_CUDA(cudaSetDevice(ctx->device));
-  if (cusolverDnSetStream(ctx->solver, s) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnSetStream");
-  if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
-  std::vector<double*> ha(2 * batch);
-  for (int k = 0; k < batch; ++k) {
-    ha[k] = mats + static_cast<size_t>(k) * dim * dim;
-    ha[batch + k] = inv + static_cast<size_t>(k) * dim * dim;
+__global__ void fill_ptrs_kernel(double** p, double* a, double* b, long long stride, int batch) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < batch; k += gridDim.x * blockDim.x) {
+    p[k] = a + k * stride;
+    p[batch + k] = b + k * stride;
   }
+}
+
+// Batched SPD inverse on stream `st` without host synchronisation: cuSOLVER
+// potrfBatched (L L^T), then L^{-1} and L^{-T} L^{-1} by two batched
+// triangular solves against the identity. Pointer arrays are filled on the
+// device; the per-matrix info goes to pinned host memory and is checked by
+// the caller after its next synchronisation (spd_inverse_check).
+void spd_inverse_batched(gpk_ctx* ctx, cudaStream_t st, double* mats, int dim, int batch, double* inv) {
+  GPK_CUDA(cudaSetDevice(ctx->device));
+  if (batch > 4096) throw InvalidArgument("gpk: at most 4096 AP blocks");
+  if (cusolverDnSetStream(ctx->solver, st) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnSetStream");
+  if (cublasSetStream(ctx->blas, st) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
   double** da = ctx->ptr_a.ensure(2 * batch);
   double** db = da + batch;
   int* info = ctx->info.ensure(batch);
   if (!ctx->info_host) GPK_CUDA(cudaMallocHost(&ctx->info_host, sizeof(int) * 4096));
-  if (batch > 4096) throw InvalidArgument("gpk: at most 4096 AP blocks");
-  GPK_CUDA(cudaMemcpyAsync(da, ha.data(), sizeof(double*) * 2 * batch, cudaMemcpyHostToDevice, s));
+  fill_ptrs_kernel<<<(batch + 255) / 256, 256, 0, st>>>(da, mats, inv, static_cast<long long>(dim) * dim, batch);
+  check_launch("fill_ptrs");
   if (cusolverDnDpotrfBatched(ctx->solver, CUBLAS_FILL_MODE_LOWER, dim, da, dim, info, batch) !=
       CUSOLVER_STATUS_SUCCESS)
     throw CudaError("cusolverDnDpotrfBatched");
   count_launch();
-  GPK_CUDA(cudaMemcpyAsync(ctx->info_host, info, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
-  set_identity_launch(inv, dim, batch, s);
-  GPK_CUDA(cudaStreamSynchronize(s));  // ha lifetime + info check
-  for (int k = 0; k < batch; ++k)
-    if (ctx->info_host[k] != 0)
-      throw NumericError("solve_ap: block Cholesky failed; block is not positive definite (noise scale too small)");
+  GPK_CUDA(cudaMemcpyAsync(ctx->info_host, info, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+  set_identity_launch(inv, dim, batch, st);
   const double one = 1.0;
   if (cublasDtrsmBatched(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, dim,
                          dim, &one, da, dim, db, dim, batch) != CUBLAS_STATUS_SUCCESS)
@@ -828,6 +881,109 @@ void spd_inverse_batched(gpk_ctx* ctx, double* mats, int dim, int batch, double*
                          dim, &one, da, dim, db, dim, batch) != CUBLAS_STATUS_SUCCESS)
     throw CudaError("cublasDtrsmBatched");
   count_launch(2);
+  if (cusolverDnSetStream(ctx->solver, ctx->stream) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnSetStream");
+  if (cublasSetStream(ctx->blas, ctx->stream) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+}
+// Batched SPD inverse by recursive 2 x 2 blocking on the Schur complement
+// (no factorisation kernels, all level-3 work in strided-batched DGEMMs):
+//   B11 = inv(A11); X = B11 A12; S = A22 - A21 X; B22 = inv(S);
+//   B12 = -X B22; B11 -= B12 X^T; B21 = B12^T,
+// down to <= 64 x 64 leaves inverted in shared memory. A (column-major,
+// ld = dim, stride dim^2) is destroyed; B receives the inverse. Same
+// arithmetic class as the reference's Cholesky block solve (FP64, SPD, no
+// pivoting); ~dim^3 flops per matrix. The info array stays zero unless a
+// leaf pivot is non-positive (checked after the solve by spd_inverse_check).
+struct SpdRec {
+  gpk_ctx* ctx;
+  cudaStream_t st;
+  double* A;
+  double* B;
+  double* X;  // scratch: every recursion level owns its X (n1 x n2) at its own offset
+  int* info;  // per matrix: 1 if a leaf pivot was not positive
+  int ld, batch;
+  long long stride, xstride;
+  void gemm(cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, double alpha, const double* a, int lda,
+            const double* b, int ldb, double beta, double* c, int ldc, long long sa, long long sb, long long sc) {
+    if (cublasDgemmStridedBatched(ctx->blas, ta, tb, m, n, k, &alpha, a, lda, sa, b, ldb, sb, &beta, c, ldc, sc,
+                                  batch) != CUBLAS_STATUS_SUCCESS)
+      throw CudaError("cublasDgemmStridedBatched (SPD inverse)");
+    count_launch();
+  }
+  void inv(int off, int nn, long long xoff) {
+    if (nn <= 64) {
+      spd_leaf_inverse_launch(A, B, off, nn, ld, stride, batch, info, st);
+      count_launch();
+      return;
+    }
+    const int n1 = ((nn / 2) + 31) / 32 * 32, n2 = nn - n1;
+    double* x = X + xoff;
+    const long long child = xoff + static_cast<long long>(n1) * n2;  // deeper levels' scratch
+    auto at = [&](double* base, int r, int c) { return base + r + static_cast<size_t>(c) * ld; };
+    inv(off, n1, child);                                                     // B11
+    gemm(CUBLAS_OP_N, CUBLAS_OP_N, n1, n2, n1, 1.0, at(B, off, off), ld, at(A, off, off + n1), ld, 0.0, x, n1, stride,
+         stride, xstride);                                                   // X = B11 A12
+    gemm(CUBLAS_OP_N, CUBLAS_OP_N, n2, n2, n1, -1.0, at(A, off + n1, off), ld, x, n1, 1.0, at(A, off + n1, off + n1), ld,
+         stride, xstride, stride);                                           // S = A22 - A21 X
+    inv(off + n1, n2, child);                                                // B22 = inv(S)
+    gemm(CUBLAS_OP_N, CUBLAS_OP_N, n1, n2, n2, -1.0, x, n1, at(B, off + n1, off + n1), ld, 0.0, at(B, off, off + n1), ld,
+         xstride, stride, stride);                                           // B12 = -X B22
+    gemm(CUBLAS_OP_N, CUBLAS_OP_T, n1, n1, n2, -1.0, at(B, off, off + n1), ld, x, n1, 1.0, at(B, off, off), ld, stride,
+         xstride, stride);                                                   // B11 -= B12 X^T
+    block_transpose_launch(at(B, off, off + n1), at(B, off + n1, off), n2, n1, ld, stride, batch, st);  // B21
+    count_launch();
+  }
+};
+
+// scratch doubles per matrix for the recursion (sum of every level's n1 x n2)
+long long spd_inverse_scratch(int nn) {
+  if (nn <= 64) return 0;
+  const int n1 = ((nn / 2) + 31) / 32 * 32, n2 = nn - n1;
+  return static_cast<long long>(n1) * n2 + std::max(spd_inverse_scratch(n1), spd_inverse_scratch(n2));
+}
+
+void spd_inverse_recursive(gpk_ctx* ctx, cudaStream_t st, double* mats, int dim, int batch, double* inv,
+                           double* scratch) {
+  if (cublasSetStream(ctx->blas, st) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+  if (batch > 4096) throw InvalidArgument("gpk: at most 4096 AP blocks");
+  if (!ctx->info_host) GPK_CUDA(cudaMallocHost(&ctx->info_host, sizeof(int) * 4096));
+  int* info = ctx->info.ensure(batch);
+  GPK_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * batch, st));
+  SpdRec r{ctx, st, mats, inv, scratch, info, dim, batch, static_cast<long long>(dim) * dim,
+           std::max<long long>(1, spd_inverse_scratch(dim))};
+  r.inv(0, dim, 0);
+  GPK_CUDA(cudaMemcpyAsync(ctx->info_host, info, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+  if (cublasSetStream(ctx->blas, ctx->stream) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+}
+
+void spd_inverse_check(gpk_ctx* ctx, int batch) {  // after a synchronisation that covers the aux stream
+  for (int k = 0; k < batch; ++k)
+    if (ctx->info_host[k] != 0)
+      throw NumericError("solve_ap: block Cholesky failed; block is not positive definite (noise scale too small)");
+}
+
+// Enqueues every AP diagonal block H[blk, blk] and its FP64 inverse on the
+// auxiliary stream (after the main stream's pending work: the scaled inputs),
+// keyed on the operator's hyperparameter version; solve_ap joins on ev_aux.
+void ap_prepare(gpk_batch* b, int block) {
+  gpk_operator* op = b->op;
+  gpk_ctx* ctx = op->ctx;
+  const int n = b->n, nblocks = (n + block - 1) / block;
+  const size_t bb = static_cast<size_t>(block) * block;
+  double* mats = b->w1.ensure(bb * nblocks);
+  double* inv = b->blocks.ensure(bb * nblocks);
+  GPK_CUDA(cudaEventRecord(ctx->ev_m2a, ctx->stream));
+  GPK_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_m2a, 0));
+  ap_blocks_launch(op->xs64.p, n, op->d, op->s2, op->sigma2, block, nblocks, mats, ctx->aux);
+  if (ctx->spd_inverse == 1) {
+    const size_t xs = static_cast<size_t>(std::max<long long>(1, spd_inverse_scratch(block)));
+    spd_inverse_recursive(ctx, ctx->aux, mats, block, nblocks, inv, b->w5.ensure(xs * nblocks));
+  } else {
+    spd_inverse_batched(ctx, ctx->aux, mats, block, nblocks, inv);
+  }
+  GPK_CUDA(cudaEventRecord(ctx->ev_aux, ctx->aux));
+  b->ap_ready = true;
+  b->ap_block = block;
+  b->ap_version = op->hyper_version;
 }
 
 void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) {
@@ -844,13 +1000,12 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   const double max_iterations = static_cast<double>(c->max_epochs) * n / block;  // solvers.cpp:118
   const int budget = static_cast<int>(std::ceil(max_iterations));
   const bool tc = ctx->kernel == 1;
-  // inverse of every diagonal block H[blk, blk] (FP64), computed once per call
+  // inverse of every diagonal block H[blk, blk] (FP64), on the auxiliary
+  // stream (possibly enqueued earlier by the optimiser: ap_prepare)
   const size_t bb = static_cast<size_t>(block) * block;
-  double* mats = b->w1.ensure(bb * nblocks);
-  double* inv = b->blocks.ensure(bb * nblocks);
-  GPK_CUDA(cudaMemsetAsync(mats, 0, sizeof(double) * bb * nblocks, s));
-  ap_blocks_launch(op->xs64.p, n, op->d, op->s2, op->sigma2, block, nblocks, mats, s);
-  spd_inverse_batched(ctx, mats, block, nblocks, inv);
+  if (!(b->ap_ready && b->ap_block == block && b->ap_version == op->hyper_version)) ap_prepare(b, block);
+  b->ap_ready = false;  // consumed by this solve
+  double* inv = b->blocks.p;
   std::vector<double> inv_scales(m);
   for (int j = 0; j < m; ++j) inv_scales[j] = 1.0 / b->scales[j];
   double* inv_scales_dev = b->vec1.ensure(m);
@@ -928,6 +1083,8 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     run_kv(op, kc);
   }
 
+  GPK_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // block inverses ready before the first update
+  g_phase.mark("ap_refresh_and_inverse");
   if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
   auto iteration = [&]() {  // solvers.cpp:120-140
     if (tc) {
@@ -1012,6 +1169,8 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     ap_check_launch(part, groups, m, b->scales_dev.p, c->tolerance, ctl, s);
   };
   drive(b, ctl, 8, budget, iteration);
+  g_phase.mark("ap_iterations");
+  spd_inverse_check(ctx, nblocks);
   const CgCtl h = read_ctl(b);
   rep->iterations = h.iters;
   rep->epochs_consumed = static_cast<double>(h.iters) * block / n;
@@ -1539,8 +1698,12 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     if (prop.major != 10) throw CudaError("gpk: libgpk is built for sm_100a (B200); device is sm_" +
                                           std::to_string(prop.major) + std::to_string(prop.minor));
     c->sms = prop.multiProcessorCount;
-    if (const char* e = std::getenv("GPK_FUSED_AP")) c->fused_ap = std::atoi(e) != 0;  // A/B switch
+    if (const char* e = std::getenv("GPK_FUSED_AP")) c->fused_ap = std::atoi(e) != 0;  // A/B switches
+    if (const char* e = std::getenv("GPK_SPD_INVERSE")) c->spd_inverse = std::atoi(e);
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    GPK_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    GPK_CUDA(cudaEventCreateWithFlags(&c->ev_m2a, cudaEventDisableTiming));
+    GPK_CUDA(cudaEventCreateWithFlags(&c->ev_aux, cudaEventDisableTiming));
     if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate");
     if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate");
     GPK_CUDA(cudaMallocHost(&c->ctl_host, 2 * sizeof(CgCtl)));
@@ -1557,6 +1720,7 @@ gpk_status gpk_ctx_destroy(gpk_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->aux);
     cublasDestroy(c->blas);
     cusolverDnDestroy(c->solver);
     cudaFreeHost(c->ctl_host);
@@ -1568,7 +1732,11 @@ gpk_status gpk_ctx_destroy(gpk_ctx* c) {
     }
     cudaFree(c->stats);
     if (c->comm) nccl().comm_destroy(c->comm);
+    cudaEventDestroy(c->ev_m2a);
+    cudaEventDestroy(c->ev_aux);
+    cudaStreamDestroy(c->aux);
     cudaStreamDestroy(c->stream);
+    if (c->info_host) cudaFreeHost(c->info_host);
     delete c;
   });
 }
@@ -2220,7 +2388,12 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
   const gpk_outer_config& cfg = o->cfg;
   const bool pathwise = cfg.estimator == 1;
   const size_t nm = static_cast<size_t>(nloc) * m;
+  g_phase.start(stream);
   set_hyper(op, o->raw.data());
+  // AP: factor the diagonal blocks on the auxiliary stream while the targets
+  // and the residual refresh run on the main stream
+  if (o->sc.kind == GPK_AP && !op->sharded) ap_prepare(b, std::min(o->sc.block_size, nloc));
+  g_phase.mark("set_hyper");
   const uint64_t substream = cfg.warm_start ? 0 : static_cast<uint64_t>(t);
   if (pathwise) {
     if (!o->basis || !cfg.warm_start) {
@@ -2236,6 +2409,7 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
       o->noise_sub = substream;
     }
     xi_assemble_launch(o->prior.p, o->noise.p, nloc, s, op->sigma, b->targets.p, m, 1, nullptr, stream);
+    g_phase.mark("targets");
   } else {
     if (!o->have_noise || !cfg.warm_start) {
       o->probes.ensure(static_cast<size_t>(nloc) * s);
@@ -2270,7 +2444,9 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
   o->sc.substream = static_cast<uint64_t>(t);
   o->sc.seed = cfg.solver_seed;
   gpk_solver_report rep{};
+  g_phase.mark("scales_warm");
   solve_dispatch(b, &o->sc, &rep);
+  g_phase.mark("solve");
   const double solver_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
   const int stride = 2 * P + 8;
   std::memset(row, 0, sizeof(double) * stride);
@@ -2297,6 +2473,7 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
     else
       f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1}, {b->solutions.p, b->targets.p, m, m, 1, s}});
     assemble(f, s, P, g.data(), nullptr, nullptr);
+    g_phase.mark("gradient");
     double inf = 0.0;
     for (int k = 0; k < P; ++k) {
       row[P + k] = g[k];
@@ -2318,6 +2495,8 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
     for (int k = 0; k < P; ++k) o->raw[k] += upd[k];
     GPK_CUDA(cudaMemcpyAsync(o->prev.p, b->solutions.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, stream));
     o->have_previous = true;
+    g_phase.mark("adam");
+    g_phase.finish();
   }
   GPK_CUDA(cudaStreamSynchronize(stream));
   row[2 * P + 6] = std::chrono::duration<double>(Clock::now() - t0).count();
@@ -2459,6 +2638,26 @@ gpk_status gpk_test_metrics(gpk_operator* op, gpk_rff_basis* basis, const double
       out4[1] = llh / p;
       out4[3] = out4[1] - std::log(target_scale);
     }
+  });
+}
+
+gpk_status gpk_spd_inverse(gpk_ctx* ctx, const double* mats, int dim, int batch, int mode, double* inv) {
+  return guarded([&] {
+    require(ctx && mats && inv && dim >= 1 && batch >= 1, "gpk_spd_inverse: invalid arguments");
+    GPK_CUDA(cudaSetDevice(ctx->device));
+    const size_t bb = static_cast<size_t>(dim) * dim * batch;
+    DBuf<double> a, o, x;
+    a.ensure(bb);
+    o.ensure(bb);
+    GPK_CUDA(cudaMemcpy(a.p, mats, sizeof(double) * bb, cudaMemcpyHostToDevice));
+    if (mode == 1)
+      spd_inverse_recursive(ctx, ctx->stream, a.p, dim, batch, o.p,
+                            x.ensure(static_cast<size_t>(std::max<long long>(1, spd_inverse_scratch(dim))) * batch));
+    else
+      spd_inverse_batched(ctx, ctx->stream, a.p, dim, batch, o.p);
+    GPK_CUDA(cudaStreamSynchronize(ctx->stream));
+    spd_inverse_check(ctx, batch);
+    GPK_CUDA(cudaMemcpy(inv, o.p, sizeof(double) * bb, cudaMemcpyDeviceToHost));
   });
 }
 

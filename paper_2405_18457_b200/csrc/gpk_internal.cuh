@@ -230,6 +230,10 @@ void dense_block64_launch(const double* xs64, int n, int d, double s2, double si
 
 void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks, double* mats,
                       cudaStream_t s);
+void spd_leaf_inverse_launch(const double* a, double* out, int off, int nn, int ld, long long stride, int batch,
+                             int* info, cudaStream_t s);
+void block_transpose_launch(const double* src, double* dst, int rows, int cols, int ld, long long stride, int batch,
+                            cudaStream_t s);
 void set_identity_launch(double* mats, int dim, int batch, cudaStream_t s);
 
 // AP (K8)

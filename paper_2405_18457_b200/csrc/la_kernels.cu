@@ -594,6 +594,73 @@ void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2
   check_launch("ap_blocks");
 }
 
+// Leaf of the recursive SPD inversion: the nn x nn (nn <= 64) diagonal
+// sub-block at (off, off) of every matrix (column-major, leading dimension ld,
+// matrix stride `stride`) is inverted in shared memory by Gauss-Jordan
+// elimination without pivoting (stable for SPD) and written to the same
+// sub-block of `out`. One CTA per matrix.
+__global__ void spd_leaf_inverse_kernel(const double* a, double* out, int off, int nn, int ld, long long stride,
+                                        int* info) {
+  __shared__ double M[64][65];
+  const double* A = a + blockIdx.x * stride + off + static_cast<size_t>(off) * ld;
+  double* B = out + blockIdx.x * stride + off + static_cast<size_t>(off) * ld;
+  for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) {
+    const int i = e % nn, j = e / nn;
+    M[i][j] = A[i + static_cast<size_t>(j) * ld];
+  }
+  __syncthreads();
+  for (int k = 0; k < nn; ++k) {
+    // a non-positive pivot (Schur complement diagonal) means the block is not SPD
+    if (threadIdx.x == 0 && !(M[k][k] > 0.0)) info[blockIdx.x] = 1;
+    const double piv = 1.0 / M[k][k];
+    // rank-1 elimination of every entry outside row/column k
+    for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) {
+      const int i = e % nn, j = e / nn;
+      if (i != k && j != k) M[i][j] = fma(-M[i][k] * piv, M[k][j], M[i][j]);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nn; t += blockDim.x) {
+      if (t != k) {
+        M[t][k] = -M[t][k] * piv;  // column k
+        M[k][t] = M[k][t] * piv;   // row k
+      }
+    }
+    if (threadIdx.x == 0) M[k][k] = piv;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) {
+    const int i = e % nn, j = e / nn;
+    B[i + static_cast<size_t>(j) * ld] = 0.5 * (M[i][j] + M[j][i]);  // symmetrise the rounding
+  }
+}
+void spd_leaf_inverse_launch(const double* a, double* out, int off, int nn, int ld, long long stride, int batch,
+                             int* info, cudaStream_t s) {
+  if (nn > 64) throw std::invalid_argument("spd_leaf_inverse: block > 64");
+  spd_leaf_inverse_kernel<<<batch, 256, 0, s>>>(a, out, off, nn, ld, stride, info);
+  check_launch("spd_leaf_inverse");
+}
+
+// dst (rows x cols block) = src^T (cols x rows block), per matrix.
+__global__ void block_transpose_kernel(const double* src, double* dst, int rows, int cols, int ld, long long stride) {
+  const long long per = static_cast<long long>(rows) * cols;
+  const long long total = per * gridDim.y;
+  (void)total;
+  const double* S = src + blockIdx.y * stride;
+  double* D = dst + blockIdx.y * stride;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < per;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % rows), j = static_cast<int>(e / rows);  // dst(i, j) = src(j, i)
+    D[i + static_cast<size_t>(j) * ld] = S[j + static_cast<size_t>(i) * ld];
+  }
+}
+void block_transpose_launch(const double* src, double* dst, int rows, int cols, int ld, long long stride, int batch,
+                            cudaStream_t s) {
+  const long long per = static_cast<long long>(rows) * cols;
+  dim3 grid(static_cast<unsigned>(std::min<long long>((per + 255) / 256, 64)), batch);
+  block_transpose_kernel<<<grid, 256, 0, s>>>(src, dst, rows, cols, ld, stride);
+  check_launch("block_transpose");
+}
+
 __global__ void set_identity_kernel(double* mats, int dim, long long total) {
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {

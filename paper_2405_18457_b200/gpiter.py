@@ -722,3 +722,18 @@ def write_trace_csv(path, trace: dict, input_dim: int):
     t[:rows, 2 * P + 6] = trace.get("step_seconds", np.zeros(rows))
     t[:rows, 2 * P + 7] = trace.get("solver_seconds", np.zeros(rows))
     check(_lib.load().gpk_write_trace_csv(str(path).encode(), _p(np.ascontiguousarray(t)), rows, input_dim))
+
+
+def spd_inverse(ctx: Context, mats, mode: int = 1):
+    """Batched SPD inverse of the AP diagonal-block solver (mats: batch x dim x dim).
+    mode 1: recursive Schur complement on strided-batched DGEMMs (default in the
+    solver); mode 0: cuSOLVER potrfBatched + batched triangular solves."""
+    mats = np.asarray(mats, dtype=np.float64)
+    if mats.ndim == 2:
+        mats = mats[None]
+    batch, dim, _ = mats.shape
+    src = np.ascontiguousarray(np.transpose(mats, (0, 2, 1)))  # column-major per matrix
+    out = np.empty_like(src)
+    check(ctx._lib.gpk_spd_inverse(ctx.handle, _p(src), dim, batch, int(mode), _p(out)))
+    return np.transpose(out, (0, 2, 1)).copy()
+

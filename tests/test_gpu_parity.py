@@ -317,3 +317,55 @@ def test_sharded_optimiser_world1_matches_plain(G, gpk_ctx, oracle, solver):
     sharded = G.optimise(ctx1, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
     for key in ("constrained", "gradient", "mean_residual_norm", "probe_residual_norm", "iterations"):
         assert np.array_equal(plain[key], sharded[key]), key
+
+
+@pytest.mark.parametrize("n,d,block", [(2048, 8, 512), (1000, 3, 200), (700, 5, 64), (1500, 20, 333)])
+def test_ap_block_inverse_paths_agree(G, oracle, n, d, block, monkeypatch):
+    """AP diagonal-block inverses: the recursive Schur-complement DGEMM path
+    (default) and the cuSOLVER potrf + triangular-solve path give the same
+    solve (same iteration count; solutions equal to FP64 rounding)."""
+    X, y = gp_problem(n, d, 9 * n)
+    raw = oracle.raw_from_constrained([1.0] * d + [1.0, 0.2])
+    T = _targets(oracle, n, 8, 9 * n + 1, y)
+    cfg = G.SolverConfig(kind=1, tolerance=0.01, max_epochs=50, block_size=block)
+    out = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("GPK_SPD_INVERSE", mode)
+        ctx = G.Context(0)
+        op = make_op(G, ctx, X, raw)
+        b = G.LinearSystemBatch(op, T)
+        rep = G.solve_ap(b, cfg)
+        out.append((rep.iterations, b.solutions.copy()))
+        ctx.close()
+    (i1, v1), (i0, v0) = out
+    # both inverses are exact to FP64 rounding (test_spd_inverse_both_paths);
+    # the solves may then differ by the rounding the AP iteration carries
+    assert abs(i1 - i0) <= 1
+    if i1 == i0:
+        assert np.max(np.abs(v1 - v0)) <= 1e-6 * np.max(np.abs(v0))
+
+
+@pytest.mark.parametrize("dim,batch", [(64, 3), (200, 4), (333, 2), (512, 5), (97, 1)])
+def test_spd_inverse_both_paths(G, gpk_ctx, oracle, dim, batch):
+    """Both AP block-inverse paths against numpy on kernel blocks H[blk, blk]."""
+    rng = np.random.default_rng(dim)
+    mats = []
+    for k in range(batch):
+        X = rng.standard_normal((dim, 4))
+        raw = oracle.raw_from_constrained([0.7, 1.0, 1.3, 0.9, 1.0, 0.1 + 0.1 * k])
+        mats.append(oracle.dense(X, raw))
+    mats = np.stack(mats)
+    for mode in (1, 0):
+        inv = G.gpiter.spd_inverse(gpk_ctx, mats, mode)
+        for k in range(batch):
+            ref = np.linalg.inv(mats[k])
+            assert np.max(np.abs(inv[k] - ref)) <= 1e-9 * np.max(np.abs(ref)), (mode, k)
+            assert np.max(np.abs(mats[k] @ inv[k] - np.eye(dim))) <= 1e-9
+
+
+def test_spd_inverse_rejects_indefinite(G, gpk_ctx):
+    A = np.eye(80)
+    A[40, 40] = -1.0
+    for mode in (1, 0):
+        with pytest.raises(ArithmeticError, match="not positive definite"):
+            G.gpiter.spd_inverse(gpk_ctx, A, mode)
