@@ -596,42 +596,81 @@ void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2
 
 // Leaf of the recursive SPD inversion: the nn x nn (nn <= 64) diagonal
 // sub-block at (off, off) of every matrix (column-major, leading dimension ld,
-// matrix stride `stride`) is inverted in shared memory by Gauss-Jordan
-// elimination without pivoting (stable for SPD) and written to the same
-// sub-block of `out`. One CTA per matrix.
-__global__ void spd_leaf_inverse_kernel(const double* a, double* out, int off, int nn, int ld, long long stride,
-                                        int* info) {
-  __shared__ double M[64][65];
+// matrix stride `stride`) is inverted by in-place Gauss-Jordan elimination
+// without pivoting (stable for SPD; the pivots are the Schur-complement
+// diagonal, a non-positive one flags the matrix) and written to the same
+// sub-block of `out`. One CTA per matrix; the 64 x 64 working matrix lives in
+// registers (thread (ty, tx) of 16 x 16 owns rows 4ty.., columns 4tx..; rows
+// and columns beyond nn are identity padding); pivot row and column are
+// exchanged through double-buffered shared memory, one barrier per step.
+__global__ void __launch_bounds__(256) spd_leaf_inverse_kernel(const double* a, double* out, int off, int nn, int ld,
+                                                               long long stride, int* info) {
+  __shared__ double colb[2][64], rowb[2][64];
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
   const double* A = a + blockIdx.x * stride + off + static_cast<size_t>(off) * ld;
   double* B = out + blockIdx.x * stride + off + static_cast<size_t>(off) * ld;
-  for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) {
-    const int i = e % nn, j = e / nn;
-    M[i][j] = A[i + static_cast<size_t>(j) * ld];
-  }
-  __syncthreads();
-  for (int k = 0; k < nn; ++k) {
-    // a non-positive pivot (Schur complement diagonal) means the block is not SPD
-    if (threadIdx.x == 0 && !(M[k][k] > 0.0)) info[blockIdx.x] = 1;
-    const double piv = 1.0 / M[k][k];
-    // rank-1 elimination of every entry outside row/column k
-    for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) {
-      const int i = e % nn, j = e / nn;
-      if (i != k && j != k) M[i][j] = fma(-M[i][k] * piv, M[k][j], M[i][j]);
+  double M[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * ty + p, j = 4 * tx + q;
+      M[p][q] = (i < nn && j < nn) ? A[i + static_cast<size_t>(j) * ld] : (i == j ? 1.0 : 0.0);
+    }
+  bool bad = false;
+  for (int k = 0; k < 64; ++k) {
+    const int buf = k & 1;
+    if (tx == (k >> 2)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q == (k & 3)) {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) colb[buf][4 * ty + p] = M[p][q];
+        }
+    }
+    if (ty == (k >> 2)) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        if (p == (k & 3)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rowb[buf][4 * tx + q] = M[p][q];
+        }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < nn; t += blockDim.x) {
-      if (t != k) {
-        M[t][k] = -M[t][k] * piv;  // column k
-        M[k][t] = M[k][t] * piv;   // row k
+    const double pk = rowb[buf][k];
+    bad |= !(pk > 0.0);
+    const double piv = 1.0 / pk;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int i = 4 * ty + p;
+      const double ci = colb[buf][i] * piv;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * tx + q;
+        const double m = M[p][q];
+        double v = fma(-ci, rowb[buf][j], m);
+        if (j == k) v = -m * piv;
+        if (i == k) v = (j == k) ? piv : m * piv;
+        M[p][q] = v;
       }
     }
-    if (threadIdx.x == 0) M[k][k] = piv;
-    __syncthreads();
   }
-  for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) {
-    const int i = e % nn, j = e / nn;
-    B[i + static_cast<size_t>(j) * ld] = 0.5 * (M[i][j] + M[j][i]);  // symmetrise the rounding
-  }
+  if (bad && threadIdx.x == 0) info[blockIdx.x] = 1;
+  // symmetrise the rounding: the recursion's Schur updates assume symmetric
+  // leaf inverses (the antisymmetric GJ rounding otherwise propagates)
+  __shared__ double S[64][65];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) S[4 * ty + p][4 * tx + q] = M[p][q];
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * ty + p, j = 4 * tx + q;
+      if (i < nn && j < nn) B[i + static_cast<size_t>(j) * ld] = 0.5 * (S[i][j] + S[j][i]);
+    }
 }
 void spd_leaf_inverse_launch(const double* a, double* out, int off, int nn, int ld, long long stride, int batch,
                              int* info, cudaStream_t s) {
