@@ -249,6 +249,8 @@ typedef struct {
   uint64_t probe_seed, feature_seed, solver_seed;
   double init_value;      /* constrained init of every parameter */
   int divergence_policy;  /* 0 skip-and-halve, 1 abort */
+  int prior_mode;         /* pathwise prior: 0 random features, 1 exact dense
+                             (jittered Cholesky draws, n <= 4096; outer_loop.cpp:140-153) */
 } gpk_outer_config;
 
 /* One row per outer step (TraceRecord, trace.hpp:10-27, plus the full

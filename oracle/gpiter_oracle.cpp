@@ -1071,6 +1071,49 @@ struct Adam {
 };
 }  // namespace
 
+PathwiseTargets pathwise_targets_from_prior(const Mat& prior_values, const Hyper& hp, uint64_t seed,
+                                            uint64_t substream) {  // rff.cpp:81-91
+  PathwiseTargets t;
+  t.prior_values = prior_values;
+  t.noise = Mat(prior_values.rows, prior_values.cols);
+  RandomStream ns(seed, streams::kNoiseDraws, substream);
+  ns.fill_gaussian(t.noise.a.data(), t.noise.size());
+  t.xi = Mat(prior_values.rows, prior_values.cols);
+  const double sigma = hp.noise_scale();
+  for (size_t e = 0; e < t.xi.a.size(); ++e) t.xi.a[e] = t.prior_values.a[e] + sigma * t.noise.a[e];
+  return t;
+}
+
+Mat jittered_kernel_cholesky(const Mat& kernel_matrix) {  // exact.cpp:52-61
+  const int n = kernel_matrix.rows;
+  double mean_diag = 0.0;
+  for (int i = 0; i < n; ++i) mean_diag += kernel_matrix(i, i);
+  mean_diag /= n;
+  for (double jitter = 1e-10; jitter <= 1.0000001e-6; jitter *= 10.0) {
+    Mat attempt = kernel_matrix;
+    for (int i = 0; i < n; ++i) attempt(i, i) += jitter * mean_diag;
+    LLT llt;
+    llt.compute(attempt);
+    if (llt.ok) return llt.L;
+  }
+  throw std::runtime_error("jittered_kernel_cholesky: factorisation failed beyond 1e-6 jitter");
+}
+
+Mat exact_dense_prior(const KernelOperator& op, const Hyper& hp, const Mat& weights) {
+  const int n = op.size(), s = weights.cols;
+  Mat kernel_matrix = op.dense_block(0, n, 0, n);
+  for (int i = 0; i < n; ++i) kernel_matrix(i, i) -= hp.noise_variance();
+  const Mat chol = jittered_kernel_cholesky(kernel_matrix);
+  Mat prior(n, s);  // chol * weights (lower triangular)
+  for (int j = 0; j < s; ++j)
+    for (int i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k <= i; ++k) acc += chol(i, k) * weights(k, j);
+      prior(i, j) = acc;
+    }
+  return prior;
+}
+
 OuterResult optimise(const Dataset& train, const OuterConfig& config, int threads, int block_rows) {
   const int n = train.n(), d = train.dim(), s = config.probe_count;
   config.solver.validate();
@@ -1086,6 +1129,7 @@ OuterResult optimise(const Dataset& train, const OuterConfig& config, int thread
   bool have_basis = false;
   RffBasis basis;
   Mat probes;
+  Mat exact_prior_weights;  // n x s, fixed draws for the ExactDense prior
   Mat previous;
   bool have_previous = false;
   for (int t = 0; t < config.steps; ++t) {
@@ -1098,7 +1142,18 @@ OuterResult optimise(const Dataset& train, const OuterConfig& config, int thread
         basis = build_rff_basis(d, config.rff_pairs, s, config.feature_seed, substream);
         have_basis = true;
       }
-      probe_targets = pathwise_targets(basis, hp, train, s, config.feature_seed, substream).xi;
+      if (config.prior_mode == 0) {
+        probe_targets = pathwise_targets(basis, hp, train, s, config.feature_seed, substream).xi;
+      } else {  // ExactDense (outer_loop.cpp:140-153)
+        if (n > kDefaultDenseCap) throw std::invalid_argument("optimise: exact prior draws need n within the dense cap");
+        if (exact_prior_weights.size() == 0 || !config.warm_start) {
+          RandomStream stream(config.feature_seed, streams::kPriorSample, substream);
+          exact_prior_weights = Mat(n, s);
+          stream.fill_gaussian(exact_prior_weights.a.data(), exact_prior_weights.size());
+        }
+        probe_targets = pathwise_targets_from_prior(exact_dense_prior(op, hp, exact_prior_weights), hp,
+                                                    config.feature_seed, substream).xi;
+      }
     } else {
       if (probes.size() == 0 || !config.warm_start)
         probes = gen_standard_probes(n, s, config.probe_seed, config.probe_distribution, substream);

@@ -226,6 +226,17 @@ struct RffBasis {
 RffBasis build_rff_basis(int d, int m_pairs, int sample_count, uint64_t seed, uint64_t substream);
 Mat rff_features(const RffBasis& basis, const Hyper& hp, const Mat& points);
 struct PathwiseTargets { Mat prior_values, noise, xi; };
+// rff.cpp:81-91: xi = prior + sigma * eps, eps from (seed, kNoiseDraws, substream)
+PathwiseTargets pathwise_targets_from_prior(const Mat& prior_values, const Hyper& hp, uint64_t seed,
+                                            uint64_t substream);
+// exact.cpp:52-61: lower Cholesky factor of K + jitter * mean(diag K) I, jitter
+// 1e-10, 1e-9, ..., 1e-6 (first success); throws beyond 1e-6
+Mat jittered_kernel_cholesky(const Mat& kernel_matrix);
+constexpr int kDefaultDenseCap = 4096;  // exact.hpp:24
+class KernelOperator;
+// ExactDense prior values (outer_loop.cpp:149-152): L W with L the jittered
+// Cholesky factor of dense(H) - sigma^2 I and W the n x s weights.
+Mat exact_dense_prior(const KernelOperator& op, const Hyper& hp, const Mat& weights);
 PathwiseTargets pathwise_targets(const RffBasis& basis, const Hyper& hp, const Dataset& data,
                                  int s, uint64_t seed, uint64_t substream);
 
@@ -256,6 +267,7 @@ struct OuterConfig {
   Vec init_constrained;  // empty: all init_value
   double init_value = 1.0;
   int divergence_policy = 0;  // 0 skip-and-halve, 1 abort
+  int prior_mode = 0;         // 0 random features, 1 exact dense (outer_loop.cpp:134-154)
 };
 
 struct TraceRow {

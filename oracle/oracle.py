@@ -45,7 +45,7 @@ class OuterConfigC(C.Structure):
                 ("rff_pairs", C.c_int), ("probe_distribution", C.c_int),
                 ("probe_seed", C.c_ulonglong), ("feature_seed", C.c_ulonglong),
                 ("solver_seed", C.c_ulonglong), ("init_value", C.c_double),
-                ("divergence_policy", C.c_int)]
+                ("divergence_policy", C.c_int), ("prior_mode", C.c_int)]
 
 
 def build():
@@ -335,10 +335,10 @@ def optimise(X, y, config: OuterConfigC, init_constrained=None, threads=1):
 
 def outer_config(estimator=1, solver=None, warm_start=False, steps=100, learning_rate=0.1,
                  probe_count=64, rff_pairs=1000, probe_distribution=0, probe_seed=0, feature_seed=0,
-                 solver_seed=0, init_value=1.0, divergence_policy=0):
+                 solver_seed=0, init_value=1.0, divergence_policy=0, prior_mode=0):
     return OuterConfigC(estimator, solver if solver is not None else solver_config(), int(warm_start),
                         steps, learning_rate, probe_count, rff_pairs, probe_distribution, probe_seed,
-                        feature_seed, solver_seed, init_value, divergence_policy)
+                        feature_seed, solver_seed, init_value, divergence_policy, prior_mode)
 
 
 def exact(X, y, raw):
@@ -367,6 +367,15 @@ def cross_apply(points, X, raw, V, threads=1):
     out = np.empty((P.shape[0], V.shape[1]), order="F")
     _check(lib().oracle_cross_apply(_p(P), P.shape[0], _p(X), X.shape[0], X.shape[1], _p(raw), _p(V), V.shape[1],
                                     _p(out), threads))
+    return out
+
+
+def exact_prior(X, raw, s, seed, substream=0):
+    """ExactDense prior values L W (outer_loop.cpp:140-153), W from (seed, 8, substream)."""
+    X, raw = _f(X), _f(raw)
+    n, d = X.shape
+    out = np.empty((n, s), order="F")
+    _check(lib().oracle_exact_prior(_p(X), n, d, _p(raw), s, C.c_ulonglong(seed), C.c_ulonglong(substream), _p(out)))
     return out
 
 

@@ -340,6 +340,7 @@ struct OuterConfigC {
   unsigned long long probe_seed, feature_seed, solver_seed;
   double init_value;
   int divergence_policy;
+  int prior_mode;
 };
 
 // Per step row of `trace` (stride 2*(d+2)+8): constrained[d+2], gradient[d+2],
@@ -363,6 +364,7 @@ int oracle_optimise(const double* x, const double* y, int n, int d, const OuterC
     oc.solver_seed = cfg->solver_seed;
     oc.init_value = cfg->init_value;
     oc.divergence_policy = cfg->divergence_policy;
+    oc.prior_mode = cfg->prior_mode;
     if (init_constrained) oc.init_constrained.assign(init_constrained, init_constrained + d + 2);
     const OuterResult r = optimise(ds, oc, threads);
     const int P = d + 2, stride = 2 * P + 8;
@@ -403,6 +405,20 @@ int oracle_cross_apply(const double* points, int p, const double* x, int n, int 
   return guarded([&] {
     put(cross_kernel_apply(make_mat(points, p, d), make_mat(x, n, d), make_hp(raw, d), make_mat(v, n, m), 1024, threads),
         out);
+  });
+}
+
+// ExactDense prior values (n x s): weights from (seed, kPriorSample, substream).
+int oracle_exact_prior(const double* x, int n, int d, const double* raw, int s, unsigned long long seed,
+                       unsigned long long substream, double* out) {
+  return guarded([&] {
+    const Dataset ds = make_data(x, nullptr, n, d);
+    const Hyper hp = make_hp(raw, d);
+    KernelOperator op(&ds, hp);
+    Mat w(n, s);
+    RandomStream st(seed, streams::kPriorSample, substream);
+    st.fill_gaussian(w.a.data(), w.size());
+    put(exact_dense_prior(op, hp, w), out);
   });
 }
 

@@ -38,7 +38,7 @@ class OuterConfigC(C.Structure):
                 ("steps", C.c_int), ("learning_rate", C.c_double), ("probe_count", C.c_int),
                 ("rff_pairs", C.c_int), ("probe_distribution", C.c_int), ("probe_seed", C.c_uint64),
                 ("feature_seed", C.c_uint64), ("solver_seed", C.c_uint64), ("init_value", C.c_double),
-                ("divergence_policy", C.c_int)]
+                ("divergence_policy", C.c_int), ("prior_mode", C.c_int)]
 
 
 _lib = None

@@ -2313,6 +2313,9 @@ struct gpk_optimiser {
   std::unique_ptr<gpk_batch> batch;
   std::unique_ptr<gpk_rff_basis> basis;
   DBuf<double> prev, prior, noise, probes, ycol;
+  // ExactDense prior: fixed weights W [n][s], dense kernel matrix and its factor
+  DBuf<double> exact_w, dense, chol, work;
+  bool have_exact_w = false;
 };
 
 namespace {
@@ -2331,6 +2334,8 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
   if (o->s < 1) throw InvalidArgument("optimise: probe_count >= 1");
   if (cfg->estimator != 1 && (cfg->probe_distribution < 0 || cfg->probe_distribution > 1))
     throw InvalidArgument("gpk_optimise: probe_distribution 0 (Gaussian) or 1 (Rademacher)");
+  if (cfg->prior_mode < 0 || cfg->prior_mode > 1)
+    throw InvalidArgument("gpk_optimise: prior_mode 0 (random features) or 1 (exact dense)");
   o->raw.resize(o->P);
   for (int k = 0; k < o->P; ++k) o->raw[k] = softplus_inverse(init_constrained ? init_constrained[k] : cfg->init_value);
   o->am.assign(o->P, 0.0);
@@ -2377,6 +2382,67 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
 }
 
 // One outer step (outer_loop.cpp:125-238). Returns false once the run aborted.
+__global__ void add_diag_kernel(double* a, int n, double v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    a[static_cast<size_t>(i) * n + i] += v;
+}
+
+// ExactDense prior (outer_loop.cpp:140-153, exact.cpp:52-61): K = dense(H) -
+// sigma^2 I in FP64, L = chol(K + jitter mean(diag K) I) for the first jitter
+// in 1e-10 .. 1e-6 that factors (cuSOLVER potrf), prior = L W with fixed
+// Gaussian weights W from (feature_seed, kPriorSample = 8, substream).
+void exact_prior_dev(gpk_optimiser* o, uint64_t substream, double* prior) {
+  gpk_ctx* ctx = o->ctx;
+  gpk_operator* op = o->op.get();
+  cudaStream_t st = ctx->stream;
+  const int n = o->n, s = o->s;
+  if (op->sharded) throw InvalidArgument("gpk_optimise: the exact dense prior runs on one GPU");
+  if (n > 4096) throw InvalidArgument("optimise: exact prior draws need n within the dense cap");
+  if (!o->have_exact_w || !o->cfg.warm_start) {
+    gaussian_fill_rows_launch(o->cfg.feature_seed, 8, substream, n, s, 0, n, o->exact_w.ensure(static_cast<size_t>(n) * s),
+                              st);
+    o->have_exact_w = true;
+  }
+  const size_t nn = static_cast<size_t>(n) * n;
+  double* K = o->dense.ensure(nn);
+  dense_block64_launch(op->xs64.p, n, op->d, op->s2, op->sigma2, 0, n, 0, n, K, n, 1, st);  // symmetric
+  add_diag_kernel<<<(n + 255) / 256, 256, 0, st>>>(K, n, -op->sigma2);
+  check_launch("add_diag");
+  // every diagonal entry is (s2 + sigma2) - sigma2 (r = 0): their mean is that value
+  const double mean_diag = (op->s2 + op->sigma2) - op->sigma2;
+  if (cusolverDnSetStream(ctx->solver, st) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnSetStream");
+  int lwork = 0;
+  double* L = o->chol.ensure(nn);
+  if (cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, L, n, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    throw CudaError("cusolverDnDpotrf_bufferSize");
+  double* work = o->work.ensure(static_cast<size_t>(std::max(lwork, 1)));
+  int* info = ctx->info.ensure(1);
+  bool ok = false;
+  for (double jitter = 1e-10; jitter <= 1.0000001e-6; jitter *= 10.0) {
+    GPK_CUDA(cudaMemcpyAsync(L, K, sizeof(double) * nn, cudaMemcpyDeviceToDevice, st));
+    add_diag_kernel<<<(n + 255) / 256, 256, 0, st>>>(L, n, jitter * mean_diag);
+    check_launch("add_diag");
+    if (cusolverDnDpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, L, n, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+      throw CudaError("cusolverDnDpotrf");
+    count_launch(2);
+    int h = 0;
+    GPK_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GPK_CUDA(cudaStreamSynchronize(st));
+    if (h == 0) {
+      ok = true;
+      break;
+    }
+  }
+  if (!ok) throw NumericError("jittered_kernel_cholesky: factorisation failed beyond 1e-6 jitter");
+  // prior (row-major [n][s] = column-major s x n) = (L W)^T^T: prior^T = W^T L^T
+  if (cublasSetStream(ctx->blas, st) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+  const double one = 1.0;
+  if (cublasDtrmm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, s, n, &one, L,
+                  n, o->exact_w.p, s, prior, s) != CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDtrmm (exact prior)");
+  count_launch();
+}
+
 bool optimiser_one_step(gpk_optimiser* o, double* row) {
   const auto t0 = Clock::now();
   gpk_ctx* ctx = o->ctx;
@@ -2396,13 +2462,17 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
   g_phase.mark("set_hyper");
   const uint64_t substream = cfg.warm_start ? 0 : static_cast<uint64_t>(t);
   if (pathwise) {
-    if (!o->basis || !cfg.warm_start) {
-      gpk_rff_basis* bp = nullptr;
-      if (gpk_rff_basis_build(ctx, o->d, cfg.rff_pairs, s, cfg.feature_seed, substream, &bp) != GPK_OK)
-        throw InvalidArgument(g_err);
-      o->basis.reset(bp);
+    if (cfg.prior_mode == 1) {  // outer_loop.cpp:140-153 (no RFF basis in this mode)
+      exact_prior_dev(o, substream, o->prior.p);
+    } else {  // outer_loop.cpp:134-139
+      if (!o->basis || !cfg.warm_start) {
+        gpk_rff_basis* bp = nullptr;
+        if (gpk_rff_basis_build(ctx, o->d, cfg.rff_pairs, s, cfg.feature_seed, substream, &bp) != GPK_OK)
+          throw InvalidArgument(g_err);
+        o->basis.reset(bp);
+      }
+      rff_prior_dev(op, o->basis.get(), s, o->prior.p);
     }
-    rff_prior_dev(op, o->basis.get(), s, o->prior.p);
     if (!o->have_noise || o->noise_sub != substream) {  // rows of this rank of the n x s draw
       gaussian_fill_rows_launch(cfg.feature_seed, 5, substream, n, s, op->row0, nloc, o->noise.p, stream);
       o->have_noise = true;

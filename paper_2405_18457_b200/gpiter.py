@@ -580,11 +580,13 @@ class OuterConfig:
     solver_seed: int = 0
     init_value: float = 1.0
     divergence_policy: int = 0
+    prior_mode: int = 0  # pathwise prior: 0 random features, 1 exact dense (n <= 4096)
 
     def c(self):
         return OuterConfigC(self.estimator, self.solver.c(), int(self.warm_start), self.steps, self.learning_rate,
                             self.probe_count, self.rff_pairs, self.probe_distribution, self.probe_seed,
-                            self.feature_seed, self.solver_seed, self.init_value, self.divergence_policy)
+                            self.feature_seed, self.solver_seed, self.init_value, self.divergence_policy,
+                            self.prior_mode)
 
 
 def optimise(ctx: Context, inputs, targets, config: OuterConfig, init_constrained=None):

@@ -369,3 +369,21 @@ def test_spd_inverse_rejects_indefinite(G, gpk_ctx):
     for mode in (1, 0):
         with pytest.raises(ArithmeticError, match="not positive definite"):
             G.gpiter.spd_inverse(gpk_ctx, A, mode)
+
+
+def test_optimise_exact_dense_prior_matches_oracle(G, gpk_ctx, oracle):
+    """ExactDense pathwise prior (outer_loop.cpp:140-153): device jittered
+    cuSOLVER Cholesky + TRMM of the stream-8 weights against the oracle."""
+    n, d = 600, 3
+    X, y = gp_problem(n, d, 611)
+    scfg = dict(kind=0, tolerance=0.01, max_epochs=100, preconditioner_rank=50)
+    ocfg = dict(estimator=1, warm_start=True, steps=3, learning_rate=0.1, probe_count=8, rff_pairs=32,
+                probe_seed=2, feature_seed=3, solver_seed=4, prior_mode=1)
+    r = G.optimise(gpk_ctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
+    ref = oracle.optimise(X, y, oracle.outer_config(solver=oracle.solver_config(**scfg), **ocfg), threads=8)
+    assert np.max(np.abs(r["constrained"] - ref["constrained"]) / ref["constrained"]) <= 1e-3
+    assert np.all(np.abs(r["iterations"] - ref["iterations"]) <= 1)
+    # the prior differs from the random-feature one
+    ocfg["prior_mode"] = 0
+    r0 = G.optimise(gpk_ctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
+    assert not np.array_equal(r0["gradient"][0], r["gradient"][0])

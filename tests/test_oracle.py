@@ -450,3 +450,41 @@ def test_sinsum_generator_standardised(oracle):
     assert np.allclose(X.astype(np.float64).mean(0), 0, atol=1e-6)
     X2, _ = oracle.sinsum_dataset(4096, 8, seed=0)
     assert np.array_equal(X, X2)
+
+
+def test_exact_dense_prior_restates_jittered_cholesky(oracle):  # outer_loop.cpp:140-153, exact.cpp:52-61
+    """ExactDense prior = L W, L the first successful Cholesky of
+    dense(H) - s2 I + jitter mean(diag) I (jitter 1e-10 ...), W from stream 8."""
+    rng = np.random.default_rng(21)
+    n, d, s = 150, 3, 5
+    X = rng.standard_normal((n, d))
+    raw = oracle.raw_from_constrained([0.8, 1.2, 1.0, 1.3, 0.2])
+    got = oracle.exact_prior(X, raw, s, seed=3, substream=0)
+    K = oracle.dense(X, raw)
+    sig2 = oracle.softplus(raw[-1]) ** 2
+    K[np.diag_indices(n)] -= sig2
+    md = np.mean(np.diag(K))
+    L = None
+    for jit in (1e-10, 1e-9, 1e-8, 1e-7, 1e-6):
+        try:
+            L = np.linalg.cholesky(K + jit * md * np.eye(n))
+            break
+        except np.linalg.LinAlgError:
+            continue
+    W = oracle.stream_draw(3, 8, 0, "gaussian", n * s).reshape((n, s), order="F")
+    ref = L @ W
+    assert np.max(np.abs(got - ref)) <= 1e-9 * np.max(np.abs(ref))
+
+
+def test_optimise_exact_dense_prior_mode(oracle):
+    X, y = gp_problem(120, 2, 433)
+    cfg = oracle.outer_config(estimator=1, warm_start=True, steps=3, probe_count=4, rff_pairs=16,
+                              solver=oracle.solver_config(kind=0, tolerance=1e-3, max_epochs=100), prior_mode=1,
+                              feature_seed=5)
+    r = oracle.optimise(X, y, cfg)
+    assert len(r["constrained"]) == 3 and np.all(np.isfinite(r["constrained"]))
+    r2 = oracle.optimise(X, y, cfg)
+    assert np.array_equal(r["constrained"], r2["constrained"])  # deterministic
+    cfg.prior_mode = 0
+    r3 = oracle.optimise(X, y, cfg)
+    assert not np.array_equal(r["gradient"][0], r3["gradient"][0])  # a different prior
