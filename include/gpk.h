@@ -287,6 +287,20 @@ gpk_status gpk_sinsum_dataset(int n, int d, int uniform, double noise, uint64_t 
  * header, columns and shortest round-trip doubles (test columns empty). */
 gpk_status gpk_write_trace_csv(const char* path, const double* trace, int rows, int d);
 
+/* ---- exact marginal likelihood (row f4; exact.cpp, outer_loop.cpp:248-296)
+ * optimise_exact: Adam on the exact MLL gradient (dense FP64 H, cuSOLVER
+ * Cholesky + inverse, one fused pass sum_ij W_ij dH_ij/dtheta with
+ * W = (alpha alpha^T - H^-1)/2). inputs column-major n x d; init_constrained
+ * null = all 1.0; trajectory (nullable) steps x (d+2) constrained, row-major;
+ * final_raw d+2. init_heuristic: the mean of optimise_exact fits on the
+ * `subset` nearest rows (stable sort of squared distances) of n_centroids
+ * centroids drawn from (seed, kCentroids = 9); subset >= n fits all rows. */
+gpk_status gpk_optimise_exact(gpk_ctx* ctx, const double* inputs, const double* targets, int n, int d,
+                              const double* init_constrained, int steps, double learning_rate, double* trajectory,
+                              double* final_raw);
+gpk_status gpk_init_heuristic(gpk_ctx* ctx, const double* inputs, const double* targets, int n, int d, int n_centroids,
+                              int subset, uint64_t seed, int adam_steps, double learning_rate, double* constrained);
+
 /* Batched SPD inverse used for the AP diagonal blocks (host buffers, batch
  * column-major dim x dim matrices). mode 1: recursive Schur complement with
  * strided-batched DGEMMs (the solver's default); mode 0: cuSOLVER

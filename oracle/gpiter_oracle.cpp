@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <numeric>
 #include <limits>
 #include <stdexcept>
 
@@ -1316,6 +1317,60 @@ void make_sinsum_dataset(int n, int d, bool uniform, double noise, uint64_t seed
   const double scale = var > 0.0 ? std::sqrt(var) : 1.0;
   y.resize(n);
   for (int i = 0; i < n; ++i) y[i] = static_cast<float>((yy[i] - mean) / scale);
+}
+
+ExactTrajectory optimise_exact(const Dataset& data, const Hyper& init, int steps, double learning_rate) {
+  ExactTrajectory tr;  // outer_loop.cpp:248-262
+  Vec raw = init.raw;
+  Adam adam(static_cast<int>(raw.size()), learning_rate);
+  for (int t = 0; t < steps; ++t) {
+    const Hyper hp = Hyper::from_raw(raw);
+    tr.constrained_per_step.push_back(hp.constrained());
+    const DenseProblem dense = build_dense_problem(data, hp);
+    const Vec grad = exact_gradient(dense, data.targets);
+    Vec neg(raw.size());
+    for (size_t k = 0; k < raw.size(); ++k) neg[k] = -(grad[k] * sigmoid(raw[k]));
+    const Vec upd = adam.update(neg);
+    for (size_t k = 0; k < raw.size(); ++k) raw[k] += upd[k];
+  }
+  tr.hp = Hyper::from_raw(raw);
+  return tr;
+}
+
+Hyper init_heuristic(const Dataset& data, int n_centroids, int subset, uint64_t seed, int adam_steps,
+                     double learning_rate) {  // outer_loop.cpp:264-296
+  const int n = data.n(), d = data.dim();
+  const Hyper init = Hyper::constant(d, 1.0);
+  if (subset >= n) return optimise_exact(data, init, adam_steps, learning_rate).hp;
+  RandomStream stream(seed, streams::kCentroids, 0);
+  Vec acc(d + 2, 0.0);
+  for (int c = 0; c < n_centroids; ++c) {
+    const int centroid = static_cast<int>(stream.next_below(static_cast<uint64_t>(n)));
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::vector<double> dist2(n);
+    for (int i = 0; i < n; ++i) {
+      double s2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double t = data.inputs(i, k) - data.inputs(centroid, k);
+        s2 += t * t;
+      }
+      dist2[i] = s2;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return dist2[a] < dist2[b]; });
+    Dataset local;
+    local.inputs = Mat(subset, d);
+    local.targets.assign(subset, 0.0);
+    for (int i = 0; i < subset; ++i) {
+      for (int k = 0; k < d; ++k) local.inputs(i, k) = data.inputs(order[i], k);
+      local.targets[i] = data.targets[order[i]];
+    }
+    const Vec fitted = optimise_exact(local, init, adam_steps, learning_rate).hp.constrained();
+    for (int k = 0; k < d + 2; ++k) acc[k] += fitted[k];
+  }
+  Vec mean(d + 2);
+  for (int k = 0; k < d + 2; ++k) mean[k] = acc[k] / n_centroids;
+  return Hyper::from_constrained(mean);
 }
 
 }  // namespace oracle

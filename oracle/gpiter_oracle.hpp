@@ -295,6 +295,15 @@ DenseProblem build_dense_problem(const Dataset& data, const Hyper& hp);
 double exact_mll(const DenseProblem& dense, const Vec& y);
 Vec exact_gradient(const DenseProblem& dense, const Vec& y);
 
+// outer_loop.cpp:248-262: Adam on the exact marginal likelihood
+struct ExactTrajectory { Hyper hp; std::vector<Vec> constrained_per_step; };
+ExactTrajectory optimise_exact(const Dataset& data, const Hyper& init, int steps, double learning_rate);
+// outer_loop.cpp:264-296: average of optimise_exact fits on the `subset`
+// nearest rows (stable sort by squared distance) of n_centroids centroids
+// drawn from (seed, kCentroids = 9, 0); subset >= n fits the whole set.
+Hyper init_heuristic(const Dataset& data, int n_centroids, int subset, uint64_t seed, int adam_steps,
+                     double learning_rate);
+
 // ---- BASELINE.json synthetic sin-sum generator (not in the reference) -----
 // X ~ N(0,I) (uniform=false) or U[-1,1]^d; y = sum_{k<4} sin(x.w_k), w_k ~ N(0, I/d),
 // + N(0, noise^2); y standardised with the reference formula

@@ -370,6 +370,28 @@ def cross_apply(points, X, raw, V, threads=1):
     return out
 
 
+def optimise_exact(X, y, steps, learning_rate=0.1, init_constrained=None):
+    """outer_loop.cpp:248-262: returns (trajectory steps x (d+2) constrained, final raw)."""
+    X, y = _f(X), _f(y)
+    n, d = X.shape
+    traj = np.empty((steps, d + 2))
+    raw = np.empty(d + 2)
+    init = _f(init_constrained) if init_constrained is not None else None
+    _check(lib().oracle_optimise_exact(_p(X), _p(y), n, d, _p(init), steps, C.c_double(learning_rate), _p(traj),
+                                       _p(raw)))
+    return traj, raw
+
+
+def init_heuristic(X, y, n_centroids, subset, seed, adam_steps, learning_rate=0.1):
+    """outer_loop.cpp:264-296: constrained hyperparameters (d+2)."""
+    X, y = _f(X), _f(y)
+    n, d = X.shape
+    out = np.empty(d + 2)
+    _check(lib().oracle_init_heuristic(_p(X), _p(y), n, d, n_centroids, subset, C.c_ulonglong(seed), adam_steps,
+                                       C.c_double(learning_rate), _p(out)))
+    return out
+
+
 def exact_prior(X, raw, s, seed, substream=0):
     """ExactDense prior values L W (outer_loop.cpp:140-153), W from (seed, 8, substream)."""
     X, raw = _f(X), _f(raw)

@@ -399,6 +399,31 @@ int oracle_exact(const double* x, const double* y, int n, int d, const double* r
   });
 }
 
+// optimise_exact: trajectory (steps x (d+2) constrained, row-major), final raw (d+2).
+int oracle_optimise_exact(const double* x, const double* y, int n, int d, const double* init_constrained, int steps,
+                          double learning_rate, double* trajectory, double* final_raw) {
+  return guarded([&] {
+    const Dataset ds = make_data(x, y, n, d);
+    const Hyper init = init_constrained ? Hyper::from_constrained(Vec(init_constrained, init_constrained + d + 2))
+                                        : Hyper::constant(d, 1.0);
+    const ExactTrajectory tr = optimise_exact(ds, init, steps, learning_rate);
+    for (int t = 0; t < steps; ++t)
+      std::memcpy(trajectory + static_cast<size_t>(t) * (d + 2), tr.constrained_per_step[t].data(),
+                  sizeof(double) * (d + 2));
+    std::memcpy(final_raw, tr.hp.raw.data(), sizeof(double) * (d + 2));
+  });
+}
+
+// init_heuristic: constrained (d+2) of the averaged fit.
+int oracle_init_heuristic(const double* x, const double* y, int n, int d, int n_centroids, int subset,
+                          unsigned long long seed, int adam_steps, double learning_rate, double* constrained) {
+  return guarded([&] {
+    const Dataset ds = make_data(x, y, n, d);
+    const Vec c = init_heuristic(ds, n_centroids, subset, seed, adam_steps, learning_rate).constrained();
+    std::memcpy(constrained, c.data(), sizeof(double) * (d + 2));
+  });
+}
+
 // k(P, X) V (p x m), P p x d, X n x d, V n x m.
 int oracle_cross_apply(const double* points, int p, const double* x, int n, int d, const double* raw, const double* v,
                        int m, double* out, int threads) {

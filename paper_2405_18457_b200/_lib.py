@@ -114,6 +114,9 @@ def _sig(lib):
         "gpk_test_metrics": (C.c_int, [H, H, dp, C.c_int, dp, dp, dp, C.c_int, C.c_double, dp]),
         "gpk_write_trace_csv": (C.c_int, [C.c_char_p, dp, C.c_int, C.c_int]),
         "gpk_spd_inverse": (C.c_int, [vp, dp, C.c_int, C.c_int, C.c_int, dp]),
+        "gpk_optimise_exact": (C.c_int, [vp, dp, dp, C.c_int, C.c_int, dp, C.c_int, C.c_double, dp, dp]),
+        "gpk_init_heuristic": (C.c_int, [vp, dp, dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int,
+                                         C.c_double, dp]),
         "gpk_sinsum_dataset": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                          C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     }

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <memory>
 #include <string>
 #include <vector>
@@ -2707,6 +2708,151 @@ gpk_status gpk_test_metrics(gpk_operator* op, gpk_rff_basis* basis, const double
       }
       out4[1] = llh / p;
       out4[3] = out4[1] - std::log(target_scale);
+    }
+  });
+}
+
+// ---------------------------------------------- exact MLL (row f4, exact.cpp)
+namespace {
+
+struct ExactWork {
+  DBuf<double> H, alpha, y, work, part;
+  DBuf<int> info;
+};
+
+// exact_gradient (exact.cpp:33-50) for the operator's current hyperparameters:
+// H = dense (FP64), Cholesky, alpha = H^-1 y, H^-1 (potri), then one fused
+// pass sum_ij W_ij dH_ij/dtheta with W = (alpha alpha^T - H^-1) / 2.
+std::vector<double> exact_gradient_dev(gpk_operator* op, ExactWork& w) {
+  gpk_ctx* ctx = op->ctx;
+  cudaStream_t st = ctx->stream;
+  const int n = op->n, d = op->d;
+  const size_t nn = static_cast<size_t>(n) * n;
+  double* H = w.H.ensure(nn);
+  dense_block64_launch(op->xs64.p, n, d, op->s2, op->sigma2, 0, n, 0, n, H, n, 1, st);  // symmetric
+  if (cusolverDnSetStream(ctx->solver, st) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnSetStream");
+  int lw1 = 0, lw2 = 0;
+  if (cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, H, n, &lw1) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDpotri_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, H, n, &lw2) != CUSOLVER_STATUS_SUCCESS)
+    throw CudaError("cusolverDn buffer size");
+  const int lwork = std::max(1, std::max(lw1, lw2));
+  double* work = w.work.ensure(static_cast<size_t>(lwork));
+  int* info = w.info.ensure(1);
+  if (cusolverDnDpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, H, n, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+    throw CudaError("cusolverDnDpotrf");
+  int h = 0;
+  GPK_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GPK_CUDA(cudaStreamSynchronize(st));
+  if (h != 0) throw NumericError("build_dense_problem: H is not positive definite");
+  double* alpha = w.alpha.ensure(n);
+  GPK_CUDA(cudaMemcpyAsync(alpha, w.y.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if (cusolverDnDpotrs(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, 1, H, n, alpha, n, info) != CUSOLVER_STATUS_SUCCESS)
+    throw CudaError("cusolverDnDpotrs");
+  if (cusolverDnDpotri(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, H, n, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+    throw CudaError("cusolverDnDpotri");
+  count_launch(3);
+  const long long blocks = exact_forms_blocks(n);
+  double* part = w.part.ensure(static_cast<size_t>(blocks) * (d + 2));
+  exact_forms_launch(op->xs64.p, n, d, H, alpha, part, st);
+  std::vector<double> hp(static_cast<size_t>(blocks) * (d + 2));
+  GPK_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, st));
+  GPK_CUDA(cudaStreamSynchronize(st));
+  std::vector<double> sum(d + 2, 0.0);
+  for (long long b = 0; b < blocks; ++b)  // fixed block order
+    for (int k = 0; k < d + 2; ++k) sum[k] += hp[static_cast<size_t>(b) * (d + 2) + k];
+  std::vector<double> g(d + 2);
+  for (int k = 0; k < d; ++k) g[k] = 3.0 * op->s2 * op->inv_ls[k] * sum[k];  // kernel.cpp:222-228
+  g[d] = (2.0 / op->s) * op->s2 * sum[d];                                     // kernel.cpp:215-217
+  g[d + 1] = 2.0 * op->sigma * sum[d + 1];                                    // kernel.cpp:207-209
+  return g;
+}
+
+// optimise_exact (outer_loop.cpp:248-262) on a device-resident dataset.
+std::vector<double> optimise_exact_dev(gpk_ctx* ctx, const double* inputs_colmajor, const double* targets, int n, int d,
+                                       std::vector<double> raw, int steps, double lr, double* trajectory) {
+  gpk_operator* opp = nullptr;
+  if (gpk_operator_create(ctx, inputs_colmajor, n, d, raw.data(), &opp) != GPK_OK) throw InvalidArgument(g_err);
+  std::unique_ptr<gpk_operator> op(opp);
+  ExactWork w;
+  w.y.ensure(n);
+  GPK_CUDA(cudaMemcpyAsync(w.y.p, targets, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  const int P = d + 2;
+  std::vector<double> m(P, 0.0), v(P, 0.0);
+  const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  for (int t = 0; t < steps; ++t) {
+    set_hyper(op.get(), raw.data());
+    if (trajectory)
+      for (int k = 0; k < P; ++k) trajectory[static_cast<size_t>(t) * P + k] = softplus(raw[k]);
+    const std::vector<double> g = exact_gradient_dev(op.get(), w);
+    const double ms = 1.0 / (1.0 - std::pow(b1, t + 1)), vs = 1.0 / (1.0 - std::pow(b2, t + 1));
+    std::vector<double> upd(P);
+    for (int k = 0; k < P; ++k) {  // outer_loop.cpp:42-55 on -raw_gradient
+      const double gr = -(g[k] * sigmoid(raw[k]));
+      m[k] = b1 * m[k] + (1.0 - b1) * gr;
+      v[k] = b2 * v[k] + (1.0 - b2) * (gr * gr);
+      upd[k] = (-lr) * (ms * m[k] / (std::sqrt(vs * v[k]) + eps));
+    }
+    for (int k = 0; k < P; ++k) raw[k] += upd[k];
+  }
+  return raw;
+}
+
+}  // namespace
+
+gpk_status gpk_optimise_exact(gpk_ctx* ctx, const double* inputs, const double* targets, int n, int d,
+                              const double* init_constrained, int steps, double learning_rate, double* trajectory,
+                              double* final_raw) {
+  return guarded([&] {
+    LaunchScope ls(ctx);
+    require(ctx && inputs && targets && final_raw && n >= 1 && d >= 1 && steps >= 0, "optimise_exact: arguments");
+    std::vector<double> raw(d + 2);
+    for (int k = 0; k < d + 2; ++k) raw[k] = softplus_inverse(init_constrained ? init_constrained[k] : 1.0);
+    raw = optimise_exact_dev(ctx, inputs, targets, n, d, raw, steps, learning_rate, trajectory);
+    std::memcpy(final_raw, raw.data(), sizeof(double) * (d + 2));
+  });
+}
+
+gpk_status gpk_init_heuristic(gpk_ctx* ctx, const double* inputs, const double* targets, int n, int d, int n_centroids,
+                              int subset, uint64_t seed, int adam_steps, double learning_rate, double* constrained) {
+  return guarded([&] {
+    LaunchScope ls(ctx);
+    require(ctx && inputs && targets && constrained && n >= 1 && d >= 1 && n_centroids >= 1 && subset >= 1,
+            "init_heuristic: arguments");
+    const int P = d + 2;
+    const std::vector<double> init(P, softplus_inverse(1.0));
+    if (subset >= n) {  // outer_loop.cpp:268-270
+      const std::vector<double> raw = optimise_exact_dev(ctx, inputs, targets, n, d, init, adam_steps, learning_rate,
+                                                         nullptr);
+      for (int k = 0; k < P; ++k) constrained[k] = softplus(raw[k]);
+      return;
+    }
+    HostStream stream(seed, 9, 0);  // kCentroids
+    std::vector<double> acc(P, 0.0), local_x(static_cast<size_t>(subset) * d), local_y(subset);
+    std::vector<int> order(n);
+    std::vector<double> dist2(n);
+    for (int c = 0; c < n_centroids; ++c) {
+      const int centroid = static_cast<int>(stream.next_u64() % static_cast<uint64_t>(n));
+      for (int i = 0; i < n; ++i) {  // squared distance in column order (inputs column-major)
+        double s2 = 0.0;
+        for (int k = 0; k < d; ++k) {
+          const double t = inputs[static_cast<size_t>(k) * n + i] - inputs[static_cast<size_t>(k) * n + centroid];
+          s2 += t * t;
+        }
+        dist2[i] = s2;
+      }
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return dist2[a] < dist2[b]; });
+      for (int i = 0; i < subset; ++i) {
+        for (int k = 0; k < d; ++k) local_x[static_cast<size_t>(k) * subset + i] = inputs[static_cast<size_t>(k) * n + order[i]];
+        local_y[i] = targets[order[i]];
+      }
+      const std::vector<double> raw = optimise_exact_dev(ctx, local_x.data(), local_y.data(), subset, d, init,
+                                                         adam_steps, learning_rate, nullptr);
+      for (int k = 0; k < P; ++k) acc[k] += softplus(raw[k]);
+    }
+    for (int k = 0; k < P; ++k) {
+      const double mean = acc[k] / n_centroids;
+      constrained[k] = softplus(softplus_inverse(mean));  // Hyperparameters::from_constrained round trip
     }
   });
 }

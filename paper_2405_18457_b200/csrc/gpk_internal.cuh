@@ -234,6 +234,9 @@ void spd_leaf_inverse_launch(const double* a, double* out, int off, int nn, int 
                              int* info, cudaStream_t s);
 void block_transpose_launch(const double* src, double* dst, int rows, int cols, int ld, long long stride, int batch,
                             cudaStream_t s);
+void exact_forms_launch(const double* xs64, int n, int d, const double* hinv, const double* alpha, double* part,
+                        cudaStream_t s);
+long long exact_forms_blocks(int n);
 void set_identity_launch(double* mats, int dim, int batch, cudaStream_t s);
 
 // AP (K8)

@@ -700,6 +700,85 @@ void block_transpose_launch(const double* src, double* dst, int rows, int cols, 
   check_launch("block_transpose");
 }
 
+// Exact marginal-likelihood gradient forms (exact.cpp:33-50): with
+// W = (alpha alpha^T - H^-1) / 2, the constrained gradient is
+// sum_ij W_ij dH_ij/dtheta; dH is evaluated on the fly (FP64, kernel.cpp:200-232
+// in scaled differences), W from alpha and the lower triangle of H^-1
+// (column-major, cuSOLVER potri). CTA = one 32 x 32 tile (ti >= tj, weight 2
+// off the diagonal tile and for i > j inside it); per-CTA partials
+// [d lengthscale sums | signal sum | diagonal sum] in a fixed order.
+__global__ void exact_forms_kernel(const double* xs64, int n, int d, const double* hinv, const double* alpha,
+                                   double* part) {
+  __shared__ double xr[32][33], xc[32][33];
+  __shared__ double red[8][34];
+  const int T = (n + 31) / 32;
+  const long long L = blockIdx.x;
+  // tile (ti, tj), ti >= tj: row-major lower-triangle enumeration
+  int ti = static_cast<int>((sqrt(8.0 * static_cast<double>(L) + 1.0) - 1.0) / 2.0);
+  while (static_cast<long long>(ti) * (ti + 1) / 2 > L) --ti;
+  while (static_cast<long long>(ti + 1) * (ti + 2) / 2 <= L) ++ti;
+  const int tj = static_cast<int>(L - static_cast<long long>(ti) * (ti + 1) / 2);
+  (void)T;
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+    const int a = e / 32, q = e % 32;
+    const int ri = ti * 32 + a, rj = tj * 32 + a;
+    xr[a][q] = (q < d && ri < n) ? xs64[static_cast<size_t>(ri) * d + q] : 0.0;
+    xc[a][q] = (q < d && rj < n) ? xs64[static_cast<size_t>(rj) * d + q] : 0.0;
+  }
+  __syncthreads();
+  double al[32], as = 0.0, an = 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) al[k] = 0.0;
+  const int c = threadIdx.x & 31;
+  const int j = tj * 32 + c;
+  for (int rr = threadIdx.x >> 5; rr < 32; rr += blockDim.x >> 5) {
+    const int i = ti * 32 + rr;
+    if (i >= n || j >= n || i < j) continue;
+    const double Wij = 0.5 * (alpha[i] * alpha[j] - hinv[static_cast<size_t>(i) + static_cast<size_t>(j) * n]);
+    const double w = (i == j) ? Wij : 2.0 * Wij;
+    double r2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double t = xc[c][k] - xr[rr][k];
+      r2 += t * t;
+    }
+    const double r = sqrt(r2);
+    const double e0 = exp(-1.7320508075688772 * r);
+    as += w * (1.0 + 1.7320508075688772 * r) * e0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < d) {
+        const double t = xc[c][k] - xr[rr][k];
+        al[k] += w * e0 * (t * t);
+      }
+    if (i == j) an += Wij;
+  }
+  // fixed-order block reduction: warp xor trees, then warps in order
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = 0; k < d + 2; ++k) {
+    double v = k < d ? al[k < 32 ? k : 0] : (k == d ? as : an);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < d + 2; k += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) v += red[w][k];
+    part[static_cast<size_t>(blockIdx.x) * (d + 2) + k] = v;
+  }
+}
+void exact_forms_launch(const double* xs64, int n, int d, const double* hinv, const double* alpha, double* part,
+                        cudaStream_t s) {
+  if (d > 32) throw std::invalid_argument("gpk: input dimension > 32 is not supported");
+  const long long T = (n + 31) / 32;
+  exact_forms_kernel<<<static_cast<unsigned>(T * (T + 1) / 2), 256, 0, s>>>(xs64, n, d, hinv, alpha, part);
+  check_launch("exact_forms");
+}
+long long exact_forms_blocks(int n) {
+  const long long T = (n + 31) / 32;
+  return T * (T + 1) / 2;
+}
+
 __global__ void set_identity_kernel(double* mats, int dim, long long total) {
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {

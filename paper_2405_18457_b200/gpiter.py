@@ -739,3 +739,29 @@ def spd_inverse(ctx: Context, mats, mode: int = 1):
     check(ctx._lib.gpk_spd_inverse(ctx.handle, _p(src), dim, batch, int(mode), _p(out)))
     return np.transpose(out, (0, 2, 1)).copy()
 
+
+def optimise_exact(ctx: Context, inputs, targets, steps: int, learning_rate: float = 0.1, init_constrained=None):
+    """optimise_exact (outer_loop.cpp:248-262) on the device: Adam on the exact
+    marginal likelihood. Returns (trajectory steps x (d+2) constrained, final raw)."""
+    X = _f64(inputs)
+    y = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1)
+    n, d = X.shape
+    traj = np.empty((steps, d + 2))
+    raw = np.empty(d + 2)
+    init = np.ascontiguousarray(init_constrained, dtype=np.float64) if init_constrained is not None else None
+    check(ctx._lib.gpk_optimise_exact(ctx.handle, _p(X), _p(y), n, d, _p(init), steps, learning_rate, _p(traj),
+                                      _p(raw)))
+    return traj, raw
+
+
+def init_heuristic(ctx: Context, inputs, targets, n_centroids: int, subset: int, seed: int, adam_steps: int,
+                   learning_rate: float = 0.1):
+    """init_heuristic (outer_loop.cpp:264-296) on the device: constrained d+2."""
+    X = _f64(inputs)
+    y = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1)
+    n, d = X.shape
+    out = np.empty(d + 2)
+    check(ctx._lib.gpk_init_heuristic(ctx.handle, _p(X), _p(y), n, d, n_centroids, subset, seed, adam_steps,
+                                      learning_rate, _p(out)))
+    return out
+

@@ -387,3 +387,28 @@ def test_optimise_exact_dense_prior_matches_oracle(G, gpk_ctx, oracle):
     ocfg["prior_mode"] = 0
     r0 = G.optimise(gpk_ctx, X, y, G.OuterConfig(solver=G.SolverConfig(**scfg), **ocfg))
     assert not np.array_equal(r0["gradient"][0], r["gradient"][0])
+
+
+@pytest.mark.parametrize("n,d,steps", [(300, 2, 15), (700, 5, 8)])
+def test_optimise_exact_matches_oracle(G, gpk_ctx, oracle, n, d, steps):
+    """Row f4: Adam on the exact MLL (cuSOLVER Cholesky/inverse + fused FP64 dH pass)."""
+    X, y = gp_problem(n, d, 13 * n)
+    traj, raw = G.gpiter.optimise_exact(gpk_ctx, X, y, steps, 0.1)
+    rtraj, rraw = oracle.optimise_exact(X, y, steps, 0.1)
+    assert np.max(np.abs(traj - rtraj) / rtraj) <= 1e-8
+    assert np.max(np.abs(raw - rraw)) <= 1e-8 * np.max(np.abs(rraw))
+    # one exact gradient against the oracle's dense restatement
+    _, g = oracle.exact(X, y, rraw)
+    _, rraw1 = oracle.optimise_exact(X, y, 1, 0.1, init_constrained=[oracle.softplus(v) for v in rraw])
+    _, graw1 = G.gpiter.optimise_exact(gpk_ctx, X, y, 1, 0.1, init_constrained=[oracle.softplus(v) for v in rraw])
+    assert np.max(np.abs(graw1 - rraw1)) <= 1e-8 * np.max(np.abs(rraw1))
+
+
+def test_init_heuristic_matches_oracle(G, gpk_ctx, oracle):
+    X, y = gp_problem(900, 3, 4321)
+    got = G.gpiter.init_heuristic(gpk_ctx, X, y, 3, 200, 11, 10, 0.1)
+    ref = oracle.init_heuristic(X, y, 3, 200, 11, 10, 0.1)
+    assert np.max(np.abs(got - ref) / ref) <= 1e-8
+    whole = G.gpiter.init_heuristic(gpk_ctx, X[:150], y[:150], 1, 150, 7, 10, 0.1)
+    _, raw = oracle.optimise_exact(X[:150], y[:150], 10, 0.1)
+    assert np.max(np.abs(whole - [oracle.softplus(v) for v in raw])) <= 1e-8

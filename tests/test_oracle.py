@@ -488,3 +488,38 @@ def test_optimise_exact_dense_prior_mode(oracle):
     cfg.prior_mode = 0
     r3 = oracle.optimise(X, y, cfg)
     assert not np.array_equal(r["gradient"][0], r3["gradient"][0])  # a different prior
+
+
+def test_init_heuristic_falls_back_to_whole_dataset(oracle):  # test_outer_loop.cpp:170-178
+    X, y = gp_problem(40, 1, 415)
+    _, raw = oracle.optimise_exact(X, y, 30, 0.1)
+    direct = np.array([oracle.softplus(r) for r in raw])
+    averaged = oracle.init_heuristic(X, y, 1, 40, 7, 30, 0.1)
+    assert np.max(np.abs(averaged - direct)) <= 1e-12
+
+
+def test_init_heuristic_averages_per_cluster_optima(oracle):  # test_outer_loop.cpp:180-211
+    per = 60
+    rng = np.random.default_rng(417)
+
+    def cluster(center, ls, seed):
+        Xc, _ = gp_problem(per, 1, seed)
+        Xc = Xc * ls + center  # lengthscale-like spread, far-apart centres
+        yc = np.sin(Xc[:, 0] / ls) + 0.1 * rng.standard_normal(per)
+        return Xc, yc
+
+    XL, yL = cluster(0.0, 0.4, 7)
+    XR, yR = cluster(40.0, 2.5, 4007)
+    X = np.vstack([XL, XR])
+    y = np.concatenate([yL, yR])
+    lsL = oracle.softplus(oracle.optimise_exact(XL, yL, 60, 0.1)[1][0])
+    lsR = oracle.softplus(oracle.optimise_exact(XR, yR, 60, 0.1)[1][0])
+    ls = oracle.init_heuristic(X, y, 6, per, 11, 60, 0.1)[0]
+    assert min(lsL, lsR) - 1e-9 <= ls <= max(lsL, lsR) + 1e-9
+
+
+def test_optimise_exact_trajectory_starts_at_init(oracle):
+    X, y = gp_problem(50, 2, 419)
+    traj, raw = oracle.optimise_exact(X, y, 5, 0.1)
+    assert np.allclose(traj[0], 1.0)
+    assert traj.shape == (5, 4) and np.all(np.isfinite(raw))
