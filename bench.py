@@ -60,6 +60,8 @@ CONFIGS = {
                block=1000, batch=500, lr_sgd=30.0),
     "C4": dict(n=393216, d=3, uniform=True, noise=0.05, kind=2, s=64, rff_pairs=1000, steps=30, max_epochs=10,
                block=1000, batch=512, lr_sgd=10.0),
+    "C5": dict(n=1835008, d=11, uniform=False, noise=0.1, kind=0, s=64, rff_pairs=2048, steps=15, max_epochs=5,
+               block=1000, batch=500, lr_sgd=30.0),
 }
 WORKLOAD = "C2"
 SEEDS = dict(data=0, probe=2, feature=3, solver=4)
@@ -67,7 +69,7 @@ SEEDS = dict(data=0, probe=2, feature=3, solver=4)
 
 def workload_config(name):
     c = CONFIGS[name]
-    desc = {"C1": "CG", "C2": "AP b=512", "C3": "CG T=10", "C4": "SGD b=512 momentum 0.9"}[name]
+    desc = {"C1": "CG", "C2": "AP b=512", "C3": "CG T=10", "C4": "SGD b=512 momentum 0.9", "C5": "CG T=5"}[name]
     return {"workload": f"{name}: n={c['n']} d={c['d']} {desc} s={c['s']} rff_pairs={c['rff_pairs']} "
                         f"warm start tol 0.01 Adam lr 0.1 (BASELINE.json configs[{list(CONFIGS).index(name)}])",
             "n": c["n"], "d": c["d"], "rhs": c["s"] + 1, "solver": desc, "l2": "flushed between timed steps",
