@@ -93,6 +93,7 @@ struct gpk_ctx {
   int kernel = 1;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32 (default)
   bool fused_ap = true;  // AP slabs: reduce + epilogue fused into the tcgen05 kernel
   int spd_inverse = 1;   // AP block inverses: 1 recursive Schur/DGEMM, 0 cuSOLVER potrf + 2 trsm
+  int kv_deep = -1;  // operator launches one CTA per SM with 16 eval warps: -1 auto (>= 1e8 entries), 0/1 forced
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
   DBuf<double> rff_feat;  // RFF feature rows (prior GEMM), reused across calls
@@ -344,7 +345,13 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   if (fused && !(tc && c.sel && c.ctl && c.spart && c.dotw == c.out && !c.row_idx && c.r0 == 0 &&
                  c.score_block % 128 == 0 && c.groups == (c.R + 127) / 128 && c.gpb == c.score_block / 128))
     throw std::logic_error("run_kv: fused AP slab preconditions");
-  int splits = fused ? 1 : tc ? kv_tc_choose_splits(c.R, Cmax, op->ctx->sms) : kv_choose_splits(c.R, Cmax, op->ctx->sms);
+  // deep variant (1 CTA/SM, 16 eval warps, 4 TMEM A buffers) measured faster
+  // on large launches (C2 -4%, d=3 -24%) and slower on small ones (C1 +26%)
+  const bool deep = tc && !fused &&
+                    (op->ctx->kv_deep >= 0 ? op->ctx->kv_deep != 0 : static_cast<double>(c.R) * Cmax >= 1e8);
+  int splits = fused ? 1
+               : tc ? kv_tc_choose_splits(c.R, Cmax, op->ctx->sms, deep ? 1 : 2)
+                    : kv_choose_splits(c.R, Cmax, op->ctx->sms);
   int cps = (Cmax + splits - 1) / splits;
   cps = (cps + 31) / 32 * 32;
   splits = std::max(1, (Cmax + cps - 1) / cps);
@@ -440,7 +447,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
     return;
   }
   if (tc)
-    kv_tc_launch(a, vpk, s);
+    kv_tc_launch(a, vpk, s, deep);
   else
     kv_slab_launch(a, op->d, s);
   if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
@@ -1701,6 +1708,7 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     c->sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("GPK_FUSED_AP")) c->fused_ap = std::atoi(e) != 0;  // A/B switches
     if (const char* e = std::getenv("GPK_SPD_INVERSE")) c->spd_inverse = std::atoi(e);
+    if (const char* e = std::getenv("GPK_KV_DEEP")) c->kv_deep = std::atoi(e);
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     GPK_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev_m2a, cudaEventDisableTiming));

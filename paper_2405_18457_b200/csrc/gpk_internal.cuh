@@ -64,14 +64,14 @@ int kv_tc_for(int m);        // columns-per-lane template parameter for m
 int kv_ld_for(int m);        // FP32 RHS leading dimension for m
 void kv_slab_launch(const KvArgs& a, int dmax, cudaStream_t s);
 int kv_choose_splits(int R, int C, int sms, int rows_per_cta = 256);
-int kv_tc_choose_splits(int R, int C, int sms);
+int kv_tc_choose_splits(int R, int C, int sms, int ctas_per_sm = 2);
 
 // tcgen05 (3xTF32) variant of the operator slab (kv_tc_kernel.cu)
 int kv_tc_npad(int m);
 size_t kv_tc_pack_floats(int m, int rows);
 void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_max, int m, const int* sel,
                        int sel_block, int n, float* vpk, const int* skip, cudaStream_t s, int rows_valid = -1);
-void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s);
+void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s, bool deep = false);
 struct KvReduceArgs;
 // AP slab with the reduce fused into the tensor-core kernel (splits == 1,
 // one accumulation group, score_block a multiple of 128): writes out, the

@@ -456,7 +456,7 @@ int kv_choose_splits(int R, int C, int sms, int rows_per_cta) {
 // (TMEM alloc, pipeline fill, FP64 epilogue, split-K partial traffic) is
 // worth ~4 chunks. Favours few long CTAs for short column ranges (AP slabs)
 // and enough CTAs to balance 148 SMs for full products.
-int kv_tc_choose_splits(int R, int C, int sms) {
+int kv_tc_choose_splits(int R, int C, int sms, int ctas_per_sm) {
   const int tiles = (R + 127) / 128;
   const int chunks = (C + BK - 1) / BK;
   int best = 1;
@@ -464,7 +464,7 @@ int kv_tc_choose_splits(int R, int C, int sms) {
   for (int s = 1; s <= std::max(1, chunks); ++s) {
     const long long ctas = static_cast<long long>(tiles) * s;
     const double per = static_cast<double>((chunks + s - 1) / s) + 4.0;
-    const long long slots = 2LL * sms;  // two co-resident CTAs per SM (256 TMEM columns each)
+    const long long slots = static_cast<long long>(ctas_per_sm) * sms;  // co-resident CTAs (TMEM columns)
     const double cost = static_cast<double>((ctas + slots - 1) / slots) * per * (1.0 + 1e-3 * s);
     if (cost < best_cost) {
       best_cost = cost;

@@ -149,23 +149,28 @@ __device__ __forceinline__ void fused_drain(const KvArgs& a, const KvReduceArgs&
   ap_epilogue(f, static_cast<int>(gridDim.x), tid, EW, ss, bscore, [] { eval_bar<EW>(); });
 }
 
-template <bool FUSED>
+// MODE 0: two CTAs per SM, 8 evaluation warps, 2 TMEM A buffers (default);
+// MODE 1: fused AP slab; MODE 2: "deep" -- one CTA per SM with 16 evaluation
+// warps and 4 A buffers (512 TMEM columns), for launches whose per-chunk
+// barrier/MMA latency dominates (small d, few rows).
+template <int MODE>
 struct TcRoles {
-  static constexpr int EW = FUSED ? 16 : EVAL_WARPS;  // evaluation warps
+  static constexpr int EW = MODE ? 16 : EVAL_WARPS;  // evaluation warps
   static constexpr int THREADS = 32 * (EW + 2);
   static constexpr int CPT = TBK * 4 / EW;            // chunk columns per eval thread
 };
 
-template <int NPAD, int DP4, bool FUSED>
-__global__ void __launch_bounds__(TcRoles<FUSED>::THREADS, FUSED ? 1 : 2)
+template <int NPAD, int DP4, int MODE>
+__global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk, const KvReduceArgs f) {
-  constexpr int EW = TcRoles<FUSED>::EW, CPT = TcRoles<FUSED>::CPT;
+  constexpr bool FUSED = MODE == 1, DEEP = MODE != 0;
+  constexpr int EW = TcRoles<MODE>::EW, CPT = TcRoles<MODE>::CPT;
   constexpr int DP = 4 * DP4;
   using L = TcLayout<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the fused AP slab runs one CTA per SM: 4 TMEM A buffers (512 columns)
-  constexpr int NAB = FUSED ? 4 : 2;
-  constexpr int TCOLS = FUSED ? 512 : TMEM_COLS;
+  constexpr int NAB = DEEP ? 4 : 2;
+  constexpr int TCOLS = DEEP ? 512 : TMEM_COLS;
   float* smB = reinterpret_cast<float*>(smem_raw);                    // [STAGES][CHUNK_FLOATS]
   float* smX = smB + STAGES * L::CHUNK_FLOATS;                        // [STAGES][TBK][DP]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * TBK * DP);
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(TcRoles<FUSED>::THREADS, FUSED ? 1 : 2)
 #endif
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
     double* part = a.part + static_cast<size_t>(split) * a.R * a.m;
-    constexpr int DCOLS = NPAD / 2;  // D columns this thread drains
+    constexpr int DCOLS = NPAD / (EW / 4);  // D columns this thread drains
     bool wrote = false;
 
     for (int k = 0; k < nq; ++k) {
@@ -381,15 +386,15 @@ __global__ void __launch_bounds__(TcRoles<FUSED>::THREADS, FUSED ? 1 : 2)
         } else {
         const bool row_ok = er < a.R;
         double* prow = part + static_cast<size_t>(er_c) * a.m;
-#pragma unroll
-        for (int q = 0; q < DCOLS / 8; ++q) {
-          const int col0 = half * DCOLS + q * 8;
-          uint32_t v[8];
-          tc_ld8(tmem + lane_addr + col0, v);
+#pragma unroll 1
+        for (int q = 0; q < DCOLS / 4; ++q) {
+          const int col0 = half * DCOLS + q * 4;
+          uint32_t v[4];
+          tc_ld4(tmem + lane_addr + col0, v);
           tc_wait_ld();
           if (row_ok) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < 4; ++e) {
               const int col = col0 + e;
               if (col < a.m) prow[col] = (wrote ? prow[col] : 0.0) + static_cast<double>(__uint_as_float(v[e]));
             }
@@ -455,48 +460,51 @@ __global__ void kv_pack_kernel(const double* v64, const float* v32, int ldv, int
   }
 }
 
-template <int NPAD, int DP4, bool FUSED>
+template <int NPAD, int DP4, int MODE>
 void launch_tc_one(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
+  constexpr bool FUSED = MODE == 1;
   using L = TcLayout<NPAD>;
   // + the fused drain's scratch behind the barriers (bars + 64 words: ~14 KB)
   const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 32 * sizeof(uint64_t) +
                       (FUSED ? 64 * sizeof(uint64_t) + sizeof(double) * (FUSED_SCRATCH_DOUBLES + TBM * 96) : 0);
   // at most 2 CTAs per SM: each allocates 256 of the 512 TMEM columns
-  const size_t smem = std::max<size_t>(need, 100 * 1024);
+  // one CTA per SM in MODE 1/2 (512 TMEM columns each): >= 120 KB keeps a
+  // second CTA off the SM; two per SM otherwise (256 columns each)
+  const size_t smem = std::max<size_t>(need, MODE ? 120 * 1024 : 100 * 1024);
   static bool configured = false;
   if (!configured) {
-    GPK_CUDA(cudaFuncSetAttribute(kv_tc_kernel<NPAD, DP4, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GPK_CUDA(cudaFuncSetAttribute(kv_tc_kernel<NPAD, DP4, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = true;
   }
   dim3 grid((a.R + TBM - 1) / TBM, a.splits);
-  kv_tc_kernel<NPAD, DP4, FUSED><<<grid, TcRoles<FUSED>::THREADS, smem, s>>>(a, vpk, f);
+  kv_tc_kernel<NPAD, DP4, MODE><<<grid, TcRoles<MODE>::THREADS, smem, s>>>(a, vpk, f);
   check_launch("kv_tc_kernel");
 }
 
-template <int NPAD, bool FUSED>
+template <int NPAD, int MODE>
 void launch_tc_n(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   switch (a.dp / 4) {
-    case 1: return launch_tc_one<NPAD, 1, FUSED>(a, vpk, f, s);
-    case 2: return launch_tc_one<NPAD, 2, FUSED>(a, vpk, f, s);
-    case 3: return launch_tc_one<NPAD, 3, FUSED>(a, vpk, f, s);
-    case 4: return launch_tc_one<NPAD, 4, FUSED>(a, vpk, f, s);
-    case 5: return launch_tc_one<NPAD, 5, FUSED>(a, vpk, f, s);
-    case 6: return launch_tc_one<NPAD, 6, FUSED>(a, vpk, f, s);
-    case 7: return launch_tc_one<NPAD, 7, FUSED>(a, vpk, f, s);
-    case 8: return launch_tc_one<NPAD, 8, FUSED>(a, vpk, f, s);
+    case 1: return launch_tc_one<NPAD, 1, MODE>(a, vpk, f, s);
+    case 2: return launch_tc_one<NPAD, 2, MODE>(a, vpk, f, s);
+    case 3: return launch_tc_one<NPAD, 3, MODE>(a, vpk, f, s);
+    case 4: return launch_tc_one<NPAD, 4, MODE>(a, vpk, f, s);
+    case 5: return launch_tc_one<NPAD, 5, MODE>(a, vpk, f, s);
+    case 6: return launch_tc_one<NPAD, 6, MODE>(a, vpk, f, s);
+    case 7: return launch_tc_one<NPAD, 7, MODE>(a, vpk, f, s);
+    case 8: return launch_tc_one<NPAD, 8, MODE>(a, vpk, f, s);
     default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
   }
 }
 
-template <bool FUSED>
+template <int MODE>
 void launch_tc(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   switch (kv_tc_npad(a.m)) {
-    case 16: return launch_tc_n<16, FUSED>(a, vpk, f, s);
-    case 32: return launch_tc_n<32, FUSED>(a, vpk, f, s);
-    case 48: return launch_tc_n<48, FUSED>(a, vpk, f, s);
-    case 64: return launch_tc_n<64, FUSED>(a, vpk, f, s);
-    case 80: return launch_tc_n<80, FUSED>(a, vpk, f, s);
+    case 16: return launch_tc_n<16, MODE>(a, vpk, f, s);
+    case 32: return launch_tc_n<32, MODE>(a, vpk, f, s);
+    case 48: return launch_tc_n<48, MODE>(a, vpk, f, s);
+    case 64: return launch_tc_n<64, MODE>(a, vpk, f, s);
+    case 80: return launch_tc_n<80, MODE>(a, vpk, f, s);
     default: throw std::invalid_argument("gpk: tensor-core operator supports m <= 80");
   }
 }
@@ -521,14 +529,17 @@ void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_ma
   check_launch("kv_pack_kernel");
 }
 
-void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s) {
+void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s, bool deep) {
   const KvReduceArgs none{};
-  launch_tc<false>(a, vpk, none, s);
+  if (deep)
+    launch_tc<2>(a, vpk, none, s);
+  else
+    launch_tc<0>(a, vpk, none, s);
 }
 
 void kv_tc_fused_launch(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   if (a.splits != 1) throw std::invalid_argument("gpk: fused slab reduce needs one column split");
-  launch_tc<true>(a, vpk, f, s);
+  launch_tc<1>(a, vpk, f, s);
 }
 
 }  // namespace gpk

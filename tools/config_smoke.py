@@ -18,10 +18,13 @@ import paper_2405_18457_b200 as G  # noqa: E402
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    argv = sys.argv[1:]
     steps = 2
-    if "--steps" in sys.argv:
-        steps = int(sys.argv[sys.argv.index("--steps") + 1])
+    if "--steps" in argv:
+        i = argv.index("--steps")
+        steps = int(argv[i + 1])
+        argv = argv[:i] + argv[i + 2:]
+    args = argv
     names = args or ["C1", "C2", "C3", "C4", "C5"]
     ctx = G.Context(0)
     for name in names:
