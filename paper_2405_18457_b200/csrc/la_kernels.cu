@@ -1259,41 +1259,53 @@ void sgd_check_launch(const double* sumsq, int m, const double* scales, double t
 // slice so every rank updates an identical replicated copy.
 __global__ void sgd_prep_kernel(const double* hv_part, const int* idx, int b, const double* targets,
                                 const double* R, int row0, int nloc, int m, int* pos, const int* nonfinite,
-                                double* slice, const int* skip) {
+                                double* slice, int grad_blocks, const int* skip) {
   SKIP_IF(skip);
   const int bm = b * m;
-  if (blockIdx.x == gridDim.x - 1) {  // old squares, pos map, flag
+  if (static_cast<int>(blockIdx.x) >= grad_blocks) {
+    // one block per column j: sum over the batch rows owned by this rank of
+    // R_old[row][j]^2 (fixed order: strided lanes, xor trees, warps in order)
+    const int j = blockIdx.x - grad_blocks;
+    __shared__ double wsum[32];
+    double acc = 0.0;
     for (int q = threadIdx.x; q < b; q += blockDim.x) {
       const int li = idx[q] - row0;
-      if (li >= 0 && li < nloc) pos[li] = q;
-    }
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-      double acc = 0.0;
-      for (int q = 0; q < b; ++q) {
-        const int li = idx[q] - row0;
-        if (li >= 0 && li < nloc) {
-          const double r = R[static_cast<size_t>(li) * m + j];
-          acc += r * r;
-        }
+      if (li >= 0 && li < nloc) {
+        const double r = R[static_cast<size_t>(li) * m + j];
+        acc += r * r;
       }
-      slice[bm + j] = acc;
     }
-    if (threadIdx.x == 0) slice[bm + m] = *nonfinite ? 1.0 : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += wsum[w];
+      slice[bm + j] = t;
+      if (j == 0) slice[bm + m] = *nonfinite ? 1.0 : 0.0;
+    }
+    if (j == 0)
+      for (int q = threadIdx.x; q < b; q += blockDim.x) {
+        const int li = idx[q] - row0;
+        if (li >= 0 && li < nloc) pos[li] = q;
+      }
     return;
   }
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bm; e += (gridDim.x - 1) * blockDim.x) {
-    const int q = e / m, j = e - q * m;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bm; e += grad_blocks * blockDim.x) {
+    const int q = e / m, jj = e - q * m;
     const int li = idx[q] - row0;
     double g = hv_part[e];
-    if (li >= 0 && li < nloc) g -= targets[static_cast<size_t>(li) * m + j];
+    if (li >= 0 && li < nloc) g -= targets[static_cast<size_t>(li) * m + jj];
     slice[e] = g;
   }
 }
 void sgd_prep_launch(const double* hv_part, const int* idx, int b, const double* targets, const double* R,
                      int row0, int nloc, int m, int* pos, const int* nonfinite, double* slice, const int* skip,
                      cudaStream_t s) {
-  const int blocks = blocks_for(static_cast<long long>(b) * m, 256, 64) + 1;
-  sgd_prep_kernel<<<blocks, 256, 0, s>>>(hv_part, idx, b, targets, R, row0, nloc, m, pos, nonfinite, slice, skip);
+  const int gb = blocks_for(static_cast<long long>(b) * m, 256, 64);
+  sgd_prep_kernel<<<gb + m, 256, 0, s>>>(hv_part, idx, b, targets, R, row0, nloc, m, pos, nonfinite, slice, gb,
+                                         skip);
   check_launch("sgd_prep");
 }
 
