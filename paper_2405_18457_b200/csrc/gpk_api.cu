@@ -281,6 +281,7 @@ void set_hyper(gpk_operator* op, const double* raw) {
     if (!std::isfinite(c) || c <= 0.0)
       throw InvalidArgument("Hyperparameters: constrained value " + std::to_string(k) + " is not finite and positive");
   }
+  if (op->raw == r && op->hyper_version > 0) return;  // unchanged: scaled inputs and AP blocks stay valid
   op->raw = r;
   ++op->hyper_version;
   op->inv_ls.resize(d);
@@ -1605,7 +1606,7 @@ void rff_prior_dev(gpk_operator* op, gpk_rff_basis* b, int s_count, double* prio
   // this rank's rows only (all rows on one GPU)
   rff_prior_gemm(op->ctx, op->x64.p + static_cast<size_t>(op->row0) * d, op->nloc, d, fd, P, b->w_dev.p, s_count,
                  amplitude, prior);
-  GPK_CUDA(cudaStreamSynchronize(s));
+  // no synchronisation: the pageable uploads above are staged before return
 }
 
 // ------------------------------------------------------------- posterior
@@ -2467,7 +2468,10 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
   set_hyper(op, o->raw.data());
   // AP: factor the diagonal blocks on the auxiliary stream while the targets
   // and the residual refresh run on the main stream
-  if (o->sc.kind == GPK_AP && !op->sharded) ap_prepare(b, std::min(o->sc.block_size, nloc));
+  if (o->sc.kind == GPK_AP && !op->sharded) {
+    const int blk = std::min(o->sc.block_size, nloc);
+    if (!(b->ap_ready && b->ap_block == blk && b->ap_version == op->hyper_version)) ap_prepare(b, blk);
+  }
   g_phase.mark("set_hyper");
   const uint64_t substream = cfg.warm_start ? 0 : static_cast<uint64_t>(t);
   if (pathwise) {
@@ -2574,6 +2578,13 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
     for (int k = 0; k < P; ++k) o->raw[k] += upd[k];
     GPK_CUDA(cudaMemcpyAsync(o->prev.p, b->solutions.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, stream));
     o->have_previous = true;
+    // AP: the next step's hyperparameters are known now -- scale the inputs and
+    // start factoring its diagonal blocks on the auxiliary stream, so the work
+    // overlaps the caller's gap between steps and the next targets/refresh
+    if (o->sc.kind == GPK_AP && !op->sharded && t + 1 < cfg.steps) {
+      set_hyper(op, o->raw.data());
+      ap_prepare(b, std::min(o->sc.block_size, nloc));
+    }
     g_phase.mark("adam");
     g_phase.finish();
   }
