@@ -77,6 +77,8 @@ double sigmoid(double x) {  // hyperparameters.cpp:19-23
 
 }  // namespace
 
+constexpr size_t kBlasWorkspace = 32u << 20;
+
 struct gpk_ctx {
   int device = 0;
   int sms = 148;
@@ -93,7 +95,9 @@ struct gpk_ctx {
   int kernel = 1;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32 (default)
   bool fused_ap = true;  // AP slabs: reduce + epilogue fused into the tcgen05 kernel
   int spd_inverse = 1;   // AP block inverses: 1 recursive Schur/DGEMM, 0 cuSOLVER potrf + 2 trsm
-  int kv_deep = -1;  // operator launches one CTA per SM with 16 eval warps: -1 auto (>= 1e8 entries), 0/1 forced
+  int kv_deep = -1;
+  bool graphs = true;  // CG/AP iteration groups as CUDA graphs (GPK_GRAPHS=0 disables)
+  void* blas_ws = nullptr;  // operator launches one CTA per SM with 16 eval warps: -1 auto (>= 1e8 entries), 0/1 forced
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
   DBuf<double> rff_feat;  // RFF feature rows (prior GEMM), reused across calls
@@ -635,16 +639,30 @@ void precond_apply_dev(gpk_precond* pc, gpk_operator* op, const double* R, int m
   // (L L^T + s2 I)^-1 R = (R - L (s2 I + L^T L)^-1 L^T R) / s2 ; L is replicated
   // (identical pivots on every rank), L^T R is a sum over rows -> partials of
   // this rank's rows, all-gathered and summed in rank order.
-  const int r = pc->achieved, G = kReduceGroups, nr = op->nr;
-  const double* Lloc = pc->L.p + static_cast<size_t>(op->row0) * pc->rank;
-  double* part = pc->part.ensure(static_cast<size_t>(nr) * G * r * m);
-  double* T = pc->T.ensure(static_cast<size_t>(r) * m);
+  const int r = pc->achieved, nr = op->nr;
+  const double* Lloc = pc->L.p + static_cast<size_t>(op->row0) * pc->rank;  // column-major view: rank x n
+  double* part = pc->part.ensure(static_cast<size_t>(nr) * r * m);
+  double* T = nr > 1 ? pc->T.ensure(static_cast<size_t>(r) * m) : part;
   double* inner = pc->inner.ensure(static_cast<size_t>(r) * m);
-  lt_times_launch(Lloc, n, r, pc->rank, R, m, part + static_cast<size_t>(op->rk) * G * r * m, G, skip, s);
-  gather_inplace(op, part, sizeof(double) * G * r * m);
-  sum_partials_launch(part, G * nr, r * m, T, skip, s);
-  small_gemm_launch(pc->minv.p, r, r, T, m, inner, skip, s);
-  woodbury_launch(R, Lloc, n, r, pc->rank, inner, m, pc->sigma2, out, skip, s);
+  cublasHandle_t h = op->ctx->blas;
+  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+  const double one = 1.0, zero = 0.0, neg = -1.0 / pc->sigma2;
+  // T (r x m, column-major) = L^T R over this rank's rows; ranks' T summed in rank order
+  if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, r, m, n, &one, Lloc, pc->rank, R, m, &zero,
+                  part + static_cast<size_t>(op->rk) * r * m, r) != CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDgemm (L^T R)");
+  gather_inplace(op, part, sizeof(double) * r * m);
+  if (nr > 1) sum_partials_launch(part, nr, r * m, T, skip, s);
+  // inner = (s2 I + L^T L)^-1 T
+  if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, r, m, r, &one, pc->minv.p, r, T, r, &zero, inner, r) !=
+      CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDgemm (Minv T)");
+  // out = R / s2 - L inner / s2  (row-major out == column-major m x n)
+  scale_launch(R, n * m, pc->sigma2, out, skip, s);
+  if (cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, m, n, r, &neg, inner, r, Lloc, pc->rank, &one, out, m) !=
+      CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDgemm (L inner)");
+  count_launch(3);
 }
 
 // ----------------------------------------------------------------- batch
@@ -737,31 +755,70 @@ void finalise(gpk_batch* b, double tol, gpk_solver_report* rep, Clock::time_poin
 // Runs `enqueue_iteration` in groups, keeping one group in flight while the
 // previous group's control block is read back; stops once ctl.stop is set.
 template <class F>
-void drive(gpk_batch* b, CgCtl* ctl, int group, int max_iters, F&& enqueue_iteration) {
+void drive(gpk_batch* b, CgCtl* ctl, int group, int max_iters, F&& enqueue_iteration, bool capturable = false) {
   gpk_ctx* ctx = b->op->ctx;
   cudaStream_t s = ctx->stream;
+  // CUDA graph of one group of iterations (CG, AP): the iteration enqueues the
+  // same launches with the same arguments every time (all control flow is on
+  // device flags), so the group is captured once per solve and replayed; a
+  // replay past the budget is a no-op (every kernel tests ctl->stop).
+  const bool use_graph = capturable && ctx->graphs && !ctx->profiling && max_iters > group;
+  cudaGraphExec_t exec = nullptr;
+  long long per_group = 0;
+  auto enqueue_group = [&](int g) {
+    if (!use_graph) {
+      for (int i = 0; i < g; ++i) enqueue_iteration();
+      return;
+    }
+    if (!exec) {
+      const long long before = g_launch_counter ? *g_launch_counter : 0;
+      cudaGraph_t graph = nullptr;
+      GPK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+      try {
+        for (int i = 0; i < group; ++i) enqueue_iteration();
+      } catch (...) {
+        cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      GPK_CUDA(cudaStreamEndCapture(s, &graph));
+      const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      GPK_CUDA(e);
+      per_group = (g_launch_counter ? *g_launch_counter : 0) - before;  // counted once at capture
+    } else {
+      count_launch(static_cast<int>(per_group));
+    }
+    GPK_CUDA(cudaGraphLaunch(exec, s));
+  };
   int issued = 0, k = 0;
   bool pending = false;
-  while (true) {
-    const int g = std::min(group, max_iters - issued);
-    if (g > 0) {
-      for (int i = 0; i < g; ++i) enqueue_iteration();
-      issued += g;
+  try {
+    while (true) {
+      const int g = use_graph ? (issued < max_iters ? group : 0) : std::min(group, max_iters - issued);
+      if (g > 0) {
+        enqueue_group(g);
+        issued += g;
+      }
+      GPK_CUDA(cudaMemcpyAsync(&ctx->ctl_host[k & 1], ctl, sizeof(CgCtl), cudaMemcpyDeviceToHost, s));
+      GPK_CUDA(cudaEventRecord(ctx->ev[k & 1], s));
+      if (pending) {
+        GPK_CUDA(cudaEventSynchronize(ctx->ev[(k - 1) & 1]));
+        if (ctx->ctl_host[(k - 1) & 1].stop) break;
+      }
+      if (g <= 0) {
+        GPK_CUDA(cudaEventSynchronize(ctx->ev[k & 1]));
+        break;
+      }
+      pending = true;
+      ++k;
     }
-    GPK_CUDA(cudaMemcpyAsync(&ctx->ctl_host[k & 1], ctl, sizeof(CgCtl), cudaMemcpyDeviceToHost, s));
-    GPK_CUDA(cudaEventRecord(ctx->ev[k & 1], s));
-    if (pending) {
-      GPK_CUDA(cudaEventSynchronize(ctx->ev[(k - 1) & 1]));
-      if (ctx->ctl_host[(k - 1) & 1].stop) break;
-    }
-    if (g <= 0) {
-      GPK_CUDA(cudaEventSynchronize(ctx->ev[k & 1]));
-      break;
-    }
-    pending = true;
-    ++k;
+    GPK_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    if (exec) cudaGraphExecDestroy(exec);
+    throw;
   }
-  GPK_CUDA(cudaStreamSynchronize(s));
+  if (exec) GPK_CUDA(cudaGraphExecDestroy(exec));
 }
 
 void init_ctl(gpk_batch* b, int budget, int iters) {
@@ -843,7 +900,7 @@ void solve_cg(gpk_batch* b, const gpk_solver_config* c, gpk_precond* pc, gpk_sol
     cg_beta_launch(part, G * nr, m, b->scales_dev.p, c->tolerance, gamma, beta, ctl, s);
     cg_direction_launch(d, p, beta, n, m, d32, tc ? 0 : kv_ld_for(m), stop, s);
   };
-  drive(b, ctl, iteration_group(op->n), c->max_epochs, iteration);
+  drive(b, ctl, iteration_group(op->n), c->max_epochs, iteration, true);
   const CgCtl h = read_ctl(b);
   rep->iterations = h.iters;
   rep->epochs_consumed = h.iters;
@@ -1177,7 +1234,7 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     run_kv(op, kc);
     ap_check_launch(part, groups, m, b->scales_dev.p, c->tolerance, ctl, s);
   };
-  drive(b, ctl, 8, budget, iteration);
+  drive(b, ctl, 8, budget, iteration, true);
   g_phase.mark("ap_iterations");
   spd_inverse_check(ctx, nblocks);
   const CgCtl h = read_ctl(b);
@@ -1710,11 +1767,16 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     if (const char* e = std::getenv("GPK_FUSED_AP")) c->fused_ap = std::atoi(e) != 0;  // A/B switches
     if (const char* e = std::getenv("GPK_SPD_INVERSE")) c->spd_inverse = std::atoi(e);
     if (const char* e = std::getenv("GPK_KV_DEEP")) c->kv_deep = std::atoi(e);
+    if (const char* e = std::getenv("GPK_GRAPHS")) c->graphs = std::atoi(e) != 0;
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     GPK_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev_m2a, cudaEventDisableTiming));
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev_aux, cudaEventDisableTiming));
     if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate");
+    // explicit workspace: cuBLAS calls inside captured CUDA graphs must not allocate
+    GPK_CUDA(cudaMalloc(&c->blas_ws, kBlasWorkspace));
+    if (cublasSetWorkspace(c->blas, c->blas_ws, kBlasWorkspace) != CUBLAS_STATUS_SUCCESS)
+      throw CudaError("cublasSetWorkspace");
     if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate");
     GPK_CUDA(cudaMallocHost(&c->ctl_host, 2 * sizeof(CgCtl)));
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev[0], cudaEventDisableTiming));
@@ -1732,6 +1794,7 @@ gpk_status gpk_ctx_destroy(gpk_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->aux);
     cublasDestroy(c->blas);
+    cudaFree(c->blas_ws);
     cusolverDnDestroy(c->solver);
     cudaFreeHost(c->ctl_host);
     cudaEventDestroy(c->ev[0]);

@@ -387,19 +387,35 @@ __device__ __forceinline__ double matern64(const double* xs64, int d, int i, int
 
 // One greedy step (pivoted_cholesky.cpp:19-39): pivot = argmax diag; column
 // = (k(:, pivot) - L[:, :m] L[pivot, :m]^T) / sqrt(best); diag -= column^2.
-__global__ void pchol_step_kernel(const double* xs64, int n, int d, double s2, const double* pval, const int* pidx,
-                                  int groups, double* L, int ldl, int mcol, double* diag, int* pivots,
-                                  int* stop_flag) {
+__global__ void __launch_bounds__(256) pchol_step_kernel(const double* xs64, int n, int d, double s2,
+                                                         const double* pval, const int* pidx, int groups, double* L,
+                                                         int ldl, int mcol, double* diag, int* pivots, int* stop_flag) {
   if (*stop_flag) return;
   __shared__ double s_best;
   __shared__ int s_piv;
-  if (threadIdx.x == 0) {
+  __shared__ double lp[1024];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {  // argmax over the group partials: larger value, then lower index (strict '>' scan order)
     double best = -DBL_MAX;
     int bi = 0x7fffffff;
-    for (int g = 0; g < groups; ++g)
-      if (pval[g] > best || (pval[g] == best && pidx[g] < bi)) { best = pval[g]; bi = pidx[g]; }
-    s_best = best;
-    s_piv = bi;
+    for (int g = lane; g < groups; g += 32)
+      if (pval[g] > best || (pval[g] == best && pidx[g] < bi)) {
+        best = pval[g];
+        bi = pidx[g];
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      s_best = best;
+      s_piv = bi;
+    }
   }
   __syncthreads();
   const double best = s_best;
@@ -408,26 +424,30 @@ __global__ void pchol_step_kernel(const double* xs64, int n, int d, double s2, c
     if (blockIdx.x == 0 && threadIdx.x == 0) *stop_flag = 1;
     return;
   }
+  for (int k = threadIdx.x; k < mcol; k += blockDim.x) lp[k] = L[static_cast<size_t>(piv) * ldl + k];
+  __syncthreads();
   const double sb = sqrt(best);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double col = matern64(xs64, d, piv, i, s2);
-    if (mcol > 0) {
-      double acc = 0.0;
-      const double* li = L + static_cast<size_t>(i) * ldl;
-      const double* lp = L + static_cast<size_t>(piv) * ldl;
-      for (int k = 0; k < mcol; ++k) acc += li[k] * lp[k];
-      col -= acc;
+  // warp per row: lanes split the rank-mcol dot product with the pivot row
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
+  for (int i = gw; i < n; i += nw) {
+    const double* li = L + static_cast<size_t>(i) * ldl;
+    double acc = 0.0;
+    for (int k = lane; k < mcol; k += 32) acc += li[k] * lp[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const double col = (matern64(xs64, d, piv, i, s2) - acc) / sb;
+      L[static_cast<size_t>(i) * ldl + mcol] = col;
+      diag[i] = (i == piv) ? 0.0 : diag[i] - col * col;
     }
-    col /= sb;
-    L[static_cast<size_t>(i) * ldl + mcol] = col;
-    diag[i] = (i == piv) ? 0.0 : diag[i] - col * col;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) pivots[mcol] = piv;
 }
 void pchol_step_launch(const double* xs64, int n, int d, double s2, const double* pval, const int* pidx, int groups,
                        double* L, int ldl, int mcol, double* diag, int* pivots, int* stop_flag, cudaStream_t s) {
-  pchol_step_kernel<<<blocks_for(n, 256, 148 * 8), 256, 0, s>>>(xs64, n, d, s2, pval, pidx, groups, L, ldl, mcol,
-                                                               diag, pivots, stop_flag);
+  if (mcol > 1024) throw std::invalid_argument("gpk: preconditioner rank > 1024 is not supported");
+  pchol_step_kernel<<<std::min((n + 7) / 8, 148 * 4), 256, 0, s>>>(xs64, n, d, s2, pval, pidx, groups, L, ldl, mcol,
+                                                                  diag, pivots, stop_flag);
   check_launch("pchol_step");
 }
 
