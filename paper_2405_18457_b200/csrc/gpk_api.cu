@@ -1458,7 +1458,10 @@ __global__ void pair_dot_kernel(const double* u, const double* w, int n, int ldu
 // FP32 copies of U and W are all-gathered to full height (every tile needs all
 // columns), the global tile list is split evenly across ranks, and the per-block
 // partial sums are all-gathered and summed in (rank, block) order.
-std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vector<PairDev>& pairs) {
+// combine (nullable, one coefficient per pair): return the single form
+// sum_p combine[p] forms_p -- on the tensor-core pass accumulated per entry.
+std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vector<PairDev>& pairs,
+                                                const double* combine = nullptr) {
   cudaStream_t s = op->ctx->stream;
   const int n = op->n, d = op->d, P = static_cast<int>(pairs.size());
   const int nloc = op->nloc, nr = op->nr, rk = op->rk;
@@ -1512,6 +1515,8 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
       pn = p;
   }
   const bool tc = op->ctx->kernel == 1 && pw >= 0 && a.mcols[pw] <= 64 && (P == 1 || pn >= 0);
+  const bool comb = tc && combine && P == 2;  // one accumulated form
+  const int pk = comb ? d + 1 : per;          // per-block partial entries
   if (tc) {
     GradTcArgs t{};
     t.xs = op->xs32.p;
@@ -1533,14 +1538,17 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
     t.symmetric = a.symmetric;
     t.pw = pw;
     t.pn = pn >= 0 ? pn : 0;
-    t.npairs = P;
+    t.npairs = comb ? 1 : P;
+    t.combined = comb ? 1 : 0;
+    t.cw = comb ? static_cast<float>(combine[pw]) : 0.f;
+    t.cn = comb ? static_cast<float>(combine[pn]) : 0.f;
     t.blocks = op->ctx->sms;
     const long long ntiles = grad_tc_tiles(n, a.symmetric);
     t.tile_begin = ntiles * rk / nr;
     t.tile_end = ntiles * (rk + 1) / nr;
     a.blocks = t.blocks;
-    part.ensure(static_cast<size_t>(nr) * a.blocks * per);
-    t.part = part.p + static_cast<size_t>(rk) * a.blocks * per;
+    part.ensure(static_cast<size_t>(nr) * a.blocks * pk);
+    t.part = part.p + static_cast<size_t>(rk) * a.blocks * pk;
     grad_tc_launch(t, s);
   } else {
     a.blocks = 2 * op->ctx->sms;
@@ -1552,9 +1560,9 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
     a.part = part.p + static_cast<size_t>(rk) * a.blocks * per;
     grad_launch(a, s);
   }
-  tot.ensure(per);
-  gather_inplace(op, part.p, sizeof(double) * a.blocks * per);
-  sum_partials_launch(part.p, a.blocks * nr, per, tot.p, nullptr, s);
+  tot.ensure(pk);
+  gather_inplace(op, part.p, sizeof(double) * a.blocks * pk);
+  sum_partials_launch(part.p, a.blocks * nr, pk, tot.p, nullptr, s);
   // noise terms: sum u.w (FP64) over this rank's rows, gathered
   const int G = kReduceGroups;
   dots.ensure(static_cast<size_t>(nr) * G * P);
@@ -1564,22 +1572,33 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
     check_launch("pair_dot");
   }
   gather_inplace(op, dots.p, sizeof(double) * G * P);
-  std::vector<double> th(per), dh(static_cast<size_t>(nr) * G * P);
-  GPK_CUDA(cudaMemcpyAsync(th.data(), tot.p, sizeof(double) * per, cudaMemcpyDeviceToHost, s));
+  std::vector<double> th(pk), dh(static_cast<size_t>(nr) * G * P);
+  GPK_CUDA(cudaMemcpyAsync(th.data(), tot.p, sizeof(double) * pk, cudaMemcpyDeviceToHost, s));
   GPK_CUDA(cudaMemcpyAsync(dh.data(), dots.p, sizeof(double) * nr * G * P, cudaMemcpyDeviceToHost, s));
   GPK_CUDA(cudaStreamSynchronize(s));
-  std::vector<std::vector<double>> out(P, std::vector<double>(d + 2, 0.0));
-  for (int p = 0; p < P; ++p) {
-    double uw = 0.0;
+  std::vector<double> uw(P, 0.0);
+  for (int p = 0; p < P; ++p)
     for (int r = 0; r < nr; ++r)
-      for (int g = 0; g < G; ++g) uw += dh[static_cast<size_t>(r) * G * P + static_cast<size_t>(p) * G + g];
-    out[p][d + 1] = 2.0 * op->sigma * uw;                                     // kernel.cpp:249-252
+      for (int g = 0; g < G; ++g) uw[p] += dh[static_cast<size_t>(r) * G * P + static_cast<size_t>(p) * G + g];
+  const int nf = comb ? 1 : P;  // forms computed on the device
+  std::vector<std::vector<double>> out(nf, std::vector<double>(d + 2, 0.0));
+  for (int p = 0; p < nf; ++p) {
+    const double u = comb ? combine[0] * uw[0] + combine[1] * uw[1] : uw[p];
+    out[p][d + 1] = 2.0 * op->sigma * u;                                      // kernel.cpp:249-252
     out[p][d] = (2.0 / op->s) * (op->s2 * th[static_cast<size_t>(p) * (d + 1) + d]);  // kernel.cpp:264
     for (int k = 0; k < d; ++k)                                                // kernel.cpp:265-268
       out[p][k] = op->inv_ls[k] * (3.0 * op->s2 * th[static_cast<size_t>(p) * (d + 1) + k]);
   }
+  if (combine && !comb) {  // combined on the host from the per-pair forms
+    std::vector<double> c(d + 2, 0.0);
+    for (int p = 0; p < P; ++p)
+      for (int k = 0; k < d + 2; ++k) c[k] += combine[p] * out[p][k];
+    return {c};
+  }
   return out;
 }
+
+
 
 void assemble(const std::vector<std::vector<double>>& f, int s_count, int P, double* values, double* quad,
               double* trace) {  // gradients.cpp:39-50
@@ -2614,11 +2633,15 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
   } else {
     std::vector<double> g(P);
     std::vector<std::vector<double>> f;
+    // values = q/2 - t/(2s) (gradients.cpp:39-50), accumulated as one form
+    const double coef[2] = {0.5, -0.5 / s};
     if (pathwise)
-      f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1}, {b->solutions.p, b->solutions.p, m, m, 1, s}});
+      f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1}, {b->solutions.p, b->solutions.p, m, m, 1, s}},
+                         coef);
     else
-      f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1}, {b->solutions.p, b->targets.p, m, m, 1, s}});
-    assemble(f, s, P, g.data(), nullptr, nullptr);
+      f = quad_forms_dev(op, {{b->solutions.p, b->solutions.p, m, m, 0, 1}, {b->solutions.p, b->targets.p, m, m, 1, s}},
+                         coef);
+    for (int k = 0; k < P; ++k) g[k] = f[0][k];
     g_phase.mark("gradient");
     double inf = 0.0;
     for (int k = 0; k < P; ++k) {

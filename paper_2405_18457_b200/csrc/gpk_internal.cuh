@@ -157,6 +157,8 @@ struct GradTcArgs {
   int symmetric;
   int pw, pn;           // output slots of the wide / narrow pair
   int npairs;
+  int combined;         // accumulate cw G + cn u w^T as one form (npairs = 1)
+  float cw, cn;
   double* part;         // [blocks][npairs*(d+1)]
   int blocks;
   long long tile_begin, tile_end;  // 128 x 128 tiles of this rank

@@ -105,10 +105,12 @@ __device__ __forceinline__ void butterfly_flush(const float (&v)[NV], int lane, 
   }
 }
 
-template <int DP4, bool NARROW>
+// COMB (with NARROW): the estimator's combination cw G + cn u w^T is formed
+// per entry and accumulated once (one set of d + 1 sums instead of two).
+template <int DP4, bool NARROW, bool COMB>
 __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a) {
   constexpr int DP = 4 * DP4;
-  constexpr int NPR = NARROW ? 2 : 1;
+  constexpr int NPR = (NARROW && !COMB) ? 2 : 1;
   constexpr int NUSED = NPR * (DP + 1);
   constexpr int NV = NUSED <= 32 ? 32 : (NUSED <= 64 ? 64 : 128);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -219,12 +221,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
     uint64_t xi2[2 * DP4];
     float u1i = 0.f;
-    uint64_t lw[DP / 2], ln[NARROW ? DP / 2 : 1];
+    uint64_t lw[DP / 2], ln[(NARROW && !COMB) ? DP / 2 : 1];
     float sw = 0.f, sn = 0.f;
 #pragma unroll
     for (int k = 0; k < DP / 2; ++k) lw[k] = 0ull;
 #pragma unroll
-    for (int k = 0; k < (NARROW ? DP / 2 : 1); ++k) ln[k] = 0ull;
+    for (int k = 0; k < ((NARROW && !COMB) ? DP / 2 : 1); ++k) ln[k] = 0ull;
     int prev_ti = -1;
     for (int k = 0; k < nq; ++k) {
       const int s = k % STAGES, b = k & 1;
@@ -299,21 +301,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
           const float r = sqrt_approx(q0 + q1);
           const float e0 = ex2_approx(r * kNegSqrt3Log2e);  // exp(-sqrt3 r)
           const float kv = fmaf(r, kSqrt3f, 1.f) * e0;      // k / s^2
-          const float gw = __uint_as_float(g[e]);
+          const float gw = COMB ? fmaf(a.cn, u1i * wc[c], a.cw * __uint_as_float(g[e])) : __uint_as_float(g[e]);
           sw = fmaf(kv, gw, sw);
           uint64_t cw2;
           const float cw = e0 * gw;
           asm("mov.b64 %0, {%1, %1};" : "=l"(cw2) : "f"(cw));
 #pragma unroll
           for (int t = 0; t < DP / 2; ++t) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(lw[t]) : "l"(sq[t]), "l"(cw2));
-          if (NARROW) {
+          if constexpr (NARROW && !COMB) {
             const float gn = u1i * wc[c];
             sn = fmaf(kv, gn, sn);
             uint64_t cn2;
             const float cnv = e0 * gn;
             asm("mov.b64 %0, {%1, %1};" : "=l"(cn2) : "f"(cnv));
 #pragma unroll
-            for (int t = 0; t < (NARROW ? DP / 2 : 1); ++t)
+            for (int t = 0; t < DP / 2; ++t)
               asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(ln[t]) : "l"(sq[t]), "l"(cn2));
           }
         }
@@ -331,9 +333,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         }
         v[DP] = sw;
         sw = 0.f;
-        if (NARROW) {
+        if constexpr (NARROW && !COMB) {
 #pragma unroll
-          for (int t = 0; t < (NARROW ? DP / 2 : 1); ++t) {
+          for (int t = 0; t < DP / 2; ++t) {
             asm("mov.b64 {%0, %1}, %2;" : "=f"(v[DP + 1 + 2 * t]), "=f"(v[DP + 2 + 2 * t]) : "l"(ln[t]));
             ln[t] = 0ull;
           }
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
     const int slot = p * (DP + 1) + (k == d ? DP : k);
     double acc = 0.0;
     for (int w = 0; w < EVAL_WARPS; ++w) acc += wacc[w * NV + slot];
-    const int po = p == 0 ? a.pw : a.pn;
+    const int po = COMB ? 0 : (p == 0 ? a.pw : a.pn);
     a.part[static_cast<size_t>(blockIdx.x) * a.npairs * per_pair + po * per_pair + k] = acc;
   }
 }
@@ -390,10 +392,10 @@ __global__ void grad_tc_pack_kernel(const float* w32, int ld, int n, int cols, i
   }
 }
 
-template <int DP4, bool NARROW>
+template <int DP4, bool NARROW, bool COMB>
 void launch_one(const GradTcArgs& a, cudaStream_t s) {
   constexpr int DP = 4 * DP4;
-  constexpr int NPR = NARROW ? 2 : 1;
+  constexpr int NPR = (NARROW && !COMB) ? 2 : 1;
   constexpr int NUSED = NPR * (DP + 1);
   constexpr int NV = NUSED <= 32 ? 32 : (NUSED <= 64 ? 64 : 128);
   // >= 120 KB keeps one CTA per SM: each allocates all 512 TMEM columns
@@ -403,20 +405,22 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
       120 * 1024);
   static size_t configured = 0;
   if (smem > configured) {
-    GPK_CUDA(cudaFuncSetAttribute(grad_tc_kernel<DP4, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GPK_CUDA(cudaFuncSetAttribute(grad_tc_kernel<DP4, NARROW, COMB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = smem;
   }
-  grad_tc_kernel<DP4, NARROW><<<a.blocks, NTHREADS, smem, s>>>(a);
+  grad_tc_kernel<DP4, NARROW, COMB><<<a.blocks, NTHREADS, smem, s>>>(a);
   check_launch("grad_tc_kernel");
 }
 
 template <int DP4>
 void launch_dp(const GradTcArgs& a, cudaStream_t s) {
-  if (a.u1)
-    launch_one<DP4, true>(a, s);
+  if (a.u1 && a.combined)
+    launch_one<DP4, true, true>(a, s);
+  else if (a.u1)
+    launch_one<DP4, true, false>(a, s);
   else
-    launch_one<DP4, false>(a, s);
+    launch_one<DP4, false, false>(a, s);
 }
 
 }  // namespace

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-{ timeout 300 python -m pytest tests -q -m gpu 2>&1 | grep -E "^E  |FAILED|passed|failed" | cut -c1-200 | head; timeout 300 python tools/config_smoke.py C1 C3 --steps 3 | cut -c1-600; } > gpurun_out/quick.log 2>&1
+{ timeout 300 python -m pytest tests -q -m gpu 2>&1 | grep -E "^E  |FAILED|passed|failed" | cut -c1-200 | head; GPK_PHASE_TIMING=1 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | grep set_hyper | tail -1; timeout 300 python bench.py --no-cpu-baseline 2>&1 | cut -c1-200; timeout 300 python tools/config_smoke.py C1 C3 --steps 3 | cut -c1-400; } > gpurun_out/quick.log 2>&1
 cat gpurun_out/quick.log
