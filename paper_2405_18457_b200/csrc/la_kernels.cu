@@ -640,21 +640,16 @@ __global__ void __launch_bounds__(256) spd_leaf_inverse_kernel(const double* a, 
   bool bad = false;
   for (int k = 0; k < 64; ++k) {
     const int buf = k & 1;
+    const int kq = k & 3;  // register selects with static indices keep M out of local memory
     if (tx == (k >> 2)) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (q == (k & 3)) {
-#pragma unroll
-          for (int p = 0; p < 4; ++p) colb[buf][4 * ty + p] = M[p][q];
-        }
+      for (int p = 0; p < 4; ++p)
+        colb[buf][4 * ty + p] = kq == 0 ? M[p][0] : kq == 1 ? M[p][1] : kq == 2 ? M[p][2] : M[p][3];
     }
     if (ty == (k >> 2)) {
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
-        if (p == (k & 3)) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) rowb[buf][4 * tx + q] = M[p][q];
-        }
+      for (int q = 0; q < 4; ++q)
+        rowb[buf][4 * tx + q] = kq == 0 ? M[0][q] : kq == 1 ? M[1][q] : kq == 2 ? M[2][q] : M[3][q];
     }
     __syncthreads();
     const double pk = rowb[buf][k];
