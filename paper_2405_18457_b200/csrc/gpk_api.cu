@@ -95,6 +95,7 @@ struct gpk_ctx {
   int kernel = 1;  // operator kernel: 0 SIMT FP32, 1 tcgen05 3xTF32 (default)
   bool fused_ap = true;  // AP slabs: reduce + epilogue fused into the tcgen05 kernel
   int spd_inverse = 1;   // AP block inverses: 1 recursive Schur/DGEMM, 0 cuSOLVER potrf + 2 trsm
+  bool ap_persistent = true;  // AP iterations in one cooperative launch (GPK_AP_PERSISTENT=0 disables)
   int kv_deep = -1;
   bool graphs = true;  // CG/AP iteration groups as CUDA graphs (GPK_GRAPHS=0 disables)
   void* blas_ws = nullptr;  // operator launches one CTA per SM with 16 eval warps: -1 auto (>= 1e8 entries), 0/1 forced
@@ -166,6 +167,7 @@ struct gpk_batch {
   DBuf<unsigned> ticket;             // last-block ticket of fused reductions (kept at 0 between uses)
   DBuf<float> apk;                   // AP block update's TF32 operator images
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
+  DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
   // AP block inverses enqueued on the auxiliary stream (ap_prepare)
   bool ap_ready = false;
   int ap_block = 0;
@@ -1234,7 +1236,56 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     run_kv(op, kc);
     ap_check_launch(part, groups, m, b->scales_dev.p, c->tolerance, ctl, s);
   };
-  drive(b, ctl, 8, budget, iteration, true);
+  const bool persistent = fused && in_place && ctx->ap_persistent && ap_persistent_supported(n, m, block, ctx->sms);
+  if (persistent) {
+    // every iteration in one cooperative launch (ap_persistent.cu)
+    ApPersistArgs pa{};
+    pa.xs = op->xs32.p;
+    pa.n = n;
+    pa.d = op->d;
+    pa.dp = op->dp;
+    pa.m = m;
+    pa.npad = kv_tc_npad(m);
+    pa.log2_s2 = static_cast<float>(std::log2(op->s2));
+    pa.sigma2 = op->sigma2;
+    pa.block = block;
+    pa.nblocks = nblocks;
+    pa.gpb = gpb_t;
+    pa.budget = budget;
+    pa.R = b->residuals.p;
+    pa.V = b->solutions.p;
+    pa.inv = inv;
+    pa.bb = static_cast<long long>(bb);
+    pa.upd = upd64;
+    pa.vpk = vpk_blk;
+    pa.dpart = part;
+    pa.spart = spart_t;
+    pa.inv_scales = inv_scales_dev;
+    pa.scales = b->scales_dev.p;
+    pa.tol = c->tolerance;
+    pa.ctl = ctl;
+    pa.sel = sel;
+    pa.gbar = b->gbar.ensure(1);
+    pa.stats = ctx->stats;
+    GPK_CUDA(cudaMemsetAsync(pa.gbar, 0, sizeof(unsigned), s));
+    cudaEvent_t* prof_end = nullptr;
+    if (ctx->profiling) {  // timed as one operator launch (it also runs the block updates)
+      if (ctx->prof_used == ctx->prof.size()) {
+        cudaEvent_t e0, e1;
+        GPK_CUDA(cudaEventCreate(&e0));
+        GPK_CUDA(cudaEventCreate(&e1));
+        ctx->prof.push_back({e0, e1});
+      }
+      auto& pr = ctx->prof[ctx->prof_used++];
+      GPK_CUDA(cudaEventRecord(pr.first, s));
+      prof_end = &pr.second;
+    }
+    ap_persistent_launch(pa, s);
+    if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
+    GPK_CUDA(cudaStreamSynchronize(s));
+  } else {
+    drive(b, ctl, 8, budget, iteration, true);
+  }
   g_phase.mark("ap_iterations");
   spd_inverse_check(ctx, nblocks);
   const CgCtl h = read_ctl(b);
@@ -1786,6 +1837,7 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     if (const char* e = std::getenv("GPK_FUSED_AP")) c->fused_ap = std::atoi(e) != 0;  // A/B switches
     if (const char* e = std::getenv("GPK_SPD_INVERSE")) c->spd_inverse = std::atoi(e);
     if (const char* e = std::getenv("GPK_KV_DEEP")) c->kv_deep = std::atoi(e);
+    if (const char* e = std::getenv("GPK_AP_PERSISTENT")) c->ap_persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("GPK_GRAPHS")) c->graphs = std::atoi(e) != 0;
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     GPK_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));

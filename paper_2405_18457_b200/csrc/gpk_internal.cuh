@@ -143,6 +143,32 @@ struct GradArgs {
 };
 void grad_launch(const GradArgs& a, cudaStream_t s);
 
+// Persistent AP solver (ap_persistent.cu): one cooperative launch per solve.
+struct ApPersistArgs {
+  const float* xs;        // scaled inputs FP32 [n + 128][dp]
+  int n, d, dp, m, npad;
+  float log2_s2;
+  double sigma2;
+  int block, nblocks, gpb, budget;
+  double* R;              // residuals [n + pad][m] (read and updated)
+  double* V;              // solutions [n][m]
+  const double* inv;      // block inverses [nblocks][block][block]
+  long long bb;
+  double* upd;            // [block][m]
+  float* vpk;             // TF32 images of upd
+  double* dpart;          // [tiles][m]
+  double* spart;          // [nblocks * gpb]
+  const double* inv_scales;
+  const double* scales;
+  double tol;
+  CgCtl* ctl;
+  int* sel;
+  unsigned* gbar;         // grid-barrier arrival counter (zeroed before the launch)
+  double* stats;          // evals x RHS, FP32-equivalent flops, FP32-pipe flops
+};
+bool ap_persistent_supported(int n, int m, int block, int sms);
+void ap_persistent_launch(const ApPersistArgs& a, cudaStream_t s);
+
 // Tensor-core gradient pass (grad_tc_kernel.cu): one wide pair (G on tcgen05)
 // plus optionally one narrow (single-column) pair.
 struct GradTcArgs {
