@@ -158,26 +158,43 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     {
       const int c_beg = tile * rpc, c_end = min(block, c_beg + rpc);
       const double* Hk = a.inv + static_cast<size_t>(sel) * a.bb;
-      const int nout = (c_end > c_beg ? c_end - c_beg : 0) * m;
-      const int kh = (block + 1) / 2;
-      for (int w = tid; w < 2 * nout; w += THREADS) {
-        const int half = w / nout, o = w % nout;
-        const int c = c_beg + o / m, j = o % m;
-        const int kb = half * kh, ke = min(block, kb + kh);
-        const double* h = Hk + static_cast<size_t>(c) * block;  // row c == column c (symmetric)
+      const int nrow = c_end > c_beg ? c_end - c_beg : 0;
+      // work item = (K split ks, column j): 4 rows share every residual load;
+      // partials in the idle pipeline buffers, added in K-split order
+      constexpr int KS = 8;
+      double* gp = reinterpret_cast<double*>(smB);  // [KS][4][m]
+      const int kq = (block + KS - 1) / KS;
+      for (int w = tid; w < KS * m; w += THREADS) {
+        const int ks = w / m, j = w % m;
+        const int kb = ks * kq, ke = min(block, kb + kq);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
         const double* rr = a.R + static_cast<size_t>(r0) * m + j;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int k = kb; k < ke; ++k) acc = fma(h[k], rr[static_cast<size_t>(k) * m], acc);
-        gemm[half * 4 * 96 + o] = acc;
+        const double* h0 = Hk + static_cast<size_t>(min(c_beg + 0, block - 1)) * block;  // row c == column c
+        const double* h1 = Hk + static_cast<size_t>(min(c_beg + 1, block - 1)) * block;
+        const double* h2 = Hk + static_cast<size_t>(min(c_beg + 2, block - 1)) * block;
+        const double* h3 = Hk + static_cast<size_t>(min(c_beg + 3, block - 1)) * block;
+#pragma unroll 8
+        for (int k = kb; k < ke; ++k) {
+          const double rv = rr[static_cast<size_t>(k) * m];
+          acc[0] = fma(h0[k], rv, acc[0]);
+          acc[1] = fma(h1[k], rv, acc[1]);
+          acc[2] = fma(h2[k], rv, acc[2]);
+          acc[3] = fma(h3[k], rv, acc[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gp[(ks * 4 + q) * m + j] = acc[q];
       }
       __syncthreads();
+      (void)nrow;
       for (int e = tid; e < (c_end - c_beg) * a.npad; e += THREADS) {
         const int q = e / a.npad, j = e % a.npad;
         const int c = c_beg + q;
         double u = 0.0;
         if (j < m) {
-          u = c < len ? gemm[q * m + j] + gemm[4 * 96 + q * m + j] : 0.0;
+          if (c < len) {
+            u = gp[q * m + j];
+            for (int ks = 1; ks < KS; ++ks) u += gp[(ks * 4 + q) * m + j];
+          }
           a.upd[static_cast<size_t>(c) * m + j] = u;
           if (c < len) a.V[static_cast<size_t>(r0 + c) * m + j] += u;
         }
