@@ -44,11 +44,13 @@ __device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, %0;" ::"n
 
 // Grid barrier for a cooperative launch: a monotonic arrival counter (zeroed
 // by the host before the launch); barrier g completes at nctas * g arrivals.
+// The CTA barrier orders the CTA's writes before thread 0's release fence
+// (cumulative), and thread 0's acquire load before everyone's later reads.
 __device__ __forceinline__ void grid_sync(unsigned* count, unsigned nctas, unsigned& gen) {
-  __threadfence();
   __syncthreads();
   ++gen;
   if (threadIdx.x == 0) {
+    __threadfence();
     atomicAdd(count, 1u);
     const unsigned target = nctas * gen;
     while (true) {
@@ -59,7 +61,6 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned nctas, unsig
     }
   }
   __syncthreads();
-  __threadfence();
 }
 
 template <int NPAD, int DP4>
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
       const int nrow = c_end > c_beg ? c_end - c_beg : 0;
       // work item = (K split ks, column j): 4 rows share every residual load;
       // partials in the idle pipeline buffers, added in K-split order
-      constexpr int KS = 8;
+      constexpr int KS = 16;
       double* gp = reinterpret_cast<double*>(smB);  // [KS][4][m]
       const int kq = (block + KS - 1) / KS;
       for (int w = tid; w < KS * m; w += THREADS) {
@@ -364,9 +365,16 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     // ---------------- B: termination test and next block (every CTA alike) ----------------
     if (warp < EW) {
       const int G = static_cast<int>(nctas);
-      for (int j = warp; j < m; j += EW) {
+      for (int j = warp; j < m; j += EW) {  // G <= 148: at most 5 loads per lane, issued together
+        double v[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          const int q = lane + 32 * i;
+          v[i] = q < G ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
+        }
         double acc = 0.0;
-        for (int q = lane; q < G; q += 32) acc += __ldcg(a.dpart + static_cast<size_t>(q) * m + j);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) acc += v[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) ss[j] = acc;
