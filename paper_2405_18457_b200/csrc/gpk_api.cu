@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -118,6 +119,7 @@ struct gpk_operator {
   int nr = 1, rk = 0, row0 = 0, nloc = 0, S = 0;
   bool sharded = false;  // built by the optimiser on a context with a communicator
   uint64_t hyper_version = 0;  // bumped by every set_hyper (AP block inverses are keyed on it)
+  DBuf<double> hyp_dev;        // {s2, sigma2} on the device (graph-replayable AP block build)
   // gradient-pass workspace (persistent across steps)
   DBuf<float> gbuf[4];
   DBuf<double> gpart, gtot, gdots;
@@ -168,6 +170,14 @@ struct gpk_batch {
   DBuf<float> apk;                   // AP block update's TF32 operator images
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
   DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
+  // CUDA graph of the AP block build + inverse (ap_prepare), keyed on its buffers
+  cudaGraphExec_t ap_graph = nullptr;
+  std::array<const void*, 6> ap_graph_key{};
+  std::pair<int, int> ap_graph_dims{0, 0};
+  long long ap_graph_launches = 0;
+  ~gpk_batch() {
+    if (ap_graph) cudaGraphExecDestroy(ap_graph);
+  }
   // AP block inverses enqueued on the auxiliary stream (ap_prepare)
   bool ap_ready = false;
   int ap_block = 0;
@@ -299,6 +309,8 @@ void set_hyper(gpk_operator* op, const double* raw) {
   cudaStream_t s = op->ctx->stream;
   double* il = op->inv_ls_dev.ensure(d);
   GPK_CUDA(cudaMemcpyAsync(il, op->inv_ls.data(), sizeof(double) * d, cudaMemcpyHostToDevice, s));
+  const double hv[2] = {op->s2, op->sigma2};
+  GPK_CUDA(cudaMemcpyAsync(op->hyp_dev.ensure(2), hv, sizeof(hv), cudaMemcpyHostToDevice, s));
   prescale_launch(op->x64.p, op->n, d, op->dp, il, op->xs32.p, op->xs64.p, s);
   GPK_CUDA(cudaStreamSynchronize(s));  // inv_ls host buffer lifetime
 }
@@ -1041,12 +1053,51 @@ void ap_prepare(gpk_batch* b, int block) {
   double* inv = b->blocks.ensure(bb * nblocks);
   GPK_CUDA(cudaEventRecord(ctx->ev_m2a, ctx->stream));
   GPK_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_m2a, 0));
-  ap_blocks_launch(op->xs64.p, n, op->d, op->s2, op->sigma2, block, nblocks, mats, ctx->aux);
-  if (ctx->spd_inverse == 1) {
-    const size_t xs = static_cast<size_t>(std::max<long long>(1, spd_inverse_scratch(block)));
-    spd_inverse_recursive(ctx, ctx->aux, mats, block, nblocks, inv, b->w5.ensure(xs * nblocks));
+  const size_t xs = static_cast<size_t>(std::max<long long>(1, spd_inverse_scratch(block)));
+  double* scratch = ctx->spd_inverse == 1 ? b->w5.ensure(xs * nblocks) : nullptr;
+  double* hyp = op->hyp_dev.p;
+  auto enqueue = [&](cudaStream_t st) {
+    ap_blocks_launch(op->xs64.p, n, op->d, hyp, block, nblocks, mats, st);
+    if (ctx->spd_inverse == 1)
+      spd_inverse_recursive(ctx, st, mats, block, nblocks, inv, scratch);
+    else
+      spd_inverse_batched(ctx, st, mats, block, nblocks, inv);
+  };
+  // the ~45 launches of the recursive inverse are captured once (fixed
+  // buffers, hyperparameters read from the device) and replayed every step
+  int* info = ctx->info.ensure(nblocks);  // allocated before the key: the graph captures its address
+  if (!ctx->info_host) GPK_CUDA(cudaMallocHost(&ctx->info_host, sizeof(int) * 4096));
+  const std::array<const void*, 6> key{op->xs64.p, mats, inv, scratch, hyp, info};
+  const bool graphable = ctx->graphs && ctx->spd_inverse == 1;
+  if (graphable && !(b->ap_graph && b->ap_graph_key == key && b->ap_graph_dims == std::make_pair(block, nblocks))) {
+    if (b->ap_graph) {
+      cudaGraphExecDestroy(b->ap_graph);
+      b->ap_graph = nullptr;
+    }
+    const long long before = g_launch_counter ? *g_launch_counter : 0;
+    cudaGraph_t g = nullptr;
+    GPK_CUDA(cudaStreamBeginCapture(ctx->aux, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue(ctx->aux);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->aux, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    GPK_CUDA(cudaStreamEndCapture(ctx->aux, &g));
+    const cudaError_t e = cudaGraphInstantiate(&b->ap_graph, g, 0);
+    cudaGraphDestroy(g);
+    GPK_CUDA(e);
+    b->ap_graph_key = key;
+    b->ap_graph_dims = {block, nblocks};
+    b->ap_graph_launches = (g_launch_counter ? *g_launch_counter : 0) - before;
+    if (g_launch_counter) *g_launch_counter = before;  // counted on replay
+  }
+  if (graphable) {
+    GPK_CUDA(cudaGraphLaunch(b->ap_graph, ctx->aux));
+    count_launch(static_cast<int>(b->ap_graph_launches));
   } else {
-    spd_inverse_batched(ctx, ctx->aux, mats, block, nblocks, inv);
+    enqueue(ctx->aux);
   }
   GPK_CUDA(cudaEventRecord(ctx->ev_aux, ctx->aux));
   b->ap_ready = true;

@@ -256,8 +256,8 @@ void dense_block64_launch(const double* xs64, int n, int d, double s2, double si
                           int rows, int c0, int cols, double* out, int ldo, int add_noise,
                           cudaStream_t s);  // out row-major [rows][ldo]
 
-void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks, double* mats,
-                      cudaStream_t s);
+void ap_blocks_launch(const double* xs64, int n, int d, const double* hyp, int block, int nblocks, double* mats,
+                      cudaStream_t s);  // hyp: device {s2, sigma2}
 void spd_leaf_inverse_launch(const double* a, double* out, int off, int nn, int ld, long long stride, int batch,
                              int* info, cudaStream_t s);
 void block_transpose_launch(const double* src, double* dst, int rows, int cols, int ld, long long stride, int batch,

@@ -575,8 +575,9 @@ void dense_block64_launch(const double* xs64, int n, int d, double s2, double si
 // tile of one block (grid.z = block index): its 32 row and 32 column points are
 // staged in shared memory, each thread forms 4 entries (same arithmetic as
 // matern64, kernel.cpp:35-39).
-__global__ void ap_blocks_kernel(const double* xs64, int n, int d, double s2, double sigma2, int block, double* mats) {
+__global__ void ap_blocks_kernel(const double* xs64, int n, int d, const double* hyp, int block, double* mats) {
   __shared__ double xr[32][33], xc[32][33];
+  const double s2 = hyp[0], sigma2 = hyp[1];  // device copy: the launch is graph-replayable
   const int k = blockIdx.z, r0 = k * block, len = min(block, n - r0);
   const int tr = blockIdx.y * 32, tcl = blockIdx.x * 32;
   for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
@@ -606,11 +607,11 @@ __global__ void ap_blocks_kernel(const double* xs64, int n, int d, double s2, do
     out[static_cast<size_t>(r) * block + cc] = v;
   }
 }
-void ap_blocks_launch(const double* xs64, int n, int d, double s2, double sigma2, int block, int nblocks, double* mats,
+void ap_blocks_launch(const double* xs64, int n, int d, const double* hyp, int block, int nblocks, double* mats,
                       cudaStream_t s) {
   if (d > 32) throw std::invalid_argument("gpk: input dimension > 32 is not supported");
   dim3 grid((block + 31) / 32, (block + 31) / 32, nblocks);
-  ap_blocks_kernel<<<grid, 256, 0, s>>>(xs64, n, d, s2, sigma2, block, mats);
+  ap_blocks_kernel<<<grid, 256, 0, s>>>(xs64, n, d, hyp, block, mats);
   check_launch("ap_blocks");
 }
 
