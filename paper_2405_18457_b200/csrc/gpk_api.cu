@@ -158,6 +158,7 @@ struct gpk_batch {
   int n = 0, m = 0;
   DBuf<double> targets, solutions, residuals;
   std::vector<double> scales;
+  bool scales_stale = false;  // scales_dev newer than the host copy (device-computed in the optimiser)
   DBuf<double> scales_dev;
   // solver workspace
   DBuf<double> w1, w2, w3, w4, w5, red, vec1, vec2, vec3;
@@ -1125,10 +1126,8 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   if (!(b->ap_ready && b->ap_block == block && b->ap_version == op->hyper_version)) ap_prepare(b, block);
   b->ap_ready = false;  // consumed by this solve
   double* inv = b->blocks.p;
-  std::vector<double> inv_scales(m);
-  for (int j = 0; j < m; ++j) inv_scales[j] = 1.0 / b->scales[j];
   double* inv_scales_dev = b->vec1.ensure(m);
-  GPK_CUDA(cudaMemcpyAsync(inv_scales_dev, inv_scales.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
+  inv_scales_launch(b->scales_dev.p, m, inv_scales_dev, s);
   // reduction groups per AP block: one resident wave (3 x 148 blocks of 8 row-warps) keeps enough
   // row loads in flight for the latency-bound fused reduce
   const int gpb = std::max(1, std::min(block / 8, 3 * ctx->sms / nblocks));
@@ -2338,6 +2337,10 @@ gpk_status gpk_batch_get(gpk_batch* b, int which, double* out) {
   return guarded([&] {
     LaunchScope ls(b->op->ctx);
     if (which == 3) {
+      if (b->scales_stale) {
+        GPK_CUDA(cudaMemcpy(b->scales.data(), b->scales_dev.p, sizeof(double) * b->m, cudaMemcpyDeviceToHost));
+        b->scales_stale = false;
+      }
       std::memcpy(out, b->scales.data(), sizeof(double) * b->m);
       return;
     }
@@ -2698,11 +2701,8 @@ bool optimiser_one_step(gpk_optimiser* o, double* row) {
                       stream);
     gather_inplace(op, part, sizeof(double) * G * m);
     sum_partials_launch(part, G * nr, m, ss, nullptr, stream);
-    std::vector<double> h(m);
-    GPK_CUDA(cudaMemcpyAsync(h.data(), ss, sizeof(double) * m, cudaMemcpyDeviceToHost, stream));
-    GPK_CUDA(cudaStreamSynchronize(stream));
-    for (int j = 0; j < m; ++j) b->scales[j] = std::sqrt(h[j]) + 1e-12;
-    GPK_CUDA(cudaMemcpyAsync(b->scales_dev.p, b->scales.data(), sizeof(double) * m, cudaMemcpyHostToDevice, stream));
+    scales_launch(ss, m, b->scales_dev.p, nullptr, stream);  // no host round trip
+    b->scales_stale = true;                                   // host copy refreshed on demand
   }
   if (cfg.warm_start && o->have_previous)
     GPK_CUDA(cudaMemcpyAsync(b->solutions.p, o->prev.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, stream));

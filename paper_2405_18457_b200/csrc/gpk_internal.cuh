@@ -265,6 +265,8 @@ void block_transpose_launch(const double* src, double* dst, int rows, int cols, 
 void exact_forms_launch(const double* xs64, int n, int d, const double* hinv, const double* alpha, double* part,
                         cudaStream_t s);
 long long exact_forms_blocks(int n);
+void scales_launch(const double* ss, int m, double* scales, double* inv, cudaStream_t s);
+void inv_scales_launch(const double* scales, int m, double* inv, cudaStream_t s);
 void set_identity_launch(double* mats, int dim, int batch, cudaStream_t s);
 
 // AP (K8)

@@ -496,6 +496,27 @@ __global__ void sum_partials_kernel(const double* part, int groups, int count, d
     if ((threadIdx.x & 31) == 0) out[e] = v;
   }
 }
+// scales_j = sqrt(ss_j) + 1e-12 (linear_system.cpp:21), inv_j = 1 / scales_j
+// (IEEE sqrt and division: the host formulas' results).
+__global__ void scales_kernel(const double* ss, int m, double* scales, double* inv) {
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const double sc = sqrt(ss[j]) + 1e-12;
+    if (scales) scales[j] = sc;
+    if (inv) inv[j] = 1.0 / sc;
+  }
+}
+void scales_launch(const double* ss, int m, double* scales, double* inv, cudaStream_t s) {
+  scales_kernel<<<1, 128, 0, s>>>(ss, m, scales, inv);
+  check_launch("scales");
+}
+__global__ void inv_scales_kernel(const double* scales, int m, double* inv) {
+  for (int j = threadIdx.x; j < m; j += blockDim.x) inv[j] = 1.0 / scales[j];
+}
+void inv_scales_launch(const double* scales, int m, double* inv, cudaStream_t s) {
+  inv_scales_kernel<<<1, 128, 0, s>>>(scales, m, inv);
+  check_launch("inv_scales");
+}
+
 void sum_partials_launch(const double* part, int groups, int count, double* out, const int* skip, cudaStream_t s) {
   sum_partials_kernel<<<blocks_for(static_cast<long long>(count) * 32, 256, 1024), 256, 0, s>>>(part, groups, count,
                                                                                                out, skip);
