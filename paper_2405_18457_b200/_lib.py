@@ -10,6 +10,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgpk.so")
+# development A/B: GPK_LIB_PATH points at another in-tree build of the same C-ABI
+LIB_PATH = os.environ.get("GPK_LIB_PATH", LIB_PATH)
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "gpk.h")
 
 GPK_OK, GPK_EINVAL, GPK_ERANGE, GPK_ENUMERIC, GPK_ECUDA, GPK_ENCCL = range(6)

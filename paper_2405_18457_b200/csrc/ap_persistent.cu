@@ -38,6 +38,9 @@ struct ApLayout {
   static constexpr int IMG_FLOATS = NPAD * TBK;
   static constexpr int CHUNK_FLOATS = 2 * IMG_FLOATS;
   static constexpr uint32_t CHUNK_BYTES = CHUNK_FLOATS * 4;
+  // the pipeline ring doubles as phase C1's staging: Hk [32][<=64] + R [<=64][<=NPAD] FP64
+  static constexpr int C1_FLOATS = (32 * 64 + 64 * NPAD) * 2;
+  static constexpr int RING_FLOATS = STAGES * CHUNK_FLOATS > C1_FLOATS ? STAGES * CHUNK_FLOATS : C1_FLOATS;
 };
 
 __device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory"); }
@@ -66,12 +69,13 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned nctas, unsig
 template <int NPAD, int DP4>
 __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersistArgs a) {
   constexpr int DP = 4 * DP4;
+  constexpr bool GRAM = GPK_GRAM && DP4 >= 6;  // (x, |x|^2, 0...) image for d >= 21, as kv_tc_kernel
   constexpr int NQ = EW / 4;       // warps per TMEM lane group
   constexpr int DC = NPAD / NQ;    // drained D columns per thread
   using L = ApLayout<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* smB = reinterpret_cast<float*>(smem_raw);
-  float* smX = smB + STAGES * L::CHUNK_FLOATS;
+  float* smX = smB + L::RING_FLOATS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * TBK * DP);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
@@ -137,64 +141,102 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   const bool row_ok = er < n;
   const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
   uint64_t xi2[2 * DP4];
+  float ni = 0.f;  // Gram form (d >= 21): |x_i|^2 seeds the distance accumulator
   if (warp < EW) {
     const float* xrow = a.xs + static_cast<size_t>(row_ok ? er : 0) * DP;
 #pragma unroll
     for (int u = 0; u < DP4; ++u) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+      float4 v = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+      if constexpr (GRAM) gram_row(v, 4 * u, a.d, ni);
       asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(v.x), "f"(v.y));
       asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(v.z), "f"(v.w));
     }
   }
+  uint64_t acc_seed;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
   int kg = 0;  // chunk counter across iterations (pipeline phases)
   int it = 0;
   int iters = sh[2];
   const int block = a.block, img = a.npad * 32;
   const int rpc = (block + static_cast<int>(nctas) - 1) / static_cast<int>(nctas);  // update rows per CTA
 
+  const bool prof = a.prof && tile == 0 && tid == 0;
+  unsigned long long pt[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tprev = 0;
+  auto mark = [&](int i) {
+    if (prof) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (i >= 0) pt[i] += t - tprev;
+      tprev = t;
+    }
+  };
+  mark(-1);
   while (!sh[1]) {
     const int sel = sh[0];
     const int r0 = sel * block, len = min(block, n - r0);
     // ---------------- C: block update (upd = Hinv_sel R_blk, V += upd, images) ----------------
     {
-      const int c_beg = tile * rpc, c_end = min(block, c_beg + rpc);
-      const double* Hk = a.inv + static_cast<size_t>(sel) * a.bb;
-      const int nrow = c_end > c_beg ? c_end - c_beg : 0;
-      // work item = (K split ks, column j): 4 rows share every residual load;
-      // partials in the idle pipeline buffers, added in K-split order
-      constexpr int KS = 16;
-      double* gp = reinterpret_cast<double*>(smB);  // [KS][4][m]
-      const int kq = (block + KS - 1) / KS;
-      for (int w = tid; w < KS * m; w += THREADS) {
-        const int ks = w / m, j = w % m;
-        const int kb = ks * kq, ke = min(block, kb + kq);
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const double* rr = a.R + static_cast<size_t>(r0) * m + j;
-        const double* h0 = Hk + static_cast<size_t>(min(c_beg + 0, block - 1)) * block;  // row c == column c
-        const double* h1 = Hk + static_cast<size_t>(min(c_beg + 1, block - 1)) * block;
-        const double* h2 = Hk + static_cast<size_t>(min(c_beg + 2, block - 1)) * block;
-        const double* h3 = Hk + static_cast<size_t>(min(c_beg + 3, block - 1)) * block;
-#pragma unroll 8
-        for (int k = kb; k < ke; ++k) {
-          const double rv = rr[static_cast<size_t>(k) * m];
-          acc[0] = fma(h0[k], rv, acc[0]);
-          acc[1] = fma(h1[k], rv, acc[1]);
-          acc[2] = fma(h2[k], rv, acc[2]);
-          acc[3] = fma(h3[k], rv, acc[3]);
+      const double* Hk = a.inv + static_cast<size_t>(sel) * a.bb;  // symmetric: row c == column c
+      // C1: 2-D split of upd = Hk R_blk over (32-row group rg, K eighth kg):
+      // the CTA stages Hk[rg rows][kg cols] and R_blk[kg rows] in the idle
+      // pipeline buffers (one round of coalesced loads) and writes its FP64
+      // partial to cpart[kg]
+      const int kq = block / 8, rgs = block / 32;
+      if (tile < rgs * 8) {
+        const int rg = tile >> 3, kgi = tile & 7, kb = kgi * kq;
+        // Hk is symmetric: sHt[k][r] = Hk[kb + k][rg*32 + r] reads whole rows.
+        // FP32 operands and accumulation: upd only sets how far this iteration
+        // projects (V += upd and R -= H upd use the same upd, so the pair stays
+        // consistent); its ~1e-6 relative error is far below the solver
+        // tolerance, and the FP64 pipe of this part is too slow for 17 MFMA per
+        // iteration (measured 6 us vs < 1 us here)
+        float* sHt = reinterpret_cast<float*>(smB);  // [kq][32]
+        float* sR = sHt + 32 * kq;                   // [kq][m]
+        for (int e = tid; e < 32 * kq; e += THREADS) {
+          const int k = e >> 5, r = e & 31, row = rg * 32 + r, kk = kb + k;
+          sHt[e] = (row < len && kk < len) ? static_cast<float>(Hk[static_cast<size_t>(kk) * block + row]) : 0.f;
         }
+        const int kv = max(0, min(kq, len - kb));
+        const double* rsrc = a.R + static_cast<size_t>(r0 + kb) * m;
+        for (int e = tid; e < kq * m; e += THREADS) sR[e] = e < kv * m ? static_cast<float>(rsrc[e]) : 0.f;
+        __syncthreads();
+        mark(6);
+        // thread (row quad rq, column j): 4 rows share every R load (4 chains)
+        for (int w = tid; w < 8 * m; w += THREADS) {
+          const int rq = w / m, j = w % m;
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+          for (int k = 0; k < kq; ++k) {
+            const float rv = sR[k * m + j];
+            const float4 h = *reinterpret_cast<const float4*>(sHt + k * 32 + 4 * rq);
+            acc[0] = fmaf(h.x, rv, acc[0]);
+            acc[1] = fmaf(h.y, rv, acc[1]);
+            acc[2] = fmaf(h.z, rv, acc[2]);
+            acc[3] = fmaf(h.w, rv, acc[3]);
+          }
+          double* dst = a.cpart + (static_cast<size_t>(kgi) * block + rg * 32 + 4 * rq) * m + j;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) gp[(ks * 4 + q) * m + j] = acc[q];
+          for (int q = 0; q < 4; ++q) dst[static_cast<size_t>(q) * m] = static_cast<double>(acc[q]);
+        }
       }
-      __syncthreads();
-      (void)nrow;
+      mark(7);
+      grid_sync(a.gbar, nctas, gen);
+      mark(8);
+      // C2: this CTA's rows of upd = the eight partials in order; V += upd and
+      // the TF32 hi/lo images of upd for the slab's MMAs
+      const int c_beg = tile * rpc, c_end = min(block, c_beg + rpc);
       for (int e = tid; e < (c_end - c_beg) * a.npad; e += THREADS) {
         const int q = e / a.npad, j = e % a.npad;
         const int c = c_beg + q;
         double u = 0.0;
         if (j < m) {
           if (c < len) {
-            u = gp[q * m + j];
-            for (int ks = 1; ks < KS; ++ks) u += gp[(ks * 4 + q) * m + j];
+            double pv[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) pv[g] = __ldcg(a.cpart + (static_cast<size_t>(g) * block + c) * m + j);
+            u = pv[0];
+#pragma unroll
+            for (int g = 1; g < 8; ++g) u += pv[g];
           }
           a.upd[static_cast<size_t>(c) * m + j] = u;
           if (c < len) a.V[static_cast<size_t>(r0 + c) * m + j] += u;
@@ -210,7 +252,10 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         base[img + off] = __uint_as_float(lb);
       }
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // C1 staging writes -> the slab's TMA
+    mark(0);
     grid_sync(a.gbar, nctas, gen);
+    mark(1);
     // ---------------- S: slab R[tile] -= H[tile, blk] upd ----------------
     const int nq = (len + TBK - 1) / TBK;
     const int c0 = r0;
@@ -262,6 +307,10 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         uint32_t hi[CPT], lo[CPT];
 #pragma unroll
         for (int t = 0; t < CPT; ++t) {
+          float r;
+          if constexpr (GRAM) {
+            r = sqrt_approx(gram_r2<DP4>(xbase + t * DP * 4, xi2, acc_seed));
+          } else {
           uint64_t acc0 = 0ull, acc1 = 0ull;
 #pragma unroll
           for (int u = 0; u < DP4; ++u) {
@@ -276,10 +325,16 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
           asm("add.rn.f32x2 %0, %1, %2;" : "=l"(accs) : "l"(acc0), "l"(acc1));
           float s0, s1;
           asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(accs));
-          const float r = sqrt_approx(s0 + s1);
+          r = sqrt_approx(s0 + s1);
+          }
           const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
           hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
           lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
+        }
+        if constexpr (GRAM) {  // pin k(x_i, x_i) (see kv_tc_kernel.cu)
+          const int cbase = c0 + q * TBK + qtr * CPT;
+          const bool hit = row_ok && static_cast<unsigned>(er - cbase) < static_cast<unsigned>(CPT);
+          if (__any_sync(0xffffffffu, hit)) gram_pin_diagonal<CPT>(hit, er - cbase, a.log2_s2, hi, lo);
         }
         const uint32_t abase = tmem + lane_addr + A_BASE + b * 64 + qtr * CPT;
         tc_st8(abase, hi);
@@ -361,49 +416,79 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     }
     kg += nq;
     ++it;
+    mark(2);
     grid_sync(a.gbar, nctas, gen);
+    mark(3);
     // ---------------- B: termination test and next block (every CTA alike) ----------------
-    if (warp < EW) {
+    // One round of loads: thread (j, p) = (tid / 8, tid % 8) sums column j of
+    // the tile partials over tiles p, p + 8, ... (all loads issued together),
+    // then a fixed xor-4/2/1 tree; thread k < nblocks sums block k's score
+    // partials in order. The order is identical in every CTA.
+    {
       const int G = static_cast<int>(nctas);
-      for (int j = warp; j < m; j += EW) {  // G <= 148: at most 5 loads per lane, issued together
-        double v[5];
+      constexpr int QH = 10;  // 2 x 10 x 8 >= 148 tiles (ap_persistent_supported)
+      const int j = tid >> 3, p = tid & 7;
+      double v[QH];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) {
-          const int q = lane + 32 * i;
-          v[i] = q < G ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
+      for (int i = 0; i < QH; ++i) {
+        const int q = p + 8 * i;
+        v[i] = (j < m && q < G) ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
+      }
+      double sp[4] = {0.0, 0.0, 0.0, 0.0};  // gpb <= 4 (ap_persistent_supported)
+      if (tid < a.nblocks) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < a.gpb) sp[q] = __ldcg(a.spart + static_cast<size_t>(tid) * a.gpb + q);
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < QH; ++i) acc += v[i];
+      if (G > 8 * QH) {
+#pragma unroll
+        for (int i = 0; i < QH; ++i) {
+          const int q = p + 8 * (QH + i);
+          v[i] = (j < m && q < G) ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
         }
-        double acc = 0.0;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) acc += v[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) ss[j] = acc;
+        for (int i = 0; i < QH; ++i) acc += v[i];
       }
-      for (int k = warp; k < a.nblocks; k += EW) {
-        double t = 0.0;
-        for (int q = lane; q < a.gpb; q += 32) t += __ldcg(a.spart + static_cast<size_t>(k) * a.gpb + q);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (p == 0 && j < m) ss[j] = sqrt(acc) / a.scales[j];
+      if (tid < a.nblocks) bscore[tid] = sqrt(((sp[0] + sp[1]) + sp[2]) + sp[3]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // probe mean over columns 1..m-1 and the first maximal block score
+      // (the serial strict '>' scan from -1 of ap_select)
+      double sum = 0.0;
+      for (int jj = 1 + lane; jj < m; jj += 32) sum += ss[jj];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0) bscore[k] = sqrt(t);
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      double best = -1.0;
+      int best_k = 0x7fffffff;
+      for (int k = lane; k < a.nblocks; k += 32)
+        if (bscore[k] > best) {
+          best = bscore[k];
+          best_k = k;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
+        if (ob > best || (ob == best && ok < best_k)) {
+          best = ob;
+          best_k = ok;
+        }
       }
-      eval_bar();
-      for (int j = tid; j < m; j += 32 * EW) ss[j] = sqrt(ss[j]) / a.scales[j];
-      eval_bar();
-      if (tid == 0) {
+      if (best_k == 0x7fffffff) best_k = 0;
+      if (lane == 0) {
         iters += 1;
         const double mean = ss[0];
-        double sum = 0.0;
-        for (int j = 1; j < m; ++j) sum += ss[j];
         const double probe = m > 1 ? sum / (m - 1) : 0.0;
         const int done = (mean <= a.tol && probe <= a.tol) ? 1 : 0;
         const int stop = (done || iters >= a.budget) ? 1 : 0;
-        int best_k = 0;
-        double best = -1.0;
-        for (int k = 0; k < a.nblocks; ++k)
-          if (bscore[k] > best) {
-            best = bscore[k];
-            best_k = k;
-          }
         sh[0] = best_k;
         sh[1] = stop;
         if (blockIdx.x == 0) {
@@ -417,7 +502,11 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
       }
     }
     __syncthreads();
+    mark(4);
+    if (prof) ++pt[9];
   }
+  if (prof)
+    for (int i = 0; i < 10; ++i) a.prof[i] += pt[i];
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -429,7 +518,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
 template <int NPAD, int DP4>
 void launch_one(const ApPersistArgs& a, cudaStream_t s) {
   using L = ApLayout<NPAD>;
-  const size_t smem = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 32 * sizeof(uint64_t) +
+  const size_t smem = sizeof(float) * (L::RING_FLOATS + STAGES * TBK * 4 * DP4) + 32 * sizeof(uint64_t) +
                       sizeof(double) * (4 * NPAD + 4 * 128 + 8 + 96 + 1024 + 2 * 4 * 96) + 8 * sizeof(int) +
                       sizeof(double) * TBM * a.m + 64;
   if (smem > 227 * 1024) throw std::invalid_argument("gpk: persistent AP kernel shared memory exceeds 227 KB");
@@ -457,6 +546,7 @@ void launch_n(const ApPersistArgs& a, cudaStream_t s) {
     case 6: return launch_one<NPAD, 6>(a, s);
     case 7: return launch_one<NPAD, 7>(a, s);
     case 8: return launch_one<NPAD, 8>(a, s);
+    case 9: return launch_one<NPAD, 9>(a, s);  // d = 32 Gram image
     default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
   }
 }

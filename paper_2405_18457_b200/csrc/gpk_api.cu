@@ -127,6 +127,8 @@ struct gpk_operator {
   int n = 0, d = 0, dp = 0;
   DBuf<double> x64;       // [n][d] unscaled
   DBuf<float> xs32;       // [n][dp]
+  int dpg = 0;            // Gram image width (gram_dp(d)); 0: direct-difference operator
+  DBuf<float> xg32;       // [n + 128][dpg] (x, |x|^2, 0...) for the tensor-core operator
   DBuf<double> xs64;      // [n][d]
   DBuf<double> inv_ls_dev;
   std::vector<double> raw, inv_ls;
@@ -135,6 +137,7 @@ struct gpk_operator {
   DBuf<float> vpk;        // packed TF32 hi/lo RHS images (tcgen05 path)
   DBuf<double> pts64, pts64s;  // posterior query points FP64 [p][d] (raw, scaled)
   DBuf<float> pts32;           // and scaled FP32 [p + 32][dp]
+  DBuf<float> ptsg32;          // and their Gram image [p + 32][dpg]
   // scratch for host-facing calls
   DBuf<float> v32;
   DBuf<double> v64, out64, tmp64;
@@ -171,6 +174,7 @@ struct gpk_batch {
   DBuf<float> apk;                   // AP block update's TF32 operator images
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
   DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
+  DBuf<double> ap_cpart;             // persistent AP: block-update partials [8][block][m]
   // CUDA graph of the AP block build + inverse (ap_prepare), keyed on its buffers
   cudaGraphExec_t ap_graph = nullptr;
   std::array<const void*, 6> ap_graph_key{};
@@ -313,6 +317,7 @@ void set_hyper(gpk_operator* op, const double* raw) {
   const double hv[2] = {op->s2, op->sigma2};
   GPK_CUDA(cudaMemcpyAsync(op->hyp_dev.ensure(2), hv, sizeof(hv), cudaMemcpyHostToDevice, s));
   prescale_launch(op->x64.p, op->n, d, op->dp, il, op->xs32.p, op->xs64.p, s);
+  if (op->dpg) gram_image_launch(op->xs32.p, op->n, d, op->dp, op->dpg, op->xg32.p, s);
   GPK_CUDA(cudaStreamSynchronize(s));  // inv_ls host buffer lifetime
 }
 
@@ -377,9 +382,12 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   splits = std::max(1, (Cmax + cps - 1) / cps);
   double* part = op->part.ensure(static_cast<size_t>(splits) * c.R * c.m);
   KvArgs a{};
-  a.xs = op->xs32.p;
+  // tensor-core kernels: Gram-form distances for d >= 21 (image width >= 24)
+  const bool gram = tc && op->dpg > 0;
+  if (gram && c.xs_rows && c.xs_rows != op->pts32.p) throw std::logic_error("run_kv: cross rows without a Gram image");
+  a.xs = gram ? op->xg32.p : op->xs32.p;
   a.n = op->n;
-  a.dp = op->dp;
+  a.dp = gram ? op->dpg : op->dp;
   a.row_idx = c.row_idx;
   a.r0 = c.r0;
   a.R = c.R;
@@ -398,7 +406,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.skip = c.skip;
   a.stats = op->ctx->stats;
   a.d = op->d;
-  a.xs_rows = c.xs_rows;
+  a.xs_rows = (gram && c.xs_rows) ? op->ptsg32.p : c.xs_rows;
   gpk_ctx* ctx = op->ctx;
   if (c.vpk && !tc) throw InvalidArgument("gpk: pre-packed operator input needs the tcgen05 kernel");
   const float* vpk = c.vpk;
@@ -1290,10 +1298,10 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   if (persistent) {
     // every iteration in one cooperative launch (ap_persistent.cu)
     ApPersistArgs pa{};
-    pa.xs = op->xs32.p;
+    pa.xs = op->dpg ? op->xg32.p : op->xs32.p;  // Gram image for d >= 21, as run_kv
     pa.n = n;
     pa.d = op->d;
-    pa.dp = op->dp;
+    pa.dp = op->dpg ? op->dpg : op->dp;
     pa.m = m;
     pa.npad = kv_tc_npad(m);
     pa.log2_s2 = static_cast<float>(std::log2(op->s2));
@@ -1307,6 +1315,7 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     pa.inv = inv;
     pa.bb = static_cast<long long>(bb);
     pa.upd = upd64;
+    pa.cpart = b->ap_cpart.ensure(static_cast<size_t>(8) * block * m);
     pa.vpk = vpk_blk;
     pa.dpart = part;
     pa.spart = spart_t;
@@ -1315,7 +1324,7 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     pa.tol = c->tolerance;
     pa.ctl = ctl;
     pa.sel = sel;
-    pa.gbar = b->gbar.ensure(1);
+    pa.gbar = b->gbar.ensure(32);  // [0] barrier counter, [4..24) optional phase clock
     pa.stats = ctx->stats;
     GPK_CUDA(cudaMemsetAsync(pa.gbar, 0, sizeof(unsigned), s));
     cudaEvent_t* prof_end = nullptr;
@@ -1330,9 +1339,23 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
       GPK_CUDA(cudaEventRecord(pr.first, s));
       prof_end = &pr.second;
     }
+    static const bool phase_clock = std::getenv("GPK_AP_PROF") != nullptr;  // development: phase split
+    if (phase_clock) {
+      pa.prof = reinterpret_cast<unsigned long long*>(b->gbar.p + 4);
+      GPK_CUDA(cudaMemsetAsync(pa.prof, 0, 10 * sizeof(unsigned long long), s));
+    }
     ap_persistent_launch(pa, s);
     if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
     GPK_CUDA(cudaStreamSynchronize(s));
+    if (phase_clock) {
+      unsigned long long h[10];
+      GPK_CUDA(cudaMemcpy(h, pa.prof, sizeof(h), cudaMemcpyDeviceToHost));
+      const double it = static_cast<double>(h[9]) * 1e3;
+      std::fprintf(stderr,
+                   "ap_persistent phases (us/iteration, %llu iterations): C1load %.2f C1 %.2f Csync %.2f C2 %.2f sync1 %.2f "
+                   "S %.2f sync2 %.2f B %.2f\n",
+                   h[9], h[6] / it, h[7] / it, h[8] / it, h[0] / it, h[1] / it, h[2] / it, h[3] / it, h[4] / it);
+    }
   } else {
     drive(b, ctl, 8, budget, iteration, true);
   }
@@ -1797,6 +1820,11 @@ void upload_points(gpk_operator* op, const double* points, int p) {
   float* p32 = op->pts32.ensure(static_cast<size_t>(p + 32) * dp);
   GPK_CUDA(cudaMemsetAsync(p32, 0, sizeof(float) * (p + 32) * dp, s));
   prescale_launch(p64, p, d, dp, op->inv_ls_dev.p, p32, op->pts64s.ensure(static_cast<size_t>(p) * d), s);
+  if (op->dpg) {
+    float* pg = op->ptsg32.ensure(static_cast<size_t>(p + 32) * op->dpg);
+    GPK_CUDA(cudaMemsetAsync(pg, 0, sizeof(float) * (p + 32) * op->dpg, s));
+    gram_image_launch(p32, p, d, dp, op->dpg, pg, s);
+  }
 }
 
 // out [p][m] = k(P, X) v, v device FP64 [n][m] (cross_kernel_apply, kernel.cpp:72-81; no noise term)
@@ -2034,6 +2062,11 @@ gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d,
     op->xs32.ensure(static_cast<size_t>(n + 128) * op->dp);
     GPK_CUDA(cudaMemsetAsync(op->xs32.p, 0, sizeof(float) * (n + 128) * op->dp, ctx->stream));
     op->xs64.ensure(static_cast<size_t>(n) * d);
+    op->dpg = gram_dp(d);
+    if (op->dpg) {
+      op->xg32.ensure(static_cast<size_t>(n + 128) * op->dpg);
+      GPK_CUDA(cudaMemsetAsync(op->xg32.p, 0, sizeof(float) * (n + 128) * op->dpg, ctx->stream));
+    }
     upload_colmajor(op.get(), inputs, n, d, op->x64.p);
     set_hyper(op.get(), raw);
     *out = op.release();

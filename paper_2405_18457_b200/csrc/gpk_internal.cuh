@@ -155,6 +155,7 @@ struct ApPersistArgs {
   const double* inv;      // block inverses [nblocks][block][block]
   long long bb;
   double* upd;            // [block][m]
+  double* cpart;          // [8][block][m] phase-C1 partials
   float* vpk;             // TF32 images of upd
   double* dpart;          // [tiles][m]
   double* spart;          // [nblocks * gpb]
@@ -165,6 +166,7 @@ struct ApPersistArgs {
   int* sel;
   unsigned* gbar;         // grid-barrier arrival counter (zeroed before the launch)
   double* stats;          // evals x RHS, FP32-equivalent flops, FP32-pipe flops
+  unsigned long long* prof;  // optional phase clock (ns, CTA 0): C, sync1, S, sync2, B, iterations
 };
 bool ap_persistent_supported(int n, int m, int block, int sms);
 void ap_persistent_launch(const ApPersistArgs& a, cudaStream_t s);
@@ -200,6 +202,15 @@ void grad_tc_launch(const GradTcArgs& a, cudaStream_t s);
 // ---- misc device kernels (la_kernels.cu) ---------------------------------
 void prescale_launch(const double* x64, int n, int d, int dp, const double* inv_ls, float* xs32,
                      double* xs64, cudaStream_t s);
+// Gram-form operator image (x, |x|^2, 0...) [n][dpg] for d >= 21 (la_kernels.cu)
+void gram_image_launch(const float* xs32, int n, int d, int dp, int dpg, float* xg, cudaStream_t s);
+// tensor-core operator kernels take the Gram image for d in [8, 31]
+#ifndef GPK_GRAM
+#define GPK_GRAM 1  // build-time A/B switch (make NVEXTRA=-DGPK_GRAM=0): direct differences everywhere
+#endif
+// Gram form for d >= 21 (measured: C2 d = 26 refresh -5%, d = 8 / 11 / 20 +2..12%);
+// image width 4 ceil((d + 1) / 4), i.e. DP4 >= 6 <=> Gram in the kernels (d = 32: DP4 9)
+inline int gram_dp(int d) { return (GPK_GRAM && d >= 21) ? (d + 4) / 4 * 4 : 0; }
 void to_f32_launch(const double* src, int n, int m, int lds, float* dst, int ldd, const int* skip,
                    cudaStream_t s);
 void transpose_launch(const double* src, int rows, int cols, int lds, double* dst, int ldd,

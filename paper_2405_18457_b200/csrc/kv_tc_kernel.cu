@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   constexpr bool FUSED = MODE == 1, DEEP = MODE != 0;
   constexpr int EW = TcRoles<MODE>::EW, CPT = TcRoles<MODE>::CPT;
   constexpr int DP = 4 * DP4;
+  constexpr bool GRAM = GPK_GRAM && DP4 >= 6;  // image (x, |x|^2, 0...): host passes it for d >= 21
   using L = TcLayout<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the fused AP slab runs one CTA per SM: 4 TMEM A buffers (512 columns)
@@ -296,16 +297,28 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     const int er_c = er < a.R ? er : 0;
     const int gi = a.row_idx ? a.row_idx[er_c] : a.r0 + er_c;
     float4 xi[DP4];
-#pragma unroll
     const float* xrow = (a.xs_rows ? a.xs_rows : a.xs) + static_cast<size_t>(gi) * DP;
+#pragma unroll
     for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(xrow) + u);
 #if GPK_EVAL_F32X2
+    // Gram form (image width >= 24, i.e. d >= 21): the row keeps (-2 x_i, 1) and
+    // |x_i|^2 seeds the accumulator, so r^2 = |x_i|^2 + |x_c|^2 - 2 x_i.x_c is
+    // one FFMA2 per two padded dimensions (x_c's image carries |x_c|^2 in slot d)
+    float ni = 0.f;
+    if constexpr (GRAM) {
+#pragma unroll
+      for (int u = 0; u < DP4; ++u) gram_row(xi[u], 4 * u, a.d, ni);
+    }
     uint64_t xi2[2 * DP4];
 #pragma unroll
     for (int u = 0; u < DP4; ++u) {
       asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(xi[u].x), "f"(xi[u].y));
       asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(xi[u].z), "f"(xi[u].w));
     }
+    uint64_t acc_seed;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
+#else
+    static_assert(!GRAM, "the Gram-form operator needs the FP32x2 evaluation loop");
 #endif
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
     double* part = a.part + static_cast<size_t>(split) * a.R * a.m;
@@ -323,8 +336,12 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
       for (int t = 0; t < CPT; ++t) {
 #if GPK_EVAL_F32X2
         // packed FP32x2 (FADD2/FFMA2): two dimensions per instruction
-        uint64_t acc0 = 0ull, acc1 = 0ull;
         const uint32_t xaddr = smem_u32(xc + t * DP);
+        float r;
+        if constexpr (GRAM) {
+          r = sqrt_approx(gram_r2<DP4>(xaddr, xi2, acc_seed));
+        } else {
+        uint64_t acc0 = 0ull, acc1 = 0ull;
 #pragma unroll
         for (int u = 0; u < DP4; ++u) {
           uint64_t c01, c23, d01, d23;
@@ -338,7 +355,8 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         asm("add.rn.f32x2 %0, %1, %2;" : "=l"(accs) : "l"(acc0), "l"(acc1));
         float s0, s1;
         asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(accs));
-        const float r = sqrt_approx(s0 + s1);
+        r = sqrt_approx(s0 + s1);
+        }
 #else
         const float4* xv = reinterpret_cast<const float4*>(xc + t * DP);
         float r2a = 0.f, r2b = 0.f;
@@ -359,6 +377,13 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         // hi + lo carries ~21-22 bits of kv.
         hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
         lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
+      }
+      if constexpr (GRAM) {
+        // the Gram form leaves O(ulp |x|^2) on the kernel diagonal: pin k(x_i, x_i)
+        // to the direct form's value (rare chunks, warp-uniform branch)
+        const int cbase = c0 + cb + k * TBK + half * CPT;
+        const bool hit = !a.xs_rows && er < a.R && static_cast<unsigned>(gi - cbase) < static_cast<unsigned>(CPT);
+        if (__any_sync(0xffffffffu, hit)) gram_pin_diagonal<CPT>(hit, gi - cbase, a.log2_s2, hi, lo);
       }
       const uint32_t abase = tmem + lane_addr + A_BASE + b * 64 + half * CPT;
       if constexpr (CPT == 16) {
@@ -493,6 +518,7 @@ void launch_tc_n(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaS
     case 6: return launch_tc_one<NPAD, 6, MODE>(a, vpk, f, s);
     case 7: return launch_tc_one<NPAD, 7, MODE>(a, vpk, f, s);
     case 8: return launch_tc_one<NPAD, 8, MODE>(a, vpk, f, s);
+    case 9: return launch_tc_one<NPAD, 9, MODE>(a, vpk, f, s);  // d = 32 Gram image
     default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
   }
 }

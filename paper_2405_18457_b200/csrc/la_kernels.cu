@@ -51,6 +51,29 @@ void prescale_launch(const double* x64, int n, int d, int dp, const double* inv_
   check_launch("prescale");
 }
 
+// Distance-by-Gram image for the tensor-core operator kernels (d >= 21): row i
+// = (x_i, |x_i|^2, 0...) with |x_i|^2 summed in FP64 from the FP32 coordinates
+// and rounded once, so r^2 = |x_i|^2 + |x_c|^2 - 2 x_i.x_c is one FFMA chain
+// over the padded row (kv_tc_kernel.cu, ap_persistent.cu).
+__global__ void gram_image_kernel(const float* xs32, int n, int d, int dp, int dpg, float* xg) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float* src = xs32 + static_cast<size_t>(i) * dp;
+    float* dst = xg + static_cast<size_t>(i) * dpg;
+    double nn = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const float v = src[k];
+      nn += static_cast<double>(v) * v;
+      dst[k] = v;
+    }
+    dst[d] = static_cast<float>(nn);
+    for (int k = d + 1; k < dpg; ++k) dst[k] = 0.f;
+  }
+}
+void gram_image_launch(const float* xs32, int n, int d, int dp, int dpg, float* xg, cudaStream_t s) {
+  gram_image_kernel<<<blocks_for(n, 256), 256, 0, s>>>(xs32, n, d, dp, dpg, xg);
+  check_launch("gram_image");
+}
+
 __global__ void to_f32_kernel(const double* src, int n, int m, int lds, float* dst, int ldd, const int* skip) {
   SKIP_IF(skip);
   const long long total = static_cast<long long>(n) * ldd;

@@ -127,5 +127,54 @@ __device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t (&v)[8]) {
                : "memory");
 }
 
+// ---- Gram-form squared distance (d >= 21; see gram_image_kernel) ----
+// Row side: slot d of the image holds |x_i|^2 -> captured into ni and
+// replaced by 1; the coordinates are scaled by -2 (exact).
+__device__ __forceinline__ void gram_row(float4& v, int k0, int d, float& ni) {
+  float* c = reinterpret_cast<float*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (k0 + e == d) {
+      ni = c[e];
+      c[e] = 1.f;
+    } else {
+      c[e] = -2.f * c[e];
+    }
+  }
+}
+// r^2 = |x_i|^2 + sum_k xt_i[k] xt_c[k] over the padded row, four FFMA2 chains
+template <int DP4>
+__device__ __forceinline__ float gram_r2(uint32_t xaddr, const uint64_t* xi2, uint64_t seed) {
+  uint64_t acc[4] = {seed, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int u = 0; u < DP4; ++u) {
+    uint64_t c01, c23;
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(c01), "=l"(c23) : "r"(xaddr + 16 * u));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[(2 * u) & 3]) : "l"(c01), "l"(xi2[2 * u]));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[(2 * u + 1) & 3]) : "l"(c23), "l"(xi2[2 * u + 1]));
+  }
+  uint64_t s01, s23, s;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s01) : "l"(acc[0]), "l"(acc[1]));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s23) : "l"(acc[2]), "l"(acc[3]));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(s01), "l"(s23));
+  float s0, s1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(s));
+  return fmaxf(s0 + s1, 0.f);
+}
+// k(x_i, x_i) = s2 exactly as the direct form evaluates it at r = 0
+template <int CPT>
+__device__ __forceinline__ void gram_pin_diagonal(bool hit, int tpos, float log2_s2, uint32_t* hi, uint32_t* lo) {
+  const float k0 = ex2_approx(log2_s2);
+  const uint32_t h0 = __float_as_uint(k0) & 0xFFFFE000u;
+  const uint32_t l0 = __float_as_uint(k0 - __uint_as_float(h0));
+#pragma unroll
+  for (int t = 0; t < CPT; ++t)
+    if (hit && tpos == t) {
+      hi[t] = h0;
+      lo[t] = l0;
+    }
+}
+
 }  // namespace tc
+
 }  // namespace gpk

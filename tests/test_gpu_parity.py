@@ -45,7 +45,9 @@ def make_op(G, ctx, X, raw):
 
 
 @pytest.mark.parametrize("n,d,m", [(300, 3, 1), (1000, 8, 17), (2048, 26, 65), (777, 20, 65), (513, 1, 9),
-                                   (1500, 11, 33), (4096, 3, 65)])
+                                   (1500, 11, 33), (4096, 3, 65),
+                                   # Gram-form distance tiles (d >= 21), incl. d = 32 (image width 36)
+                                   (900, 21, 17), (1100, 24, 65), (640, 32, 33), (1000, 31, 80)])
 def test_apply_matches_oracle(G, kctx, oracle, n, d, m):
     X, _ = gp_problem(n, d, 1000 + n)
     raw = default_test_raw(d, oracle)
@@ -85,7 +87,7 @@ def test_apply_is_deterministic(G, kctx, oracle):
     assert np.array_equal(op.apply(V), op.apply(V))
 
 
-@pytest.mark.parametrize("n,d,m,b", [(2000, 3, 65, 512), (600, 8, 17, 37), (50, 2, 3, 5)])
+@pytest.mark.parametrize("n,d,m,b", [(2000, 3, 65, 512), (600, 8, 17, 37), (50, 2, 3, 5), (700, 24, 17, 61)])
 def test_apply_rows_matches_oracle(G, kctx, oracle, n, d, m, b):
     X, _ = gp_problem(n, d, 2 * n)
     raw = default_test_raw(d, oracle)

@@ -71,3 +71,21 @@ def test_gpu_posterior_matches_oracle(gpk_ctx, oracle):
     gz = G.sample_posterior(op, None, P[:3], vy, np.zeros((n, 3)))
     assert np.max(np.abs(gz[:, 1] - got[:3])) <= 2e-5 * np.max(np.abs(got))
     assert np.array_equal(gz[:, 0], gz[:, 1]) and np.array_equal(gz[:, 1], gz[:, 2])
+
+
+@pytest.mark.gpu
+def test_gpu_cross_kernel_gram_form_matches_oracle(gpk_ctx, oracle):
+    """k(P, X) V for d >= 21, where the tensor-core operator takes distances in
+    Gram form from the points' own (x, |x|^2) image (no kernel diagonal)."""
+    import paper_2405_18457_b200 as G
+    n, d, p = 1500, 24, 333
+    X, y = gp_problem(n, d, 21)
+    raw = default_test_raw(d, oracle)
+    P, _ = gp_problem(p, d, 22)
+    P[:5] = X[:5]  # coincident points: r = 0 through the Gram form
+    rng = np.random.default_rng(5)
+    op = G.KernelOperator(X, G.Hyperparameters.from_raw(raw), gpk_ctx)
+    V = rng.standard_normal((n, 65))
+    gv = G.cross_kernel_apply(op, P, V)
+    rv = oracle.cross_apply(P, X, raw, V, threads=8)
+    assert max(np.max(np.abs(gv[:, j] - rv[:, j])) / np.max(np.abs(rv[:, j])) for j in range(65)) <= 2e-5
