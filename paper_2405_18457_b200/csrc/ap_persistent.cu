@@ -39,7 +39,7 @@ struct ApLayout {
   static constexpr int CHUNK_FLOATS = 2 * IMG_FLOATS;
   static constexpr uint32_t CHUNK_BYTES = CHUNK_FLOATS * 4;
   // the pipeline ring doubles as phase C1's staging: Hk [32][<=64] + R [<=64][<=NPAD] FP64
-  static constexpr int C1_FLOATS = (32 * 64 + 64 * NPAD) * 2;
+  static constexpr int C1_FLOATS = (32 * (64 + 4) + 64 * 88) * 2;
   static constexpr int RING_FLOATS = STAGES * CHUNK_FLOATS > C1_FLOATS ? STAGES * CHUNK_FLOATS : C1_FLOATS;
 };
 
@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   }
   uint64_t acc_seed;
   asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
+  const float sigma2f = static_cast<float>(a.sigma2);
   int kg = 0;  // chunk counter across iterations (pipeline phases)
   int it = 0;
   int iters = sh[2];
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   auto mark = [&](int i) {
     if (prof) {
       unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (globaltimer is too coarse)
       if (i >= 0) pt[i] += t - tprev;
       tprev = t;
     }
@@ -184,39 +185,69 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
       const int kq = block / 8, rgs = block / 32;
       if (tile < rgs * 8) {
         const int rg = tile >> 3, kgi = tile & 7, kb = kgi * kq;
-        // Hk is symmetric: sHt[k][r] = Hk[kb + k][rg*32 + r] reads whole rows.
-        // FP32 operands and accumulation: upd only sets how far this iteration
-        // projects (V += upd and R -= H upd use the same upd, so the pair stays
-        // consistent); its ~1e-6 relative error is far below the solver
-        // tolerance, and the FP64 pipe of this part is too slow for 17 MFMA per
-        // iteration (measured 6 us vs < 1 us here)
-        float* sHt = reinterpret_cast<float*>(smB);  // [kq][32]
-        float* sR = sHt + 32 * kq;                   // [kq][m]
-        for (int e = tid; e < 32 * kq; e += THREADS) {
-          const int k = e >> 5, r = e & 31, row = rg * 32 + r, kk = kb + k;
-          sHt[e] = (row < len && kk < len) ? static_cast<float>(Hk[static_cast<size_t>(kk) * block + row]) : 0.f;
-        }
+        // FP64 throughout: upd's error must not scale with the block's
+        // condition number (an FP32 Hk or FP32 products give relative errors
+        // ~1e-7 kappa: a non-contracting block step for kappa ~ 1e6). The
+        // 32 x m x kq product runs on the FP64 tensor cores (mma.sync m8n8k4):
+        // sH [32][kq + 4] and sR [kq][88] (zero-padded columns) are strided so
+        // the fragment loads are bank-conflict free.
+        constexpr int SRS = 88;
+        const int sha = kq + 4;
+        double* sH = reinterpret_cast<double*>(smB);  // [32][kq + 4]
+        double* sR = sH + 32 * sha;                   // [kq][SRS]
+        // one round of loads (all issued before the first store); columns of sR
+        // beyond m only feed discarded output columns and are left as they are
+        constexpr int HN = (32 * 64 + THREADS - 1) / THREADS, RN = (64 * 80 + THREADS - 1) / THREADS;
         const int kv = max(0, min(kq, len - kb));
         const double* rsrc = a.R + static_cast<size_t>(r0 + kb) * m;
-        for (int e = tid; e < kq * m; e += THREADS) sR[e] = e < kv * m ? static_cast<float>(rsrc[e]) : 0.f;
+        double hv[HN], rv[RN];
+#pragma unroll
+        for (int i = 0; i < HN; ++i) {
+          // Hk symmetric: read row kb + k, columns rg*32 + r (32 consecutive words per warp)
+          const int e = tid + i * THREADS, k = e >> 5, r = e & 31, row = rg * 32 + r, kk = kb + k;
+          hv[i] = (e < 32 * kq && row < len && kk < len) ? Hk[static_cast<size_t>(kk) * block + row] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < RN; ++i) {
+          const int e = tid + i * THREADS;
+          rv[i] = e < kv * m ? rsrc[e] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < HN; ++i) {
+          const int e = tid + i * THREADS;
+          if (e < 32 * kq) sH[(e & 31) * sha + (e >> 5)] = hv[i];
+        }
+#pragma unroll
+        for (int i = 0; i < RN; ++i) {
+          const int e = tid + i * THREADS;
+          if (e < kq * m) sR[(e / m) * SRS + e % m] = rv[i];
+        }
         __syncthreads();
         mark(6);
-        // thread (row quad rq, column j): 4 rows share every R load (4 chains)
-        for (int w = tid; w < 8 * m; w += THREADS) {
-          const int rq = w / m, j = w % m;
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-          for (int k = 0; k < kq; ++k) {
-            const float rv = sR[k * m + j];
-            const float4 h = *reinterpret_cast<const float4*>(sHt + k * 32 + 4 * rq);
-            acc[0] = fmaf(h.x, rv, acc[0]);
-            acc[1] = fmaf(h.y, rv, acc[1]);
-            acc[2] = fmaf(h.z, rv, acc[2]);
-            acc[3] = fmaf(h.w, rv, acc[3]);
-          }
-          double* dst = a.cpart + (static_cast<size_t>(kgi) * block + rg * 32 + 4 * rq) * m + j;
+        // warp w < ceil(m / 8): column tile w, all four 8-row tiles
+        const int ntiles = (m + 7) / 8;
+        if (warp < ntiles) {
+          const int fr = lane >> 2, fc = lane & 3;
+          double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+          for (int k0 = 0; k0 < kq; k0 += 4) {
+            const double bv = sR[(k0 + fc) * SRS + warp * 8 + fr];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) dst[static_cast<size_t>(q) * m] = static_cast<double>(acc[q]);
+            for (int mt = 0; mt < 4; ++mt) {
+              const double av = sH[(mt * 8 + fr) * sha + k0 + fc];
+              asm volatile(
+                  "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                  : "+d"(acc[mt][0]), "+d"(acc[mt][1])
+                  : "d"(av), "d"(bv));
+            }
+          }
+          const int col = warp * 8 + 2 * fc;
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            double* dst = a.cpart + (static_cast<size_t>(kgi) * block + rg * 32 + mt * 8 + fr) * m;
+            if (col < m) dst[col] = acc[mt][0];
+            if (col + 1 < m) dst[col + 1] = acc[mt][1];
+          }
         }
       }
       mark(7);
@@ -331,10 +362,11 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
           hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
           lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
         }
-        if constexpr (GRAM) {  // pin k(x_i, x_i) (see kv_tc_kernel.cu)
+        {  // diagonal entries: k(x_i, x_i) + sigma^2 (H = K + sigma^2 I on the slab, so
+           // the drain needs no upd rows); also pins the Gram form's r = 0
           const int cbase = c0 + q * TBK + qtr * CPT;
           const bool hit = row_ok && static_cast<unsigned>(er - cbase) < static_cast<unsigned>(CPT);
-          if (__any_sync(0xffffffffu, hit)) gram_pin_diagonal<CPT>(hit, er - cbase, a.log2_s2, hi, lo);
+          if (__any_sync(0xffffffffu, hit)) gram_pin_diagonal<CPT>(hit, er - cbase, a.log2_s2, hi, lo, sigma2f);
         }
         const uint32_t abase = tmem + lane_addr + A_BASE + b * 64 + qtr * CPT;
         tc_st8(abase, hi);
@@ -347,8 +379,6 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
       // ---- drain: R_tile -= D (+ sigma^2 upd on the block's own rows) ----
       mbar_wait(d_full, it & 1);
       tc_fence_after();
-      const bool diag = row_ok && er >= c0 && er < c0 + len;
-      const int vr = er - c0;
       double rowdot = 0.0;
 #pragma unroll 1
       for (int q = 0; q < DC / 4; ++q) {
@@ -363,7 +393,6 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
           cs[e] = 0.0;
           if (row_ok && j < m) {
             double acc = static_cast<double>(__uint_as_float(v[e]));
-            if (diag) acc += a.sigma2 * a.upd[static_cast<size_t>(vr) * m + j];
             const double val = Rt[static_cast<size_t>(lrow) * m + j] - acc;
             Rt[static_cast<size_t>(lrow) * m + j] = val;
             a.R[static_cast<size_t>(er) * m + j] = val;
@@ -417,89 +446,116 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     kg += nq;
     ++it;
     mark(2);
-    grid_sync(a.gbar, nctas, gen);
-    mark(3);
-    // ---------------- B: termination test and next block (every CTA alike) ----------------
-    // One round of loads: thread (j, p) = (tid / 8, tid % 8) sums column j of
-    // the tile partials over tiles p, p + 8, ... (all loads issued together),
-    // then a fixed xor-4/2/1 tree; thread k < nblocks sums block k's score
-    // partials in order. The order is identical in every CTA.
-    {
-      const int G = static_cast<int>(nctas);
-      constexpr int QH = 10;  // 2 x 10 x 8 >= 148 tiles (ap_persistent_supported)
-      const int j = tid >> 3, p = tid & 7;
-      double v[QH];
-#pragma unroll
-      for (int i = 0; i < QH; ++i) {
-        const int q = p + 8 * i;
-        v[i] = (j < m && q < G) ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
-      }
-      double sp[4] = {0.0, 0.0, 0.0, 0.0};  // gpb <= 4 (ap_persistent_supported)
-      if (tid < a.nblocks) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q < a.gpb) sp[q] = __ldcg(a.spart + static_cast<size_t>(tid) * a.gpb + q);
-      }
-      double acc = 0.0;
-#pragma unroll
-      for (int i = 0; i < QH; ++i) acc += v[i];
-      if (G > 8 * QH) {
-#pragma unroll
-        for (int i = 0; i < QH; ++i) {
-          const int q = p + 8 * (QH + i);
-          v[i] = (j < m && q < G) ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < QH; ++i) acc += v[i];
-      }
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      if (p == 0 && j < m) ss[j] = sqrt(acc) / a.scales[j];
-      if (tid < a.nblocks) bscore[tid] = sqrt(((sp[0] + sp[1]) + sp[2]) + sp[3]);
+    // ---------------- B: termination test and next block ----------------
+    // The last CTA to finish its slab (arrival ticket) sums the tile partials
+    // in a fixed order, tests termination, picks the next block (ap_check /
+    // ap_select, strict '>' from -1) and publishes {sel, stop} with a release
+    // flag; the other CTAs wait on the flag. Replaces a grid barrier plus a
+    // redundant reduction in every CTA.
+    if (tid == 0) iters += 1;  // every CTA counts iterations (budget test)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const unsigned t = atomicAdd(a.gbar + 1, 1u);
+      sh[3] = (t == nctas * static_cast<unsigned>(it) - 1u) ? 1 : 0;
     }
     __syncthreads();
-    if (warp == 0) {
-      // probe mean over columns 1..m-1 and the first maximal block score
-      // (the serial strict '>' scan from -1 of ap_select)
-      double sum = 0.0;
-      for (int jj = 1 + lane; jj < m; jj += 32) sum += ss[jj];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      double best = -1.0;
-      int best_k = 0x7fffffff;
-      for (int k = lane; k < a.nblocks; k += 32)
-        if (bscore[k] > best) {
-          best = bscore[k];
-          best_k = k;
+    mark(3);
+    if (sh[3]) {
+      __threadfence();
+      // one round of loads: thread (j, p) = (tid / 8, tid % 8) sums column j of
+      // the tile partials over tiles p, p + 8, ... then a fixed xor-4/2/1 tree;
+      // thread k < nblocks sums block k's score partials in order
+      {
+        const int G = static_cast<int>(nctas);
+        constexpr int QH = 10;  // 2 x 10 x 8 >= 148 tiles (ap_persistent_supported)
+        const int j = tid >> 3, p = tid & 7;
+        double v[QH];
+  #pragma unroll
+        for (int i = 0; i < QH; ++i) {
+          const int q = p + 8 * i;
+          v[i] = (j < m && q < G) ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
         }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
-        if (ob > best || (ob == best && ok < best_k)) {
-          best = ob;
-          best_k = ok;
+        double sp[4] = {0.0, 0.0, 0.0, 0.0};  // gpb <= 4 (ap_persistent_supported)
+        if (tid < a.nblocks) {
+  #pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < a.gpb) sp[q] = __ldcg(a.spart + static_cast<size_t>(tid) * a.gpb + q);
         }
+        double acc = 0.0;
+  #pragma unroll
+        for (int i = 0; i < QH; ++i) acc += v[i];
+        if (G > 8 * QH) {
+  #pragma unroll
+          for (int i = 0; i < QH; ++i) {
+            const int q = p + 8 * (QH + i);
+            v[i] = (j < m && q < G) ? __ldcg(a.dpart + static_cast<size_t>(q) * m + j) : 0.0;
+          }
+  #pragma unroll
+          for (int i = 0; i < QH; ++i) acc += v[i];
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (p == 0 && j < m) ss[j] = sqrt(acc) / a.scales[j];
+        if (tid < a.nblocks) bscore[tid] = sqrt(((sp[0] + sp[1]) + sp[2]) + sp[3]);
       }
-      if (best_k == 0x7fffffff) best_k = 0;
-      if (lane == 0) {
-        iters += 1;
-        const double mean = ss[0];
-        const double probe = m > 1 ? sum / (m - 1) : 0.0;
-        const int done = (mean <= a.tol && probe <= a.tol) ? 1 : 0;
-        const int stop = (done || iters >= a.budget) ? 1 : 0;
-        sh[0] = best_k;
-        sh[1] = stop;
-        if (blockIdx.x == 0) {
+      __syncthreads();
+      if (warp == 0) {
+        // probe mean over columns 1..m-1 and the first maximal block score
+        // (the serial strict '>' scan from -1 of ap_select)
+        double sum = 0.0;
+        for (int jj = 1 + lane; jj < m; jj += 32) sum += ss[jj];
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        double best = -1.0;
+        int best_k = 0x7fffffff;
+        for (int k = lane; k < a.nblocks; k += 32)
+          if (bscore[k] > best) {
+            best = bscore[k];
+            best_k = k;
+          }
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
+          if (ob > best || (ob == best && ok < best_k)) {
+            best = ob;
+            best_k = ok;
+          }
+        }
+        if (best_k == 0x7fffffff) best_k = 0;
+        if (lane == 0) {
+          const double mean = ss[0];
+          const double probe = m > 1 ? sum / (m - 1) : 0.0;
+          const int done = (mean <= a.tol && probe <= a.tol) ? 1 : 0;
+          const int stop = (done || iters >= a.budget) ? 1 : 0;
+          sh[0] = best_k;
+          sh[1] = stop;
           a.ctl->iters = iters;
           a.ctl->mean_norm = mean;
           a.ctl->probe_norm = probe;
           a.ctl->done = done;
           a.ctl->stop = stop;
           *a.sel = best_k;
+          a.gbar[3] = static_cast<unsigned>(best_k);  // broadcast to the other CTAs
+          a.gbar[4] = static_cast<unsigned>(stop);
         }
       }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.gbar + 2), "r"(static_cast<unsigned>(it)) : "memory");
+      }
+    } else if (tid == 0) {
+      while (true) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.gbar + 2) : "memory");
+        if (v >= static_cast<unsigned>(it)) break;
+        __nanosleep(32);
+      }
+      sh[0] = static_cast<int>(__ldcg(a.gbar + 3));
+      sh[1] = static_cast<int>(__ldcg(a.gbar + 4));
     }
     __syncthreads();
     mark(4);

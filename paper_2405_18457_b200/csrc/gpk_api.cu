@@ -1324,9 +1324,9 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     pa.tol = c->tolerance;
     pa.ctl = ctl;
     pa.sel = sel;
-    pa.gbar = b->gbar.ensure(32);  // [0] barrier counter, [4..24) optional phase clock
+    pa.gbar = b->gbar.ensure(32);  // [0..5) barrier, ticket, flag, sel, stop; [8..28) optional phase clock
     pa.stats = ctx->stats;
-    GPK_CUDA(cudaMemsetAsync(pa.gbar, 0, sizeof(unsigned), s));
+    GPK_CUDA(cudaMemsetAsync(pa.gbar, 0, 8 * sizeof(unsigned), s));  // barrier, ticket, flag, sel, stop
     cudaEvent_t* prof_end = nullptr;
     if (ctx->profiling) {  // timed as one operator launch (it also runs the block updates)
       if (ctx->prof_used == ctx->prof.size()) {
@@ -1341,7 +1341,7 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     }
     static const bool phase_clock = std::getenv("GPK_AP_PROF") != nullptr;  // development: phase split
     if (phase_clock) {
-      pa.prof = reinterpret_cast<unsigned long long*>(b->gbar.p + 4);
+      pa.prof = reinterpret_cast<unsigned long long*>(b->gbar.p + 8);
       GPK_CUDA(cudaMemsetAsync(pa.prof, 0, 10 * sizeof(unsigned long long), s));
     }
     ap_persistent_launch(pa, s);
@@ -1350,10 +1350,10 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     if (phase_clock) {
       unsigned long long h[10];
       GPK_CUDA(cudaMemcpy(h, pa.prof, sizeof(h), cudaMemcpyDeviceToHost));
-      const double it = static_cast<double>(h[9]) * 1e3;
+      const double it = static_cast<double>(h[9]) * 1.9e3;  // cycles -> us at ~1.9 GHz
       std::fprintf(stderr,
-                   "ap_persistent phases (us/iteration, %llu iterations): C1load %.2f C1 %.2f Csync %.2f C2 %.2f sync1 %.2f "
-                   "S %.2f sync2 %.2f B %.2f\n",
+                   "ap_persistent phases (us/iteration at 1.9 GHz, %llu iterations): C1load %.2f C1 %.2f Csync %.2f C2 %.2f sync1 %.2f "
+                   "S %.2f ticket %.2f B %.2f\n",
                    h[9], h[6] / it, h[7] / it, h[8] / it, h[0] / it, h[1] / it, h[2] / it, h[3] / it, h[4] / it);
     }
   } else {
@@ -1918,7 +1918,14 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     if (const char* e = std::getenv("GPK_AP_PERSISTENT")) c->ap_persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("GPK_GRAPHS")) c->graphs = std::atoi(e) != 0;
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    GPK_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    {  // the auxiliary stream (AP block inverses: chains of small latency-bound
+       // launches) runs at the highest priority, so its blocks are scheduled
+       // between the waves of the main stream's large operator launches
+      int lo = 0, hi = 0;
+      GPK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const char* e = std::getenv("GPK_AUX_PRIORITY");
+      GPK_CUDA(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, (e && std::atoi(e) == 0) ? lo : hi));
+    }
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev_m2a, cudaEventDisableTiming));
     GPK_CUDA(cudaEventCreateWithFlags(&c->ev_aux, cudaEventDisableTiming));
     if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate");

@@ -164,7 +164,7 @@ struct ApPersistArgs {
   double tol;
   CgCtl* ctl;
   int* sel;
-  unsigned* gbar;         // grid-barrier arrival counter (zeroed before the launch)
+  unsigned* gbar;         // [0] grid-barrier arrivals, [1] slab ticket, [2] decision flag, [3] sel, [4] stop (zeroed)
   double* stats;          // evals x RHS, FP32-equivalent flops, FP32-pipe flops
   unsigned long long* prof;  // optional phase clock (ns, CTA 0): C, sync1, S, sync2, B, iterations
 };

@@ -161,10 +161,12 @@ __device__ __forceinline__ float gram_r2(uint32_t xaddr, const uint64_t* xi2, ui
   asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(s));
   return fmaxf(s0 + s1, 0.f);
 }
-// k(x_i, x_i) = s2 exactly as the direct form evaluates it at r = 0
+// k(x_i, x_i) = s2 exactly as the direct form evaluates it at r = 0, plus
+// `add` (the persistent AP slab folds the noise term sigma^2 into the entry)
 template <int CPT>
-__device__ __forceinline__ void gram_pin_diagonal(bool hit, int tpos, float log2_s2, uint32_t* hi, uint32_t* lo) {
-  const float k0 = ex2_approx(log2_s2);
+__device__ __forceinline__ void gram_pin_diagonal(bool hit, int tpos, float log2_s2, uint32_t* hi, uint32_t* lo,
+                                                  float add = 0.f) {
+  const float k0 = ex2_approx(log2_s2) + add;
   const uint32_t h0 = __float_as_uint(k0) & 0xFFFFE000u;
   const uint32_t l0 = __float_as_uint(k0 - __uint_as_float(h0));
 #pragma unroll
