@@ -1511,30 +1511,86 @@ void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, c
   check_launch("sgd_unscatter");
 }
 
-// ------------------------------------------------------------ RFF (K5)
-// Feature rows for the GEMM form of the prior: F[i][2p] = amp cos(theta_ip),
-// F[i][2p+1] = amp sin(theta_ip), theta_ip = x_i . (Omega_p / l) in FP64
-// (rff.cpp:36-54); one thread per (i, p), consecutive p -> coalesced rows;
-// freq is [d][pairs] (already divided by the lengthscales).
-__global__ void rff_features_kernel(const double* x64, int n, int d, const double* freq, int pairs, double amplitude,
-                                    double* F) {
-  const long long total = static_cast<long long>(n) * pairs;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long i = e / pairs;
-    const int p = static_cast<int>(e % pairs);
-    double ang = 0.0;  // freq is [d][pairs]: consecutive p read consecutive words
-    for (int k = 0; k < d; ++k) ang += x64[i * d + k] * freq[static_cast<size_t>(k) * pairs + p];
+// sin and cos of an FP64 angle to ~1 ulp for |t| < 2^30: Cody-Waite
+// reduction by pi/2 in three parts (fma, exact products), then the Taylor
+// series on |r| <= pi/4 through r^17 / r^18 (truncation < 1e-19). CUDA's
+// sincos(double) takes a slow table path (local memory) for the heavy-tailed
+// Matern frequencies; this one is branch-free (~30 DFMA).
+__device__ __forceinline__ void sincos_rr(double t, double* sn, double* cs) {
+  const double q = rint(t * 0.63661977236758134308);                    // 2 / pi
+  double r = fma(-q, 1.5707963267948965579989817342720925807952880859375, t);  // pi/2 in 3 parts
+  r = fma(-q, 6.123233995736766035868820147291818e-17, r);
+  r = fma(-q, -1.4973849048591698329435778716705e-33, r);
+  const double z = r * r;
+  // sin r = r (1 - z/3! + z^2/5! - ... - z^8/17!)
+  double ps = 2.8114572543455207632e-15;      //  1/17!
+  ps = fma(ps, z, -7.6471637318198164759e-13);  // -1/15!
+  ps = fma(ps, z, 1.6059043836821614599e-10);   //  1/13!
+  ps = fma(ps, z, -2.5052108385441718775e-08);  // -1/11!
+  ps = fma(ps, z, 2.7557319223985890653e-06);   //  1/9!
+  ps = fma(ps, z, -1.9841269841269841270e-04);  // -1/7!
+  ps = fma(ps, z, 8.3333333333333333333e-03);   //  1/5!
+  ps = fma(ps, z, -1.6666666666666666667e-01);  // -1/3!
+  const double sr = fma(ps * z, r, r);
+  // cos r = 1 - z/2! + z^2/4! - ... + z^9/18!
+  double pc = -1.5619206968586225796e-16;      // -1/18!
+  pc = fma(pc, z, 4.7794773323873852974e-14);   //  1/16!
+  pc = fma(pc, z, -1.1470745597729724714e-11);  // -1/14!
+  pc = fma(pc, z, 2.0876756987868098979e-09);   //  1/12!
+  pc = fma(pc, z, -2.7557319223985890653e-07);  // -1/10!
+  pc = fma(pc, z, 2.4801587301587301587e-05);   //  1/8!
+  pc = fma(pc, z, -1.3888888888888888889e-03);  // -1/6!
+  pc = fma(pc, z, 4.1666666666666666667e-02);   //  1/4!
+  pc = fma(pc, z, -0.5);
+  const double cr = fma(pc, z, 1.0);
+  const int n = static_cast<int>(static_cast<long long>(q) & 3);
+  const double s0 = (n & 1) ? cr : sr, c0 = (n & 1) ? sr : cr;
+  *sn = (n & 2) ? -s0 : s0;
+  *cs = ((n + 1) & 2) ? -c0 : c0;
+}
+
+// F[i][2p] = amp cos(theta_ip), F[i][2p+1] = amp sin(theta_ip),
+// theta_ip = x_i . (Omega_p / l) in FP64 (rff.cpp:36-54). Block = 128
+// consecutive features p (one per thread, Omega_p in registers) x 64 rows
+// (x tile in shared memory, read as warp broadcasts); lanes write consecutive
+// (cos, sin) pairs of a row. freq is [d][pairs] (already divided by the
+// lengthscales).
+constexpr int RFF_TP = 128, RFF_TR = 64;
+__global__ void __launch_bounds__(RFF_TP) rff_features_kernel(const double* x64, int n, int d, const double* freq,
+                                                              int pairs, double amplitude, double* F) {
+  __shared__ double xt[RFF_TR][32];
+  const int p = blockIdx.x * RFF_TP + threadIdx.x;
+  const int i0 = blockIdx.y * RFF_TR;
+  const int rows = min(RFF_TR, n - i0);
+  for (int e = threadIdx.x; e < rows * d; e += RFF_TP) xt[e / d][e % d] = x64[static_cast<size_t>(i0) * d + e];
+  double w[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) w[k] = (k < d && p < pairs) ? freq[static_cast<size_t>(k) * pairs + p] : 0.0;
+  __syncthreads();
+  if (p >= pairs) return;
+  double2* out = reinterpret_cast<double2*>(F);
+  for (int r = 0; r < rows; ++r) {
+    double a0 = 0.0, a1 = 0.0;  // two chains, summed in a fixed order
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) {
+      if (k < d) a0 = fma(xt[r][k], w[k], a0);
+      if (k + 1 < d) a1 = fma(xt[r][k + 1], w[k + 1], a1);
+    }
+    const double ang = a0 + a1;
     double sn, c;
-    sincos(ang, &sn, &c);
-    F[i * 2 * pairs + 2 * p] = amplitude * c;
-    F[i * 2 * pairs + 2 * p + 1] = amplitude * sn;
+    if (fabs(ang) < 1073741824.0) {
+      sincos_rr(ang, &sn, &c);
+    } else {
+      sincos(ang, &sn, &c);  // huge angles: the library's full-precision reduction
+    }
+    out[static_cast<size_t>(i0 + r) * pairs + p] = make_double2(amplitude * c, amplitude * sn);
   }
 }
 void rff_features_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude, double* F,
                          cudaStream_t s) {
-  rff_features_kernel<<<blocks_for(static_cast<long long>(n) * pairs, 256), 256, 0, s>>>(x64, n, d, freq, pairs,
-                                                                                      amplitude, F);
+  if (n <= 0) return;
+  const dim3 grid((pairs + RFF_TP - 1) / RFF_TP, (n + RFF_TR - 1) / RFF_TR);
+  rff_features_kernel<<<grid, RFF_TP, 0, s>>>(x64, n, d, freq, pairs, amplitude, F);
   check_launch("rff_features");
 }
 
