@@ -97,9 +97,10 @@ struct gpk_ctx {
   bool fused_ap = true;  // AP slabs: reduce + epilogue fused into the tcgen05 kernel
   int spd_inverse = 1;   // AP block inverses: 1 recursive Schur/DGEMM, 0 cuSOLVER potrf + 2 trsm
   bool ap_persistent = true;  // AP iterations in one cooperative launch (GPK_AP_PERSISTENT=0 disables)
-  int kv_deep = -1;
+  int kv_deep = -1;  // operator launches one CTA per SM with 16 eval warps: -1 auto (>= 1e8 entries), 0/1 forced
+  bool kv_streamk = false;  // deep launches as stream-K (GPK_KV_STREAMK=1); measured 1-7% slower than the 2-D grid
   bool graphs = true;  // CG/AP iteration groups as CUDA graphs (GPK_GRAPHS=0 disables)
-  void* blas_ws = nullptr;  // operator launches one CTA per SM with 16 eval warps: -1 auto (>= 1e8 entries), 0/1 forced
+  void* blas_ws = nullptr;  // cuBLAS workspace (graph capture)
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
   DBuf<double> rff_feat;  // RFF feature rows (prior GEMM), reused across calls
@@ -380,6 +381,22 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   int cps = (Cmax + splits - 1) / splits;
   cps = (cps + 31) / 32 * 32;
   splits = std::max(1, (Cmax + cps - 1) / cps);
+  // deep launches with a host-known column range run stream-K: one persistent
+  // CTA per SM over the (row tile, chunk) units; a tile's partials occupy the
+  // split slots 0 .. (number of CTAs that touched it) - 1
+  const bool streamk = deep && !c.sel && op->ctx->kv_streamk;
+  int sk_G = 0, sk_Q = 0;
+  long long sk_U = 0;
+  if (streamk) {
+    const long long T = (c.R + 127) / 128;
+    sk_Q = (Cmax + 31) / 32;
+    sk_U = T * sk_Q;
+    sk_G = static_cast<int>(std::min<long long>(op->ctx->sms, sk_U));
+    int maxseg = 1;
+    for (long long t = 0; t < T; ++t)
+      maxseg = std::max(maxseg, static_cast<int>(sk_last(t, sk_Q, sk_G, sk_U) - sk_first(t, sk_Q, sk_G, sk_U) + 1));
+    splits = maxseg;
+  }
   double* part = op->part.ensure(static_cast<size_t>(splits) * c.R * c.m);
   KvArgs a{};
   // tensor-core kernels: Gram-form distances for d >= 21 (image width >= 24)
@@ -407,6 +424,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.stats = op->ctx->stats;
   a.d = op->d;
   a.xs_rows = (gram && c.xs_rows) ? op->ptsg32.p : c.xs_rows;
+  a.sk_ctas = sk_G;
   gpk_ctx* ctx = op->ctx;
   if (c.vpk && !tc) throw InvalidArgument("gpk: pre-packed operator input needs the tcgen05 kernel");
   const float* vpk = c.vpk;
@@ -469,13 +487,16 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   r.ap_bb = c.ap_bb;
   r.ap_upd = c.ap_upd;
   r.nodiag = c.xs_rows != nullptr;
+  r.sk_G = sk_G;
+  r.sk_Q = sk_Q;
+  r.sk_U = sk_U;
   if (fused) {
     kv_tc_fused_launch(a, vpk, r, s);
     if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
     return;
   }
   if (tc)
-    kv_tc_launch(a, vpk, s, deep);
+    kv_tc_launch(a, vpk, s, streamk ? 3 : (deep ? 2 : 0));
   else
     kv_slab_launch(a, op->d, s);
   if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
@@ -1915,6 +1936,7 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     if (const char* e = std::getenv("GPK_FUSED_AP")) c->fused_ap = std::atoi(e) != 0;  // A/B switches
     if (const char* e = std::getenv("GPK_SPD_INVERSE")) c->spd_inverse = std::atoi(e);
     if (const char* e = std::getenv("GPK_KV_DEEP")) c->kv_deep = std::atoi(e);
+    if (const char* e = std::getenv("GPK_KV_STREAMK")) c->kv_streamk = std::atoi(e) != 0;
     if (const char* e = std::getenv("GPK_AP_PERSISTENT")) c->ap_persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("GPK_GRAPHS")) c->graphs = std::atoi(e) != 0;
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

@@ -55,6 +55,7 @@ struct KvArgs {
   float log2_s2;       // log2(signal variance)
   double* part;        // [splits][R][m]
   int splits, cols_per_split, flush_chunks;
+  int sk_ctas;         // stream-K launch (MODE 3): persistent CTAs
   const int* skip;     // device flag: nonzero => no-op (solver predication)
   double* stats;       // device counters [evals x RHS, algorithmic flops] or null
   int d;               // true input dimension (flop accounting)
@@ -71,8 +72,17 @@ int kv_tc_npad(int m);
 size_t kv_tc_pack_floats(int m, int rows);
 void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_max, int m, const int* sel,
                        int sel_block, int n, float* vpk, const int* skip, cudaStream_t s, int rows_valid = -1);
-void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s, bool deep = false);
+void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s, int mode = 0);  // 0 normal, 2 deep, 3 stream-K (grid = a.sk_G)
 struct KvReduceArgs;
+// stream-K decomposition of a full operator product (kv_tc_kernel MODE 3):
+// U = tiles x Q chunk units over G persistent CTAs, CTA b owns units
+// [b U / G, (b + 1) U / G); tile t is split among CTAs sk_first(t)..sk_last(t)
+__host__ __device__ inline long long sk_first(long long t, int Q, int G, long long U) {
+  return ((t * Q + 1) * G - 1) / U;
+}
+__host__ __device__ inline long long sk_last(long long t, int Q, int G, long long U) {
+  return (((t + 1) * Q) * G - 1) / U;
+}
 // AP slab with the reduce fused into the tensor-core kernel (splits == 1,
 // one accumulation group, score_block a multiple of 128): writes out, the
 // per-tile dpart/spart partials and runs the AP epilogue in the last CTA.
@@ -81,6 +91,10 @@ void kv_tc_fused_launch(const KvArgs& a, const float* vpk, const KvReduceArgs& f
 struct KvReduceArgs {
   const double* part;
   int splits, R, m;
+  // stream-K operator launch (kv_tc_kernel MODE 3): tile t's partials are the
+  // split slots 0..nseg(t)-1 written by CTAs sk_first(t).. (sk_G == 0: splits)
+  int sk_G, sk_Q;
+  long long sk_U;
   const double* vdiag;  // FP64 RHS for the diagonal term, [C][ldvd] (row c - c0), or null
   int ldvd;
   const float* vdiag32; // fallback FP32 RHS for the diagonal

@@ -276,6 +276,12 @@ void launch_tc(const KvArgs& a, cudaStream_t s) {
 }
 
 // ---- split reduction + diagonal term ------------------------------------
+__device__ __forceinline__ int splits_of_row(const KvReduceArgs& a, int r) {
+  if (!a.sk_G) return a.splits;
+  const long long t = r / 128;
+  return static_cast<int>(sk_last(t, a.sk_Q, a.sk_G, a.sk_U) - sk_first(t, a.sk_Q, a.sk_G, a.sk_U) + 1);
+}
+
 __global__ void kv_reduce_kernel(const KvReduceArgs a) {
   if (a.skip && *a.skip) return;
   int c0 = a.c0, C = a.C;
@@ -288,7 +294,8 @@ __global__ void kv_reduce_kernel(const KvReduceArgs a) {
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(e / a.m), j = static_cast<int>(e % a.m);
     double acc = 0.0;
-    for (int s = 0; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
+    const int ns = splits_of_row(a, r);
+    for (int s = 0; s < ns; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
     const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
     if (!a.nodiag && gi >= c0 && gi < c0 + C) {
       const int vr = gi - c0 - a.vshift;
@@ -348,6 +355,7 @@ __global__ void __launch_bounds__(256, 3) kv_reduce_dot_kernel(const KvReduceArg
     const int gi = a.row_idx ? a.row_idx[r] : a.r0 + r;
     const bool diag = !a.nodiag && gi >= c0 && gi < c0 + C;
     const int vr = gi - c0 - a.vshift;
+    const int ns = splits_of_row(a, r);
     double pv[MQ][2], bv[MQ], dv[MQ], wv[MQ];
 #pragma unroll
     for (int q = 0; q < MQ; ++q) {
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(256, 3) kv_reduce_dot_kernel(const KvReduceArg
       const bool ok = j < a.m;
 #pragma unroll
       for (int s = 0; s < 2; ++s)
-        pv[q][s] = (ok && s < a.splits) ? __ldcs(a.part + (static_cast<size_t>(s) * a.R + r) * a.m + j) : 0.0;
+        pv[q][s] = (ok && s < ns) ? __ldcs(a.part + (static_cast<size_t>(s) * a.R + r) * a.m + j) : 0.0;
       bv[q] = (ok && a.base) ? a.base[static_cast<size_t>(r) * a.ldb + j] : 0.0;
       dv[q] = 0.0;
       if (ok && diag)
@@ -369,8 +377,8 @@ __global__ void __launch_bounds__(256, 3) kv_reduce_dot_kernel(const KvReduceArg
       const int j = lane + 32 * q;
       if (j < a.m) {
         double acc = pv[q][0];
-        if (a.splits > 1) acc += pv[q][1];
-        for (int s = 2; s < a.splits; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
+        if (ns > 1) acc += pv[q][1];
+        for (int s = 2; s < ns; ++s) acc += a.part[(static_cast<size_t>(s) * a.R + r) * a.m + j];
         if (diag) acc += a.sigma2 * dv[q];
         const double val = bv[q] + a.alpha * acc;
         a.out[static_cast<size_t>(r) * a.ldo + j] = val;

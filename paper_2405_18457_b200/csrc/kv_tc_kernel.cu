@@ -152,7 +152,11 @@ __device__ __forceinline__ void fused_drain(const KvArgs& a, const KvReduceArgs&
 // MODE 0: two CTAs per SM, 8 evaluation warps, 2 TMEM A buffers (default);
 // MODE 1: fused AP slab; MODE 2: "deep" -- one CTA per SM with 16 evaluation
 // warps and 4 A buffers (512 TMEM columns), for launches whose per-chunk
-// barrier/MMA latency dominates (small d, few rows).
+// barrier/MMA latency dominates (small d, few rows); MODE 3: the deep CTA as
+// a persistent stream-K worker -- one CTA per SM walks a contiguous range of
+// the (row tile, 32-column chunk) units, so every SM gets the same number of
+// chunks (no partial last wave, one TMEM allocation and pipeline fill per SM)
+// and writes one partial per row tile it touches (sk_first .. sk_last).
 template <int MODE>
 struct TcRoles {
   static constexpr int EW = MODE ? 16 : EVAL_WARPS;  // evaluation warps
@@ -163,7 +167,7 @@ struct TcRoles {
 template <int NPAD, int DP4, int MODE>
 __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk, const KvReduceArgs f) {
-  constexpr bool FUSED = MODE == 1, DEEP = MODE != 0;
+  constexpr bool FUSED = MODE == 1, DEEP = MODE != 0, SK = MODE == 3;
   constexpr int EW = TcRoles<MODE>::EW, CPT = TcRoles<MODE>::CPT;
   constexpr int DP = 4 * DP4;
   constexpr bool GRAM = GPK_GRAM && DP4 >= 6;  // image (x, |x|^2, 0...): host passes it for d >= 21
@@ -195,6 +199,51 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   const int ce = min(C, cb + a.cols_per_split);
   const int nq = ce > cb ? (ce - cb + TBK - 1) / TBK : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // chunk schedule: stream-K units [u0, u0 + nk) of U = tiles x Q, or this
+  // CTA's nq chunks of one tile
+  int Q = 1, nk = nq;
+  long long U = 1, u0 = 0;
+  if constexpr (SK) {
+    Q = (C + TBK - 1) / TBK;
+    U = static_cast<long long>((a.R + TBM - 1) / TBM) * Q;
+    u0 = blockIdx.x * U / gridDim.x;
+    nk = static_cast<int>((blockIdx.x + 1) * U / gridDim.x - u0);
+  }
+  const int flush = a.flush_chunks;
+  // walks this CTA's units in order: row tile t, chunk q, accumulation-group
+  // boundaries (incremental: no per-chunk 64-bit division)
+  struct Walk {
+    int t, q, gp, k;
+    bool first, last;
+  };
+  auto walk_begin = [&]() {
+    Walk w;
+    if constexpr (SK) {
+      w.t = static_cast<int>(u0 / Q);
+      w.q = static_cast<int>(u0 - static_cast<long long>(w.t) * Q);
+    } else {
+      w.t = tile;
+      w.q = cb / TBK;  // cb is a multiple of TBK
+    }
+    w.gp = 0;
+    w.k = 0;
+    w.first = true;
+    w.last = nk == 1 || (SK && w.q + 1 == Q) || flush == 1;
+    return w;
+  };
+  auto walk_next = [&](Walk& w) {
+    const bool tile_end = SK && w.q + 1 == Q;
+    w.gp = w.last ? 0 : w.gp + 1;
+    ++w.k;
+    if (tile_end) {
+      w.q = 0;
+      ++w.t;
+    } else {
+      ++w.q;
+    }
+    w.first = w.gp == 0;
+    w.last = w.k + 1 == nk || (SK && w.q + 1 == Q) || w.gp + 1 == flush;
+  };
 
   if (a.stats && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
     const double entries = static_cast<double>(a.R) * C;
@@ -227,8 +276,6 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int flush = a.flush_chunks;
-  const int ngroups = (nq + flush - 1) / flush;
 
   // fused AP slab: the tile's rows of `base` (the residual) are staged in smem
   // by one bulk copy issued before the chunk loop, so the drain never waits on
@@ -247,26 +294,27 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   if (warp == EW) {
     // ---------------- producer ----------------
     if (lane == 0) {
-      for (int k = 0; k < nq; ++k) {
+      Walk w = walk_begin();
+      for (int k = 0; k < nk; ++k, walk_next(w)) {
         const int s = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[s], ((k - STAGES) / STAGES) & 1);
-        const int chunk = (cb / TBK) + k;  // cb is a multiple of TBK
+        const int chunk = w.q;
         const uint32_t xbytes = TBK * DP * 4;
         mbar_expect_tx(&full[s], L::CHUNK_BYTES + xbytes);
         bulk_g2s(smB + s * L::CHUNK_FLOATS, vpk + static_cast<size_t>(chunk) * L::CHUNK_FLOATS, L::CHUNK_BYTES,
                  &full[s]);
-        bulk_g2s(smX + s * TBK * DP, a.xs + static_cast<size_t>(c0 + cb + k * TBK) * DP, xbytes, &full[s]);
+        bulk_g2s(smX + s * TBK * DP, a.xs + static_cast<size_t>(c0 + chunk * TBK) * DP, xbytes, &full[s]);
       }
     }
   } else if (warp == EW + 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
-      for (int k = 0; k < nq; ++k) {
+      int g = 0;  // accumulation groups issued
+      Walk w = walk_begin();
+      for (int k = 0; k < nk; ++k, walk_next(w)) {
         const int s = k % STAGES, b = k % NAB;
-        const int g = k / flush;
-        const bool first_in_group = (k % flush) == 0;
-        const bool last_in_group = ((k + 1) % flush) == 0 || k + 1 == nq;
+        const bool first_in_group = w.first, last_in_group = w.last;
         mbar_wait(&full[s], (k / STAGES) & 1);
         mbar_wait(&a_full[b], (k / NAB) & 1);
         if (first_in_group && g > 0) mbar_wait(d_empty, (g - 1) & 1);
@@ -285,7 +333,10 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         }
         tc_commit(&empty[s]);
         tc_commit(&a_empty[b]);
-        if (last_in_group) tc_commit(d_full);
+        if (last_in_group) {
+          tc_commit(d_full);
+          ++g;
+        }
       }
     }
   } else {
@@ -293,40 +344,59 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     const int lg = warp & 3;           // TMEM lane group
     const int half = warp >> 2;        // chunk columns [CPT*half, CPT*half + CPT)
     const int row = lg * 32 + lane;    // row within the tile == TMEM lane
-    const int er = tile * TBM + row;
-    const int er_c = er < a.R ? er : 0;
-    const int gi = a.row_idx ? a.row_idx[er_c] : a.r0 + er_c;
+    // per-row-tile state (reloaded when a stream-K CTA moves to the next tile)
+    int er = 0, er_c = 0, gi = 0;
+#if !GPK_EVAL_F32X2
+    static_assert(!GRAM, "the Gram-form operator needs the FP32x2 evaluation loop");
     float4 xi[DP4];
-    const float* xrow = (a.xs_rows ? a.xs_rows : a.xs) + static_cast<size_t>(gi) * DP;
-#pragma unroll
-    for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(xrow) + u);
-#if GPK_EVAL_F32X2
+#else
     // Gram form (image width >= 24, i.e. d >= 21): the row keeps (-2 x_i, 1) and
     // |x_i|^2 seeds the accumulator, so r^2 = |x_i|^2 + |x_c|^2 - 2 x_i.x_c is
     // one FFMA2 per two padded dimensions (x_c's image carries |x_c|^2 in slot d)
-    float ni = 0.f;
-    if constexpr (GRAM) {
-#pragma unroll
-      for (int u = 0; u < DP4; ++u) gram_row(xi[u], 4 * u, a.d, ni);
-    }
     uint64_t xi2[2 * DP4];
-#pragma unroll
-    for (int u = 0; u < DP4; ++u) {
-      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(xi[u].x), "f"(xi[u].y));
-      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(xi[u].z), "f"(xi[u].w));
-    }
-    uint64_t acc_seed;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
-#else
-    static_assert(!GRAM, "the Gram-form operator needs the FP32x2 evaluation loop");
+    uint64_t acc_seed = 0ull;
 #endif
-    const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
-    double* part = a.part + static_cast<size_t>(split) * a.R * a.m;
-    constexpr int DCOLS = NPAD / (EW / 4);  // D columns this thread drains
+    double* part = nullptr;
     bool wrote = false;
+    auto setup_rows = [&](int t) {
+      er = t * TBM + row;
+      er_c = er < a.R ? er : 0;
+      gi = a.row_idx ? a.row_idx[er_c] : a.r0 + er_c;
+      const float* xrow = (a.xs_rows ? a.xs_rows : a.xs) + static_cast<size_t>(gi) * DP;
+#if GPK_EVAL_F32X2
+      float4 xi[DP4];
+#endif
+#pragma unroll
+      for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+#if GPK_EVAL_F32X2
+      float ni = 0.f;
+      if constexpr (GRAM) {
+#pragma unroll
+        for (int u = 0; u < DP4; ++u) gram_row(xi[u], 4 * u, a.d, ni);
+      }
+#pragma unroll
+      for (int u = 0; u < DP4; ++u) {
+        asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(xi[u].x), "f"(xi[u].y));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(xi[u].z), "f"(xi[u].w));
+      }
+      asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
+#endif
+      // partial slot: the split, or this CTA's position among the tile's stream-K workers
+      const long long slot = SK ? blockIdx.x - sk_first(t, Q, gridDim.x, U) : split;
+      part = a.part + static_cast<size_t>(slot) * a.R * a.m;
+      wrote = false;
+    };
+    if (!SK) setup_rows(tile);
+    const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
+    constexpr int DCOLS = NPAD / (EW / 4);  // D columns this thread drains
+    int g = 0;  // accumulation groups drained
 
-    for (int k = 0; k < nq; ++k) {
+    Walk w = walk_begin();
+    for (int k = 0; k < nk; ++k, walk_next(w)) {
       const int s = k % STAGES, b = k % NAB;
+      const int q = w.q;
+      const bool last_in_group = w.last;
+      if (SK && (k == 0 || q == 0)) setup_rows(w.t);
       mbar_wait(&full[s], (k / STAGES) & 1);
       if (k >= NAB) mbar_wait(&a_empty[b], ((k - NAB) / NAB) & 1);
       tc_fence_after();
@@ -381,7 +451,7 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
       if constexpr (GRAM) {
         // the Gram form leaves O(ulp |x|^2) on the kernel diagonal: pin k(x_i, x_i)
         // to the direct form's value (rare chunks, warp-uniform branch)
-        const int cbase = c0 + cb + k * TBK + half * CPT;
+        const int cbase = c0 + q * TBK + half * CPT;
         const bool hit = !a.xs_rows && er < a.R && static_cast<unsigned>(gi - cbase) < static_cast<unsigned>(CPT);
         if (__any_sync(0xffffffffu, hit)) gram_pin_diagonal<CPT>(hit, gi - cbase, a.log2_s2, hi, lo);
       }
@@ -398,10 +468,9 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[b]);
 
-      const bool last_in_group = ((k + 1) % flush) == 0 || k + 1 == nq;
       if (last_in_group) {
-        const int g = k / flush;
         mbar_wait(d_full, g & 1);
+        ++g;
         tc_fence_after();
         if constexpr (FUSED) {
           // single accumulation group (host guarantees): D holds the whole slab
@@ -432,12 +501,11 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         if (lane == 0) mbar_arrive(d_empty);
       }
     }
-    if (nq == 0 && er < a.R) {  // empty split: zero partial
+    if (!SK && nq == 0 && er < a.R) {  // empty split: zero partial
       double* prow = part + static_cast<size_t>(er) * a.m;
       for (int col = half * DCOLS; col < min(a.m, (half + 1) * DCOLS); ++col) prow[col] = 0.0;
     }
   }
-  (void)ngroups;
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -502,7 +570,7 @@ void launch_tc_one(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cud
                                   static_cast<int>(smem)));
     configured = true;
   }
-  dim3 grid((a.R + TBM - 1) / TBM, a.splits);
+  const dim3 grid = MODE == 3 ? dim3(a.sk_ctas) : dim3((a.R + TBM - 1) / TBM, a.splits);
   kv_tc_kernel<NPAD, DP4, MODE><<<grid, TcRoles<MODE>::THREADS, smem, s>>>(a, vpk, f);
   check_launch("kv_tc_kernel");
 }
@@ -555,9 +623,11 @@ void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_ma
   check_launch("kv_pack_kernel");
 }
 
-void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s, bool deep) {
+void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s, int mode) {
   const KvReduceArgs none{};
-  if (deep)
+  if (mode == 3)
+    launch_tc<3>(a, vpk, none, s);
+  else if (mode == 2)
     launch_tc<2>(a, vpk, none, s);
   else
     launch_tc<0>(a, vpk, none, s);

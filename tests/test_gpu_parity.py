@@ -414,3 +414,19 @@ def test_init_heuristic_matches_oracle(G, gpk_ctx, oracle):
     whole = G.gpiter.init_heuristic(gpk_ctx, X[:150], y[:150], 1, 150, 7, 10, 0.1)
     _, raw = oracle.optimise_exact(X[:150], y[:150], 10, 0.1)
     assert np.max(np.abs(whole - [oracle.softplus(v) for v in raw])) <= 1e-8
+
+
+@pytest.mark.parametrize("n,d,m", [(4096, 26, 65), (2100, 3, 17)])
+def test_apply_streamk_matches_oracle(G, oracle, n, d, m, monkeypatch):
+    """The stream-K operator launch (GPK_KV_STREAMK=1, deep mode forced): one
+    persistent CTA per SM over (row tile, chunk) units, partial slots per tile."""
+    monkeypatch.setenv("GPK_KV_STREAMK", "1")
+    monkeypatch.setenv("GPK_KV_DEEP", "1")
+    ctx = G.Context(0)
+    X, _ = gp_problem(n, d, 77 + n)
+    raw = default_test_raw(d, oracle)
+    V = np.asfortranarray(np.random.default_rng(n).standard_normal((n, m)))
+    got = make_op(G, ctx, X, raw).apply(V)
+    ctx.close()
+    ref = oracle.apply(X, raw, V, threads=8)
+    assert colrel(got, ref) <= OP_TOL
