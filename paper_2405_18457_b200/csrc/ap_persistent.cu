@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   uint64_t* d_empty = d_full + 1;
   uint64_t* r_full = d_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + 3);
+  uint64_t* p_full = d_full + 4;  // tile partials staged for the last CTA's reduction
   double* red = reinterpret_cast<double*>(bars + 32);  // [4][NPAD]
   double* rd = red + 4 * NPAD;                           // [NQ][128]
   double* ssc = rd + NQ * 128;                           // [8]
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     mbar_init(d_full, 1);
     mbar_init(d_empty, EW);
     mbar_init(r_full, 1);
+    mbar_init(p_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     sh[0] = *a.sel;
     sh[1] = a.ctl->stop;
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
   const float sigma2f = static_cast<float>(a.sigma2);
   int kg = 0;  // chunk counter across iterations (pipeline phases)
+  int pphase = 0;  // uses of p_full (this CTA was last)
   int it = 0;
   int iters = sh[2];
   const int block = a.block, img = a.npad * 32;
@@ -455,6 +458,11 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     if (tid == 0) iters += 1;  // every CTA counts iterations (budget test)
     __syncthreads();
     if (tid == 0) {
+      if (a.prof && it <= 64) {  // development timeline: ticket time of every CTA (globaltimer)
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        a.prof[16 + (it - 1) * 160 + tile] = gt;
+      }
       __threadfence();
       const unsigned t = atomicAdd(a.gbar + 1, 1u);
       sh[3] = (t == nctas * static_cast<unsigned>(it) - 1u) ? 1 : 0;
@@ -463,11 +471,38 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     mark(3);
     if (sh[3]) {
       __threadfence();
-      // one round of loads: thread (j, p) = (tid / 8, tid % 8) sums column j of
-      // the tile partials over tiles p, p + 8, ... then a fixed xor-4/2/1 tree;
-      // thread k < nblocks sums block k's score partials in order
-      {
-        const int G = static_cast<int>(nctas);
+      // thread (j, p) = (tid / 8, tid % 8) sums column j of the tile partials
+      // over tiles p, p + 8, ... then a fixed xor-4/2/1 tree; thread k < nblocks
+      // sums block k's score partials in order. The partials arrive by one bulk
+      // copy into the idle pipeline buffers when they fit, else as one round of
+      // loads per thread (same order either way).
+      const int G = static_cast<int>(nctas);
+      const uint32_t pbytes = static_cast<uint32_t>(G) * m * 8u;
+      const bool staged = pbytes <= (L::RING_FLOATS + STAGES * TBK * DP) * 4u && (pbytes % 16u) == 0u;
+      if (staged) {
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // other CTAs' generic writes -> bulk read
+          mbar_expect_tx(p_full, pbytes);
+          bulk_g2s(smB, a.dpart, pbytes, p_full);
+        }
+        double sp[4] = {0.0, 0.0, 0.0, 0.0};  // gpb <= 4 (ap_persistent_supported)
+        if (tid < a.nblocks) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < a.gpb) sp[q] = __ldcg(a.spart + static_cast<size_t>(tid) * a.gpb + q);
+        }
+        mbar_wait(p_full, pphase & 1);
+        const double* st = reinterpret_cast<const double*>(smB);
+        const int j = tid >> 3, p = tid & 7;
+        double acc = 0.0;
+        if (j < m)
+          for (int q = p; q < G; q += 8) acc += st[static_cast<size_t>(q) * m + j];
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (p == 0 && j < m) ss[j] = sqrt(acc) / a.scales[j];
+        if (tid < a.nblocks) bscore[tid] = sqrt(((sp[0] + sp[1]) + sp[2]) + sp[3]);
+      } else {
         constexpr int QH = 10;  // 2 x 10 x 8 >= 148 tiles (ap_persistent_supported)
         const int j = tid >> 3, p = tid & 7;
         double v[QH];
@@ -500,6 +535,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         if (p == 0 && j < m) ss[j] = sqrt(acc) / a.scales[j];
         if (tid < a.nblocks) bscore[tid] = sqrt(((sp[0] + sp[1]) + sp[2]) + sp[3]);
       }
+      if (staged) ++pphase;
       __syncthreads();
       if (warp == 0) {
         // probe mean over columns 1..m-1 and the first maximal block score
@@ -544,6 +580,11 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
       }
       __syncthreads();
       if (tid == 0) {
+        if (a.prof && it <= 64) {
+          unsigned long long gt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          a.prof[16 + (it - 1) * 160 + 159] = gt;
+        }
         __threadfence();
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.gbar + 2), "r"(static_cast<unsigned>(it)) : "memory");
       }

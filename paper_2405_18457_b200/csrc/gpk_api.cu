@@ -176,6 +176,7 @@ struct gpk_batch {
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
   DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
   DBuf<double> ap_cpart;             // persistent AP: block-update partials [8][block][m]
+  DBuf<unsigned long long> ap_prof;  // persistent AP development phase clock (GPK_AP_PROF)
   // CUDA graph of the AP block build + inverse (ap_prepare), keyed on its buffers
   cudaGraphExec_t ap_graph = nullptr;
   std::array<const void*, 6> ap_graph_key{};
@@ -1362,15 +1363,34 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     }
     static const bool phase_clock = std::getenv("GPK_AP_PROF") != nullptr;  // development: phase split
     if (phase_clock) {
-      pa.prof = reinterpret_cast<unsigned long long*>(b->gbar.p + 8);
-      GPK_CUDA(cudaMemsetAsync(pa.prof, 0, 10 * sizeof(unsigned long long), s));
+      pa.prof = b->ap_prof.ensure(16 + 64 * 160);
+      GPK_CUDA(cudaMemsetAsync(pa.prof, 0, (16 + 64 * 160) * sizeof(unsigned long long), s));
     }
     ap_persistent_launch(pa, s);
     if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
     GPK_CUDA(cudaStreamSynchronize(s));
     if (phase_clock) {
-      unsigned long long h[10];
-      GPK_CUDA(cudaMemcpy(h, pa.prof, sizeof(h), cudaMemcpyDeviceToHost));
+      std::vector<unsigned long long> hv(16 + 64 * 160);
+      GPK_CUDA(cudaMemcpy(hv.data(), pa.prof, hv.size() * 8, cudaMemcpyDeviceToHost));
+      const unsigned long long* h = hv.data();
+      {  // ticket spread (first ticket -> last ticket) and last ticket -> decision release, ns
+        double spread = 0, rel = 0;
+        int cnt = 0;
+        for (int it = 0; it < 64 && it < static_cast<int>(h[9]); ++it) {
+          const unsigned long long* row = h + 16 + it * 160;
+          unsigned long long lo = ~0ull, hi = 0;
+          for (int c = 0; c < (n + 127) / 128; ++c) {
+            lo = std::min(lo, row[c]);
+            hi = std::max(hi, row[c]);
+          }
+          if (row[159] == 0 || lo == 0) continue;
+          spread += static_cast<double>(hi - lo);
+          rel += static_cast<double>(row[159] - hi);
+          ++cnt;
+        }
+        if (cnt) std::fprintf(stderr, "ap_persistent tickets: spread %.2f us, last ticket -> release %.2f us\n",
+                              spread / cnt / 1e3, rel / cnt / 1e3);
+      }
       const double it = static_cast<double>(h[9]) * 1.9e3;  // cycles -> us at ~1.9 GHz
       std::fprintf(stderr,
                    "ap_persistent phases (us/iteration at 1.9 GHz, %llu iterations): C1load %.2f C1 %.2f Csync %.2f C2 %.2f sync1 %.2f "
