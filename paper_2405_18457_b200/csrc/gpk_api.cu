@@ -18,6 +18,7 @@
 #include <numeric>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gpk.h"
@@ -41,6 +42,66 @@ struct OutOfRange : std::out_of_range {
   using std::out_of_range::out_of_range;
 };
 
+// Device buffers come from the device's default stream-ordered pool with an
+// unbounded release threshold: freed blocks stay mapped and are handed to the
+// next allocation of the process, so creating / destroying operators, batches
+// and optimisers (every gpk_optimise call) costs no cudaMalloc/cudaFree
+// page-table work. A free first waits for the device (the old cudaFree's
+// implicit synchronisation, without the unmap), an allocation is ordered on
+// the legacy stream and waited for, so no stream ever touches a block another
+// stream still uses. GPK_DEVICE_POOL=0 restores cudaMalloc/cudaFree.
+bool device_pool_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GPK_DEVICE_POOL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+// Tensor-core Gram distances for d >= GPK_TGRAM_MIN_D (default 21: measured
+// C2 d = 26 full product -5%; d = 11 +15%, d = 20 +1% on one B200);
+// GPK_TGRAM=0 keeps the FP32 distance loops everywhere.
+bool tg_enabled(int d) {
+  static const int min_d = [] {
+    const char* e = std::getenv("GPK_TGRAM");
+    if (e && std::atoi(e) == 0) return 1 << 30;
+    const char* m = std::getenv("GPK_TGRAM_MIN_D");
+    return m ? std::atoi(m) : 21;
+  }();
+  return d >= min_d && d <= 32;
+}
+
+void* device_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (!device_pool_enabled()) {
+    GPK_CUDA(cudaMalloc(&p, bytes));
+    return p;
+  }
+  static std::array<bool, 64> configured{};
+  int dev = 0;
+  GPK_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !configured[dev]) {
+    cudaMemPool_t pool;
+    GPK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;
+    GPK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured[dev] = true;
+  }
+  GPK_CUDA(cudaMallocAsync(&p, bytes, 0));
+  GPK_CUDA(cudaStreamSynchronize(0));
+  return p;
+}
+
+void device_free(void* p) {
+  if (!p) return;
+  if (!device_pool_enabled()) {
+    cudaFree(p);
+    return;
+  }
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, 0);
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -48,14 +109,12 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() {
-    if (p) cudaFree(p);
-  }
+  ~DBuf() { device_free(p); }
   T* ensure(size_t count) {
     if (count > cap) {
-      if (p) cudaFree(p);
+      device_free(p);
       p = nullptr;
-      GPK_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+      p = static_cast<T*>(device_alloc(std::max<size_t>(count, 1) * sizeof(T)));
       cap = count;
     }
     return p;
@@ -129,6 +188,8 @@ struct gpk_operator {
   DBuf<double> x64;       // [n][d] unscaled
   DBuf<float> xs32;       // [n][dp]
   int dpg = 0;            // Gram image width (gram_dp(d)); 0: direct-difference operator
+  bool tg = false;        // tensor-core Gram distances in the tcgen05 operator (tg_enabled)
+  DBuf<float> xtg;        // their column images (tg_image_launch), rebuilt with the scaled inputs
   DBuf<float> xg32;       // [n + 128][dpg] (x, |x|^2, 0...) for the tensor-core operator
   DBuf<double> xs64;      // [n][d]
   DBuf<double> inv_ls_dev;
@@ -320,6 +381,7 @@ void set_hyper(gpk_operator* op, const double* raw) {
   GPK_CUDA(cudaMemcpyAsync(op->hyp_dev.ensure(2), hv, sizeof(hv), cudaMemcpyHostToDevice, s));
   prescale_launch(op->x64.p, op->n, d, op->dp, il, op->xs32.p, op->xs64.p, s);
   if (op->dpg) gram_image_launch(op->xs32.p, op->n, d, op->dp, op->dpg, op->xg32.p, s);
+  if (op->tg) tg_image_launch(op->xs32.p, op->n, d, op->dp, op->xtg.p, s);
   GPK_CUDA(cudaStreamSynchronize(s));  // inv_ls host buffer lifetime
 }
 
@@ -400,8 +462,10 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   }
   double* part = op->part.ensure(static_cast<size_t>(splits) * c.R * c.m);
   KvArgs a{};
-  // tensor-core kernels: Gram-form distances for d >= 21 (image width >= 24)
-  const bool gram = tc && op->dpg > 0;
+  // tensor-core Gram distances (whole 32-column chunks from column c0)
+  const bool tgram = tc && op->tg && (deep || fused) && !streamk && (c.sel ? c.sel_block % 32 == 0 : c.c0 % 32 == 0);
+  // else FP32 Gram-form distances for d >= 21 (image width >= 24)
+  const bool gram = tc && !tgram && op->dpg > 0;
   if (gram && c.xs_rows && c.xs_rows != op->pts32.p) throw std::logic_error("run_kv: cross rows without a Gram image");
   a.xs = gram ? op->xg32.p : op->xs32.p;
   a.n = op->n;
@@ -425,6 +489,9 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.stats = op->ctx->stats;
   a.d = op->d;
   a.xs_rows = (gram && c.xs_rows) ? op->ptsg32.p : c.xs_rows;
+  a.xtg = tgram ? op->xtg.p : nullptr;
+  static const int kv_dbg = std::getenv("GPK_KV_DBG") ? std::atoi(std::getenv("GPK_KV_DBG")) : 0;
+  a.dbg = kv_dbg;
   a.sk_ctas = sk_G;
   gpk_ctx* ctx = op->ctx;
   if (c.vpk && !tc) throw InvalidArgument("gpk: pre-packed operator input needs the tcgen05 kernel");
@@ -1776,35 +1843,59 @@ void assemble(const std::vector<std::vector<double>>& f, int s_count, int P, dou
 }
 
 // ------------------------------------------------------------------ RFF
+// Normal draw i of RandomStream(seed, stream, substream) (rng.cpp:64-77):
+// draw pair q = i/2 takes u64 words 2q and 2q+1 of the Philox stream (block
+// q/2), Box-Muller returns the cosine first and the cached sine second. Same
+// arithmetic as the sequential stream, so any slice of a stream can be drawn
+// on its own (bit-identical to the sequential order).
+double gauss_at(uint64_t seed, uint64_t stream, uint64_t sub, uint64_t i) {
+  const uint64_t q = i >> 1;
+  const U64x4 blk = philox4x64(q >> 1, sub, 0, 0, seed, stream);
+  const int w = static_cast<int>(q & 1) * 2;
+  const double u1 = static_cast<double>((blk.v[w] >> 11) + 1) * 0x1.0p-53;
+  const double u2 = static_cast<double>(blk.v[w + 1] >> 11) * 0x1.0p-53;
+  const double radius = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * 3.141592653589793 * u2;
+  return (i & 1) ? radius * std::sin(angle) : radius * std::cos(angle);
+}
+
+// runs body(lo, hi) over [0, count) on up to 16 host threads
+template <class F>
+void host_parallel(size_t count, size_t min_per_thread, F body) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t T = std::max<size_t>(1, std::min<size_t>(hw, count / std::max<size_t>(min_per_thread, 1)));
+  if (T == 1) {
+    body(size_t{0}, count);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < T; ++t) pool.emplace_back([&, t] { body(count * t / T, count * (t + 1) / T); });
+  body(size_t{0}, count / T);
+  for (auto& th : pool) th.join();
+}
+
 void build_basis_host(gpk_rff_basis* b) {  // rff.cpp:10-34
   const int P = b->pairs, d = b->d, S = b->samples;
   b->freq.assign(static_cast<size_t>(P) * d, 0.0);
-  HostStream fs(b->seed, 3, b->substream);
-  auto gauss = [](HostStream& st) -> double {
-    if (st.has_cached) {
-      st.has_cached = false;
-      return st.cached;
+  // frequency row p consumes normals [p(3+d), (p+1)(3+d)) of stream kFrequencies:
+  // three for the chi-square scale, then d directions
+  host_parallel(static_cast<size_t>(P), 64, [&](size_t lo, size_t hi) {
+    for (size_t p = lo; p < hi; ++p) {
+      const uint64_t base = static_cast<uint64_t>(p) * (3 + d);
+      double chi2 = 0.0;
+      for (int i = 0; i < 3; ++i) {
+        const double g = gauss_at(b->seed, 3, b->substream, base + i);
+        chi2 += g * g;
+      }
+      const double scale = std::sqrt(3.0 / chi2);
+      for (int k = 0; k < d; ++k)
+        b->freq[static_cast<size_t>(k) * P + p] = scale * gauss_at(b->seed, 3, b->substream, base + 3 + k);
     }
-    const double u1 = static_cast<double>((st.next_u64() >> 11) + 1) * 0x1.0p-53;
-    const double u2 = static_cast<double>(st.next_u64() >> 11) * 0x1.0p-53;
-    const double radius = std::sqrt(-2.0 * std::log(u1));
-    const double angle = 2.0 * 3.141592653589793 * u2;
-    st.cached = radius * std::sin(angle);
-    st.has_cached = true;
-    return radius * std::cos(angle);
-  };
-  for (int p = 0; p < P; ++p) {
-    double chi2 = 0.0;
-    for (int i = 0; i < 3; ++i) {
-      const double g = gauss(fs);
-      chi2 += g * g;
-    }
-    const double scale = std::sqrt(3.0 / chi2);
-    for (int k = 0; k < d; ++k) b->freq[static_cast<size_t>(k) * P + p] = scale * gauss(fs);
-  }
+  });
   b->weights.assign(static_cast<size_t>(2 * P) * S, 0.0);
-  HostStream ws(b->seed, 4, b->substream);
-  for (auto& w : b->weights) w = gauss(ws);
+  host_parallel(b->weights.size(), 4096, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) b->weights[i] = gauss_at(b->seed, 4, b->substream, i);
+  });
 }
 
 // prior (row-major [rows][s]) = F W: FP64 feature rows (rff_features_kernel)
@@ -2111,6 +2202,8 @@ gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d,
     op->xs32.ensure(static_cast<size_t>(n + 128) * op->dp);
     GPK_CUDA(cudaMemsetAsync(op->xs32.p, 0, sizeof(float) * (n + 128) * op->dp, ctx->stream));
     op->xs64.ensure(static_cast<size_t>(n) * d);
+    op->tg = tg_enabled(d);
+    if (op->tg) op->xtg.ensure(tg_image_floats(n, d));
     op->dpg = gram_dp(d);
     if (op->dpg) {
       op->xg32.ensure(static_cast<size_t>(n + 128) * op->dpg);

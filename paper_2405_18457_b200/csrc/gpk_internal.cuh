@@ -60,6 +60,8 @@ struct KvArgs {
   double* stats;       // device counters [evals x RHS, algorithmic flops] or null
   int d;               // true input dimension (flop accounting)
   const float* xs_rows;  // scaled FP32 inputs of the rows (cross kernel k(P, X)); null: xs
+  int dbg;               // development: bit0 KV hi.hi only, bit1 Gram hi.hi only (GPK_KV_DBG)
+  const float* xtg;      // tensor-core Gram column images (tg_image_kernel) or null; needs c0 % 32 == 0
 };
 int kv_tc_for(int m);        // columns-per-lane template parameter for m
 int kv_ld_for(int m);        // FP32 RHS leading dimension for m
@@ -140,6 +142,8 @@ struct KvReduceArgs {
   double* ap_upd;
 };
 void kv_reduce_launch(const KvReduceArgs& a, cudaStream_t s);
+// tensor-core Gram-distance operator kernels (kv_tc_tg.cu); mode as kv_tc_launch, 1 = fused AP slab
+void kv_tc_tg_launch(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s, int mode);
 
 // ---- gradient pass (K4) ---------------------------------------------------
 struct GradArgs {
@@ -218,6 +222,11 @@ void prescale_launch(const double* x64, int n, int d, int dp, const double* inv_
                      double* xs64, cudaStream_t s);
 // Gram-form operator image (x, |x|^2, 0...) [n][dpg] for d >= 21 (la_kernels.cu)
 void gram_image_launch(const float* xs32, int n, int d, int dp, int dpg, float* xg, cudaStream_t s);
+// tensor-core Gram column images (kv_tc_kernel TG): per 32-column chunk
+// [B hi | B lo] (-2 x', canonical K-major TF32 images, K = kg) and |x'|^2
+int tg_kg(int d);
+size_t tg_image_floats(int n, int d);
+void tg_image_launch(const float* xs32, int n, int d, int dp, float* xtg, cudaStream_t s);
 // tensor-core operator kernels take the Gram image for d in [8, 31]
 #ifndef GPK_GRAM
 #define GPK_GRAM 1  // build-time A/B switch (make NVEXTRA=-DGPK_GRAM=0): direct differences everywhere

@@ -164,21 +164,43 @@ struct TcRoles {
   static constexpr int CPT = TBK * 4 / EW;            // chunk columns per eval thread
 };
 
-template <int NPAD, int DP4, int MODE>
+// TG: tensor-core Gram distances. Per 32-column chunk one more set of
+// tcgen05 MMAs computes G = -2 X_rows X_c^T (3xTF32: hi.lo + lo.hi + hi.hi,
+// M = 128, N = 32, K = KG = 8 ceil(d / 8)) into TMEM columns [TG_COL, +32);
+// the evaluation warps read their row's G (one tcgen05.ld per chunk) and form
+// r^2 = (|x_i|^2 + |x_c|^2) + G with the norms of the same 22-bit split
+// coordinates in FP32, so the per-entry FP32 work is the Matern profile only.
+// A operand: the tile's rows as TF32 hi / lo images in TMEM (written by the
+// eval warps when a tile starts; A in shared memory would cost the MMA a
+// 4 KB operand read per K step); B operand + column norms: per-chunk
+// images built once per hyperparameter set (tg_image_kernel), bulk-copied
+// with the V chunk.
+constexpr int TG_COL = 96;   // TMEM column of the Gram tile (D uses [0, NPAD <= 80))
+constexpr int TGA_COL = 384; // TMEM columns of the row images hi | lo (KG each), behind 4 A buffers
+template <int DP4>
+struct TgShape {
+  static constexpr int KG = ((DP4 + 1) / 2) * 8;  // K of the Gram MMAs (multiple of 8, >= 4 DP4)
+  static constexpr int CHUNK = 2 * TBK * KG + TBK;  // floats per column chunk: B hi | B lo | |x_c|^2
+};
+
+template <int NPAD, int DP4, int MODE, bool TG>
 __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     kv_tc_kernel(const KvArgs a, const float* __restrict__ vpk, const KvReduceArgs f) {
   constexpr bool FUSED = MODE == 1, DEEP = MODE != 0, SK = MODE == 3;
+  static_assert(!(TG && (SK || MODE == 0)), "tensor-core Gram distances: one row tile per CTA, 512 TMEM columns");
   constexpr int EW = TcRoles<MODE>::EW, CPT = TcRoles<MODE>::CPT;
   constexpr int DP = 4 * DP4;
-  constexpr bool GRAM = GPK_GRAM && DP4 >= 6;  // image (x, |x|^2, 0...): host passes it for d >= 21
+  constexpr bool GRAM = !TG && GPK_GRAM && DP4 >= 6;  // image (x, |x|^2, 0...): host passes it for d >= 21
+  constexpr int KG = TgShape<DP4>::KG;
+  constexpr int XST = TG ? TgShape<DP4>::CHUNK : TBK * DP;  // floats of column data per stage
   using L = TcLayout<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the fused AP slab runs one CTA per SM: 4 TMEM A buffers (512 columns)
   constexpr int NAB = DEEP ? 4 : 2;
   constexpr int TCOLS = DEEP ? 512 : TMEM_COLS;
   float* smB = reinterpret_cast<float*>(smem_raw);                    // [STAGES][CHUNK_FLOATS]
-  float* smX = smB + STAGES * L::CHUNK_FLOATS;                        // [STAGES][TBK][DP]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * TBK * DP);
+  float* smX = smB + STAGES * L::CHUNK_FLOATS;                        // [STAGES][XST]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * XST);
   uint64_t* full = bars;              // [STAGES]
   uint64_t* empty = bars + STAGES;    // [STAGES]
   uint64_t* a_full = bars + 2 * STAGES;         // [NAB]
@@ -187,6 +209,9 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   uint64_t* d_empty = bars + 2 * STAGES + 9;
   uint64_t* base_full = bars + 2 * STAGES + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 11);
+  uint64_t* g_full = bars + 2 * STAGES + 12;     // TG: Gram tile of the chunk in TMEM
+  uint64_t* g_empty = bars + 2 * STAGES + 13;    // TG: eval warps have read it
+  uint64_t* arow_full = bars + 2 * STAGES + 14;  // TG: row images written
 
   if (a.skip && *a.skip) return;
   int c0 = a.c0, C = a.C;
@@ -264,6 +289,11 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     mbar_init(d_full, 1);
     mbar_init(d_empty, EW);
     if (FUSED) mbar_init(base_full, 1);  // base tile landed
+    if (TG) {
+      mbar_init(g_full, 1);
+      mbar_init(g_empty, EW);
+      mbar_init(arow_full, 4);  // the four eval warps of chunk-column group 0 own the 128 rows
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -299,23 +329,58 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         const int s = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[s], ((k - STAGES) / STAGES) & 1);
         const int chunk = w.q;
-        const uint32_t xbytes = TBK * DP * 4;
+        const uint32_t xbytes = XST * 4;
         mbar_expect_tx(&full[s], L::CHUNK_BYTES + xbytes);
         bulk_g2s(smB + s * L::CHUNK_FLOATS, vpk + static_cast<size_t>(chunk) * L::CHUNK_FLOATS, L::CHUNK_BYTES,
                  &full[s]);
-        bulk_g2s(smX + s * TBK * DP, a.xs + static_cast<size_t>(c0 + chunk * TBK) * DP, xbytes, &full[s]);
+        if constexpr (TG)  // host guarantees c0 % TBK == 0
+          bulk_g2s(smX + s * XST, a.xtg + static_cast<size_t>(c0 / TBK + chunk) * XST, xbytes, &full[s]);
+        else
+          bulk_g2s(smX + s * XST, a.xs + static_cast<size_t>(c0 + chunk * TBK) * DP, xbytes, &full[s]);
       }
     }
   } else if (warp == EW + 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+      // TG: G(k) = -2 X_rows X_c(k)^T, the cross terms first and hi.hi last
+      // (truncating accumulation: the small terms go in while D is small)
+      auto gram_mma = [&](int k) {
+        const int s = k % STAGES;
+        const uint32_t ah = tmem + TGA_COL, al = ah + KG;
+        const uint32_t bh = smem_u32(smX + s * XST), bl = bh + TBK * KG * 4;
+        constexpr uint32_t gdesc = tf32_idesc(TBK, TBM);
+        constexpr uint32_t SBO = (KG / 4) * 128;
+        if (!(a.dbg & 2))
+#pragma unroll
+        for (int ks = 0; ks < KG / 8; ++ks) {
+          tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
+          tc_mma_tf32(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+        }
+#pragma unroll
+        for (int ks = 0; ks < KG / 8; ++ks)
+          tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc,
+                      ((a.dbg & 2) && ks == 0) ? 0u : 1u);
+        tc_commit(g_full);
+      };
+      if (TG && nk > 0) {
+        mbar_wait(arow_full, 0);
+        mbar_wait(&full[0], 0);
+        tc_fence_after();
+        gram_mma(0);
+      }
       int g = 0;  // accumulation groups issued
       Walk w = walk_begin();
       for (int k = 0; k < nk; ++k, walk_next(w)) {
         const int s = k % STAGES, b = k % NAB;
         const bool first_in_group = w.first, last_in_group = w.last;
         mbar_wait(&full[s], (k / STAGES) & 1);
+        if (TG && k + 1 < nk) {  // next chunk's Gram tile once the eval warps hold this one's
+          mbar_wait(&full[(k + 1) % STAGES], ((k + 1) / STAGES) & 1);
+          mbar_wait(g_empty, k & 1);
+          tc_fence_after();
+          gram_mma(k + 1);
+        }
         mbar_wait(&a_full[b], (k / NAB) & 1);
         if (first_in_group && g > 0) mbar_wait(d_empty, (g - 1) & 1);
         tc_fence_after();
@@ -328,8 +393,10 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
           const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
           const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
           tc_mma_tf32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
-          tc_mma_tf32(tmem, ah + kk * 8, dl, idesc, 1u);
-          tc_mma_tf32(tmem, al + kk * 8, dh, idesc, 1u);
+          if (!(a.dbg & 1)) {
+            tc_mma_tf32(tmem, ah + kk * 8, dl, idesc, 1u);
+            tc_mma_tf32(tmem, al + kk * 8, dh, idesc, 1u);
+          }
         }
         tc_commit(&empty[s]);
         tc_commit(&a_empty[b]);
@@ -358,6 +425,7 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
 #endif
     double* part = nullptr;
     bool wrote = false;
+    float tg_ni = 0.f;  // TG: |x_i|^2 of the split coordinates
     auto setup_rows = [&](int t) {
       er = t * TBM + row;
       er_c = er < a.R ? er : 0;
@@ -368,18 +436,55 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
 #endif
 #pragma unroll
       for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+      if constexpr (TG) {
+        // row images for the Gram MMAs (canonical K-major no-swizzle layout:
+        // element (row, k) at ((row/8) (KG/4) + k/4) 32 + (row%8) 4 + k%4)
+        float hv[4 * DP4], lv[4 * DP4];
+        float ni = 0.f;
+#pragma unroll
+        for (int u = 0; u < DP4; ++u) {
+          const float* c = reinterpret_cast<const float*>(&xi[u]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            tg_split(c[e], hv[4 * u + e], lv[4 * u + e]);
+            ni = tg_norm_step(ni, hv[4 * u + e], lv[4 * u + e]);
+          }
+        }
+        tg_ni = ni;
+        if (half == 0) {  // this warp's 32 rows (TMEM lanes) of the hi | lo row images
+          const uint32_t ta = tmem + (static_cast<uint32_t>(lg * 32) << 16) + TGA_COL;
+#pragma unroll
+          for (int k8 = 0; k8 < KG / 8; ++k8) {
+            uint32_t hw[8], lw[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int k = 8 * k8 + e;
+              hw[e] = k < 4 * DP4 ? __float_as_uint(hv[k]) : 0u;
+              lw[e] = k < 4 * DP4 ? __float_as_uint(lv[k]) : 0u;
+            }
+            tc_st8(ta + 8 * k8, hw);
+            tc_st8(ta + KG + 8 * k8, lw);
+          }
+          tc_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(arow_full);
+        }
+      }
 #if GPK_EVAL_F32X2
       float ni = 0.f;
       if constexpr (GRAM) {
 #pragma unroll
         for (int u = 0; u < DP4; ++u) gram_row(xi[u], 4 * u, a.d, ni);
       }
+      if constexpr (!TG) {
 #pragma unroll
-      for (int u = 0; u < DP4; ++u) {
-        asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(xi[u].x), "f"(xi[u].y));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(xi[u].z), "f"(xi[u].w));
+        for (int u = 0; u < DP4; ++u) {
+          asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(xi[u].x), "f"(xi[u].y));
+          asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(xi[u].z), "f"(xi[u].w));
+        }
+        asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
       }
-      asm("mov.b64 %0, {%1, %2};" : "=l"(acc_seed) : "f"(ni), "f"(0.f));
 #endif
       // partial slot: the split, or this CTA's position among the tile's stream-K workers
       const long long slot = SK ? blockIdx.x - sk_first(t, Q, gridDim.x, U) : split;
@@ -400,10 +505,40 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
       mbar_wait(&full[s], (k / STAGES) & 1);
       if (k >= NAB) mbar_wait(&a_empty[b], ((k - NAB) / NAB) & 1);
       tc_fence_after();
-      const float* xc = smX + s * TBK * DP + half * CPT * DP;
+      const float* xc = smX + s * XST + half * CPT * DP;
       uint32_t hi[CPT], lo[CPT];
+      float tg_r2[TG ? CPT : 1];
+      if constexpr (TG) {
+        mbar_wait(g_full, k & 1);
+        tc_fence_after();
+        uint32_t gv[CPT];
+        if constexpr (CPT == 16)
+          tc_ld16(tmem + lane_addr + TG_COL + half * CPT, gv);
+        else
+          tc_ld8(tmem + lane_addr + TG_COL + half * CPT, gv);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(g_empty);
+        const float4* ncs = reinterpret_cast<const float4*>(smX + s * XST + 2 * TBK * KG + half * CPT);
+#pragma unroll
+        for (int t4 = 0; t4 < CPT / 4; ++t4) {
+          const float4 nc = ncs[t4];
+          tg_r2[4 * t4] = (tg_ni + nc.x) + __uint_as_float(gv[4 * t4]);
+          tg_r2[4 * t4 + 1] = (tg_ni + nc.y) + __uint_as_float(gv[4 * t4 + 1]);
+          tg_r2[4 * t4 + 2] = (tg_ni + nc.z) + __uint_as_float(gv[4 * t4 + 2]);
+          tg_r2[4 * t4 + 3] = (tg_ni + nc.w) + __uint_as_float(gv[4 * t4 + 3]);
+        }
+      }
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
+        if constexpr (TG) {
+        const float r = sqrt_approx(fmaxf(tg_r2[t], 0.f));
+        const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
+        hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
+        lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
+        continue;
+        }
 #if GPK_EVAL_F32X2
         // packed FP32x2 (FADD2/FFMA2): two dimensions per instruction
         const uint32_t xaddr = smem_u32(xc + t * DP);
@@ -448,7 +583,7 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
         lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
       }
-      if constexpr (GRAM) {
+      if constexpr (GRAM || TG) {
         // the Gram form leaves O(ulp |x|^2) on the kernel diagonal: pin k(x_i, x_i)
         // to the direct form's value (rare chunks, warp-uniform branch)
         const int cbase = c0 + q * TBK + half * CPT;
@@ -553,58 +688,75 @@ __global__ void kv_pack_kernel(const double* v64, const float* v32, int ldv, int
   }
 }
 
-template <int NPAD, int DP4, int MODE>
+template <int NPAD, int DP4, int MODE, bool TG>
 void launch_tc_one(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   constexpr bool FUSED = MODE == 1;
   using L = TcLayout<NPAD>;
+  constexpr int XST = TG ? TgShape<DP4>::CHUNK : TBK * 4 * DP4;
   // + the fused drain's scratch behind the barriers (bars + 64 words: ~14 KB)
-  const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * TBK * 4 * DP4) + 32 * sizeof(uint64_t) +
-                      (FUSED ? 64 * sizeof(uint64_t) + sizeof(double) * (FUSED_SCRATCH_DOUBLES + TBM * 96) : 0);
+  const size_t need = sizeof(float) * (STAGES * L::CHUNK_FLOATS + STAGES * XST) +
+                      32 * sizeof(uint64_t) +
+                      (FUSED ? 64 * sizeof(uint64_t) + sizeof(double) * (FUSED_SCRATCH_DOUBLES + TBM * ((a.m + 1) / 2 * 2)) : 0);
   // at most 2 CTAs per SM: each allocates 256 of the 512 TMEM columns
   // one CTA per SM in MODE 1/2 (512 TMEM columns each): >= 120 KB keeps a
   // second CTA off the SM; two per SM otherwise (256 columns each)
   const size_t smem = std::max<size_t>(need, MODE ? 120 * 1024 : 100 * 1024);
-  static bool configured = false;
-  if (!configured) {
-    GPK_CUDA(cudaFuncSetAttribute(kv_tc_kernel<NPAD, DP4, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (smem > 227 * 1024) throw std::invalid_argument("gpk: operator kernel shared memory exceeds 227 KB");
+  static size_t configured = 0;
+  if (smem > configured) {
+    configured = smem;
+    GPK_CUDA(cudaFuncSetAttribute(kv_tc_kernel<NPAD, DP4, MODE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    configured = true;
   }
   const dim3 grid = MODE == 3 ? dim3(a.sk_ctas) : dim3((a.R + TBM - 1) / TBM, a.splits);
-  kv_tc_kernel<NPAD, DP4, MODE><<<grid, TcRoles<MODE>::THREADS, smem, s>>>(a, vpk, f);
+  kv_tc_kernel<NPAD, DP4, MODE, TG><<<grid, TcRoles<MODE>::THREADS, smem, s>>>(a, vpk, f);
   check_launch("kv_tc_kernel");
 }
 
-template <int NPAD, int MODE>
+template <int NPAD, int MODE, bool TG>
 void launch_tc_n(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   switch (a.dp / 4) {
-    case 1: return launch_tc_one<NPAD, 1, MODE>(a, vpk, f, s);
-    case 2: return launch_tc_one<NPAD, 2, MODE>(a, vpk, f, s);
-    case 3: return launch_tc_one<NPAD, 3, MODE>(a, vpk, f, s);
-    case 4: return launch_tc_one<NPAD, 4, MODE>(a, vpk, f, s);
-    case 5: return launch_tc_one<NPAD, 5, MODE>(a, vpk, f, s);
-    case 6: return launch_tc_one<NPAD, 6, MODE>(a, vpk, f, s);
-    case 7: return launch_tc_one<NPAD, 7, MODE>(a, vpk, f, s);
-    case 8: return launch_tc_one<NPAD, 8, MODE>(a, vpk, f, s);
-    case 9: return launch_tc_one<NPAD, 9, MODE>(a, vpk, f, s);  // d = 32 Gram image
+    case 1: return launch_tc_one<NPAD, 1, MODE, TG>(a, vpk, f, s);
+    case 2: return launch_tc_one<NPAD, 2, MODE, TG>(a, vpk, f, s);
+    case 3: return launch_tc_one<NPAD, 3, MODE, TG>(a, vpk, f, s);
+    case 4: return launch_tc_one<NPAD, 4, MODE, TG>(a, vpk, f, s);
+    case 5: return launch_tc_one<NPAD, 5, MODE, TG>(a, vpk, f, s);
+    case 6: return launch_tc_one<NPAD, 6, MODE, TG>(a, vpk, f, s);
+    case 7: return launch_tc_one<NPAD, 7, MODE, TG>(a, vpk, f, s);
+    case 8: return launch_tc_one<NPAD, 8, MODE, TG>(a, vpk, f, s);
+    case 9:
+      if constexpr (!TG) return launch_tc_one<NPAD, 9, MODE, TG>(a, vpk, f, s);  // d = 32 Gram image
+      [[fallthrough]];
     default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
   }
 }
 
-template <int MODE>
+template <int MODE, bool TG>
 void launch_tc(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   switch (kv_tc_npad(a.m)) {
-    case 16: return launch_tc_n<16, MODE>(a, vpk, f, s);
-    case 32: return launch_tc_n<32, MODE>(a, vpk, f, s);
-    case 48: return launch_tc_n<48, MODE>(a, vpk, f, s);
-    case 64: return launch_tc_n<64, MODE>(a, vpk, f, s);
-    case 80: return launch_tc_n<80, MODE>(a, vpk, f, s);
+    case 16: return launch_tc_n<16, MODE, TG>(a, vpk, f, s);
+    case 32: return launch_tc_n<32, MODE, TG>(a, vpk, f, s);
+    case 48: return launch_tc_n<48, MODE, TG>(a, vpk, f, s);
+    case 64: return launch_tc_n<64, MODE, TG>(a, vpk, f, s);
+    case 80: return launch_tc_n<80, MODE, TG>(a, vpk, f, s);
     default: throw std::invalid_argument("gpk: tensor-core operator supports m <= 80");
   }
 }
 
 }  // namespace
 
+#if GPK_KV_TC_TG
+// tensor-core Gram variants (built in kv_tc_tg.cu: a second translation unit
+// keeps the two instantiation sets compiling in parallel)
+void kv_tc_tg_launch(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s, int mode) {
+  if (mode == 1)
+    launch_tc<1, true>(a, vpk, f, s);
+  else if (mode == 2)
+    launch_tc<2, true>(a, vpk, f, s);
+  else
+    throw std::logic_error("gpk: tensor-core Gram distances need the one-CTA-per-SM launches (deep, fused)");
+}
+#else
 int kv_tc_npad(int m) { return std::max(16, (m + 15) / 16 * 16); }
 
 size_t kv_tc_pack_floats(int m, int rows) {
@@ -625,17 +777,20 @@ void kv_tc_pack_launch(const double* v64, const float* v32, int ldv, int rows_ma
 
 void kv_tc_launch(const KvArgs& a, const float* vpk, cudaStream_t s, int mode) {
   const KvReduceArgs none{};
+  if (a.xtg) return kv_tc_tg_launch(a, vpk, none, s, mode);
   if (mode == 3)
-    launch_tc<3>(a, vpk, none, s);
+    launch_tc<3, false>(a, vpk, none, s);
   else if (mode == 2)
-    launch_tc<2>(a, vpk, none, s);
+    launch_tc<2, false>(a, vpk, none, s);
   else
-    launch_tc<0>(a, vpk, none, s);
+    launch_tc<0, false>(a, vpk, none, s);
 }
 
 void kv_tc_fused_launch(const KvArgs& a, const float* vpk, const KvReduceArgs& f, cudaStream_t s) {
   if (a.splits != 1) throw std::invalid_argument("gpk: fused slab reduce needs one column split");
-  launch_tc<1>(a, vpk, f, s);
+  if (a.xtg) return kv_tc_tg_launch(a, vpk, f, s, 1);
+  launch_tc<1, false>(a, vpk, f, s);
 }
+#endif  // GPK_KV_TC_TG
 
 }  // namespace gpk

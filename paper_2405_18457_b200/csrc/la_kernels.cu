@@ -14,6 +14,7 @@
 #include <cmath>
 
 #include "gpk_internal.cuh"
+#include "tc_util.cuh"
 #include "philox.cuh"
 
 namespace gpk {
@@ -72,6 +73,42 @@ __global__ void gram_image_kernel(const float* xs32, int n, int d, int dp, int d
 void gram_image_launch(const float* xs32, int n, int d, int dp, int dpg, float* xg, cudaStream_t s) {
   gram_image_kernel<<<blocks_for(n, 256), 256, 0, s>>>(xs32, n, d, dp, dpg, xg);
   check_launch("gram_image");
+}
+
+// Column images of the tensor-core Gram distances (kv_tc_kernel TG): chunk q
+// of 32 points holds B hi | B lo, the TF32 pieces of -2 x'_c in the canonical
+// K-major no-swizzle layout (element (j, k) at ((j/8) (KG/4) + k/4) 32 +
+// (j%8) 4 + k%4, K = KG), then |x'_c|^2 for the 32 points. Covers the 128
+// zero rows of padding of xs32 as well (zero images and norms).
+int tg_kg(int d) { return ((d + 3) / 4 + 1) / 2 * 8; }
+size_t tg_image_floats(int n, int d) {
+  const int kg = tg_kg(d);
+  return static_cast<size_t>((n + 128) / 32) * (64 * kg + 32);
+}
+__global__ void tg_image_kernel(const float* xs32, int nchunks, int dp, int kg, float* xtg) {
+  const int total = nchunks * 32;
+  const int chunk = 64 * kg + 32;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    const float* src = xs32 + static_cast<size_t>(c) * dp;
+    float* base = xtg + static_cast<size_t>(c / 32) * chunk;
+    const int j = c % 32;
+    float nn = 0.f;
+    for (int k = 0; k < kg; ++k) {
+      float hi = 0.f, lo = 0.f;
+      if (k < dp) tc::tg_split(src[k], hi, lo);
+      if (k < dp) nn = tc::tg_norm_step(nn, hi, lo);
+      const int off = ((j / 8) * (kg / 4) + k / 4) * 32 + (j % 8) * 4 + k % 4;
+      base[off] = -2.f * hi;
+      base[32 * kg + off] = -2.f * lo;
+    }
+    base[64 * kg + j] = nn;
+  }
+}
+void tg_image_launch(const float* xs32, int n, int d, int dp, float* xtg, cudaStream_t s) {
+  const int nchunks = (n + 128) / 32;
+  tg_image_kernel<<<blocks_for(static_cast<long long>(nchunks) * 32, 256), 256, 0, s>>>(xs32, nchunks, dp, tg_kg(d),
+                                                                                      xtg);
+  check_launch("tg_image");
 }
 
 __global__ void to_f32_kernel(const double* src, int n, int m, int lds, float* dst, int ldd, const int* skip) {

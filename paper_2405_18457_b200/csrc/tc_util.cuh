@@ -76,11 +76,33 @@ __device__ __forceinline__ void tc_ld4(uint32_t taddr, uint32_t (&v)[4]) {
                : "r"(taddr)
                : "memory");
 }
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+      "[%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
+}
+// Tensor-core Gram distances (kv_tc_kernel TG, tg_image_kernel): a scaled
+// coordinate enters as x' = hi + lo, two TF32 values (22 significant bits);
+// the MMAs form -2 x'_i.x'_c from hi.hi + hi.lo + lo.hi and both sides compute
+// |x'|^2 with this same FP32 chain (zero padding adds nothing), so the row
+// and column norms of one point are bitwise equal.
+__device__ __forceinline__ void tg_split(float x, float& hi, float& lo) {
+  hi = __uint_as_float(tf32_rna(x));
+  lo = __uint_as_float(tf32_rna(x - hi));
+}
+__device__ __forceinline__ float tg_norm_step(float acc, float hi, float lo) {
+  const float xp = hi + lo;  // exact: at most 22 significant bits
+  return fmaf(xp, xp, acc);
 }
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
