@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         }
       }
     } else if (warp == EW + 1) {
-      if (lane == 0) {
+      if (lane == 0) {  // single-thread issue: measured faster here than the warp-converged loop
         constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
         if (it > 0) mbar_wait(d_empty, (it - 1) & 1);  // previous slab's D drained
         for (int q = 0; q < nq; ++q) {

@@ -58,15 +58,16 @@ bool device_pool_enabled() {
   return on;
 }
 
-// Tensor-core Gram distances for d >= GPK_TGRAM_MIN_D (default 21: measured
-// C2 d = 26 full product -5%; d = 11 +15%, d = 20 +1% on one B200);
+// Tensor-core Gram distances for d >= GPK_TGRAM_MIN_D (default 16; measured
+// on one B200 with the warp-converged MMA issue: full products at d = 26
+// -21%, d = 20 -15%, d = 11 +2%, d = 3 +16%);
 // GPK_TGRAM=0 keeps the FP32 distance loops everywhere.
 bool tg_enabled(int d) {
   static const int min_d = [] {
     const char* e = std::getenv("GPK_TGRAM");
     if (e && std::atoi(e) == 0) return 1 << 30;
     const char* m = std::getenv("GPK_TGRAM_MIN_D");
-    return m ? std::atoi(m) : 21;
+    return m ? std::atoi(m) : 16;
   }();
   return d >= min_d && d <= 32;
 }

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
     }
   } else if (warp == 9) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    if (lane == 0) {  // single-thread issue: measured faster here than the warp-converged loop
       constexpr uint32_t idesc = tf32_idesc(CN, TBM);
       const uint32_t sbo = static_cast<uint32_t>(KP / 4) * 128u;
       int prev_ti = -1, rows_loaded = 0;

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     }
   } else if (warp == EW + 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    if (GPK_MMA_WARP || lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
       // TG: G(k) = -2 X_rows X_c(k)^T, the cross terms first and hi.hi last
       // (truncating accumulation: the small terms go in while D is small)
@@ -354,14 +354,14 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         if (!(a.dbg & 2))
 #pragma unroll
         for (int ks = 0; ks < KG / 8; ++ks) {
-          tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
-          tc_mma_tf32(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+          MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
+          MMA_TF32(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
         }
 #pragma unroll
         for (int ks = 0; ks < KG / 8; ++ks)
-          tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc,
+          MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc,
                       ((a.dbg & 2) && ks == 0) ? 0u : 1u);
-        tc_commit(g_full);
+        MMA_COMMIT(g_full);
       };
       if (TG && nk > 0) {
         mbar_wait(arow_full, 0);
@@ -392,16 +392,16 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         for (int kk = 0; kk < TBK / 8; ++kk) {
           const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
           const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
-          tc_mma_tf32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
+          MMA_TF32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
           if (!(a.dbg & 1)) {
-            tc_mma_tf32(tmem, ah + kk * 8, dl, idesc, 1u);
-            tc_mma_tf32(tmem, al + kk * 8, dh, idesc, 1u);
+            MMA_TF32(tmem, ah + kk * 8, dl, idesc, 1u);
+            MMA_TF32(tmem, al + kk * 8, dh, idesc, 1u);
           }
         }
-        tc_commit(&empty[s]);
-        tc_commit(&a_empty[b]);
+        MMA_COMMIT(&empty[s]);
+        MMA_COMMIT(&a_empty[b]);
         if (last_in_group) {
-          tc_commit(d_full);
+          MMA_COMMIT(d_full);
           ++g;
         }
       }

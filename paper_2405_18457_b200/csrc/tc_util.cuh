@@ -55,6 +55,40 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-converged variants: every lane of the issuing warp executes them and
+// elect.sync picks the one lane that issues (the warp stays converged around
+// the MMA stream instead of running it in single-thread divergent code).
+__device__ __forceinline__ void tc_mma_tf32_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// Issue loops of the tcgen05 kernels: the whole MMA warp runs them and
+// elect.sync issues (GPK_MMA_WARP=0: lane 0 alone, in divergent code, where
+// ptxas wraps every MMA in an elect/branch waterfall: measured ~17% slower on
+// the C2 operator product)
+#ifndef GPK_MMA_WARP
+#define GPK_MMA_WARP 1
+#endif
+#if GPK_MMA_WARP
+#define MMA_TF32 tc_mma_tf32_w
+#define MMA_COMMIT tc_commit_w
+#else
+#define MMA_TF32 tc_mma_tf32
+#define MMA_COMMIT tc_commit
+#endif
 __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
