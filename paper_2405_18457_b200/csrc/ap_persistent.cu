@@ -32,6 +32,14 @@ using namespace tc;
 
 constexpr int TBM = 128, TBK = 32, STAGES = 3, EW = 16, THREADS = 32 * (EW + 2), CPT = TBK * 4 / EW;
 constexpr int NAB = 4, A_BASE = 128, TCOLS = 512;
+// tensor-core Gram distances (as kv_tc_kernel TG): Gram tile G = -2 X_tile X_c^T
+// at TMEM columns [TG_COL, +32), the tile's row images hi | lo at TGA_COL
+constexpr int TG_COL = 96, TGA_COL = 384;
+template <int DP4>
+struct TgShape {
+  static constexpr int KG = ((DP4 + 1) / 2) * 8;
+  static constexpr int CHUNK = 2 * TBK * KG + TBK;
+};
 
 template <int NPAD>
 struct ApLayout {
@@ -66,17 +74,19 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned nctas, unsig
   __syncthreads();
 }
 
-template <int NPAD, int DP4>
+template <int NPAD, int DP4, bool TG>
 __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersistArgs a) {
   constexpr int DP = 4 * DP4;
-  constexpr bool GRAM = GPK_GRAM && DP4 >= 6;  // (x, |x|^2, 0...) image for d >= 21, as kv_tc_kernel
+  constexpr bool GRAM = !TG && GPK_GRAM && DP4 >= 6;  // (x, |x|^2, 0...) image for d >= 21, as kv_tc_kernel
+  constexpr int KG = TgShape<DP4>::KG;
+  constexpr int XST = TG ? TgShape<DP4>::CHUNK : TBK * DP;  // column data floats per stage
   constexpr int NQ = EW / 4;       // warps per TMEM lane group
   constexpr int DC = NPAD / NQ;    // drained D columns per thread
   using L = ApLayout<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* smB = reinterpret_cast<float*>(smem_raw);
   float* smX = smB + L::RING_FLOATS;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * TBK * DP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smX + STAGES * XST);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* a_full = bars + 2 * STAGES;
@@ -86,6 +96,9 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   uint64_t* r_full = d_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + 3);
   uint64_t* p_full = d_full + 4;  // tile partials staged for the last CTA's reduction
+  uint64_t* g_full = d_full + 5;     // TG: Gram tile of the chunk in TMEM
+  uint64_t* g_empty = d_full + 6;    // TG: eval warps have read it
+  uint64_t* arow_full = d_full + 7;  // TG: row images written
   double* red = reinterpret_cast<double*>(bars + 32);  // [4][NPAD]
   double* rd = red + 4 * NPAD;                           // [NQ][128]
   double* ssc = rd + NQ * 128;                           // [8]
@@ -114,6 +127,11 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     mbar_init(d_empty, EW);
     mbar_init(r_full, 1);
     mbar_init(p_full, 1);
+    if (TG) {
+      mbar_init(g_full, 1);
+      mbar_init(g_empty, EW);
+      mbar_init(arow_full, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     sh[0] = *a.sel;
     sh[1] = a.ctl->stop;
@@ -144,7 +162,41 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
   uint64_t xi2[2 * DP4];
   float ni = 0.f;  // Gram form (d >= 21): |x_i|^2 seeds the distance accumulator
-  if (warp < EW) {
+  if (warp < EW && TG) {
+    // row images hi | lo of the 22-bit split coordinates in TMEM (the Gram
+    // MMAs' A operand) and |x'_i|^2 (kv_tc_kernel TG, tg_image_kernel)
+    const float* xrow = a.xs + static_cast<size_t>(row_ok ? er : 0) * DP;
+    float hv[4 * DP4], lv[4 * DP4];
+#pragma unroll
+    for (int u = 0; u < DP4; ++u) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+      const float c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        tg_split(c[e], hv[4 * u + e], lv[4 * u + e]);
+        ni = tg_norm_step(ni, hv[4 * u + e], lv[4 * u + e]);
+      }
+    }
+    if (qtr == 0) {
+      const uint32_t ta = tmem + lane_addr + TGA_COL;
+#pragma unroll
+      for (int k8 = 0; k8 < KG / 8; ++k8) {
+        uint32_t hw[8], lw[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int k = 8 * k8 + e;
+          hw[e] = k < 4 * DP4 ? __float_as_uint(hv[k]) : 0u;
+          lw[e] = k < 4 * DP4 ? __float_as_uint(lv[k]) : 0u;
+        }
+        tc_st8(ta + 8 * k8, hw);
+        tc_st8(ta + KG + 8 * k8, lw);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(arow_full);
+    }
+  } else if (warp < EW) {
     const float* xrow = a.xs + static_cast<size_t>(row_ok ? er : 0) * DP;
 #pragma unroll
     for (int u = 0; u < DP4; ++u) {
@@ -299,20 +351,53 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         for (int q = 0; q < nq; ++q) {
           const int k = kg + q, s = k % STAGES;
           if (k >= STAGES) mbar_wait(&empty[s], ((k - STAGES) / STAGES) & 1);
-          const uint32_t xbytes = TBK * DP * 4;
+          const uint32_t xbytes = XST * 4;
           mbar_expect_tx(&full[s], L::CHUNK_BYTES + xbytes);
           bulk_g2s(smB + s * L::CHUNK_FLOATS, a.vpk + static_cast<size_t>(q) * L::CHUNK_FLOATS, L::CHUNK_BYTES,
                    &full[s]);
-          bulk_g2s(smX + s * TBK * DP, a.xs + static_cast<size_t>(c0 + q * TBK) * DP, xbytes, &full[s]);
+          if constexpr (TG)  // block % 32 == 0 (ap_persistent_supported)
+            bulk_g2s(smX + s * XST, a.xtg + static_cast<size_t>(c0 / TBK + q) * XST, xbytes, &full[s]);
+          else
+            bulk_g2s(smX + s * XST, a.xs + static_cast<size_t>(c0 + q * TBK) * DP, xbytes, &full[s]);
         }
       }
     } else if (warp == EW + 1) {
       if (lane == 0) {  // single-thread issue: measured faster here than the warp-converged loop
         constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+        // TG: G(k) = -2 X_tile X_c(k)^T, cross terms first, hi.hi last
+        auto gram_mma = [&](int k) {
+          const int s = k % STAGES;
+          const uint32_t ah = tmem + TGA_COL, al = ah + KG;
+          const uint32_t bh = smem_u32(smX + s * XST), bl = bh + TBK * KG * 4;
+          constexpr uint32_t gdesc = tf32_idesc(TBK, TBM);
+          constexpr uint32_t SBO = (KG / 4) * 128;
+#pragma unroll
+          for (int ks = 0; ks < KG / 8; ++ks) {
+            tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
+            tc_mma_tf32(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+          }
+#pragma unroll
+          for (int ks = 0; ks < KG / 8; ++ks)
+            tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+          tc_commit(g_full);
+        };
+        if (TG && nq > 0) {
+          if (it == 0) mbar_wait(arow_full, 0);
+          if (kg > 0) mbar_wait(g_empty, (kg - 1) & 1);  // previous slab's last Gram tile read
+          mbar_wait(&full[kg % STAGES], (kg / STAGES) & 1);
+          tc_fence_after();
+          gram_mma(kg);
+        }
         if (it > 0) mbar_wait(d_empty, (it - 1) & 1);  // previous slab's D drained
         for (int q = 0; q < nq; ++q) {
           const int k = kg + q, s = k % STAGES, b = k % NAB;
           mbar_wait(&full[s], (k / STAGES) & 1);
+          if (TG && q + 1 < nq) {  // next chunk's Gram tile once the eval warps hold this one's
+            mbar_wait(&full[(k + 1) % STAGES], ((k + 1) / STAGES) & 1);
+            mbar_wait(g_empty, k & 1);
+            tc_fence_after();
+            gram_mma(k + 1);
+          }
           mbar_wait(&a_full[b], (k / NAB) & 1);
           tc_fence_after();
           const uint32_t bh = smem_u32(smB + s * L::CHUNK_FLOATS);
@@ -337,12 +422,34 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         mbar_wait(&full[s], (k / STAGES) & 1);
         if (k >= NAB) mbar_wait(&a_empty[b], ((k - NAB) / NAB) & 1);
         tc_fence_after();
-        const uint32_t xbase = smem_u32(smX + s * TBK * DP + qtr * CPT * DP);
+        const uint32_t xbase = smem_u32(smX + s * XST + qtr * CPT * DP);
         uint32_t hi[CPT], lo[CPT];
+        float tg_r2[TG ? CPT : 1];
+        if constexpr (TG) {
+          mbar_wait(g_full, k & 1);
+          tc_fence_after();
+          uint32_t gv[CPT];
+          tc_ld8(tmem + lane_addr + TG_COL + qtr * CPT, gv);
+          tc_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(g_empty);
+          const float4* ncs = reinterpret_cast<const float4*>(smX + s * XST + 2 * TBK * KG + qtr * CPT);
+#pragma unroll
+          for (int t4 = 0; t4 < CPT / 4; ++t4) {
+            const float4 nc = ncs[t4];
+            tg_r2[4 * t4] = (ni + nc.x) + __uint_as_float(gv[4 * t4]);
+            tg_r2[4 * t4 + 1] = (ni + nc.y) + __uint_as_float(gv[4 * t4 + 1]);
+            tg_r2[4 * t4 + 2] = (ni + nc.z) + __uint_as_float(gv[4 * t4 + 2]);
+            tg_r2[4 * t4 + 3] = (ni + nc.w) + __uint_as_float(gv[4 * t4 + 3]);
+          }
+        }
 #pragma unroll
         for (int t = 0; t < CPT; ++t) {
           float r;
-          if constexpr (GRAM) {
+          if constexpr (TG) {
+            r = sqrt_approx(fmaxf(tg_r2[t], 0.f));
+          } else if constexpr (GRAM) {
             r = sqrt_approx(gram_r2<DP4>(xbase + t * DP * 4, xi2, acc_seed));
           } else {
           uint64_t acc0 = 0ull, acc1 = 0ull;
@@ -612,39 +719,54 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   }
 }
 
-template <int NPAD, int DP4>
+template <int NPAD, int DP4, bool TG>
 void launch_one(const ApPersistArgs& a, cudaStream_t s) {
   using L = ApLayout<NPAD>;
-  const size_t smem = sizeof(float) * (L::RING_FLOATS + STAGES * TBK * 4 * DP4) + 32 * sizeof(uint64_t) +
+  constexpr int XST = TG ? TgShape<DP4>::CHUNK : TBK * 4 * DP4;
+  const size_t smem = sizeof(float) * (L::RING_FLOATS + STAGES * XST) + 32 * sizeof(uint64_t) +
                       sizeof(double) * (4 * NPAD + 4 * 128 + 8 + 96 + 1024 + 2 * 4 * 96) + 8 * sizeof(int) +
                       sizeof(double) * TBM * a.m + 64;
   if (smem > 227 * 1024) throw std::invalid_argument("gpk: persistent AP kernel shared memory exceeds 227 KB");
   static size_t configured = 0;
   if (smem > configured) {
-    GPK_CUDA(cudaFuncSetAttribute(ap_persistent_kernel<NPAD, DP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GPK_CUDA(cudaFuncSetAttribute(ap_persistent_kernel<NPAD, DP4, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = smem;
   }
   ApPersistArgs args = a;
   void* params[] = {&args};
-  GPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ap_persistent_kernel<NPAD, DP4>),
+  GPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ap_persistent_kernel<NPAD, DP4, TG>),
                                        dim3((a.n + TBM - 1) / TBM), dim3(THREADS), params, smem, s));
   count_launch();
 }
 
-template <int NPAD>
+template <int NPAD, bool TG>
 void launch_n(const ApPersistArgs& a, cudaStream_t s) {
   switch (a.dp / 4) {
-    case 1: return launch_one<NPAD, 1>(a, s);
-    case 2: return launch_one<NPAD, 2>(a, s);
-    case 3: return launch_one<NPAD, 3>(a, s);
-    case 4: return launch_one<NPAD, 4>(a, s);
-    case 5: return launch_one<NPAD, 5>(a, s);
-    case 6: return launch_one<NPAD, 6>(a, s);
-    case 7: return launch_one<NPAD, 7>(a, s);
-    case 8: return launch_one<NPAD, 8>(a, s);
-    case 9: return launch_one<NPAD, 9>(a, s);  // d = 32 Gram image
+    case 1: return launch_one<NPAD, 1, TG>(a, s);
+    case 2: return launch_one<NPAD, 2, TG>(a, s);
+    case 3: return launch_one<NPAD, 3, TG>(a, s);
+    case 4: return launch_one<NPAD, 4, TG>(a, s);
+    case 5: return launch_one<NPAD, 5, TG>(a, s);
+    case 6: return launch_one<NPAD, 6, TG>(a, s);
+    case 7: return launch_one<NPAD, 7, TG>(a, s);
+    case 8: return launch_one<NPAD, 8, TG>(a, s);
+    case 9:
+      if constexpr (!TG) return launch_one<NPAD, 9, TG>(a, s);  // d = 32 Gram image
+      [[fallthrough]];
     default: throw std::invalid_argument("gpk: input dimension > 32 is not supported");
+  }
+}
+
+template <bool TG>
+void launch_tg(const ApPersistArgs& a, cudaStream_t s) {
+  switch (kv_tc_npad(a.m)) {
+    case 16: return launch_n<16, TG>(a, s);
+    case 32: return launch_n<32, TG>(a, s);
+    case 48: return launch_n<48, TG>(a, s);
+    case 64: return launch_n<64, TG>(a, s);
+    case 80: return launch_n<80, TG>(a, s);
+    default: throw std::invalid_argument("gpk: persistent AP supports m <= 80");
   }
 }
 
@@ -656,14 +778,10 @@ bool ap_persistent_supported(int n, int m, int block, int sms) {
 }
 
 void ap_persistent_launch(const ApPersistArgs& a, cudaStream_t s) {
-  switch (kv_tc_npad(a.m)) {
-    case 16: return launch_n<16>(a, s);
-    case 32: return launch_n<32>(a, s);
-    case 48: return launch_n<48>(a, s);
-    case 64: return launch_n<64>(a, s);
-    case 80: return launch_n<80>(a, s);
-    default: throw std::invalid_argument("gpk: persistent AP supports m <= 80");
-  }
+  if (a.xtg)
+    launch_tg<true>(a, s);
+  else
+    launch_tg<false>(a, s);
 }
 
 }  // namespace gpk

@@ -1388,10 +1388,13 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
   if (persistent) {
     // every iteration in one cooperative launch (ap_persistent.cu)
     ApPersistArgs pa{};
-    pa.xs = op->dpg ? op->xg32.p : op->xs32.p;  // Gram image for d >= 21, as run_kv
+    // tensor-core Gram distances when the operator has their images, else the
+    // FP32 Gram image for d >= 21 (as run_kv)
+    pa.xtg = op->tg ? op->xtg.p : nullptr;
+    pa.xs = (op->dpg && !op->tg) ? op->xg32.p : op->xs32.p;
     pa.n = n;
     pa.d = op->d;
-    pa.dp = op->dpg ? op->dpg : op->dp;
+    pa.dp = (op->dpg && !op->tg) ? op->dpg : op->dp;
     pa.m = m;
     pa.npad = kv_tc_npad(m);
     pa.log2_s2 = static_cast<float>(std::log2(op->s2));

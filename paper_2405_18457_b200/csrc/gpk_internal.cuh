@@ -185,6 +185,7 @@ struct ApPersistArgs {
   unsigned* gbar;         // [0] grid-barrier arrivals, [1] slab ticket, [2] decision flag, [3] sel, [4] stop (zeroed)
   double* stats;          // evals x RHS, FP32-equivalent flops, FP32-pipe flops
   unsigned long long* prof;  // optional phase clock (ns, CTA 0): C, sync1, S, sync2, B, iterations
+  const float* xtg;       // tensor-core Gram column images (tg_image_launch) or null; xs plain when set
 };
 bool ap_persistent_supported(int n, int m, int block, int sms);
 void ap_persistent_launch(const ApPersistArgs& a, cudaStream_t s);
