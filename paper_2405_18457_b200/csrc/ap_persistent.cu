@@ -35,6 +35,16 @@ constexpr int NAB = 4, A_BASE = 128, TCOLS = 512;
 // tensor-core Gram distances (as kv_tc_kernel TG): Gram tile G = -2 X_tile X_c^T
 // at TMEM columns [TG_COL, +32), the tile's row images hi | lo at TGA_COL
 constexpr int TG_COL = 96, TGA_COL = 384;
+#ifndef AP_MMA_WARP
+#define AP_MMA_WARP 1  // measured with the Gram MMAs: C2 slab phase 26.0 -> 19.7 us (without them the lane-0 loop was faster)
+#endif
+#if AP_MMA_WARP
+#define AP_MMA tc_mma_tf32_w
+#define AP_COMMIT tc_commit_w
+#else
+#define AP_MMA tc_mma_tf32
+#define AP_COMMIT tc_commit
+#endif
 template <int DP4>
 struct TgShape {
   static constexpr int KG = ((DP4 + 1) / 2) * 8;
@@ -362,7 +372,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         }
       }
     } else if (warp == EW + 1) {
-      if (lane == 0) {  // single-thread issue: measured faster here than the warp-converged loop
+      if (AP_MMA_WARP || lane == 0) {  // AP_MMA_WARP=0: lane 0 alone in divergent code (see tc_util.cuh)
         constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
         // TG: G(k) = -2 X_tile X_c(k)^T, cross terms first, hi.hi last
         auto gram_mma = [&](int k) {
@@ -373,13 +383,13 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
           constexpr uint32_t SBO = (KG / 4) * 128;
 #pragma unroll
           for (int ks = 0; ks < KG / 8; ++ks) {
-            tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
-            tc_mma_tf32(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+            AP_MMA(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
+            AP_MMA(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
           }
 #pragma unroll
           for (int ks = 0; ks < KG / 8; ++ks)
-            tc_mma_tf32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
-          tc_commit(g_full);
+            AP_MMA(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+          AP_COMMIT(g_full);
         };
         if (TG && nq > 0) {
           if (it == 0) mbar_wait(arow_full, 0);
@@ -407,14 +417,14 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
           for (int kk = 0; kk < TBK / 8; ++kk) {
             const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
             const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
-            tc_mma_tf32(tmem, ah + kk * 8, dh, idesc, (q == 0 && kk == 0) ? 0u : 1u);
-            tc_mma_tf32(tmem, ah + kk * 8, dl, idesc, 1u);
-            tc_mma_tf32(tmem, al + kk * 8, dh, idesc, 1u);
+            AP_MMA(tmem, ah + kk * 8, dh, idesc, (q == 0 && kk == 0) ? 0u : 1u);
+            AP_MMA(tmem, ah + kk * 8, dl, idesc, 1u);
+            AP_MMA(tmem, al + kk * 8, dh, idesc, 1u);
           }
-          tc_commit(&empty[s]);
-          tc_commit(&a_empty[b]);
+          AP_COMMIT(&empty[s]);
+          AP_COMMIT(&a_empty[b]);
         }
-        tc_commit(d_full);
+        AP_COMMIT(d_full);
       }
     } else {
       for (int q = 0; q < nq; ++q) {
