@@ -1299,8 +1299,9 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
     run_kv(op, kc);
   }
 
+  g_phase.mark("ap_refresh");
   GPK_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // block inverses ready before the first update
-  g_phase.mark("ap_refresh_and_inverse");
+  g_phase.mark("ap_inverse_wait");
   if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
   auto iteration = [&]() {  // solvers.cpp:120-140
     if (tc) {
