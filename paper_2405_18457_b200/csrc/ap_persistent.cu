@@ -35,6 +35,9 @@ constexpr int NAB = 4, A_BASE = 128, TCOLS = 512;
 // tensor-core Gram distances (as kv_tc_kernel TG): Gram tile G = -2 X_tile X_c^T
 // at TMEM columns [TG_COL, +32), the tile's row images hi | lo at TGA_COL
 constexpr int TG_COL = 96, TGA_COL = 384;
+#ifndef AP_DECIDE_ALL
+#define AP_DECIDE_ALL 1
+#endif
 #ifndef AP_MMA_WARP
 #define AP_MMA_WARP 1  // measured with the Gram MMAs: C2 slab phase 26.0 -> 19.7 us (without them the lane-0 loop was faster)
 #endif
@@ -117,12 +120,14 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   double* gemm = bscore + 1024;                          // [2][4 * 96] phase-C K halves
   int* sh = reinterpret_cast<int*>(gemm + 2 * 4 * 96);   // [0] sel, [1] stop
   double* Rt = reinterpret_cast<double*>(sh + 8);        // [128][m] residual tile
+  double* scl = Rt + TBM * a.m;                          // [m] column scales (termination test)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = blockIdx.x, m = a.m, n = a.n;
   const int rows_t = min(TBM, n - tile * TBM);
   const unsigned nctas = gridDim.x;
   unsigned gen = 0;
+  for (int j = threadIdx.x; j < a.m; j += blockDim.x) scl[j] = a.scales[j];
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -567,12 +572,20 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     ++it;
     mark(2);
     // ---------------- B: termination test and next block ----------------
-    // The last CTA to finish its slab (arrival ticket) sums the tile partials
-    // in a fixed order, tests termination, picks the next block (ap_check /
-    // ap_select, strict '>' from -1) and publishes {sel, stop} with a release
-    // flag; the other CTAs wait on the flag. Replaces a grid barrier plus a
-    // redundant reduction in every CTA.
+    // Every CTA (AP_DECIDE_ALL, default) or the last CTA to finish its slab
+    // (arrival ticket) sums the tile partials in a fixed order, tests
+    // termination and picks the next block (ap_check / ap_select, strict '>'
+    // from -1); CTA 0 (or the last CTA) writes the control block. With one
+    // deciding CTA the others wait on a release flag carrying the decision;
+    // measured: that CTA's rarely-run code path costs ~4 us of instruction
+    // fetch per iteration, while a grid barrier + the same bitwise decision
+    // in every CTA keeps the path hot on every SM.
     if (tid == 0) iters += 1;  // every CTA counts iterations (budget test)
+#if AP_DECIDE_ALL
+    grid_sync(a.gbar, nctas, gen);  // every tile's partials are published
+    mark(3);
+    if (true) {
+#else
     __syncthreads();
     if (tid == 0) {
       if (a.prof && it <= 64) {  // development timeline: ticket time of every CTA (globaltimer)
@@ -588,6 +601,12 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
     mark(3);
     if (sh[3]) {
       __threadfence();
+#endif
+      if (a.prof && it <= 64 && tid == 0 && tile == 0) {  // development timeline
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(gt));
+        a.prof[16 + (it - 1) * 160 + 155] = gt;
+      }
       // thread (j, p) = (tid / 8, tid % 8) sums column j of the tile partials
       // over tiles p, p + 8, ... then a fixed xor-4/2/1 tree; thread k < nblocks
       // sums block k's score partials in order. The partials arrive by one bulk
@@ -609,6 +628,11 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
             if (q < a.gpb) sp[q] = __ldcg(a.spart + static_cast<size_t>(tid) * a.gpb + q);
         }
         mbar_wait(p_full, pphase & 1);
+        if (a.prof && it <= 64 && tid == 0 && tile == 0) {  // development timeline
+          unsigned long long gt;
+          asm volatile("mov.u64 %0, %%clock64;" : "=l"(gt));
+          a.prof[16 + (it - 1) * 160 + 156] = gt;
+        }
         const double* st = reinterpret_cast<const double*>(smB);
         const int j = tid >> 3, p = tid & 7;
         double acc = 0.0;
@@ -617,7 +641,7 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         acc += __shfl_xor_sync(0xffffffffu, acc, 4);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (p == 0 && j < m) ss[j] = sqrt(acc) / a.scales[j];
+        if (p == 0 && j < m) ss[j] = sqrt(acc) / scl[j];
         if (tid < a.nblocks) bscore[tid] = sqrt(((sp[0] + sp[1]) + sp[2]) + sp[3]);
       } else {
         constexpr int QH = 10;  // 2 x 10 x 8 >= 148 tiles (ap_persistent_supported)
@@ -649,11 +673,16 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         acc += __shfl_xor_sync(0xffffffffu, acc, 4);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (p == 0 && j < m) ss[j] = sqrt(acc) / a.scales[j];
+        if (p == 0 && j < m) ss[j] = sqrt(acc) / scl[j];
         if (tid < a.nblocks) bscore[tid] = sqrt(((sp[0] + sp[1]) + sp[2]) + sp[3]);
       }
       if (staged) ++pphase;
       __syncthreads();
+      if (a.prof && it <= 64 && tid == 0 && tile == 0) {  // development timeline
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(gt));
+        a.prof[16 + (it - 1) * 160 + 157] = gt;
+      }
       if (warp == 0) {
         // probe mean over columns 1..m-1 and the first maximal block score
         // (the serial strict '>' scan from -1 of ap_select)
@@ -685,35 +714,39 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
           const int stop = (done || iters >= a.budget) ? 1 : 0;
           sh[0] = best_k;
           sh[1] = stop;
-          a.ctl->iters = iters;
-          a.ctl->mean_norm = mean;
-          a.ctl->probe_norm = probe;
-          a.ctl->done = done;
-          a.ctl->stop = stop;
-          *a.sel = best_k;
-          a.gbar[3] = static_cast<unsigned>(best_k);  // broadcast to the other CTAs
-          a.gbar[4] = static_cast<unsigned>(stop);
+          if (!AP_DECIDE_ALL || tile == 0) {
+            a.ctl->iters = iters;
+            a.ctl->mean_norm = mean;
+            a.ctl->probe_norm = probe;
+            a.ctl->done = done;
+            a.ctl->stop = stop;
+            *a.sel = best_k;
+          }
+          if (a.prof && it <= 64 && tile == 0) {
+            unsigned long long gt;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(gt));
+            a.prof[16 + (it - 1) * 160 + 159] = gt;
+          }
+#if !AP_DECIDE_ALL
+          // the decision travels in the release word itself (iteration << 12 |
+          // stop << 11 | block; nblocks <= 148 here), so a waiting CTA needs one
+          // acquire load; this thread's ctl / sel stores are ordered before it
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.gbar + 2),
+                       "r"((static_cast<unsigned>(it) << 12) | (static_cast<unsigned>(stop) << 11) |
+                           static_cast<unsigned>(best_k))
+                       : "memory");
+#endif
         }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        if (a.prof && it <= 64) {
-          unsigned long long gt;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-          a.prof[16 + (it - 1) * 160 + 159] = gt;
-        }
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.gbar + 2), "r"(static_cast<unsigned>(it)) : "memory");
       }
     } else if (tid == 0) {
+      unsigned v;
       while (true) {
-        unsigned v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.gbar + 2) : "memory");
-        if (v >= static_cast<unsigned>(it)) break;
+        if ((v >> 12) >= static_cast<unsigned>(it)) break;
         __nanosleep(32);
       }
-      sh[0] = static_cast<int>(__ldcg(a.gbar + 3));
-      sh[1] = static_cast<int>(__ldcg(a.gbar + 4));
+      sh[0] = static_cast<int>(v & 2047u);
+      sh[1] = static_cast<int>((v >> 11) & 1u);
     }
     __syncthreads();
     mark(4);
@@ -735,7 +768,7 @@ void launch_one(const ApPersistArgs& a, cudaStream_t s) {
   constexpr int XST = TG ? TgShape<DP4>::CHUNK : TBK * 4 * DP4;
   const size_t smem = sizeof(float) * (L::RING_FLOATS + STAGES * XST) + 32 * sizeof(uint64_t) +
                       sizeof(double) * (4 * NPAD + 4 * 128 + 8 + 96 + 1024 + 2 * 4 * 96) + 8 * sizeof(int) +
-                      sizeof(double) * TBM * a.m + 64;
+                      sizeof(double) * (TBM + 1) * a.m + 64;
   if (smem > 227 * 1024) throw std::invalid_argument("gpk: persistent AP kernel shared memory exceeds 227 KB");
   static size_t configured = 0;
   if (smem > configured) {

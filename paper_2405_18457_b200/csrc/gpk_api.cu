@@ -1460,8 +1460,22 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
           rel += static_cast<double>(row[159] - hi);
           ++cnt;
         }
-        if (cnt) std::fprintf(stderr, "ap_persistent tickets: spread %.2f us, last ticket -> release %.2f us\n",
-                              spread / cnt / 1e3, rel / cnt / 1e3);
+        (void)rel;
+        if (cnt) std::fprintf(stderr, "ap_persistent tickets: spread %.2f us\n", spread / cnt / 1e3);
+        double seg[3] = {0, 0, 0};
+        int c2 = 0;
+        for (int it = 0; it < 64 && it < static_cast<int>(h[9]); ++it) {
+          const unsigned long long* row = h + 16 + it * 160;
+          unsigned long long hi = 0;
+          for (int c = 0; c < (n + 127) / 128; ++c) hi = std::max(hi, row[c]);
+          if (!row[155] || !row[156] || !row[157] || !row[159]) continue;  // SM clock64 stamps of the last CTA
+          seg[0] += static_cast<double>(row[156] - row[155]);
+          seg[1] += static_cast<double>(row[157] - row[156]);
+          seg[2] += static_cast<double>(row[159] - row[157]);
+          ++c2;
+        }
+        if (c2) std::fprintf(stderr, "ap_persistent last CTA (us at 1.9 GHz): ticket->partials %.2f, sums %.2f, select %.2f\n",
+                             seg[0] / c2 / 1.9e3, seg[1] / c2 / 1.9e3, seg[2] / c2 / 1.9e3);
       }
       const double it = static_cast<double>(h[9]) * 1.9e3;  // cycles -> us at ~1.9 GHz
       std::fprintf(stderr,
