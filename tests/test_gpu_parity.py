@@ -430,3 +430,23 @@ def test_apply_streamk_matches_oracle(G, oracle, n, d, m, monkeypatch):
     ctx.close()
     ref = oracle.apply(X, raw, V, threads=8)
     assert colrel(got, ref) <= OP_TOL
+
+
+@pytest.mark.parametrize("env", [{"GPK_KV_DEEP": "1", "GPK_TGRAM_MIN_D": "1"},  # deep launch, Gram MMAs at every d
+                                 {"GPK_KV_DEEP": "1", "GPK_TGRAM": "0"},        # deep launch, FP32 distances
+                                 {"GPK_KV_DEEP": "0", "GPK_TGRAM_MIN_D": "1"}],  # two CTAs per SM (no Gram MMAs)
+                         ids=["deep-gram", "deep-fp32", "shallow"])
+def test_operator_variants_match_oracle(env):
+    """The launch variants the size heuristics pick at BASELINE sizes (one CTA
+    per SM with tensor-core Gram distances for the C2 refresh and the AP
+    solver), forced at oracle-checkable sizes in a fresh process."""
+    import json
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "_variant_probe.py")], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    errs = json.loads(r.stdout.strip().splitlines()[-1])
+    assert max(errs.values()) <= OP_TOL, errs
