@@ -491,8 +491,6 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.d = op->d;
   a.xs_rows = (gram && c.xs_rows) ? op->ptsg32.p : c.xs_rows;
   a.xtg = tgram ? op->xtg.p : nullptr;
-  static const int kv_dbg = std::getenv("GPK_KV_DBG") ? std::atoi(std::getenv("GPK_KV_DBG")) : 0;
-  a.dbg = kv_dbg;
   a.sk_ctas = sk_G;
   gpk_ctx* ctx = op->ctx;
   if (c.vpk && !tc) throw InvalidArgument("gpk: pre-packed operator input needs the tcgen05 kernel");

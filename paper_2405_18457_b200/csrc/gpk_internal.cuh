@@ -60,7 +60,6 @@ struct KvArgs {
   double* stats;       // device counters [evals x RHS, algorithmic flops] or null
   int d;               // true input dimension (flop accounting)
   const float* xs_rows;  // scaled FP32 inputs of the rows (cross kernel k(P, X)); null: xs
-  int dbg;               // development: bit0 KV hi.hi only, bit1 Gram hi.hi only (GPK_KV_DBG)
   const float* xtg;      // tensor-core Gram column images (tg_image_kernel) or null; needs c0 % 32 == 0
 };
 int kv_tc_for(int m);        // columns-per-lane template parameter for m

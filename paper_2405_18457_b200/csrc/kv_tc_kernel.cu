@@ -351,7 +351,6 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         const uint32_t bh = smem_u32(smX + s * XST), bl = bh + TBK * KG * 4;
         constexpr uint32_t gdesc = tf32_idesc(TBK, TBM);
         constexpr uint32_t SBO = (KG / 4) * 128;
-        if (!(a.dbg & 2))
 #pragma unroll
         for (int ks = 0; ks < KG / 8; ++ks) {
           MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
@@ -359,8 +358,7 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         }
 #pragma unroll
         for (int ks = 0; ks < KG / 8; ++ks)
-          MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc,
-                      ((a.dbg & 2) && ks == 0) ? 0u : 1u);
+          MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
         MMA_COMMIT(g_full);
       };
       if (TG && nk > 0) {
@@ -393,10 +391,8 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
           const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
           const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
           MMA_TF32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
-          if (!(a.dbg & 1)) {
-            MMA_TF32(tmem, ah + kk * 8, dl, idesc, 1u);
-            MMA_TF32(tmem, al + kk * 8, dh, idesc, 1u);
-          }
+          MMA_TF32(tmem, ah + kk * 8, dl, idesc, 1u);
+          MMA_TF32(tmem, al + kk * 8, dh, idesc, 1u);
         }
         MMA_COMMIT(&empty[s]);
         MMA_COMMIT(&a_empty[b]);
