@@ -450,3 +450,29 @@ def test_operator_variants_match_oracle(env):
     assert r.returncode == 0, r.stderr[-2000:]
     errs = json.loads(r.stdout.strip().splitlines()[-1])
     assert max(errs.values()) <= OP_TOL, errs
+
+
+def test_optimiser_buffers_are_reused(G, gpk_ctx):
+    """Device buffers come from the stream-ordered pool (GPK_DEVICE_POOL): a
+    destroyed optimiser's buffers serve the next one, so repeated
+    create/step/destroy cycles do not grow device memory, and destroy does not
+    synchronise-and-unmap every buffer."""
+    import time
+    import torch
+    X32, y32 = G.sinsum_dataset(4096, 8, False, 0.1, 0)
+    X, y = X32.astype(np.float64), y32.astype(np.float64)
+    sc = G.SolverConfig(kind=0, tolerance=0.01, max_epochs=20, preconditioner_rank=100)
+    oc = G.OuterConfig(estimator=1, solver=sc, warm_start=True, steps=2, learning_rate=0.1, probe_count=16,
+                       rff_pairs=256, probe_seed=2, feature_seed=3, solver_seed=4)
+    used, close_s = [], []
+    for _ in range(4):
+        opt = G.Optimiser(gpk_ctx, X, y, oc, init_constrained=[1.0] * 8 + [1.0, 0.1])
+        opt.step(2)
+        gpk_ctx.synchronize()
+        t = time.perf_counter()
+        opt.close()
+        close_s.append(time.perf_counter() - t)
+        free, total = torch.cuda.mem_get_info()
+        used.append(total - free)
+    assert max(used[1:]) - used[1] <= 64 << 20, used
+    assert min(close_s[1:]) < 5e-3, close_s

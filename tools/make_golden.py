@@ -92,5 +92,16 @@ def main(names):
         print(f"wrote tests/golden/{name}.npz", flush=True)
 
 
+def main_full_c2():
+    """BASELINE configs[1] at its stated step count (20 Adam steps): the
+    oracle's constrained trajectory and per-step solver counts/norms only."""
+    out = {"traj_" + k: v for k, v in trajectory("c2", steps=20).items()}
+    np.savez_compressed(os.path.join(OUT, "c2_20.npz"), **out)
+    print("wrote tests/golden/c2_20.npz", flush=True)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c4", "c5"])
+    if sys.argv[1:] == ["c2_20"]:
+        main_full_c2()
+    else:
+        main(sys.argv[1:] or ["c1", "c4", "c5"])
