@@ -14,6 +14,7 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 CFG = {  # mirrors tools/make_golden.py
     "c1": dict(n=4096, d=8, uniform=False, noise=0.1, s=16, pairs=512),
     "c2": dict(n=16384, d=26, uniform=False, noise=0.1, s=64, pairs=1024),
+    "c3": dict(n=43008, d=20, uniform=False, noise=0.1, s=64, pairs=1000),
     "c4": dict(n=393216, d=3, uniform=True, noise=0.05, s=64, pairs=1000),
     "c5": dict(n=1835008, d=11, uniform=False, noise=0.1, s=64, pairs=2048),
 }
@@ -33,7 +34,7 @@ def rhs(oracle, n, m):
     return np.asfortranarray(oracle.stream_draw(11, 2, 0, "gaussian", n * m).reshape((n, m), order="F"))
 
 
-@pytest.mark.parametrize("name,rows", [("c1", 256), ("c2", 64), ("c4", 16), ("c5", 8)])
+@pytest.mark.parametrize("name,rows", [("c1", 256), ("c2", 64), ("c3", 32), ("c4", 16), ("c5", 8)])
 def test_oracle_reproduces_slab_fixture(oracle, name, rows):
     g = load(name)
     X, _ = inputs(oracle, name)
@@ -56,7 +57,7 @@ def test_c1_trajectory_fixture_is_sane():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_gpu_slab_matches_fixture(gpk_ctx, oracle, name):
     import paper_2405_18457_b200 as G
     g = load(name)
@@ -163,3 +164,33 @@ def test_gpu_c2_full_trajectory_matches_fixture(gpk_ctx):
         assert np.max(np.abs(a - b) / b) <= 1e-4, key
     gg = g["traj_gradient"]
     assert np.max(np.abs(r["gradient"] - gg) / np.abs(gg).max(axis=1, keepdims=True)) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_gpu_c3_trajectory_matches_fixture(gpk_ctx):
+    """BASELINE configs[2]: n=43008 d=20, pathwise s=64, CG early-stopped at
+    10 epochs per step (preconditioner rank 100), first 2 Adam steps, against
+    the FP64 oracle (tools/make_golden.py c3). The 10-iteration CG stops far
+    from tau (residual ~0.05), where the iterates carry the FP32 operator's
+    rounding (an FP64 CG with 1e-7 relative noise on H.d
+    moves such residuals by tens of percent), so residual norms and gradients
+    are checked at the level measured here (mean residual 14%, probe 0.6%,
+    gradient 0.6% of the step's largest component), the trajectory at the
+    north-star 1e-3 and the (budget-bound) iteration counts exactly."""
+    import paper_2405_18457_b200 as G
+    g = load("c3")
+    c = CFG["c3"]
+    X32, y32 = G.sinsum_dataset(c["n"], c["d"], c["uniform"], c["noise"], 0)
+    sc = G.SolverConfig(kind=0, tolerance=0.01, max_epochs=10, preconditioner_rank=100)
+    oc = G.OuterConfig(estimator=1, solver=sc, warm_start=True, steps=2, learning_rate=0.1, probe_count=64,
+                       rff_pairs=1000, probe_seed=2, feature_seed=3, solver_seed=4)
+    r = G.optimise(gpk_ctx, X32.astype(np.float64), y32.astype(np.float64), oc,
+                   init_constrained=[1.0] * 20 + [1.0, 0.1])
+    ref = g["traj_constrained"]
+    assert np.max(np.abs(r["constrained"] - ref) / ref) <= 1e-3
+    assert np.array_equal(r["iterations"], g["traj_iterations"])
+    assert np.max(np.abs(r["mean_residual_norm"] - g["traj_mean_residual_norm"]) / g["traj_mean_residual_norm"]) <= 0.25
+    assert np.max(np.abs(r["probe_residual_norm"] - g["traj_probe_residual_norm"]) /
+                  g["traj_probe_residual_norm"]) <= 0.02
+    gg = g["traj_gradient"]
+    assert np.max(np.abs(r["gradient"] - gg) / np.abs(gg).max(axis=1, keepdims=True)) <= 0.02
