@@ -58,6 +58,18 @@ bool device_pool_enabled() {
   return on;
 }
 
+// Reference dense_cache_cap (outer_loop.hpp:60): the optimiser's operators
+// with n <= 4096 keep the FP64 kernel matrix (operators created through the
+// operator API do not, as KernelOperatorOptions::dense_cache defaults to
+// false); GPK_DENSE_CAP overrides (0: never).
+int dense_cache_cap() {
+  static const int cap = [] {
+    const char* e = std::getenv("GPK_DENSE_CAP");
+    return e ? std::atoi(e) : 4096;
+  }();
+  return cap;
+}
+
 // Tensor-core Gram distances for d >= GPK_TGRAM_MIN_D (default 16; measured
 // on one B200 with the warp-converged MMA issue: full products at d = 26
 // -21%, d = 20 -15%, d = 11 +2%, d = 3 +16%);
@@ -191,6 +203,11 @@ struct gpk_operator {
   int dpg = 0;            // Gram image width (gram_dp(d)); 0: direct-difference operator
   bool tg = false;        // tensor-core Gram distances in the tcgen05 operator (tg_enabled)
   DBuf<float> xtg;        // their column images (tg_image_launch), rebuilt with the scaled inputs
+  // dense FP64 kernel matrix K (no noise) for n <= dense_cache_cap, as the
+  // reference caches H for small problems (kernel.cpp:83-109,
+  // outer_loop.cpp:72); full unsharded products then run as one DGEMM
+  bool dense = false;
+  DBuf<double> kdense;
   DBuf<float> xg32;       // [n + 128][dpg] (x, |x|^2, 0...) for the tensor-core operator
   DBuf<double> xs64;      // [n][d]
   DBuf<double> inv_ls_dev;
@@ -383,6 +400,9 @@ void set_hyper(gpk_operator* op, const double* raw) {
   prescale_launch(op->x64.p, op->n, d, op->dp, il, op->xs32.p, op->xs64.p, s);
   if (op->dpg) gram_image_launch(op->xs32.p, op->n, d, op->dp, op->dpg, op->xg32.p, s);
   if (op->tg) tg_image_launch(op->xs32.p, op->n, d, op->dp, op->xtg.p, s);
+  if (op->dense)
+    dense_block64_launch(op->xs64.p, op->n, d, op->s2, op->sigma2, 0, op->n, 0, op->n,
+                         op->kdense.ensure(static_cast<size_t>(op->n) * op->n), op->n, 0, s);
   GPK_CUDA(cudaStreamSynchronize(s));  // inv_ls host buffer lifetime
 }
 
@@ -424,6 +444,17 @@ struct KvCall {
   const float* xs_rows = nullptr;  // cross kernel: rows from these scaled points, no noise diagonal
   bool fused = false;              // AP slab: reduce + epilogue inside the tcgen05 kernel
 };
+
+__global__ void stats_add_kernel(double* st, double entries, int m, int d, const int* skip) {
+  if (skip && *skip) return;
+  atomicAdd(st, entries * m);
+  atomicAdd(st + 1, entries * (2.0 * m + 3.0 * d + 6.0));
+  atomicAdd(st + 2, entries * (3.0 * d + 6.0));
+}
+void stats_add_launch(double* st, double entries, int m, int d, const int* skip, cudaStream_t s) {
+  stats_add_kernel<<<1, 1, 0, s>>>(st, entries, m, d, skip);
+  check_launch("stats_add");
+}
 
 void run_kv(gpk_operator* op, const KvCall& c) {
   cudaStream_t s = op->ctx->stream;
@@ -495,7 +526,12 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   gpk_ctx* ctx = op->ctx;
   if (c.vpk && !tc) throw InvalidArgument("gpk: pre-packed operator input needs the tcgen05 kernel");
   const float* vpk = c.vpk;
-  if (tc && !vpk) {
+  // dense cache (n <= dense_cache_cap): a full unsharded product with an FP64
+  // RHS is K V by cuBLAS DGEMM in FP64 (the reference's cached path), reduced
+  // by kv_reduce as one split
+  const bool dense = op->dense && !op->sharded && !fused && !c.sel && !c.row_idx && !c.xs_rows && c.vdiag &&
+                     c.r0 == 0 && c.R == op->n && c.c0 == 0 && c.C == op->n;
+  if (tc && !vpk && !dense) {
     float* buf = op->vpk.ensure(kv_tc_pack_floats(c.m, Cmax));
     kv_tc_pack_launch(c.vdiag, c.v, c.vdiag ? c.m : a.ldv, Cmax, c.m, c.sel, c.sel_block, op->n, buf, c.skip, s);
     vpk = buf;
@@ -562,10 +598,23 @@ void run_kv(gpk_operator* op, const KvCall& c) {
     if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
     return;
   }
-  if (tc)
+  if (dense) {
+    // part (row-major [n][m]) = K V: column-major part^T (m x n) = V^T K (K symmetric)
+    gpk_ctx* cx = op->ctx;
+    if (cublasSetStream(cx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
+    const double one = 1.0, zero = 0.0;
+    if (cublasDgemm(cx->blas, CUBLAS_OP_N, CUBLAS_OP_N, c.m, op->n, op->n, &one, c.vdiag, c.m, op->kdense.p, op->n,
+                    &zero, part, c.m) != CUBLAS_STATUS_SUCCESS)
+      throw CudaError("cublasDgemm (dense operator)");
+    count_launch();
+    if (a.stats) stats_add_launch(a.stats, static_cast<double>(op->n) * op->n, c.m, op->d, c.skip, s);
+    r.splits = 1;
+    r.sk_G = 0;
+  } else if (tc) {
     kv_tc_launch(a, vpk, s, streamk ? 3 : (deep ? 2 : 0));
-  else
+  } else {
     kv_slab_launch(a, op->d, s);
+  }
   if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
   kv_reduce_launch(r, s);
 }
@@ -2746,6 +2795,11 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
     opp->nloc -= opp->row0;
     opp->S = (((n + ctx->nranks - 1) / ctx->nranks) + 31) / 32 * 32;
     if (opp->nloc < 1) throw InvalidArgument("gpk_optimise: fewer rows than ranks * 32");
+  }
+  if (!opp->sharded && n <= dense_cache_cap()) {  // outer_loop.cpp:72: options.dense_cache = n <= cap
+    opp->dense = true;
+    dense_block64_launch(opp->xs64.p, n, d, opp->s2, opp->sigma2, 0, n, 0, n,
+                         opp->kdense.ensure(static_cast<size_t>(n) * n), n, 0, ctx->stream);
   }
   const int nloc = opp->nloc;
   cudaStream_t stream = ctx->stream;

@@ -95,12 +95,16 @@ def test_gpu_c1_trajectory_matches_fixture(gpk_ctx):
     ref = g["traj_constrained"]
     # north star: hyperparameter trajectory within 1e-3 relative
     assert np.max(np.abs(r["constrained"] - ref) / ref) <= 1e-3
+    # n = 4096 is within the reference's dense_cache_cap, so the optimiser
+    # applies H as a cached FP64 matrix (DGEMM), as outer_loop.cpp:72 does.
     # At this initialisation (noise 0.1) preconditioned CG to tau = 0.01 is
-    # sensitive to operator rounding: an FP64 CG whose H.d carries 1e-7
-    # relative noise already needs +2 iterations. The
-    # FP32 (3xTF32) operator needs 0-4 more than the FP64 oracle here.
+    # still sensitive to summation order: measured 7 of
+    # 10 steps with the oracle's iteration count, the others within 2;
+    # gradients within 3.6e-5 of each step's largest component.
     di = r["iterations"] - g["traj_iterations"]
-    assert np.all(di >= -1) and np.all(di <= 5), di
+    assert np.all(np.abs(di) <= 2), di
+    gg = g["traj_gradient"]
+    assert np.max(np.abs(r["gradient"] - gg) / np.abs(gg).max(axis=1, keepdims=True)) <= 1e-4
     # both runs meet the tolerance or exhaust the same 50-epoch budget
     for k in range(len(di)):
         if r["iterations"][k] < 50:

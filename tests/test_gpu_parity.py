@@ -304,9 +304,10 @@ def test_optimise_trajectory_matches_oracle(G, kctx, oracle):
 def test_sharded_optimiser_world1_matches_plain(G, gpk_ctx, oracle, solver):
     """The row-sharded optimiser (NCCL communicator, all-gathered packed
     directions / SGD gradient partials and partial sums) on a 1-rank
-    communicator reproduces the plain single-GPU run bit for bit."""
+    communicator reproduces the plain single-GPU run bit for bit (n above
+    the dense-cache cap, so both run the tcgen05 operator)."""
     from paper_2405_18457_b200 import parallel as P
-    n, d = 2048, 8
+    n, d = 4224, 8
     X32, y32 = G.sinsum_dataset(n, d, False, 0.1, 0)
     X, y = X32.astype(np.float64), y32.astype(np.float64)
     scfg = dict(kind=0, tolerance=0.01, max_epochs=50, preconditioner_rank=100) if solver == "cg" else \
