@@ -91,19 +91,46 @@ def outer_config(G, name, steps):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    polled every 5 ms from a thread (nvidia-smi -lms 100 as the fallback)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, device):
         self.device = device
         self.rows = []
         self._stop = threading.Event()
         self._proc = None
+        self._thread = None
+        self._nvml = None
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._nvml = pynvml
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception:
+                        break
+                    self.rows.append((float(sm), float(mx), int(bits)))
+                    time.sleep(0.005)
+
+            self._thread = threading.Thread(target=poll, daemon=True)
+            self._thread.start()
+            return
+        except Exception:
+            self._nvml = None
         try:
             self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                                            "--format=csv,noheader,nounits", "-lms", "100"],
@@ -113,13 +140,24 @@ class ClockSampler:
             self._proc = None
 
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self._proc.stdout:
             if self._stop.is_set():
                 break
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            try:
+                bits = 0
+                for k, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        bits |= self.REASONS[k]
+                self.rows.append((float(r[1]), float(r[2]), bits))
+            except (ValueError, IndexError):
+                continue
 
     def stop(self):
         self._stop.set()
+        if self._thread:
+            self._thread.join(timeout=1)
         if self._proc:
             self._proc.terminate()
             try:
@@ -128,19 +166,11 @@ class ClockSampler:
                 self._proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            try:
-                sm.append(float(r[1]))
-                mx.append(float(r[2]))
-                for k, v in zip(names, r[5:9]):
-                    if v.strip().lower() == "active":
-                        reasons.add(k)
-            except (ValueError, IndexError):
-                continue
+        sm = [r[0] for r in self.rows]
+        mx = [r[1] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, b in self.REASONS.items() if r[2] & b})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "source": "nvml 5 ms" if self._nvml else "nvidia-smi 100 ms"}
 
 
 def dist_setup():
