@@ -86,6 +86,10 @@ const char* gpk_version(void);
 gpk_status gpk_ctx_create(int device, gpk_ctx** out);
 gpk_status gpk_ctx_destroy(gpk_ctx* ctx);
 gpk_status gpk_ctx_synchronize(gpk_ctx* ctx);
+/* Makes the context stream wait for all work issued so far on the context's
+ * auxiliary stream (the AP block factorisations the optimiser starts for the
+ * next step), so an event recorded on the stream afterwards covers both. */
+gpk_status gpk_ctx_join(gpk_ctx* ctx);
 /* Number of this library's kernel launches issued on the context so far. */
 gpk_status gpk_ctx_launch_count(gpk_ctx* ctx, long long* out);
 /* The CUDA stream (cudaStream_t) all work of this context is issued on. */

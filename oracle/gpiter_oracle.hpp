@@ -125,6 +125,7 @@ class KernelOperator {
   int n_ = 0, d_ = 0;
   Vec inv_ls_;
   std::vector<double> xs_;  // scaled inputs, row-major n x d (values == Eigen col-major copy)
+  std::vector<double> xst_;  // the same, dimension-major d x n
   double signal_variance_ = 0.0, noise_variance_ = 0.0;
 };
 

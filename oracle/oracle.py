@@ -53,6 +53,27 @@ def build():
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
 
 
+def use_timing_build():
+    """Switch this process to the -march=native -ffast-math timing build (bench.py's
+    CPU arms only; parity checks always use the strict build). Compiled on the
+    host that runs it, into a directory keyed on its CPU model and flags."""
+    global _LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("oracle: choose the build before the first call")
+    import hashlib
+    import platform
+    try:
+        info = open("/proc/cpuinfo").read()
+        key = [ln for ln in info.splitlines() if ln.startswith(("model name", "flags"))][:2]
+    except OSError:
+        key = [platform.processor()]
+    tag = hashlib.sha1("\n".join(key).encode()).hexdigest()[:12]
+    out = os.path.join(_HERE, "build", "native-" + tag)
+    subprocess.run(["make", "-s", "-C", _HERE, "native", f"NATIVE_OUT={out}"], check=True)
+    _LIB_PATH = os.path.join(out, "liboracle.so")
+    return _LIB_PATH
+
+
 def lib():
     global _lib
     if _lib is None:

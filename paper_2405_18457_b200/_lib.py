@@ -58,6 +58,7 @@ def _sig(lib):
         "gpk_ctx_create": (C.c_int, [C.c_int, C.POINTER(H)]),
         "gpk_ctx_destroy": (C.c_int, [H]),
         "gpk_ctx_synchronize": (C.c_int, [H]),
+        "gpk_ctx_join": (C.c_int, [H]),
         "gpk_ctx_launch_count": (C.c_int, [H, C.POINTER(C.c_longlong)]),
         "gpk_ctx_stream": (C.c_int, [H, C.POINTER(vp)]),
         "gpk_ctx_set_profiling": (C.c_int, [H, C.c_int]),

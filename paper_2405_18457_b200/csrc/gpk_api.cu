@@ -2172,6 +2172,13 @@ gpk_status gpk_ctx_destroy(gpk_ctx* c) {
 gpk_status gpk_ctx_synchronize(gpk_ctx* c) {
   return guarded([&] { GPK_CUDA(cudaStreamSynchronize(c->stream)); });
 }
+gpk_status gpk_ctx_join(gpk_ctx* c) {
+  return guarded([&] {
+    GPK_CUDA(cudaSetDevice(c->device));
+    GPK_CUDA(cudaEventRecord(c->ev_aux, c->aux));
+    GPK_CUDA(cudaStreamWaitEvent(c->stream, c->ev_aux, 0));
+  });
+}
 gpk_status gpk_ctx_launch_count(gpk_ctx* c, long long* out) {
   return guarded([&] { *out = c->launches; });
 }

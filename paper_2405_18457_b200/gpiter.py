@@ -116,6 +116,10 @@ class Context:
     def synchronize(self):
         check(self._lib.gpk_ctx_synchronize(self.handle))
 
+    def join(self):
+        """Stream-orders the auxiliary stream's pending work before later work (gpk_ctx_join)."""
+        check(self._lib.gpk_ctx_join(self.handle))
+
     def launch_count(self):
         v = C.c_longlong()
         check(self._lib.gpk_ctx_launch_count(self.handle, C.byref(v)))
