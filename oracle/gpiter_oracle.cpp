@@ -17,6 +17,9 @@
 
 namespace oracle {
 
+const OracleBackend* g_backend = nullptr;
+int g_sgd_iteration_cap = -1;
+
 namespace {
 // Dynamic parallel-for over [0, count) with std::thread (no OpenMP in this
 // toolchain). Each index is processed by exactly one worker, so results that
@@ -309,6 +312,10 @@ void KernelOperator::fill_rows(int row0, int count, double* out) const {
 Mat KernelOperator::apply(const Mat& v) const {
   if (v.rows != n_) throw std::invalid_argument("KernelOperator::apply: dimension mismatch");
   if (!v.all_finite()) throw std::invalid_argument("KernelOperator::apply: non-finite input");
+  if (g_backend && g_backend->apply) {
+    Mat out;
+    if (g_backend->apply(*this, nullptr, n_, v, out)) return out;
+  }
   const int m = v.cols;
   const std::vector<double> vr = to_row_major(v);
   std::vector<double> out(static_cast<size_t>(n_) * m);
@@ -329,6 +336,10 @@ std::vector<std::vector<double>> tiles_buf(std::max(1, std::min(threads_, tiles)
 Mat KernelOperator::apply_rows(const std::vector<int>& rows, const Mat& v) const {
   const int m = v.cols;
   const int count = static_cast<int>(rows.size());
+  if (g_backend && g_backend->apply) {
+    Mat out;
+    if (g_backend->apply(*this, rows.data(), count, v, out)) return out;
+  }
   const std::vector<double> vr = to_row_major(v);
   std::vector<double> out(static_cast<size_t>(count) * m);
   const int chunk = 8;
@@ -445,6 +456,14 @@ std::vector<Vec> KernelOperator::derivative_quadratic_forms_many(
     double acc = 0.0;
     for (size_t e = 0; e < u->size(); ++e) acc += u->a[e] * w->a[e];
     grads[p][d + 1] = 2.0 * hp_.noise_scale() * acc;
+  }
+  if (g_backend && g_backend->quad_forms) {
+    std::vector<Vec> dev;
+    if (g_backend->quad_forms(*this, pairs, dev)) {
+      for (size_t p = 0; p < count; ++p)
+        for (int q = 0; q <= d; ++q) grads[p][q] = dev[p][q];
+      return grads;
+    }
   }
   // Row-major copies of W for contiguous row access.
   std::vector<std::vector<double>> wr(count), ur(count);
@@ -798,10 +817,16 @@ SolverReport solve_sgd(LinearSystemBatch& batch, const SolverConfig& config,
   const int cols = batch.columns();
   SolverReport report;
   report.residuals_estimated = true;
+  if (g_backend && g_backend->solve_sgd && g_backend->solve_sgd(batch, config, report, batches_out, record)) {
+    finalise(report, batch, config.tolerance, start);
+    return report;
+  }
   batch.residuals = batch.targets;
   Mat momentum(n, cols);
   RandomStream rng(config.seed, streams::kSolver, config.substream);
-  const double max_iterations = static_cast<double>(config.max_epochs) * n / b;
+  const double max_iterations = g_sgd_iteration_cap >= 0
+                                    ? std::min<double>(g_sgd_iteration_cap, static_cast<double>(config.max_epochs) * n / b)
+                                    : static_cast<double>(config.max_epochs) * n / b;
   const double step = config.learning_rate / b;
   int t = 0;
   while (t < max_iterations && !termination_check(batch, config.tolerance).done) {
@@ -937,7 +962,8 @@ PathwiseTargets pathwise_targets(const RffBasis& basis, const Hyper& hp, const D
   PathwiseTargets t;
   t.prior_values = Mat(n, s);
   const int RB = 1024;
-  for (int r0 = 0; r0 < n; r0 += RB) {
+  const bool dev = g_backend && g_backend->prior && g_backend->prior(basis, hp, data, s, t.prior_values);
+  for (int r0 = dev ? n : 0; r0 < n; r0 += RB) {
     const int rows = std::min(RB, n - r0);
     Mat pts(rows, d);
     for (int i = 0; i < rows; ++i)

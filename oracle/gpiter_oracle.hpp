@@ -115,6 +115,9 @@ class KernelOperator {
   double signal_variance() const { return signal_variance_; }
   double noise_variance() const { return noise_variance_; }
   int threads() const { return threads_; }
+  int dim() const { return d_; }
+  const double* scaled_inputs() const { return xs_.data(); }  // row-major n x d
+  const Vec& inverse_lengthscales() const { return inv_ls_; }
 
  private:
   void fill_rows(int row0, int count, double* out) const;
@@ -312,5 +315,29 @@ Hyper init_heuristic(const Dataset& data, int n_centroids, int subset, uint64_t 
 // Inputs are rounded to FP32 (the dataset file format); targets too.
 void make_sinsum_dataset(int n, int d, bool uniform, double noise, uint64_t seed,
                          std::vector<float>& x_rowmajor, std::vector<float>& y);
+
+// ---- oracle-at-scale hook (oracle/gpu/, test infrastructure) -------------
+// The CPU oracle leaves this null. liboracle_gpu.so (the same restatement
+// linked with oracle/gpu/oracle_gpu.cu) sets it, and the O(n^2) passes below
+// then run as naive FP64 CUDA restatements of the same loops (same sums, not
+// the same summation order), so the BASELINE configurations C4/C5 whose CPU
+// cost is 1e13..1e15 flops per epoch can be run through the unchanged
+// optimise / solve_* / estimator code. Each hook returns false to decline
+// (the CPU code then runs).
+struct OracleBackend {
+  // out = H[rows, :] v, rows == nullptr: all n rows (kernel.cpp:133-168)
+  bool (*apply)(const KernelOperator& op, const int* rows, int count, const Mat& v, Mat& out);
+  // derivative_quadratic_forms_many (kernel.cpp:238-272)
+  bool (*quad_forms)(const KernelOperator& op, const std::vector<std::pair<const Mat*, const Mat*>>& pairs,
+                     std::vector<Vec>& out);
+  // rff prior values rff_features(X) W[:, :s] (rff.cpp:64-73)
+  bool (*prior)(const RffBasis& basis, const Hyper& hp, const Dataset& data, int s, Mat& prior);
+  // solve_sgd (solvers.cpp:147-184) with the n x m state device-resident
+  bool (*solve_sgd)(LinearSystemBatch& b, const SolverConfig& c, SolverReport& rep,
+                    std::vector<std::vector<int>>* batches_out, int record);
+};
+extern const OracleBackend* g_backend;
+// Test knob: stop solve_sgd after this many iterations (-1: the epoch budget only).
+extern int g_sgd_iteration_cap;
 
 }  // namespace oracle

@@ -74,6 +74,42 @@ def use_timing_build():
     return _LIB_PATH
 
 
+_gpu_lib = None
+
+
+class gpu_backend:
+    """Context manager: oracle calls inside run through oracle/build/liboracle_gpu.so,
+    the same restatement with its O(n^2) passes (apply, apply_rows, quadratic forms,
+    RFF prior, solve_sgd) as naive FP64 CUDA kernels (oracle/gpu/oracle_gpu.cu) --
+    the oracle-at-scale for C4/C5. Needs a GPU; test infrastructure only."""
+
+    def __init__(self, device=0):
+        self.device = device
+
+    def __enter__(self):
+        global _lib, _gpu_lib
+        if _gpu_lib is None:
+            path = os.path.join(_HERE, "build", "liboracle_gpu.so")
+            if not os.path.exists(path):
+                subprocess.run(["make", "-s", "-C", _HERE, "gpu"], check=True)
+            _gpu_lib = C.CDLL(path)
+            _gpu_lib.oracle_last_error.restype = C.c_char_p
+            _gpu_lib.oracle_softplus.restype = C.c_double
+            _gpu_lib.oracle_softplus.argtypes = [C.c_double]
+            _gpu_lib.oracle_sigmoid.restype = C.c_double
+            _gpu_lib.oracle_sigmoid.argtypes = [C.c_double]
+        if _gpu_lib.oracle_gpu_enable(self.device, 1) != 0:
+            raise RuntimeError("oracle_gpu_enable failed (no GPU?)")
+        self._saved = lib()
+        _lib = _gpu_lib
+        return self
+
+    def __exit__(self, *exc):
+        global _lib
+        _lib = self._saved
+        return False
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -286,6 +322,11 @@ def solve(X, raw, targets, config, warm=None, explicit_rank=-1, threads=1, recor
     if batches is not None:
         out["batches"] = batches
     return out
+
+
+def set_sgd_iteration_cap(cap):
+    """Test knob: solve_sgd stops after `cap` iterations (-1: epoch budget only)."""
+    lib().oracle_set_sgd_iteration_cap(int(cap))
 
 
 def termination_check(targets, residuals, tol):

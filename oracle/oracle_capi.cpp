@@ -93,6 +93,8 @@ SolverConfig to_cfg(const SolverConfigC* c) {
 
 extern "C" {
 
+void oracle_set_sgd_iteration_cap(int cap) { g_sgd_iteration_cap = cap; }
+
 const char* oracle_last_error() { return g_err.c_str(); }
 
 void oracle_philox(const unsigned long long* counter, const unsigned long long* key, unsigned long long* out) {

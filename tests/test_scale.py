@@ -1,0 +1,173 @@
+"""Parity at the two BASELINE configurations the CPU oracle cannot run in full.
+
+The fixtures tests/golden/c4_scale.npz and c5_scale.npz come from the
+oracle-at-scale (oracle/gpu/oracle_gpu.cu: the FP64 restatement with its O(n^2)
+passes as naive FP64 CUDA kernels; tools/make_golden_scale.py). It is pinned
+two ways: against the CPU oracle on small problems (GPU test below, 1e-10) and
+against the CPU oracle at full C4 size on the first SGD iterations (CPU test
+below, the whole 393216 x 65 state). The product is then held to the
+north-star bars against the fixtures (GPU tests)."""
+import os
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+C4 = dict(n=393216, d=3, uniform=True, noise=0.05)
+C5 = dict(n=1835008, d=11, uniform=False, noise=0.1)
+
+
+def fixture(name):
+    path = os.path.join(GOLD, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated (tools/make_golden_scale.py on a GPU box)")
+    return dict(np.load(path))
+
+
+def c4_problem(oracle):
+    X32, y32 = oracle.sinsum_dataset(C4["n"], C4["d"], C4["uniform"], C4["noise"], 0)
+    X = np.asfortranarray(X32.astype(np.float64))
+    n, m = X.shape[0], 65
+    T = np.asfortranarray(oracle.stream_draw(11, 2, 0, "gaussian", n * m).reshape((n, m), order="F"))
+    return X, y32.astype(np.float64), T
+
+
+def c4_sgd_config(oracle):
+    return oracle.solver_config(kind=2, tolerance=0.01, max_epochs=10, batch_size=512, learning_rate=10.0,
+                                momentum=0.9, seed=4)
+
+
+def test_c4_sgd_replay_cpu_oracle_matches_scale_fixture(oracle):
+    """The CPU oracle's first 8 SGD iterations at the full C4 size (n = 393216,
+    65 RHS, minibatch 512) against the oracle-at-scale's: pins the GPU
+    restatement of solve_sgd/apply_rows at the headline configuration."""
+    g = fixture("c4_scale.npz")
+    X, _, T = c4_problem(oracle)
+    oracle.set_sgd_iteration_cap(int(g["replay_iterations"]))
+    try:
+        r = oracle.solve(X, g["replay_raw"], T, c4_sgd_config(oracle), threads=os.cpu_count())
+    finally:
+        oracle.set_sgd_iteration_cap(-1)
+    assert r["iterations"] == int(g["replay_iterations"])
+    sol = r["solutions"][g["replay_rows"]]
+    ref = g["replay_solutions"]
+    assert np.max(np.abs(sol - ref)) <= 1e-11 * np.max(np.abs(ref))
+    assert np.allclose(r["solutions"].sum(axis=0), g["replay_colsum"], rtol=1e-11, atol=1e-11)
+    assert abs(r["mean_residual_norm"] - g["replay_mean_residual_norm"]) <= 1e-12 * g["replay_mean_residual_norm"]
+    assert abs(r["probe_residual_norm"] - g["replay_probe_residual_norm"]) <= 1e-12 * g["replay_probe_residual_norm"]
+
+
+@pytest.mark.gpu
+def test_gpu_oracle_at_scale_matches_cpu_oracle(oracle):
+    """Every pass the oracle-at-scale replaces, against the CPU oracle on a
+    problem the CPU finishes in seconds (FP64 both sides; sums in another
+    order, so within 1e-10 relative, not bitwise)."""
+    n, d, s = 1536, 5, 16
+    m = s + 1
+    X32, y32 = oracle.sinsum_dataset(n, d, False, 0.1, 0)
+    X = np.asfortranarray(X32.astype(np.float64))
+    raw = oracle.raw_from_constrained([0.8, 1.1, 0.9, 1.3, 0.7, 1.2, 0.2])
+    rng = np.random.default_rng(5)
+    V = np.asfortranarray(rng.standard_normal((n, m)))
+    rows = np.sort(rng.choice(n, 300, replace=False)).astype(np.int32)
+    U = np.asfortranarray(rng.standard_normal((n, s)))
+    vy = rng.standard_normal(n)
+
+    def passes():
+        hv = oracle.apply(X, raw, V, threads=4)
+        hr = oracle.apply_rows(X, raw, rows, V, threads=4)
+        gr = oracle.gradient(X, raw, vy, U, threads=4)
+        pt = oracle.pathwise_targets(X, raw, 256, s, s, 3)
+        sgd = oracle.solve(X, raw, V, oracle.solver_config(kind=2, tolerance=1e-9, max_epochs=3, batch_size=128,
+                                                           learning_rate=5.0, momentum=0.9, seed=4), threads=4)
+        cg = oracle.solve(X, raw, V, oracle.solver_config(kind=0, tolerance=1e-3, max_epochs=40), threads=4)
+        return hv, hr, gr, pt, sgd, cg
+
+    cpu = passes()
+    with oracle.gpu_backend(0):
+        dev = passes()
+    for a, b in zip(cpu[:2], dev[:2]):
+        assert np.max(np.abs(a - b)) <= 1e-10 * np.max(np.abs(a))
+    for k in ("values", "quadratic_term", "trace_term"):
+        a, b = cpu[2][k], dev[2][k]
+        assert np.max(np.abs(a - b)) <= 1e-10 * np.max(np.abs(a)), k
+    assert np.max(np.abs(cpu[3]["prior_values"] - dev[3]["prior_values"])) <= \
+        1e-10 * np.max(np.abs(cpu[3]["prior_values"]))
+    for key in ("sgd", "cg"):
+        a, b = cpu[4 if key == "sgd" else 5], dev[4 if key == "sgd" else 5]
+        assert a["iterations"] == b["iterations"]
+        assert np.max(np.abs(a["solutions"] - b["solutions"])) <= 1e-9 * np.max(np.abs(a["solutions"]))
+        assert abs(a["mean_residual_norm"] - b["mean_residual_norm"]) <= 1e-8 * a["mean_residual_norm"]
+
+
+def _product_c4(gpk_ctx, g):
+    import paper_2405_18457_b200 as G
+    X32, _ = G.sinsum_dataset(C4["n"], C4["d"], C4["uniform"], C4["noise"], 0)
+    return G.KernelOperator(X32.astype(np.float64), G.Hyperparameters.from_raw(g["replay_raw"]), gpk_ctx)
+
+
+@pytest.mark.gpu
+def test_gpu_c4_sgd_solve_matches_scale_fixture(gpk_ctx, oracle):
+    """One full C4 SGD solve (10 epochs = 7680 minibatch iterations, 65 RHS)
+    against the oracle-at-scale: north-star bars on the (tracked) residual
+    norms (1e-4 relative) and the iteration count (exact: budget-bound)."""
+    import paper_2405_18457_b200 as G
+    g = fixture("c4_scale.npz")
+    op = _product_c4(gpk_ctx, g)
+    _, _, T = c4_problem(oracle)
+    batch = G.LinearSystemBatch(op, T)
+    rep = G.solve_sgd(batch, G.SolverConfig(kind=2, tolerance=0.01, max_epochs=10, batch_size=512,
+                                            learning_rate=10.0, momentum=0.9, seed=4))
+    assert rep.iterations == int(g["full_iterations"])
+    for key in ("mean_residual_norm", "probe_residual_norm"):
+        ref = float(g["full_" + key])
+        assert abs(getattr(rep, key) - ref) <= 1e-4 * ref, (key, getattr(rep, key), ref)
+    sol = batch.solutions
+    ref = g["full_solutions"]
+    err = np.max(np.abs(sol[g["full_rows"]] - ref), axis=0) / np.max(np.abs(ref), axis=0)
+    assert np.max(err) <= 1e-4, np.max(err)
+
+
+def _optimise(G, gpk_ctx, cfg, steps, name_cfg, s, pairs, kind, max_epochs, batch, lr):
+    X32, y32 = G.sinsum_dataset(cfg["n"], cfg["d"], cfg["uniform"], cfg["noise"], 0)
+    sc = G.SolverConfig(kind=kind, tolerance=0.01, max_epochs=max_epochs, batch_size=batch, learning_rate=lr,
+                        momentum=0.9, preconditioner_rank=100)
+    oc = G.OuterConfig(estimator=1, solver=sc, warm_start=True, steps=steps, learning_rate=0.1, probe_count=s,
+                       rff_pairs=pairs, probe_seed=2, feature_seed=3, solver_seed=4)
+    return G.optimise(gpk_ctx, X32.astype(np.float64), y32.astype(np.float64), oc,
+                      init_constrained=[1.0] * cfg["d"] + [1.0, 0.1])
+
+
+def _check_steps(r, g, norm_tol=1e-4, grad_tol=1e-4):
+    assert np.max(np.abs(r["constrained"] - g["traj_constrained"]) / g["traj_constrained"]) <= 1e-3
+    assert np.all(np.abs(r["iterations"] - g["traj_iterations"]) <= 1), (r["iterations"], g["traj_iterations"])
+    same = r["iterations"] == g["traj_iterations"]
+    for key in ("mean_residual_norm", "probe_residual_norm"):
+        a, b = r[key][same], g["traj_" + key][same]
+        assert np.max(np.abs(a - b) / b) <= norm_tol, (key, a, b)
+    gg = g["traj_gradient"]
+    rel = np.abs(r["gradient"] - gg) / np.maximum(np.abs(gg), 1e-3 * np.abs(gg).max(axis=1, keepdims=True))
+    assert np.max(rel) <= grad_tol, np.max(rel)
+
+
+@pytest.mark.gpu
+def test_gpu_c4_steps_match_scale_fixture(gpk_ctx):
+    """BASELINE configs[3]: the first 2 marginal-likelihood steps (SGD b=512,
+    momentum 0.9, lr 10, 10 epochs per step, pathwise s=64, 1000 RFF pairs,
+    warm start) against the oracle-at-scale at the north-star bars."""
+    import paper_2405_18457_b200 as G
+    g = fixture("c4_scale.npz")
+    r = _optimise(G, gpk_ctx, C4, 2, "C4", 64, 1000, 2, 10, 512, 10.0)
+    _check_steps(r, g)
+
+
+@pytest.mark.gpu
+def test_gpu_c5_step_matches_scale_fixture(gpk_ctx):
+    """BASELINE configs[4]: the first marginal-likelihood step (CG early-stopped
+    at 5 epochs, rank-100 preconditioner, pathwise s=64, 2048 RFF pairs) of the
+    1.8M-point problem against the oracle-at-scale."""
+    import paper_2405_18457_b200 as G
+    g = fixture("c5_scale.npz")
+    r = _optimise(G, gpk_ctx, C5, 1, "C5", 64, 2048, 0, 5, 500, 30.0)
+    _check_steps(r, g)
