@@ -105,6 +105,13 @@ class KernelOperator {
     return out;
   }
   Matrix dense() const { return dense_block(0, n_, 0, n_); }
+  // kernel.hpp:71 -- std::out_of_range for a parameter index outside [0, d + 2)
+  Matrix derivative_apply(int k, const Matrix& v) const {
+    if (v.rows != n_) throw std::invalid_argument("KernelOperator::derivative_apply: dimension mismatch");
+    Matrix out(n_, v.cols);
+    check(gpk_derivative_apply(op_, k, v.data(), v.cols, out.data()));
+    return out;
+  }
   Vector kernel_column(int i) const {
     Vector out(n_);
     check(gpk_kernel_column(op_, i, out.data()));

@@ -145,6 +145,10 @@ gpk_status gpk_apply_rows(gpk_operator* op, const int* rows, int count, const do
 gpk_status gpk_apply_columns(gpk_operator* op, int c0, int len, const double* u, int m, double* out);
 /* Dense H[r0:r0+rows, c0:c0+cols] (kernel.cpp:179-184), evaluated in FP64. */
 gpk_status gpk_dense_block(gpk_operator* op, int r0, int rows, int c0, int cols, double* out);
+/* (dH/dtheta_k) V for parameter k of [l_1..l_d, signal, noise] in FP64, V n x m
+ * column-major (derivative_apply, kernel.hpp:71, kernel.cpp:200-236):
+ * GPK_ERANGE for k outside [0, d+2) as the reference's std::out_of_range. */
+gpk_status gpk_derivative_apply(gpk_operator* op, int k, const double* v, int m, double* out);
 /* Column i of K (no noise) in FP64 (kernel.cpp:188-194); diag(K) (196-198). */
 gpk_status gpk_kernel_column(gpk_operator* op, int i, double* out);
 gpk_status gpk_kernel_diagonal(gpk_operator* op, double* out);

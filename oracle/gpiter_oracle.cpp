@@ -19,6 +19,25 @@ namespace oracle {
 
 const OracleBackend* g_backend = nullptr;
 int g_sgd_iteration_cap = -1;
+int g_apply_order = 0;
+double g_apply_noise = 0.0;
+namespace {
+unsigned long long g_apply_calls = 0;
+// Sensitivity knob: out *= 1 + eps u, u in [-1, 1) from a counter hash
+// (splitmix64 of (call, element)), deterministic across runs.
+void perturb(std::vector<double>& out) {
+  if (g_apply_noise == 0.0) return;
+  const unsigned long long call = g_apply_calls++;
+  for (size_t e = 0; e < out.size(); ++e) {
+    unsigned long long z = call * 0x9E3779B97F4A7C15ull + e + 1;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const double u = static_cast<double>(z >> 11) * 0x1.0p-52 - 1.0;
+    out[e] *= 1.0 + g_apply_noise * u;
+  }
+}
+}  // namespace
 
 namespace {
 // Dynamic parallel-for over [0, count) with std::thread (no OpenMP in this
@@ -224,6 +243,20 @@ void accumulate_rows_product(const double* a, int rows, int n, const double* v, 
   }
 }
 
+// Sensitivity variant (test knob g_apply_order = 1): the same products summed
+// in descending column order.
+void accumulate_rows_product_reversed(const double* a, int rows, int n, const double* v, int m, double* out) {
+  for (int r = 0; r < rows; ++r) {
+    double* acc = out + static_cast<size_t>(r) * m;
+    std::fill(acc, acc + m, 0.0);
+    for (int c = n - 1; c >= 0; --c) {
+      const double coeff = a[static_cast<size_t>(r) * n + c];
+      const double* vrow = v + static_cast<size_t>(c) * m;
+      for (int j = 0; j < m; ++j) acc[j] += coeff * vrow[j];
+    }
+  }
+}
+
 std::vector<double> to_row_major(const Mat& v) {
   std::vector<double> out(v.size());
   for (int i = 0; i < v.rows; ++i)
@@ -314,7 +347,12 @@ Mat KernelOperator::apply(const Mat& v) const {
   if (!v.all_finite()) throw std::invalid_argument("KernelOperator::apply: non-finite input");
   if (g_backend && g_backend->apply) {
     Mat out;
-    if (g_backend->apply(*this, nullptr, n_, v, out)) return out;
+    if (g_backend->apply(*this, nullptr, n_, v, out)) {
+      if (g_apply_noise != 0.0) {
+        perturb(out.a);  // column-major here; any fixed element order will do
+      }
+      return out;
+    }
   }
   const int m = v.cols;
   const std::vector<double> vr = to_row_major(v);
@@ -327,8 +365,12 @@ std::vector<std::vector<double>> tiles_buf(std::max(1, std::min(threads_, tiles)
     const int r0 = t * block_rows_;
     const int rows = std::min(block_rows_, n_ - r0);
     fill_rows(r0, rows, tile.data());
-    accumulate_rows_product(tile.data(), rows, n_, vr.data(), m, out.data() + static_cast<size_t>(r0) * m);
+    if (g_apply_order == 1)
+      accumulate_rows_product_reversed(tile.data(), rows, n_, vr.data(), m, out.data() + static_cast<size_t>(r0) * m);
+    else
+      accumulate_rows_product(tile.data(), rows, n_, vr.data(), m, out.data() + static_cast<size_t>(r0) * m);
   });
+  perturb(out);
   return from_row_major(out, n_, m);
 }
 

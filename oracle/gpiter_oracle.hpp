@@ -339,5 +339,10 @@ struct OracleBackend {
 extern const OracleBackend* g_backend;
 // Test knob: stop solve_sgd after this many iterations (-1: the epoch budget only).
 extern int g_sgd_iteration_cap;
+// Sensitivity knobs for apply() (the full H.V product; tests only):
+// g_apply_order 1 sums each output in descending column order; g_apply_noise
+// eps multiplies every output entry by 1 + eps u, u uniform in [-1, 1).
+extern int g_apply_order;
+extern double g_apply_noise;
 
 }  // namespace oracle

@@ -329,6 +329,12 @@ def set_sgd_iteration_cap(cap):
     lib().oracle_set_sgd_iteration_cap(int(cap))
 
 
+def set_apply_sensitivity(order=0, noise=0.0):
+    """Test knobs of KernelOperator::apply: order 1 sums in descending column
+    order, noise eps perturbs every output entry by a factor 1 + eps u, u ~ U[-1, 1)."""
+    lib().oracle_set_apply_sensitivity(int(order), C.c_double(noise))
+
+
 def termination_check(targets, residuals, tol):
     T, R = _f(targets), _f(residuals)
     mean, probe, done = C.c_double(), C.c_double(), C.c_int()

@@ -94,6 +94,10 @@ SolverConfig to_cfg(const SolverConfigC* c) {
 extern "C" {
 
 void oracle_set_sgd_iteration_cap(int cap) { g_sgd_iteration_cap = cap; }
+void oracle_set_apply_sensitivity(int order, double noise) {
+  g_apply_order = order;
+  g_apply_noise = noise;
+}
 
 const char* oracle_last_error() { return g_err.c_str(); }
 

@@ -73,6 +73,7 @@ def _sig(lib):
         "gpk_apply_rows": (C.c_int, [H, ip, C.c_int, dp, C.c_int, dp]),
         "gpk_apply_columns": (C.c_int, [H, C.c_int, C.c_int, dp, C.c_int, dp]),
         "gpk_dense_block": (C.c_int, [H, C.c_int, C.c_int, C.c_int, C.c_int, dp]),
+        "gpk_derivative_apply": (C.c_int, [H, C.c_int, dp, C.c_int, dp]),
         "gpk_kernel_column": (C.c_int, [H, C.c_int, dp]),
         "gpk_kernel_diagonal": (C.c_int, [H, dp]),
         "gpk_derivative_quadratic_forms_many": (C.c_int, [H, C.c_int, C.POINTER(dp), C.POINTER(dp), ip, dp]),

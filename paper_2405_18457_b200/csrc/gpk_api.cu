@@ -172,6 +172,7 @@ struct gpk_ctx {
   int kv_deep = -1;  // operator launches one CTA per SM with 16 eval warps: -1 auto (>= 1e8 entries), 0/1 forced
   bool kv_streamk = false;  // deep launches as stream-K (GPK_KV_STREAMK=1); measured 1-7% slower than the 2-D grid
   bool graphs = true;  // CG/AP iteration groups as CUDA graphs (GPK_GRAPHS=0 disables)
+  bool sgd_lazy = true;  // SGD: lazily evaluated momentum + sgd_slab_kernel (GPK_SGD_LAZY=0: full-state passes)
   void* blas_ws = nullptr;  // cuBLAS workspace (graph capture)
   DBuf<double*> ptr_a, ptr_b;  // batched-factorisation pointer arrays
   DBuf<int> info;
@@ -253,6 +254,11 @@ struct gpk_batch {
   DBuf<unsigned> ticket;             // last-block ticket of fused reductions (kept at 0 between uses)
   DBuf<float> apk;                   // AP block update's TF32 operator images
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
+  // lazy-momentum SGD (sgd_lazy.cu): FP32 records, last-update iterations,
+  // S / rho^Delta tables, slab partials, apply-block partials, flags
+  DBuf<float> sgd_rec, sgd_s32;
+  DBuf<int> sgd_tau, sgd_flags;
+  DBuf<double> sgd_tab, sgd_part, sgd_gpart;
   DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
   DBuf<double> ap_cpart;             // persistent AP: block-update partials [8][block][m]
   DBuf<unsigned long long> ap_prof;  // persistent AP development phase clock (GPK_AP_PROF)
@@ -516,7 +522,13 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   a.part = part;
   a.splits = splits;
   a.cols_per_split = cps;
-  a.flush_chunks = fused ? std::max(16, (cps + 31) / 32) : 16;
+  // FP32 TMEM accumulation spans flush_chunks 32-column chunks before the FP64
+  // partial (GPK_FLUSH_CHUNKS: parity experiments; default 16 = 512 columns)
+  static const int flush_default = [] {
+    const char* e = std::getenv("GPK_FLUSH_CHUNKS");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
+  a.flush_chunks = fused ? std::max(flush_default, (cps + 31) / 32) : flush_default;
   a.skip = c.skip;
   a.stats = op->ctx->stats;
   a.d = op->d;
@@ -1619,6 +1631,180 @@ void solve_sgd_tc(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* r
   finalise(b, c->tolerance, rep, start);
 }
 
+// Per-launch CUDA-event bracket of an operator launch while profiling is on
+// (gpk_ctx_stats' launch count and milliseconds).
+cudaEvent_t* prof_begin(gpk_ctx* ctx, cudaStream_t s) {
+  if (!ctx->profiling) return nullptr;
+  if (ctx->prof_used == ctx->prof.size()) {
+    cudaEvent_t e0, e1;
+    GPK_CUDA(cudaEventCreate(&e0));
+    GPK_CUDA(cudaEventCreate(&e1));
+    ctx->prof.push_back({e0, e1});
+  }
+  auto& pr = ctx->prof[ctx->prof_used++];
+  GPK_CUDA(cudaEventRecord(pr.first, s));
+  return &pr.second;
+}
+
+// SGD with lazily evaluated momentum (sgd_lazy.cu): per iteration the
+// minibatch product on the tensor cores builds V(t) from the rows' FP32
+// records, and only the b minibatch rows of the state are written. One rank
+// or row-sharded: the slab contracts against this rank's rows,
+// the b x m partials (+ own diagonal / target terms, old residual squares)
+// are all-gathered and summed in rank order, so every rank holds the same g
+// and takes the same decisions. Iterations run as CUDA graphs of 256
+// (minibatches for the group generated at its start from the device counter).
+bool sgd_lazy_supported(gpk_operator* op, int m, int bs) {
+  return op->ctx->kernel == 1 && op->ctx->sgd_lazy && m <= 80 && op->dp <= 16 && bs <= 1024;
+}
+
+void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep, int bs, int budget,
+                    double step, Clock::time_point start) {
+  gpk_operator* op = b->op;
+  gpk_ctx* ctx = op->ctx;
+  cudaStream_t s = ctx->stream;
+  const int n = op->n, nloc = b->n, m = b->m, G = kReduceGroups, nr = op->nr;
+  const int row0 = op->sharded ? op->row0 : 0;
+  const size_t nm = static_cast<size_t>(nloc) * m;
+  GPK_CUDA(cudaMemcpyAsync(b->residuals.p, b->targets.p, sizeof(double) * nm, cudaMemcpyDeviceToDevice, s));
+  double* Mb = b->w1.ensure(nm);
+  GPK_CUDA(cudaMemsetAsync(Mb, 0, sizeof(double) * nm, s));
+  int moff = 0;
+  const int rw = sgd_record_width(m, &moff);
+  const int rows_pad = (nloc + 31) / 32 * 32;
+  float* rec = b->sgd_rec.ensure(static_cast<size_t>(rows_pad) * rw);
+  int* tau = b->sgd_tau.ensure(rows_pad);
+  sgd_records_init_launch(b->solutions.p, nloc, rows_pad, m, rw, moff, rec, tau, s);
+  // P(Delta) = rho^Delta, S(Delta) = rho + ... + rho^Delta by the recurrence an
+  // untouched row follows in the reference (momentum *= rho; solutions += momentum)
+  {
+    std::vector<double> tab(2 * static_cast<size_t>(budget + 1));
+    std::vector<float> t32(budget + 1);
+    double* S = tab.data();
+    double* P = tab.data() + budget + 1;
+    P[0] = 1.0;
+    S[0] = 0.0;
+    for (int k = 1; k <= budget; ++k) {
+      P[k] = P[k - 1] * c->momentum;
+      S[k] = S[k - 1] + P[k];
+    }
+    for (int k = 0; k <= budget; ++k) t32[k] = static_cast<float>(S[k]);
+    GPK_CUDA(cudaMemcpyAsync(b->sgd_tab.ensure(tab.size()), tab.data(), sizeof(double) * tab.size(),
+                             cudaMemcpyHostToDevice, s));
+    GPK_CUDA(cudaMemcpyAsync(b->sgd_s32.ensure(t32.size()), t32.data(), sizeof(float) * t32.size(),
+                             cudaMemcpyHostToDevice, s));
+    GPK_CUDA(cudaStreamSynchronize(s));
+  }
+  const double* s64 = b->sgd_tab.p;
+  const double* p64 = b->sgd_tab.p + budget + 1;
+  const int tiles = (bs + 127) / 128;
+  int splits = std::max(1, ctx->sms / tiles);
+  int cps = (nloc + splits - 1) / splits;
+  cps = (cps + 31) / 32 * 32;
+  splits = std::max(1, (nloc + cps - 1) / cps);
+  double* part = b->sgd_part.ensure(static_cast<size_t>(splits) * bs * m);
+  const long long stride = (static_cast<long long>(bs) * m + m + 1 + 31) / 32 * 32;  // doubles per rank slice
+  double* gbuf = b->w4.ensure(static_cast<size_t>(nr) * stride);
+  double* red = b->red.ensure(static_cast<size_t>(nr) * G * 2 * m + 8);
+  double* sumsq = b->vec1.ensure(m);
+  int* flags = b->sgd_flags.ensure(2);
+  GPK_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+  unsigned* ticket = b->ticket.ensure(1);
+  GPK_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
+  double* gpart = b->sgd_gpart.ensure(static_cast<size_t>((bs + 7) / 8) * m);
+  col_reduce_launch(b->residuals.p, nullptr, nloc, m, m, 2, red + static_cast<size_t>(op->rk) * G * m, G, nullptr, s);
+  gather_inplace(op, red, sizeof(double) * G * m);
+  sum_partials_launch(red, G * nr, m, sumsq, nullptr, s);
+  init_ctl(b, budget, -1);
+  CgCtl* ctl = b->ctl.p;
+  sgd_check_launch(sumsq, m, b->scales_dev.p, c->tolerance, flags, ctl, s);  // initial test (loop head)
+  const int chunk = 256;
+  int* idxbuf = b->ibuf.ensure(static_cast<size_t>(chunk) * bs);
+
+  SgdSlabArgs sa{};
+  sa.xs = op->xs32.p;
+  sa.n = n;
+  sa.dp = op->dp;
+  sa.d = op->d;
+  sa.idxbuf = idxbuf;
+  sa.idx_chunk = chunk;
+  sa.R = bs;
+  sa.c0 = row0;
+  sa.C = nloc;
+  sa.rec = rec;
+  sa.rw = rw;
+  sa.moff = moff;
+  sa.tau = tau;
+  sa.s32 = b->sgd_s32.p;
+  sa.budget = budget;
+  sa.ctl = ctl;
+  sa.log2_s2 = static_cast<float>(std::log2(op->s2));
+  sa.part = part;
+  sa.m = m;
+  sa.splits = splits;
+  sa.cols_per_split = cps;
+  static const int flush = [] {
+    const char* e = std::getenv("GPK_SGD_FLUSH");  // FP32 TMEM accumulation span in 32-column chunks
+    return e ? std::max(5, std::atoi(e)) : 8;
+  }();
+  sa.flush = flush;
+  sa.stats = ctx->stats;
+  SgdStepArgs ta{};
+  ta.ctl = ctl;
+  ta.idxbuf = idxbuf;
+  ta.idx_chunk = chunk;
+  ta.b = bs;
+  ta.m = m;
+  ta.row0 = row0;
+  ta.nloc = nloc;
+  ta.part = part;
+  ta.splits = splits;
+  ta.resid = b->residuals.p;
+  ta.Vb = b->solutions.p;
+  ta.Mb = Mb;
+  ta.B = b->targets.p;
+  ta.tau = tau;
+  ta.s64 = s64;
+  ta.p64 = p64;
+  ta.budget = budget;
+  ta.sigma2 = op->sigma2;
+  ta.rho = c->momentum;
+  ta.step = step;
+  ta.tol = c->tolerance;
+  ta.slice = gbuf + static_cast<size_t>(op->sharded ? op->rk : 0) * stride;
+  ta.gbuf = gbuf;
+  ta.stride = stride;
+  ta.nr = nr;
+  ta.nonfinite = flags;
+  ta.nonfinite_now = flags + 1;
+  ta.rec = rec;
+  ta.rw = rw;
+  ta.moff = moff;
+  ta.gpart = gpart;
+  ta.ticket = ticket;
+  ta.sumsq = sumsq;
+  ta.scales = b->scales_dev.p;
+  int t = 0;
+  auto iteration = [&]() {  // solvers.cpp:164-178
+    if (t % chunk == 0) sgd_batches_dev_launch(c->seed, c->substream, n, bs, &ctl->iters, chunk, idxbuf, &ctl->stop, s);
+    cudaEvent_t* pe = prof_begin(ctx, s);
+    sgd_slab_launch(sa, s);
+    if (pe) GPK_CUDA(cudaEventRecord(*pe, s));
+    sgd_reduce_launch(ta, s);
+    gather_inplace(op, gbuf, sizeof(double) * stride);
+    sgd_apply_launch(ta, s);
+    ++t;
+  };
+  drive(b, ctl, chunk, budget, iteration, true);
+  sgd_materialise_launch(b->solutions.p, Mb, tau, s64, budget, ctl, nloc, m, s);
+  const CgCtl h = read_ctl(b);
+  rep->iterations = h.iters;
+  rep->epochs_consumed = static_cast<double>(h.iters) * bs / n;
+  rep->aborted = h.aborted;
+  if (h.aborted) std::strncpy(rep->abort_reason, "sgd divergence: non-finite iterate", 127);
+  finalise(b, c->tolerance, rep, start);
+}
+
 void solve_sgd(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) {
   validate(c);
   const auto start = Clock::now();
@@ -1632,6 +1818,7 @@ void solve_sgd(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep)
   const double max_iterations = static_cast<double>(c->max_epochs) * n / bs;
   const int budget = static_cast<int>(std::ceil(max_iterations));
   const double step = c->learning_rate / bs;
+  if (sgd_lazy_supported(op, m, bs)) return solve_sgd_lazy(b, c, rep, bs, budget, step, start);
   if (op->ctx->kernel == 1) return solve_sgd_tc(b, c, rep, bs, budget, step, start);
   if (op->nr > 1) throw InvalidArgument("gpk: the sharded operator needs the tcgen05 kernel");
   const size_t nm = static_cast<size_t>(n) * m;
@@ -1967,9 +2154,20 @@ void build_basis_host(gpk_rff_basis* b) {  // rff.cpp:10-34
 // prior (row-major [rows][s]) = F W: FP64 feature rows (rff_features_kernel)
 // in chunks of <= 512 MB, contracted with the weights by cuBLAS DGEMM
 // (prior^T = W^T F^T in column-major terms; W is stored [samples][2P]).
+// prior (row-major [rows][s_count]) = Phi(x) W: the streaming kernel (Phi never
+// materialised); GPK_RFF_STREAM=0 selects the earlier features + cuBLAS DGEMM
+// path (row chunks of <= 512 MB of Phi) for A/B runs.
 void rff_prior_gemm(gpk_ctx* ctx, const double* x64, int rows, int d, const double* fd, int P, const double* W,
                     int s_count, double amplitude, double* prior) {
   cudaStream_t s = ctx->stream;
+  static const bool stream_k5 = [] {
+    const char* e = std::getenv("GPK_RFF_STREAM");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (stream_k5) {
+    rff_prior_launch(x64, rows, d, fd, P, amplitude, W, 2 * P, s_count, prior, s);
+    return;
+  }
   const int F = 2 * P;
   const long long chunk = std::max<long long>(1, std::min<long long>(rows, (512LL << 20) / (8LL * F)));
   double* feat = ctx->rff_feat.ensure(static_cast<size_t>(chunk) * F);
@@ -2116,6 +2314,7 @@ gpk_status gpk_ctx_create(int device, gpk_ctx** out) {
     if (const char* e = std::getenv("GPK_KV_STREAMK")) c->kv_streamk = std::atoi(e) != 0;
     if (const char* e = std::getenv("GPK_AP_PERSISTENT")) c->ap_persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("GPK_GRAPHS")) c->graphs = std::atoi(e) != 0;
+    if (const char* e = std::getenv("GPK_SGD_LAZY")) c->sgd_lazy = std::atoi(e) != 0;
     GPK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     {  // the auxiliary stream (AP block inverses: chains of small latency-bound
        // launches) runs at the highest priority, so its blocks are scheduled
@@ -2422,6 +2621,26 @@ gpk_status gpk_dense_block(gpk_operator* op, int r0, int rows, int c0, int cols,
     dense_block64_launch(op->xs64.p, op->n, op->d, op->s2, op->sigma2, r0, rows, c0, cols, o, cols, 1,
                          op->ctx->stream);
     download_colmajor(op, o, rows, cols, out);
+  });
+}
+
+gpk_status gpk_derivative_apply(gpk_operator* op, int k, const double* v, int m, double* out) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    const int n = op->n, d = op->d;
+    if (k < 0 || k >= d + 2) throw OutOfRange("KernelOperator::derivative_apply: parameter index");
+    require(m >= 1 && m <= 80, "KernelOperator::derivative_apply: 1 <= columns <= 80");
+    if (k == d + 1) {  // dH/dsigma = 2 sigma I (kernel.cpp:205-208)
+      const double two_sigma = 2.0 * op->sigma;
+      for (size_t e = 0; e < static_cast<size_t>(n) * m; ++e) out[e] = two_sigma * v[e];
+      return;
+    }
+    double* v64 = op->v64.ensure(static_cast<size_t>(n) * m);
+    upload_colmajor(op, v, n, m, v64);
+    double* o = op->out64.ensure(static_cast<size_t>(n) * m);
+    const double coef = k == d ? 2.0 / op->s : 3.0 * op->s2 * op->inv_ls[k];
+    deriv_apply_launch(op->xs64.p, n, d, k, op->s2, coef, v64, m, o, op->ctx->stream);
+    download_colmajor(op, o, n, m, out);
   });
 }
 

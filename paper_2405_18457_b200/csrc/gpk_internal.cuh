@@ -217,6 +217,68 @@ void grad_tc_pack_launch(const float* w32, int ld, int n, int cols, int kp, floa
                          const float* n_w, int n_ld, float* u1, float* w1, cudaStream_t s);
 void grad_tc_launch(const GradTcArgs& a, cudaStream_t s);
 
+// ---- SGD with lazily evaluated momentum (sgd_lazy.cu) ----------------------
+// Per local row: FP32 record [V32 (m) | pad | M32 (m) | pad] of width rw
+// (sgd_record_width: M32 at moff), the FP64 base state (Vb = the batch's
+// solutions, Mb) and tau = the iteration of its last update (-1: none).
+struct SgdSlabArgs {
+  const float* xs;      // scaled inputs FP32 [n + 128][dp] (global rows)
+  int n, dp, d;
+  const int* idxbuf;    // minibatches: iteration t uses idxbuf + (t % idx_chunk) * R
+  int idx_chunk;
+  int R;                // minibatch size (output rows)
+  int c0, C;            // this rank's columns (global row0, local count)
+  const float* rec;     // [rows_pad][rw]
+  int rw, moff;
+  const int* tau;       // [rows_pad]
+  const float* s32;     // S(Delta), Delta = 0..budget
+  int budget;
+  const CgCtl* ctl;     // iteration t = ctl->iters; no-op once ctl->stop
+  float log2_s2;
+  double* part;         // [splits][R][m] FP64 partials
+  int m, splits, cols_per_split, flush;
+  double* stats;
+};
+struct SgdStepArgs {
+  CgCtl* ctl;
+  const int* idxbuf;
+  int idx_chunk, b, m, row0, nloc;
+  const double* part;   // slab partials
+  int splits;
+  double* resid;        // R [nloc][m] (tracked residual estimate)
+  double* Vb;           // [nloc][m]
+  double* Mb;           // [nloc][m]
+  const double* B;      // targets [nloc][m]
+  int* tau;
+  const double* s64;    // S(Delta)
+  const double* p64;    // rho^Delta
+  int budget;
+  double sigma2, rho, step, tol;
+  double* slice;        // this rank's slice of gbuf: [b*m] partial g, [m] old R^2, [1] flag
+  const double* gbuf;   // all ranks' slices (stride doubles apart)
+  long long stride;
+  int nr;
+  int* nonfinite;       // carried divergence flag (own rows)
+  int* nonfinite_now;   // this iteration's (bit 0 any, bit 1 g itself)
+  float* rec;
+  int rw, moff;
+  double* gpart;        // [blocks][m]
+  unsigned* ticket;     // kept at 0 between launches
+  double* sumsq;        // [m] tracked sum of R^2 per column
+  const double* scales;
+};
+int sgd_record_width(int m, int* moff);
+void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s);
+void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s);
+void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s);
+void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
+                             cudaStream_t s);
+void sgd_materialise_launch(double* Vb, const double* Mb, const int* tau, const double* s64, int budget,
+                            const CgCtl* ctl, int nloc, int m, cudaStream_t s);
+// minibatches for iterations [*first, *first + count) (device-read start)
+void sgd_batches_dev_launch(uint64_t seed, uint64_t substream, int n, int b, const int* first, int count, int* out,
+                            const int* skip, cudaStream_t s);
+
 // ---- misc device kernels (la_kernels.cu) ---------------------------------
 void prescale_launch(const double* x64, int n, int d, int dp, const double* inv_ls, float* xs32,
                      double* xs64, cudaStream_t s);
@@ -359,6 +421,13 @@ void sgd_update_pack_launch(double* M, double* V, double* R, float* vpk, int npa
 void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, const int* skip, cudaStream_t s);
 
 // RFF (K5) + noise (K9)
+// derivative_apply for k <= d (kernel.cpp:200-236), FP64: out [n][m] row-major;
+// coef = 3 s2 / l_k (k < d) or 2 / s (k == d)
+void deriv_apply_launch(const double* xs64, int n, int d, int k, double sv, double coef, const double* v, int m,
+                        double* out, cudaStream_t s);
+// streaming K5: prior [n][s_count] = Phi(x) W without materialising Phi (W column-major, ld ldw)
+void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude,
+                      const double* W, int ldw, int s_count, double* prior, cudaStream_t s);
 void rff_features_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude, double* F,
                          cudaStream_t s);
   // prior row-major [n][s]

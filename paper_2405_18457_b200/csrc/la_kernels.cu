@@ -1181,11 +1181,13 @@ void ap_check_launch(const double* part, int groups, int m, const double* scales
 // (seed, kSolver = 6, substream). The modulo reductions are independent and
 // run in parallel; the sequential collision pass touches only a bitmap; the
 // sorted output is the bitmap's set bits in ascending order.
-__global__ void sgd_batches_kernel(uint64_t seed, uint64_t substream, int n, int b, int first, int* out) {
+__global__ void sgd_batches_kernel(uint64_t seed, uint64_t substream, int n, int b, int first, int* out,
+                                   const int* first_dev = nullptr, const int* skip = nullptr) {
   extern __shared__ unsigned bitmap[];
   __shared__ int tvals[1024];
   __shared__ int wcount[1025];
-  const int t = first + blockIdx.x;
+  if (skip && *skip) return;
+  const int t = (first_dev ? *first_dev : first) + blockIdx.x;
   const int words = (n + 31) / 32;
   for (int w = threadIdx.x; w < words; w += blockDim.x) bitmap[w] = 0u;
   for (int q = threadIdx.x; q < b; q += blockDim.x) {
@@ -1226,8 +1228,7 @@ __global__ void sgd_batches_kernel(uint64_t seed, uint64_t substream, int n, int
     }
   }
 }
-void sgd_batches_launch(uint64_t seed, uint64_t substream, int n, int b, int first, int count, int* out,
-                        cudaStream_t s) {
+size_t sgd_batches_smem(int n, int b) {
   if (b > 1024) throw std::invalid_argument("gpk: SGD batch_size > 1024 is not supported");
   const size_t smem = sizeof(unsigned) * ((n + 31) / 32);
   if (smem > 200 * 1024) throw std::invalid_argument("gpk: SGD sampling supports n <= 1.6M");
@@ -1238,7 +1239,18 @@ void sgd_batches_launch(uint64_t seed, uint64_t substream, int n, int b, int fir
                                   static_cast<int>(smem)));
     configured = smem;
   }
+  return smem;
+}
+void sgd_batches_launch(uint64_t seed, uint64_t substream, int n, int b, int first, int count, int* out,
+                        cudaStream_t s) {
+  const size_t smem = sgd_batches_smem(n, b);
   sgd_batches_kernel<<<count, 256, smem, s>>>(seed, substream, n, b, first, out);
+  check_launch("sgd_batches");
+}
+void sgd_batches_dev_launch(uint64_t seed, uint64_t substream, int n, int b, const int* first, int count, int* out,
+                            const int* skip, cudaStream_t s) {
+  const size_t smem = sgd_batches_smem(n, b);
+  sgd_batches_kernel<<<count, 256, smem, s>>>(seed, substream, n, b, 0, out, first, skip);
   check_launch("sgd_batches");
 }
 
@@ -1623,6 +1635,174 @@ __global__ void __launch_bounds__(RFF_TP) rff_features_kernel(const double* x64,
     out[static_cast<size_t>(i0 + r) * pairs + p] = make_double2(amplitude * c, amplitude * sn);
   }
 }
+// derivative_apply (kernel.cpp:200-236): out[r][j] = sum_c dK_k[r][c] v[c][j]
+// in FP64 for parameter k < d (lengthscale: 3 s2 (1/l_k) e^{-sqrt3 r} dxs_k^2)
+// or k == d (signal: (2/s) k(r)); the noise case (2 sigma V) never reaches the
+// device. CTA = 32 rows; per 32-column chunk the entries go to shared memory
+// and each thread accumulates 4 rows x its columns j = lane + 32 u (ascending c).
+__global__ void __launch_bounds__(256) deriv_apply_kernel(const double* __restrict__ xs, int n, int d, int k,
+                                                          double sv, double coef, const double* __restrict__ v,
+                                                          int m, double* __restrict__ out) {
+  __shared__ double xr[32][33];
+  __shared__ double xc[32][33];
+  __shared__ double kt[32][33];
+  __shared__ double vt[32][80];
+  const int tid = threadIdx.x, lane = tid & 31, rg = tid >> 5;
+  const int r0 = blockIdx.x * 32;
+  for (int e = tid; e < 32 * d; e += 256) {
+    const int r = e / d, q = e % d;
+    xr[r][q] = r0 + r < n ? xs[static_cast<size_t>(r0 + r) * d + q] : 0.0;
+  }
+  double acc[4][3] = {};
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int cn = min(32, n - c0);
+    __syncthreads();
+    for (int e = tid; e < 32 * d; e += 256) {
+      const int c = e / d, q = e % d;
+      xc[c][q] = c < cn ? xs[static_cast<size_t>(c0 + c) * d + q] : 0.0;
+    }
+    for (int e = tid; e < 32 * m; e += 256) {
+      const int c = e / m, j = e % m;
+      vt[c][j] = c < cn ? v[static_cast<size_t>(c0 + c) * m + j] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += 256) {
+      const int c = e >> 5, r = e & 31;
+      double r2 = 0.0;
+      for (int q = 0; q < d; ++q) {
+        const double t = xc[c][q] - xr[r][q];
+        r2 += t * t;
+      }
+      const double rr = sqrt(r2);
+      double val;
+      if (k == d) {
+        val = coef * (sv * (1.0 + kSqrt3 * rr) * exp(-kSqrt3 * rr));
+      } else {
+        const double dk = xc[c][k] - xr[r][k];
+        val = coef * exp(-kSqrt3 * rr) * (dk * dk);
+      }
+      kt[c][r] = c < cn ? val : 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < cn; ++c)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double kv = kt[c][rg * 4 + a];
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+          if (lane + 32 * u < m) acc[a][u] = fma(kv, vt[c][lane + 32 * u], acc[a][u]);
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = r0 + rg * 4 + a;
+    if (r >= n) continue;
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (lane + 32 * u < m) out[static_cast<size_t>(r) * m + lane + 32 * u] = acc[a][u];
+  }
+}
+void deriv_apply_launch(const double* xs64, int n, int d, int k, double sv, double coef, const double* v, int m,
+                        double* out, cudaStream_t s) {
+  if (d > 32 || m > 80) throw std::invalid_argument("gpk: derivative_apply supports d <= 32 and m <= 80");
+  deriv_apply_kernel<<<(n + 31) / 32, 256, 0, s>>>(xs64, n, d, k, sv, coef, v, m, out);
+  check_launch("deriv_apply");
+}
+
+// K5, streaming (rff.cpp:36-54, 64-73): prior[i][j] = sum_q phi_q(x_i) W[q][j]
+// without materialising Phi. CTA = 64 rows x 64 samples; per chunk of 16
+// pairs the CTA forms phi (FP64 angles, sincos, interleaved cos/sin as
+// rff.cpp:48-52) for its rows in shared memory next to the chunk of W, and
+// each thread accumulates a 4 x 4 block of the product over features in
+// ascending order (FP64 FMA).
+constexpr int RP_ROWS = 64, RP_COLS = 64, RP_PAIRS = 16, RP_F = 2 * RP_PAIRS;
+__global__ void __launch_bounds__(256) rff_prior_kernel(const double* __restrict__ x64, int n, int d,
+                                                        const double* __restrict__ freq, int pairs, double amplitude,
+                                                        const double* __restrict__ W, int ldw, int s_count,
+                                                        double* __restrict__ prior) {
+  extern __shared__ double rp_sm[];
+  double* xt = rp_sm;                      // [64][d]
+  double* ph = xt + RP_ROWS * d;           // [32 features][64 rows]
+  double* wt = ph + RP_F * RP_ROWS;        // [32 features][64 samples]
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.x * RP_ROWS, j0 = blockIdx.y * RP_COLS;
+  const int rows = min(RP_ROWS, n - i0);
+  for (int e = tid; e < RP_ROWS * d; e += 256) xt[e] = e < rows * d ? x64[static_cast<size_t>(i0) * d + e] : 0.0;
+  const int tr = tid >> 4, tc = tid & 15;  // rows 4 tr .. 4 tr + 3, samples 4 tc .. 4 tc + 3
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int p0 = 0; p0 < pairs; p0 += RP_PAIRS) {
+    const int pn = min(RP_PAIRS, pairs - p0);
+    __syncthreads();
+    for (int e = tid; e < RP_ROWS * RP_PAIRS; e += 256) {
+      const int r = e & (RP_ROWS - 1), pp = e / RP_ROWS;
+      double cv = 0.0, sv = 0.0;
+      if (pp < pn) {
+        double a0 = 0.0, a1 = 0.0;  // two chains summed in a fixed order, as rff_features_kernel
+        for (int k = 0; k < d; k += 2) {
+          a0 = fma(xt[r * d + k], freq[static_cast<size_t>(k) * pairs + p0 + pp], a0);
+          if (k + 1 < d) a1 = fma(xt[r * d + k + 1], freq[static_cast<size_t>(k + 1) * pairs + p0 + pp], a1);
+        }
+        const double ang = a0 + a1;
+        if (fabs(ang) < 1073741824.0)
+          sincos_rr(ang, &sv, &cv);
+        else
+          sincos(ang, &sv, &cv);
+        cv *= amplitude;
+        sv *= amplitude;
+      }
+      ph[(2 * pp) * RP_ROWS + r] = cv;
+      ph[(2 * pp + 1) * RP_ROWS + r] = sv;
+    }
+    for (int e = tid; e < RP_F * RP_COLS; e += 256) {
+      const int q = e & (RP_F - 1), c = e / RP_F;
+      wt[q * RP_COLS + c] =
+          (q < 2 * pn && j0 + c < s_count) ? W[static_cast<size_t>(j0 + c) * ldw + 2 * p0 + q] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int q = 0; q < RP_F; ++q) {
+      const double2 pa = *reinterpret_cast<const double2*>(ph + q * RP_ROWS + 4 * tr);
+      const double2 pb = *reinterpret_cast<const double2*>(ph + q * RP_ROWS + 4 * tr + 2);
+      const double2 wa = *reinterpret_cast<const double2*>(wt + q * RP_COLS + 4 * tc);
+      const double2 wb = *reinterpret_cast<const double2*>(wt + q * RP_COLS + 4 * tc + 2);
+      const double pv[4] = {pa.x, pa.y, pb.x, pb.y}, wv[4] = {wa.x, wa.y, wb.x, wb.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(pv[a], wv[b], acc[a][b]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = 4 * tr + a;
+    if (r >= rows) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + 4 * tc + b;
+      if (j < s_count) prior[static_cast<size_t>(i0 + r) * s_count + j] = acc[a][b];
+    }
+  }
+}
+void rff_prior_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude,
+                      const double* W, int ldw, int s_count, double* prior, cudaStream_t s) {
+  if (n <= 0) return;
+  if (d > 32) throw std::invalid_argument("gpk: RFF prior supports d <= 32");
+  const size_t smem = sizeof(double) * (RP_ROWS * d + RP_F * RP_ROWS + RP_F * RP_COLS);
+  static size_t configured = 0;
+  if (smem > configured) {
+    GPK_CUDA(cudaFuncSetAttribute(rff_prior_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  const dim3 grid((n + RP_ROWS - 1) / RP_ROWS, (s_count + RP_COLS - 1) / RP_COLS);
+  rff_prior_kernel<<<grid, 256, smem, s>>>(x64, n, d, freq, pairs, amplitude, W, ldw, s_count, prior);
+  check_launch("rff_prior");
+}
+
 void rff_features_launch(const double* x64, int n, int d, const double* freq, int pairs, double amplitude, double* F,
                          cudaStream_t s) {
   if (n <= 0) return;

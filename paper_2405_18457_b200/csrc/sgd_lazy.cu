@@ -1,0 +1,562 @@
+// SGD (solvers.cpp:147-184) with the momentum recurrence evaluated lazily,
+// and its minibatch product H[idx, :] V on the tcgen05 tensor cores.
+//
+// The reference updates every row of the n x m momentum and solution each
+// iteration (M *= rho; M[idx] -= (lr/b) g; V += M), i.e. ~4 n m doubles of
+// memory traffic per iteration for b = 512 rows of actual change. A row i
+// that is not in the minibatch evolves in closed form: if (Vb, Mb) is its
+// state right after iteration tau (its last update), then after
+// Delta = t - tau - 1 further iterations
+//   M(t) = rho^Delta Mb,   V(t) = Vb + S(Delta) Mb,   S(Delta) = rho + ... + rho^Delta.
+// So each iteration writes only its b minibatch rows (FP64 base state, their
+// FP32 records, tau), and the operator kernel materialises V(t) on the fly
+// from the FP32 records while it builds its tensor-core B operand -- the full
+// state is read once per iteration by the kernel that needs it anyway, and
+// never written. P(Delta) = rho^Delta and S(Delta) are tables built by
+// repeated multiplication / addition (the reference's own recurrence for an
+// untouched row), so the closed form differs from the reference only in
+// rounding (one multiply-add instead of Delta of them).
+//
+// sgd_slab_kernel: CTA = one 128-row tile of the minibatch x a column range
+// (its split); 22 warps:
+//   warps 0-15  evaluation: k(x_i, x_c) in FP32 (MUFU sqrt/ex2), TF32 hi/lo
+//               split, tcgen05.st into a TMEM A buffer (5-deep ring); every
+//               F chunks they drain the FP32 TMEM accumulator into FP64
+//               registers (D double-buffered, drain deferred L chunks so the
+//               MMA never waits), FP64 partial per split at the end.
+//   warp 16     producer: cp.async.bulk of the chunk's 32 FP32 records
+//               (V32 | M32), tau and x_c rows into a 4-stage staging ring.
+//   warps 17-20 B builders: V(t) = V32 + S(Delta) M32 in FP32, TF32 hi/lo,
+//               stored in the canonical K-major UMMA layout (3-stage ring).
+//   warp 21     MMA: per 32-column chunk 12 tcgen05.mma.kind::tf32
+//               (M = 128, N = NPAD, K = 8): D += A_hi B_hi + A_hi B_lo + A_lo B_hi.
+// sgd_reduce_kernel: split partials -> the rank's slice of g (+ sigma^2 V(t)
+// and -B on its own rows, old residual squares); sgd_apply_kernel: rank-order
+// sum of the slices = g, the lazy update of the own minibatch rows, R[idx] =
+// -g, the incremental residual norms and the termination / divergence test.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "gpk_internal.cuh"
+#include "tc_util.cuh"
+
+namespace gpk {
+
+namespace {
+using namespace tc;
+
+constexpr int TBM = 128, TBK = 32;
+constexpr int EW = 16;                 // evaluation warps
+constexpr int BW = 4;                  // B-builder warps
+constexpr int PROD_WARP = EW;          // 16
+constexpr int BUILD_WARP0 = EW + 1;    // 17..20
+constexpr int MMA_WARP = EW + 1 + BW;  // 21
+constexpr int NTHREADS = 32 * (MMA_WARP + 1);
+constexpr int ST = 4;    // staging stages
+constexpr int SB = 3;    // B stages
+constexpr int NAB = 5;   // TMEM A buffers (64 columns each, from column 192)
+constexpr int A_COL0 = 192;
+constexpr int D_COL1 = 96;  // second accumulator (the first at column 0)
+constexpr int CPT = 8;      // chunk columns per evaluation thread
+constexpr int DEFER = 4;    // drain of group g runs after chunk (g + 1) F + DEFER is evaluated
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int NPAD, int DP4>
+struct SgdLayout {
+  static constexpr int DP = 4 * DP4;
+  static constexpr int IMG = NPAD * TBK;  // floats of one TF32 image of a chunk
+};
+
+template <int NPAD, int DP4>
+__global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs a) {
+  using L = SgdLayout<NPAD, DP4>;
+  constexpr int DP = L::DP;
+  constexpr int DC = NPAD / 4;  // D columns drained per evaluation thread
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int rw = a.rw;
+  const int st_floats = TBK * rw + TBK * DP + TBK;  // records | x_c | tau
+  float* smB = reinterpret_cast<float*>(smem_raw);         // [SB][2 * IMG]
+  float* smS = smB + SB * 2 * L::IMG;                      // [ST][st_floats]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smS + ST * st_floats);
+  uint64_t* st_full = bars;                 // [ST]
+  uint64_t* st_empty = bars + ST;           // [ST]
+  uint64_t* b_full = bars + 2 * ST;         // [SB]
+  uint64_t* b_empty = b_full + SB;          // [SB]
+  uint64_t* a_full = b_empty + SB;          // [NAB]
+  uint64_t* a_empty = a_full + NAB;         // [NAB]
+  uint64_t* d_full = a_empty + NAB;         // [2]
+  uint64_t* d_empty = d_full + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+
+  if (a.ctl->stop) return;
+  const int t_iter = a.ctl->iters;
+  const int* idx = a.idxbuf + static_cast<size_t>(t_iter % a.idx_chunk) * a.R;
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int cb = split * a.cols_per_split;
+  const int ce = min(a.C, cb + a.cols_per_split);
+  const int nk = ce > cb ? (ce - cb + TBK - 1) / TBK : 0;
+  const int F = a.flush;
+  const int ngroups = (nk + F - 1) / F;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (a.stats && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    const double entries = static_cast<double>(a.R) * a.C;
+    atomicAdd(a.stats, entries * a.m);
+    atomicAdd(a.stats + 1, entries * (2.0 * a.m + 3.0 * a.d + 6.0));
+    atomicAdd(a.stats + 2, entries * (3.0 * a.d + 6.0));
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], EW + BW);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&b_full[s], BW);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int b = 0; b < NAB; ++b) {
+      mbar_init(&a_full[b], EW);
+      mbar_init(&a_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&d_full[b], 1);
+      mbar_init(&d_empty[b], EW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == PROD_WARP) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint32_t rec_bytes = TBK * rw * 4u, x_bytes = TBK * DP * 4u;
+      for (int k = 0; k < nk; ++k) {
+        const int s = k % ST;
+        if (k >= ST) mbar_wait(&st_empty[s], ((k / ST) - 1) & 1);
+        const size_t c = static_cast<size_t>(cb) + static_cast<size_t>(k) * TBK;  // local column of the chunk
+        float* dst = smS + s * st_floats;
+        mbar_expect_tx(&st_full[s], rec_bytes + x_bytes + TBK * 4u);
+        bulk_g2s(dst, a.rec + c * rw, rec_bytes, &st_full[s]);
+        bulk_g2s(dst + TBK * rw, a.xs + (a.c0 + c) * DP, x_bytes, &st_full[s]);
+        bulk_g2s(dst + TBK * rw + TBK * DP, a.tau + c, TBK * 4u, &st_full[s]);
+      }
+    }
+  } else if (warp >= BUILD_WARP0 && warp < MMA_WARP) {
+    // ---------------- B builders: V(t) images ----------------
+    const int bt = tid - BUILD_WARP0 * 32;  // 0..127
+    // the elements this thread writes: w = bt + 128 u; ln = w & 31 is fixed,
+    // core = (bt >> 5) + 4 u, so its chunk column c takes two values
+    const int ln = bt & 31;
+    const int cA = ((bt >> 5) & 7) * 4 + (ln & 3);
+    const int cB = (((bt >> 5) + 4) & 7) * 4 + (ln & 3);
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % ST, sb = k % SB;
+      mbar_wait(&st_full[s], (k / ST) & 1);
+      if (k >= SB) mbar_wait(&b_empty[sb], ((k / SB) - 1) & 1);
+      const float* rec = smS + s * st_floats;
+      const int* tau = reinterpret_cast<const int*>(rec + TBK * rw + TBK * DP);
+      const int dA = min(max(t_iter - tau[cA] - 1, 0), a.budget);
+      const int dB = min(max(t_iter - tau[cB] - 1, 0), a.budget);
+      const float sA = __ldg(a.s32 + dA), sB = __ldg(a.s32 + dB);
+      float* bh = smB + sb * 2 * L::IMG;
+      float* bl = bh + L::IMG;
+#pragma unroll 4
+      for (int u = 0; u < L::IMG / 128; ++u) {
+        const int w = bt + 128 * u;
+        const int core = w >> 5;
+        const int j = (core >> 3) * 8 + (ln >> 2);
+        const int c = (u & 1) ? cB : cA;
+        const float sc = (u & 1) ? sB : sA;
+        float v = 0.f;
+        if (j < a.m) v = fmaf(sc, rec[c * rw + a.moff + j], rec[c * rw + j]);
+        const float h = __uint_as_float(tf32_rna(v));
+        bh[w] = h;
+        bl[w] = __uint_as_float(tf32_rna(v - h));
+      }
+      fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&b_full[sb]);
+        mbar_arrive(&st_empty[s]);
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+    for (int k = 0; k < nk; ++k) {
+      const int sb = k % SB, ab = k % NAB, g = k / F;
+      const bool first = (k % F) == 0, last = (k % F) == F - 1 || k + 1 == nk;
+      mbar_wait(&b_full[sb], (k / SB) & 1);
+      mbar_wait(&a_full[ab], (k / NAB) & 1);
+      if (first && g >= 2) mbar_wait(&d_empty[g & 1], ((g >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t dt = tmem + ((g & 1) ? D_COL1 : 0);
+      const uint32_t bh = smem_u32(smB + sb * 2 * L::IMG);
+      const uint32_t bl = bh + L::IMG * 4;
+      const uint32_t ah = tmem + A_COL0 + ab * 64, al = ah + 32;
+#pragma unroll
+      for (int kk = 0; kk < TBK / 8; ++kk) {
+        const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
+        const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
+        MMA_TF32(dt, ah + kk * 8, dh, idesc, (first && kk == 0) ? 0u : 1u);
+        MMA_TF32(dt, ah + kk * 8, dl, idesc, 1u);
+        MMA_TF32(dt, al + kk * 8, dh, idesc, 1u);
+      }
+      MMA_COMMIT(&b_empty[sb]);
+      MMA_COMMIT(&a_empty[ab]);
+      if (last) MMA_COMMIT(&d_full[g & 1]);
+    }
+  } else {
+    // ---------------- evaluation + drain ----------------
+    const int lg = warp & 3, quarter = warp >> 2;
+    const int row = lg * 32 + lane;
+    const int er = tile * TBM + row;
+    const bool row_ok = er < a.R;
+    const int gi = row_ok ? idx[er] : 0;
+    float4 xi[DP4];
+    const float* xrow = a.xs + static_cast<size_t>(gi) * DP;
+#pragma unroll
+    for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+    const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
+    double acc[DC];
+#pragma unroll
+    for (int e = 0; e < DC; ++e) acc[e] = 0.0;
+    auto drain = [&](int g) {
+      mbar_wait(&d_full[g & 1], (g >> 1) & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + lane_addr + ((g & 1) ? D_COL1 : 0) + quarter * DC;
+#pragma unroll
+      for (int q = 0; q < DC / 4; ++q) {
+        uint32_t v[4];
+        tc_ld4(base + 4 * q, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * q + e] += static_cast<double>(__uint_as_float(v[e]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_empty[g & 1]);
+    };
+    int drained = 0;
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % ST, ab = k % NAB;
+      mbar_wait(&st_full[s], (k / ST) & 1);
+      if (k >= NAB) mbar_wait(&a_empty[ab], ((k / NAB) - 1) & 1);
+      tc_fence_after();
+      const float* xc = smS + s * st_floats + TBK * rw + quarter * CPT * DP;
+      uint32_t hi[CPT], lo[CPT];
+#pragma unroll
+      for (int t = 0; t < CPT; ++t) {
+        float r2a = 0.f, r2b = 0.f;
+#pragma unroll
+        for (int u = 0; u < DP4; ++u) {
+          const float4 c = reinterpret_cast<const float4*>(xc + t * DP)[u];
+          const float d0 = c.x - xi[u].x, d1 = c.y - xi[u].y, d2 = c.z - xi[u].z, d3 = c.w - xi[u].w;
+          r2a = fmaf(d0, d0, r2a);
+          r2b = fmaf(d1, d1, r2b);
+          r2a = fmaf(d2, d2, r2a);
+          r2b = fmaf(d3, d3, r2b);
+        }
+        const float r = sqrt_approx(r2a + r2b);
+        const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
+        hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
+        lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
+      }
+      const uint32_t abase = tmem + lane_addr + A_COL0 + ab * 64 + quarter * CPT;
+      tc_st8(abase, hi);
+      tc_st8(abase + 32, lo);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&a_full[ab]);
+        mbar_arrive(&st_empty[s]);
+      }
+      // deferred drain: group g once chunk (g + 1) F + DEFER is in flight
+      if (k >= DEFER && (k - DEFER) % F == 0 && (k - DEFER) / F >= 1) drain(drained++);
+    }
+    while (drained < ngroups) drain(drained++);
+    if (row_ok) {
+      double* prow = a.part + (static_cast<size_t>(split) * a.R + er) * a.m;
+#pragma unroll
+      for (int e = 0; e < DC; ++e) {
+        const int j = quarter * DC + e;
+        if (j < a.m) prow[j] = acc[e];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int NPAD, int DP4>
+void launch_one(const SgdSlabArgs& a, cudaStream_t s) {
+  constexpr int DP = 4 * DP4;
+  const size_t st_floats = static_cast<size_t>(TBK) * a.rw + TBK * DP + TBK;
+  const size_t smem = sizeof(float) * (SB * 2 * NPAD * TBK + ST * st_floats) + 64 * sizeof(uint64_t);
+  if (smem > 227 * 1024) throw std::invalid_argument("gpk: SGD slab kernel shared memory exceeds 227 KB");
+  static size_t configured = 0;
+  if (smem > configured) {
+    GPK_CUDA(cudaFuncSetAttribute(sgd_slab_kernel<NPAD, DP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  sgd_slab_kernel<NPAD, DP4><<<dim3((a.R + TBM - 1) / TBM, a.splits), NTHREADS, smem, s>>>(a);
+  check_launch("sgd_slab_kernel");
+}
+
+template <int NPAD>
+void launch_n(const SgdSlabArgs& a, cudaStream_t s) {
+  switch (a.dp / 4) {
+    case 1: return launch_one<NPAD, 1>(a, s);
+    case 2: return launch_one<NPAD, 2>(a, s);
+    case 3: return launch_one<NPAD, 3>(a, s);
+    case 4: return launch_one<NPAD, 4>(a, s);
+    default: throw std::invalid_argument("gpk: the SGD slab kernel supports d <= 16");
+  }
+}
+
+// ---- per-iteration reduction / update kernels ------------------------------
+// slice[q][j] = sum_s part[s][q][j] (+ sigma^2 V(t)[i][j] - B[i][j] if row i =
+// idx[q] is this rank's); slice[bm + j] = sum over own q of R[i][j]^2 (old
+// residual estimate), slice[bm + m] = this rank's pending divergence flag.
+__global__ void sgd_reduce_kernel(SgdStepArgs a) {
+  if (a.ctl->stop) return;
+  const int t = a.ctl->iters;
+  const int* idx = a.idxbuf + static_cast<size_t>(t % a.idx_chunk) * a.b;
+  const int m = a.m, bm = a.b * m;
+  const int gb = gridDim.x - m;
+  if (static_cast<int>(blockIdx.x) >= gb) {
+    const int j = blockIdx.x - gb;
+    __shared__ double wsum[32];
+    double acc = 0.0;
+    for (int q = threadIdx.x; q < a.b; q += blockDim.x) {
+      const int li = idx[q] - a.row0;
+      if (li >= 0 && li < a.nloc) {
+        const double r = a.resid[static_cast<size_t>(li) * m + j];
+        acc += r * r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += wsum[w];
+      a.slice[bm + j] = tot;
+      if (j == 0) a.slice[bm + m] = *a.nonfinite ? 1.0 : 0.0;
+    }
+    return;
+  }
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bm; e += gb * blockDim.x) {
+    const int q = e / m, j = e - q * m;
+    double g = 0.0;
+    for (int s = 0; s < a.splits; ++s) g += a.part[static_cast<size_t>(s) * bm + e];
+    const int li = idx[q] - a.row0;
+    if (li >= 0 && li < a.nloc) {
+      const size_t o = static_cast<size_t>(li) * m + j;
+      const int dl = min(max(t - a.tau[li] - 1, 0), a.budget);
+      const double v = fma(a.s64[dl], a.Mb[o], a.Vb[o]);  // V(t) of the row
+      g = fma(a.sigma2, v, g) - a.B[o];
+    }
+    a.slice[e] = g;
+  }
+}
+
+// g = sum of the rank slices (rank order); own minibatch rows: M(t+1) = rho
+// M(t) - (lr/b) g, V(t+1) = V(t) + M(t+1) as the new base, tau = t, FP32
+// records; R[i] = -g. Block partials of sum_q g^2 per column; the last block
+// to finish updates the residual norms and takes the termination decision
+// (solvers.cpp:164-178: test after the update, abort on a non-finite iterate).
+constexpr int APPLY_ROWS = 8;
+__global__ void sgd_apply_kernel(SgdStepArgs a) {
+  if (a.ctl->stop) return;
+  const int t = a.ctl->iters;
+  const int* idx = a.idxbuf + static_cast<size_t>(t % a.idx_chunk) * a.b;
+  const int m = a.m, bm = a.b * m;
+  __shared__ double gs[APPLY_ROWS][80];
+  __shared__ int bad_g, bad_row;
+  __shared__ unsigned last;
+  if (threadIdx.x == 0) bad_g = bad_row = 0;
+  __syncthreads();
+  const int rl = threadIdx.x / m, j = threadIdx.x - rl * m;  // blockDim.x = APPLY_ROWS * m
+  const int q = blockIdx.x * APPLY_ROWS + rl;
+  double g2 = 0.0;
+  if (rl < APPLY_ROWS && q < a.b) {
+    double g = a.gbuf[static_cast<size_t>(q) * m + j];
+    for (int r = 1; r < a.nr; ++r) g += a.gbuf[static_cast<size_t>(r) * a.stride + static_cast<size_t>(q) * m + j];
+    if (!isfinite(g)) bad_g = 1;
+    g2 = g * g;
+    const int li = idx[q] - a.row0;
+    if (li >= 0 && li < a.nloc) {
+      const size_t o = static_cast<size_t>(li) * m + j;
+      const int dl = min(max(t - a.tau[li] - 1, 0), a.budget);
+      const double mb = a.Mb[o];
+      const double mt = a.p64[dl] * mb;                      // M(t)
+      const double vt = fma(a.s64[dl], mb, a.Vb[o]);         // V(t)
+      const double mn = __dsub_rn(__dmul_rn(mt, a.rho), __dmul_rn(a.step, g));
+      const double vn = __dadd_rn(vt, mn);
+      if (!isfinite(vn) || !isfinite(mn)) bad_row = 1;
+      a.Mb[o] = mn;
+      a.Vb[o] = vn;
+      a.resid[o] = -g;
+      float* rec = a.rec + static_cast<size_t>(li) * a.rw;
+      rec[j] = static_cast<float>(vn);
+      rec[a.moff + j] = static_cast<float>(mn);
+    }
+  }
+  if (rl < APPLY_ROWS) gs[rl][j] = g2;
+  __syncthreads();  // every thread of the block has read tau of its row
+  if (rl < APPLY_ROWS && j == 0 && q < a.b) {
+    const int li = idx[q] - a.row0;
+    if (li >= 0 && li < a.nloc) a.tau[li] = t;
+  }
+  // block partial of sum g^2 per column (rows in order)
+  if (threadIdx.x < m) {
+    double s = 0.0;
+    for (int r = 0; r < APPLY_ROWS; ++r) s += gs[r][threadIdx.x];
+    a.gpart[static_cast<size_t>(blockIdx.x) * m + threadIdx.x] = s;
+  }
+  if (threadIdx.x == 0 && (bad_g || bad_row)) atomicOr(a.nonfinite_now, bad_g ? 3 : 1);  // bit 1: g itself
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double ss[128];
+  if (threadIdx.x < m) {
+    const int jj = threadIdx.x;
+    double s = 0.0;
+    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) s += a.gpart[static_cast<size_t>(b) * m + jj];
+    double old = 0.0;
+    for (int r = 0; r < a.nr; ++r) old += a.gbuf[static_cast<size_t>(r) * a.stride + bm + jj];
+    const double v = a.sumsq[jj] + (s - old);
+    a.sumsq[jj] = v;
+    ss[jj] = fmax(v, 0.0);
+  }
+  __syncthreads();
+  // divergence (solvers.cpp:173-177): one rank -- a non-finite updated row, now;
+  // sharded -- a non-finite g (identical on every rank) now, a rank's own
+  // non-finite row through its next slice, so every rank stops at the same
+  // iteration (their collectives must match)
+  double pend = 0.0;
+  for (int r = 0; r < a.nr; ++r) pend += a.gbuf[static_cast<size_t>(r) * a.stride + bm + m];
+  const int now = *a.nonfinite_now;
+  const bool diverged = (a.nr == 1 ? now != 0 : (now & 2) != 0) || pend != 0.0;
+  if (threadIdx.x == 0) {
+    *a.ticket = 0u;
+    if (now) *a.nonfinite = 1;
+  }
+  if (threadIdx.x < 32) {  // termination_check on the tracked residuals (linear_system.cpp:47-53)
+    double probe = 0.0;
+    for (int jj = 1 + threadIdx.x; jj < m; jj += 32) probe += sqrt(ss[jj]) / a.scales[jj];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) probe += __shfl_xor_sync(0xffffffffu, probe, o);
+    if (threadIdx.x == 0) {
+      const double mean = sqrt(ss[0]) / a.scales[0];
+      probe = m > 1 ? probe / (m - 1) : 0.0;
+      CgCtl* c = a.ctl;
+      c->iters += 1;
+      c->mean_norm = mean;
+      c->probe_norm = probe;
+      c->done = mean <= a.tol && probe <= a.tol;
+      c->aborted = diverged ? 1 : 0;
+      c->stop = (c->done || c->aborted || c->iters >= c->budget) ? 1 : 0;
+    }
+  }
+}
+
+// initial records from the warm-start solution: V32 = V0, M32 = 0, tau = -1
+__global__ void sgd_records_init_kernel(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec,
+                                        int* tau) {
+  const long long total = static_cast<long long>(rows_pad) * rw;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / rw), c = static_cast<int>(e % rw);
+    float v = 0.f;
+    if (i < nloc && c < m) v = static_cast<float>(V[static_cast<size_t>(i) * m + c]);
+    rec[e] = v;
+    if (c == 0) tau[i] = -1;
+  }
+}
+
+// V(T) for every own row at the end of the solve (in place on the base)
+__global__ void sgd_materialise_kernel(double* Vb, const double* Mb, const int* tau, const double* s64, int budget,
+                                       const CgCtl* ctl, int nloc, int m) {
+  const int T = ctl->iters;
+  const long long total = static_cast<long long>(nloc) * m;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / m);
+    const int dl = min(max(T - tau[i] - 1, 0), budget);
+    Vb[e] = fma(s64[dl], Mb[e], Vb[e]);
+  }
+}
+
+}  // namespace
+
+int sgd_record_width(int m, int* moff) {
+  int half = (m + 3) / 4 * 4;
+  while ((2 * half) % 32 != 8) half += 4;  // rows 8 banks apart: conflict-free B builds
+  if (moff) *moff = half;
+  return 2 * half;
+}
+
+void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s) {
+  switch (kv_tc_npad(a.m)) {
+    case 16: return launch_n<16>(a, s);
+    case 32: return launch_n<32>(a, s);
+    case 48: return launch_n<48>(a, s);
+    case 64: return launch_n<64>(a, s);
+    case 80: return launch_n<80>(a, s);
+    default: throw std::invalid_argument("gpk: the SGD slab kernel supports m <= 80");
+  }
+}
+
+void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s) {
+  const int gb = std::max(1, std::min(148 * 2, (a.b * a.m + 255) / 256));
+  sgd_reduce_kernel<<<gb + a.m, 256, 0, s>>>(a);
+  check_launch("sgd_reduce");
+}
+
+void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s) {
+  if (a.m > 80) throw std::invalid_argument("gpk: SGD apply supports m <= 80");
+  const int threads = ((APPLY_ROWS * a.m + 31) / 32) * 32;
+  sgd_apply_kernel<<<(a.b + APPLY_ROWS - 1) / APPLY_ROWS, threads, 0, s>>>(a);
+  check_launch("sgd_apply");
+}
+
+void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
+                             cudaStream_t s) {
+  const long long total = static_cast<long long>(rows_pad) * rw;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  sgd_records_init_kernel<<<blocks, 256, 0, s>>>(V, nloc, rows_pad, m, rw, moff, rec, tau);
+  check_launch("sgd_records_init");
+}
+
+void sgd_materialise_launch(double* Vb, const double* Mb, const int* tau, const double* s64, int budget,
+                            const CgCtl* ctl, int nloc, int m, cudaStream_t s) {
+  const long long total = static_cast<long long>(nloc) * m;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  sgd_materialise_kernel<<<blocks, 256, 0, s>>>(Vb, Mb, tau, s64, budget, ctl, nloc, m);
+  check_launch("sgd_materialise");
+}
+
+}  // namespace gpk

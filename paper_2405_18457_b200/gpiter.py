@@ -236,6 +236,13 @@ class KernelOperator:
     def dense(self):
         return self.dense_block(0, self.n, 0, self.n)
 
+    def derivative_apply(self, k, v):
+        """(dH/dtheta_k) V (kernel.hpp:71): lengthscales k < d, signal k = d, noise k = d + 1."""
+        V = _f64(v)
+        out = np.empty(V.shape, order="F")
+        check(self._lib.gpk_derivative_apply(self.handle, int(k), _p(V), V.shape[1], _p(out)))
+        return out
+
     def kernel_column(self, i):
         out = np.empty(self.n)
         check(self._lib.gpk_kernel_column(self.handle, i, _p(out)))

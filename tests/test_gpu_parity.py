@@ -119,6 +119,21 @@ def test_dense_block_and_kernel_column_fp64(G, gpk_ctx, oracle):
     assert np.all(op.kernel_diagonal() == s2)
 
 
+@pytest.mark.parametrize("n,d,m", [(300, 4, 3), (700, 11, 17), (257, 2, 65)])
+def test_derivative_apply_matches_oracle(G, gpk_ctx, oracle, n, d, m):
+    """derivative_apply(k, V) (kernel.hpp:71, kernel.cpp:200-236) for every
+    parameter, FP64 on the device, against the oracle's restatement."""
+    X, _ = gp_problem(n, d, 3 * n)
+    raw = default_test_raw(d, oracle)
+    V = np.asfortranarray(np.random.default_rng(m).standard_normal((n, m)))
+    op = make_op(G, gpk_ctx, X, raw)
+    for k in range(d + 2):
+        got, ref = op.derivative_apply(k, V), oracle.derivative_apply(X, raw, k, V)
+        assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref)), k
+    with pytest.raises(IndexError):
+        op.derivative_apply(d + 2, V)
+
+
 @pytest.mark.parametrize("n,d,s", [(500, 2, 8), (1200, 20, 64), (2048, 26, 64), (700, 3, 16), (300, 3, 80),
                                    (129, 5, 2)])
 def test_quadratic_forms_match_oracle(G, kctx, oracle, n, d, s):

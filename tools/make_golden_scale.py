@@ -107,6 +107,22 @@ def main():
                     "trajectory_rel": float(np.max(np.abs(r["constrained"] - g["traj_constrained"]) /
                                                    g["traj_constrained"]))}
                 print(name, json.dumps(rep[name]), flush=True)
+            # sensitivity of the C3 step to operator rounding: the FP64 oracle
+            # with every H.V entry perturbed by a relative 1e-12 / 1e-7
+            for noise in (1e-12, 1e-7):
+                O.set_apply_sensitivity(0, noise)
+                g = np.load(os.path.join(GOLD, "c3.npz"))
+                r = traj("C3", 2)
+                O.set_apply_sensitivity(0, 0.0)
+                gg = g["traj_gradient"]
+                rep[f"C3_noise_{noise:g}"] = {
+                    "iterations": r["iterations"].tolist(),
+                    "mean_norm_rel": (np.abs(r["mean_residual_norm"] - g["traj_mean_residual_norm"]) /
+                                      g["traj_mean_residual_norm"]).tolist(),
+                    "probe_norm_rel": (np.abs(r["probe_residual_norm"] - g["traj_probe_residual_norm"]) /
+                                       g["traj_probe_residual_norm"]).tolist(),
+                    "gradient_rel_of_max": (np.abs(r["gradient"] - gg).max(axis=1) / np.abs(gg).max(axis=1)).tolist()}
+                print(f"C3 noise {noise:g}", json.dumps(rep[f"C3_noise_{noise:g}"]), flush=True)
             json.dump(rep, open(os.path.join(OUT, "scale_validate.json"), "w"), indent=1)
         if "c4" in what:
             out = sgd_replay(REPLAY_ITERS)
