@@ -256,7 +256,7 @@ struct gpk_batch {
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
   // lazy-momentum SGD (sgd_lazy.cu): FP32 records, last-update iterations,
   // S / rho^Delta tables, slab partials, apply-block partials, flags
-  DBuf<float> sgd_rec, sgd_s32;
+  DBuf<float> sgd_rec, sgd_s32, sgd_xg;
   DBuf<int> sgd_tau, sgd_flags;
   DBuf<double> sgd_tab, sgd_part, sgd_gpart;
   DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
@@ -1672,7 +1672,7 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   int moff = 0;
   const int rw = sgd_record_width(m, &moff);
   const int rows_pad = (nloc + 31) / 32 * 32;
-  float* rec = b->sgd_rec.ensure(static_cast<size_t>(rows_pad) * rw);
+  float* rec = b->sgd_rec.ensure(static_cast<size_t>(rows_pad / 32) * rw);  // one record per 32-row chunk
   int* tau = b->sgd_tau.ensure(rows_pad);
   sgd_records_init_launch(b->solutions.p, nloc, rows_pad, m, rw, moff, rec, tau, s);
   // P(Delta) = rho^Delta, S(Delta) = rho + ... + rho^Delta by the recurrence an
@@ -1737,6 +1737,19 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   sa.tau = tau;
   sa.s32 = b->sgd_s32.p;
   sa.budget = budget;
+  sa.ntab = std::min(budget + 1, 4096);  // 16 KB of shared memory
+  // Gram-form distances when the padded row has a free slot for |x|^2
+  // (GPK_SGD_GRAM=1; measured: no faster at C4 and 8x the distance rounding
+  // at d = 11, so direct differences by default)
+  static const bool sgd_gram = [] {
+    const char* e = std::getenv("GPK_SGD_GRAM");
+    return e && std::atoi(e) != 0;
+  }();
+  if (sgd_gram && op->d < op->dp) {
+    float* xg = b->sgd_xg.ensure(static_cast<size_t>(n + 128) * op->dp);
+    sgd_gram_image_launch(op->xs32.p, n + 128, n, op->d, op->dp, xg, s);
+    sa.xg = xg;
+  }
   sa.ctl = ctl;
   sa.log2_s2 = static_cast<float>(std::log2(op->s2));
   sa.part = part;

@@ -218,8 +218,9 @@ void grad_tc_pack_launch(const float* w32, int ld, int n, int cols, int kp, floa
 void grad_tc_launch(const GradTcArgs& a, cudaStream_t s);
 
 // ---- SGD with lazily evaluated momentum (sgd_lazy.cu) ----------------------
-// Per local row: FP32 record [V32 (m) | pad | M32 (m) | pad] of width rw
-// (sgd_record_width: M32 at moff), the FP64 base state (Vb = the batch's
+// Per 32-row chunk of local rows: an FP32 record [V32 image | M32 image] of
+// rw floats (sgd_record_width; M32 at moff), each image in the B operand's
+// canonical K-major layout; per row the FP64 base state (Vb = the batch's
 // solutions, Mb) and tau = the iteration of its last update (-1: none).
 struct SgdSlabArgs {
   const float* xs;      // scaled inputs FP32 [n + 128][dp] (global rows)
@@ -228,11 +229,13 @@ struct SgdSlabArgs {
   int idx_chunk;
   int R;                // minibatch size (output rows)
   int c0, C;            // this rank's columns (global row0, local count)
-  const float* rec;     // [rows_pad][rw]
+  const float* rec;     // [rows_pad / 32][rw]
   int rw, moff;
   const int* tau;       // [rows_pad]
   const float* s32;     // S(Delta), Delta = 0..budget
   int budget;
+  int ntab;             // leading entries of s32 staged in shared memory
+  const float* xg;      // Gram column image (-2 x, |x|^2, 0...) [n + 128][dp] or null (direct differences)
   const CgCtl* ctl;     // iteration t = ctl->iters; no-op once ctl->stop
   float log2_s2;
   double* part;         // [splits][R][m] FP64 partials
@@ -270,6 +273,7 @@ struct SgdStepArgs {
 int sgd_record_width(int m, int* moff);
 void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s);
 void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s);
+void sgd_gram_image_launch(const float* xs, int rows, int n, int d, int dp, float* xg, cudaStream_t s);
 void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s);
 void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
                              cudaStream_t s);

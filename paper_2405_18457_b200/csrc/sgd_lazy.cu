@@ -62,6 +62,50 @@ constexpr int D_COL1 = 96;  // second accumulator (the first at column 0)
 constexpr int CPT = 8;      // chunk columns per evaluation thread
 constexpr int DEFER = 4;    // drain of group g runs after chunk (g + 1) F + DEFER is evaluated
 
+// shared memory: B ring | staging ring | barriers (64 words) | S of the chunk
+// columns [SB][32] | S table [ntab]
+template <int NPAD>
+__host__ __device__ constexpr size_t sgd_smem_bytes(int rw, int dp, int ntab) {
+  return sizeof(float) * (SB * 2 * NPAD * 32 + ST * (static_cast<size_t>(rw) + 32 * dp + 32)) +
+         64 * sizeof(uint64_t) + SB * 32 * sizeof(float) + static_cast<size_t>(ntab) * sizeof(float);
+}
+
+// position of element (c, j) of a chunk's V (or M) image: the canonical
+// K-major UMMA layout of the B operand (see kv_pack_kernel)
+__host__ __device__ __forceinline__ int sgd_record_pos(int c, int j) {
+  return ((j >> 3) * 8 + (c >> 2)) * 32 + (j & 7) * 4 + (c & 3);
+}
+
+// Waiting with back-off for the roles that run ahead of the pipeline (producer,
+// B builders) or only issue (MMA): a failed probe sleeps `ns` instead of
+// re-probing, so the waiting warps leave issue slots and the MIO queue
+// (mbarrier probes share it with LDS / MUFU) to the evaluation warps.
+template <int NS>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (NS > 0) __nanosleep(NS);
+  }
+}
+// spin without suspend hint or sleep (latency-critical consumers)
+#ifndef SGD_SPIN
+#define SGD_SPIN 1
+#endif
+#if SGD_SPIN
+#define SGD_WAIT mbar_wait_spin
+#else
+#define SGD_WAIT mbar_wait
+#endif
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) { mbar_wait_backoff<0>(bar, parity); }
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <int NPAD, int DP4>
@@ -70,14 +114,14 @@ struct SgdLayout {
   static constexpr int IMG = NPAD * TBK;  // floats of one TF32 image of a chunk
 };
 
-template <int NPAD, int DP4>
+template <int NPAD, int DP4, bool GRAM, int DX>
 __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs a) {
   using L = SgdLayout<NPAD, DP4>;
   constexpr int DP = L::DP;
   constexpr int DC = NPAD / 4;  // D columns drained per evaluation thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int rw = a.rw;
-  const int st_floats = TBK * rw + TBK * DP + TBK;  // records | x_c | tau
+  const int rw = a.rw;                              // floats of one chunk record (V image | M image)
+  const int st_floats = rw + TBK * DP + TBK;        // record | x_c | tau
   float* smB = reinterpret_cast<float*>(smem_raw);         // [SB][2 * IMG]
   float* smS = smB + SB * 2 * L::IMG;                      // [ST][st_floats]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smS + ST * st_floats);
@@ -90,6 +134,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
   uint64_t* d_full = a_empty + NAB;         // [2]
   uint64_t* d_empty = d_full + 2;           // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+  float* sS = reinterpret_cast<float*>(d_empty + 4);  // [SB][32] S(Delta) of the chunk's columns
+  float* stab = sS + SB * 32;                          // [ntab] S(Delta) table
 
   if (a.ctl->stop) return;
   const int t_iter = a.ctl->iters;
@@ -132,6 +178,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  for (int e = tid; e < a.ntab; e += NTHREADS) stab[e] = __ldg(a.s32 + e);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -140,49 +187,67 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
   if (warp == PROD_WARP) {
     // ---------------- producer ----------------
     if (lane == 0) {
-      const uint32_t rec_bytes = TBK * rw * 4u, x_bytes = TBK * DP * 4u;
+      const uint32_t rec_bytes = rw * 4u, x_bytes = TBK * DP * 4u;
       for (int k = 0; k < nk; ++k) {
         const int s = k % ST;
-        if (k >= ST) mbar_wait(&st_empty[s], ((k / ST) - 1) & 1);
+        if (k >= ST) mbar_wait_backoff<256>(&st_empty[s], ((k / ST) - 1) & 1);
         const size_t c = static_cast<size_t>(cb) + static_cast<size_t>(k) * TBK;  // local column of the chunk
         float* dst = smS + s * st_floats;
         mbar_expect_tx(&st_full[s], rec_bytes + x_bytes + TBK * 4u);
-        bulk_g2s(dst, a.rec + c * rw, rec_bytes, &st_full[s]);
-        bulk_g2s(dst + TBK * rw, a.xs + (a.c0 + c) * DP, x_bytes, &st_full[s]);
-        bulk_g2s(dst + TBK * rw + TBK * DP, a.tau + c, TBK * 4u, &st_full[s]);
+        bulk_g2s(dst, a.rec + (c / TBK) * rw, rec_bytes, &st_full[s]);
+        bulk_g2s(dst + rw, (GRAM ? a.xg : a.xs) + (a.c0 + c) * DP, x_bytes, &st_full[s]);
+        bulk_g2s(dst + rw + TBK * DP, a.tau + c, TBK * 4u, &st_full[s]);
       }
     }
   } else if (warp >= BUILD_WARP0 && warp < MMA_WARP) {
     // ---------------- B builders: V(t) images ----------------
+    // The chunk record holds V32 and M32 already in the B operand's canonical
+    // K-major layout (j-groups < JG), so V(t) = V32 + S(Delta_c) M32 is float4
+    // in, float4 out; per chunk the first builder warp looks up S(Delta_c) of
+    // the 32 columns.
     const int bt = tid - BUILD_WARP0 * 32;  // 0..127
-    // the elements this thread writes: w = bt + 128 u; ln = w & 31 is fixed,
-    // core = (bt >> 5) + 4 u, so its chunk column c takes two values
-    const int ln = bt & 31;
-    const int cA = ((bt >> 5) & 7) * 4 + (ln & 3);
-    const int cB = (((bt >> 5) + 4) & 7) * 4 + (ln & 3);
+    const int jgroups = a.moff / 256;       // JG: j-groups stored (8 j x 32 c each)
     for (int k = 0; k < nk; ++k) {
       const int s = k % ST, sb = k % SB;
-      mbar_wait(&st_full[s], (k / ST) & 1);
-      if (k >= SB) mbar_wait(&b_empty[sb], ((k / SB) - 1) & 1);
+      mbar_wait_backoff<64>(&st_full[s], (k / ST) & 1);
       const float* rec = smS + s * st_floats;
-      const int* tau = reinterpret_cast<const int*>(rec + TBK * rw + TBK * DP);
-      const int dA = min(max(t_iter - tau[cA] - 1, 0), a.budget);
-      const int dB = min(max(t_iter - tau[cB] - 1, 0), a.budget);
-      const float sA = __ldg(a.s32 + dA), sB = __ldg(a.s32 + dB);
-      float* bh = smB + sb * 2 * L::IMG;
-      float* bl = bh + L::IMG;
-#pragma unroll 4
-      for (int u = 0; u < L::IMG / 128; ++u) {
-        const int w = bt + 128 * u;
-        const int core = w >> 5;
-        const int j = (core >> 3) * 8 + (ln >> 2);
-        const int c = (u & 1) ? cB : cA;
-        const float sc = (u & 1) ? sB : sA;
-        float v = 0.f;
-        if (j < a.m) v = fmaf(sc, rec[c * rw + a.moff + j], rec[c * rw + j]);
-        const float h = __uint_as_float(tf32_rna(v));
-        bh[w] = h;
-        bl[w] = __uint_as_float(tf32_rna(v - h));
+      if (warp == BUILD_WARP0) {
+        const int* tau = reinterpret_cast<const int*>(rec + rw + TBK * DP);
+        const int dl = min(max(t_iter - tau[lane] - 1, 0), a.budget);
+        sS[sb * 32 + lane] = dl < a.ntab ? stab[dl] : __ldg(a.s32 + dl);
+      }
+      if (k >= SB) mbar_wait_backoff<128>(&b_empty[sb], ((k / SB) - 1) & 1);
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * BW) : "memory");
+      const float4* v4 = reinterpret_cast<const float4*>(rec);
+      const float4* m4 = reinterpret_cast<const float4*>(rec + a.moff);
+      const float4* s4 = reinterpret_cast<const float4*>(sS + sb * 32);
+      float4* bh = reinterpret_cast<float4*>(smB + sb * 2 * L::IMG);
+      float4* bl = bh + L::IMG / 4;
+#pragma unroll 5
+      for (int f = bt; f < L::IMG / 4; f += 32 * BW) {
+        const int core = f >> 3;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((core >> 3) < jgroups) {
+          const float4 vv = v4[f], mm = m4[f], sc = s4[core & 7];
+          v.x = fmaf(sc.x, mm.x, vv.x);
+          v.y = fmaf(sc.y, mm.y, vv.y);
+          v.z = fmaf(sc.z, mm.z, vv.z);
+          v.w = fmaf(sc.w, mm.w, vv.w);
+        }
+        // hi = v rounded to TF32 (nearest, ties away: add half of the 13
+        // dropped bits, clear them), lo = v - hi exactly; the tensor core reads
+        // lo's top 19 bits
+        float4 h, l;
+        h.x = __uint_as_float((__float_as_uint(v.x) + 0x1000u) & 0xFFFFE000u);
+        h.y = __uint_as_float((__float_as_uint(v.y) + 0x1000u) & 0xFFFFE000u);
+        h.z = __uint_as_float((__float_as_uint(v.z) + 0x1000u) & 0xFFFFE000u);
+        h.w = __uint_as_float((__float_as_uint(v.w) + 0x1000u) & 0xFFFFE000u);
+        l.x = v.x - h.x;
+        l.y = v.y - h.y;
+        l.z = v.z - h.z;
+        l.w = v.w - h.w;
+        bh[f] = h;
+        bl[f] = l;
       }
       fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
       __syncwarp();
@@ -194,12 +259,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
   } else if (warp == MMA_WARP) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+    int sb = 0, bph = 0, ab = 0, aph = 0, g = 0, kf = 0;
     for (int k = 0; k < nk; ++k) {
-      const int sb = k % SB, ab = k % NAB, g = k / F;
-      const bool first = (k % F) == 0, last = (k % F) == F - 1 || k + 1 == nk;
-      mbar_wait(&b_full[sb], (k / SB) & 1);
-      mbar_wait(&a_full[ab], (k / NAB) & 1);
-      if (first && g >= 2) mbar_wait(&d_empty[g & 1], ((g >> 1) - 1) & 1);
+      const bool first = kf == 0, last = kf == F - 1 || k + 1 == nk;
+      SGD_WAIT(&b_full[sb], bph);
+      SGD_WAIT(&a_full[ab], aph);
+      if (first && g >= 2) SGD_WAIT(&d_empty[g & 1], ((g >> 1) - 1) & 1);
       tc_fence_after();
       const uint32_t dt = tmem + ((g & 1) ? D_COL1 : 0);
       const uint32_t bh = smem_u32(smB + sb * 2 * L::IMG);
@@ -216,6 +281,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
       MMA_COMMIT(&b_empty[sb]);
       MMA_COMMIT(&a_empty[ab]);
       if (last) MMA_COMMIT(&d_full[g & 1]);
+      if (++sb == SB) { sb = 0; bph ^= 1; }
+      if (++ab == NAB) { ab = 0; aph ^= 1; }
+      if (++kf == F) { kf = 0; ++g; }
     }
   } else {
     // ---------------- evaluation + drain ----------------
@@ -224,11 +292,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
     const int er = tile * TBM + row;
     const bool row_ok = er < a.R;
     const int gi = row_ok ? idx[er] : 0;
-    float4 xi[DP4];
+    uint64_t xi2[2 * DP4];
+    uint64_t seed = 0ull;  // GRAM: (|x_i|^2, 0)
     const float* xrow = a.xs + static_cast<size_t>(gi) * DP;
+    float ni = 0.f;
 #pragma unroll
-    for (int u = 0; u < DP4; ++u) xi[u] = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+    for (int u = 0; u < DP4; ++u) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(xrow) + u);
+      float e[4] = {x.x, x.y, x.z, x.w};
+      if constexpr (GRAM) {  // (x, 1 at slot d, 0...) against the column image (-2 x, |x|^2, 0...)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (4 * u + q < a.d) ni = fmaf(e[q], e[q], ni);
+          e[q] = (4 * u + q == a.d) ? 1.f : e[q];
+        }
+      }
+      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u]) : "f"(e[0]), "f"(e[1]));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(e[2]), "f"(e[3]));
+    }
+    asm("mov.b64 %0, {%1, %2};" : "=l"(seed) : "f"(ni), "f"(0.f));
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
+    // this thread's FP64 accumulators: its row, columns quarter * DC .. + DC
+    // (registers; measured 12% faster than shared-memory accumulators)
     double acc[DC];
 #pragma unroll
     for (int e = 0; e < DC; ++e) acc[e] = 0.0;
@@ -248,44 +333,87 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
       __syncwarp();
       if (lane == 0) mbar_arrive(&d_empty[g & 1]);
     };
-    int drained = 0;
+    int drained = 0, next_drain = F + DEFER;
+    // ring positions kept incrementally (no divisions in the chunk loop)
+    int s = 0, sph = 0, ab = 0, aph = 0;  // a_empty waited from the second pass over the ring on
+    float4 xr = make_float4(0.f, 0.f, 0.f, 0.f);  // DX > 0: the row's coordinates
+    if constexpr (DX > 0) xr = __ldg(reinterpret_cast<const float4*>(xrow));
+    // Chunk k's entries are computed before its A buffer is waited for, and
+    // its TMEM stores complete while chunk k + 1 is computed: the wait::st and
+    // the a_full arrive of chunk k run at the top of chunk k + 1's store.
+    int pend = -1;  // A buffer whose stores are still in flight
+    auto publish = [&]() {
+      if (pend < 0) return;
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[pend]);
+      pend = -1;
+    };
     for (int k = 0; k < nk; ++k) {
-      const int s = k % ST, ab = k % NAB;
-      mbar_wait(&st_full[s], (k / ST) & 1);
-      if (k >= NAB) mbar_wait(&a_empty[ab], ((k / NAB) - 1) & 1);
-      tc_fence_after();
-      const float* xc = smS + s * st_floats + TBK * rw + quarter * CPT * DP;
+      SGD_WAIT(&st_full[s], sph);
+      const float* xc = smS + s * st_floats + rw + quarter * CPT * DP;
       uint32_t hi[CPT], lo[CPT];
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
-        float r2a = 0.f, r2b = 0.f;
+        if constexpr (DX > 0) {  // exactly DX <= 4 dimensions, scalar FP32
+          const float4 c = *reinterpret_cast<const float4*>(xc + t * DP);
+          const float d0 = c.x - xr.x;
+          float r2 = d0 * d0;
+          if (DX > 1) { const float d1 = c.y - xr.y; r2 = fmaf(d1, d1, r2); }
+          if (DX > 2) { const float d2 = c.z - xr.z; r2 = fmaf(d2, d2, r2); }
+          if (DX > 3) { const float d3 = c.w - xr.w; r2 = fmaf(d3, d3, r2); }
+          const float r = sqrt_approx(r2);
+          const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
+          hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
+          lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
+          continue;
+        }
+        // packed FP32x2 (FADD2/FFMA2): two dimensions per instruction
+        const uint32_t xaddr = smem_u32(xc + t * DP);
+        uint64_t acc0 = seed, acc1 = 0ull;
 #pragma unroll
         for (int u = 0; u < DP4; ++u) {
-          const float4 c = reinterpret_cast<const float4*>(xc + t * DP)[u];
-          const float d0 = c.x - xi[u].x, d1 = c.y - xi[u].y, d2 = c.z - xi[u].z, d3 = c.w - xi[u].w;
-          r2a = fmaf(d0, d0, r2a);
-          r2b = fmaf(d1, d1, r2b);
-          r2a = fmaf(d2, d2, r2a);
-          r2b = fmaf(d3, d3, r2b);
+          uint64_t c01, c23;
+          asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(c01), "=l"(c23) : "r"(xaddr + 16 * u));
+          if constexpr (GRAM) {  // r^2 = |x_i|^2 + x_i.(-2 x_c) + |x_c|^2
+            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc0) : "l"(c01), "l"(xi2[2 * u]));
+            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc1) : "l"(c23), "l"(xi2[2 * u + 1]));
+          } else {
+            uint64_t d01, d23;
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(c01), "l"(xi2[2 * u]));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(c23), "l"(xi2[2 * u + 1]));
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc0) : "l"(d01));
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc1) : "l"(d23));
+          }
         }
-        const float r = sqrt_approx(r2a + r2b);
+        uint64_t accs;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(accs) : "l"(acc0), "l"(acc1));
+        float s0, s1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(accs));
+        const float r = sqrt_approx(GRAM ? fmaxf(s0 + s1, 0.f) : s0 + s1);
         const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
         hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
         lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[s]);  // x_c consumed
+      if (k >= NAB) SGD_WAIT(&a_empty[ab], aph);
+      publish();  // chunk k - 1
+      tc_fence_after();
       const uint32_t abase = tmem + lane_addr + A_COL0 + ab * 64 + quarter * CPT;
       tc_st8(abase, hi);
       tc_st8(abase + 32, lo);
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&a_full[ab]);
-        mbar_arrive(&st_empty[s]);
-      }
+      pend = ab;
+      if (++s == ST) { s = 0; sph ^= 1; }
+      if (++ab == NAB) { ab = 0; if (k >= NAB) aph ^= 1; }
       // deferred drain: group g once chunk (g + 1) F + DEFER is in flight
-      if (k >= DEFER && (k - DEFER) % F == 0 && (k - DEFER) / F >= 1) drain(drained++);
+      if (k == next_drain) {
+        drain(drained++);
+        next_drain += F;
+      }
     }
+    publish();
     while (drained < ngroups) drain(drained++);
     if (row_ok) {
       double* prow = a.part + (static_cast<size_t>(split) * a.R + er) * a.m;
@@ -304,29 +432,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
   }
 }
 
-template <int NPAD, int DP4>
+template <int NPAD, int DP4, bool GRAM, int DX = 0>
 void launch_one(const SgdSlabArgs& a, cudaStream_t s) {
   constexpr int DP = 4 * DP4;
-  const size_t st_floats = static_cast<size_t>(TBK) * a.rw + TBK * DP + TBK;
-  const size_t smem = sizeof(float) * (SB * 2 * NPAD * TBK + ST * st_floats) + 64 * sizeof(uint64_t);
+  const size_t smem = sgd_smem_bytes<NPAD>(a.rw, DP, a.ntab);
   if (smem > 227 * 1024) throw std::invalid_argument("gpk: SGD slab kernel shared memory exceeds 227 KB");
   static size_t configured = 0;
   if (smem > configured) {
-    GPK_CUDA(cudaFuncSetAttribute(sgd_slab_kernel<NPAD, DP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    GPK_CUDA(cudaFuncSetAttribute(sgd_slab_kernel<NPAD, DP4, GRAM, DX>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     configured = smem;
   }
-  sgd_slab_kernel<NPAD, DP4><<<dim3((a.R + TBM - 1) / TBM, a.splits), NTHREADS, smem, s>>>(a);
+  sgd_slab_kernel<NPAD, DP4, GRAM, DX><<<dim3((a.R + TBM - 1) / TBM, a.splits), NTHREADS, smem, s>>>(a);
   check_launch("sgd_slab_kernel");
 }
 
 template <int NPAD>
 void launch_n(const SgdSlabArgs& a, cudaStream_t s) {
   switch (a.dp / 4) {
-    case 1: return launch_one<NPAD, 1>(a, s);
-    case 2: return launch_one<NPAD, 2>(a, s);
-    case 3: return launch_one<NPAD, 3>(a, s);
-    case 4: return launch_one<NPAD, 4>(a, s);
+    case 1:
+      if (a.xg) return launch_one<NPAD, 1, true>(a, s);
+      switch (a.d) {  // exact-dimension scalar distance loops for d <= 4
+        case 1: return launch_one<NPAD, 1, false, 1>(a, s);
+        case 2: return launch_one<NPAD, 1, false, 2>(a, s);
+        case 3: return launch_one<NPAD, 1, false, 3>(a, s);
+        default: return launch_one<NPAD, 1, false, 4>(a, s);
+      }
+    case 2: return a.xg ? launch_one<NPAD, 2, true>(a, s) : launch_one<NPAD, 2, false>(a, s);
+    case 3: return a.xg ? launch_one<NPAD, 3, true>(a, s) : launch_one<NPAD, 3, false>(a, s);
+    case 4: return a.xg ? launch_one<NPAD, 4, true>(a, s) : launch_one<NPAD, 4, false>(a, s);
     default: throw std::invalid_argument("gpk: the SGD slab kernel supports d <= 16");
   }
 }
@@ -416,9 +550,9 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
       a.Mb[o] = mn;
       a.Vb[o] = vn;
       a.resid[o] = -g;
-      float* rec = a.rec + static_cast<size_t>(li) * a.rw;
-      rec[j] = static_cast<float>(vn);
-      rec[a.moff + j] = static_cast<float>(mn);
+      const size_t ro = static_cast<size_t>(li / 32) * a.rw + sgd_record_pos(li % 32, j);
+      a.rec[ro] = static_cast<float>(vn);
+      a.rec[ro + a.moff] = static_cast<float>(mn);
     }
   }
   if (rl < APPLY_ROWS) gs[rl][j] = g2;
@@ -483,17 +617,37 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
   }
 }
 
+// Gram column image for the SGD slab: (-2 x, |x|^2 at slot d, 0...) of the
+// scaled FP32 inputs (rows beyond n zero), |x|^2 by the same FP32 chain the
+// kernel uses for its rows
+__global__ void sgd_gram_image_kernel(const float* xs, int rows, int n, int d, int dp, float* xg) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    float ni = 0.f;
+    for (int k = 0; k < dp; ++k) {
+      const float x = i < n ? xs[static_cast<size_t>(i) * dp + k] : 0.f;
+      if (k < d) ni = fmaf(x, x, ni);
+      xg[static_cast<size_t>(i) * dp + k] = k < d ? -2.f * x : 0.f;
+    }
+    if (i < n) xg[static_cast<size_t>(i) * dp + d] = ni;
+  }
+}
+
 // initial records from the warm-start solution: V32 = V0, M32 = 0, tau = -1
-__global__ void sgd_records_init_kernel(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec,
+__global__ void sgd_records_init_kernel(const double* V, int nloc, int nchunks, int m, int rw, int moff, float* rec,
                                         int* tau) {
-  const long long total = static_cast<long long>(rows_pad) * rw;
+  const long long total = static_cast<long long>(nchunks) * rw;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int i = static_cast<int>(e / rw), c = static_cast<int>(e % rw);
+    const int q = static_cast<int>(e / rw), w = static_cast<int>(e % rw);
     float v = 0.f;
-    if (i < nloc && c < m) v = static_cast<float>(V[static_cast<size_t>(i) * m + c]);
+    if (w < moff) {  // V image: element (c, j) at ((j / 8) 8 + c / 4) 32 + (j % 8) 4 + c % 4
+      const int core = w >> 5, ln = w & 31;
+      const int j = (core >> 3) * 8 + (ln >> 2), c = (core & 7) * 4 + (ln & 3);
+      const int i = q * 32 + c;
+      if (i < nloc && j < m) v = static_cast<float>(V[static_cast<size_t>(i) * m + j]);
+    }
     rec[e] = v;
-    if (c == 0) tau[i] = -1;
+    if (w < 32) tau[q * 32 + w] = -1;
   }
 }
 
@@ -513,10 +667,9 @@ __global__ void sgd_materialise_kernel(double* Vb, const double* Mb, const int* 
 }  // namespace
 
 int sgd_record_width(int m, int* moff) {
-  int half = (m + 3) / 4 * 4;
-  while ((2 * half) % 32 != 8) half += 4;  // rows 8 banks apart: conflict-free B builds
-  if (moff) *moff = half;
-  return 2 * half;
+  const int img = 256 * ((m + 7) / 8);  // j-groups of 8 x 32 chunk columns
+  if (moff) *moff = img;
+  return 2 * img;
 }
 
 void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s) {
@@ -528,6 +681,11 @@ void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s) {
     case 80: return launch_n<80>(a, s);
     default: throw std::invalid_argument("gpk: the SGD slab kernel supports m <= 80");
   }
+}
+
+void sgd_gram_image_launch(const float* xs, int rows, int n, int d, int dp, float* xg, cudaStream_t s) {
+  sgd_gram_image_kernel<<<std::max(1, std::min(148 * 4, (rows + 255) / 256)), 256, 0, s>>>(xs, rows, n, d, dp, xg);
+  check_launch("sgd_gram_image");
 }
 
 void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s) {
@@ -545,9 +703,10 @@ void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s) {
 
 void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
                              cudaStream_t s) {
-  const long long total = static_cast<long long>(rows_pad) * rw;
+  const int nchunks = rows_pad / 32;
+  const long long total = static_cast<long long>(nchunks) * rw;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-  sgd_records_init_kernel<<<blocks, 256, 0, s>>>(V, nloc, rows_pad, m, rw, moff, rec, tau);
+  sgd_records_init_kernel<<<blocks, 256, 0, s>>>(V, nloc, nchunks, m, rw, moff, rec, tau);
   check_launch("sgd_records_init");
 }
 
