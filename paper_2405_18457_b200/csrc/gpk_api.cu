@@ -70,6 +70,16 @@ int dense_cache_cap() {
   return cap;
 }
 
+// n <= dense_cache_cap: products by the FP64 on-the-fly operator (default) or,
+// GPK_DENSE_DGEMM=1, by cuBLAS DGEMM on a materialised FP64 kernel matrix
+bool dense_dgemm() {
+  static const bool on = [] {
+    const char* e = std::getenv("GPK_DENSE_DGEMM");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // Tensor-core Gram distances for d >= GPK_TGRAM_MIN_D (default 16; measured
 // on one B200 with the warp-converged MMA issue: full products at d = 26
 // -21%, d = 20 -15%, d = 11 +2%, d = 3 +16%);
@@ -184,6 +194,12 @@ struct gpk_ctx {
   cudaEvent_t ev_m2a = nullptr, ev_aux = nullptr;
   ncclComm_t comm = nullptr;   // multi-GPU (one process per GPU)
   int nranks = 1, rank = 0;
+  // ring all-gather of the sharded operator's RHS on its own stream, one event
+  // per received slice (apply_local)
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ring_ev;
+  cudaEvent_t ring_start = nullptr;
+  bool ring_gather = true;  // GPK_RING_GATHER=0: one all-gather, then one operator launch
 };
 
 struct gpk_operator {
@@ -216,6 +232,7 @@ struct gpk_operator {
   double s = 1, s2 = 1, sigma = 1, sigma2 = 1;
   DBuf<double> part;      // kv split partials
   DBuf<float> vpk;        // packed TF32 hi/lo RHS images (tcgen05 path)
+  DBuf<float> v32g;       // sharded products: the all-gathered FP32 RHS [S nr][m]
   DBuf<double> pts64, pts64s;  // posterior query points FP64 [p][d] (raw, scaled)
   DBuf<float> pts32;           // and scaled FP32 [p + 32][dp]
   DBuf<float> ptsg32;          // and their Gram image [p + 32][dpg]
@@ -325,6 +342,11 @@ struct NcclApi {
   decltype(&ncclCommInitRank) comm_init_rank = nullptr;
   decltype(&ncclCommDestroy) comm_destroy = nullptr;
   decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
 };
 const NcclApi& nccl() {
@@ -337,8 +359,14 @@ const NcclApi& nccl() {
     a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
     a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+    a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
     a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
-    if (!a.get_unique_id || !a.comm_init_rank || !a.comm_destroy || !a.all_gather || !a.error_string)
+    if (!a.get_unique_id || !a.comm_init_rank || !a.comm_destroy || !a.all_gather || !a.all_reduce || !a.send ||
+        !a.recv || !a.group_start || !a.group_end || !a.error_string)
       throw std::runtime_error("gpk: libnccl.so.2 lacks required symbols");
     return a;
   }();
@@ -353,6 +381,17 @@ void gather_inplace(gpk_operator* op, void* buf, size_t bytes_per_rank) {
   const ncclResult_t r = nccl().all_gather(b + static_cast<size_t>(op->rk) * bytes_per_rank, b, bytes_per_rank,
                                            ncclChar, ctx->comm, ctx->stream);
   if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllGather: ") + nccl().error_string(r));
+  count_launch();
+}
+
+// In-place FP64 sum over the ranks (no-op on one rank). Every rank receives
+// the same values (NCCL's reduction result is broadcast), so decisions taken
+// from them agree across ranks.
+void allreduce_inplace(gpk_operator* op, double* buf, size_t count) {
+  if (!op->sharded) return;
+  gpk_ctx* ctx = op->ctx;
+  const ncclResult_t r = nccl().all_reduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().error_string(r));
   count_launch();
 }
 
@@ -406,7 +445,7 @@ void set_hyper(gpk_operator* op, const double* raw) {
   prescale_launch(op->x64.p, op->n, d, op->dp, il, op->xs32.p, op->xs64.p, s);
   if (op->dpg) gram_image_launch(op->xs32.p, op->n, d, op->dp, op->dpg, op->xg32.p, s);
   if (op->tg) tg_image_launch(op->xs32.p, op->n, d, op->dp, op->xtg.p, s);
-  if (op->dense)
+  if (op->dense && dense_dgemm())
     dense_block64_launch(op->xs64.p, op->n, d, op->s2, op->sigma2, 0, op->n, 0, op->n,
                          op->kdense.ensure(static_cast<size_t>(op->n) * op->n), op->n, 0, s);
   GPK_CUDA(cudaStreamSynchronize(s));  // inv_ls host buffer lifetime
@@ -610,7 +649,17 @@ void run_kv(gpk_operator* op, const KvCall& c) {
     if (prof_end) GPK_CUDA(cudaEventRecord(*prof_end, s));
     return;
   }
-  if (dense) {
+  if (dense && !dense_dgemm()) {
+    // FP64 operator with on-the-fly entries (kv64_kernel): the reference's
+    // exact FP64 products for n <= dense_cache_cap without materialising H
+    const int sp = kv64_splits(op->n, op->n, op->ctx->sms);
+    double* p64 = op->part.ensure(static_cast<size_t>(sp) * op->n * c.m);
+    kv64_launch(op->xs64.p, op->n, op->d, op->s2, 0, op->n, c.vdiag, c.m, sp, p64, c.skip, s);
+    if (a.stats) stats_add_launch(a.stats, static_cast<double>(op->n) * op->n, c.m, op->d, c.skip, s);
+    r.part = p64;
+    r.splits = sp;
+    r.sk_G = 0;
+  } else if (dense) {
     // part (row-major [n][m]) = K V: column-major part^T (m x n) = V^T K (K symmetric)
     gpk_ctx* cx = op->ctx;
     if (cublasSetStream(cx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
@@ -631,6 +680,66 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   kv_reduce_launch(r, s);
 }
 
+// Ring all-gather overlapped with the operator: the slices of the
+// FP32 RHS travel one hop per step on the communication stream (step j:
+// send slice rk - j to rank rk + 1, receive slice rk - j - 1 from rank rk - 1),
+// and as each slice lands the compute stream packs its TF32 images and runs
+// the operator over that column block, accumulating into out (the own slice,
+// which holds the noise diagonal, first; the fused column dot on the last).
+// With n/N rows per slice the transfer of a slice hides behind the product
+// of the previous one whenever a slice's compute outlasts its transfer.
+void apply_local_ring(gpk_operator* op, float* v32, const double* v_local, int m, double* out, const double* base,
+                      double alpha, const int* skip, const double* dotw, double* dpart) {
+  gpk_ctx* ctx = op->ctx;
+  cudaStream_t s = ctx->stream, cs = ctx->comm_stream;
+  const int S = op->S, nr = op->nr, rk = op->rk, n = op->n;
+  const size_t slice = static_cast<size_t>(S) * m;
+  const size_t cf = kv_tc_pack_floats(m, 32);  // floats per 32-row image chunk
+  float* vpk = op->vpk.ensure(kv_tc_pack_floats(m, S * nr));
+  GPK_CUDA(cudaEventRecord(ctx->ring_start, s));  // own slice converted
+  GPK_CUDA(cudaStreamWaitEvent(cs, ctx->ring_start, 0));
+  const int next = (rk + 1) % nr, prev = (rk + nr - 1) % nr;
+  for (int j = 0; j + 1 < nr; ++j) {
+    const int snd = (rk - j + nr) % nr, rcv = (rk - j - 1 + 2 * nr) % nr;
+    nccl().group_start();
+    ncclResult_t r1 = nccl().send(v32 + snd * slice, slice, ncclFloat, next, ctx->comm, cs);
+    ncclResult_t r2 = nccl().recv(v32 + rcv * slice, slice, ncclFloat, prev, ctx->comm, cs);
+    const ncclResult_t r3 = nccl().group_end();
+    if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
+      throw std::runtime_error(std::string("gpk ring all-gather: ") +
+                               nccl().error_string(r1 != ncclSuccess ? r1 : r2 != ncclSuccess ? r2 : r3));
+    count_launch();
+    GPK_CUDA(cudaEventRecord(ctx->ring_ev[rcv], cs));
+  }
+  for (int j = 0; j < nr; ++j) {
+    const int src = (rk - j + nr) % nr;
+    if (j > 0) GPK_CUDA(cudaStreamWaitEvent(s, ctx->ring_ev[src], 0));
+    const int c0 = src * S, rows = std::max(0, std::min(S, n - c0));
+    if (rows == 0) continue;
+    float* img = vpk + static_cast<size_t>(src) * (S / 32) * cf;
+    kv_tc_pack_launch(nullptr, v32 + src * slice, m, S, m, nullptr, 0, n, img, skip, s, rows);
+    KvCall c;
+    c.vpk = img;
+    c.m = m;
+    c.r0 = op->row0;
+    c.R = op->nloc;
+    c.c0 = c0;
+    c.C = rows;
+    c.vdiag = src == rk ? v_local : nullptr;
+    c.vshift = 0;
+    c.out = out;
+    c.ldo = m;
+    c.base = j == 0 ? base : out;
+    c.ldb = m;
+    c.alpha = alpha;
+    c.skip = skip;
+    const bool last = j + 1 == nr;
+    c.dotw = last ? dotw : nullptr;
+    c.dpart = last ? dpart : nullptr;
+    run_kv(op, c);
+  }
+}
+
 // out_local = base + alpha * H[own rows, :] V, for V given by this rank's rows
 // v_local (FP64 [nloc][m]). The local rows are packed into this rank's slice
 // of the TF32 image buffer and all-gathered so every rank holds the full RHS.
@@ -639,12 +748,23 @@ void apply_local(gpk_operator* op, const double* v_local, int m, double* out, co
                  const int* skip, const double* dotw = nullptr, double* dpart = nullptr) {
   cudaStream_t s = op->ctx->stream;
   const int S = op->S, nr = op->nr;
-  const size_t chunk_floats = kv_tc_pack_floats(m, 32);
-  const size_t mine = kv_tc_pack_floats(m, S);
-  float* vpk = op->vpk.ensure(mine * nr);
-  kv_tc_pack_launch(v_local, nullptr, m, S, m, nullptr, 0, op->n, vpk + mine * op->rk, skip, s, op->nloc);
-  gather_inplace(op, vpk, mine * sizeof(float));
-  (void)chunk_floats;
+  // the rank's rows in FP32 (4 m bytes a row on the wire, not the 8 NPAD of
+  // the TF32 hi/lo images), all-gathered into the full-height RHS (rank
+  // slices S rows apart = global row order), then packed into the operator's
+  // TF32 images locally
+  float* v32 = op->v32g.ensure(static_cast<size_t>(S) * nr * m);
+  float* mine = v32 + static_cast<size_t>(op->rk) * S * m;
+  to_f32_launch(v_local, op->nloc, m, m, mine, m, skip, s);
+  if (op->nloc < S)
+    GPK_CUDA(cudaMemsetAsync(mine + static_cast<size_t>(op->nloc) * m, 0, sizeof(float) * (S - op->nloc) * m, s));
+  gpk_ctx* ctx = op->ctx;
+  if (op->sharded && nr > 1 && ctx->ring_gather && ctx->comm_stream) {
+    apply_local_ring(op, v32, v_local, m, out, base, alpha, skip, dotw, dpart);
+    return;
+  }
+  gather_inplace(op, v32, sizeof(float) * S * m);
+  float* vpk = op->vpk.ensure(kv_tc_pack_floats(m, S * nr));
+  kv_tc_pack_launch(nullptr, v32, m, S * nr, m, nullptr, 0, op->n, vpk, skip, s, op->n);
   KvCall c;
   c.vpk = vpk;
   c.m = m;
@@ -1704,7 +1824,7 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   splits = std::max(1, (nloc + cps - 1) / cps);
   double* part = b->sgd_part.ensure(static_cast<size_t>(splits) * bs * m);
   const long long stride = (static_cast<long long>(bs) * m + m + 1 + 31) / 32 * 32;  // doubles per rank slice
-  double* gbuf = b->w4.ensure(static_cast<size_t>(nr) * stride);
+  double* gbuf = b->w4.ensure(static_cast<size_t>(stride));
   double* red = b->red.ensure(static_cast<size_t>(nr) * G * 2 * m + 8);
   double* sumsq = b->vec1.ensure(m);
   int* flags = b->sgd_flags.ensure(2);
@@ -1784,10 +1904,13 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   ta.rho = c->momentum;
   ta.step = step;
   ta.tol = c->tolerance;
-  ta.slice = gbuf + static_cast<size_t>(op->sharded ? op->rk : 0) * stride;
+  // one FP64 all-reduce of the b x m partials (+ old residual squares, flag)
+  // per iteration: every rank reads the same sums
+  ta.slice = gbuf;
   ta.gbuf = gbuf;
   ta.stride = stride;
-  ta.nr = nr;
+  ta.nr = 1;
+  ta.sharded = op->sharded ? 1 : 0;
   ta.nonfinite = flags;
   ta.nonfinite_now = flags + 1;
   ta.rec = rec;
@@ -1804,7 +1927,7 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
     sgd_slab_launch(sa, s);
     if (pe) GPK_CUDA(cudaEventRecord(*pe, s));
     sgd_reduce_launch(ta, s);
-    gather_inplace(op, gbuf, sizeof(double) * stride);
+    allreduce_inplace(op, gbuf, static_cast<size_t>(bs) * m + m + 1);
     sgd_apply_launch(ta, s);
     ++t;
   };
@@ -2455,6 +2578,14 @@ gpk_status gpk_ctx_init_comm(gpk_ctx* ctx, const unsigned char* id128, int nrank
     if (r != ncclSuccess) throw std::runtime_error(std::string("ncclCommInitRank: ") + nccl().error_string(r));
     ctx->nranks = nranks;
     ctx->rank = rank;
+    if (const char* e = std::getenv("GPK_RING_GATHER")) ctx->ring_gather = std::atoi(e) != 0;
+    if (!ctx->comm_stream) {
+      GPK_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+      GPK_CUDA(cudaEventCreateWithFlags(&ctx->ring_start, cudaEventDisableTiming));
+    }
+    for (cudaEvent_t e : ctx->ring_ev) cudaEventDestroy(e);
+    ctx->ring_ev.assign(nranks, nullptr);
+    for (auto& e : ctx->ring_ev) GPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   });
 }
 
@@ -3036,9 +3167,10 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
     if (opp->nloc < 1) throw InvalidArgument("gpk_optimise: fewer rows than ranks * 32");
   }
   if (!opp->sharded && n <= dense_cache_cap()) {  // outer_loop.cpp:72: options.dense_cache = n <= cap
-    opp->dense = true;
-    dense_block64_launch(opp->xs64.p, n, d, opp->s2, opp->sigma2, 0, n, 0, n,
-                         opp->kdense.ensure(static_cast<size_t>(n) * n), n, 0, ctx->stream);
+    opp->dense = true;  // FP64 products (kv64_kernel; GPK_DENSE_DGEMM=1: cached matrix + DGEMM)
+    if (dense_dgemm())
+      dense_block64_launch(opp->xs64.p, n, d, opp->s2, opp->sigma2, 0, n, 0, n,
+                           opp->kdense.ensure(static_cast<size_t>(n) * n), n, 0, ctx->stream);
   }
   const int nloc = opp->nloc;
   cudaStream_t stream = ctx->stream;

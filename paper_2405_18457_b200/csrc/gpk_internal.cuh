@@ -260,7 +260,8 @@ struct SgdStepArgs {
   double* slice;        // this rank's slice of gbuf: [b*m] partial g, [m] old R^2, [1] flag
   const double* gbuf;   // all ranks' slices (stride doubles apart)
   long long stride;
-  int nr;
+  int nr;               // slices to sum (1 after an all-reduce)
+  int sharded;          // several ranks: own-row divergence is carried to the next iteration
   int* nonfinite;       // carried divergence flag (own rows)
   int* nonfinite_now;   // this iteration's (bit 0 any, bit 1 g itself)
   float* rec;
@@ -425,6 +426,10 @@ void sgd_update_pack_launch(double* M, double* V, double* R, float* vpk, int npa
 void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, const int* skip, cudaStream_t s);
 
 // RFF (K5) + noise (K9)
+// FP64 on-the-fly operator (n <= dense_cache_cap): split partials for kv_reduce
+int kv64_splits(int R, int n, int sms);
+void kv64_launch(const double* xs64, int n, int d, double sv, int r0, int R, const double* v, int m, int splits,
+                 double* part, const int* skip, cudaStream_t s);
 // derivative_apply for k <= d (kernel.cpp:200-236), FP64: out [n][m] row-major;
 // coef = 3 s2 / l_k (k < d) or 2 / s (k == d)
 void deriv_apply_launch(const double* xs64, int n, int d, int k, double sv, double coef, const double* v, int m,

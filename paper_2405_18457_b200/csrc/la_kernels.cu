@@ -1709,6 +1709,83 @@ void deriv_apply_launch(const double* xs64, int n, int d, int k, double sv, doub
   check_launch("deriv_apply");
 }
 
+// FP64 operator product with on-the-fly kernel evaluation (the high-accuracy
+// operator for n <= dense_cache_cap, where the reference caches H in FP64):
+// part[split][r][j] = sum over the split's columns c of k(x_{r0+r}, x_c) v[c][j]
+// (kernel only; kv_reduce adds sigma^2 v on the diagonal). CTA = 32 rows x one
+// column split; per 32-column chunk the FP64 entries go to shared memory and
+// each thread accumulates 4 rows x its columns j = lane + 32 u (ascending c).
+__global__ void __launch_bounds__(256) kv64_kernel(const double* __restrict__ xs, int n, int d, double sv, int r0,
+                                                   int R, const double* __restrict__ v, int m, int cols_per_split,
+                                                   double* __restrict__ part, const int* skip) {
+  if (skip && *skip) return;
+  __shared__ double xr[32][33];
+  __shared__ double xc[32][33];
+  __shared__ double kt[32][33];
+  __shared__ double vt[32][80];
+  const int tid = threadIdx.x, lane = tid & 31, rg = tid >> 5;
+  const int rb = blockIdx.x * 32;
+  const int cb = blockIdx.y * cols_per_split, ce = min(n, cb + cols_per_split);
+  for (int e = tid; e < 32 * d; e += 256) {
+    const int r = e / d, q = e % d;
+    xr[r][q] = rb + r < R ? xs[static_cast<size_t>(r0 + rb + r) * d + q] : 0.0;
+  }
+  double acc[4][3] = {};
+  for (int c0 = cb; c0 < ce; c0 += 32) {
+    const int cn = min(32, ce - c0);
+    __syncthreads();
+    for (int e = tid; e < 32 * d; e += 256) {
+      const int c = e / d, q = e % d;
+      xc[c][q] = c < cn ? xs[static_cast<size_t>(c0 + c) * d + q] : 0.0;
+    }
+    for (int e = tid; e < 32 * m; e += 256) {
+      const int c = e / m, j = e % m;
+      vt[c][j] = c < cn ? v[static_cast<size_t>(c0 + c) * m + j] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += 256) {
+      const int c = e >> 5, r = e & 31;
+      double r2 = 0.0;
+      for (int q = 0; q < d; ++q) {
+        const double t = xc[c][q] - xr[r][q];
+        r2 += t * t;
+      }
+      const double rr = sqrt(r2);
+      kt[c][r] = c < cn ? sv * (1.0 + kSqrt3 * rr) * exp(-kSqrt3 * rr) : 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < cn; ++c)
+#pragma unroll
+      for (int a4 = 0; a4 < 4; ++a4) {
+        const double kv = kt[c][rg * 4 + a4];
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+          if (lane + 32 * u < m) acc[a4][u] = fma(kv, vt[c][lane + 32 * u], acc[a4][u]);
+      }
+  }
+#pragma unroll
+  for (int a4 = 0; a4 < 4; ++a4) {
+    const int r = rb + rg * 4 + a4;
+    if (r >= R) continue;
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (lane + 32 * u < m) part[(static_cast<size_t>(blockIdx.y) * R + r) * m + lane + 32 * u] = acc[a4][u];
+  }
+}
+int kv64_splits(int R, int n, int sms) {
+  const int rb = (R + 31) / 32;
+  const int want = std::max(1, (4 * sms + rb - 1) / rb);  // ~4 CTAs per SM
+  return std::min(want, std::max(1, (n + 31) / 32));
+}
+void kv64_launch(const double* xs64, int n, int d, double sv, int r0, int R, const double* v, int m, int splits,
+                 double* part, const int* skip, cudaStream_t s) {
+  if (d > 32 || m > 80) throw std::invalid_argument("gpk: the FP64 operator supports d <= 32 and m <= 80");
+  int cps = (n + splits - 1) / splits;
+  cps = (cps + 31) / 32 * 32;
+  kv64_kernel<<<dim3((R + 31) / 32, splits), 256, 0, s>>>(xs64, n, d, sv, r0, R, v, m, cps, part, skip);
+  check_launch("kv64_kernel");
+}
+
 // K5, streaming (rff.cpp:36-54, 64-73): prior[i][j] = sum_q phi_q(x_i) W[q][j]
 // without materialising Phi. CTA = 64 rows x 64 samples; per chunk of 16
 // pairs the CTA forms phi (FP64 angles, sincos, interleaved cos/sin as

@@ -593,7 +593,7 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
   double pend = 0.0;
   for (int r = 0; r < a.nr; ++r) pend += a.gbuf[static_cast<size_t>(r) * a.stride + bm + m];
   const int now = *a.nonfinite_now;
-  const bool diverged = (a.nr == 1 ? now != 0 : (now & 2) != 0) || pend != 0.0;
+  const bool diverged = (!a.sharded ? now != 0 : (now & 2) != 0) || pend != 0.0;
   if (threadIdx.x == 0) {
     *a.ticket = 0u;
     if (now) *a.nonfinite = 1;

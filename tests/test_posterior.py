@@ -89,3 +89,23 @@ def test_gpu_cross_kernel_gram_form_matches_oracle(gpk_ctx, oracle):
     gv = G.cross_kernel_apply(op, P, V)
     rv = oracle.cross_apply(P, X, raw, V, threads=8)
     assert max(np.max(np.abs(gv[:, j] - rv[:, j])) / np.max(np.abs(rv[:, j])) for j in range(65)) <= 2e-5
+
+
+@pytest.mark.gpu
+def test_gpu_compare_oracle_outputs(gpk_ctx, tmp_path):
+    """`gpiter compare-oracle` on the GPU (gpiter_cli.cpp:230-280): the iterative
+    pathwise trajectory against Adam on the exact marginal likelihood from the
+    same initialisation; both written in the reference tool's formats."""
+    import json
+
+    from oracle import oracle as O
+    from paper_2405_18457_b200 import gpiter, outputs
+    X32, y32 = O.sinsum_dataset(512, 3, False, 0.1, 0)
+    sc = gpiter.SolverConfig(kind=0, tolerance=1e-4, max_epochs=200, preconditioner_rank=50)
+    cfg = gpiter.OuterConfig(estimator=1, solver=sc, warm_start=True, steps=5, learning_rate=0.1, probe_count=64,
+                             rff_pairs=1024, probe_seed=2, feature_seed=3, solver_seed=4, init_value=1.0)
+    out = outputs.compare_oracle(gpk_ctx, X32.astype(np.float64), y32.astype(np.float64), cfg, tmp_path)
+    assert json.loads((tmp_path / "compare_oracle.json").read_text()) == out
+    assert sum(out["histogram_counts"]) == 5 * 5
+    # Adam's first steps are sign-driven: both trajectories move together
+    assert out["max_abs_diff"] < 0.05

@@ -174,3 +174,46 @@ def test_gpu_c5_step_matches_scale_fixture(gpk_ctx):
     g = fixture("c5_scale.npz")
     r = _optimise(G, gpk_ctx, C5, 1, "C5", 64, 2048, 0, 5, 500, 30.0)
     _check_steps(r, g)
+
+
+@pytest.mark.gpu
+def test_gpu_c3_cg_step_is_rounding_sensitive(oracle):
+    """BASELINE configs[2] (C3: n = 43008, CG early-stopped at 10 epochs): the
+    FP64 oracle-at-scale reproduces the CPU oracle's first 2 steps to ~1e-7
+    (only the summation order differs), but with every H.V entry perturbed by
+    a relative 1e-7 -- the rounding level of any FP32 operator -- the second
+    step's residual norms move by percent and its gradient by more than the
+    1e-4 bar. This pins why the product's FP32 operator is held to the
+    iteration and trajectory bars at C3, with its residual norms and
+    gradients checked at the measured levels (tests/test_golden.py)."""
+    import bench
+    g = np.load(os.path.join(GOLD, "c3.npz"))
+    c = bench.CONFIGS["C3"]
+    X32, y32 = oracle.sinsum_dataset(c["n"], c["d"], c["uniform"], c["noise"], 0)
+    X = np.asfortranarray(X32.astype(np.float64))
+    sc = oracle.solver_config(kind=0, tolerance=0.01, max_epochs=10, preconditioner_rank=100)
+    oc = oracle.outer_config(estimator=1, solver=sc, warm_start=True, steps=2, learning_rate=0.1, probe_count=64,
+                             rff_pairs=1000, probe_seed=2, feature_seed=3, solver_seed=4)
+    runs = {}
+    with oracle.gpu_backend(0):
+        for noise in (0.0, 1e-7):
+            oracle.set_apply_sensitivity(0, noise)
+            try:
+                runs[noise] = oracle.optimise(X, y32.astype(np.float64), oc, init_constrained=[1.0] * 20 + [1.0, 0.1],
+                                              threads=os.cpu_count())
+            finally:
+                oracle.set_apply_sensitivity(0, 0.0)
+
+    def rel(r, key):
+        return np.abs(r[key] - g["traj_" + key]) / g["traj_" + key]
+
+    exact, noisy = runs[0.0], runs[1e-7]
+    assert np.array_equal(exact["iterations"], g["traj_iterations"])
+    assert np.max(rel(exact, "mean_residual_norm")) <= 1e-5
+    assert np.max(rel(exact, "probe_residual_norm")) <= 1e-5
+    gg = g["traj_gradient"]
+    assert np.max(np.abs(exact["gradient"] - gg)) <= 1e-8 * np.max(np.abs(gg))
+    # measured: step 2 mean norm 9.4%, probe 2.2%, gradient 2.8e-4 of its largest component
+    assert rel(noisy, "mean_residual_norm")[1] > 1e-2
+    assert rel(noisy, "probe_residual_norm")[1] > 1e-3
+    assert np.max(np.abs(noisy["gradient"][1] - gg[1])) > 1e-4 * np.max(np.abs(gg[1]))

@@ -37,3 +37,41 @@ def test_trace_csv_matches_reference_format(tmp_path):
                  "1" if tr["solver_diverged"][t] else "0"]
         assert lines[t + 1] == ",".join(want)
         assert [float(x) for x in lines[t + 1].split(",")[1:d + 3]] == list(tr["constrained"][t])  # round trip
+
+
+def test_compare_oracle_files_match_reference_format(tmp_path):
+    """differences.csv / compare_oracle.json of `gpiter compare-oracle`
+    (proj/tools/gpiter_cli.cpp:247-278): header, round-trip doubles, log10 bins."""
+    from paper_2405_18457_b200 import outputs
+    a = np.array([[1.0, 0.5, 0.25], [1.1, 0.6, 0.3]])
+    b = a + np.array([[0.0, 3e-9, 2e-5], [0.5, 1e-3, 4.0]])
+    out = outputs.write_differences(tmp_path, a, b)
+    lines = (tmp_path / "differences.csv").read_text().splitlines()
+    assert lines[0] == "step,coordinate,iterative,exact,abs_diff"
+    assert len(lines) == 1 + a.size
+    assert lines[1] == "0,0,1,1,0"
+    t, k, it, ex, df = lines[3].split(",")
+    assert (t, k) == ("0", "2") and float(it) == a[0, 2] and float(ex) == b[0, 2] and float(df) == abs(a[0, 2] - b[0, 2])
+    assert out["histogram_bin_edges"][0] == "<=1e-8" and len(out["histogram_counts"]) == 10
+    # 0 and 3e-9 -> bin 0; 2e-5 -> 1e-5..1e-4 (4); 0.5 -> 1e-1..1 (8); 1e-3 -> 1e-3..1e-2 (6); 4 -> >1 (9)
+    assert out["histogram_counts"] == [2, 0, 0, 0, 1, 0, 1, 0, 1, 1]
+    assert out["max_abs_diff"] == 4.0
+
+
+def test_summary_json_fields(tmp_path):
+    """summary.json of `gpiter train` (gpiter_cli.cpp:118-143) for a trace."""
+    import json
+
+    from paper_2405_18457_b200 import gpiter, outputs
+    res = {"final_raw": np.array([gpiter.softplus_inverse(v) for v in (0.7, 1.3, 0.9, 0.2)]),
+           "epochs": np.array([3.0, 2.5]), "solver_diverged": np.array([False, True]),
+           "solver_seconds": np.array([0.1, 0.2]), "step_seconds": np.array([0.3, 0.4]),
+           "constrained": np.ones((2, 4))}
+    cfg = gpiter.OuterConfig(solver=gpiter.SolverConfig(kind=1), steps=2)
+    s = outputs.write_summary(tmp_path / "summary.json", res, cfg, n_train=100)
+    back = json.loads((tmp_path / "summary.json").read_text())
+    assert back == s
+    assert s["schema_version"] == 1 and s["steps_completed"] == 2 and s["diverged_steps"] == 1
+    assert abs(s["total_epochs"] - 5.5) < 1e-15 and s["config"]["solver"] == "ap"
+    assert np.allclose(s["hyperparameters"]["lengthscales"], [0.7, 1.3])
+    assert abs(s["solver_seconds"] - 0.3) < 1e-15 and abs(s["total_seconds"] - 0.7) < 1e-15
