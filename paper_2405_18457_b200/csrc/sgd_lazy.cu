@@ -498,10 +498,19 @@ __global__ void sgd_reduce_kernel(SgdStepArgs a) {
     }
     return;
   }
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bm; e += gb * blockDim.x) {
+  // four lanes per element: lane k of the quad sums splits k, k + 4, ...
+  // (independent loads in flight), the quad combines (s0 + s1) + (s2 + s3)
+  const int quad = threadIdx.x & 3;
+  for (int e4 = blockIdx.x * blockDim.x + threadIdx.x; e4 < 4 * bm; e4 += gb * blockDim.x) {
+    const int e = e4 >> 2;
     const int q = e / m, j = e - q * m;
     double g = 0.0;
-    for (int s = 0; s < a.splits; ++s) g += a.part[static_cast<size_t>(s) * bm + e];
+#pragma unroll 4
+    for (int s = quad; s < a.splits; s += 4) g += a.part[static_cast<size_t>(s) * bm + e];
+    const unsigned act = __activemask();  // whole quads (4 bm is a multiple of 4)
+    g += __shfl_xor_sync(act, g, 1);
+    g += __shfl_xor_sync(act, g, 2);
+    if (quad != 0) continue;
     const int li = idx[q] - a.row0;
     if (li >= 0 && li < a.nloc) {
       const size_t o = static_cast<size_t>(li) * m + j;
@@ -575,10 +584,21 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
   if (!last) return;
   __threadfence();
   __shared__ double ss[128];
+  __shared__ double red8[8][80];
+  {  // column sums of the block partials: thread (jj, k) sums blocks k, k + 8, ... then 8 partials in order
+    const int jj = threadIdx.x % m, k = threadIdx.x / m;
+    if (k < 8) {
+      double s = 0.0;
+      for (int b = k; b < static_cast<int>(gridDim.x); b += 8) s += a.gpart[static_cast<size_t>(b) * m + jj];
+      red8[k][jj] = s;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x < m) {
     const int jj = threadIdx.x;
     double s = 0.0;
-    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) s += a.gpart[static_cast<size_t>(b) * m + jj];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red8[k][jj];
     double old = 0.0;
     for (int r = 0; r < a.nr; ++r) old += a.gbuf[static_cast<size_t>(r) * a.stride + bm + jj];
     const double v = a.sumsq[jj] + (s - old);
@@ -689,7 +709,7 @@ void sgd_gram_image_launch(const float* xs, int rows, int n, int d, int dp, floa
 }
 
 void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s) {
-  const int gb = std::max(1, std::min(148 * 2, (a.b * a.m + 255) / 256));
+  const int gb = std::max(1, (4 * a.b * a.m + 255) / 256);  // one thread per (element, quarter of the splits)
   sgd_reduce_kernel<<<gb + a.m, 256, 0, s>>>(a);
   check_launch("sgd_reduce");
 }
