@@ -70,12 +70,16 @@ int dense_cache_cap() {
   return cap;
 }
 
-// n <= dense_cache_cap: products by the FP64 on-the-fly operator (default) or,
-// GPK_DENSE_DGEMM=1, by cuBLAS DGEMM on a materialised FP64 kernel matrix
+// n <= dense_cache_cap: FP64 products as the reference computes them there
+// (outer_loop.cpp:72 caches H in FP64) -- by DGEMM on the cached FP64 kernel
+// matrix (default: 0.16 ms per C1 CG iteration), or with GPK_DENSE_KV64=1 by
+// the FP64 on-the-fly operator kv64_kernel, which never materialises H but
+// re-evaluates n^2 FP64 exponentials per product (3x slower at C1, measured
+// 23.7 vs 7.3 ms per step, with the same iteration counts).
 bool dense_dgemm() {
   static const bool on = [] {
-    const char* e = std::getenv("GPK_DENSE_DGEMM");
-    return e && std::atoi(e) != 0;
+    const char* e = std::getenv("GPK_DENSE_KV64");
+    return !(e && std::atoi(e) != 0);
   }();
   return on;
 }
@@ -273,7 +277,7 @@ struct gpk_batch {
   DBuf<double> spart_t;              // fused AP slabs: block-score partial per 128-row tile
   // lazy-momentum SGD (sgd_lazy.cu): FP32 records, last-update iterations,
   // S / rho^Delta tables, slab partials, apply-block partials, flags
-  DBuf<float> sgd_rec, sgd_s32, sgd_xg;
+  DBuf<float> sgd_rec, sgd_s32, sgd_xg, sgd_xsoa;
   DBuf<int> sgd_tau, sgd_flags;
   DBuf<double> sgd_tab, sgd_part, sgd_gpart;
   DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
@@ -1865,6 +1869,11 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
     const char* e = std::getenv("GPK_SGD_GRAM");
     return e && std::atoi(e) != 0;
   }();
+  if (op->dp == 4) {  // d <= 4: the slab evaluates two columns per FP32x2 instruction from SoA coordinates
+    float* xq = b->sgd_xsoa.ensure(static_cast<size_t>(n + 128) * op->dp);
+    sgd_soa_image_launch(op->xs32.p, n + 128, op->dp, xq, s);
+    sa.xsoa = xq;
+  }
   if (sgd_gram && op->d < op->dp) {
     float* xg = b->sgd_xg.ensure(static_cast<size_t>(n + 128) * op->dp);
     sgd_gram_image_launch(op->xs32.p, n + 128, n, op->d, op->dp, xg, s);
@@ -3167,7 +3176,7 @@ void optimiser_init(gpk_optimiser* o, gpk_ctx* ctx, const double* inputs, const 
     if (opp->nloc < 1) throw InvalidArgument("gpk_optimise: fewer rows than ranks * 32");
   }
   if (!opp->sharded && n <= dense_cache_cap()) {  // outer_loop.cpp:72: options.dense_cache = n <= cap
-    opp->dense = true;  // FP64 products (kv64_kernel; GPK_DENSE_DGEMM=1: cached matrix + DGEMM)
+    opp->dense = true;  // FP64 products (cached matrix + DGEMM; GPK_DENSE_KV64=1: kv64_kernel on the fly)
     if (dense_dgemm())
       dense_block64_launch(opp->xs64.p, n, d, opp->s2, opp->sigma2, 0, n, 0, n,
                            opp->kdense.ensure(static_cast<size_t>(n) * n), n, 0, ctx->stream);

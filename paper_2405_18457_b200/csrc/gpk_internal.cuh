@@ -236,6 +236,7 @@ struct SgdSlabArgs {
   int budget;
   int ntab;             // leading entries of s32 staged in shared memory
   const float* xg;      // Gram column image (-2 x, |x|^2, 0...) [n + 128][dp] or null (direct differences)
+  const float* xsoa;    // d <= 4: column coordinates per 32-row chunk in SoA order [chunk][dp][32]
   const CgCtl* ctl;     // iteration t = ctl->iters; no-op once ctl->stop
   float log2_s2;
   double* part;         // [splits][R][m] FP64 partials
@@ -275,6 +276,7 @@ int sgd_record_width(int m, int* moff);
 void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s);
 void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s);
 void sgd_gram_image_launch(const float* xs, int rows, int n, int d, int dp, float* xg, cudaStream_t s);
+void sgd_soa_image_launch(const float* xs, int rows, int dp, float* out, cudaStream_t s);
 void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s);
 void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
                              cudaStream_t s);

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
         float* dst = smS + s * st_floats;
         mbar_expect_tx(&st_full[s], rec_bytes + x_bytes + TBK * 4u);
         bulk_g2s(dst, a.rec + (c / TBK) * rw, rec_bytes, &st_full[s]);
-        bulk_g2s(dst + rw, (GRAM ? a.xg : a.xs) + (a.c0 + c) * DP, x_bytes, &st_full[s]);
+        bulk_g2s(dst + rw, (GRAM ? a.xg : DX > 0 ? a.xsoa : a.xs) + (a.c0 + c) * DP, x_bytes, &st_full[s]);
         bulk_g2s(dst + rw + TBK * DP, a.tau + c, TBK * 4u, &st_full[s]);
       }
     }
@@ -336,8 +336,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
     int drained = 0, next_drain = F + DEFER;
     // ring positions kept incrementally (no divisions in the chunk loop)
     int s = 0, sph = 0, ab = 0, aph = 0;  // a_empty waited from the second pass over the ring on
-    float4 xr = make_float4(0.f, 0.f, 0.f, 0.f);  // DX > 0: the row's coordinates
-    if constexpr (DX > 0) xr = __ldg(reinterpret_cast<const float4*>(xrow));
+    // DX > 0: the row's coordinates duplicated into FP32x2 pairs, and the
+    // profile constants as pairs
+    uint64_t xik2[4] = {0ull, 0ull, 0ull, 0ull}, k_s3 = 0ull, k_one = 0ull, k_c = 0ull, k_l2s2 = 0ull;
+    if constexpr (DX > 0) {
+      const float4 xr = __ldg(reinterpret_cast<const float4*>(xrow));
+      const float xe[4] = {xr.x, xr.y, xr.z, xr.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) asm("mov.b64 %0, {%1, %1};" : "=l"(xik2[k]) : "f"(xe[k]));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_s3) : "f"(kSqrt3f));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_one) : "f"(1.f));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_c) : "f"(kNegSqrt3Log2e));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_l2s2) : "f"(a.log2_s2));
+    }
     // Chunk k's entries are computed before its A buffer is waited for, and
     // its TMEM stores complete while chunk k + 1 is computed: the wait::st and
     // the a_full arrive of chunk k run at the top of chunk k + 1's store.
@@ -356,17 +367,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
       uint32_t hi[CPT], lo[CPT];
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
-        if constexpr (DX > 0) {  // exactly DX <= 4 dimensions, scalar FP32
-          const float4 c = *reinterpret_cast<const float4*>(xc + t * DP);
-          const float d0 = c.x - xr.x;
-          float r2 = d0 * d0;
-          if (DX > 1) { const float d1 = c.y - xr.y; r2 = fmaf(d1, d1, r2); }
-          if (DX > 2) { const float d2 = c.z - xr.z; r2 = fmaf(d2, d2, r2); }
-          if (DX > 3) { const float d3 = c.w - xr.w; r2 = fmaf(d3, d3, r2); }
-          const float r = sqrt_approx(r2);
-          const float kv = fmaf(r, kSqrt3f, 1.f) * ex2_approx(fmaf(r, kNegSqrt3Log2e, a.log2_s2));
-          hi[t] = __float_as_uint(kv) & 0xFFFFE000u;
-          lo[t] = __float_as_uint(kv - __uint_as_float(hi[t]));
+        if constexpr (DX > 0) {  // exactly DX <= 4 dimensions, two columns per FP32x2 instruction
+          if (t & 1) continue;   // (t, t + 1) done together
+          // column coordinates of this chunk in SoA order: xq[k * 32 + c]
+          const float* xq = smS + s * st_floats + rw + quarter * CPT + t;
+          uint64_t r2;
+#pragma unroll
+          for (int k = 0; k < DX; ++k) {
+            const uint64_t cc = *reinterpret_cast<const uint64_t*>(xq + k * 32);
+            uint64_t dd;
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dd) : "l"(cc), "l"(xik2[k]));
+            if (k == 0)
+              asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r2) : "l"(dd));
+            else
+              asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(r2) : "l"(dd));
+          }
+          float ra, rb;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r2));
+          ra = sqrt_approx(ra);
+          rb = sqrt_approx(rb);
+          uint64_t rr, tt, uu, ee, kk;
+          asm("mov.b64 %0, {%1, %2};" : "=l"(rr) : "f"(ra), "f"(rb));
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(tt) : "l"(rr), "l"(k_s3), "l"(k_one));
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(uu) : "l"(rr), "l"(k_c), "l"(k_l2s2));
+          float ua, ub;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(ua), "=f"(ub) : "l"(uu));
+          ua = ex2_approx(ua);
+          ub = ex2_approx(ub);
+          asm("mov.b64 %0, {%1, %2};" : "=l"(ee) : "f"(ua), "f"(ub));
+          asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(kk) : "l"(tt), "l"(ee));
+          float ka, kb;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(ka), "=f"(kb) : "l"(kk));
+          hi[t] = __float_as_uint(ka) & 0xFFFFE000u;
+          hi[t + 1] = __float_as_uint(kb) & 0xFFFFE000u;
+          uint64_t hh, ll;
+          asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "r"(hi[t]), "r"(hi[t + 1]));
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ll) : "l"(kk), "l"(hh));
+          asm("mov.b64 {%0, %1}, %2;" : "=r"(lo[t]), "=r"(lo[t + 1]) : "l"(ll));
           continue;
         }
         // packed FP32x2 (FADD2/FFMA2): two dimensions per instruction
@@ -652,6 +689,17 @@ __global__ void sgd_gram_image_kernel(const float* xs, int rows, int n, int d, i
   }
 }
 
+// Column coordinates per 32-row chunk in SoA order (chunk q: [dp][32]) for
+// the exact-dimension FP32x2 evaluation (two columns per instruction)
+__global__ void sgd_soa_image_kernel(const float* xs, int rows, int dp, float* out) {
+  const long long total = static_cast<long long>(rows) * dp;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / dp), k = static_cast<int>(e % dp);
+    out[(static_cast<size_t>(i / 32) * dp + k) * 32 + (i % 32)] = xs[e];
+  }
+}
+
 // initial records from the warm-start solution: V32 = V0, M32 = 0, tau = -1
 __global__ void sgd_records_init_kernel(const double* V, int nloc, int nchunks, int m, int rw, int moff, float* rec,
                                         int* tau) {
@@ -706,6 +754,13 @@ void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s) {
 void sgd_gram_image_launch(const float* xs, int rows, int n, int d, int dp, float* xg, cudaStream_t s) {
   sgd_gram_image_kernel<<<std::max(1, std::min(148 * 4, (rows + 255) / 256)), 256, 0, s>>>(xs, rows, n, d, dp, xg);
   check_launch("sgd_gram_image");
+}
+
+void sgd_soa_image_launch(const float* xs, int rows, int dp, float* out, cudaStream_t s) {
+  const long long total = static_cast<long long>(rows) * dp;
+  sgd_soa_image_kernel<<<static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 8)), 256, 0, s>>>(xs, rows, dp,
+                                                                                                          out);
+  check_launch("sgd_soa_image");
 }
 
 void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s) {

@@ -96,9 +96,8 @@ def test_gpu_c1_trajectory_matches_fixture(gpk_ctx):
     # north star: hyperparameter trajectory within 1e-3 relative
     assert np.max(np.abs(r["constrained"] - ref) / ref) <= 1e-3
     # n = 4096 is within the reference's dense_cache_cap, so the optimiser
-    # applies H in FP64 (kv64_kernel: entries evaluated on the fly, never
-    # materialised), as exact as the reference's cached products
-    # (outer_loop.cpp:72). At this initialisation (noise 0.1) preconditioned
+    # applies H in FP64 as the reference does there (outer_loop.cpp:72: the
+    # cached FP64 kernel matrix; GPK_DENSE_KV64=1 evaluates it on the fly). At this initialisation (noise 0.1) preconditioned
     # CG to tau = 0.01 is sensitive to the summation order itself: the FP64
     # oracle moves its step-1 iteration count by one and its mean residual
     # norm by 40% under a 1e-12 perturbation of H.V
