@@ -64,14 +64,24 @@ struct Hyperparameters {
   int count() const { return static_cast<int>(raw.size()); }
 };
 
+// KernelOperatorOptions (kernel.hpp:27-30); block_rows has no meaning here
+// (no tile of H is materialised), dense_cache selects FP64 full products.
+struct KernelOperatorOptions {
+  int block_rows = 1024;
+  bool dense_cache = false;
+};
+
 // KernelOperator (kernel.hpp:37-97). `inputs` is the Dataset's n x d matrix.
 class KernelOperator {
  public:
-  KernelOperator(Context& ctx, const Matrix& inputs, const Hyperparameters& hp) : hp_(hp) {
+  KernelOperator(Context& ctx, const Matrix& inputs, const Hyperparameters& hp,
+                 KernelOperatorOptions options = {})
+      : hp_(hp) {
     if (static_cast<int>(hp.raw.size()) != inputs.cols + 2)
       throw std::invalid_argument("KernelOperator: dataset dimension does not match hyperparameters");
     check(gpk_operator_create(ctx.get(), inputs.data(), inputs.rows, inputs.cols, hp.raw.data(), &op_));
     n_ = inputs.rows;
+    if (options.dense_cache) check(gpk_operator_set_dense_cache(op_, 1));
   }
   ~KernelOperator() { gpk_operator_destroy(op_); }
   KernelOperator(const KernelOperator&) = delete;

@@ -133,6 +133,11 @@ gpk_status gpk_shard_rows(int n, int nranks, int rank, int* row0, int* row1);
 gpk_status gpk_operator_create(gpk_ctx* ctx, const double* inputs, int n, int d,
                                const double* raw, gpk_operator** out);
 gpk_status gpk_operator_set_hyperparameters(gpk_operator* op, const double* raw);
+/* KernelOperatorOptions::dense_cache (kernel.hpp:27-30): FP64 products for
+ * full H V (the reference holds H in FP64). Here H is never materialised:
+ * entries are evaluated in FP64 on the fly (GPK_DENSE_KV64=0: cached FP64
+ * matrix + DGEMM, as the reference). Single-rank operators only. */
+gpk_status gpk_operator_set_dense_cache(gpk_operator* op, int enable);
 gpk_status gpk_operator_destroy(gpk_operator* op);
 gpk_status gpk_operator_size(const gpk_operator* op, int* n, int* d);
 

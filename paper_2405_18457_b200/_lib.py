@@ -67,6 +67,7 @@ def _sig(lib):
         "gpk_ctx_stats": (C.c_int, [H, dp]),
         "gpk_operator_create": (C.c_int, [H, dp, C.c_int, C.c_int, dp, C.POINTER(H)]),
         "gpk_operator_set_hyperparameters": (C.c_int, [H, dp]),
+        "gpk_operator_set_dense_cache": (C.c_int, [H, C.c_int]),
         "gpk_operator_destroy": (C.c_int, [H]),
         "gpk_operator_size": (C.c_int, [H, ip, ip]),
         "gpk_apply": (C.c_int, [H, dp, C.c_int, dp]),

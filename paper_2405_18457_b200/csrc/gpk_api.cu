@@ -70,16 +70,15 @@ int dense_cache_cap() {
   return cap;
 }
 
-// n <= dense_cache_cap: FP64 products as the reference computes them there
-// (outer_loop.cpp:72 caches H in FP64) -- by DGEMM on the cached FP64 kernel
-// matrix (default: 0.16 ms per C1 CG iteration), or with GPK_DENSE_KV64=1 by
-// the FP64 on-the-fly operator kv64_kernel, which never materialises H but
-// re-evaluates n^2 FP64 exponentials per product (3x slower at C1, measured
-// 23.7 vs 7.3 ms per step, with the same iteration counts).
+// n <= dense_cache_cap: FP64 products, as the reference computes them there
+// (outer_loop.cpp:72 caches H in FP64). Default: the FP64 on-the-fly
+// operator kv64v2_kernel, which never materialises H (entries evaluated in
+// FP64 and contracted in registers); GPK_DENSE_KV64=0 keeps the reference's
+// cached FP64 kernel matrix and applies it by cuBLAS DGEMM instead.
 bool dense_dgemm() {
   static const bool on = [] {
     const char* e = std::getenv("GPK_DENSE_KV64");
-    return !(e && std::atoi(e) != 0);
+    return e && std::atoi(e) == 0;
   }();
   return on;
 }
@@ -656,7 +655,7 @@ void run_kv(gpk_operator* op, const KvCall& c) {
   if (dense && !dense_dgemm()) {
     // FP64 operator with on-the-fly entries (kv64_kernel): the reference's
     // exact FP64 products for n <= dense_cache_cap without materialising H
-    const int sp = kv64_splits(op->n, op->n, op->ctx->sms);
+    const int sp = kv64_splits_for(op->n, op->n, c.m, op->d, op->ctx->sms);
     double* p64 = op->part.ensure(static_cast<size_t>(sp) * op->n * c.m);
     kv64_launch(op->xs64.p, op->n, op->d, op->s2, 0, op->n, c.vdiag, c.m, sp, p64, c.skip, s);
     if (a.stats) stats_add_launch(a.stats, static_cast<double>(op->n) * op->n, c.m, op->d, c.skip, s);
@@ -1484,6 +1483,7 @@ void solve_ap(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* rep) 
 
   g_phase.mark("ap_refresh");
   GPK_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // block inverses ready before the first update
+  ap_info_gate_launch(ctx->info.p, nblocks, ctl, s);  // a failed block inverse: no update runs
   g_phase.mark("ap_inverse_wait");
   if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream");
   auto iteration = [&]() {  // solvers.cpp:120-140
@@ -1743,6 +1743,10 @@ void solve_sgd_tc(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report* r
     // stop before it is set for the next one: test the pre-check flag)
     sgd_update_pack_launch(M, b->solutions.p, b->residuals.p, vpk, npad, pos, grad, c->momentum, step, nloc, m,
                            nonfinite, &ctl->pad, s);
+    // one rank: abort in the iteration that formed the non-finite iterate;
+    // sharded: a rank's own non-finite rows reach every rank through its next
+    // slice, so all ranks stop at the same iteration (one later)
+    if (!op->sharded) sgd_diverge_now_launch(nonfinite, ctl, s);
     sgd_unscatter_launch(idx, bs, row0, nloc, pos, &ctl->pad, s);
     ++t;
   };
@@ -2649,6 +2653,19 @@ gpk_status gpk_operator_set_hyperparameters(gpk_operator* op, const double* raw)
 
 gpk_status gpk_operator_destroy(gpk_operator* op) {
   return guarded([&] { delete op; });
+}
+
+gpk_status gpk_operator_set_dense_cache(gpk_operator* op, int enable) {
+  return guarded([&] {
+    LaunchScope ls(op->ctx);
+    require(!op->sharded, "KernelOperator: dense_cache on a row-sharded operator");
+    op->dense = enable != 0;
+    if (op->dense && dense_dgemm()) {
+      dense_block64_launch(op->xs64.p, op->n, op->d, op->s2, op->sigma2, 0, op->n, 0, op->n,
+                           op->kdense.ensure(static_cast<size_t>(op->n) * op->n), op->n, 0, op->ctx->stream);
+      GPK_CUDA(cudaStreamSynchronize(op->ctx->stream));
+    }
+  });
 }
 
 gpk_status gpk_operator_size(const gpk_operator* op, int* n, int* d) {

@@ -426,10 +426,13 @@ void sgd_update_pack_launch(double* M, double* V, double* R, float* vpk, int npa
                             const double* grad, double rho, double step, int nloc, int m, int* nonfinite,
                             const int* skip, cudaStream_t s);
 void sgd_unscatter_launch(const int* idx, int b, int row0, int nloc, int* pos, const int* skip, cudaStream_t s);
+void ap_info_gate_launch(const int* info, int nblocks, CgCtl* ctl, cudaStream_t s);
+void sgd_diverge_now_launch(const int* nonfinite, CgCtl* ctl, cudaStream_t s);
 
 // RFF (K5) + noise (K9)
 // FP64 on-the-fly operator (n <= dense_cache_cap): split partials for kv_reduce
 int kv64_splits(int R, int n, int sms);
+int kv64_splits_for(int R, int n, int m, int d, int sms);
 void kv64_launch(const double* xs64, int n, int d, double sv, int r0, int R, const double* v, int m, int splits,
                  double* part, const int* skip, cudaStream_t s);
 // derivative_apply for k <= d (kernel.cpp:200-236), FP64: out [n][m] row-major;

@@ -1548,6 +1548,40 @@ void sgd_update_pack_launch(double* M, double* V, double* R, float* vpk, int npa
   check_launch("sgd_update_pack");
 }
 
+// AP: a block inverse whose factorisation failed stops the solve before its
+// first update (the solutions are never touched), solvers.cpp:104-113 throws
+// from factor_for; the host raises after the solve from the info copy.
+__global__ void ap_info_gate_kernel(const int* info, int nblocks, CgCtl* ctl) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nblocks; k += blockDim.x)
+    if (info[k] != 0) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0 && bad) {
+    ctl->aborted = 1;
+    ctl->stop = 1;
+  }
+}
+void ap_info_gate_launch(const int* info, int nblocks, CgCtl* ctl, cudaStream_t s) {
+  ap_info_gate_kernel<<<1, 256, 0, s>>>(info, nblocks, ctl);
+  check_launch("ap_info_gate");
+}
+
+// Single-rank divergence test right after the update (solvers.cpp:172-176:
+// the reference tests the iterate it just formed and reports t + 1 updates).
+// pad = stop before this iteration's check, i.e. the update ran.
+__global__ void sgd_diverge_now_kernel(const int* nonfinite, CgCtl* ctl) {
+  if (ctl->pad == 0 && *nonfinite && !ctl->aborted) {
+    ctl->aborted = 1;
+    ctl->stop = 1;
+  }
+}
+void sgd_diverge_now_launch(const int* nonfinite, CgCtl* ctl, cudaStream_t s) {
+  sgd_diverge_now_kernel<<<1, 1, 0, s>>>(nonfinite, ctl);
+  check_launch("sgd_diverge_now");
+}
+
 __global__ void sgd_unscatter_kernel(const int* idx, int b, int row0, int nloc, int* pos, const int* skip) {
   SKIP_IF(skip);
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < b; q += gridDim.x * blockDim.x) {
@@ -1772,14 +1806,151 @@ __global__ void __launch_bounds__(256) kv64_kernel(const double* __restrict__ xs
       if (lane + 32 * u < m) part[(static_cast<size_t>(blockIdx.y) * R + r) * m + lane + 32 * u] = acc[a4][u];
   }
 }
+// kv64 v2 (m <= 32): CTA = 128 rows x one column split, 256 threads; thread
+// (row, half) keeps its row's coordinates and its FP64 accumulators in
+// registers and, per 32-column chunk, evaluates the 16 entries of its half
+// and contracts each at once into its m accumulators (x_c and V rows are
+// shared-memory broadcasts; no entry ever leaves registers). The two halves
+// are combined in a fixed order at the end. DP-pipe bound: ~45 FP64 ops per
+// entry for the Matern profile + m FMAs.
+template <int DM, int MJ>
+__global__ void __launch_bounds__(256, 2) kv64v2_kernel(const double* __restrict__ xs, int n, int d, double sv,
+                                                         int r0, int R, const double* __restrict__ v, int m,
+                                                         int cols_per_split, double* __restrict__ part,
+                                                         const int* skip) {
+  if (skip && *skip) return;
+  constexpr int HJ = MJ / 2;  // the halves are combined in two passes of HJ columns
+  constexpr int LOOP = 2 * 32 * (DM + MJ), COMB = 128 * (HJ + 1);
+  __shared__ __align__(16) double sm[LOOP > COMB ? LOOP : COMB];
+  auto xc = reinterpret_cast<double(*)[32][DM]>(sm);
+  auto vt = reinterpret_cast<double(*)[32][MJ]>(sm + 2 * 32 * DM);
+  auto comb = reinterpret_cast<double(*)[HJ + 1]>(sm);
+  const int tid = threadIdx.x, row = tid & 127, h = tid >> 7;
+  const int er = blockIdx.x * 128 + row;
+  const int cb = blockIdx.y * cols_per_split, ce = min(n, cb + cols_per_split);
+  double xr[DM];
+#pragma unroll
+  for (int q = 0; q < DM; ++q) xr[q] = (er < R && q < d) ? xs[static_cast<size_t>(r0 + er) * d + q] : 0.0;
+  double acc[MJ];
+#pragma unroll
+  for (int j = 0; j < MJ; ++j) acc[j] = 0.0;
+  constexpr int XE = 32 * DM, VE = 32 * MJ;
+  constexpr int PER = (XE + VE + 255) / 256;
+  auto fetch = [&](int c0, double* pre) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u;
+      double val = 0.0;
+      if (e < XE) {
+        const int c = e / DM, q = e % DM;
+        if (c0 + c < ce && q < d) val = xs[static_cast<size_t>(c0 + c) * d + q];
+      } else if (e < XE + VE) {
+        const int c = (e - XE) / MJ, j = (e - XE) % MJ;
+        if (c0 + c < ce && j < m) val = v[static_cast<size_t>(c0 + c) * m + j];
+      }
+      pre[u] = val;
+    }
+  };
+  auto stash = [&](int buf, const double* pre) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u;
+      if (e < XE)
+        (&xc[buf][0][0])[e] = pre[u];
+      else if (e < XE + VE)
+        (&vt[buf][0][0])[e - XE] = pre[u];
+    }
+  };
+  double pre[PER];
+  int buf = 0;
+  if (cb < ce) {
+    fetch(cb, pre);
+    stash(0, pre);
+  }
+  __syncthreads();
+  for (int c0 = cb; c0 < ce; c0 += 32) {
+    const bool more = c0 + 32 < ce;
+    if (more) fetch(c0 + 32, pre);  // in flight during this chunk
+#pragma unroll 2
+    for (int cc = 0; cc < 16; ++cc) {
+      const int c = h * 16 + cc;
+      double r2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < DM; q += 2) {
+        const double2 x2 = *reinterpret_cast<const double2*>(&xc[buf][c][q]);
+        const double t0 = x2.x - xr[q], t1 = x2.y - xr[q + 1];
+        r2 = fma(t0, t0, r2);
+        r2 = fma(t1, t1, r2);
+      }
+      const double rr = sqrt(r2);
+      // zero V rows beyond the split make the padded columns contribute 0
+      const double kv = sv * (1.0 + kSqrt3 * rr) * exp(-kSqrt3 * rr);
+#pragma unroll
+      for (int j = 0; j < MJ; j += 2) {
+        const double2 w = *reinterpret_cast<const double2*>(&vt[buf][c][j]);
+        acc[j] = fma(kv, w.x, acc[j]);
+        acc[j + 1] = fma(kv, w.y, acc[j + 1]);
+      }
+    }
+    if (more) stash(buf ^ 1, pre);
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* out = part + (static_cast<size_t>(blockIdx.y) * R + er) * m;
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    if (h == 1) {
+#pragma unroll
+      for (int j = 0; j < HJ; ++j) comb[row][j] = acc[p * HJ + j];
+    }
+    __syncthreads();
+    if (h == 0 && er < R) {
+#pragma unroll
+      for (int j = 0; j < HJ; ++j)
+        if (p * HJ + j < m) out[p * HJ + j] = acc[p * HJ + j] + comb[row][j];
+    }
+    __syncthreads();
+  }
+}
+
 int kv64_splits(int R, int n, int sms) {
   const int rb = (R + 31) / 32;
   const int want = std::max(1, (4 * sms + rb - 1) / rb);  // ~4 CTAs per SM
   return std::min(want, std::max(1, (n + 31) / 32));
 }
+int kv64v2_splits(int R, int n, int sms) {
+  const int rb = (R + 127) / 128;
+  const int want = std::max(1, (2 * sms + rb - 1) / rb);  // two resident CTAs per SM
+  return std::min(want, std::max(1, (n + 31) / 32));
+}
+int kv64_splits_for(int R, int n, int m, int d, int sms) {
+  return (m <= 32 && d <= 16) ? kv64v2_splits(R, n, sms) : kv64_splits(R, n, sms);
+}
+
+template <int DM, int MJ>
+void kv64v2_launch_t(const double* xs64, int n, int d, double sv, int r0, int R, const double* v, int m,
+                     int splits, double* part, const int* skip, cudaStream_t s) {
+  int cps = (n + splits - 1) / splits;
+  cps = (cps + 31) / 32 * 32;
+  kv64v2_kernel<DM, MJ><<<dim3((R + 127) / 128, splits), 256, 0, s>>>(xs64, n, d, sv, r0, R, v, m, cps, part, skip);
+  check_launch("kv64v2_kernel");
+}
+template <int DM>
+void kv64v2_launch_d(const double* xs64, int n, int d, double sv, int r0, int R, const double* v, int m,
+                     int splits, double* part, const int* skip, cudaStream_t s) {
+  if (m <= 8) return kv64v2_launch_t<DM, 8>(xs64, n, d, sv, r0, R, v, m, splits, part, skip, s);
+  if (m <= 18) return kv64v2_launch_t<DM, 18>(xs64, n, d, sv, r0, R, v, m, splits, part, skip, s);
+  return kv64v2_launch_t<DM, 32>(xs64, n, d, sv, r0, R, v, m, splits, part, skip, s);
+}
+
 void kv64_launch(const double* xs64, int n, int d, double sv, int r0, int R, const double* v, int m, int splits,
                  double* part, const int* skip, cudaStream_t s) {
   if (d > 32 || m > 80) throw std::invalid_argument("gpk: the FP64 operator supports d <= 32 and m <= 80");
+  if (m <= 32 && d <= 16) {  // splits from kv64_splits_for
+    if (d <= 4) return kv64v2_launch_d<4>(xs64, n, d, sv, r0, R, v, m, splits, part, skip, s);
+    if (d <= 8) return kv64v2_launch_d<8>(xs64, n, d, sv, r0, R, v, m, splits, part, skip, s);
+    return kv64v2_launch_d<16>(xs64, n, d, sv, r0, R, v, m, splits, part, skip, s);
+  }
   int cps = (n + splits - 1) / splits;
   cps = (cps + 31) / 32 * 32;
   kv64_kernel<<<dim3((R + 31) / 32, splits), 256, 0, s>>>(xs64, n, d, sv, r0, R, v, m, cps, part, skip);

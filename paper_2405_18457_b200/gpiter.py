@@ -177,7 +177,7 @@ def default_context():
 
 # ---- KernelOperator (kernel.hpp:37-97) ------------------------------------
 class KernelOperator:
-    def __init__(self, inputs, hp: Hyperparameters, ctx: Context | None = None):
+    def __init__(self, inputs, hp: Hyperparameters, ctx: Context | None = None, dense_cache: bool = False):
         self.ctx = ctx or default_context()
         self._lib = self.ctx._lib
         X = _f64(inputs)
@@ -190,6 +190,8 @@ class KernelOperator:
         h = C.c_void_p()
         check(self._lib.gpk_operator_create(self.ctx.handle, _p(X), n, d, _p(hp.raw), C.byref(h)))
         self.handle = h
+        if dense_cache:  # KernelOperatorOptions::dense_cache: FP64 full products
+            check(self._lib.gpk_operator_set_dense_cache(h, 1))
 
     def size(self):
         return self.n

@@ -58,6 +58,23 @@ def test_apply_matches_oracle(G, kctx, oracle, n, d, m):
     assert colrel(got, ref) <= OP_TOL
 
 
+@pytest.mark.parametrize("n,d,m", [(4096, 8, 17), (1000, 3, 5), (777, 13, 33), (600, 20, 65), (300, 16, 9),
+                                   (129, 1, 1)])
+def test_apply_dense_cache_fp64_matches_oracle(G, gpk_ctx, oracle, n, d, m):
+    """KernelOperatorOptions::dense_cache (kernel.hpp:27-30): full products in
+    FP64 with entries evaluated on the fly (kv64 kernels; H never held), to
+    FP64 rounding of the oracle's ascending-column sums; the C1 optimiser
+    (n <= dense_cache_cap) runs this operator."""
+    X, _ = gp_problem(n, d, 2000 + n)
+    raw = default_test_raw(d, oracle)
+    V = np.asfortranarray(np.random.default_rng(n + 1).standard_normal((n, m)))
+    op = G.KernelOperator(X, G.Hyperparameters.from_raw(raw), gpk_ctx, dense_cache=True)
+    got = op.apply(V)
+    ref = oracle.apply(X, raw, V, threads=8)
+    assert colrel(got, ref) <= 1e-12
+    assert np.array_equal(op.apply(V), got)  # deterministic
+
+
 def test_apply_identity_is_dense(G, kctx, oracle):
     n, d = 64, 3
     X, _ = gp_problem(n, d, 101)
@@ -255,6 +272,30 @@ def test_sgd_zero_lr_and_divergence(G, gpk_ctx, oracle):  # test_solvers.cpp:268
     rep2 = G.solve_sgd(b2, G.SolverConfig(kind=2, tolerance=1e-10, max_epochs=50, batch_size=16,
                                           learning_rate=1e6))
     assert rep2.aborted and "divergence" in rep2.abort_reason
+    # the oracle diverges too; the GPU's FP32 operator images overflow at
+    # ~3.4e38 rather than FP64's ~1.8e308, so it can only stop earlier
+    o2 = oracle.solve(X, raw, T, oracle.solver_config(kind=2, tolerance=1e-10, max_epochs=50, batch_size=16,
+                                                      learning_rate=1e6))
+    assert o2["aborted"] and rep2.iterations <= o2["iterations"]
+
+
+@pytest.mark.parametrize("d", [2, 20])  # d = 2: lazy-momentum slab kernel; d = 20: full-state SGD path
+def test_sgd_divergence_iteration_count(G, gpk_ctx, oracle, d):  # solvers.cpp:168-177
+    """A non-finite iterate aborts in the iteration that formed it (t + 1
+    updates reported, as solve_sgd does), on every SGD code path."""
+    n = 256
+    X, y = gp_problem(n, d, 333)
+    raw = oracle.raw_from_constrained([1.0] * d + [1.0, 0.4])
+    T = _targets(oracle, n, 2, 334, y)
+    T[5, 1] = np.inf
+    op = make_op(G, gpk_ctx, X, raw)
+    cfg = dict(kind=2, tolerance=1e-10, max_epochs=5, batch_size=16, learning_rate=1.0)
+    ref = oracle.solve(X, raw, T, oracle.solver_config(**cfg))
+    b = G.LinearSystemBatch(op, T)
+    rep = G.solve_sgd(b, G.SolverConfig(**cfg))
+    assert ref["aborted"] and rep.aborted
+    assert rep.iterations == ref["iterations"], (rep.iterations, ref["iterations"])
+    assert rep.epochs_consumed == ref["epochs_consumed"]
 
 
 def test_sgd_minibatches_bit_exact(G, gpk_ctx, oracle):
@@ -387,6 +428,27 @@ def test_spd_inverse_rejects_indefinite(G, gpk_ctx):
     for mode in (1, 0):
         with pytest.raises(ArithmeticError, match="not positive definite"):
             G.gpiter.spd_inverse(gpk_ctx, A, mode)
+
+
+def test_ap_non_pd_block_raises_before_any_update(G, gpk_ctx, oracle):  # solvers.cpp:104-113
+    """Duplicated points and noise 1e-12 make the diagonal blocks numerically
+    indefinite: the oracle's factor_for throws; the device solve stops before
+    its first update (solutions untouched) and raises the same error."""
+    n = 256
+    X = np.zeros((n, 2))
+    X[:, 0] = np.repeat(np.arange(4), 64) * 5.0
+    raw = oracle.raw_from_constrained([1.0, 1.0, 1.0, 1e-12])
+    T = np.asfortranarray(np.random.default_rng(0).standard_normal((n, 3)))
+    cfg = dict(kind=1, block_size=64, tolerance=1e-6, max_epochs=5)
+    with pytest.raises(Exception, match="not positive definite"):
+        oracle.solve(X, raw, T, oracle.solver_config(**cfg))
+    op = make_op(G, gpk_ctx, X, raw)
+    W = np.asfortranarray(np.random.default_rng(1).standard_normal((n, 3)))
+    b = G.LinearSystemBatch(op, T)
+    b.warm_start(W)
+    with pytest.raises(ArithmeticError, match="not positive definite"):
+        G.solve(b, G.SolverConfig(**cfg))
+    assert np.array_equal(b.solutions, W)
 
 
 def test_optimise_exact_dense_prior_matches_oracle(G, gpk_ctx, oracle):

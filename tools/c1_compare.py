@@ -1,3 +1,5 @@
+"""C1 (BASELINE configs[0]) 10-step trajectory on the GPU against tests/golden/c1.npz: iteration counts,
+residual norms and per-step gradient errors (GPK_DENSE_KV64=0 selects the cached-matrix DGEMM path)."""
 import numpy as np, sys, os
 sys.path.insert(0, os.getcwd())
 import paper_2405_18457_b200 as G
@@ -15,3 +17,5 @@ for k in ["mean_residual_norm", "probe_residual_norm"]:
     print(k, np.max(np.abs(r[k] - g["traj_" + k]) / g["traj_" + k]))
 gg = g["traj_gradient"]; print("grad rel", np.max(np.abs(r["gradient"] - gg) / np.abs(gg).max(axis=1, keepdims=True)))
 print("step seconds", list(np.round(r["step_seconds"], 5)))
+print("grad rel-of-max per step", [f"{v:.2e}" for v in (np.abs(r["gradient"] - gg) / np.abs(gg).max(axis=1, keepdims=True)).max(axis=1)])
+print("mean norm rel per step", [f"{v:.2e}" for v in np.abs(r["mean_residual_norm"] - g["traj_mean_residual_norm"]) / g["traj_mean_residual_norm"]])
