@@ -1800,8 +1800,9 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   int moff = 0;
   const int rw = sgd_record_width(m, &moff);
   const int rows_pad = (nloc + 31) / 32 * 32;
-  float* rec = b->sgd_rec.ensure(static_cast<size_t>(rows_pad / 32) * rw);  // one record per 32-row chunk
-  int* tau = b->sgd_tau.ensure(rows_pad);
+  // one record per 32-row chunk, plus a zero record past the end (64-column slab chunks)
+  float* rec = b->sgd_rec.ensure(static_cast<size_t>(rows_pad / 32 + 1) * rw);
+  int* tau = b->sgd_tau.ensure(rows_pad + 32);
   sgd_records_init_launch(b->solutions.p, nloc, rows_pad, m, rw, moff, rec, tau, s);
   // P(Delta) = rho^Delta, S(Delta) = rho + ... + rho^Delta by the recurrence an
   // untouched row follows in the reference (momentum *= rho; solutions += momentum)
@@ -1826,9 +1827,16 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   const double* s64 = b->sgd_tab.p;
   const double* p64 = b->sgd_tab.p + budget + 1;
   const int tiles = (bs + 127) / 128;
+  // d <= 4: the 64-column slab pipeline (GPK_SGD_CH64=0: 32-column chunks)
+  static const bool ch64_env = [] {
+    const char* e = std::getenv("GPK_SGD_CH64");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool ch64 = ch64_env && op->dp == 4;
+  const int cq = ch64 ? 64 : 32;
   int splits = std::max(1, ctx->sms / tiles);
   int cps = (nloc + splits - 1) / splits;
-  cps = (cps + 31) / 32 * 32;
+  cps = (cps + cq - 1) / cq * cq;
   splits = std::max(1, (nloc + cps - 1) / cps);
   double* part = b->sgd_part.ensure(static_cast<size_t>(splits) * bs * m);
   const long long stride = (static_cast<long long>(bs) * m + m + 1 + 31) / 32 * 32;  // doubles per rank slice
@@ -1893,7 +1901,8 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
     const char* e = std::getenv("GPK_SGD_FLUSH");  // FP32 TMEM accumulation span in 32-column chunks
     return e ? std::max(5, std::atoi(e)) : 8;
   }();
-  sa.flush = flush;
+  sa.flush = ch64 ? std::max(3, flush / 2) : flush;  // same FP32 accumulation span in 64-column chunks
+  sa.ch64 = ch64 ? 1 : 0;
   sa.stats = ctx->stats;
   SgdStepArgs ta{};
   ta.ctl = ctl;

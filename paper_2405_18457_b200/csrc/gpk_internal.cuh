@@ -242,6 +242,7 @@ struct SgdSlabArgs {
   double* part;         // [splits][R][m] FP64 partials
   int m, splits, cols_per_split, flush;
   double* stats;
+  int ch64;             // 64-column pipeline (d <= 4 with xsoa; cols_per_split a multiple of 64)
 };
 struct SgdStepArgs {
   CgCtl* ctl;

@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "gpk_internal.cuh"
@@ -469,6 +470,507 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
   }
 }
 
+// Development instrumentation (build with -DSGD_PROF=1, tools/sgd_prof.sh):
+// per-role barrier-wait cycles of the 64-column slab, summed over CTAs and
+// warps (lane 0), read back with gpk_debug_sgd_prof.
+#ifndef SGD_PROF
+#define SGD_PROF 0
+#endif
+#if SGD_PROF
+__device__ unsigned long long g_sgd_prof[16];
+#define PROF_T0 prof_t0 = clock64()
+#define PROF_ADD(i) prof_acc[i] += clock64() - prof_t0
+#else
+#define PROF_T0
+#define PROF_ADD(i)
+#endif
+
+// ---- 64-column pipeline (d <= 4, FP32x2 SoA evaluation) -----------------
+// The same roles as sgd_slab_kernel, with 64-column chunks (two 32-column
+// records per stage): every evaluation thread computes 16 entries per
+// barrier round instead of 8, which halves the per-entry share of the
+// mbarrier waits / arrivals, TMEM-address and ring bookkeeping that made up
+// ~45% of the evaluation warps' instructions at 32 columns
+// (profiles/r02_sass_hot_sgd_slab_C4_v2_soa.txt). TMEM: D double buffer at
+// columns 0 / 96, two A buffers of 128 columns (hi 64 | lo 64) from 192.
+// Stages: staging ring 3 x (2 records + SoA x + tau), B ring 2 x (hi | lo of
+// two 32-column images); the B images' zero j-groups are written once.
+namespace c64 {
+constexpr int CH = 64;
+constexpr int ST = 3;
+constexpr int SB = 2;
+constexpr int NAB = 2;
+constexpr int A_COL0 = 192;
+constexpr int DEFER = 2;
+constexpr int CPT = 16;  // entries per evaluation thread per chunk
+
+template <int NPAD>
+__host__ __device__ constexpr size_t smem_bytes(int rw, int dp, int ntab) {
+  return sizeof(float) * (SB * 4 * static_cast<size_t>(NPAD) * 32 + ST * (2 * static_cast<size_t>(rw) + 2 * 32 * dp + CH)) +
+         64 * sizeof(uint64_t) + SB * CH * sizeof(float) + static_cast<size_t>(ntab) * sizeof(float);
+}
+}  // namespace c64
+
+template <int NPAD, int DX, int NBW>
+__global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(const SgdSlabArgs a) {
+  constexpr int CH = c64::CH, ST = c64::ST, SB = c64::SB, NAB = c64::NAB, A_COL0 = c64::A_COL0,
+                DEFER = c64::DEFER;
+  constexpr int BW = NBW, MMA_WARP = EW + 1 + NBW, NTHREADS = 32 * (MMA_WARP + 1);
+  constexpr int IMG = NPAD * 32;  // floats of one 32-column TF32 image
+  constexpr int DC = NPAD / 4;
+  constexpr int DP = 4;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int rw = a.rw;
+  const int st_floats = 2 * rw + 2 * 32 * DP + CH;  // 2 records | 2 SoA x | tau
+  float* smB = reinterpret_cast<float*>(smem_raw);  // [SB][hi0 | hi1 | lo0 | lo1]
+  float* smS = smB + SB * 4 * IMG;                  // [ST][st_floats]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smS + ST * st_floats);
+  uint64_t* st_full = bars;
+  uint64_t* st_empty = bars + ST;
+  uint64_t* b_full = bars + 2 * ST;
+  uint64_t* b_empty = b_full + SB;
+  uint64_t* a_full = b_empty + SB;       // [NAB][2]: one per 32-column half of the A buffer
+  uint64_t* a_empty = a_full + 2 * NAB;  // [NAB]
+  uint64_t* d_full = a_empty + NAB;
+  uint64_t* d_empty = d_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+  float* sS = reinterpret_cast<float*>(bars + 64);  // [SB][CH]
+  float* stab = sS + SB * CH;
+
+  if (a.ctl->stop) return;
+  const int t_iter = a.ctl->iters;
+  const int* idx = a.idxbuf + static_cast<size_t>(t_iter % a.idx_chunk) * a.R;
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int cb = split * a.cols_per_split;  // multiple of 64
+  const int ce = min(a.C, cb + a.cols_per_split);
+  const int nk = ce > cb ? (ce - cb + CH - 1) / CH : 0;
+  const int F = a.flush;
+  const int ngroups = (nk + F - 1) / F;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int jgroups = a.moff / 256;
+
+  if (a.stats && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    const double entries = static_cast<double>(a.R) * a.C;
+    atomicAdd(a.stats, entries * a.m);
+    atomicAdd(a.stats + 1, entries * (2.0 * a.m + 3.0 * a.d + 6.0));
+    atomicAdd(a.stats + 2, entries * (3.0 * a.d + 6.0));
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], EW + BW);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&b_full[s], BW);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int b = 0; b < NAB; ++b) {
+      mbar_init(&a_full[2 * b], EW);
+      mbar_init(&a_full[2 * b + 1], EW);
+      mbar_init(&a_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&d_full[b], 1);
+      mbar_init(&d_empty[b], EW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int e = tid; e < a.ntab; e += NTHREADS) stab[e] = __ldg(a.s32 + e);
+  // zero j-groups (>= JG) of every B image: written once, never rebuilt
+  for (int sb = 0; sb < SB; ++sb)
+    for (int f = tid; f < 4 * IMG; f += NTHREADS)
+      if (((f % IMG) >> 8) >= jgroups) smB[sb * 4 * IMG + f] = 0.f;
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // one CTA per SM allocating all 512 columns: the allocation starts at
+  // column 0, lane 0. The MMA issue uses that constant so ptxas keeps every
+  // operand in uniform registers (no per-MMA elect/broadcast of the TMEM
+  // addresses: ~18 -> ~6 instructions per MMA).
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0) __trap();
+#if SGD_PROF
+  const long long prof_start = clock64();
+  long long prof_t0 = 0;
+  long long prof_acc[10] = {};
+#endif
+
+  if (warp == PROD_WARP) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint32_t rec_bytes = 2 * rw * 4u, x_bytes = 2 * 32 * DP * 4u;
+      for (int k = 0; k < nk; ++k) {
+        const int s = k % ST;
+        PROF_T0;
+        if (k >= ST) mbar_wait_backoff<256>(&st_empty[s], ((k / ST) - 1) & 1);
+        PROF_ADD(0);
+        const size_t c = static_cast<size_t>(cb) + static_cast<size_t>(k) * CH;
+        float* dst = smS + s * st_floats;
+        mbar_expect_tx(&st_full[s], rec_bytes + x_bytes + CH * 4u);
+        bulk_g2s(dst, a.rec + (c / 32) * rw, rec_bytes, &st_full[s]);
+        bulk_g2s(dst + 2 * rw, a.xsoa + (a.c0 + c) * DP, x_bytes, &st_full[s]);
+        bulk_g2s(dst + 2 * rw + 2 * 32 * DP, a.tau + c, CH * 4u, &st_full[s]);
+      }
+    }
+  } else if (warp >= BUILD_WARP0 && warp < MMA_WARP) {
+    // ---------------- B builders: V(t) = V32 + S(Delta) M32 -> TF32 hi / lo ----------------
+    // thread bt handles float4 f = bt + 128 i of the live j-groups of both
+    // 32-column images; the S(Delta) quadruple of f is (f / 8) % 8 = (bt / 8) % 8
+    // for every i (128 / 8 = 16), so it is loaded once per half
+    const int bt = tid - BUILD_WARP0 * 32;  // 0..127
+    const int live = jgroups * 64;          // float4s of one 32-column image in live j-groups
+    const int squad = (bt >> 3) & 7;
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % ST, sb = k % SB;
+      PROF_T0;
+      mbar_wait_backoff<64>(&st_full[s], (k / ST) & 1);
+      PROF_ADD(1);
+      const float* rec = smS + s * st_floats;
+      if (warp == BUILD_WARP0) {
+        const int* tau = reinterpret_cast<const int*>(rec + 2 * rw + 2 * 32 * DP);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int dl = min(max(t_iter - tau[h * 32 + lane] - 1, 0), a.budget);
+          sS[sb * CH + h * 32 + lane] = dl < a.ntab ? stab[dl] : __ldg(a.s32 + dl);
+        }
+      }
+      PROF_T0;
+      if (k >= SB) mbar_wait_backoff<128>(&b_empty[sb], ((k / SB) - 1) & 1);
+      PROF_ADD(2);
+      PROF_T0;
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * BW) : "memory");
+      PROF_ADD(3);
+#if SGD_PROF
+      const long long prof_b0 = clock64();
+#endif
+      float4* bbase = reinterpret_cast<float4*>(smB + sb * 4 * IMG);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 sc = reinterpret_cast<const float4*>(sS + sb * CH + h * 32)[squad];
+        const float4* v4 = reinterpret_cast<const float4*>(rec + h * rw);
+        const float4* m4 = reinterpret_cast<const float4*>(rec + h * rw + a.moff);
+        float4* bh = bbase + h * (IMG / 4);
+        float4* bl = bbase + (2 + h) * (IMG / 4);
+        const float2 s01 = make_float2(sc.x, sc.y), s23 = make_float2(sc.z, sc.w);
+        const float4* m4b = m4;
+#pragma unroll 5
+        for (int f = bt; f < live; f += 32 * BW) {
+          // V(t) in packed FP32x2; hi = V(t) truncated to TF32 (one LOP per
+          // element: the builders are the slab's critical path), lo = V(t) - hi
+          // exactly (the tensor core reads its top 11 bits)
+          const float4 vv = v4[f], mm = m4b[f];
+          const float2 v01 = __ffma2_rn(s01, make_float2(mm.x, mm.y), make_float2(vv.x, vv.y));
+          const float2 v23 = __ffma2_rn(s23, make_float2(mm.z, mm.w), make_float2(vv.z, vv.w));
+          float4 h;
+          h.x = __uint_as_float(__float_as_uint(v01.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v01.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v23.x) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v23.y) & 0xFFFFE000u);
+          const float2 l01 = __fadd2_rn(v01, make_float2(-h.x, -h.y));
+          const float2 l23 = __fadd2_rn(v23, make_float2(-h.z, -h.w));
+          bh[f] = h;
+          bl[f] = make_float4(l01.x, l01.y, l23.x, l23.y);
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&b_full[sb]);
+        mbar_arrive(&st_empty[s]);
+      }
+#if SGD_PROF
+      prof_acc[4] += clock64() - prof_b0;  // build (slot 14 at the end)
+#endif
+    }
+  } else if (warp == MMA_WARP) {
+    // ---------------- MMA issuer: 2 x 12 MMAs per 64-column chunk ----------------
+    // Each 32-column half of A starts as soon as the evaluation warps publish
+    // it. The whole warp waits; one elected lane issues from an if-block whose
+    // operands are all warp-uniform (constant TMEM base, descriptors as 32-bit
+    // offsets of one per-stage base word), so ptxas keeps them in uniform
+    // registers: ~2.5 instructions per MMA instead of ~18 with the per-MMA
+    // elect/broadcast of MMA_TF32 (the issue warp had become the bottleneck).
+    constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+    constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14);  // SBO 1 KiB, version 1 (bit 46)
+    const uint32_t smb0 = smem_u32(smB);
+    const uint32_t bfull0 = smem_u32(b_full), bempty0 = smem_u32(b_empty), afull0 = smem_u32(a_full),
+                   aempty0 = smem_u32(a_empty), dfull0 = smem_u32(d_full), dempty0 = smem_u32(d_empty);
+    auto wait_u = [](uint32_t bar, uint32_t parity) {
+      asm volatile(
+          "{\n\t.reg .pred P1;\nW_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+          "@!P1 bra W_%=;\n\t}" ::"r"(bar),
+          "r"(parity)
+          : "memory");
+    };
+    auto elect_one = []() -> uint32_t {
+      uint32_t pred = 0;
+      asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+      return pred;
+    };
+    auto mma = [](uint32_t d, uint32_t a, uint32_t blo, uint32_t acc) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\t"
+          "mov.b64 bd, {%2, %3};\n\t"
+          "setp.ne.b32 p, %5, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bd, %4, p;\n\t}" ::"r"(d),
+          "r"(a), "r"(blo), "n"(DESC_HI), "n"(idesc), "r"(acc)
+          : "memory");
+    };
+    auto commit = [](uint32_t bar) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                   : "memory");
+    };
+    int sb = 0, bph = 0, ab = 0, aph = 0, g = 0, kf = 0;
+    for (int k = 0; k < nk; ++k) {
+      const bool first = kf == 0, last = kf == F - 1 || k + 1 == nk;
+      PROF_T0;
+      wait_u(bfull0 + 8 * sb, bph);
+      PROF_ADD(4);
+      PROF_T0;
+      if (first && g >= 2) wait_u(dempty0 + 8 * (g & 1), ((g >> 1) - 1) & 1);
+      PROF_ADD(5);
+      const uint32_t dt = tmem + ((g & 1) ? D_COL1 : 0);
+      const uint32_t blo0 = (((smb0 + sb * 4 * IMG * 4) & 0x3FFFF) >> 4) | (8u << 16);  // LBO 128 B
+      const uint32_t ah = tmem + A_COL0 + ab * 128;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        PROF_T0;
+        wait_u(afull0 + 8 * (2 * ab + h), aph);
+        PROF_ADD(6);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = 4 * h + k4;
+            const uint32_t bh = blo0 + ((h * IMG * 4 + k4 * 256) >> 4);
+            const uint32_t bl = bh + ((2 * IMG * 4) >> 4);
+            mma(dt, ah + kk * 8, bh, (first && kk == 0) ? 0u : 1u);
+            mma(dt, ah + kk * 8, bl, 1u);
+            mma(dt, ah + 64 + kk * 8, bh, 1u);
+          }
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
+        commit(bempty0 + 8 * sb);
+        commit(aempty0 + 8 * ab);
+        if (last) commit(dfull0 + 8 * (g & 1));
+      }
+      __syncwarp();
+      if (++sb == SB) { sb = 0; bph ^= 1; }
+      if (++ab == NAB) { ab = 0; aph ^= 1; }
+      if (++kf == F) { kf = 0; ++g; }
+    }
+  } else {
+    // ---------------- evaluation + drain ----------------
+    const int lg = warp & 3, quarter = warp >> 2;
+    const int row = lg * 32 + lane;
+    const int er = tile * TBM + row;
+    const bool row_ok = er < a.R;
+    const int gi = row_ok ? idx[er] : 0;
+    const float* xrow = a.xs + static_cast<size_t>(gi) * a.dp;
+    const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
+    double acc[DC];
+#pragma unroll
+    for (int e = 0; e < DC; ++e) acc[e] = 0.0;
+    auto drain = [&](int g) {
+      PROF_T0;
+      mbar_wait(&d_full[g & 1], (g >> 1) & 1);
+      PROF_ADD(7);
+      tc_fence_after();
+      const uint32_t base = tmem + lane_addr + ((g & 1) ? D_COL1 : 0) + quarter * DC;
+#pragma unroll
+      for (int q = 0; q < DC / 4; ++q) {
+        uint32_t v[4];
+        tc_ld4(base + 4 * q, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * q + e] += static_cast<double>(__uint_as_float(v[e]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_empty[g & 1]);
+    };
+    uint64_t xik2[4], k_s3, k_one, k_c, k_l2s2;
+    {
+      const float4 xr = __ldg(reinterpret_cast<const float4*>(xrow));
+      const float xe[4] = {xr.x, xr.y, xr.z, xr.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) asm("mov.b64 %0, {%1, %1};" : "=l"(xik2[q]) : "f"(xe[q]));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_s3) : "f"(kSqrt3f));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_one) : "f"(1.f));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_c) : "f"(kNegSqrt3Log2e));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(k_l2s2) : "f"(a.log2_s2));
+    }
+    // this thread's 16 columns: 8 q .. 8 q + 7 of each 32-column half (half h:
+    // chunk columns 32 h + 8 q ..), so each half of the A buffer is complete --
+    // and published to the MMA warp -- after one eval8 of every evaluation warp
+    const uint32_t st_base = smem_u32(smS);
+    const uint32_t xoff = static_cast<uint32_t>((2 * rw + quarter * 8) * 4);
+    constexpr uint32_t XHALF = 32 * DP * 4;  // bytes between the halves' SoA x
+    const uint32_t st_full0 = smem_u32(st_full), st_empty0 = smem_u32(st_empty);
+    const uint32_t a_full0 = smem_u32(a_full), a_empty0 = smem_u32(a_empty);
+    const uint32_t acol = tmem + lane_addr + A_COL0 + quarter * 8;
+    auto wait_u32 = [](uint32_t bar, uint32_t parity) {
+      uint32_t done = 0;
+      do {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+      } while (!done);
+    };
+    auto arrive_u32 = [](uint32_t bar) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    };
+    // eight entries (four FP32x2 column pairs) starting at column pair base xq
+    auto eval8 = [&](uint32_t xq, uint32_t (&hi)[8], uint32_t (&lo)[8]) {
+#pragma unroll
+      for (int t = 0; t < 8; t += 2) {
+        uint64_t r2;
+#pragma unroll
+        for (int q = 0; q < DX; ++q) {
+          uint64_t cc, dd;
+          asm volatile("ld.shared.b64 %0, [%1];" : "=l"(cc) : "r"(xq + (q * 32 + t) * 4));
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dd) : "l"(cc), "l"(xik2[q]));
+          if (q == 0)
+            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r2) : "l"(dd));
+          else
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(r2) : "l"(dd));
+        }
+        float ra, rb;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r2));
+        ra = sqrt_approx(ra);
+        rb = sqrt_approx(rb);
+        uint64_t rr, tt, uu, ee, kk;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(rr) : "f"(ra), "f"(rb));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(tt) : "l"(rr), "l"(k_s3), "l"(k_one));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(uu) : "l"(rr), "l"(k_c), "l"(k_l2s2));
+        float ua, ub;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(ua), "=f"(ub) : "l"(uu));
+        ua = ex2_approx(ua);
+        ub = ex2_approx(ub);
+        asm("mov.b64 %0, {%1, %2};" : "=l"(ee) : "f"(ua), "f"(ub));
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(kk) : "l"(tt), "l"(ee));
+        float ka, kb;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(ka), "=f"(kb) : "l"(kk));
+        hi[t] = __float_as_uint(ka) & 0xFFFFE000u;
+        hi[t + 1] = __float_as_uint(kb) & 0xFFFFE000u;
+        uint64_t hh, ll;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "r"(hi[t]), "r"(hi[t + 1]));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ll) : "l"(kk), "l"(hh));
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(lo[t]), "=r"(lo[t + 1]) : "l"(ll));
+      }
+    };
+    int drained = 0, next_drain = F + DEFER;
+    int pend = -1;  // a_full barrier (2 ab + h) of the half whose stores are in flight
+    auto publish = [&]() {
+      if (pend < 0) return;
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_u32(a_full0 + 8 * pend);
+      pend = -1;
+    };
+    int s = 0, sph = 0, ab = 0;
+    for (int k = 0; k < nk; ++k) {
+      PROF_T0;
+      wait_u32(st_full0 + 8 * s, sph);
+      PROF_ADD(8);
+      const uint32_t xq = st_base + static_cast<uint32_t>(s * st_floats * 4) + xoff;
+      uint32_t hi[8], lo[8];
+      eval8(xq, hi, lo);
+      publish();  // previous chunk's second half
+      // buffer ab's previous use (chunk k - NAB) was use k / NAB - 1 of it
+      PROF_T0;
+      if (k >= NAB) wait_u32(a_empty0 + 8 * ab, ((k / NAB) - 1) & 1);
+      PROF_ADD(9);
+      tc_fence_after();
+      const uint32_t abase = acol + ab * 128;
+      tc_st8(abase, hi);
+      tc_st8(abase + 64, lo);
+      pend = 2 * ab;
+      eval8(xq + XHALF, hi, lo);
+      __syncwarp();
+      if (lane == 0) arrive_u32(st_empty0 + 8 * s);  // x_c consumed
+      publish();  // this chunk's first half
+      tc_st8(abase + 32, hi);
+      tc_st8(abase + 96, lo);
+      pend = 2 * ab + 1;
+      if (++s == ST) { s = 0; sph ^= 1; }
+      if (++ab == NAB) ab = 0;
+      if (k == next_drain) {
+        drain(drained++);
+        next_drain += F;
+      }
+    }
+    publish();
+    while (drained < ngroups) drain(drained++);
+    if (row_ok) {
+      double* prow = a.part + (static_cast<size_t>(split) * a.R + er) * a.m;
+#pragma unroll
+      for (int e = 0; e < DC; ++e) {
+        const int j = quarter * DC + e;
+        if (j < a.m) prow[j] = acc[e];
+      }
+    }
+  }
+#if SGD_PROF
+  if (lane == 0) {
+    const int slot = warp == PROD_WARP ? 10 : (warp >= BUILD_WARP0 && warp < MMA_WARP) ? 11 : warp == MMA_WARP ? 12 : 13;
+    atomicAdd(&g_sgd_prof[slot], static_cast<unsigned long long>(clock64() - prof_start));
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      const bool bld = warp >= BUILD_WARP0 && warp < MMA_WARP;
+      const int slot = (bld && i == 4) ? 14 : i;
+      if (prof_acc[i]) atomicAdd(&g_sgd_prof[slot], static_cast<unsigned long long>(prof_acc[i]));
+    }
+  }
+#endif
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int NPAD, int DX, int NBW>
+void launch_64_t(const SgdSlabArgs& a, cudaStream_t s) {
+  const size_t smem = c64::smem_bytes<NPAD>(a.rw, 4, a.ntab);
+  if (smem > 227 * 1024) throw std::invalid_argument("gpk: SGD slab kernel (64) shared memory exceeds 227 KB");
+  static size_t configured = 0;
+  if (smem > configured) {
+    GPK_CUDA(cudaFuncSetAttribute(sgd_slab64_kernel<NPAD, DX, NBW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  sgd_slab64_kernel<NPAD, DX, NBW><<<dim3((a.R + TBM - 1) / TBM, a.splits), 32 * (EW + 2 + NBW), smem, s>>>(a);
+  check_launch("sgd_slab64_kernel");
+}
+template <int NPAD, int DX>
+void launch_64(const SgdSlabArgs& a, cudaStream_t s) {
+  // B-builder warps: 8 (measured at C4: 230 vs 240 us per launch with 4;
+  // the builders' smem round trips queue behind the evaluation warps' MUFU
+  // work, so more of them in flight); GPK_SGD_BW=4 selects four
+  static const int bw = [] {
+    const char* e = std::getenv("GPK_SGD_BW");
+    return e ? std::atoi(e) : 8;
+  }();
+  if (bw == 4) return launch_64_t<NPAD, DX, 4>(a, s);
+  return launch_64_t<NPAD, DX, 8>(a, s);
+}
+
 template <int NPAD, int DP4, bool GRAM, int DX = 0>
 void launch_one(const SgdSlabArgs& a, cudaStream_t s) {
   constexpr int DP = 4 * DP4;
@@ -489,6 +991,12 @@ void launch_n(const SgdSlabArgs& a, cudaStream_t s) {
   switch (a.dp / 4) {
     case 1:
       if (a.xg) return launch_one<NPAD, 1, true>(a, s);
+      if (a.ch64) switch (a.d) {  // 64-column pipeline
+          case 1: return launch_64<NPAD, 1>(a, s);
+          case 2: return launch_64<NPAD, 2>(a, s);
+          case 3: return launch_64<NPAD, 3>(a, s);
+          default: return launch_64<NPAD, 4>(a, s);
+        }
       switch (a.d) {  // exact-dimension scalar distance loops for d <= 4
         case 1: return launch_one<NPAD, 1, false, 1>(a, s);
         case 2: return launch_one<NPAD, 1, false, 2>(a, s);
@@ -778,7 +1286,7 @@ void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s) {
 
 void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
                              cudaStream_t s) {
-  const int nchunks = rows_pad / 32;
+  const int nchunks = rows_pad / 32 + 1;  // + one zero record: a 64-column chunk may end past rows_pad
   const long long total = static_cast<long long>(nchunks) * rw;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
   sgd_records_init_kernel<<<blocks, 256, 0, s>>>(V, nloc, nchunks, m, rw, moff, rec, tau);
@@ -794,3 +1302,15 @@ void sgd_materialise_launch(double* Vb, const double* Mb, const int* tau, const 
 }
 
 }  // namespace gpk
+
+#if SGD_PROF
+extern "C" int gpk_debug_sgd_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, gpk::g_sgd_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(gpk::g_sgd_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
