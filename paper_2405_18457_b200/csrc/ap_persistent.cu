@@ -38,16 +38,6 @@ constexpr int TG_COL = 96, TGA_COL = 384;
 #ifndef AP_DECIDE_ALL
 #define AP_DECIDE_ALL 1
 #endif
-#ifndef AP_MMA_WARP
-#define AP_MMA_WARP 1  // measured with the Gram MMAs: C2 slab phase 26.0 -> 19.7 us (without them the lane-0 loop was faster)
-#endif
-#if AP_MMA_WARP
-#define AP_MMA tc_mma_tf32_w
-#define AP_COMMIT tc_commit_w
-#else
-#define AP_MMA tc_mma_tf32
-#define AP_COMMIT tc_commit
-#endif
 template <int DP4>
 struct TgShape {
   static constexpr int KG = ((DP4 + 1) / 2) * 8;
@@ -161,7 +151,10 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // one CTA per SM allocating all 512 columns: the allocation starts at 0
+  // (a compile-time base keeps the MMA issue warp-uniform, tc_util.cuh)
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0) __trap();
   // the residual tile (after the host-side refresh) lives in smem for the solve
   if (tid == 0) {
     const uint32_t bytes = static_cast<uint32_t>(rows_t) * m * 8u;
@@ -377,24 +370,26 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
         }
       }
     } else if (warp == EW + 1) {
-      if (AP_MMA_WARP || lane == 0) {  // AP_MMA_WARP=0: lane 0 alone in divergent code (see tc_util.cuh)
+      {  // whole warp: waits and operands; one elected lane issues (tc_util.cuh)
         constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+        constexpr uint32_t gdesc = tf32_idesc(TBK, TBM);
+        constexpr uint32_t GHI = tc_desc_hi((KG / 4) * 128), VHI = tc_desc_hi((TBK / 4) * 128);
         // TG: G(k) = -2 X_tile X_c(k)^T, cross terms first, hi.hi last
         auto gram_mma = [&](int k) {
           const int s = k % STAGES;
           const uint32_t ah = tmem + TGA_COL, al = ah + KG;
-          const uint32_t bh = smem_u32(smX + s * XST), bl = bh + TBK * KG * 4;
-          constexpr uint32_t gdesc = tf32_idesc(TBK, TBM);
-          constexpr uint32_t SBO = (KG / 4) * 128;
+          const uint32_t bh = tc_desc_lo(smem_u32(smX + s * XST), 128), bl = bh + ((TBK * KG * 4) >> 4);
+          if (tc_elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < KG / 8; ++ks) {
-            AP_MMA(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
-            AP_MMA(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+            for (int ks = 0; ks < KG / 8; ++ks) {
+              tc_mma_u<GHI, gdesc>(tmem + TG_COL, ah + ks * 8, bl + ks * 16, ks ? 1u : 0u);
+              tc_mma_u<GHI, gdesc>(tmem + TG_COL, al + ks * 8, bh + ks * 16, 1u);
+            }
+#pragma unroll
+            for (int ks = 0; ks < KG / 8; ++ks) tc_mma_u<GHI, gdesc>(tmem + TG_COL, ah + ks * 8, bh + ks * 16, 1u);
+            tc_commit_u(g_full);
           }
-#pragma unroll
-          for (int ks = 0; ks < KG / 8; ++ks)
-            AP_MMA(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
-          AP_COMMIT(g_full);
+          __syncwarp();
         };
         if (TG && nq > 0) {
           if (it == 0) mbar_wait(arow_full, 0);
@@ -415,21 +410,23 @@ __global__ void __launch_bounds__(THREADS, 1) ap_persistent_kernel(const ApPersi
           }
           mbar_wait(&a_full[b], (k / NAB) & 1);
           tc_fence_after();
-          const uint32_t bh = smem_u32(smB + s * L::CHUNK_FLOATS);
-          const uint32_t bl = bh + L::IMG_FLOATS * 4;
+          const uint32_t bh = tc_desc_lo(smem_u32(smB + s * L::CHUNK_FLOATS), 128);
+          const uint32_t bl = bh + ((L::IMG_FLOATS * 4) >> 4);
           const uint32_t ah = tmem + A_BASE + b * 64, al = ah + 32;
+          if (tc_elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < TBK / 8; ++kk) {
-            const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
-            const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
-            AP_MMA(tmem, ah + kk * 8, dh, idesc, (q == 0 && kk == 0) ? 0u : 1u);
-            AP_MMA(tmem, ah + kk * 8, dl, idesc, 1u);
-            AP_MMA(tmem, al + kk * 8, dh, idesc, 1u);
+            for (int kk = 0; kk < TBK / 8; ++kk) {
+              tc_mma_u<VHI, idesc>(tmem, ah + kk * 8, bh + kk * 16, (q == 0 && kk == 0) ? 0u : 1u);
+              tc_mma_u<VHI, idesc>(tmem, ah + kk * 8, bl + kk * 16, 1u);
+              tc_mma_u<VHI, idesc>(tmem, al + kk * 8, bh + kk * 16, 1u);
+            }
+            tc_commit_u(&empty[s]);
+            tc_commit_u(&a_empty[b]);
           }
-          AP_COMMIT(&empty[s]);
-          AP_COMMIT(&a_empty[b]);
+          __syncwarp();
         }
-        AP_COMMIT(d_full);
+        if (tc_elect_one()) tc_commit_u(d_full);
+        __syncwarp();
       }
     } else {
       for (int q = 0; q < nq; ++q) {

@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // one CTA per SM allocating all 512 columns: the allocation starts at 0
+  // (a compile-time base keeps the MMA issue warp-uniform, tc_util.cuh)
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0) __trap();
 
   if (warp == 8) {
     // ---------------- producer ----------------
@@ -180,9 +183,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
     }
   } else if (warp == 9) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {  // single-thread issue: measured faster here than the warp-converged loop
+    {  // whole warp: waits and operands; one elected lane issues (tc_util.cuh)
       constexpr uint32_t idesc = tf32_idesc(CN, TBM);
-      const uint32_t sbo = static_cast<uint32_t>(KP / 4) * 128u;
+      const uint32_t HI = tc_desc_hi(static_cast<uint32_t>(KP / 4) * 128u);
       int prev_ti = -1, rows_loaded = 0;
       for (int k = 0; k < nq; ++k) {
         const int s = k % STAGES, b = k & 1;
@@ -196,23 +199,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         mbar_wait(&full[s], (k / STAGES) & 1);
         if (k >= 2) mbar_wait(&d_empty[b], ((k - 2) / 2) & 1);
         tc_fence_after();
-        const uint32_t bh = smem_u32(smB + s * NPIECE * img);
-        const uint32_t bm = bh + img * 4, bl = bm + img * 4;
+        const uint32_t bh = tc_desc_lo(smem_u32(smB + s * NPIECE * img), 128);
+        const uint32_t bm = bh + ((img * 4) >> 4), bl = bm + ((img * 4) >> 4);
         const uint32_t dt = tmem + b * CN;
         const uint32_t ah = tmem + A_BASE, am = ah + KP, al = am + KP;
-        for (int kk = 0; kk < KP / 8; ++kk) {
-          const uint64_t dh = umma_desc(bh + kk * 256, 128, sbo);
-          const uint64_t dm = umma_desc(bm + kk * 256, 128, sbo);
-          const uint64_t dl = umma_desc(bl + kk * 256, 128, sbo);
-          tc_mma_tf32(dt, ah + kk * 8, dh, idesc, kk == 0 ? 0u : 1u);
-          tc_mma_tf32(dt, ah + kk * 8, dm, idesc, 1u);
-          tc_mma_tf32(dt, am + kk * 8, dh, idesc, 1u);
-          tc_mma_tf32(dt, am + kk * 8, dm, idesc, 1u);
-          tc_mma_tf32(dt, ah + kk * 8, dl, idesc, 1u);
-          tc_mma_tf32(dt, al + kk * 8, dh, idesc, 1u);
+        if (tc_elect_one()) {
+          for (int kk = 0; kk < KP / 8; ++kk) {
+            tc_mma_ur<idesc>(dt, ah + kk * 8, bh + kk * 16, HI, kk == 0 ? 0u : 1u);
+            tc_mma_ur<idesc>(dt, ah + kk * 8, bm + kk * 16, HI, 1u);
+            tc_mma_ur<idesc>(dt, am + kk * 8, bh + kk * 16, HI, 1u);
+            tc_mma_ur<idesc>(dt, am + kk * 8, bm + kk * 16, HI, 1u);
+            tc_mma_ur<idesc>(dt, ah + kk * 8, bl + kk * 16, HI, 1u);
+            tc_mma_ur<idesc>(dt, al + kk * 8, bh + kk * 16, HI, 1u);
+          }
+          tc_commit_u(&empty[s]);
+          tc_commit_u(&d_full[b]);
         }
-        tc_commit(&empty[s]);
-        tc_commit(&d_full[b]);
+        __syncwarp();
       }
     }
   } else {

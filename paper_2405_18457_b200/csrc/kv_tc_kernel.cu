@@ -305,7 +305,12 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // one CTA per SM allocating all 512 columns (deep variants): the allocation
+  // starts at 0, and the compile-time base keeps the MMA issue warp-uniform
+  // (tc_util.cuh); two CTAs per SM read their base from the allocation
+  constexpr bool UNI = TCOLS == 512;
+  const uint32_t tmem = UNI ? 0u : *tmem_slot;
+  if (UNI && tid == 0 && *tmem_slot != 0) __trap();
 
   // fused AP slab: the tile's rows of `base` (the residual) are staged in smem
   // by one bulk copy issued before the chunk loop, so the drain never waits on
@@ -341,25 +346,41 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     }
   } else if (warp == EW + 1) {
     // ---------------- MMA issuer ----------------
-    if (GPK_MMA_WARP || lane == 0) {
+    if (UNI || GPK_MMA_WARP || lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+      constexpr uint32_t gdesc = tf32_idesc(TBK, TBM);
+      constexpr uint32_t GSBO = (KG / 4) * 128, VSBO = (TBK / 4) * 128;
       // TG: G(k) = -2 X_rows X_c(k)^T, the cross terms first and hi.hi last
       // (truncating accumulation: the small terms go in while D is small)
       auto gram_mma = [&](int k) {
         const int s = k % STAGES;
         const uint32_t ah = tmem + TGA_COL, al = ah + KG;
         const uint32_t bh = smem_u32(smX + s * XST), bl = bh + TBK * KG * 4;
-        constexpr uint32_t gdesc = tf32_idesc(TBK, TBM);
-        constexpr uint32_t SBO = (KG / 4) * 128;
+        if constexpr (UNI) {
+          const uint32_t dh = tc_desc_lo(bh, 128), dl = tc_desc_lo(bl, 128);
+          if (tc_elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < KG / 8; ++ks) {
-          MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, SBO), gdesc, ks ? 1u : 0u);
-          MMA_TF32(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
+            for (int ks = 0; ks < KG / 8; ++ks) {
+              tc_mma_u<tc_desc_hi(GSBO), gdesc>(tmem + TG_COL, ah + ks * 8, dl + ks * 16, ks ? 1u : 0u);
+              tc_mma_u<tc_desc_hi(GSBO), gdesc>(tmem + TG_COL, al + ks * 8, dh + ks * 16, 1u);
+            }
+#pragma unroll
+            for (int ks = 0; ks < KG / 8; ++ks)
+              tc_mma_u<tc_desc_hi(GSBO), gdesc>(tmem + TG_COL, ah + ks * 8, dh + ks * 16, 1u);
+            tc_commit_u(g_full);
+          }
+          __syncwarp();
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < KG / 8; ++ks) {
+            MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bl + ks * 256, 128, GSBO), gdesc, ks ? 1u : 0u);
+            MMA_TF32(tmem + TG_COL, al + ks * 8, umma_desc(bh + ks * 256, 128, GSBO), gdesc, 1u);
+          }
+#pragma unroll
+          for (int ks = 0; ks < KG / 8; ++ks)
+            MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, GSBO), gdesc, 1u);
+          MMA_COMMIT(g_full);
         }
-#pragma unroll
-        for (int ks = 0; ks < KG / 8; ++ks)
-          MMA_TF32(tmem + TG_COL, ah + ks * 8, umma_desc(bh + ks * 256, 128, SBO), gdesc, 1u);
-        MMA_COMMIT(g_full);
       };
       if (TG && nk > 0) {
         mbar_wait(arow_full, 0);
@@ -386,19 +407,36 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
         const uint32_t bl = bh + L::IMG_FLOATS * 4;
         const uint32_t ah = tmem + A_BASE + b * 64;
         const uint32_t al = ah + 32;
+        if constexpr (UNI) {
+          const uint32_t dh = tc_desc_lo(bh, 128), dl = tc_desc_lo(bl, 128);
+          if (tc_elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < TBK / 8; ++kk) {
-          const uint64_t dh = umma_desc(bh + kk * 256, 128, (TBK / 4) * 128);
-          const uint64_t dl = umma_desc(bl + kk * 256, 128, (TBK / 4) * 128);
-          MMA_TF32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
-          MMA_TF32(tmem, ah + kk * 8, dl, idesc, 1u);
-          MMA_TF32(tmem, al + kk * 8, dh, idesc, 1u);
-        }
-        MMA_COMMIT(&empty[s]);
-        MMA_COMMIT(&a_empty[b]);
-        if (last_in_group) {
-          MMA_COMMIT(d_full);
-          ++g;
+            for (int kk = 0; kk < TBK / 8; ++kk) {
+              tc_mma_u<tc_desc_hi(VSBO), idesc>(tmem, ah + kk * 8, dh + kk * 16, (first_in_group && kk == 0) ? 0u : 1u);
+              tc_mma_u<tc_desc_hi(VSBO), idesc>(tmem, ah + kk * 8, dl + kk * 16, 1u);
+              tc_mma_u<tc_desc_hi(VSBO), idesc>(tmem, al + kk * 8, dh + kk * 16, 1u);
+            }
+            tc_commit_u(&empty[s]);
+            tc_commit_u(&a_empty[b]);
+            if (last_in_group) tc_commit_u(d_full);
+          }
+          __syncwarp();
+          if (last_in_group) ++g;
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < TBK / 8; ++kk) {
+            const uint64_t dh = umma_desc(bh + kk * 256, 128, VSBO);
+            const uint64_t dl = umma_desc(bl + kk * 256, 128, VSBO);
+            MMA_TF32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
+            MMA_TF32(tmem, ah + kk * 8, dl, idesc, 1u);
+            MMA_TF32(tmem, al + kk * 8, dh, idesc, 1u);
+          }
+          MMA_COMMIT(&empty[s]);
+          MMA_COMMIT(&a_empty[b]);
+          if (last_in_group) {
+            MMA_COMMIT(d_full);
+            ++g;
+          }
         }
       }
     }

@@ -89,6 +89,51 @@ __device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
 #define MMA_TF32 tc_mma_tf32
 #define MMA_COMMIT tc_commit
 #endif
+// ---- warp-uniform single-thread issue -------------------------------------
+// The whole issuing warp runs the waits and the operand arithmetic; one lane,
+// chosen by tc_elect_one(), issues from an if-block. With a compile-time TMEM
+// base (one CTA per SM allocating all 512 columns: the allocation starts at 0)
+// and descriptors formed as 32-bit offsets of one base word (the start-address
+// field is the low 14 bits), every operand is warp-uniform, so ptxas keeps
+// them in uniform registers: ~2.5 instructions per MMA instead of ~18 for
+// MMA_TF32's per-MMA elect and register broadcasts.
+__device__ __forceinline__ uint32_t tc_elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred;
+}
+// low word of umma_desc(saddr, lbo, sbo); the high word is tc_desc_hi(sbo)
+__device__ __forceinline__ uint32_t tc_desc_lo(uint32_t saddr, uint32_t lbo) {
+  return ((saddr & 0x3FFFF) >> 4) | ((lbo >> 4) << 16);
+}
+constexpr uint32_t tc_desc_hi(uint32_t sbo) { return ((sbo >> 4) & 0x3FFF) | (1u << 14); }
+template <uint32_t HI, uint32_t IDESC>
+__device__ __forceinline__ void tc_mma_u(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\t"
+      "mov.b64 bd, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bd, %4, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "r"(b_lo), "n"(HI), "n"(IDESC), "r"(accumulate)
+      : "memory");
+}
+// the same with the descriptor's high word at run time (SBO from a kernel argument)
+template <uint32_t IDESC>
+__device__ __forceinline__ void tc_mma_ur(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t b_hi,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\t"
+      "mov.b64 bd, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bd, %4, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "r"(b_lo), "r"(b_hi), "n"(IDESC), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_u(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
