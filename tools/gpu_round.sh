@@ -13,6 +13,6 @@ timeout 600 python tools/one_step.py C4 1 > gpurun_out/one_step_plain_$TAG.log 2
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 60000 --csv \
   --log-file gpurun_out/launches_C4_$TAG.csv python tools/one_step.py C4 1 > gpurun_out/launches_ncu_$TAG.log 2>&1
 timeout 300 python tools/sgd_timing.py 393216 1 > gpurun_out/sgd_timing_$TAG.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgd_slab_kernel -s 20 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgd_slab64_kernel -s 20 -c 1 \
   -o gpurun_out/full_sgd_slab_$TAG -f python tools/sgd_timing.py 393216 1 > gpurun_out/ncu_slab_$TAG.log 2>&1
 echo done
