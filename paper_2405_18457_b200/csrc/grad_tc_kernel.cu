@@ -46,8 +46,18 @@ using namespace tc;
 constexpr int TBM = 128;  // tile edge (rows per CTA pass, columns per tile)
 constexpr int CN = 64;    // columns per chunk == MMA N
 constexpr int STAGES = 3;
-constexpr int NTHREADS = 320;
-constexpr int EVAL_WARPS = 8;
+// Evaluation warps: 16 for d <= 8 (a quarter of each 64-column chunk each,
+// four per SM sub-partition: with 8 the C4 pass ran at 15 % warp occupancy
+// and 48 % issue), 8 above (half a chunk each: the wider distance loops need
+// the registers); the first 8 also write the row tile's U pieces into TMEM;
+// then the producer warp and the MMA warp.
+constexpr int A_WRITERS = 8;
+template <int DP4>
+struct GradRoles {
+  static constexpr int EW = DP4 <= 2 ? 16 : 8;
+  static constexpr int NT = 32 * (EW + 2);
+  static constexpr int CW = CN / (EW / 4);  // chunk columns per evaluation warp
+};
 constexpr int TMEM_COLS = 512;  // one CTA per SM
 constexpr int A_BASE = 2 * CN;  // D buffers at TMEM columns [0, 64) and [64, 128); A pieces from 128
 constexpr int NPIECE = 3;
@@ -108,7 +118,8 @@ __device__ __forceinline__ void butterfly_flush(const float (&v)[NV], int lane, 
 // COMB (with NARROW): the estimator's combination cw G + cn u w^T is formed
 // per entry and accumulated once (one set of d + 1 sums instead of two).
 template <int DP4, bool NARROW, bool COMB>
-__global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a) {
+__global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const GradTcArgs a) {
+  constexpr int EVAL_WARPS = GradRoles<DP4>::EW, NTHREADS = GradRoles<DP4>::NT, CW = GradRoles<DP4>::CW;
   constexpr int DP = 4 * DP4;
   constexpr int NPR = (NARROW && !COMB) ? 2 : 1;
   constexpr int NUSED = NPR * (DP + 1);
@@ -148,7 +159,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
       mbar_init(&d_full[b], 1);
       mbar_init(&d_empty[b], EVAL_WARPS);
     }
-    mbar_init(a_full, EVAL_WARPS);
+    mbar_init(a_full, A_WRITERS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
   constexpr uint32_t tmem = 0;
   if (tid == 0 && *tmem_slot != 0) __trap();
 
-  if (warp == 8) {
+  if (warp == EVAL_WARPS) {
     // ---------------- producer ----------------
     if (lane == 0) {
       const uint32_t bbytes = NPIECE * img * 4u, xbytes = CN * DP * 4u, wbytes = NARROW ? CN * 4u : 0u;
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         if (NARROW) bulk_g2s(smW + s * CN, a.w1 + col0, wbytes, &full[s]);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == EVAL_WARPS + 1) {
     // ---------------- MMA issuer ----------------
     {  // whole warp: waits and operands; one elected lane issues (tc_util.cuh)
       constexpr uint32_t idesc = tf32_idesc(CN, TBM);
@@ -220,7 +231,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
     }
   } else {
     // ---------------- A writers + evaluation ----------------
-    const int lg = warp & 3, half = warp >> 2;
+    const int lg = warp & 3, half = warp >> 2;  // half: A-writer column half (warps < 8); quarter of the chunk
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
     uint64_t xi2[2 * DP4];
     float u1i = 0.f;
@@ -241,6 +252,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         const int i = ti * TBM + lg * 32 + lane;  // < T * 128: xs / u1 are padded to that
         const bool row_ok = i < a.n;
         const float* urow = a.ua + static_cast<size_t>(row_ok ? i : 0) * a.lda;
+        if (warp < A_WRITERS) {
         for (int q = 0; q < KP / 16; ++q) {
           uint32_t hi[8], md[8], lo[8];
 #pragma unroll
@@ -258,6 +270,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full);
+        }
 #pragma unroll
         for (int u = 0; u < DP4; ++u) {
           const float4 v = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(i) * DP) + u);
@@ -269,19 +282,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
       mbar_wait(&full[s], (k / STAGES) & 1);
       mbar_wait(&d_full[b], (k / 2) & 1);
       tc_fence_after();
-      const uint32_t xbase = smem_u32(smX + s * CN * DP + half * 32 * DP);
-      const float* wc = smW + s * CN + half * 32;
+      const uint32_t xbase = smem_u32(smX + s * CN * DP + half * CW * DP);  // half: the warp's column group here
+      const float* wc = smW + s * CN + half * CW;
 #pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < CW / 8; ++q) {
         uint32_t g[8];
-        tc_ld8(tmem + lane_addr + b * CN + half * 32 + q * 8, g);
+        tc_ld8(tmem + lane_addr + b * CN + half * CW + q * 8, g);
         tc_wait_ld();
-        if (q == 3) {  // D buffer fully read: let the next-but-one chunk's MMAs in
+        if (q == CW / 8 - 1) {  // D buffer fully read: let the next-but-one chunk's MMAs in
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&d_empty[b]);
         }
-#pragma unroll 2
+#pragma unroll(DP4 <= 2 ? 8 : 2)
         for (int e = 0; e < 8; ++e) {
           const int c = q * 8 + e;
           uint64_t sq[DP / 2];
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_tc_kernel(const GradTcArgs a
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // x_c / w reads of this stage done
-      {  // chunk complete: flush its FP32 sums into the warp's FP64 slots
+      if (k & 1) {  // tile pair complete (two chunks): flush its FP32 sums into the warp's FP64 slots
         float v[NV];
 #pragma unroll
         for (int t = 0; t < NV; ++t) v[t] = 0.f;
@@ -404,7 +417,7 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
   // >= 120 KB keeps one CTA per SM: each allocates all 512 TMEM columns
   const size_t smem = std::max<size_t>(
       sizeof(float) * (STAGES * NPIECE * CN * a.kp + STAGES * CN * DP + STAGES * CN) +
-          sizeof(double) * EVAL_WARPS * NV + 16 * sizeof(uint64_t),
+          sizeof(double) * GradRoles<DP4>::EW * NV + 16 * sizeof(uint64_t),
       120 * 1024);
   static size_t configured = 0;
   if (smem > configured) {
@@ -412,7 +425,7 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
                                   static_cast<int>(smem)));
     configured = smem;
   }
-  grad_tc_kernel<DP4, NARROW, COMB><<<a.blocks, NTHREADS, smem, s>>>(a);
+  grad_tc_kernel<DP4, NARROW, COMB><<<a.blocks, GradRoles<DP4>::NT, smem, s>>>(a);
   check_launch("grad_tc_kernel");
 }
 
