@@ -277,6 +277,7 @@ struct gpk_batch {
   // lazy-momentum SGD (sgd_lazy.cu): FP32 records, last-update iterations,
   // S / rho^Delta tables, slab partials, apply-block partials, flags
   DBuf<float> sgd_rec, sgd_s32, sgd_xg, sgd_xsoa;
+  DBuf<double> sgd_gpart2;  // fused SGD finish: per-block g^2 and old R^2 partials
   DBuf<int> sgd_tau, sgd_flags;
   DBuf<double> sgd_tab, sgd_part, sgd_gpart;
   DBuf<unsigned> gbar;               // persistent AP: grid-barrier counter
@@ -1942,15 +1943,27 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   ta.ticket = ticket;
   ta.sumsq = sumsq;
   ta.scales = b->scales_dev.p;
+  // one rank: reduce + apply fused into one kernel (GPK_SGD_FUSED_FINISH=0: separate)
+  static const bool finish_env = [] {
+    const char* e = std::getenv("GPK_SGD_FUSED_FINISH");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool fused_finish = finish_env && !op->sharded;
+  SgdStepArgs tf = ta;
+  if (fused_finish) tf.gpart = b->sgd_gpart2.ensure(static_cast<size_t>(sgd_finish_blocks(bs)) * 2 * m);
   int t = 0;
   auto iteration = [&]() {  // solvers.cpp:164-178
     if (t % chunk == 0) sgd_batches_dev_launch(c->seed, c->substream, n, bs, &ctl->iters, chunk, idxbuf, &ctl->stop, s);
     cudaEvent_t* pe = prof_begin(ctx, s);
     sgd_slab_launch(sa, s);
     if (pe) GPK_CUDA(cudaEventRecord(*pe, s));
-    sgd_reduce_launch(ta, s);
-    allreduce_inplace(op, gbuf, static_cast<size_t>(bs) * m + m + 1);
-    sgd_apply_launch(ta, s);
+    if (fused_finish) {
+      sgd_finish_launch(tf, s);
+    } else {
+      sgd_reduce_launch(ta, s);
+      allreduce_inplace(op, gbuf, static_cast<size_t>(bs) * m + m + 1);
+      sgd_apply_launch(ta, s);
+    }
     ++t;
   };
   drive(b, ctl, chunk, budget, iteration, true);

@@ -279,6 +279,8 @@ void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s);
 void sgd_gram_image_launch(const float* xs, int rows, int n, int d, int dp, float* xg, cudaStream_t s);
 void sgd_soa_image_launch(const float* xs, int rows, int dp, float* out, cudaStream_t s);
 void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s);
+void sgd_finish_launch(const SgdStepArgs& a, cudaStream_t s);  // single rank: reduce + apply fused
+int sgd_finish_blocks(int b);
 void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
                              cudaStream_t s);
 void sgd_materialise_launch(double* Vb, const double* Mb, const int* tau, const double* s64, int budget,

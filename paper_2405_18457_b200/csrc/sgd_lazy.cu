@@ -1182,6 +1182,137 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
   }
 }
 
+// Single rank: the reduce and apply kernels fused (one launch per iteration
+// fewer, no g round trip). Block = FIN_ROWS minibatch rows x m columns x 4
+// lanes; the quad of an element sums the split partials s = lane, lane + 4,
+// ... and combines (s0 + s1) + (s2 + s3) as sgd_reduce_kernel; lane 0 then
+// applies the row's lazy update exactly as sgd_apply_kernel, keeping the old
+// residual square for the incremental norms. The last block sums the block
+// partials of g^2 and of the old squares in block order and takes the
+// termination / divergence decision (solvers.cpp:164-178).
+constexpr int FIN_ROWS = 2;
+__global__ void sgd_finish_kernel(SgdStepArgs a) {
+  if (a.ctl->stop) return;
+  const int t = a.ctl->iters;
+  const int* idx = a.idxbuf + static_cast<size_t>(t % a.idx_chunk) * a.b;
+  const int m = a.m, bm = a.b * m;
+  __shared__ double gs[FIN_ROWS][80], os[FIN_ROWS][80];
+  __shared__ int bad_g, bad_row;
+  __shared__ unsigned last;
+  if (threadIdx.x == 0) bad_g = bad_row = 0;
+  __syncthreads();
+  const int quad = threadIdx.x & 3, e_loc = threadIdx.x >> 2;  // blockDim.x = 4 FIN_ROWS m (rounded to 32)
+  const int rl = e_loc / m, j = e_loc - rl * m;
+  const int q = blockIdx.x * FIN_ROWS + rl;
+  const bool act = rl < FIN_ROWS && q < a.b;
+  double g = 0.0;
+  if (act) {
+    const int e = q * m + j;
+#pragma unroll 4
+    for (int sp = quad; sp < a.splits; sp += 4) g += a.part[static_cast<size_t>(sp) * bm + e];
+  }
+  g += __shfl_xor_sync(0xffffffffu, g, 1);
+  g += __shfl_xor_sync(0xffffffffu, g, 2);
+  double g2 = 0.0, o2 = 0.0;
+  int li = -1;
+  if (act && quad == 0) {
+    li = idx[q];
+    const size_t o = static_cast<size_t>(li) * m + j;
+    const int dl = min(max(t - a.tau[li] - 1, 0), a.budget);
+    const double mb = a.Mb[o];
+    const double vt = fma(a.s64[dl], mb, a.Vb[o]);  // V(t)
+    g = fma(a.sigma2, vt, g) - a.B[o];
+    if (!isfinite(g)) bad_g = 1;
+    g2 = g * g;
+    const double old = a.resid[o];
+    o2 = old * old;
+    const double mt = a.p64[dl] * mb;  // M(t)
+    const double mn = __dsub_rn(__dmul_rn(mt, a.rho), __dmul_rn(a.step, g));
+    const double vn = __dadd_rn(vt, mn);
+    if (!isfinite(vn) || !isfinite(mn)) bad_row = 1;
+    a.Mb[o] = mn;
+    a.Vb[o] = vn;
+    a.resid[o] = -g;
+    const size_t ro = static_cast<size_t>(li / 32) * a.rw + sgd_record_pos(li % 32, j);
+    a.rec[ro] = static_cast<float>(vn);
+    a.rec[ro + a.moff] = static_cast<float>(mn);
+  }
+  if (quad == 0 && rl < FIN_ROWS) {
+    gs[rl][j] = g2;
+    os[rl][j] = o2;
+  }
+  __syncthreads();  // every thread of the block has read tau of its row
+  if (act && quad == 0 && j == 0) a.tau[li] = t;
+  if (threadIdx.x < m) {  // block partials, rows in order
+    double sg = 0.0, so = 0.0;
+#pragma unroll
+    for (int r = 0; r < FIN_ROWS; ++r) {
+      sg += gs[r][threadIdx.x];
+      so += os[r][threadIdx.x];
+    }
+    a.gpart[static_cast<size_t>(blockIdx.x) * 2 * m + threadIdx.x] = sg;
+    a.gpart[static_cast<size_t>(blockIdx.x) * 2 * m + m + threadIdx.x] = so;
+  }
+  if (threadIdx.x == 0 && (bad_g || bad_row)) atomicOr(a.nonfinite_now, bad_g ? 3 : 1);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double ss[128];
+  __shared__ double red8[8][2][80];
+  {  // column sums of the block partials: thread (jj, k) sums blocks k, k + 8, ... then 8 partials in order
+    for (int w = threadIdx.x; w < 8 * m; w += blockDim.x) {
+      const int jj = w % m, k = w / m;
+      double sg = 0.0, so = 0.0;
+#pragma unroll 8
+      for (int b = k; b < static_cast<int>(gridDim.x); b += 8) {  // loads issued ahead, adds in block order
+        sg += __ldcg(a.gpart + static_cast<size_t>(b) * 2 * m + jj);
+        so += __ldcg(a.gpart + static_cast<size_t>(b) * 2 * m + m + jj);
+      }
+      red8[k][0][jj] = sg;
+      red8[k][1][jj] = so;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < m) {
+    const int jj = threadIdx.x;
+    double sg = 0.0, so = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sg += red8[k][0][jj];
+      so += red8[k][1][jj];
+    }
+    const double v = a.sumsq[jj] + (sg - so);
+    a.sumsq[jj] = v;
+    ss[jj] = fmax(v, 0.0);
+  }
+  __syncthreads();
+  const int now = *a.nonfinite_now;
+  if (threadIdx.x == 0) {
+    *a.ticket = 0u;
+    if (now) *a.nonfinite = 1;
+  }
+  if (threadIdx.x < 32) {  // termination_check on the tracked residuals (linear_system.cpp:47-53)
+    double probe = 0.0;
+    for (int jj = 1 + threadIdx.x; jj < m; jj += 32) probe += sqrt(ss[jj]) / a.scales[jj];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) probe += __shfl_xor_sync(0xffffffffu, probe, o);
+    if (threadIdx.x == 0) {
+      const double mean = sqrt(ss[0]) / a.scales[0];
+      probe = m > 1 ? probe / (m - 1) : 0.0;
+      CgCtl* c = a.ctl;
+      c->iters += 1;
+      c->mean_norm = mean;
+      c->probe_norm = probe;
+      c->done = mean <= a.tol && probe <= a.tol;
+      c->aborted = now ? 1 : 0;
+      c->stop = (c->done || c->aborted || c->iters >= c->budget) ? 1 : 0;
+    }
+  }
+}
+
 // Gram column image for the SGD slab: (-2 x, |x|^2 at slot d, 0...) of the
 // scaled FP32 inputs (rows beyond n zero), |x|^2 by the same FP32 chain the
 // kernel uses for its rows
@@ -1283,6 +1414,14 @@ void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s) {
   sgd_apply_kernel<<<(a.b + APPLY_ROWS - 1) / APPLY_ROWS, threads, 0, s>>>(a);
   check_launch("sgd_apply");
 }
+
+void sgd_finish_launch(const SgdStepArgs& a, cudaStream_t s) {
+  if (a.m > 80) throw std::invalid_argument("gpk: SGD finish supports m <= 80");
+  const int threads = ((4 * FIN_ROWS * a.m + 31) / 32) * 32;
+  sgd_finish_kernel<<<(a.b + FIN_ROWS - 1) / FIN_ROWS, threads, 0, s>>>(a);
+  check_launch("sgd_finish");
+}
+int sgd_finish_blocks(int b) { return (b + FIN_ROWS - 1) / FIN_ROWS; }
 
 void sgd_records_init_launch(const double* V, int nloc, int rows_pad, int m, int rw, int moff, float* rec, int* tau,
                              cudaStream_t s) {
