@@ -83,16 +83,17 @@ bool dense_dgemm() {
   return on;
 }
 
-// Tensor-core Gram distances for d >= GPK_TGRAM_MIN_D (default 16; measured
-// on one B200 with the warp-converged MMA issue: full products at d = 26
-// -21%, d = 20 -15%, d = 11 +2%, d = 3 +16%);
+// Tensor-core Gram distances for d >= GPK_TGRAM_MIN_D (default 9; measured
+// on one B200 with the warp-uniform MMA issue, full products: d = 11 -16%,
+// d = 13 -24% (C5's product 145 -> 122 ms at n = 262144), d = 20/26 on by
+// then already; round 1 with per-MMA elect issue: d = 11 +2%, d = 3 +16%);
 // GPK_TGRAM=0 keeps the FP32 distance loops everywhere.
 bool tg_enabled(int d) {
   static const int min_d = [] {
     const char* e = std::getenv("GPK_TGRAM");
     if (e && std::atoi(e) == 0) return 1 << 30;
     const char* m = std::getenv("GPK_TGRAM_MIN_D");
-    return m ? std::atoi(m) : 16;
+    return m ? std::atoi(m) : 9;
   }();
   return d >= min_d && d <= 32;
 }
