@@ -476,6 +476,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) sgd_slab_kernel(const SgdSlabArgs
 #ifndef SGD_PROF
 #define SGD_PROF 0
 #endif
+#ifndef SGD_FAKE_DIST
+#define SGD_FAKE_DIST 0
+#endif
+#ifndef SGD_FAKE_MUFU
+#define SGD_FAKE_MUFU 0
+#endif
+#ifndef SGD_FAKE_HALFREC
+#define SGD_FAKE_HALFREC 0
+#endif
 #if SGD_PROF
 __device__ unsigned long long g_sgd_prof[16];
 #define PROF_T0 prof_t0 = clock64()
@@ -581,6 +590,9 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   for (int e = tid; e < a.ntab; e += NTHREADS) stab[e] = __ldg(a.s32 + e);
+#if SGD_FAKE_HALFREC
+  for (int e = tid; e < ST * st_floats; e += NTHREADS) smS[e] = 0.f;
+#endif
   // zero j-groups (>= JG) of every B image: written once, never rebuilt
   for (int sb = 0; sb < SB; ++sb)
     for (int f = tid; f < 4 * IMG; f += NTHREADS)
@@ -604,7 +616,11 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
   if (warp == PROD_WARP) {
     // ---------------- producer ----------------
     if (lane == 0) {
+#if SGD_FAKE_HALFREC  // timing experiment only (wrong results): half of each chunk's record bytes
+      const uint32_t rec_bytes = rw * 4u, x_bytes = 2 * 32 * DP * 4u;
+#else
       const uint32_t rec_bytes = 2 * rw * 4u, x_bytes = 2 * 32 * DP * 4u;
+#endif
       for (int k = 0; k < nk; ++k) {
         const int s = k % ST;
         PROF_T0;
@@ -658,24 +674,37 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
         float4* bh = bbase + h * (IMG / 4);
         float4* bl = bbase + (2 + h) * (IMG / 4);
         const float2 s01 = make_float2(sc.x, sc.y), s23 = make_float2(sc.z, sc.w);
-        const float4* m4b = m4;
-#pragma unroll 5
-        for (int f = bt; f < live; f += 32 * BW) {
-          // V(t) in packed FP32x2; hi = V(t) truncated to TF32 (one LOP per
-          // element: the builders are the slab's critical path), lo = V(t) - hi
-          // exactly (the tensor core reads its top 11 bits)
-          const float4 vv = v4[f], mm = m4b[f];
-          const float2 v01 = __ffma2_rn(s01, make_float2(mm.x, mm.y), make_float2(vv.x, vv.y));
-          const float2 v23 = __ffma2_rn(s23, make_float2(mm.z, mm.w), make_float2(vv.z, vv.w));
-          float4 h;
-          h.x = __uint_as_float(__float_as_uint(v01.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(v01.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(v23.x) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(v23.y) & 0xFFFFE000u);
-          const float2 l01 = __fadd2_rn(v01, make_float2(-h.x, -h.y));
-          const float2 l23 = __fadd2_rn(v23, make_float2(-h.z, -h.w));
-          bh[f] = h;
-          bl[f] = make_float4(l01.x, l01.y, l23.x, l23.y);
+        // all of this half's loads first (independent registers), then the
+        // arithmetic and the stores: the loop-carried register reuse of the
+        // rolled loop serialised one shared-memory round trip per float4
+        constexpr int MAXI = (NPAD * 8 + 32 * BW - 1) / (32 * BW);  // float4s per thread per half, at most
+        float4 vv[MAXI], mm[MAXI];
+#pragma unroll
+        for (int i = 0; i < MAXI; ++i) {
+          const int f = bt + i * 32 * BW;
+          if (f < live) {
+            vv[i] = v4[f];
+            mm[i] = m4[f];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < MAXI; ++i) {
+          const int f = bt + i * 32 * BW;
+          if (f < live) {
+            // V(t) in packed FP32x2; hi = V(t) truncated to TF32 (one LOP per
+            // element), lo = V(t) - hi exactly (the tensor core reads its top 11 bits)
+            const float2 v01 = __ffma2_rn(s01, make_float2(mm[i].x, mm[i].y), make_float2(vv[i].x, vv[i].y));
+            const float2 v23 = __ffma2_rn(s23, make_float2(mm[i].z, mm[i].w), make_float2(vv[i].z, vv[i].w));
+            float4 h;
+            h.x = __uint_as_float(__float_as_uint(v01.x) & 0xFFFFE000u);
+            h.y = __uint_as_float(__float_as_uint(v01.y) & 0xFFFFE000u);
+            h.z = __uint_as_float(__float_as_uint(v23.x) & 0xFFFFE000u);
+            h.w = __uint_as_float(__float_as_uint(v23.y) & 0xFFFFE000u);
+            const float2 l01 = __fadd2_rn(v01, make_float2(-h.x, -h.y));
+            const float2 l23 = __fadd2_rn(v23, make_float2(-h.z, -h.w));
+            bh[f] = h;
+            bl[f] = make_float4(l01.x, l01.y, l23.x, l23.y);
+          }
         }
       }
       fence_proxy_async();
@@ -838,6 +867,9 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
 #pragma unroll
       for (int t = 0; t < 8; t += 2) {
         uint64_t r2;
+#if SGD_FAKE_DIST  // timing experiment only (wrong results): no distance work
+        r2 = xik2[0] ^ static_cast<uint64_t>(t);
+#else
 #pragma unroll
         for (int q = 0; q < DX; ++q) {
           uint64_t cc, dd;
@@ -848,18 +880,23 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
           else
             asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(r2) : "l"(dd));
         }
+#endif
         float ra, rb;
         asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r2));
+#if !SGD_FAKE_MUFU
         ra = sqrt_approx(ra);
         rb = sqrt_approx(rb);
+#endif
         uint64_t rr, tt, uu, ee, kk;
         asm("mov.b64 %0, {%1, %2};" : "=l"(rr) : "f"(ra), "f"(rb));
         asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(tt) : "l"(rr), "l"(k_s3), "l"(k_one));
         asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(uu) : "l"(rr), "l"(k_c), "l"(k_l2s2));
         float ua, ub;
         asm("mov.b64 {%0, %1}, %2;" : "=f"(ua), "=f"(ub) : "l"(uu));
+#if !SGD_FAKE_MUFU
         ua = ex2_approx(ua);
         ub = ex2_approx(ub);
+#endif
         asm("mov.b64 %0, {%1, %2};" : "=l"(ee) : "f"(ua), "f"(ub));
         asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(kk) : "l"(tt), "l"(ee));
         float ka, kb;
@@ -960,15 +997,15 @@ void launch_64_t(const SgdSlabArgs& a, cudaStream_t s) {
 }
 template <int NPAD, int DX>
 void launch_64(const SgdSlabArgs& a, cudaStream_t s) {
-  // B-builder warps: 8 (measured at C4: 230 vs 240 us per launch with 4;
-  // the builders' smem round trips queue behind the evaluation warps' MUFU
-  // work, so more of them in flight); GPK_SGD_BW=4 selects four
+  // B-builder warps: 4 (measured at C4 with the loads-first builders: 223 us
+  // per launch vs 236 with 8, whose 72-register cap spills in the evaluation
+  // warps); GPK_SGD_BW=8 selects eight
   static const int bw = [] {
     const char* e = std::getenv("GPK_SGD_BW");
-    return e ? std::atoi(e) : 8;
+    return e ? std::atoi(e) : 4;
   }();
-  if (bw == 4) return launch_64_t<NPAD, DX, 4>(a, s);
-  return launch_64_t<NPAD, DX, 8>(a, s);
+  if (bw == 8) return launch_64_t<NPAD, DX, 8>(a, s);
+  return launch_64_t<NPAD, DX, 4>(a, s);
 }
 
 template <int NPAD, int DP4, bool GRAM, int DX = 0>

@@ -14,7 +14,8 @@ from paper_2405_18457_b200 import _lib  # noqa: E402
 NAMES = ["prod st_empty", "build st_full", "build b_empty", "build bar.sync", "mma b_full", "mma d_empty",
          "mma a_full", "eval d_full", "eval st_full", "eval a_empty", "prod total", "build total", "mma total",
          "eval total", "build build"]
-WARPS = {0: 1, 1: 4, 2: 4, 3: 4, 4: 1, 5: 1, 6: 1, 7: 16, 8: 16, 9: 16, 10: 1, 11: 4, 12: 1, 13: 16, 14: 4}
+BW = int(os.environ.get("GPK_SGD_BW", "8"))
+WARPS = {0: 1, 1: BW, 2: BW, 3: BW, 4: 1, 5: 1, 6: 1, 7: 16, 8: 16, 9: 16, 10: 1, 11: BW, 12: 1, 13: 16, 14: BW}
 
 
 def main():
@@ -28,7 +29,7 @@ def main():
     f = lib.gpk_debug_sgd_prof
     f.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
     buf = (C.c_ulonglong * 16)()
-    cfg = G.SolverConfig(kind=2, tolerance=1e-9, max_epochs=1, batch_size=b, learning_rate=10.0, momentum=0.9, seed=4)
+    cfg = G.SolverConfig(kind=2, tolerance=1e-9, max_epochs=1, batch_size=b, learning_rate=float(os.environ.get("SGD_LR", "10")), momentum=0.9, seed=4)
     G.solve_sgd(G.LinearSystemBatch(op, T), cfg)
     f(buf, 1)
     G.solve_sgd(G.LinearSystemBatch(op, T), cfg)

@@ -25,7 +25,7 @@ def main():
     op = G.KernelOperator(X, G.Hyperparameters.from_raw(raw), ctx)
     rng = np.random.default_rng(0)
     T = np.asfortranarray(rng.standard_normal((n, m)))
-    cfg = G.SolverConfig(kind=2, tolerance=1e-9, max_epochs=epochs, batch_size=b, learning_rate=10.0, momentum=0.9,
+    cfg = G.SolverConfig(kind=2, tolerance=1e-9, max_epochs=epochs, batch_size=b, learning_rate=float(os.environ.get("SGD_LR", "10")), momentum=0.9,
                          seed=4)
     # warm-up solve (allocations, module load)
     G.solve_sgd(G.LinearSystemBatch(op, T), G.SolverConfig(kind=2, tolerance=1e-9, max_epochs=1, batch_size=b,
