@@ -1220,14 +1220,15 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
 }
 
 // Single rank: the reduce and apply kernels fused (one launch per iteration
-// fewer, no g round trip). Block = FIN_ROWS minibatch rows x m columns x 4
-// lanes; the quad of an element sums the split partials s = lane, lane + 4,
-// ... and combines (s0 + s1) + (s2 + s3) as sgd_reduce_kernel; lane 0 then
-// applies the row's lazy update exactly as sgd_apply_kernel, keeping the old
-// residual square for the incremental norms. The last block sums the block
-// partials of g^2 and of the old squares in block order and takes the
-// termination / divergence decision (solvers.cpp:164-178).
-constexpr int FIN_ROWS = 2;
+// fewer, no g round trip). Block = FIN_ROWS minibatch rows x m columns; the
+// thread of an element sums the split partials in four interleaved chains
+// s = c, c + 4, ... and combines (s0 + s1) + (s2 + s3) (sgd_reduce_kernel's
+// order), then applies the row's lazy update exactly as sgd_apply_kernel,
+// keeping the old residual square for the incremental norms. The last of the
+// b / FIN_ROWS = 64 blocks sums the block partials of g^2 and of the old
+// squares in block order and takes the termination / divergence decision
+// (solvers.cpp:164-178).
+constexpr int FIN_ROWS = 8;
 __global__ void sgd_finish_kernel(SgdStepArgs a) {
   if (a.ctl->stop) return;
   const int t = a.ctl->iters;
@@ -1238,21 +1239,24 @@ __global__ void sgd_finish_kernel(SgdStepArgs a) {
   __shared__ unsigned last;
   if (threadIdx.x == 0) bad_g = bad_row = 0;
   __syncthreads();
-  const int quad = threadIdx.x & 3, e_loc = threadIdx.x >> 2;  // blockDim.x = 4 FIN_ROWS m (rounded to 32)
-  const int rl = e_loc / m, j = e_loc - rl * m;
+  const int rl = threadIdx.x / m, j = threadIdx.x - rl * m;  // blockDim.x = FIN_ROWS m (rounded to 32)
   const int q = blockIdx.x * FIN_ROWS + rl;
   const bool act = rl < FIN_ROWS && q < a.b;
   double g = 0.0;
   if (act) {
     const int e = q * m + j;
-#pragma unroll 4
-    for (int sp = quad; sp < a.splits; sp += 4) g += a.part[static_cast<size_t>(sp) * bm + e];
+    double c4[4] = {0.0, 0.0, 0.0, 0.0};
+    int sp = 0;
+    for (; sp + 4 <= a.splits; sp += 4) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) c4[c] += __ldcg(a.part + static_cast<size_t>(sp + c) * bm + e);
+    }
+    for (int c = 0; sp + c < a.splits; ++c) c4[c] += __ldcg(a.part + static_cast<size_t>(sp + c) * bm + e);
+    g = (c4[0] + c4[1]) + (c4[2] + c4[3]);
   }
-  g += __shfl_xor_sync(0xffffffffu, g, 1);
-  g += __shfl_xor_sync(0xffffffffu, g, 2);
   double g2 = 0.0, o2 = 0.0;
   int li = -1;
-  if (act && quad == 0) {
+  if (act) {
     li = idx[q];
     const size_t o = static_cast<size_t>(li) * m + j;
     const int dl = min(max(t - a.tau[li] - 1, 0), a.budget);
@@ -1274,12 +1278,12 @@ __global__ void sgd_finish_kernel(SgdStepArgs a) {
     a.rec[ro] = static_cast<float>(vn);
     a.rec[ro + a.moff] = static_cast<float>(mn);
   }
-  if (quad == 0 && rl < FIN_ROWS) {
+  if (rl < FIN_ROWS) {
     gs[rl][j] = g2;
     os[rl][j] = o2;
   }
   __syncthreads();  // every thread of the block has read tau of its row
-  if (act && quad == 0 && j == 0) a.tau[li] = t;
+  if (act && j == 0) a.tau[li] = t;
   if (threadIdx.x < m) {  // block partials, rows in order
     double sg = 0.0, so = 0.0;
 #pragma unroll
@@ -1454,7 +1458,7 @@ void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s) {
 
 void sgd_finish_launch(const SgdStepArgs& a, cudaStream_t s) {
   if (a.m > 80) throw std::invalid_argument("gpk: SGD finish supports m <= 80");
-  const int threads = ((4 * FIN_ROWS * a.m + 31) / 32) * 32;
+  const int threads = ((FIN_ROWS * a.m + 31) / 32) * 32;
   sgd_finish_kernel<<<(a.b + FIN_ROWS - 1) / FIN_ROWS, threads, 0, s>>>(a);
   check_launch("sgd_finish");
 }
