@@ -221,6 +221,7 @@ struct gpk_operator {
   int n = 0, d = 0, dp = 0;
   DBuf<double> x64;       // [n][d] unscaled
   DBuf<float> xs32;       // [n][dp]
+  DBuf<float> gpk_xsoa;   // gradient pass, d <= 4: SoA image of xs32 per 32-row chunk
   int dpg = 0;            // Gram image width (gram_dp(d)); 0: direct-difference operator
   bool tg = false;        // tensor-core Gram distances in the tcgen05 operator (tg_enabled)
   DBuf<float> xtg;        // their column images (tg_image_launch), rebuilt with the scaled inputs
@@ -2200,6 +2201,16 @@ std::vector<std::vector<double>> quad_forms_dev(gpk_operator* op, const std::vec
     t.cw = comb ? static_cast<float>(combine[pw]) : 0.f;
     t.cn = comb ? static_cast<float>(combine[pn]) : 0.f;
     t.blocks = op->ctx->sms;
+    static const bool grad_dx = [] {  // GPK_GRAD_DX=0: padded-dimension evaluation at d <= 4
+      const char* e = std::getenv("GPK_GRAD_DX");
+      return !(e && std::atoi(e) == 0);
+    }();
+    if (grad_dx && op->dp == 4) {  // SoA column coordinates for the exact-dimension path
+      const size_t rows = static_cast<size_t>(rows_pad);
+      float* xq = op->gpk_xsoa.ensure(rows * 4);
+      sgd_soa_image_launch(op->xs32.p, rows_pad, 4, xq, s);
+      t.xsoa = xq;
+    }
     const long long ntiles = grad_tc_tiles(n, a.symmetric);
     t.tile_begin = ntiles * rk / nr;
     t.tile_end = ntiles * (rk + 1) / nr;

@@ -208,6 +208,7 @@ struct GradTcArgs {
   double* part;         // [blocks][npairs*(d+1)]
   int blocks;
   long long tile_begin, tile_end;  // 128 x 128 tiles of this rank
+  const float* xsoa;    // d <= 4: column coordinates per 32-row chunk in SoA order (nullptr: AoS xs)
 };
 int grad_tc_kp(int cols);
 int grad_tc_rows_pad(int n);
@@ -277,7 +278,7 @@ int sgd_record_width(int m, int* moff);
 void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s);
 void sgd_reduce_launch(const SgdStepArgs& a, cudaStream_t s);
 void sgd_gram_image_launch(const float* xs, int rows, int n, int d, int dp, float* xg, cudaStream_t s);
-void sgd_soa_image_launch(const float* xs, int rows, int dp, float* out, cudaStream_t s);
+void sgd_soa_image_launch(const float* xs, int rows, int dp, float* out, cudaStream_t s);  // [rows/32][dp][32]
 void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s);
 void sgd_finish_launch(const SgdStepArgs& a, cudaStream_t s);  // single rank: reduce + apply fused
 int sgd_finish_blocks(int b);

@@ -134,7 +134,12 @@ __device__ __forceinline__ void butterfly_flush(const float (&v)[NV], int lane, 
 
 // COMB (with NARROW): the estimator's combination cw G + cn u w^T is formed
 // per entry and accumulated once (one set of d + 1 sums instead of two).
-template <int DP4, bool NARROW, bool COMB>
+// DX > 0 (d = DX <= 4): the column coordinates come as SoA pairs (the
+// operator's xsoa image) and every FP32x2 instruction evaluates two columns
+// (distances, kernel profile, lengthscale sums) instead of two padded
+// dimensions of one column -- about half the FMA-pipe work per entry, which
+// bounds this pass at small d.
+template <int DP4, bool NARROW, bool COMB, int DX = 0>
 __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const GradTcArgs a) {
   constexpr int EVAL_WARPS = GradRoles<DP4>::EW, NTHREADS = GradRoles<DP4>::NT, CW = GradRoles<DP4>::CW;
   constexpr int DP = 4 * DP4;
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
         const int col0 = tcol * TBM + (k & 1) * CN;
         mbar_expect_tx(&full[s], bbytes + xbytes + wbytes);
         bulk_g2s(smB + s * NPIECE * img, a.bpk + static_cast<size_t>(col0 / CN) * NPIECE * img, bbytes, &full[s]);
-        bulk_g2s(smX + s * CN * DP, a.xs + static_cast<size_t>(col0) * DP, xbytes, &full[s]);
+        bulk_g2s(smX + s * CN * DP, (DX > 0 ? a.xsoa : a.xs) + static_cast<size_t>(col0) * DP, xbytes, &full[s]);
         if (NARROW) bulk_g2s(smW + s * CN, a.w1 + col0, wbytes, &full[s]);
       }
     }
@@ -258,6 +263,12 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
     float u1i = 0.f;
     uint64_t lw[DP / 2], ln[(NARROW && !COMB) ? DP / 2 : 1];
     float sw = 0.f, sn = 0.f;
+    // DX path: per-dimension sums as (even, odd column) pairs, and the row's
+    // coordinates duplicated into pairs
+    constexpr int NX = DX > 0 ? DX : 1;
+    uint64_t lwp[NX], lnp[NX], swp = 0ull, snp = 0ull, xik2[NX];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) lwp[k] = lnp[k] = xik2[k] = 0ull;
 #pragma unroll
     for (int k = 0; k < DP / 2; ++k) lw[k] = 0ull;
 #pragma unroll
@@ -301,6 +312,12 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
           asm("mov.b64 %0, {%1, %2};" : "=l"(xi2[2 * u + 1]) : "f"(v.z), "f"(v.w));
         }
         if (NARROW) u1i = __ldg(a.u1 + i);
+        if constexpr (DX > 0) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(a.xs + static_cast<size_t>(i) * DP));
+          const float xe[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int k = 0; k < DX; ++k) asm("mov.b64 %0, {%1, %1};" : "=l"(xik2[k]) : "f"(xe[k]));
+        }
       }
       mbar_wait(&full[s], (k / STAGES) & 1);
       mbar_wait(&d_full[b], (k / 2) & 1);
@@ -316,6 +333,61 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&d_empty[b]);
+        }
+        if constexpr (DX > 0) {
+          const int cc0 = half * CW + q * 8;  // first chunk column of this group of 8
+          const uint32_t xg = smem_u32(smX + s * CN * DP + (cc0 >> 5) * DP * 32 + (cc0 & 31));
+          uint64_t k_s3, k_one, k_c;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(k_s3) : "f"(kSqrt3f));
+          asm("mov.b64 %0, {%1, %1};" : "=l"(k_one) : "f"(1.f));
+          asm("mov.b64 %0, {%1, %1};" : "=l"(k_c) : "f"(kNegSqrt3Log2e));
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            uint64_t sqv[DX], r2 = 0ull;
+#pragma unroll
+            for (int qd = 0; qd < DX; ++qd) {
+              uint64_t cc, dd;
+              asm volatile("ld.shared.b64 %0, [%1];" : "=l"(cc) : "r"(xg + (qd * 32 + e) * 4));
+              asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dd) : "l"(cc), "l"(xik2[qd]));
+              asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(sqv[qd]) : "l"(dd));
+              if (qd == 0)
+                r2 = sqv[0];
+              else
+                asm("add.rn.f32x2 %0, %0, %1;" : "+l"(r2) : "l"(sqv[qd]));
+            }
+            float ra, rb;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r2));
+            ra = sqrt_approx(ra);
+            rb = sqrt_approx(rb);
+            uint64_t rr, uu, ee, kv2, gw2, cw2;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(rr) : "f"(ra), "f"(rb));
+            asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(uu) : "l"(rr), "l"(k_c));
+            float ua, ub;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(ua), "=f"(ub) : "l"(uu));
+            ua = ex2_approx(ua);  // exp(-sqrt3 r)
+            ub = ex2_approx(ub);
+            asm("mov.b64 %0, {%1, %2};" : "=l"(ee) : "f"(ua), "f"(ub));
+            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(kv2) : "l"(rr), "l"(k_s3), "l"(k_one));
+            asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(kv2) : "l"(kv2), "l"(ee));  // k / s^2
+            const float ga = __uint_as_float(g[e]), gb = __uint_as_float(g[e + 1]);
+            const float gwa = COMB ? fmaf(a.cn, u1i * wc[q * 8 + e], a.cw * ga) : ga;
+            const float gwb = COMB ? fmaf(a.cn, u1i * wc[q * 8 + e + 1], a.cw * gb) : gb;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(gw2) : "f"(gwa), "f"(gwb));
+            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(swp) : "l"(kv2), "l"(gw2));
+            asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(cw2) : "l"(ee), "l"(gw2));
+#pragma unroll
+            for (int qd = 0; qd < DX; ++qd) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(lwp[qd]) : "l"(sqv[qd]), "l"(cw2));
+            if constexpr (NARROW && !COMB) {
+              uint64_t gn2, cn2;
+              asm("mov.b64 %0, {%1, %2};" : "=l"(gn2) : "f"(u1i * wc[q * 8 + e]), "f"(u1i * wc[q * 8 + e + 1]));
+              asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(snp) : "l"(kv2), "l"(gn2));
+              asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(cn2) : "l"(ee), "l"(gn2));
+#pragma unroll
+              for (int qd = 0; qd < DX; ++qd)
+                asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(lnp[qd]) : "l"(sqv[qd]), "l"(cn2));
+            }
+          }
+          continue;
         }
 #pragma unroll(DP4 <= 2 ? 8 : 2)
         for (int e = 0; e < 8; ++e) {
@@ -365,6 +437,22 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
         float v[NV];
 #pragma unroll
         for (int t = 0; t < NV; ++t) v[t] = 0.f;
+        if constexpr (DX > 0) {  // (even, odd) column pairs -> one sum each
+          auto fold = [](uint64_t& p) {
+            float x, y;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(p));
+            p = 0ull;
+            return x + y;
+          };
+#pragma unroll
+          for (int qd = 0; qd < DX; ++qd) v[qd] = fold(lwp[qd]);
+          v[DP] = fold(swp);
+          if constexpr (NARROW && !COMB) {
+#pragma unroll
+            for (int qd = 0; qd < DX; ++qd) v[DP + 1 + qd] = fold(lnp[qd]);
+            v[2 * DP + 1] = fold(snp);
+          }
+        } else {
 #pragma unroll
         for (int t = 0; t < DP / 2; ++t) {
           asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2 * t]), "=f"(v[2 * t + 1]) : "l"(lw[t]));
@@ -380,6 +468,7 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
           }
           v[2 * DP + 1] = sn;
           sn = 0.f;
+        }
         }
         const double weight = (a.symmetric && tcol != ti) ? 2.0 : 1.0;
         butterfly_flush<NV>(v, lane, wacc + warp * NV, NUSED, weight);
@@ -431,7 +520,7 @@ __global__ void grad_tc_pack_kernel(const float* w32, int ld, int n, int cols, i
   }
 }
 
-template <int DP4, bool NARROW, bool COMB>
+template <int DP4, bool NARROW, bool COMB, int DX = 0>
 void launch_one(const GradTcArgs& a, cudaStream_t s) {
   constexpr int DP = 4 * DP4;
   constexpr int NPR = (NARROW && !COMB) ? 2 : 1;
@@ -444,22 +533,35 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
       120 * 1024);
   static size_t configured = 0;
   if (smem > configured) {
-    GPK_CUDA(cudaFuncSetAttribute(grad_tc_kernel<DP4, NARROW, COMB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GPK_CUDA(cudaFuncSetAttribute(grad_tc_kernel<DP4, NARROW, COMB, DX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = smem;
   }
-  grad_tc_kernel<DP4, NARROW, COMB><<<a.blocks, GradRoles<DP4>::NT, smem, s>>>(a);
+  grad_tc_kernel<DP4, NARROW, COMB, DX><<<a.blocks, GradRoles<DP4>::NT, smem, s>>>(a);
   check_launch("grad_tc_kernel");
 }
 
+template <int DP4, int DX = 0>
+void launch_dx(const GradTcArgs& a, cudaStream_t s) {
+  if (a.u1 && a.combined)
+    launch_one<DP4, true, true, DX>(a, s);
+  else if (a.u1)
+    launch_one<DP4, true, false, DX>(a, s);
+  else
+    launch_one<DP4, false, false, DX>(a, s);
+}
 template <int DP4>
 void launch_dp(const GradTcArgs& a, cudaStream_t s) {
-  if (a.u1 && a.combined)
-    launch_one<DP4, true, true>(a, s);
-  else if (a.u1)
-    launch_one<DP4, true, false>(a, s);
-  else
-    launch_one<DP4, false, false>(a, s);
+  if constexpr (DP4 == 1) {
+    if (a.xsoa) switch (a.d) {  // exact-dimension column-pair evaluation
+        case 1: return launch_dx<1, 1>(a, s);
+        case 2: return launch_dx<1, 2>(a, s);
+        case 3: return launch_dx<1, 3>(a, s);
+        case 4: return launch_dx<1, 4>(a, s);
+        default: break;
+      }
+  }
+  launch_dx<DP4>(a, s);
 }
 
 }  // namespace
