@@ -522,8 +522,11 @@ __host__ __device__ constexpr size_t smem_bytes(int rw, int dp, int ntab) {
 
 template <int NPAD, int DX, int NBW>
 __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(const SgdSlabArgs a) {
-  constexpr int CH = c64::CH, ST = c64::ST, SB = c64::SB, NAB = c64::NAB, A_COL0 = c64::A_COL0,
-                DEFER = c64::DEFER;
+  constexpr int CH = c64::CH, ST = c64::ST, SB = c64::SB, DEFER = c64::DEFER;
+  // TMEM: D double buffer at columns 0 / 80, then a ring of NS = 5 A slots of
+  // one 32-column half each (hi 32 | lo 32) from column 160: half j of the
+  // solve (chunk j / 2, half j % 2) uses slot j % 5
+  constexpr int NS = 5, A_COL0 = 160, D1 = 80;
   constexpr int BW = NBW, MMA_WARP = EW + 1 + NBW, NTHREADS = 32 * (MMA_WARP + 1);
   constexpr int IMG = NPAD * 32;  // floats of one 32-column TF32 image
   constexpr int DC = NPAD / 4;
@@ -538,9 +541,9 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
   uint64_t* st_empty = bars + ST;
   uint64_t* b_full = bars + 2 * ST;
   uint64_t* b_empty = b_full + SB;
-  uint64_t* a_full = b_empty + SB;       // [NAB][2]: one per 32-column half of the A buffer
-  uint64_t* a_empty = a_full + 2 * NAB;  // [NAB]
-  uint64_t* d_full = a_empty + NAB;
+  uint64_t* a_full = b_empty + SB;  // [NS]
+  uint64_t* a_empty = a_full + NS;  // [NS]
+  uint64_t* d_full = a_empty + NS;
   uint64_t* d_empty = d_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
   float* sS = reinterpret_cast<float*>(bars + 64);  // [SB][CH]
@@ -573,9 +576,8 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       mbar_init(&b_full[s], BW);
       mbar_init(&b_empty[s], 1);
     }
-    for (int b = 0; b < NAB; ++b) {
-      mbar_init(&a_full[2 * b], EW);
-      mbar_init(&a_full[2 * b + 1], EW);
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(&a_full[b], EW);
       mbar_init(&a_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -765,13 +767,13 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       PROF_T0;
       if (first && g >= 2) wait_u(dempty0 + 8 * (g & 1), ((g >> 1) - 1) & 1);
       PROF_ADD(5);
-      const uint32_t dt = tmem + ((g & 1) ? D_COL1 : 0);
+      const uint32_t dt = tmem + ((g & 1) ? D1 : 0);
       const uint32_t blo0 = (((smb0 + sb * 4 * IMG * 4) & 0x3FFFF) >> 4) | (8u << 16);  // LBO 128 B
-      const uint32_t ah = tmem + A_COL0 + ab * 128;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+        const uint32_t ah = tmem + A_COL0 + ab * 64;
         PROF_T0;
-        wait_u(afull0 + 8 * (2 * ab + h), aph);
+        wait_u(afull0 + 8 * ab, aph);
         PROF_ADD(6);
         tc_fence_after();
         if (elect_one()) {
@@ -780,21 +782,21 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
             const int kk = 4 * h + k4;
             const uint32_t bh = blo0 + ((h * IMG * 4 + k4 * 256) >> 4);
             const uint32_t bl = bh + ((2 * IMG * 4) >> 4);
-            mma(dt, ah + kk * 8, bh, (first && kk == 0) ? 0u : 1u);
-            mma(dt, ah + kk * 8, bl, 1u);
-            mma(dt, ah + 64 + kk * 8, bh, 1u);
+            mma(dt, ah + k4 * 8, bh, (first && kk == 0) ? 0u : 1u);
+            mma(dt, ah + k4 * 8, bl, 1u);
+            mma(dt, ah + 32 + k4 * 8, bh, 1u);
           }
+          commit(aempty0 + 8 * ab);  // the slot is free once these MMAs have read it
         }
         __syncwarp();
+        if (++ab == NS) { ab = 0; aph ^= 1; }
       }
       if (elect_one()) {
         commit(bempty0 + 8 * sb);
-        commit(aempty0 + 8 * ab);
         if (last) commit(dfull0 + 8 * (g & 1));
       }
       __syncwarp();
       if (++sb == SB) { sb = 0; bph ^= 1; }
-      if (++ab == NAB) { ab = 0; aph ^= 1; }
       if (++kf == F) { kf = 0; ++g; }
     }
   } else {
@@ -814,7 +816,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       mbar_wait(&d_full[g & 1], (g >> 1) & 1);
       PROF_ADD(7);
       tc_fence_after();
-      const uint32_t base = tmem + lane_addr + ((g & 1) ? D_COL1 : 0) + quarter * DC;
+      const uint32_t base = tmem + lane_addr + ((g & 1) ? D1 : 0) + quarter * DC;
 #pragma unroll
       for (int q = 0; q < DC / 4; ++q) {
         uint32_t v[4];
@@ -919,7 +921,24 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       if (lane == 0) arrive_u32(a_full0 + 8 * pend);
       pend = -1;
     };
-    int s = 0, sph = 0, ab = 0;
+    int s = 0, sph = 0;
+    int slot = 0, use = 0;  // the A slot of the next half and its use count
+    auto store_half = [&](const uint32_t (&hi)[8], const uint32_t (&lo)[8]) {
+      publish();  // the previous half
+      PROF_T0;
+      if (use > 0) wait_u32(a_empty0 + 8 * slot, (use - 1) & 1);  // the slot's previous half consumed
+      PROF_ADD(9);
+      tc_fence_after();
+      const uint32_t abase = acol + slot * 64;
+      tc_st8(abase, hi);
+      tc_st8(abase + 32, lo);
+      pend = slot;
+
+      if (++slot == NS) {
+        slot = 0;
+        ++use;
+      }
+    };
     for (int k = 0; k < nk; ++k) {
       PROF_T0;
       wait_u32(st_full0 + 8 * s, sph);
@@ -927,25 +946,12 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       const uint32_t xq = st_base + static_cast<uint32_t>(s * st_floats * 4) + xoff;
       uint32_t hi[8], lo[8];
       eval8(xq, hi, lo);
-      publish();  // previous chunk's second half
-      // buffer ab's previous use (chunk k - NAB) was use k / NAB - 1 of it
-      PROF_T0;
-      if (k >= NAB) wait_u32(a_empty0 + 8 * ab, ((k / NAB) - 1) & 1);
-      PROF_ADD(9);
-      tc_fence_after();
-      const uint32_t abase = acol + ab * 128;
-      tc_st8(abase, hi);
-      tc_st8(abase + 64, lo);
-      pend = 2 * ab;
+      store_half(hi, lo);
       eval8(xq + XHALF, hi, lo);
       __syncwarp();
       if (lane == 0) arrive_u32(st_empty0 + 8 * s);  // x_c consumed
-      publish();  // this chunk's first half
-      tc_st8(abase + 32, hi);
-      tc_st8(abase + 96, lo);
-      pend = 2 * ab + 1;
+      store_half(hi, lo);
       if (++s == ST) { s = 0; sph ^= 1; }
-      if (++ab == NAB) ab = 0;
       if (k == next_drain) {
         drain(drained++);
         next_drain += F;
