@@ -501,17 +501,15 @@ __device__ unsigned long long g_sgd_prof[16];
 // mbarrier waits / arrivals, TMEM-address and ring bookkeeping that made up
 // ~45% of the evaluation warps' instructions at 32 columns
 // (profiles/r02_sass_hot_sgd_slab_C4_v2_soa.txt). TMEM: D double buffer at
-// columns 0 / 96, two A buffers of 128 columns (hi 64 | lo 64) from 192.
-// Stages: staging ring 3 x (2 records + SoA x + tau), B ring 2 x (hi | lo of
-// two 32-column images); the B images' zero j-groups are written once.
+// columns 0 / 80, then a ring of five A slots of one 32-column half each
+// (hi 32 | lo 32). Stages: staging ring 3 x (2 records + SoA x + tau), B ring
+// 2 x (hi | lo of two 32-column images); the B images' zero j-groups are
+// written once.
 namespace c64 {
 constexpr int CH = 64;
 constexpr int ST = 3;
 constexpr int SB = 2;
-constexpr int NAB = 2;
-constexpr int A_COL0 = 192;
 constexpr int DEFER = 2;
-constexpr int CPT = 16;  // entries per evaluation thread per chunk
 
 template <int NPAD>
 __host__ __device__ constexpr size_t smem_bytes(int rw, int dp, int ntab) {
