@@ -1836,8 +1836,15 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
     return !(e && std::atoi(e) == 0);
   }();
   const bool ch64 = ch64_env && op->dp == 4;
+  // the 64-column slab as CTA pairs (cta_group::2, each CTA builds half of the
+  // B operand; GPK_SGD_PAIR=0: one CTA per row tile)
+  static const bool pair_env = [] {
+    const char* e = std::getenv("GPK_SGD_PAIR");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool pair = ch64 && pair_env && kv_tc_npad(m) % 16 == 0;
   const int cq = ch64 ? 64 : 32;
-  int splits = std::max(1, ctx->sms / tiles);
+  int splits = std::max(1, ctx->sms / (pair ? (tiles + 1) / 2 * 2 : tiles));
   int cps = (nloc + splits - 1) / splits;
   cps = (cps + cq - 1) / cq * cq;
   splits = std::max(1, (nloc + cps - 1) / cps);
@@ -1906,6 +1913,7 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   }();
   sa.flush = ch64 ? std::max(3, flush / 2) : flush;  // same FP32 accumulation span in 64-column chunks
   sa.ch64 = ch64 ? 1 : 0;
+  sa.pair = pair ? 1 : 0;
   sa.stats = ctx->stats;
   SgdStepArgs ta{};
   ta.ctl = ctl;

@@ -244,6 +244,7 @@ struct SgdSlabArgs {
   int m, splits, cols_per_split, flush;
   double* stats;
   int ch64;             // 64-column pipeline (d <= 4 with xsoa; cols_per_split a multiple of 64)
+  int pair;             // ch64 as CTA pairs (cta_group::2, M = 256; needs NPAD % 16 == 0)
 };
 struct SgdStepArgs {
   CgCtl* ctl;

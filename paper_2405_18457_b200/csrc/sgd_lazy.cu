@@ -505,33 +505,79 @@ __device__ unsigned long long g_sgd_prof[16];
 // (hi 32 | lo 32). Stages: staging ring 3 x (2 records + SoA x + tau), B ring
 // 2 x (hi | lo of two 32-column images); the B images' zero j-groups are
 // written once.
+// ---- CTA pairs (cta_group::2) ------------------------------------------------
+#ifndef SGD_PAIR_ACQ_CLUSTER
+#define SGD_PAIR_ACQ_CLUSTER 0
+#endif
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared-memory word in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// Arrive on a barrier of either CTA of the pair. CTA-scope release (the
+// default), as for a local arrive: the data it publishes -- TMEM stores
+// (completed by tcgen05.wait::st) and B images (fence.proxy.async) -- is read
+// by the pair's tensor core, not by a thread of the other CTA; a cluster-scope
+// release here made every evaluation warp ~1.8x slower (per-role profile).
+__device__ __forceinline__ void arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+
 namespace c64 {
 constexpr int CH = 64;
 constexpr int ST = 3;
 constexpr int SB = 2;
 constexpr int DEFER = 2;
 
-template <int NPAD>
-__host__ __device__ constexpr size_t smem_bytes(int rw, int dp, int ntab) {
-  return sizeof(float) * (SB * 4 * static_cast<size_t>(NPAD) * 32 + ST * (2 * static_cast<size_t>(rw) + 2 * 32 * dp + CH)) +
+// NB = B-image rows held by one CTA (NPAD, or NPAD / 2 in a CTA pair), rws =
+// staged floats of one 32-column record
+template <int NB>
+__host__ __device__ constexpr size_t smem_bytes(int rws, int dp, int ntab) {
+  return sizeof(float) * (SB * 4 * static_cast<size_t>(NB) * 32 + ST * (2 * static_cast<size_t>(rws) + 2 * 32 * dp + CH)) +
          64 * sizeof(uint64_t) + SB * CH * sizeof(float) + static_cast<size_t>(ntab) * sizeof(float);
 }
 }  // namespace c64
 
-template <int NPAD, int DX, int NBW>
+// PAIR: the two CTAs of a cluster (row tiles 2p, 2p + 1 of one column split)
+// run as one cta_group::2 MMA of M = 256: each keeps its own 128 rows of A in
+// its TMEM and receives its 128 rows of D, and each holds half of the B
+// operand's N = NPAD RHS rows (CTA r: j-groups [r NPAD/16, (r + 1) NPAD/16)),
+// so each stages and builds half of every record -- the B builders' shared
+// memory traffic, the single-CTA bound, is halved per CTA. The even CTA's MMA
+// warp issues for both; the peer's evaluation, builder and drain warps arrive
+// on the leader's barriers, the MMA completions are multicast to both.
+template <int NPAD, int DX, int NBW, bool PAIR>
 __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(const SgdSlabArgs a) {
   constexpr int CH = c64::CH, ST = c64::ST, SB = c64::SB, DEFER = c64::DEFER;
+  static_assert(!PAIR || NPAD % 16 == 0, "cta_group::2 needs N a multiple of 16");
   // TMEM: D double buffer at columns 0 / 80, then a ring of NS = 5 A slots of
   // one 32-column half each (hi 32 | lo 32) from column 160: half j of the
   // solve (chunk j / 2, half j % 2) uses slot j % 5
   constexpr int NS = 5, A_COL0 = 160, D1 = 80;
   constexpr int BW = NBW, MMA_WARP = EW + 1 + NBW, NTHREADS = 32 * (MMA_WARP + 1);
-  constexpr int IMG = NPAD * 32;  // floats of one 32-column TF32 image
+  constexpr int NB = PAIR ? NPAD / 2 : NPAD;  // B-image rows (RHS) held by this CTA
+  constexpr int LG = NB / 8;                  // their j-groups
+  constexpr int IMG = NB * 32;                // floats of this CTA's part of one 32-column TF32 image
   constexpr int DC = NPAD / 4;
   constexpr int DP = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int rw = a.rw;
-  const int st_floats = 2 * rw + 2 * 32 * DP + CH;  // 2 records | 2 SoA x | tau
+  const int jgroups = a.moff / 256;
+  const uint32_t crank = PAIR ? cluster_rank() : 0u;
+  const int g0 = static_cast<int>(crank) * LG;                         // first j-group held here
+  const int lgl = PAIR ? max(0, min(jgroups - g0, LG)) : jgroups;      // live j-groups held here
+  const int rws = PAIR ? 2 * LG * 256 : rw;                            // staged floats of one record
+  const int mo = PAIR ? LG * 256 : a.moff;                             // M image within a staged record
+  const int st_floats = 2 * rws + 2 * 32 * DP + CH;  // 2 records | 2 SoA x | tau
   float* smB = reinterpret_cast<float*>(smem_raw);  // [SB][hi0 | hi1 | lo0 | lo1]
   float* smS = smB + SB * 4 * IMG;                  // [ST][st_floats]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smS + ST * st_floats);
@@ -557,7 +603,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
   const int F = a.flush;
   const int ngroups = (nk + F - 1) / F;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int jgroups = a.moff / 256;
+  constexpr uint32_t NPEER = PAIR ? 2u : 1u;
 
   if (a.stats && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
     const double entries = static_cast<double>(a.R) * a.C;
@@ -571,35 +617,42 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       mbar_init(&st_empty[s], EW + BW);
     }
     for (int s = 0; s < SB; ++s) {
-      mbar_init(&b_full[s], BW);
+      mbar_init(&b_full[s], NPEER * BW);
       mbar_init(&b_empty[s], 1);
     }
     for (int b = 0; b < NS; ++b) {
-      mbar_init(&a_full[b], EW);
+      mbar_init(&a_full[b], NPEER * EW);
       mbar_init(&a_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&d_full[b], 1);
-      mbar_init(&d_empty[b], EW);
+      mbar_init(&d_empty[b], NPEER * EW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   for (int e = tid; e < a.ntab; e += NTHREADS) stab[e] = __ldg(a.s32 + e);
 #if SGD_FAKE_HALFREC
   for (int e = tid; e < ST * st_floats; e += NTHREADS) smS[e] = 0.f;
 #endif
-  // zero j-groups (>= JG) of every B image: written once, never rebuilt
+  // zero j-groups (>= the live ones) of every B image: written once, never rebuilt
   for (int sb = 0; sb < SB; ++sb)
     for (int f = tid; f < 4 * IMG; f += NTHREADS)
-      if (((f % IMG) >> 8) >= jgroups) smB[sb * 4 * IMG + f] = 0.f;
+      if (((f % IMG) >> 8) >= lgl) smB[sb * 4 * IMG + f] = 0.f;
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   // one CTA per SM allocating all 512 columns: the allocation starts at
   // column 0, lane 0. The MMA issue uses that constant so ptxas keeps every
@@ -619,7 +672,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
 #if SGD_FAKE_HALFREC  // timing experiment only (wrong results): half of each chunk's record bytes
       const uint32_t rec_bytes = rw * 4u, x_bytes = 2 * 32 * DP * 4u;
 #else
-      const uint32_t rec_bytes = 2 * rw * 4u, x_bytes = 2 * 32 * DP * 4u;
+      const uint32_t rec_bytes = PAIR ? 4u * lgl * 1024u : 2 * rw * 4u, x_bytes = 2 * 32 * DP * 4u;
 #endif
       for (int k = 0; k < nk; ++k) {
         const int s = k % ST;
@@ -629,9 +682,19 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
         const size_t c = static_cast<size_t>(cb) + static_cast<size_t>(k) * CH;
         float* dst = smS + s * st_floats;
         mbar_expect_tx(&st_full[s], rec_bytes + x_bytes + CH * 4u);
-        bulk_g2s(dst, a.rec + (c / 32) * rw, rec_bytes, &st_full[s]);
-        bulk_g2s(dst + 2 * rw, a.xsoa + (a.c0 + c) * DP, x_bytes, &st_full[s]);
-        bulk_g2s(dst + 2 * rw + 2 * 32 * DP, a.tau + c, CH * 4u, &st_full[s]);
+        if constexpr (PAIR) {  // this CTA's j-groups of the V and M images of both records
+          if (lgl > 0)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float* src = a.rec + (c / 32 + h) * rw + g0 * 256;
+              bulk_g2s(dst + h * rws, src, lgl * 1024u, &st_full[s]);
+              bulk_g2s(dst + h * rws + mo, src + a.moff, lgl * 1024u, &st_full[s]);
+            }
+        } else {
+          bulk_g2s(dst, a.rec + (c / 32) * rw, rec_bytes, &st_full[s]);
+        }
+        bulk_g2s(dst + 2 * rws, a.xsoa + (a.c0 + c) * DP, x_bytes, &st_full[s]);
+        bulk_g2s(dst + 2 * rws + 2 * 32 * DP, a.tau + c, CH * 4u, &st_full[s]);
       }
     }
   } else if (warp >= BUILD_WARP0 && warp < MMA_WARP) {
@@ -640,7 +703,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
     // 32-column images; the S(Delta) quadruple of f is (f / 8) % 8 = (bt / 8) % 8
     // for every i (128 / 8 = 16), so it is loaded once per half
     const int bt = tid - BUILD_WARP0 * 32;  // 0..127
-    const int live = jgroups * 64;          // float4s of one 32-column image in live j-groups
+    const int live = lgl * 64;              // float4s of one 32-column image in live j-groups
     const int squad = (bt >> 3) & 7;
     for (int k = 0; k < nk; ++k) {
       const int s = k % ST, sb = k % SB;
@@ -649,7 +712,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       PROF_ADD(1);
       const float* rec = smS + s * st_floats;
       if (warp == BUILD_WARP0) {
-        const int* tau = reinterpret_cast<const int*>(rec + 2 * rw + 2 * 32 * DP);
+        const int* tau = reinterpret_cast<const int*>(rec + 2 * rws + 2 * 32 * DP);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int dl = min(max(t_iter - tau[h * 32 + lane] - 1, 0), a.budget);
@@ -669,15 +732,15 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const float4 sc = reinterpret_cast<const float4*>(sS + sb * CH + h * 32)[squad];
-        const float4* v4 = reinterpret_cast<const float4*>(rec + h * rw);
-        const float4* m4 = reinterpret_cast<const float4*>(rec + h * rw + a.moff);
+        const float4* v4 = reinterpret_cast<const float4*>(rec + h * rws);
+        const float4* m4 = reinterpret_cast<const float4*>(rec + h * rws + mo);
         float4* bh = bbase + h * (IMG / 4);
         float4* bl = bbase + (2 + h) * (IMG / 4);
         const float2 s01 = make_float2(sc.x, sc.y), s23 = make_float2(sc.z, sc.w);
         // all of this half's loads first (independent registers), then the
         // arithmetic and the stores: the loop-carried register reuse of the
         // rolled loop serialised one shared-memory round trip per float4
-        constexpr int MAXI = (NPAD * 8 + 32 * BW - 1) / (32 * BW);  // float4s per thread per half, at most
+        constexpr int MAXI = (NB * 8 + 32 * BW - 1) / (32 * BW);  // float4s per thread per half, at most
         float4 vv[MAXI], mm[MAXI];
 #pragma unroll
         for (int i = 0; i < MAXI; ++i) {
@@ -710,33 +773,45 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&b_full[sb]);
+        if constexpr (PAIR)
+          arrive_cluster(mapa_u32(smem_u32(&b_full[sb]), 0));
+        else
+          mbar_arrive(&b_full[sb]);
         mbar_arrive(&st_empty[s]);
       }
 #if SGD_PROF
       prof_acc[4] += clock64() - prof_b0;  // build (slot 14 at the end)
 #endif
     }
-  } else if (warp == MMA_WARP) {
+  } else if (warp == MMA_WARP && crank == 0) {
     // ---------------- MMA issuer: 2 x 12 MMAs per 64-column chunk ----------------
+    // (in a pair: the even CTA's, M = 256, completions multicast to both CTAs)
     // Each 32-column half of A starts as soon as the evaluation warps publish
     // it. The whole warp waits; one elected lane issues from an if-block whose
     // operands are all warp-uniform (constant TMEM base, descriptors as 32-bit
     // offsets of one per-stage base word), so ptxas keeps them in uniform
     // registers: ~2.5 instructions per MMA instead of ~18 with the per-MMA
     // elect/broadcast of MMA_TF32 (the issue warp had become the bottleneck).
-    constexpr uint32_t idesc = tf32_idesc(NPAD, TBM);
+    constexpr uint32_t idesc = tf32_idesc(NPAD, PAIR ? 2 * TBM : TBM);
     constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14);  // SBO 1 KiB, version 1 (bit 46)
     const uint32_t smb0 = smem_u32(smB);
     const uint32_t bfull0 = smem_u32(b_full), bempty0 = smem_u32(b_empty), afull0 = smem_u32(a_full),
                    aempty0 = smem_u32(a_empty), dfull0 = smem_u32(d_full), dempty0 = smem_u32(d_empty);
     auto wait_u = [](uint32_t bar, uint32_t parity) {
-      asm volatile(
-          "{\n\t.reg .pred P1;\nW_%=:\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-          "@!P1 bra W_%=;\n\t}" ::"r"(bar),
-          "r"(parity)
-          : "memory");
+      if constexpr (PAIR && SGD_PAIR_ACQ_CLUSTER)  // (development A/B)
+        asm volatile(
+            "{\n\t.reg .pred P1;\nW_%=:\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra W_%=;\n\t}" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+      else
+        asm volatile(
+            "{\n\t.reg .pred P1;\nW_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra W_%=;\n\t}" ::"r"(bar),
+            "r"(parity)
+            : "memory");
     };
     auto elect_one = []() -> uint32_t {
       uint32_t pred = 0;
@@ -744,17 +819,33 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       return pred;
     };
     auto mma = [](uint32_t d, uint32_t a, uint32_t blo, uint32_t acc) {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\t"
-          "mov.b64 bd, {%2, %3};\n\t"
-          "setp.ne.b32 p, %5, 0;\n\t"
-          "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bd, %4, p;\n\t}" ::"r"(d),
-          "r"(a), "r"(blo), "n"(DESC_HI), "n"(idesc), "r"(acc)
-          : "memory");
+      if constexpr (PAIR)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\t"
+            "mov.b64 bd, {%2, %3};\n\t"
+            "setp.ne.b32 p, %5, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], bd, %4, p;\n\t}" ::"r"(d),
+            "r"(a), "r"(blo), "n"(DESC_HI), "n"(idesc), "r"(acc)
+            : "memory");
+      else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\t"
+            "mov.b64 bd, {%2, %3};\n\t"
+            "setp.ne.b32 p, %5, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bd, %4, p;\n\t}" ::"r"(d),
+            "r"(a), "r"(blo), "n"(DESC_HI), "n"(idesc), "r"(acc)
+            : "memory");
     };
     auto commit = [](uint32_t bar) {
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                   : "memory");
+      if constexpr (PAIR)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                bar),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
+      else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                     : "memory");
     };
     int sb = 0, bph = 0, ab = 0, aph = 0, g = 0, kf = 0;
     for (int k = 0; k < nk; ++k) {
@@ -797,7 +888,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       if (++sb == SB) { sb = 0; bph ^= 1; }
       if (++kf == F) { kf = 0; ++g; }
     }
-  } else {
+  } else if (warp < EW) {
     // ---------------- evaluation + drain ----------------
     const int lg = warp & 3, quarter = warp >> 2;
     const int row = lg * 32 + lane;
@@ -825,7 +916,12 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&d_empty[g & 1]);
+      if (lane == 0) {
+        if constexpr (PAIR)
+          arrive_cluster(mapa_u32(smem_u32(&d_empty[g & 1]), 0));
+        else
+          mbar_arrive(&d_empty[g & 1]);
+      }
     };
     uint64_t xik2[4], k_s3, k_one, k_c, k_l2s2;
     {
@@ -842,7 +938,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
     // chunk columns 32 h + 8 q ..), so each half of the A buffer is complete --
     // and published to the MMA warp -- after one eval8 of every evaluation warp
     const uint32_t st_base = smem_u32(smS);
-    const uint32_t xoff = static_cast<uint32_t>((2 * rw + quarter * 8) * 4);
+    const uint32_t xoff = static_cast<uint32_t>((2 * rws + quarter * 8) * 4);
     constexpr uint32_t XHALF = 32 * DP * 4;  // bytes between the halves' SoA x
     const uint32_t st_full0 = smem_u32(st_full), st_empty0 = smem_u32(st_empty);
     const uint32_t a_full0 = smem_u32(a_full), a_empty0 = smem_u32(a_empty);
@@ -911,12 +1007,18 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
     };
     int drained = 0, next_drain = F + DEFER;
     int pend = -1;  // a_full barrier (2 ab + h) of the half whose stores are in flight
+    const uint32_t a_full_lead = PAIR ? mapa_u32(a_full0, 0) : a_full0;  // the MMA issuer's a_full
     auto publish = [&]() {
       if (pend < 0) return;
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_u32(a_full0 + 8 * pend);
+      if (lane == 0) {
+        if constexpr (PAIR)
+          arrive_cluster(a_full_lead + 8 * pend);
+        else
+          arrive_u32(a_full0 + 8 * pend);
+      }
       pend = -1;
     };
     int s = 0, sph = 0;
@@ -980,23 +1082,46 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
 #endif
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done before either CTA frees TMEM
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
-template <int NPAD, int DX, int NBW>
+template <int NPAD, int DX, int NBW, bool PAIR>
 void launch_64_t(const SgdSlabArgs& a, cudaStream_t s) {
-  const size_t smem = c64::smem_bytes<NPAD>(a.rw, 4, a.ntab);
+  constexpr int NB = PAIR ? NPAD / 2 : NPAD;
+  const int rws = PAIR ? 2 * (NB / 8) * 256 : a.rw;
+  const size_t smem = c64::smem_bytes<NB>(rws, 4, a.ntab);
   if (smem > 227 * 1024) throw std::invalid_argument("gpk: SGD slab kernel (64) shared memory exceeds 227 KB");
   static size_t configured = 0;
+  auto kern = sgd_slab64_kernel<NPAD, DX, NBW, PAIR>;
   if (smem > configured) {
-    GPK_CUDA(cudaFuncSetAttribute(sgd_slab64_kernel<NPAD, DX, NBW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    GPK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     configured = smem;
   }
-  sgd_slab64_kernel<NPAD, DX, NBW><<<dim3((a.R + TBM - 1) / TBM, a.splits), 32 * (EW + 2 + NBW), smem, s>>>(a);
+  const int tiles = (a.R + TBM - 1) / TBM;
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((tiles + 1) / 2 * 2, a.splits, 1);  // whole pairs of row tiles
+    cfg.blockDim = dim3(32 * (EW + 2 + NBW), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GPK_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  } else {
+    kern<<<dim3(tiles, a.splits), 32 * (EW + 2 + NBW), smem, s>>>(a);
+  }
   check_launch("sgd_slab64_kernel");
 }
 template <int NPAD, int DX>
@@ -1008,8 +1133,10 @@ void launch_64(const SgdSlabArgs& a, cudaStream_t s) {
     const char* e = std::getenv("GPK_SGD_BW");
     return e ? std::atoi(e) : 4;
   }();
-  if (bw == 8) return launch_64_t<NPAD, DX, 8>(a, s);
-  return launch_64_t<NPAD, DX, 4>(a, s);
+  if constexpr (NPAD % 16 == 0)
+    if (a.pair) return launch_64_t<NPAD, DX, 4, true>(a, s);
+  if (bw == 8) return launch_64_t<NPAD, DX, 8, false>(a, s);
+  return launch_64_t<NPAD, DX, 4, false>(a, s);
 }
 
 template <int NPAD, int DP4, bool GRAM, int DX = 0>
