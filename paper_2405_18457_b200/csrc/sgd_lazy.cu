@@ -534,13 +534,20 @@ __device__ __forceinline__ void arrive_cluster(uint32_t caddr) {
 
 namespace c64 {
 constexpr int CH = 64;
-constexpr int ST = 3;
 constexpr int SB = 2;
 constexpr int DEFER = 2;
+// staging stages and TMEM A half-slots: 3 / 5 for one CTA per row tile; a CTA
+// pair stages half-records, so it has room for 4 / 4, and the evaluation warps
+// walk the rings in passes of 4 chunks with every stage, slot, barrier address
+// and phase a compile-time constant of the position in the pass
+template <bool PAIR>
+constexpr int st_stages() { return PAIR ? 4 : 3; }
+template <bool PAIR>
+constexpr int a_slots() { return PAIR ? 4 : 5; }
 
 // NB = B-image rows held by one CTA (NPAD, or NPAD / 2 in a CTA pair), rws =
 // staged floats of one 32-column record
-template <int NB>
+template <int NB, int ST>
 __host__ __device__ constexpr size_t smem_bytes(int rws, int dp, int ntab) {
   return sizeof(float) * (SB * 4 * static_cast<size_t>(NB) * 32 + ST * (2 * static_cast<size_t>(rws) + 2 * 32 * dp + CH)) +
          64 * sizeof(uint64_t) + SB * CH * sizeof(float) + static_cast<size_t>(ntab) * sizeof(float);
@@ -557,12 +564,12 @@ __host__ __device__ constexpr size_t smem_bytes(int rws, int dp, int ntab) {
 // on the leader's barriers, the MMA completions are multicast to both.
 template <int NPAD, int DX, int NBW, bool PAIR>
 __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(const SgdSlabArgs a) {
-  constexpr int CH = c64::CH, ST = c64::ST, SB = c64::SB, DEFER = c64::DEFER;
+  constexpr int CH = c64::CH, ST = c64::st_stages<PAIR>(), SB = c64::SB, DEFER = c64::DEFER;
   static_assert(!PAIR || NPAD % 16 == 0, "cta_group::2 needs N a multiple of 16");
   // TMEM: D double buffer at columns 0 / 80, then a ring of NS = 5 A slots of
   // one 32-column half each (hi 32 | lo 32) from column 160: half j of the
   // solve (chunk j / 2, half j % 2) uses slot j % 5
-  constexpr int NS = 5, A_COL0 = 160, D1 = 80;
+  constexpr int NS = c64::a_slots<PAIR>(), A_COL0 = 160, D1 = 80;
   constexpr int BW = NBW, MMA_WARP = EW + 1 + NBW, NTHREADS = 32 * (MMA_WARP + 1);
   constexpr int NB = PAIR ? NPAD / 2 : NPAD;  // B-image rows (RHS) held by this CTA
   constexpr int LG = NB / 8;                  // their j-groups
@@ -1039,25 +1046,78 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
         ++use;
       }
     };
-    for (int k = 0; k < nk; ++k) {
-      PROF_T0;
-      wait_u32(st_full0 + 8 * s, sph);
-      PROF_ADD(8);
-      const uint32_t xq = st_base + static_cast<uint32_t>(s * st_floats * 4) + xoff;
-      uint32_t hi[8], lo[8];
-      eval8(xq, hi, lo);
-      store_half(hi, lo);
-      eval8(xq + XHALF, hi, lo);
-      __syncwarp();
-      if (lane == 0) arrive_u32(st_empty0 + 8 * s);  // x_c consumed
-      store_half(hi, lo);
-      if (++s == ST) { s = 0; sph ^= 1; }
-      if (k == next_drain) {
-        drain(drained++);
-        next_drain += F;
+    if constexpr (PAIR) {
+      // passes of 4 chunks: chunk u of a pass uses stage u and A slots 2u % 4,
+      // (2u + 1) % 4 (half j of the solve uses slot j % 4), so after unrolling
+      // every barrier / TMEM address is an immediate and every phase a
+      // constant: the ring bookkeeping was ~40 % of the warps' instructions
+      static_assert(ST == 4 && NS == 4, "pass layout");
+      constexpr uint32_t STB = static_cast<uint32_t>((4 * LG * 256 + 2 * 32 * DP + CH) * 4);  // bytes per stage
+      auto pub = [&](int slot) {  // the half in `slot` is stored: hand it to the MMA issuer
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_cluster(a_full_lead + 8 * slot);
+      };
+      auto put = [&](int slot, bool reuse, uint32_t parity, const uint32_t (&hi)[8], const uint32_t (&lo)[8]) {
+        PROF_T0;
+        if (reuse) wait_u32(a_empty0 + 8 * slot, parity);  // the slot's previous half consumed
+        PROF_ADD(9);
+        tc_fence_after();
+        tc_st8(acol + slot * 64, hi);
+        tc_st8(acol + slot * 64 + 32, lo);
+      };
+      int pass = 0;
+      for (int k0 = 0; k0 < nk; k0 += 4, ++pass) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u;
+          if (k < nk) {
+            const int s0 = (2 * u) % 4, s1 = (2 * u + 1) % 4;
+            const bool reuse = pass > 0 || u >= 2;
+            const uint32_t aph = u >= 2 ? 0u : 1u;
+            PROF_T0;
+            wait_u32(st_full0 + 8 * u, static_cast<uint32_t>(pass & 1));
+            PROF_ADD(8);
+            const uint32_t xq = st_base + u * STB + xoff;
+            uint32_t hi[8], lo[8];
+            eval8(xq, hi, lo);
+            if (k > 0) pub((2 * u + 3) % 4);  // the previous half
+            put(s0, reuse, aph, hi, lo);
+            eval8(xq + XHALF, hi, lo);
+            __syncwarp();
+            if (lane == 0) arrive_u32(st_empty0 + 8 * u);  // x_c consumed
+            pub(s0);
+            put(s1, reuse, aph, hi, lo);
+            if (k == next_drain) {
+              drain(drained++);
+              next_drain += F;
+            }
+          }
+        }
       }
+      if (nk > 0) pub((2 * nk - 1) % 4);
+    } else {
+      for (int k = 0; k < nk; ++k) {
+        PROF_T0;
+        wait_u32(st_full0 + 8 * s, sph);
+        PROF_ADD(8);
+        const uint32_t xq = st_base + static_cast<uint32_t>(s * st_floats * 4) + xoff;
+        uint32_t hi[8], lo[8];
+        eval8(xq, hi, lo);
+        store_half(hi, lo);
+        eval8(xq + XHALF, hi, lo);
+        __syncwarp();
+        if (lane == 0) arrive_u32(st_empty0 + 8 * s);  // x_c consumed
+        store_half(hi, lo);
+        if (++s == ST) { s = 0; sph ^= 1; }
+        if (k == next_drain) {
+          drain(drained++);
+          next_drain += F;
+        }
+      }
+      publish();
     }
-    publish();
     while (drained < ngroups) drain(drained++);
     if (row_ok) {
       double* prow = a.part + (static_cast<size_t>(split) * a.R + er) * a.m;
@@ -1096,7 +1156,7 @@ template <int NPAD, int DX, int NBW, bool PAIR>
 void launch_64_t(const SgdSlabArgs& a, cudaStream_t s) {
   constexpr int NB = PAIR ? NPAD / 2 : NPAD;
   const int rws = PAIR ? 2 * (NB / 8) * 256 : a.rw;
-  const size_t smem = c64::smem_bytes<NB>(rws, 4, a.ntab);
+  const size_t smem = c64::smem_bytes<NB, c64::st_stages<PAIR>()>(rws, 4, a.ntab);
   if (smem > 227 * 1024) throw std::invalid_argument("gpk: SGD slab kernel (64) shared memory exceeds 227 KB");
   static size_t configured = 0;
   auto kern = sgd_slab64_kernel<NPAD, DX, NBW, PAIR>;
