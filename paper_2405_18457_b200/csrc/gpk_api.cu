@@ -1959,16 +1959,34 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
     return !(e && std::atoi(e) == 0);
   }();
   const bool fused_finish = finish_env && !op->sharded;
+  // slab -> finish -> slab chained by programmatic dependent launch: each
+  // kernel's launch and prologue (barriers, TMEM, S table, zero B groups)
+  // overlap its predecessor's tail (GPK_SGD_PDL=0: plain stream order)
+  static const bool pdl_env = [] {
+    const char* e = std::getenv("GPK_SGD_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool pdl = pdl_env && fused_finish && ch64 && !ctx->profiling;
+  sa.pdl = pdl ? 1 : 0;
+  ta.pdl = 0;
   SgdStepArgs tf = ta;
+  tf.pdl = pdl ? 1 : 0;
   if (fused_finish) tf.gpart = b->sgd_gpart2.ensure(static_cast<size_t>(sgd_finish_blocks(bs)) * 2 * m);
   int t = 0;
   auto iteration = [&]() {  // solvers.cpp:164-178
     if (t % chunk == 0) sgd_batches_dev_launch(c->seed, c->substream, n, bs, &ctl->iters, chunk, idxbuf, &ctl->stop, s);
-    cudaEvent_t* pe = prof_begin(ctx, s);
+    // profiling brackets the slab; GPK_PROF_SGD_FINISH=1 (development) brackets the finish kernel instead
+    static const bool prof_finish = [] {
+      const char* e = std::getenv("GPK_PROF_SGD_FINISH");
+      return e && std::atoi(e) != 0;
+    }();
+    cudaEvent_t* pe = prof_finish ? nullptr : prof_begin(ctx, s);
     sgd_slab_launch(sa, s);
     if (pe) GPK_CUDA(cudaEventRecord(*pe, s));
     if (fused_finish) {
+      pe = prof_finish ? prof_begin(ctx, s) : nullptr;
       sgd_finish_launch(tf, s);
+      if (pe) GPK_CUDA(cudaEventRecord(*pe, s));
     } else {
       sgd_reduce_launch(ta, s);
       allreduce_inplace(op, gbuf, static_cast<size_t>(bs) * m + m + 1);

@@ -245,6 +245,7 @@ struct SgdSlabArgs {
   double* stats;
   int ch64;             // 64-column pipeline (d <= 4 with xsoa; cols_per_split a multiple of 64)
   int pair;             // ch64 as CTA pairs (cta_group::2, M = 256; needs NPAD % 16 == 0)
+  int pdl;              // launch with programmatic stream serialization (prologue overlaps the previous kernel)
 };
 struct SgdStepArgs {
   CgCtl* ctl;
@@ -274,6 +275,7 @@ struct SgdStepArgs {
   unsigned* ticket;     // kept at 0 between launches
   double* sumsq;        // [m] tracked sum of R^2 per column
   const double* scales;
+  int pdl;              // sgd_finish: launch with programmatic stream serialization
 };
 int sgd_record_width(int m, int* moff);
 void sgd_slab_launch(const SgdSlabArgs& a, cudaStream_t s);

@@ -532,6 +532,10 @@ __device__ __forceinline__ void arrive_cluster(uint32_t caddr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
 
+// programmatic dependent launch (no-ops when the kernel was launched without the attribute)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 namespace c64 {
 constexpr int CH = 64;
 constexpr int SB = 2;
@@ -600,24 +604,16 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
   float* sS = reinterpret_cast<float*>(bars + 64);  // [SB][CH]
   float* stab = sS + SB * CH;
 
-  if (a.ctl->stop) return;
-  const int t_iter = a.ctl->iters;
-  const int* idx = a.idxbuf + static_cast<size_t>(t_iter % a.idx_chunk) * a.R;
+  // Everything up to griddep_wait() touches only this CTA's shared memory,
+  // TMEM and launch-constant inputs, so under programmatic dependent launch
+  // it overlaps the previous iteration's finish kernel (which wrote ctl, the
+  // minibatch rows' records and tau).
   const int tile = blockIdx.x, split = blockIdx.y;
   const int cb = split * a.cols_per_split;  // multiple of 64
   const int ce = min(a.C, cb + a.cols_per_split);
-  const int nk = ce > cb ? (ce - cb + CH - 1) / CH : 0;
-  const int F = a.flush;
-  const int ngroups = (nk + F - 1) / F;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t NPEER = PAIR ? 2u : 1u;
 
-  if (a.stats && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
-    const double entries = static_cast<double>(a.R) * a.C;
-    atomicAdd(a.stats, entries * a.m);
-    atomicAdd(a.stats + 1, entries * (2.0 * a.m + 3.0 * a.d + 6.0));
-    atomicAdd(a.stats + 2, entries * (3.0 * a.d + 6.0));
-  }
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&st_full[s], 1);
@@ -661,6 +657,21 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
+  griddep_wait();    // the previous kernel's writes (ctl, records, tau, idx) are visible from here
+  griddep_launch();  // the finish kernel may be scheduled as this grid's CTAs retire
+  // once the solve has stopped the launch is a no-op: zero chunks, no partials
+  const bool stopped = a.ctl->stop != 0;
+  const int t_iter = a.ctl->iters;
+  const int* idx = a.idxbuf + static_cast<size_t>(t_iter % a.idx_chunk) * a.R;
+  const int nk = (!stopped && ce > cb) ? (ce - cb + CH - 1) / CH : 0;
+  const int F = a.flush;
+  const int ngroups = (nk + F - 1) / F;
+  if (!stopped && a.stats && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    const double entries = static_cast<double>(a.R) * a.C;
+    atomicAdd(a.stats, entries * a.m);
+    atomicAdd(a.stats + 1, entries * (2.0 * a.m + 3.0 * a.d + 6.0));
+    atomicAdd(a.stats + 2, entries * (3.0 * a.d + 6.0));
+  }
   // one CTA per SM allocating all 512 columns: the allocation starts at
   // column 0, lane 0. The MMA issue uses that constant so ptxas keeps every
   // operand in uniform registers (no per-MMA elect/broadcast of the TMEM
@@ -900,7 +911,7 @@ __global__ void __launch_bounds__(32 * (EW + 2 + NBW), 1) sgd_slab64_kernel(cons
     const int lg = warp & 3, quarter = warp >> 2;
     const int row = lg * 32 + lane;
     const int er = tile * TBM + row;
-    const bool row_ok = er < a.R;
+    const bool row_ok = !stopped && er < a.R;
     const int gi = row_ok ? idx[er] : 0;
     const float* xrow = a.xs + static_cast<size_t>(gi) * a.dp;
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
@@ -1165,23 +1176,28 @@ void launch_64_t(const SgdSlabArgs& a, cudaStream_t s) {
     configured = smem;
   }
   const int tiles = (a.R + TBM - 1) / TBM;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(PAIR ? (tiles + 1) / 2 * 2 : tiles, a.splits, 1);  // PAIR: whole pairs of row tiles
+  cfg.blockDim = dim3(32 * (EW + 2 + NBW), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   if constexpr (PAIR) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((tiles + 1) / 2 * 2, a.splits, 1);  // whole pairs of row tiles
-    cfg.blockDim = dim3(32 * (EW + 2 + NBW), 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    GPK_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
-  } else {
-    kern<<<dim3(tiles, a.splits), 32 * (EW + 2 + NBW), smem, s>>>(a);
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (a.pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  GPK_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   check_launch("sgd_slab64_kernel");
 }
 template <int NPAD, int DX>
@@ -1421,6 +1437,11 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
 // (solvers.cpp:164-178).
 constexpr int FIN_ROWS = 8;
 __global__ void sgd_finish_kernel(SgdStepArgs a) {
+  // programmatic dependent launch: the next slab kernel may start its prologue
+  // now (it waits for this grid's completion before it reads anything this
+  // grid writes); this grid waits for the slab's partials
+  griddep_launch();
+  griddep_wait();
   if (a.ctl->stop) return;
   const int t = a.ctl->iters;
   const int* idx = a.idxbuf + static_cast<size_t>(t % a.idx_chunk) * a.b;
@@ -1650,7 +1671,16 @@ void sgd_apply_launch(const SgdStepArgs& a, cudaStream_t s) {
 void sgd_finish_launch(const SgdStepArgs& a, cudaStream_t s) {
   if (a.m > 80) throw std::invalid_argument("gpk: SGD finish supports m <= 80");
   const int threads = ((FIN_ROWS * a.m + 31) / 32) * 32;
-  sgd_finish_kernel<<<(a.b + FIN_ROWS - 1) / FIN_ROWS, threads, 0, s>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.b + FIN_ROWS - 1) / FIN_ROWS, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  GPK_CUDA(cudaLaunchKernelEx(&cfg, sgd_finish_kernel, a));
   check_launch("sgd_finish");
 }
 int sgd_finish_blocks(int b) { return (b + FIN_ROWS - 1) / FIN_ROWS; }
