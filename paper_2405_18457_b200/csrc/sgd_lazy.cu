@@ -1444,8 +1444,11 @@ __global__ void sgd_finish_kernel(SgdStepArgs a) {
   griddep_wait();
   if (a.ctl->stop) return;
   const int t = a.ctl->iters;
+  const int ctl_budget = a.ctl->budget;
   const int* idx = a.idxbuf + static_cast<size_t>(t % a.idx_chunk) * a.b;
   const int m = a.m, bm = a.b * m;
+  // (only the last block uses it; loaded here so the load is off its serial tail)
+  const double sumsq_old = static_cast<int>(threadIdx.x) < m ? a.sumsq[threadIdx.x] : 0.0;
   __shared__ double gs[FIN_ROWS][80], os[FIN_ROWS][80];
   __shared__ int bad_g, bad_row;
   __shared__ unsigned last;
@@ -1454,32 +1457,55 @@ __global__ void sgd_finish_kernel(SgdStepArgs a) {
   const int rl = threadIdx.x / m, j = threadIdx.x - rl * m;  // blockDim.x = FIN_ROWS m (rounded to 32)
   const int q = blockIdx.x * FIN_ROWS + rl;
   const bool act = rl < FIN_ROWS && q < a.b;
+  // FIN_DEEP split partials in flight per round; element e of the splits goes
+  // to chain e % 4, each chain in increasing e, whatever the depth. The rounds
+  // are unpredicated so that ptxas issues all of a round's loads before the
+  // first add (a predicated round compiled, depending on unrelated code, to a
+  // load-add-load-add chain: 26.7 instead of 16.8 us per launch at C4's 37
+  // splits; depth 4: 24.2 us; depth 20 spills).
+#ifndef FIN_DEEP
+#define FIN_DEEP 16
+#endif
+  int li = -1;
   double g = 0.0;
   if (act) {
     const int e = q * m + j;
     double c4[4] = {0.0, 0.0, 0.0, 0.0};
+    // unpredicated rounds of FIN_DEEP loads (all in flight before the first
+    // add), then rounds of four, then the tail; sp stays a multiple of 4
     int sp = 0;
-    for (; sp + 4 <= a.splits; sp += 4) {
+#if FIN_DEEP > 4
+    for (; sp + FIN_DEEP <= a.splits; sp += FIN_DEEP) {
+      double v[FIN_DEEP];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) c4[c] += __ldcg(a.part + static_cast<size_t>(sp + c) * bm + e);
+      for (int i = 0; i < FIN_DEEP; ++i) v[i] = __ldcg(a.part + static_cast<size_t>(sp + i) * bm + e);
+#pragma unroll
+      for (int i = 0; i < FIN_DEEP; ++i) c4[i & 3] += v[i];
+    }
+#endif
+    for (; sp + 4 <= a.splits; sp += 4) {
+      double v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = __ldcg(a.part + static_cast<size_t>(sp + c) * bm + e);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) c4[c] += v[c];
     }
     for (int c = 0; sp + c < a.splits; ++c) c4[c] += __ldcg(a.part + static_cast<size_t>(sp + c) * bm + e);
     g = (c4[0] + c4[1]) + (c4[2] + c4[3]);
   }
   double g2 = 0.0, o2 = 0.0;
-  int li = -1;
   if (act) {
     li = idx[q];
     const size_t o = static_cast<size_t>(li) * m + j;
     const int dl = min(max(t - a.tau[li] - 1, 0), a.budget);
     const double mb = a.Mb[o];
-    const double vt = fma(a.s64[dl], mb, a.Vb[o]);  // V(t)
-    g = fma(a.sigma2, vt, g) - a.B[o];
+    const double vb = a.Vb[o], bt = a.B[o], old = a.resid[o], sd = a.s64[dl], pd = a.p64[dl];
+    const double vt = fma(sd, mb, vb);  // V(t)
+    g = fma(a.sigma2, vt, g) - bt;
     if (!isfinite(g)) bad_g = 1;
     g2 = g * g;
-    const double old = a.resid[o];
     o2 = old * old;
-    const double mt = a.p64[dl] * mb;  // M(t)
+    const double mt = pd * mb;  // M(t)
     const double mn = __dsub_rn(__dmul_rn(mt, a.rho), __dmul_rn(a.step, g));
     const double vn = __dadd_rn(vt, mn);
     if (!isfinite(vn) || !isfinite(mn)) bad_row = 1;
@@ -1513,6 +1539,7 @@ __global__ void sgd_finish_kernel(SgdStepArgs a) {
   __syncthreads();
   if (!last) return;
   __threadfence();
+  const int now = __ldcg(a.nonfinite_now);
   __shared__ double ss[128];
   __shared__ double red8[8][2][80];
   {  // column sums of the block partials: thread (jj, k) sums blocks k, k + 8, ... then 8 partials in order
@@ -1537,12 +1564,11 @@ __global__ void sgd_finish_kernel(SgdStepArgs a) {
       sg += red8[k][0][jj];
       so += red8[k][1][jj];
     }
-    const double v = a.sumsq[jj] + (sg - so);
+    const double v = sumsq_old + (sg - so);
     a.sumsq[jj] = v;
     ss[jj] = fmax(v, 0.0);
   }
   __syncthreads();
-  const int now = *a.nonfinite_now;
   if (threadIdx.x == 0) {
     *a.ticket = 0u;
     if (now) *a.nonfinite = 1;
@@ -1556,12 +1582,13 @@ __global__ void sgd_finish_kernel(SgdStepArgs a) {
       const double mean = sqrt(ss[0]) / a.scales[0];
       probe = m > 1 ? probe / (m - 1) : 0.0;
       CgCtl* c = a.ctl;
-      c->iters += 1;
+      const int done = (mean <= a.tol && probe <= a.tol) ? 1 : 0;
+      c->iters = t + 1;
       c->mean_norm = mean;
       c->probe_norm = probe;
-      c->done = mean <= a.tol && probe <= a.tol;
+      c->done = done;
       c->aborted = now ? 1 : 0;
-      c->stop = (c->done || c->aborted || c->iters >= c->budget) ? 1 : 0;
+      c->stop = (done || now || t + 1 >= ctl_budget) ? 1 : 0;
     }
   }
 }
