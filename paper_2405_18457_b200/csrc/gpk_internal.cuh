@@ -208,6 +208,7 @@ struct GradTcArgs {
   double* part;         // [blocks][npairs*(d+1)]
   int blocks;
   long long tile_begin, tile_end;  // 128 x 128 tiles of this rank
+  int wave;                         // row-wave tile schedule (set by the launcher: rows >= 8 CTAs)
   const float* xsoa;    // d <= 4: column coordinates per 32-row chunk in SoA order (nullptr: AoS xs)
 };
 int grad_tc_kp(int cols);

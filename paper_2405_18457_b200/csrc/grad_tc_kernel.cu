@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "gpk_internal.cuh"
 #include "tc_util.cuh"
@@ -62,7 +63,7 @@ constexpr int TMEM_COLS = 512;  // one CTA per SM
 constexpr int A_BASE = 2 * CN;  // D buffers at TMEM columns [0, 64) and [64, 128); A pieces from 128
 constexpr int NPIECE = 3;
 
-__device__ __forceinline__ void tile_coords_tc(long long L, int T, int symmetric, int& ti, int& tc) {
+__host__ __device__ __forceinline__ void tile_coords_tc(long long L, int T, int symmetric, int& ti, int& tc) {
   if (!symmetric) {
     ti = static_cast<int>(L / T);
     tc = static_cast<int>(L % T);
@@ -78,16 +79,71 @@ __device__ __forceinline__ void tile_coords_tc(long long L, int T, int symmetric
   tc = r + static_cast<int>(L - off(r));
 }
 
-// (ti, tc) of consecutive tile pairs: the closed form once (FP64 sqrt), then
-// one step per pair (it ran per chunk in every warp: 5 % of the pass's stalls)
+// The tile pairs of one CTA, in the order it visits them. The rank's share of
+// the tile list is the linear range [tb, te) (rows ti, columns tc >= ti of the
+// symmetric list, or all T x T); two schedules:
+//  * contiguous (small problems): CTA b takes the b-th 1/G of the range in
+//    list order -- even shares for any T, but every CTA streams its own
+//    columns, so the column images are re-read from DRAM once they exceed L2;
+//  * waves (rows >= 8 G): CTA b takes whole rows, one per wave of G rows (the
+//    position within the wave alternates direction, so the shares stay within
+//    one row of each other), and walks each row from its LAST column down:
+//    all CTAs of a wave start at column tile T - 1 and move in step, so a
+//    column tile is fetched from DRAM once per wave and read by the other
+//    CTAs from L2 (C4: 359 GB -> ~8 GB of DRAM reads per pass).
+// Every role builds the same walk; next() is one step per tile pair (the
+// closed-form FP64 sqrt ran per chunk in every warp: 5 % of the pass's stalls).
 struct TileWalk {
   int ti, tc, T, sym;
-  __device__ __forceinline__ void init(long long L, int T_, int sym_) {
+  // waves
+  int wave, G, b, w, R, r0, c0, r1, c1, lo;
+  __device__ __forceinline__ int row_lo(int r) const { return r == r0 ? c0 : (sym ? r : 0); }
+  __device__ __forceinline__ int row_hi(int r) const { return r == r1 ? c1 : T - 1; }
+  __device__ __forceinline__ bool next_row() {
+    ++w;
+    const int idx = w * G + ((w & 1) ? G - 1 - b : b);
+    if (idx >= R) return false;
+    ti = r0 + idx;
+    lo = row_lo(ti);
+    tc = row_hi(ti);
+    return true;
+  }
+  // returns the number of tile pairs of this CTA
+  __device__ __forceinline__ long long init(long long tb, long long te, int T_, int sym_, int wave_, int G_, int b_) {
     T = T_;
     sym = sym_;
-    tile_coords_tc(L, T, sym, ti, tc);
+    wave = wave_;
+    G = G_;
+    b = b_;
+    if (te <= tb) return 0;
+    if (!wave) {
+      const long long per = (te - tb + G - 1) / G;
+      const long long L0 = tb + b * per;
+      const long long L1 = min(te, L0 + per);
+      if (L1 <= L0) return 0;
+      tile_coords_tc(L0, T, sym, ti, tc);
+      return L1 - L0;
+    }
+    tile_coords_tc(tb, T, sym, r0, c0);
+    tile_coords_tc(te - 1, T, sym, r1, c1);
+    R = r1 - r0 + 1;
+    long long cnt = 0;
+    for (int ww = 0; ww * G < R; ++ww) {
+      const int idx = ww * G + ((ww & 1) ? G - 1 - b : b);
+      if (idx < R) cnt += row_hi(r0 + idx) - row_lo(r0 + idx) + 1;
+    }
+    w = -1;
+    if (cnt > 0) next_row();
+    return cnt;
   }
   __device__ __forceinline__ void next() {
+    if (wave) {
+      if (tc > lo)
+        --tc;
+      else
+        next_row();
+      return;
+    }
     if (++tc == T) {
       ++ti;
       tc = sym ? ti : 0;
@@ -166,10 +222,11 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
   const long long ntiles = a.symmetric ? static_cast<long long>(T) * (T + 1) / 2 : static_cast<long long>(T) * T;
   const long long tb = a.tile_end >= 0 ? a.tile_begin : 0;
   const long long te = a.tile_end >= 0 ? min(a.tile_end, ntiles) : ntiles;
-  const long long per = (te - tb + gridDim.x - 1) / gridDim.x;
-  const long long L0 = tb + blockIdx.x * per;
-  const long long L1 = min(te, L0 + per);
-  const int nq = L1 > L0 ? static_cast<int>(2 * (L1 - L0)) : 0;
+  int nq;
+  {
+    TileWalk tw0;
+    nq = static_cast<int>(2 * tw0.init(tb, te, T, a.symmetric, a.wave, gridDim.x, blockIdx.x));
+  }
 
   for (int e = tid; e < EVAL_WARPS * NV; e += NTHREADS) wacc[e] = 0.0;
   if (tid == 0) {
@@ -203,7 +260,7 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
     if (lane == 0) {
       const uint32_t bbytes = NPIECE * img * 4u, xbytes = CN * DP * 4u, wbytes = NARROW ? CN * 4u : 0u;
       TileWalk tw;
-      tw.init(L0, T, a.symmetric);
+      tw.init(tb, te, T, a.symmetric, a.wave, gridDim.x, blockIdx.x);
       for (int k = 0; k < nq; ++k) {
         const int s = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[s], ((k - STAGES) / STAGES) & 1);
@@ -223,7 +280,7 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
       const uint32_t HI = tc_desc_hi(static_cast<uint32_t>(KP / 4) * 128u);
       int prev_ti = -1, rows_loaded = 0;
       TileWalk tw;
-      tw.init(L0, T, a.symmetric);
+      tw.init(tb, te, T, a.symmetric, a.wave, gridDim.x, blockIdx.x);
       for (int k = 0; k < nq; ++k) {
         const int s = k % STAGES, b = k & 1;
         if (k > 0 && (k & 1) == 0) tw.next();
@@ -275,7 +332,7 @@ __global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const Gr
     for (int k = 0; k < ((NARROW && !COMB) ? DP / 2 : 1); ++k) ln[k] = 0ull;
     int prev_ti = -1;
     TileWalk tw;
-    tw.init(L0, T, a.symmetric);
+    tw.init(tb, te, T, a.symmetric, a.wave, gridDim.x, blockIdx.x);
     for (int k = 0; k < nq; ++k) {
       const int s = k % STAGES, b = k & 1;
       if (k > 0 && (k & 1) == 0) tw.next();
@@ -583,8 +640,27 @@ void grad_tc_pack_launch(const float* w32, int ld, int n, int cols, int kp, floa
   check_launch("grad_tc_pack");
 }
 
-void grad_tc_launch(const GradTcArgs& a, cudaStream_t s) {
+void grad_tc_launch(const GradTcArgs& a0, cudaStream_t s) {
+  GradTcArgs a = a0;
   if (a.kp < 16 || a.kp > 64 || a.kp % 16) throw std::invalid_argument("gpk: tensor-core grad pass needs 1 < s <= 64");
+  {  // row-wave schedule once the rank's share spans >= 8 rows per CTA (GPK_GRAD_WAVE=0 / 1: never / always)
+    static const int wave_env = [] {
+      const char* e = std::getenv("GPK_GRAD_WAVE");
+      return e ? std::atoi(e) : -1;
+    }();
+    const int T = (a.n + TBM - 1) / TBM;
+    const long long ntiles = grad_tc_tiles(a.n, a.symmetric);
+    const long long tb = a.tile_end >= 0 ? a.tile_begin : 0;
+    const long long te = a.tile_end >= 0 ? std::min(a.tile_end, ntiles) : ntiles;
+    int rows = 0;
+    if (te > tb) {
+      int r0, c0, r1, c1;
+      tile_coords_tc(tb, T, a.symmetric, r0, c0);
+      tile_coords_tc(te - 1, T, a.symmetric, r1, c1);
+      rows = r1 - r0 + 1;
+    }
+    a.wave = wave_env >= 0 ? (wave_env != 0) : (rows >= 8 * a.blocks);
+  }
   switch (a.dp / 4) {
     case 1: return launch_dp<1>(a, s);
     case 2: return launch_dp<2>(a, s);
