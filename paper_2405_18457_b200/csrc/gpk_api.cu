@@ -507,7 +507,62 @@ void stats_add_launch(double* st, double entries, int m, int d, const int* skip,
   check_launch("stats_add");
 }
 
+void run_kv_one(gpk_operator* op, const KvCall& c);
+
+// Column panels for products whose packed RHS images exceed the L2: every row
+// tile streams all of the images, and once the concurrently running CTAs have
+// drifted apart over a stream larger than the cache each of them re-reads it
+// from DRAM (measured at n = 524288, m = 65: 390-420 GB of DRAM reads per
+// product against 0.37 GB of images, and the entry rate falls from 5.6e11/s
+// at n <= 262144 to 5.2e11/s at n = 1048576). Running the product panel by
+// panel -- all row tiles over one L2-sized block of columns, accumulating into
+// out in FP64 as the sharded ring does per slice -- keeps a panel's images
+// resident. GPK_KV_PANEL_MB: image bytes per panel (default 48; 0: off).
+int kv_panel_cols(gpk_operator* op, const KvCall& c) {
+  static const bool panel_env = std::getenv("GPK_KV_PANEL_MB") != nullptr;  // (set: panels at any size, for tests)
+  static const int panel_mb = [] {
+    const char* e = std::getenv("GPK_KV_PANEL_MB");
+    return e ? std::atoi(e) : 48;
+  }();
+  const bool tc = op->ctx->kernel == 1 && c.m <= 80;
+  if (panel_mb <= 0 || !tc || c.fused || c.sel || c.ctl || c.spart || c.inv_scales || !c.out) return 0;
+  const size_t col_bytes = kv_tc_pack_floats(c.m, 32) / 32 * sizeof(float);
+  const size_t panel_bytes = static_cast<size_t>(panel_mb) << 20;
+  if (static_cast<size_t>(c.C) * col_bytes <= 2 * panel_bytes || (!panel_env && static_cast<double>(c.R) * c.C < 1e9)) return 0;
+  const int pc = static_cast<int>(panel_bytes / col_bytes) / 1024 * 1024;
+  return pc >= 1024 ? pc : 0;
+}
+
 void run_kv(gpk_operator* op, const KvCall& c) {
+  const int pc = kv_panel_cols(op, c);
+  if (pc == 0) return run_kv_one(op, c);
+  cudaStream_t s = op->ctx->stream;
+  const float* vpk = c.vpk;
+  if (!vpk) {  // the images of the whole column range once (as run_kv_one would)
+    float* buf = op->vpk.ensure(kv_tc_pack_floats(c.m, c.C));
+    kv_tc_pack_launch(c.vdiag, c.v, c.vdiag ? c.m : kv_ld_for(c.m), c.C, c.m, nullptr, 0, op->n, buf, c.skip, s);
+    vpk = buf;
+  }
+  const size_t cf = kv_tc_pack_floats(c.m, 32);  // floats per 32-column image chunk
+  for (int off = 0; off < c.C; off += pc) {
+    KvCall p = c;
+    p.vpk = vpk + static_cast<size_t>(off / 32) * cf;
+    p.c0 = c.c0 + off;
+    p.C = std::min(pc, c.C - off);
+    p.vshift = c.vshift - off;  // the diagonal rows index vdiag relative to the whole range's first column
+    if (off > 0) {
+      p.base = c.out;
+      p.ldb = c.ldo;
+    }
+    if (off + pc < c.C) {  // the fused column dot belongs to the complete result
+      p.dotw = nullptr;
+      p.dpart = nullptr;
+    }
+    run_kv_one(op, p);
+  }
+}
+
+void run_kv_one(gpk_operator* op, const KvCall& c) {
   cudaStream_t s = op->ctx->stream;
   const int Cmax = c.sel ? c.sel_block : c.C;
   const bool tc = op->ctx->kernel == 1 && c.m <= 80;
