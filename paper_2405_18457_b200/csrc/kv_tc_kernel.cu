@@ -194,6 +194,14 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   constexpr int KG = TgShape<DP4>::KG;
   constexpr int XST = TG ? TgShape<DP4>::CHUNK : TBK * DP;  // floats of column data per stage
   using L = TcLayout<NPAD>;
+  // One-CTA-per-SM product launches double-buffer the FP32 accumulator D when
+  // the 512 TMEM columns have room for a second one (A ring [128, 384); with
+  // tensor-core Gram distances the row images end at 384 + 2 KG): the MMA warp
+  // starts the next accumulation group in the other buffer while the
+  // evaluation warps drain this one two chunks later, so neither waits.
+  constexpr bool DBUF = DEEP && !FUSED && NPAD / (EW / 4) <= 20 && NPAD <= 80 && (!TG || KG <= 24);
+  constexpr uint32_t D1_COL = TG ? 432 : 384;
+  constexpr int DRAIN_DEFER = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the fused AP slab runs one CTA per SM: 4 TMEM A buffers (512 columns)
   constexpr int NAB = DEEP ? 4 : 2;
@@ -212,6 +220,8 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
   uint64_t* g_full = bars + 2 * STAGES + 12;     // TG: Gram tile of the chunk in TMEM
   uint64_t* g_empty = bars + 2 * STAGES + 13;    // TG: eval warps have read it
   uint64_t* arow_full = bars + 2 * STAGES + 14;  // TG: row images written
+  uint64_t* d_full1 = bars + 2 * STAGES + 15;    // DBUF: the second accumulator
+  uint64_t* d_empty1 = bars + 2 * STAGES + 16;
 
   if (a.skip && *a.skip) return;
   int c0 = a.c0, C = a.C;
@@ -288,6 +298,10 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     }
     mbar_init(d_full, 1);
     mbar_init(d_empty, EW);
+    if (DBUF) {
+      mbar_init(d_full1, 1);
+      mbar_init(d_empty1, EW);
+    }
     if (FUSED) mbar_init(base_full, 1);  // base tile landed
     if (TG) {
       mbar_init(g_full, 1);
@@ -401,7 +415,13 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
           gram_mma(k + 1);
         }
         mbar_wait(&a_full[b], (k / NAB) & 1);
-        if (first_in_group && g > 0) mbar_wait(d_empty, (g - 1) & 1);
+        if constexpr (DBUF) {
+          if (first_in_group && g >= 2) mbar_wait((g & 1) ? d_empty1 : d_empty, ((g >> 1) - 1) & 1);
+        } else {
+          if (first_in_group && g > 0) mbar_wait(d_empty, (g - 1) & 1);
+        }
+        const uint32_t dacc = tmem + ((DBUF && (g & 1)) ? D1_COL : 0u);
+        uint64_t* const dfull_g = (DBUF && (g & 1)) ? d_full1 : d_full;
         tc_fence_after();
         const uint32_t bh = smem_u32(smB + s * L::CHUNK_FLOATS);
         const uint32_t bl = bh + L::IMG_FLOATS * 4;
@@ -412,13 +432,13 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
           if (tc_elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < TBK / 8; ++kk) {
-              tc_mma_u<tc_desc_hi(VSBO), idesc>(tmem, ah + kk * 8, dh + kk * 16, (first_in_group && kk == 0) ? 0u : 1u);
-              tc_mma_u<tc_desc_hi(VSBO), idesc>(tmem, ah + kk * 8, dl + kk * 16, 1u);
-              tc_mma_u<tc_desc_hi(VSBO), idesc>(tmem, al + kk * 8, dh + kk * 16, 1u);
+              tc_mma_u<tc_desc_hi(VSBO), idesc>(dacc, ah + kk * 8, dh + kk * 16, (first_in_group && kk == 0) ? 0u : 1u);
+              tc_mma_u<tc_desc_hi(VSBO), idesc>(dacc, ah + kk * 8, dl + kk * 16, 1u);
+              tc_mma_u<tc_desc_hi(VSBO), idesc>(dacc, al + kk * 8, dh + kk * 16, 1u);
             }
             tc_commit_u(&empty[s]);
             tc_commit_u(&a_empty[b]);
-            if (last_in_group) tc_commit_u(d_full);
+            if (last_in_group) tc_commit_u(dfull_g);
           }
           __syncwarp();
           if (last_in_group) ++g;
@@ -427,14 +447,14 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
           for (int kk = 0; kk < TBK / 8; ++kk) {
             const uint64_t dh = umma_desc(bh + kk * 256, 128, VSBO);
             const uint64_t dl = umma_desc(bl + kk * 256, 128, VSBO);
-            MMA_TF32(tmem, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
-            MMA_TF32(tmem, ah + kk * 8, dl, idesc, 1u);
-            MMA_TF32(tmem, al + kk * 8, dh, idesc, 1u);
+            MMA_TF32(dacc, ah + kk * 8, dh, idesc, (first_in_group && kk == 0) ? 0u : 1u);
+            MMA_TF32(dacc, ah + kk * 8, dl, idesc, 1u);
+            MMA_TF32(dacc, al + kk * 8, dh, idesc, 1u);
           }
           MMA_COMMIT(&empty[s]);
           MMA_COMMIT(&a_empty[b]);
           if (last_in_group) {
-            MMA_COMMIT(d_full);
+            MMA_COMMIT(dfull_g);
             ++g;
           }
         }
@@ -541,6 +561,7 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
     if (!SK) setup_rows(tile);
     const uint32_t lane_addr = static_cast<uint32_t>(lg * 32) << 16;
     int g = 0;  // accumulation groups drained
+    [[maybe_unused]] int pending = 0;  // DBUF: a completed group whose drain is deferred
 
     Walk w = walk_begin();
     for (int k = 0; k < nk; ++k, walk_next(w)) {
@@ -649,6 +670,45 @@ __global__ void __launch_bounds__(TcRoles<MODE>::THREADS, MODE ? 1 : 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[b]);
 
+      if constexpr (DBUF) {
+        // drain of group gd: D buffer gd & 1 -> the FP64 registers
+        auto drain_regs = [&](int gd) {
+          mbar_wait((gd & 1) ? d_full1 : d_full, (gd >> 1) & 1);
+          tc_fence_after();
+          const uint32_t dcol = tmem + lane_addr + ((gd & 1) ? D1_COL : 0u) + half * DCOLS;
+          uint32_t v[DCOLS];
+#pragma unroll
+          for (int q4 = 0; q4 < DCOLS / 4; ++q4) tc_ld4(dcol + q4 * 4, *reinterpret_cast<uint32_t(*)[4]>(v + 4 * q4));
+          tc_wait_ld();
+#pragma unroll
+          for (int e = 0; e < DCOLS; ++e) acc64[e] += static_cast<double>(__uint_as_float(v[e]));
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive((gd & 1) ? d_empty1 : d_empty);
+        };
+        // the previous group, DRAIN_DEFER chunks into this one (its MMAs are long done)
+        if (pending && (w.gp + 1 == DRAIN_DEFER || last_in_group)) {
+          drain_regs(g++);
+          pending = 0;
+        }
+        if (last_in_group) {
+          const bool seg_end = k + 1 == nk || (SK && q + 1 == Q);  // the (CTA, tile) segment ends here
+          if (seg_end) {
+            drain_regs(g++);
+            if (er < a.R) {
+              double* prow = part + static_cast<size_t>(er_c) * a.m;
+#pragma unroll
+              for (int e = 0; e < DCOLS; ++e) {
+                const int col = half * DCOLS + e;
+                if (col < a.m) prow[col] = acc64[e];
+              }
+            }
+            wrote = true;
+          } else {
+            pending = 1;
+          }
+        }
+      } else
       if (last_in_group) {
         mbar_wait(d_full, g & 1);
         ++g;
