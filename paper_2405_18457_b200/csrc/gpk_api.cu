@@ -1856,6 +1856,7 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   double* Mb = b->w1.ensure(nm);
   GPK_CUDA(cudaMemsetAsync(Mb, 0, sizeof(double) * nm, s));
   int moff = 0;
+  int s32_sat = 0;  // first Delta from which the FP32 S table is constant
   const int rw = sgd_record_width(m, &moff);
   const int rows_pad = (nloc + 31) / 32 * 32;
   // one record per 32-row chunk, plus a zero record past the end (64-column slab chunks)
@@ -1876,6 +1877,12 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
       S[k] = S[k - 1] + P[k];
     }
     for (int k = 0; k <= budget; ++k) t32[k] = static_cast<float>(S[k]);
+    // S(Delta) is non-decreasing and converges to rho / (1 - rho): in FP32 it is
+    // constant from some Delta on (rho = 0.9: ~170), so the slab clamps Delta
+    // there -- the same values, a table of a few hundred entries in shared
+    // memory instead of 4096, and no global look-ups for long-untouched rows
+    s32_sat = budget;
+    while (s32_sat > 0 && t32[s32_sat - 1] == t32[budget]) --s32_sat;
     GPK_CUDA(cudaMemcpyAsync(b->sgd_tab.ensure(tab.size()), tab.data(), sizeof(double) * tab.size(),
                              cudaMemcpyHostToDevice, s));
     GPK_CUDA(cudaMemcpyAsync(b->sgd_s32.ensure(t32.size()), t32.data(), sizeof(float) * t32.size(),
@@ -1937,8 +1944,8 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   sa.moff = moff;
   sa.tau = tau;
   sa.s32 = b->sgd_s32.p;
-  sa.budget = budget;
-  sa.ntab = std::min(budget + 1, 4096);  // 16 KB of shared memory
+  sa.budget = s32_sat < 4096 ? s32_sat : budget;  // Delta clamp: S32(Delta) == S32(s32_sat) beyond it
+  sa.ntab = std::min(sa.budget + 1, 4096);         // staged in shared memory (<= 16 KB)
   // Gram-form distances when the padded row has a free slot for |x|^2
   // (GPK_SGD_GRAM=1; measured: no faster at C4 and 8x the distance rounding
   // at d = 11, so direct differences by default)
