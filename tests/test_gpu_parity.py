@@ -512,8 +512,11 @@ def test_apply_streamk_matches_oracle(G, oracle, n, d, m, monkeypatch):
 
 @pytest.mark.parametrize("env", [{"GPK_KV_DEEP": "1", "GPK_TGRAM_MIN_D": "1"},  # deep launch, Gram MMAs at every d
                                  {"GPK_KV_DEEP": "1", "GPK_TGRAM": "0"},        # deep launch, FP32 distances
-                                 {"GPK_KV_DEEP": "0", "GPK_TGRAM_MIN_D": "1"}],  # two CTAs per SM (no Gram MMAs)
-                         ids=["deep-gram", "deep-fp32", "shallow"])
+                                 {"GPK_KV_DEEP": "0", "GPK_TGRAM_MIN_D": "1"},  # two CTAs per SM (no Gram MMAs)
+                                 {"GPK_KV_DEEP": "1", "GPK_KV_PANEL_MB": "1"},  # column panels of large products
+                                 {"GPK_KV_DEEP": "1", "GPK_FLUSH_CHUNKS": "2"},  # double-buffered D, short groups
+                                 {"GPK_GRAD_WAVE": "1"}],                       # gradient pass in row waves
+                         ids=["deep-gram", "deep-fp32", "shallow", "panels", "dbuf-short-groups", "grad-wave"])
 def test_operator_variants_match_oracle(env):
     """The launch variants the size heuristics pick at BASELINE sizes (one CTA
     per SM with tensor-core Gram distances for the C2 refresh and the AP
