@@ -47,15 +47,18 @@ using namespace tc;
 constexpr int TBM = 128;  // tile edge (rows per CTA pass, columns per tile)
 constexpr int CN = 64;    // columns per chunk == MMA N
 constexpr int STAGES = 3;
-// Evaluation warps: 16 for d <= 8 (a quarter of each 64-column chunk each,
-// four per SM sub-partition: with 8 the C4 pass ran at 15 % warp occupancy
-// and 48 % issue), 8 above (half a chunk each: the wider distance loops need
-// the registers); the first 8 also write the row tile's U pieces into TMEM;
-// then the producer warp and the MMA warp.
+// Evaluation warps: 16 (a quarter of each 64-column chunk each, four per SM
+// sub-partition: with 8 the C4 pass ran at 15 % warp occupancy and 48 % issue)
+// while the wider distance loops fit the 96-register budget of 18 warps: d <= 12
+// for every pair set, d <= 20 for the estimator's combined / single-pair passes
+// (LEAN; the two-pair pass spills from d = 13); 8 above (half a chunk each).
+// Measured at d = 11, n = 524288: 0.797 -> 0.730 s per gradient call. The
+// first 8 warps also write the row tile's U pieces into TMEM; then the
+// producer warp and the MMA warp.
 constexpr int A_WRITERS = 8;
-template <int DP4>
+template <int DP4, bool LEAN>
 struct GradRoles {
-  static constexpr int EW = DP4 <= 2 ? 16 : 8;
+  static constexpr int EW = (DP4 <= 3 || (LEAN && DP4 <= 5)) ? 16 : 8;
   static constexpr int NT = 32 * (EW + 2);
   static constexpr int CW = CN / (EW / 4);  // chunk columns per evaluation warp
 };
@@ -196,8 +199,9 @@ __device__ __forceinline__ void butterfly_flush(const float (&v)[NV], int lane, 
 // dimensions of one column -- about half the FMA-pipe work per entry, which
 // bounds this pass at small d.
 template <int DP4, bool NARROW, bool COMB, int DX = 0>
-__global__ void __launch_bounds__(GradRoles<DP4>::NT, 1) grad_tc_kernel(const GradTcArgs a) {
-  constexpr int EVAL_WARPS = GradRoles<DP4>::EW, NTHREADS = GradRoles<DP4>::NT, CW = GradRoles<DP4>::CW;
+__global__ void __launch_bounds__((GradRoles<DP4, (COMB || !NARROW)>::NT), 1) grad_tc_kernel(const GradTcArgs a) {
+  using Roles = GradRoles<DP4, (COMB || !NARROW)>;
+  constexpr int EVAL_WARPS = Roles::EW, NTHREADS = Roles::NT, CW = Roles::CW;
   constexpr int DP = 4 * DP4;
   constexpr int NPR = (NARROW && !COMB) ? 2 : 1;
   constexpr int NUSED = NPR * (DP + 1);
@@ -586,7 +590,7 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
   // >= 120 KB keeps one CTA per SM: each allocates all 512 TMEM columns
   const size_t smem = std::max<size_t>(
       sizeof(float) * (STAGES * NPIECE * CN * a.kp + STAGES * CN * DP + STAGES * CN) +
-          sizeof(double) * GradRoles<DP4>::EW * NV + 16 * sizeof(uint64_t),
+          sizeof(double) * GradRoles<DP4, (COMB || !NARROW)>::EW * NV + 16 * sizeof(uint64_t),
       120 * 1024);
   static size_t configured = 0;
   if (smem > configured) {
@@ -594,7 +598,7 @@ void launch_one(const GradTcArgs& a, cudaStream_t s) {
                                   static_cast<int>(smem)));
     configured = smem;
   }
-  grad_tc_kernel<DP4, NARROW, COMB, DX><<<a.blocks, GradRoles<DP4>::NT, smem, s>>>(a);
+  grad_tc_kernel<DP4, NARROW, COMB, DX><<<a.blocks, GradRoles<DP4, (COMB || !NARROW)>::NT, smem, s>>>(a);
   check_launch("grad_tc_kernel");
 }
 
