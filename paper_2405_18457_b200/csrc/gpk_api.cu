@@ -1919,7 +1919,7 @@ void solve_sgd_lazy(gpk_batch* b, const gpk_solver_config* c, gpk_solver_report*
   GPK_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
   unsigned* ticket = b->ticket.ensure(1);
   GPK_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
-  double* gpart = b->sgd_gpart.ensure(static_cast<size_t>((bs + 7) / 8) * m);
+  double* gpart = b->sgd_gpart.ensure(static_cast<size_t>(sgd_finish_blocks(bs)) * m);  // APPLY_ROWS == FIN_ROWS
   col_reduce_launch(b->residuals.p, nullptr, nloc, m, m, 2, red + static_cast<size_t>(op->rk) * G * m, G, nullptr, s);
   gather_inplace(op, red, sizeof(double) * G * m);
   sum_partials_launch(red, G * nr, m, sumsq, nullptr, s);

@@ -1316,7 +1316,12 @@ __global__ void sgd_reduce_kernel(SgdStepArgs a) {
 // records; R[i] = -g. Block partials of sum_q g^2 per column; the last block
 // to finish updates the residual norms and takes the termination decision
 // (solvers.cpp:164-178: test after the update, abort on a non-finite iterate).
-constexpr int APPLY_ROWS = 8;
+// minibatch rows per block of the apply / finish kernels (the same in both: their block partials are summed
+// in one order). Measured at C4: 4 rows (128 blocks) 20.7 us per finish launch, 8 rows 17.0 us; 16 exceeds 1024 threads.
+#ifndef SGD_FIN_ROWS
+#define SGD_FIN_ROWS 8
+#endif
+constexpr int APPLY_ROWS = SGD_FIN_ROWS;
 __global__ void sgd_apply_kernel(SgdStepArgs a) {
   if (a.ctl->stop) return;
   const int t = a.ctl->iters;
@@ -1435,7 +1440,7 @@ __global__ void sgd_apply_kernel(SgdStepArgs a) {
 // b / FIN_ROWS = 64 blocks sums the block partials of g^2 and of the old
 // squares in block order and takes the termination / divergence decision
 // (solvers.cpp:164-178).
-constexpr int FIN_ROWS = 8;
+constexpr int FIN_ROWS = SGD_FIN_ROWS;
 __global__ void sgd_finish_kernel(SgdStepArgs a) {
   // programmatic dependent launch: the next slab kernel may start its prologue
   // now (it waits for this grid's completion before it reads anything this
